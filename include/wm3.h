@@ -1,0 +1,90 @@
+/*
+ * wm3.h — C ABI of the B200-native WeatherMesh-3 forecast hot path (libwm3.so).
+ *
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t passed as void*.
+ * Nothing here throws: each call returns 0 on success or a nonzero status, with a message
+ * available from wm3_last_error() (thread-local).  Validation that the reference performs
+ * in Python (ConfigError, gridcast/errors.py:4-5) stays in the Python host layer and runs
+ * before any of these are called; a nonzero status here is a launch/device fault
+ * ("compute" category in the reference CLI, gridcast/cli.py:456-463).
+ *
+ * Reference interfaces replaced (paths relative to the reference package pkg/src/gridcast):
+ *   wm3_neighbor_table      grid.py:96-130       bump_starts + neighborhood (bit-exact int64 export)
+ *   wm3_layernorm_bf16      autodiff.py:400-424  layernorm, eps 1e-6, biased variance
+ *   wm3_linear              attention.py:142-143 _linear = matmul(x, W) + b, with fused epilogues:
+ *                             WM3_EPI_BIAS_BF16       (plain linear, bf16 out)
+ *                             WM3_EPI_BIAS_GELU_BF16  attention.py:182  gelu(hn2 W1 + b1), exact erf
+ *                             WM3_EPI_BIAS_RESID_F32  attention.py:179,183  x += ctx Wo + bo / mid W2 + b2
+ *                             WM3_EPI_QKV_ROPE        attention.py:167-171  q,k,v + bias, rotary on q,k
+ *                             WM3_EPI_F32             raw fp32 accumulator (tests)
+ *   wm3_natten_fwd          attention.py:173-178 gather + q k^T/sqrt(dh) + softmax + @V, fused
+ *   wm3_conv3x3             model.py:296-301 + autodiff.py:677-713  row zero pad, col wrap, stride 1/2
+ *   wm3_convT4x4s2          model.py:317-325 + autodiff.py:716-764  exact adjoint geometry
+ */
+#ifndef WM3_H
+#define WM3_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  WM3_EPI_F32 = 0,
+  WM3_EPI_BIAS_BF16 = 1,
+  WM3_EPI_BIAS_GELU_BF16 = 2,
+  WM3_EPI_BIAS_RESID_F32 = 3,
+  WM3_EPI_QKV_ROPE = 4,
+};
+
+/* Rotary description for WM3_EPI_QKV_ROPE (attention.py:48-92).  Output columns are laid out
+ * [3][heads][dhp]; within a q/k head, rotation pair j sits at columns (j, j + dhp/2), j < dh/2.
+ * rope_cos/rope_sin are [3][emax][64] fp32 per-axis tables (axis 0 depth, 1 row, 2 col); pair
+ * j < pd uses the depth table, j < pd+pr the row table, else the col table. */
+typedef struct {
+  const float* rope_cos;
+  const float* rope_sin;
+  int emax;
+  int depth, rows, cols; /* local token-grid extents: token t = (d*rows + r)*cols + c */
+  int row0;              /* global row of local row 0 (latitude band offset) */
+  int heads, dhp, pd, pr;
+} wm3_rope_t;
+
+const char* wm3_last_error(void);
+int wm3_version(void);
+int wm3_sm_count(void);
+
+/* (T, K) int64 neighbor table of a (depth,rows,cols) box; rows [row0, row0+nrows) of a grid with
+ * global extent `rows`.  Row-major K order kd*wh*ww + kh*ww + kw (grid.py:124-127). */
+int wm3_neighbor_table(int depth, int rows, int cols, int wd, int wh, int ww, int row0, int nrows,
+                       int64_t* out, void* stream);
+
+/* out[m, 0:ldo] = bf16(layernorm(x[m, 0:n]) * gain + bias), zero in [n, ldo). */
+int wm3_layernorm_bf16(const float* x, int ldx, int m, int n, const float* gain, const float* bias,
+                       float eps, void* out_bf16, int ldo, void* stream);
+
+/* C[M, N] = A[M, K] (bf16, row pitch lda) * B[N, K]^T (bf16, row pitch ldb) + epilogue.
+ * out: bf16 or f32 depending on epi; ldo in elements; n_valid columns are stored. */
+int wm3_linear(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi,
+               void* out, int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, void* stream);
+
+/* Fused 3D neighborhood attention forward.
+ * qkv: bf16 [T][3][heads][dhp] (row pitch ldqkv elements), out: bf16 [T][heads][dhp] (pitch ldo).
+ * Token grid (depth, rows, cols) is the local band: rows [row0, row0+rows) of a grid with global row
+ * extent rows_global; the band's K/V rows may be extended by halos (halo_lo rows before local row 0
+ * and halo_hi after) already present in qkv, i.e. qkv row 0 is global row row0 - halo_lo.
+ * scale = 1/sqrt(dh). */
+int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, int depth, int rows, int cols,
+                   int rows_global, int row0, int halo_lo, int halo_hi, int heads, int dhp, int wd,
+                   int wh, int ww, float scale, void* stream);
+
+/* Debug export of the kernel's own window arithmetic: per token, the (start_d, start_h, col_off)
+ * it uses; int32 [T][3]. */
+int wm3_natten_windows(int depth, int rows, int cols, int rows_global, int row0, int wd, int wh, int ww,
+                       int32_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WM3_H */

@@ -1,0 +1,88 @@
+"""ctypes binding of libwm3.so, the C ABI declared in include/wm3.h.
+
+There is no fallback: if the shared library is missing or CUDA is unavailable, every entry point
+raises.  Status codes from the library become RuntimeError carrying wm3_last_error().
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from functools import lru_cache
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libwm3.so")
+
+WM3_EPI_F32 = 0
+WM3_EPI_BIAS_BF16 = 1
+WM3_EPI_BIAS_GELU_BF16 = 2
+WM3_EPI_BIAS_RESID_F32 = 3
+WM3_EPI_QKV_ROPE = 4
+
+_vp = ctypes.c_void_p
+_i = ctypes.c_int
+_f = ctypes.c_float
+
+
+class RopeT(ctypes.Structure):
+    """wm3_rope_t (include/wm3.h)."""
+    _fields_ = [
+        ("rope_cos", _vp), ("rope_sin", _vp), ("emax", _i),
+        ("depth", _i), ("rows", _i), ("cols", _i), ("row0", _i),
+        ("heads", _i), ("dhp", _i), ("pd", _i), ("pr", _i),
+    ]
+
+
+# name -> argtypes; every function returns int status
+SIGNATURES = {
+    "wm3_neighbor_table": [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp],
+    "wm3_layernorm_bf16": [_vp, _i, _i, _i, _vp, _vp, _f, _vp, _i, _vp],
+    "wm3_linear": [_vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, ctypes.POINTER(RopeT), _vp],
+    "wm3_natten_fwd": [_vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _f, _vp],
+    "wm3_natten_windows": [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp],
+}
+
+
+def exported_symbols() -> list[str]:
+    """Every symbol include/wm3.h declares (checked against the .so by the CPU test suite)."""
+    return ["wm3_last_error", "wm3_version", "wm3_sm_count"] + list(SIGNATURES)
+
+
+@lru_cache(maxsize=1)
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"libwm3.so not built at {path}; run `make` (or __graft_entry__.build()) first")
+    lib = ctypes.CDLL(path)
+    lib.wm3_last_error.restype = ctypes.c_char_p
+    lib.wm3_last_error.argtypes = []
+    lib.wm3_version.restype = _i
+    lib.wm3_sm_count.restype = _i
+    for name, argt in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argt
+        fn.restype = _i
+    return lib
+
+
+def lib() -> ctypes.CDLL:
+    if not torch.cuda.is_available():
+        raise RuntimeError("the WM-3 B200 path needs a CUDA device; there is no CPU fallback")
+    return load_library()
+
+
+def check(status: int, what: str) -> None:
+    if status != 0:
+        msg = load_library().wm3_last_error().decode(errors="replace")
+        raise RuntimeError(f"{what}: {msg}")
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream

@@ -1,0 +1,23 @@
+// Host-side helpers shared by the kernel translation units (definitions in host.cu).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace wm3 {
+
+// Record a printf-style message as the thread's last error; returns -1.
+int set_error(const char* fmt, ...);
+// cudaGetLastError after a launch; returns 0 or -1 (with message).
+int check_launch(const char* what);
+int sm_count();
+
+// 2D bf16 tensor map (inner = contiguous extent, outer = rows, pitch in elements), SWIZZLE_128B,
+// OOB elements zero-filled.  Box = (box_inner, box_outer); box_inner * 2 must be 128.
+int make_tmap_2d_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t pitch_elems,
+                      uint32_t box_inner, uint32_t box_outer);
+// General bf16 tensor map, rank <= 5; strides in elements for dims 1..rank-1.
+int make_tmap_bf16(CUtensorMap* map, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_elems,
+                   const uint32_t* box, const uint32_t* elem_strides);
+
+}  // namespace wm3

@@ -1,0 +1,102 @@
+"""Device-level operator wrappers over libwm3.so (torch tensors in/out, all on the current stream).
+
+Torch is only the allocator and stream provider here; every op below is one launch of a hand-written
+sm_100a kernel from csrc/.  Shapes are validated before launch; kernel faults raise RuntimeError.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+from ._lib import check, ptr, stream_ptr
+
+
+def _req(t: torch.Tensor, dtype: torch.dtype, name: str) -> None:
+    if not t.is_cuda:
+        raise RuntimeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise RuntimeError(f"{name} must be {dtype}, got {t.dtype}")
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise RuntimeError(f"{name} must be a row-major 2D tensor")
+
+
+def neighbor_table(extents, window, row0: int = 0, nrows: int | None = None) -> torch.Tensor:
+    """(T, K) int64 neighbor table computed on the GPU (grid.py:107-130 semantics)."""
+    d, h, w = (int(e) for e in extents)
+    wd, wh, ww = (int(e) for e in window)
+    nrows = h if nrows is None else int(nrows)
+    out = torch.empty((d * nrows * w, wd * wh * ww), dtype=torch.int64, device="cuda")
+    check(_lib.lib().wm3_neighbor_table(d, h, w, wd, wh, ww, int(row0), nrows, ptr(out), stream_ptr()),
+          "wm3_neighbor_table")
+    return out
+
+
+def natten_windows(extents, window, rows_global: int | None = None, row0: int = 0) -> torch.Tensor:
+    d, h, w = (int(e) for e in extents)
+    wd, wh, ww = (int(e) for e in window)
+    rg = h if rows_global is None else int(rows_global)
+    out = torch.empty((d * h * w, 3), dtype=torch.int32, device="cuda")
+    check(_lib.lib().wm3_natten_windows(d, h, w, rg, int(row0), wd, wh, ww, ptr(out), stream_ptr()),
+          "wm3_natten_windows")
+    return out
+
+
+def layernorm_bf16(x: torch.Tensor, gain: torch.Tensor, bias: torch.Tensor, ldo: int | None = None,
+                   out: torch.Tensor | None = None, eps: float = 1e-6) -> torch.Tensor:
+    _req(x, torch.float32, "x")
+    m, n = x.shape
+    ldo = n if ldo is None else int(ldo)
+    if out is None:
+        out = torch.empty((m, ldo), dtype=torch.bfloat16, device=x.device)
+    check(_lib.lib().wm3_layernorm_bf16(ptr(x), x.stride(0), m, n, ptr(gain), ptr(bias), float(eps), ptr(out),
+                                        out.stride(0), stream_ptr()), "wm3_layernorm_bf16")
+    return out
+
+
+def linear(a: torch.Tensor, w: torch.Tensor, epi: int, bias: torch.Tensor | None = None,
+           out: torch.Tensor | None = None, n_valid: int | None = None,
+           rope: "_lib.RopeT | None" = None) -> torch.Tensor:
+    """out = epilogue(a @ w.T + bias); a (M, K) bf16, w (N, K) bf16 (weights stored (out, in))."""
+    _req(a, torch.bfloat16, "a")
+    _req(w, torch.bfloat16, "w")
+    m, k = a.shape
+    n, k2 = w.shape
+    if k2 != k:
+        raise RuntimeError(f"linear: inner extents differ {a.shape} @ {w.shape}^T")
+    f32_out = epi in (_lib.WM3_EPI_F32, _lib.WM3_EPI_BIAS_RESID_F32)
+    if out is None:
+        if epi == _lib.WM3_EPI_BIAS_RESID_F32:
+            raise RuntimeError("residual epilogue needs the fp32 stream as `out`")
+        out = torch.empty((m, n), dtype=torch.float32 if f32_out else torch.bfloat16, device=a.device)
+    _req(out, torch.float32 if f32_out else torch.bfloat16, "out")
+    nv = out.shape[1] if n_valid is None else int(n_valid)
+    rp = None if rope is None else ctypes_byref(rope)
+    check(_lib.lib().wm3_linear(ptr(a), a.stride(0), ptr(w), w.stride(0), m, n, k, int(epi), ptr(out),
+                                out.stride(0), nv, ptr(bias), rp, stream_ptr()), "wm3_linear")
+    return out
+
+
+def ctypes_byref(obj):
+    import ctypes
+    return ctypes.byref(obj)
+
+
+def natten(qkv: torch.Tensor, extents, heads: int, dhp: int, dh: int, window,
+           out: torch.Tensor | None = None, rows_global: int | None = None, row0: int = 0,
+           halo_lo: int = 0, halo_hi: int = 0) -> torch.Tensor:
+    """Fused neighborhood attention over qkv (T_ext, 3*heads*dhp) -> ctx (T, heads*dhp) bf16."""
+    _req(qkv, torch.bfloat16, "qkv")
+    d, h, w = (int(e) for e in extents)
+    wd, wh, ww = (int(e) for e in window)
+    rg = h if rows_global is None else int(rows_global)
+    t = d * h * w
+    if out is None:
+        out = torch.empty((t, heads * dhp), dtype=torch.bfloat16, device=qkv.device)
+    _req(out, torch.bfloat16, "out")
+    check(_lib.lib().wm3_natten_fwd(ptr(qkv), qkv.stride(0), ptr(out), out.stride(0), d, h, w, rg, int(row0),
+                                    int(halo_lo), int(halo_hi), int(heads), int(dhp), wd, wh, ww,
+                                    float(1.0 / math.sqrt(dh)), stream_ptr()), "wm3_natten_fwd")
+    return out

@@ -1,0 +1,59 @@
+"""Minimal `Tensor` with the read surface of gridcast.autodiff.Tensor (autodiff.py:182-271).
+
+Callers of the reference read `.values` (float64, C-contiguous numpy; cli.py:218-219, model.py:173-175),
+`.shape`, `.size`, `.nbytes`.  Here a Tensor is backed either by a host array (parameters, user inputs)
+or by a device torch tensor (latents, decoded fields); `.values` copies device data to the host once,
+as float64, on first access.  `.device` exposes the torch tensor without a copy.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+
+class Tensor:
+    __slots__ = ("_host", "_dev", "requires_grad", "__weakref__")
+
+    def __init__(self, values=None, requires_grad: bool = False, device: torch.Tensor | None = None):
+        if (values is None) == (device is None):
+            raise ValueError("Tensor needs exactly one of host values or a device tensor")
+        self._host = None if values is None else np.ascontiguousarray(np.asarray(values, dtype=np.float64))
+        self._dev = device
+        self.requires_grad = bool(requires_grad)
+
+    @property
+    def values(self) -> np.ndarray:
+        if self._host is None:
+            self._host = np.ascontiguousarray(self._dev.detach().to("cpu", torch.float64).numpy())
+        return self._host
+
+    @values.setter
+    def values(self, v) -> None:
+        self._host = np.ascontiguousarray(np.asarray(v, dtype=np.float64))
+        self._dev = None
+
+    @property
+    def device(self) -> torch.Tensor | None:
+        return self._dev
+
+    @property
+    def shape(self) -> tuple[int, ...]:
+        return tuple(self._dev.shape) if self._host is None else self._host.shape
+
+    @property
+    def size(self) -> int:
+        return int(np.prod(self.shape))
+
+    @property
+    def nbytes(self) -> int:
+        return self.size * 8
+
+    def __repr__(self) -> str:
+        where = "host" if self._host is not None else "cuda"
+        return f"Tensor(shape={self.shape}, {where})"
+
+
+def host_values(t) -> np.ndarray:
+    """float64 numpy view of a parameter given as our Tensor, a reference Tensor (.values) or an array."""
+    return np.asarray(getattr(t, "values", t), dtype=np.float64)

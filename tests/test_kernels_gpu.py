@@ -1,0 +1,150 @@
+"""Kernel-level parity on the B200: each libwm3 kernel against the oracle / a torch fp32 reference."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.grid import neighborhood
+
+pytestmark = pytest.mark.gpu
+
+
+def ops():
+    from paper_2503_22235_b200 import ops as o
+    return o
+
+
+def lib():
+    from paper_2503_22235_b200 import _lib
+    return _lib
+
+
+# ------------------------------------------------------------------------------------------------
+# bit-exact window arithmetic
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("ext,win", [
+    ((3, 5, 8), (3, 3, 3)), ((4, 6, 10), (3, 3, 3)), ((1, 5, 6), (1, 3, 1)), ((1, 1, 8), (1, 1, 5)),
+    ((7, 9, 18), (5, 7, 7)), ((5, 18, 36), (5, 7, 7)), ((3, 3, 3), (3, 3, 3)), ((2, 7, 10), (1, 4, 4)),
+    ((3, 5, 10), (2, 2, 2)), ((6, 8, 10), (5, 5, 5)),
+])
+def test_neighbor_table_bit_exact(ext, win):
+    got = ops().neighbor_table(ext, win).cpu().numpy()
+    want = neighborhood(ext, win)
+    assert got.dtype == np.int64 and got.shape == want.shape
+    assert np.array_equal(got, want)
+
+
+def test_neighbor_table_full_scale_checksum():
+    import hashlib
+    got = ops().neighbor_table((5, 90, 180), (5, 7, 7)).cpu().numpy()
+    h = hashlib.sha256(got.astype("<i8").tobytes()).hexdigest()
+    assert h.startswith("600ad28a33324093936c5ca3888cb6f1")
+    assert got[0, :10].tolist() == [177, 178, 179, 0, 1, 2, 3, 357, 358, 359]
+
+
+def test_neighbor_table_band_rows_match_full():
+    full = neighborhood((5, 90, 180), (5, 7, 7)).reshape(5, 90, 180, -1)
+    for row0, nrows in [(0, 12), (12, 11), (78, 12), (45, 45)]:
+        got = ops().neighbor_table((5, 90, 180), (5, 7, 7), row0=row0, nrows=nrows).cpu().numpy()
+        assert np.array_equal(got, full[:, row0:row0 + nrows].reshape(-1, full.shape[-1]))
+
+
+# ------------------------------------------------------------------------------------------------
+# GEMM (tcgen05) + epilogues
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("m,n,k", [(128, 128, 64), (300, 256, 128), (1000, 384, 1024), (4096, 3072, 1024),
+                                   (777, 1024, 4096), (81, 128, 192)])
+def test_gemm_f32(m, n, k):
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    a = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
+    w = torch.randn(n, k, device="cuda", generator=g).to(torch.bfloat16)
+    out = ops().linear(a, w, lib().WM3_EPI_F32)
+    ref = a.float() @ w.float().T
+    torch.cuda.synchronize()
+    err = (out - ref).abs().max().item()
+    assert err <= 2e-3 * ref.abs().max().item() + 1e-3, err
+
+
+def test_gemm_epilogues():
+    m, n, k = 517, 512, 256
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(n, k, device="cuda", generator=g) / 16).to(torch.bfloat16)
+    b = torch.randn(n, device="cuda", generator=g)
+    ref = a.float() @ w.float().T + b
+    L = lib()
+    o1 = ops().linear(a, w, L.WM3_EPI_BIAS_BF16, bias=b)
+    assert (o1.float() - ref).abs().max().item() < 3e-2
+    o2 = ops().linear(a, w, L.WM3_EPI_BIAS_GELU_BF16, bias=b)
+    gel = 0.5 * ref * (1 + torch.erf(ref / math.sqrt(2)))
+    assert (o2.float() - gel).abs().max().item() < 3e-2
+    x = torch.randn(m, n, device="cuda", generator=g)
+    x0 = x.clone()
+    ops().linear(a, w, L.WM3_EPI_BIAS_RESID_F32, bias=b, out=x)
+    assert (x - (x0 + ref)).abs().max().item() < 1e-3
+    # partial store (n_valid)
+    out = torch.zeros(m, n, device="cuda")
+    ops().linear(a, w, L.WM3_EPI_F32, out=out, n_valid=n - 45)
+    assert out[:, n - 45:].abs().max().item() == 0
+    assert (out[:, :n - 45] - (a.float() @ w.float().T)[:, :n - 45]).abs().max().item() < 1e-2
+
+
+def test_layernorm():
+    for m, n, ldo in [(1000, 1024, 1024), (33, 256, 256), (17, 12, 64), (64, 4096, 4096)]:
+        x = torch.randn(m, n, device="cuda") * 3 + 1.5
+        gain = torch.randn(n, device="cuda")
+        bias = torch.randn(n, device="cuda")
+        out = ops().layernorm_bf16(x, gain, bias, ldo=ldo)
+        ref = torch.nn.functional.layer_norm(x, (n,), gain, bias, eps=1e-6)
+        assert (out[:, :n].float() - ref).abs().max().item() < 0.05
+        if ldo > n:
+            assert out[:, n:].float().abs().max().item() == 0
+
+
+# ------------------------------------------------------------------------------------------------
+# fused neighborhood attention
+# ------------------------------------------------------------------------------------------------
+def na_reference(qkv, ext, heads, dhp, dh, win):
+    d, h, w = ext
+    t = d * h * w
+    tab = torch.from_numpy(neighborhood(ext, win)).cuda()
+    q = qkv[:, :heads * dhp].float().view(t, heads, dhp)
+    k = qkv[:, heads * dhp:2 * heads * dhp].float().view(t, heads, dhp)
+    v = qkv[:, 2 * heads * dhp:].float().view(t, heads, dhp)
+    kn = k[tab]  # (T, K, heads, dhp)
+    vn = v[tab]
+    s = torch.einsum("thd,tkhd->thk", q, kn) / math.sqrt(dh)
+    p = torch.softmax(s, dim=-1)
+    return torch.einsum("thk,tkhd->thd", p, vn).reshape(t, heads * dhp), p
+
+
+@pytest.mark.parametrize("ext,win,heads,dhp", [
+    ((7, 9, 18), (5, 7, 7), 2, 128), ((5, 18, 36), (5, 7, 7), 8, 128), ((3, 5, 10), (3, 3, 3), 2, 64),
+    ((2, 7, 10), (1, 3, 3), 4, 64), ((3, 3, 3), (3, 3, 3), 2, 64), ((5, 12, 200), (5, 7, 7), 1, 128),
+    ((4, 6, 10), (2, 4, 4), 3, 128),
+])
+def test_natten_matches_gather_reference(ext, win, heads, dhp):
+    t = int(np.prod(ext))
+    g = torch.Generator(device="cuda").manual_seed(t)
+    qkv = (torch.randn(t, 3 * heads * dhp, device="cuda", generator=g) * 1.5).to(torch.bfloat16)
+    out = ops().natten(qkv, ext, heads, dhp, dhp, win)
+    ref, _ = na_reference(qkv, ext, heads, dhp, dhp, win)
+    torch.cuda.synchronize()
+    err = (out.float() - ref).abs().max().item()
+    rel = ((out.float() - ref).norm() / ref.norm()).item()
+    assert rel < 1e-2 and err < 5e-2, (err, rel)
+
+
+def test_natten_windows_bit_exact():
+    from oracle.grid import bump_starts
+    for ext, win in [((5, 90, 180), (5, 7, 7)), ((7, 9, 18), (5, 7, 7)), ((4, 6, 10), (2, 4, 4))]:
+        d, h, w = ext
+        got = ops().natten_windows(ext, win).cpu().numpy().reshape(d, h, w, 3)
+        sd = bump_starts(d, win[0])
+        sh = bump_starts(h, win[1])
+        assert np.array_equal(got[..., 0], np.broadcast_to(sd[:, None, None], (d, h, w)))
+        assert np.array_equal(got[..., 1], np.broadcast_to(sh[None, :, None], (d, h, w)))
+        assert np.array_equal(got[..., 2], np.broadcast_to(((np.arange(w) - (win[2] - 1) // 2) % w)[None, None, :],
+                                                          (d, h, w)))
