@@ -1,0 +1,113 @@
+"""Operator-level drop-in for gridcast.attention (attention.py): natten_block and helpers.
+
+`natten_block(x, params, prefix, extents, window, heads)` has the reference signature and error behaviour
+(ConfigError before any launch, attention.py:150-155 and grid.py:98-99,119-120) and returns a new Tensor;
+the input is never mutated.  The compute is the 7-launch device chain of blocks.block_forward.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib, ops
+from .blocks import rope_axis_tables
+from .errors import ConfigError
+from .params import block_param_names, init_block_params  # noqa: F401  (re-exported API)
+from .runtime import CACHE
+from .tensor import Tensor
+
+__all__ = ["natten_block", "attention_weights", "rotary_tables", "apply_rotary", "init_block_params",
+           "block_param_names", "to_device_f32", "validate_block_args"]
+
+
+def to_device_f32(x) -> torch.Tensor:
+    """A fresh fp32 CUDA copy of x (our Tensor, anything with .values, numpy array or torch tensor)."""
+    if isinstance(x, Tensor) and x.device is not None:
+        src = x.device
+    elif isinstance(x, torch.Tensor):
+        src = x
+    else:
+        src = torch.from_numpy(np.ascontiguousarray(np.asarray(getattr(x, "values", x), dtype=np.float32)))
+    return src.to(device="cuda", dtype=torch.float32, copy=True).contiguous()
+
+
+def validate_block_args(shape, extents, window, heads: int) -> int:
+    """attention.py:150-159 checks, in order; returns the head dim."""
+    t, dim = shape
+    d, h, w = (int(e) for e in extents)
+    if t != d * h * w:
+        raise ConfigError(f"token count {t} != prod of extents {tuple(extents)}")
+    if dim % heads:
+        raise ConfigError(f"dim {dim} not divisible by heads {heads}")
+    for win, ext in zip(window, (d, h, w)):
+        if win > ext:
+            raise ConfigError(f"window {win} exceeds axis extent {ext}")
+    dh = dim // heads
+    if dh % 2:
+        raise ConfigError(f"rotary head dim must be even, got {dh}")
+    if dh // 2 < 3:
+        raise ConfigError(f"head dim {dh} leaves fewer than one rotary pair per axis")
+    return dh
+
+
+def natten_block(x, params: dict, prefix: str, extents, window, heads: int) -> Tensor:
+    shape = tuple(x.shape)
+    dh = validate_block_args(shape, extents, window, heads)
+    xd = to_device_f32(x)
+    bw = CACHE.block(params, prefix, heads)
+    if bw.hidden != shape[1]:
+        raise ConfigError(f"parameters {prefix} have width {bw.hidden}, tokens have {shape[1]}")
+    from .blocks import block_forward
+    block_forward(xd, bw, CACHE.workspace(shape[0], bw), CACHE.rope(extents, dh), tuple(extents), tuple(window))
+    return Tensor(device=xd)
+
+
+def attention_weights(x_values, params: dict, prefix: str, extents, window, heads: int) -> np.ndarray:
+    """Softmax weights (T, heads, K) for inspection (attention.py:187-212).
+
+    q and k come from the same fused LN + QKV/rotary kernels as the block; the probe then evaluates the
+    scores on the neighbor table exported by the window kernel.
+    """
+    xd = to_device_f32(x_values)
+    t, dim = xd.shape
+    dh = validate_block_args((t, dim), extents, window, heads)
+    bw = CACHE.block(params, prefix, heads)
+    ws = CACHE.workspace(t, bw)
+    rope = CACHE.rope(extents, dh)
+    ops.layernorm_bf16(xd, bw.ln1_g, bw.ln1_b, out=ws.hn)
+    ops.linear(ws.hn, bw.w_qkv, _lib.WM3_EPI_QKV_ROPE, bias=bw.b_qkv, out=ws.qkv,
+               rope=rope.struct(extents, 0, bw.heads, bw.dhp))
+    table = ops.neighbor_table(extents, window)
+    sec = heads * bw.dhp
+    q = ws.qkv[:, :sec].float().view(t, heads, bw.dhp)
+    k = ws.qkv[:, sec:2 * sec].float().view(t, heads, bw.dhp)
+    s = torch.einsum("thd,tkhd->thk", q, k[table]) / math.sqrt(dh)
+    return torch.softmax(s, dim=-1).double().cpu().numpy()
+
+
+def rotary_tables(extents, head_dim: int):
+    """cos/sin (T, 1, head_dim // 2) float64 (attention.py:48-84), assembled from the per-axis tables."""
+    d, h, w = (int(e) for e in extents)
+    n = head_dim // 2
+    rope_axis_tables(extents, head_dim)  # same validation as the device tables
+    di, hi, wi = np.unravel_index(np.arange(d * h * w), (d, h, w))
+    from .blocks import _wavelengths, pair_split
+    pd, pr, pc = pair_split(n)
+    ang = np.empty((d * h * w, n))
+    ang[:, :pd] = 2.0 * math.pi * di[:, None] / _wavelengths(d, pd)[None, :]
+    ang[:, pd:pd + pr] = 2.0 * math.pi * hi[:, None] / _wavelengths(h, pr)[None, :]
+    ang[:, pd + pr:] = 2.0 * math.pi * wi[:, None] * np.arange(1, pc + 1)[None, :] / w
+    return np.ascontiguousarray(np.cos(ang)[:, None, :]), np.ascontiguousarray(np.sin(ang)[:, None, :])
+
+
+def apply_rotary(x, cos, sin):
+    """Rotate feature pairs (j, j + dh/2) of x (T, heads, dh) by per-token phases (attention.py:87-92)."""
+    xv = np.asarray(getattr(x, "values", x))
+    cv = np.asarray(getattr(cos, "values", cos))
+    sv = np.asarray(getattr(sin, "values", sin))
+    half = xv.shape[-1] // 2
+    a, b = xv[..., :half], xv[..., half:]
+    return Tensor(np.concatenate([a * cv - b * sv, a * sv + b * cv], axis=-1))

@@ -1,0 +1,226 @@
+"""Device-resident neighborhood-attention block: weight layout, rotary tables, forward chain.
+
+One block (attention.py:146-184) is seven launches on one stream:
+  LN1 -> [QKV GEMM + bias + rotary] -> [fused NA] -> [O-proj GEMM + bias + residual]
+      -> LN2 -> [W1 GEMM + bias + GELU] -> [W2 GEMM + bias + residual]
+The residual stream x stays fp32 (T, hidden) in HBM; GEMM operands are bf16, accumulation fp32 in TMEM.
+
+Weight layout (built once per parameter set, from the reference's (in, out) float64 matrices):
+  * every GEMM weight is stored (out, in) = K-major bf16 so both UMMA operands are K-major SW128 tiles;
+  * K and N are padded to the kernels' granularity with zero rows/columns (exact);
+  * heads are padded to dhp in {64, 128}; within a q/k head the rotary pair (j, j + dh/2) of the reference
+    is placed at columns (j, j + dhp/2) — the same permutation on q and k leaves q.k unchanged.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib, ops
+from .errors import ConfigError
+from .params import block_param_names
+from .tensor import host_values
+
+
+def round_up(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+def head_pad(dh: int) -> int:
+    if dh <= 64:
+        return 64
+    if dh <= 128:
+        return 128
+    raise ConfigError(f"head dim {dh} > 128 is not supported by the fused attention kernel")
+
+
+# ------------------------------------------------------------------------------------------------
+# rotary phases (attention.py:39-84), as per-axis fp32 tables for the QKV epilogue
+# ------------------------------------------------------------------------------------------------
+def pair_split(n_pairs: int) -> tuple[int, int, int]:
+    base = n_pairs // 3
+    return base, base, n_pairs - 2 * base
+
+
+def _wavelengths(extent: int, n: int) -> np.ndarray:
+    lo, hi = 4.0, max(8.0, 2.0 * extent)
+    if n == 1:
+        return np.array([hi])
+    return lo * (hi / lo) ** (np.arange(n) / (n - 1))
+
+
+def rope_axis_tables(extents, head_dim: int):
+    """(cos, sin) float32 arrays of shape (3, emax, 64): axis 0 depth, 1 row, 2 col; unused = (1, 0)."""
+    if head_dim % 2:
+        raise ConfigError(f"rotary head dim must be even, got {head_dim}")
+    n = head_dim // 2
+    if n < 3:
+        raise ConfigError(f"head dim {head_dim} leaves fewer than one rotary pair per axis")
+    pd, pr, pc = pair_split(n)
+    d, h, w = (int(e) for e in extents)
+    emax = max(d, h, w)
+    ang = np.zeros((3, emax, 64), dtype=np.float64)
+    use = np.zeros((3, 64), dtype=bool)
+    ang[0, :d, :pd] = 2.0 * math.pi * np.arange(d)[:, None] / _wavelengths(d, pd)[None, :]
+    use[0, :pd] = True
+    ang[1, :h, pd:pd + pr] = 2.0 * math.pi * np.arange(h)[:, None] / _wavelengths(h, pr)[None, :]
+    use[1, pd:pd + pr] = True
+    ang[2, :w, pd + pr:n] = 2.0 * math.pi * np.arange(w)[:, None] * np.arange(1, pc + 1)[None, :] / w
+    use[2, pd + pr:n] = True
+    cos = np.where(use[:, None, :], np.cos(ang), 1.0).astype(np.float32)
+    sin = np.where(use[:, None, :], np.sin(ang), 0.0).astype(np.float32)
+    return cos, sin, pd, pr, emax
+
+
+# ------------------------------------------------------------------------------------------------
+# weights
+# ------------------------------------------------------------------------------------------------
+@dataclass
+class BlockWeights:
+    hidden: int
+    heads: int
+    dh: int
+    dhp: int
+    kp: int        # padded hidden as a GEMM K (LN output pitch)
+    np_: int       # padded hidden as a GEMM N
+    nm: int        # padded MLP width
+    ln1_g: torch.Tensor
+    ln1_b: torch.Tensor
+    w_qkv: torch.Tensor
+    b_qkv: torch.Tensor
+    w_o: torch.Tensor
+    b_o: torch.Tensor
+    ln2_g: torch.Tensor
+    ln2_b: torch.Tensor
+    w_1: torch.Tensor
+    b_1: torch.Tensor
+    w_2: torch.Tensor
+    b_2: torch.Tensor
+
+
+def _qk_perm(heads: int, dh: int, dhp: int) -> np.ndarray:
+    """Padded column -> reference column (or -1) for a q/k section."""
+    m = np.full(heads * dhp, -1, dtype=np.int64)
+    half, halfp = dh // 2, dhp // 2
+    for hh in range(heads):
+        for j in range(half):
+            m[hh * dhp + j] = hh * dh + j
+            m[hh * dhp + halfp + j] = hh * dh + half + j
+    return m
+
+
+def _v_perm(heads: int, dh: int, dhp: int) -> np.ndarray:
+    m = np.full(heads * dhp, -1, dtype=np.int64)
+    for hh in range(heads):
+        m[hh * dhp: hh * dhp + dh] = hh * dh + np.arange(dh)
+    return m
+
+
+def _gather_cols(w: np.ndarray, perm: np.ndarray) -> np.ndarray:
+    """w (in, out) -> (in, len(perm)) picking columns perm (-1 -> zero)."""
+    out = np.zeros((w.shape[0], perm.size), dtype=np.float64)
+    ok = perm >= 0
+    out[:, ok] = w[:, perm[ok]]
+    return out
+
+
+def _kmajor_bf16(w_in_out: np.ndarray, n_pad: int, k_pad: int, device) -> torch.Tensor:
+    """(in, out) float64 -> (n_pad, k_pad) bf16, zero padded."""
+    k, n = w_in_out.shape
+    buf = np.zeros((n_pad, k_pad), dtype=np.float32)
+    buf[:n, :k] = w_in_out.T
+    return torch.from_numpy(buf).to(device=device, dtype=torch.bfloat16)
+
+
+def _vec(v: np.ndarray, n_pad: int, device) -> torch.Tensor:
+    buf = np.zeros(n_pad, dtype=np.float32)
+    buf[: v.size] = v
+    return torch.from_numpy(buf).to(device)
+
+
+def prepare_block(params: dict, prefix: str, heads: int, device="cuda") -> BlockWeights:
+    names = block_param_names(prefix)
+    missing = [n for n in names if n not in params]
+    if missing:
+        raise ConfigError(f"missing block parameters {missing[:3]}...")
+    p = {n[len(prefix) + 1:]: host_values(params[n]) for n in names}
+    hidden = p["ln1.gain"].shape[0]
+    if hidden % heads:
+        raise ConfigError(f"dim {hidden} not divisible by heads {heads}")
+    dh = hidden // heads
+    dhp = head_pad(dh)
+    kp = round_up(hidden, 64)
+    np_ = round_up(hidden, 32)
+    nm = round_up(p["mlp.w1"].shape[1], 64)
+    qk = _qk_perm(heads, dh, dhp)
+    vv = _v_perm(heads, dh, dhp)
+    w_qkv = np.concatenate([_gather_cols(p["attn.wq"], qk), _gather_cols(p["attn.wk"], qk),
+                            _gather_cols(p["attn.wv"], vv)], axis=1)
+    b_qkv = np.concatenate([_gather_cols(p["attn.bq"][None], qk)[0], _gather_cols(p["attn.bk"][None], qk)[0],
+                            _gather_cols(p["attn.bv"][None], vv)[0]])
+    # O-proj input rows follow the padded ctx layout (v order)
+    wo = np.zeros((heads * dhp, hidden), dtype=np.float64)
+    ok = vv >= 0
+    wo[ok] = p["attn.wo"][vv[ok]]
+    return BlockWeights(
+        hidden=hidden, heads=heads, dh=dh, dhp=dhp, kp=kp, np_=np_, nm=nm,
+        ln1_g=_vec(p["ln1.gain"], hidden, device), ln1_b=_vec(p["ln1.bias"], hidden, device),
+        w_qkv=_kmajor_bf16(w_qkv, 3 * heads * dhp, kp, device), b_qkv=_vec(b_qkv, 3 * heads * dhp, device),
+        w_o=_kmajor_bf16(wo, np_, heads * dhp, device), b_o=_vec(p["attn.bo"], np_, device),
+        ln2_g=_vec(p["ln2.gain"], hidden, device), ln2_b=_vec(p["ln2.bias"], hidden, device),
+        w_1=_kmajor_bf16(p["mlp.w1"], nm, kp, device), b_1=_vec(p["mlp.b1"], nm, device),
+        w_2=_kmajor_bf16(p["mlp.w2"], np_, nm, device), b_2=_vec(p["mlp.b2"], np_, device),
+    )
+
+
+# ------------------------------------------------------------------------------------------------
+# forward
+# ------------------------------------------------------------------------------------------------
+class RopeTables:
+    """Device copy of the per-axis rotary tables for one (global extents, dh), plus the ctypes struct."""
+
+    def __init__(self, extents, dh: int, device="cuda"):
+        cos, sin, pd, pr, emax = rope_axis_tables(extents, dh)
+        self.cos = torch.from_numpy(cos).to(device)
+        self.sin = torch.from_numpy(sin).to(device)
+        self.pd, self.pr, self.emax = pd, pr, emax
+        self.extents = tuple(int(e) for e in extents)
+
+    def struct(self, local_extents, row0: int, heads: int, dhp: int) -> _lib.RopeT:
+        d, h, w = local_extents
+        return _lib.RopeT(self.cos.data_ptr(), self.sin.data_ptr(), self.emax, d, h, w, int(row0), heads, dhp,
+                          self.pd, self.pr)
+
+
+class Workspace:
+    """Scratch activations for one (tokens, block geometry); reused across blocks and steps."""
+
+    def __init__(self, tokens: int, bw: BlockWeights, device="cuda", kv_tokens: int | None = None):
+        self.tokens = tokens
+        self.hn = torch.empty((tokens, bw.kp), dtype=torch.bfloat16, device=device)
+        self.qkv = torch.empty((kv_tokens or tokens, 3 * bw.heads * bw.dhp), dtype=torch.bfloat16, device=device)
+        self.ctx = torch.empty((tokens, bw.heads * bw.dhp), dtype=torch.bfloat16, device=device)
+        self.mid = torch.empty((tokens, bw.nm), dtype=torch.bfloat16, device=device)
+
+    def fits(self, tokens: int, bw: BlockWeights) -> bool:
+        return (self.tokens == tokens and self.hn.shape[1] == bw.kp and self.mid.shape[1] == bw.nm
+                and self.qkv.shape[1] == 3 * bw.heads * bw.dhp)
+
+
+def block_forward(x: torch.Tensor, bw: BlockWeights, ws: Workspace, rope: RopeTables, extents, window) -> None:
+    """In-place x (T, hidden) fp32 <- natten_block(x).  7 launches on the current stream."""
+    d, h, w = extents
+    t = d * h * w
+    L = _lib
+    ops.layernorm_bf16(x, bw.ln1_g, bw.ln1_b, out=ws.hn)
+    rs = rope.struct(extents, 0, bw.heads, bw.dhp)
+    ops.linear(ws.hn, bw.w_qkv, L.WM3_EPI_QKV_ROPE, bias=bw.b_qkv, out=ws.qkv, rope=rs)
+    ops.natten(ws.qkv, extents, bw.heads, bw.dhp, bw.dh, window, out=ws.ctx)
+    ops.linear(ws.ctx, bw.w_o, L.WM3_EPI_BIAS_RESID_F32, bias=bw.b_o, out=x, n_valid=bw.hidden)
+    ops.layernorm_bf16(x, bw.ln2_g, bw.ln2_b, out=ws.hn)
+    ops.linear(ws.hn, bw.w_1, L.WM3_EPI_BIAS_GELU_BF16, bias=bw.b_1, out=ws.mid)
+    ops.linear(ws.mid, bw.w_2, L.WM3_EPI_BIAS_RESID_F32, bias=bw.b_2, out=x, n_valid=bw.hidden)

@@ -324,7 +324,9 @@ using namespace wm3;
 extern "C" int wm3_linear(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi, void* out,
                           int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, void* stream) {
   if (m <= 0 || n <= 0 || k <= 0) return set_error("wm3_linear: bad sizes m=%d n=%d k=%d", m, n, k);
-  if ((lda % 8) || (ldb % 8) || (ldo % 8)) return set_error("wm3_linear: pitches must be multiples of 8");
+  const bool f32_out = (epi == WM3_EPI_F32 || epi == WM3_EPI_BIAS_RESID_F32);
+  if ((lda % 8) || (ldb % 8) || (ldo % (f32_out ? 4 : 8)))
+    return set_error("wm3_linear: pitches must be multiples of 8 (bf16) / 4 (f32 out)");
   if (n % 32) return set_error("wm3_linear: n=%d must be a multiple of 32", n);
   if (epi != WM3_EPI_F32 && bias == nullptr) return set_error("wm3_linear: bias required");
   EpiParams ep{};

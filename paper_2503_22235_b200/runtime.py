@@ -1,0 +1,70 @@
+"""Device-resident state: prepared weights, rotary tables and workspaces, cached per parameter set.
+
+The reference recomputes nothing across calls except its neighbor/rotary caches (grid.py:104,
+attention.py:45).  Here every weight is converted once (float64 host -> bf16/fp32 device, re-laid out for
+the kernels) and reused until the caller's parameter arrays change: the cache key of a block is the
+identity of its 16 host arrays, and the arrays are held so their ids cannot be recycled.
+"""
+
+from __future__ import annotations
+
+import threading
+
+import torch
+
+from .blocks import BlockWeights, RopeTables, Workspace, prepare_block
+from .params import block_param_names
+
+_lock = threading.Lock()
+
+
+def _fingerprint(params: dict, names) -> tuple:
+    return tuple(id(getattr(params[n], "values", params[n])) for n in names if n in params)
+
+
+class WeightCache:
+    def __init__(self):
+        self._blocks: dict = {}
+        self._ropes: dict = {}
+        self._ws: dict = {}
+
+    def block(self, params: dict, prefix: str, heads: int) -> BlockWeights:
+        names = block_param_names(prefix)
+        key = (id(params), prefix, heads)
+        fp = _fingerprint(params, names)
+        with _lock:
+            hit = self._blocks.get(key)
+            if hit is not None and hit[0] == fp:
+                return hit[2]
+        bw = prepare_block(params, prefix, heads)
+        keep = [getattr(params[n], "values", params[n]) for n in names]
+        with _lock:
+            self._blocks[key] = (fp, keep, bw)
+        return bw
+
+    def rope(self, extents, dh: int) -> RopeTables:
+        key = (tuple(int(e) for e in extents), int(dh), torch.cuda.current_device())
+        with _lock:
+            r = self._ropes.get(key)
+            if r is None:
+                r = RopeTables(extents, dh)
+                self._ropes[key] = r
+            return r
+
+    def workspace(self, tokens: int, bw: BlockWeights, tag: str = "main", kv_tokens: int | None = None) -> Workspace:
+        key = (tag, tokens, bw.kp, bw.nm, bw.heads, bw.dhp, kv_tokens, torch.cuda.current_device())
+        with _lock:
+            ws = self._ws.get(key)
+            if ws is None:
+                ws = Workspace(tokens, bw, kv_tokens=kv_tokens)
+                self._ws[key] = ws
+            return ws
+
+    def clear(self) -> None:
+        with _lock:
+            self._blocks.clear()
+            self._ropes.clear()
+            self._ws.clear()
+
+
+CACHE = WeightCache()

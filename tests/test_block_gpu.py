@@ -1,0 +1,102 @@
+"""Block-level parity on the B200: natten_block (drop-in API) vs the float64 oracle.
+
+Tolerances: bf16 GEMM operands with fp32 accumulation and an fp32 residual stream give
+block outputs within relative L2 1e-2 of the float64 oracle; the residual *update* (y - x) within 3e-2.
+Zero-residual parameters must reproduce the input bit for bit (attention.py:127-136, fp32 x + 0).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import model as om
+
+pytestmark = pytest.mark.gpu
+
+
+def _api():
+    from paper_2503_22235_b200 import attention
+    return attention
+
+
+def _params(dim, heads, seed=0, zero_residual=False):
+    from paper_2503_22235_b200.params import init_block_params
+    return init_block_params(np.random.default_rng(seed), dim, heads, "blk", zero_residual=zero_residual)
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.mark.parametrize("ext,win,dim,heads", [
+    ((7, 9, 18), (5, 7, 7), 256, 2),      # SURVEY §8d mid shape: depth bump, row bump, col wrap
+    ((2, 7, 10), (1, 3, 3), 24, 4),       # reference test_attention.py geometry, dh = 6
+    ((3, 5, 10), (3, 3, 3), 48, 4),       # desk latent
+    ((3, 3, 3), (3, 3, 3), 12, 2),        # tiny latent: global window
+    ((4, 6, 10), (2, 4, 4), 384, 3),      # even windows
+])
+def test_block_matches_oracle(ext, win, dim, heads):
+    t = int(np.prod(ext))
+    params = _params(dim, heads, seed=t)
+    x = np.random.default_rng(2).standard_normal((t, dim))
+    y = _api().natten_block(x, params, "blk", ext, win, heads).values
+    want = om.natten_block(x, params, "blk", ext, win, heads)
+    assert _rel(y, want) < 1e-2
+    assert _rel(y - x, want - x) < 3e-2
+
+
+def test_block_full_width_band():
+    """(5,18,36) at the full-scale width D=1024, 8 heads, window (5,7,7) (SURVEY config-2 parity shape)."""
+    ext, win, dim, heads = (5, 18, 36), (5, 7, 7), 1024, 8
+    t = int(np.prod(ext))
+    params = _params(dim, heads, seed=0)
+    x = np.random.default_rng(2).standard_normal((t, dim))
+    y = _api().natten_block(x, params, "blk", ext, win, heads).values
+    want = om.natten_block(x, params, "blk", ext, win, heads, chunk=128)
+    assert _rel(y, want) < 1e-2
+    assert _rel(y - x, want - x) < 3e-2
+
+
+def test_zero_residual_is_identity_bitwise():
+    ext, win, dim, heads = (7, 9, 18), (5, 7, 7), 256, 2
+    t = int(np.prod(ext))
+    params = _params(dim, heads, zero_residual=True)
+    x = np.random.default_rng(3).standard_normal((t, dim)).astype(np.float32).astype(np.float64)
+    y = _api().natten_block(x, params, "blk", ext, win, heads).values
+    assert np.array_equal(y, x)
+
+
+def test_longitude_roll_equivariance():
+    ext, win, dim, heads = (2, 7, 10), (1, 3, 3), 24, 4
+    d, h, w = ext
+    params = _params(dim, heads, seed=3)
+    x = np.random.default_rng(4).standard_normal((d, h, w, dim))
+    y = _api().natten_block(x.reshape(-1, dim), params, "blk", ext, win, heads).values.reshape(d, h, w, dim)
+    for shift in (1, 3, w - 2):
+        xs = np.roll(x, shift, axis=2)
+        ys = _api().natten_block(xs.reshape(-1, dim), params, "blk", ext, win, heads).values
+        assert _rel(ys.reshape(d, h, w, dim), np.roll(y, shift, axis=2)) < 1e-2
+
+
+def test_attention_weights_probe():
+    ext, win, dim, heads = (2, 7, 10), (1, 3, 3), 24, 4
+    t = int(np.prod(ext))
+    params = _params(dim, heads, seed=1)
+    x = np.random.default_rng(5).standard_normal((t, dim))
+    got = _api().attention_weights(x, params, "blk", ext, win, heads)
+    want = om.attention_weights(x, params, "blk", ext, win, heads)
+    assert got.shape == (t, heads, 9)
+    np.testing.assert_allclose(got.sum(-1), 1.0, atol=1e-5)
+    assert (got > 0).all()
+    assert np.abs(got - want).max() < 2e-2
+
+
+def test_block_errors_before_launch():
+    from paper_2503_22235_b200.errors import ConfigError
+    params = _params(24, 4)
+    x = np.zeros((140, 24))
+    with pytest.raises(ConfigError):
+        _api().natten_block(x, params, "blk", (2, 7, 10), (3, 3, 3), 4)
+    with pytest.raises(ConfigError):
+        _api().natten_block(x, params, "blk", (2, 7, 10), (1, 3, 3), 5)
+    with pytest.raises(ConfigError):
+        _api().natten_block(x[:100], params, "blk", (2, 7, 10), (1, 3, 3), 4)
