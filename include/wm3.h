@@ -39,7 +39,8 @@ enum {
 };
 
 /* Rotary description for WM3_EPI_QKV_ROPE (attention.py:48-92).  Output columns are laid out
- * [3][heads][dhp]; within a q/k head, rotation pair j sits at columns (j, j + dhp/2), j < dh/2.
+ * [3][heads][dhp]; within a q/k head, rotation pair j (reference columns j, j + dh/2) sits at the
+ * adjacent columns (2j, 2j + 1), j < dh/2 (a permutation shared by q and k leaves q.k unchanged).
  * rope_cos/rope_sin are [3][emax][64] fp32 per-axis tables (axis 0 depth, 1 row, 2 col); pair
  * j < pd uses the depth table, j < pd+pr the row table, else the col table. */
 typedef struct {
@@ -68,6 +69,12 @@ int wm3_layernorm_bf16(const float* x, int ldx, int m, int n, const float* gain,
  * out: bf16 or f32 depending on epi; ldo in elements; n_valid columns are stored. */
 int wm3_linear(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi,
                void* out, int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, void* stream);
+
+/* As wm3_linear, but output row r goes to plane r / plane_rows, row r % plane_rows of a buffer whose
+ * planes are plane_stride_rows rows apart (latitude-band layout with halo rows between depth planes). */
+int wm3_linear_planes(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi,
+                      void* out, int ldo, int n_valid, const float* bias, const wm3_rope_t* rope,
+                      int planes, int plane_rows, long long plane_stride_rows, void* stream);
 
 /* Fused 3D neighborhood attention forward.
  * qkv: bf16 [T][3][heads][dhp] (row pitch ldqkv elements), out: bf16 [T][heads][dhp] (pitch ldo).

@@ -9,7 +9,7 @@ Weight layout (built once per parameter set, from the reference's (in, out) floa
   * every GEMM weight is stored (out, in) = K-major bf16 so both UMMA operands are K-major SW128 tiles;
   * K and N are padded to the kernels' granularity with zero rows/columns (exact);
   * heads are padded to dhp in {64, 128}; within a q/k head the rotary pair (j, j + dh/2) of the reference
-    is placed at columns (j, j + dhp/2) — the same permutation on q and k leaves q.k unchanged.
+    is placed at the adjacent columns (2j, 2j + 1) — the same permutation on q and k leaves q.k unchanged.
 """
 
 from __future__ import annotations
@@ -103,13 +103,17 @@ class BlockWeights:
 
 
 def _qk_perm(heads: int, dh: int, dhp: int) -> np.ndarray:
-    """Padded column -> reference column (or -1) for a q/k section."""
+    """Padded column -> reference column (or -1) for a q/k section.
+
+    Rotary pair j of the reference, columns (j, j + dh/2) (attention.py:87-92), lands on the adjacent
+    columns (2j, 2j + 1) so every 64-column epilogue chunk holds whole pairs.
+    """
     m = np.full(heads * dhp, -1, dtype=np.int64)
-    half, halfp = dh // 2, dhp // 2
+    half = dh // 2
     for hh in range(heads):
         for j in range(half):
-            m[hh * dhp + j] = hh * dh + j
-            m[hh * dhp + halfp + j] = hh * dh + half + j
+            m[hh * dhp + 2 * j] = hh * dh + j
+            m[hh * dhp + 2 * j + 1] = hh * dh + half + j
     return m
 
 

@@ -2,12 +2,14 @@
 //
 //   C[M, N] = A[M, K] * B[N, K]^T     A: activations bf16 (K-major), B: weights bf16 pre-transposed
 //                                     to (out, in) so both operands are K-major SWIZZLE_128B tiles.
-// Roles (one CTA per SM, 256 threads):
-//   warp 0      TMA producer: A/B k-blocks into a STAGES-deep smem ring (mbarrier full/empty)
-//   warp 1      MMA issuer: one thread issues tcgen05.mma 128xBNx16, accumulator in TMEM,
-//               double-buffered (2 x BN columns) so the epilogue of tile i overlaps MMAs of tile i+1
-//   warp 2      TMEM allocator
-//   warps 4..7  epilogue: tcgen05.ld 32 columns at a time, bias / GELU / residual / rotary, store
+// Roles (one CTA per SM, 384 threads):
+//   warp 0       TMA producer: A/B k-blocks into a STAGES-deep smem ring (mbarrier full/empty)
+//   warp 1       MMA issuer: one thread issues tcgen05.mma 128xBNx16, accumulator in TMEM,
+//                double-buffered (2 x BN columns) so the epilogue of tile i overlaps the MMAs of tile i+1
+//   warp 2       TMEM allocator
+//   warps 4..11  epilogue, two groups of 4 warps (each group covers the 128 TMEM lanes) working on
+//                alternating column chunks: tcgen05.ld -> bias / GELU / rotary / residual in registers ->
+//                SWIZZLE_128B smem staging -> TMA store (coalesced, asynchronous, clipped at the edges).
 // Reference semantics: attention.py:142-143 (_linear), :167-171 (q,k,v + rotary), :179 and :183
 // (residual adds), :182 (exact-erf GELU, autodiff.py:372-382).
 #include "common.cuh"
@@ -17,99 +19,42 @@
 namespace wm3 {
 
 struct EpiParams {
-  void* out;
-  int ldo;
-  int n_valid;
+  const float* resid;  // fp32 residual stream (read), same buffer the output map writes
+  int ld_resid;
   const float* bias;
+  int n_valid;
+  int out_plane_rows;  // output rows per plane of the (cols, rows, planes) output map
+  int out_planes;
   wm3_rope_t rope;
 };
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_THREADS = 384;
+constexpr int EPI_WARP0 = 4;
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int STAGES = (BN == 256) ? 4 : 6;
+  static constexpr int STAGES = 4;
+  static constexpr int STAGING_PER_GROUP = (BN == 256) ? 1 : 2;
   static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
   static constexpr uint32_t B_BYTES = BN * GEMM_BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t STAGING_BYTES = 16384;  // 128 rows x 128 B
+  static constexpr uint32_t SMEM =
+      STAGES * STAGE_BYTES + 2 * STAGING_PER_GROUP * STAGING_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = 2 * BN;
 };
 
-DEVI void store_bf16x32(__nv_bfloat16* dst, const float* v, int nvalid) {
-  if (nvalid >= 32) {
-    uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint4 u;
-      u.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
-      u.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
-      u.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
-      u.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
-      d4[q] = u;
-    }
-  } else {
-    for (int e = 0; e < nvalid; ++e) dst[e] = __float2bfloat16_rn(v[e]);
-  }
-}
-
 template <int EPI>
-DEVI void epi_simple_chunk(const EpiParams& ep, uint32_t (&r)[32], int row, int n) {
-  float v[32];
-#pragma unroll
-  for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
-  const int nvalid = min(32, ep.n_valid - n);
-  if (nvalid <= 0) return;
-  if (EPI != WM3_EPI_F32 && ep.bias != nullptr) {
-    if (nvalid >= 32) {
-      const float4* b4 = reinterpret_cast<const float4*>(ep.bias + n);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        float4 b = __ldg(b4 + q);
-        v[4 * q + 0] += b.x; v[4 * q + 1] += b.y; v[4 * q + 2] += b.z; v[4 * q + 3] += b.w;
-      }
-    } else {
-      for (int e = 0; e < nvalid; ++e) v[e] += __ldg(ep.bias + n + e);
-    }
-  }
-  if (EPI == WM3_EPI_BIAS_GELU_BF16) {
-#pragma unroll
-    for (int e = 0; e < 32; ++e) v[e] = gelu_erf(v[e]);
-  }
-  if (EPI == WM3_EPI_F32 || EPI == WM3_EPI_BIAS_RESID_F32) {
-    float* dst = reinterpret_cast<float*>(ep.out) + static_cast<size_t>(row) * ep.ldo + n;
-    if (nvalid >= 32) {
-      float4* d4 = reinterpret_cast<float4*>(dst);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        if (EPI == WM3_EPI_BIAS_RESID_F32) {
-          float4 x = d4[q];
-          o.x += x.x; o.y += x.y; o.z += x.z; o.w += x.w;
-        }
-        d4[q] = o;
-      }
-    } else {
-      for (int e = 0; e < nvalid; ++e) dst[e] = (EPI == WM3_EPI_BIAS_RESID_F32 ? dst[e] : 0.f) + v[e];
-    }
-  } else {
-    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(ep.out) + static_cast<size_t>(row) * ep.ldo + n;
-    store_bf16x32(dst, v, nvalid);
-  }
-}
+struct EpiTraits {
+  static constexpr bool F32 = (EPI == WM3_EPI_F32 || EPI == WM3_EPI_BIAS_RESID_F32);
+  static constexpr int CW = F32 ? 32 : 64;  // columns per staged chunk (128 B rows)
+};
 
-// q/k/v + bias, rotary (NeoX half split, attention.py:87-92) on the q and k sections.
-template <int BN>
-DEVI void epi_qkv_rope(const EpiParams& ep, uint32_t taddr, int row, int n0, int M) {
-  const wm3_rope_t& rp = ep.rope;
-  const int dhp = rp.dhp;
-  const int half = dhp >> 1;
-  const int heads_per_tile = BN / dhp;
-  const int qk_cols = 2 * rp.heads * dhp;
-  // token coordinates (global row for the rotary phase; attention.py:242 uses global (d,h,w))
-  int t = row < M ? row : 0;
+// Rotary on interleaved pairs: columns (2i, 2i+1) of a q/k head hold the reference pair (i, i + dh/2).
+DEVI void rope_chunk(const wm3_rope_t& rp, int row, int M, int col0_in_head, float (&v)[64]) {
+  const int t = row < M ? row : 0;
   const int c = t % rp.cols;
   const int rr = (t / rp.cols) % rp.rows + rp.row0;
   const int d = t / (rp.cols * rp.rows);
@@ -120,52 +65,34 @@ DEVI void epi_qkv_rope(const EpiParams& ep, uint32_t taddr, int row, int n0, int
   const float* sh = rp.rope_sin + (1 * rp.emax + rr) * 64;
   const float* sw = rp.rope_sin + (2 * rp.emax + c) * 64;
   const int pd = rp.pd, pdr = rp.pd + rp.pr;
-  for (int hh = 0; hh < heads_per_tile; ++hh) {
-    for (int cc = 0; cc < dhp / 64; ++cc) {
-      const int j0 = 32 * cc;
-      const int col1 = hh * dhp + j0;
-      const int col2 = col1 + half;
-      uint32_t r1[32], r2[32];
-      tmem_ld32(taddr + col1, r1);
-      tmem_ld32(taddr + col2, r2);
-      tmem_ld_wait();
-      const int n1 = n0 + col1, n2 = n0 + col2;
-      if (row >= M || n1 >= ep.n_valid) continue;
-      float a[32], b[32];
+  const int i0 = col0_in_head >> 1;
 #pragma unroll
-      for (int e = 0; e < 32; ++e) {
-        a[e] = __uint_as_float(r1[e]) + __ldg(ep.bias + n1 + e);
-        b[e] = __uint_as_float(r2[e]) + __ldg(ep.bias + n2 + e);
-      }
-      if (n1 < qk_cols) {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int j = j0 + e;
-          const float* cp = j < pd ? cd : (j < pdr ? ch : cw);
-          const float* sp = j < pd ? sd : (j < pdr ? sh : sw);
-          const float cs = __ldg(cp + j), sn = __ldg(sp + j);
-          const float x1 = a[e], x2 = b[e];
-          a[e] = x1 * cs - x2 * sn;
-          b[e] = x1 * sn + x2 * cs;
-        }
-      }
-      __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(ep.out) + static_cast<size_t>(row) * ep.ldo;
-      store_bf16x32(base + n1, a, min(32, ep.n_valid - n1));
-      store_bf16x32(base + n2, b, min(32, ep.n_valid - n2));
-    }
+  for (int e = 0; e < 32; ++e) {
+    const int i = i0 + e;
+    const float* cp = i < pd ? cd : (i < pdr ? ch : cw);
+    const float* sp = i < pd ? sd : (i < pdr ? sh : sw);
+    const float cs = __ldg(cp + i), sn = __ldg(sp + i);
+    const float x1 = v[2 * e], x2 = v[2 * e + 1];
+    v[2 * e] = x1 * cs - x2 * sn;
+    v[2 * e + 1] = x1 * sn + x2 * cs;
   }
 }
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, EpiParams ep) {
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmOut, int M, int N, int K, EpiParams ep) {
   using Cfg = GemmCfg<BN>;
+  using Tr = EpiTraits<EPI>;
   constexpr int STAGES = Cfg::STAGES;
+  constexpr int CW = Tr::CW;
+  constexpr int NUNITS = BN / CW;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  const uint32_t staging0 = sbase + STAGES * Cfg::STAGE_BYTES;
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + 2 * Cfg::STAGING_PER_GROUP * Cfg::STAGING_BYTES);
   const uint32_t bar0 = smem_u32(bars);
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
@@ -183,13 +110,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    tma_prefetch(&tmOut);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
-      mbar_init(tempty_bar(a), 4);
+      mbar_init(tempty_bar(a), 8);
     }
     fence_barrier_init();
   }
@@ -250,26 +178,118 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (acc == 0) aphase ^= 1;
       }
     }
-  } else if (warp >= 4) {
-    const int q = warp & 3;
+  } else if (warp >= EPI_WARP0) {
+    const int g = (warp - EPI_WARP0) >> 2;  // epilogue group
+    const int q = warp & 3;                  // TMEM lane quarter
+    const int r_in_tile = 32 * q + lane;
+    const bool elected = (warp == EPI_WARP0 + 4 * g) && lane == 0;
+    const int bar_id = 1 + g;
     int acc = 0;
     uint32_t aphase = 0;
+    int sbuf = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const int m0 = (tile / nn) * GEMM_BM;
       const int n0 = (tile % nn) * BN;
+      const int row = m0 + r_in_tile;
+      const bool row_ok = row < M;
+      // residual prefetch of this group's first chunk (overlaps the mainloop wait)
+      float4 xa[8], xb[8];
+      if (EPI == WM3_EPI_BIAS_RESID_F32) {
+        const float4* src = reinterpret_cast<const float4*>(ep.resid + static_cast<size_t>(row) * ep.ld_resid +
+                                                            n0 + g * CW);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          xa[j] = (row_ok && n0 + g * CW + 4 * j < ep.n_valid) ? src[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
       mbar_wait(tfull_bar(acc), aphase);
       tc_fence_after();
-      const int row = m0 + 32 * q + lane;
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(32 * q) << 16);
-      if (EPI == WM3_EPI_QKV_ROPE) {
-        epi_qkv_rope<BN>(ep, taddr, row, n0, M);
-      } else {
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+#pragma unroll
+      for (int u = g; u < NUNITS; u += 2) {
+        const int n = n0 + u * CW;
+        if (EPI == WM3_EPI_BIAS_RESID_F32 && u + 2 < NUNITS) {
+          const float4* src =
+              reinterpret_cast<const float4*>(ep.resid + static_cast<size_t>(row) * ep.ld_resid + n + 2 * CW);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            xb[j] = (row_ok && n + 2 * CW + 4 * j < ep.n_valid) ? src[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        if (Tr::F32) {
           uint32_t r[32];
-          tmem_ld32(taddr + 32 * c, r);
+          tmem_ld32(taddr + u * CW, r);
           tmem_ld_wait();
-          if (row < M) epi_simple_chunk<EPI>(ep, r, row, n0 + 32 * c);
+          float v[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
+          if (EPI == WM3_EPI_BIAS_RESID_F32) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 b = (n + 4 * j < ep.n_valid) ? __ldg(reinterpret_cast<const float4*>(ep.bias + n) + j)
+                                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+              v[4 * j + 0] += b.x + xa[j].x;
+              v[4 * j + 1] += b.y + xa[j].y;
+              v[4 * j + 2] += b.z + xa[j].z;
+              v[4 * j + 3] += b.w + xa[j].w;
+            }
+          }
+          // staging row: 8 x 16 B chunks of 4 floats
+          if (elected) bulk_wait_read<Cfg::STAGING_PER_GROUP - 1>();
+          named_bar_sync(bar_id, 128);
+          const uint32_t st = staging0 + (g * Cfg::STAGING_PER_GROUP + sbuf) * Cfg::STAGING_BYTES;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            st_shared_v4(st + sw128_off(r_in_tile, j), __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                         __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+        } else {
+          uint32_t r0[32], r1[32];
+          tmem_ld32(taddr + u * CW, r0);
+          tmem_ld32(taddr + u * CW + 32, r1);
+          tmem_ld_wait();
+          float v[64];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            v[e] = __uint_as_float(r0[e]);
+            v[32 + e] = __uint_as_float(r1[e]);
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float4 b = (n + 4 * j < ep.n_valid) ? __ldg(reinterpret_cast<const float4*>(ep.bias + n) + j)
+                                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[4 * j + 0] += b.x; v[4 * j + 1] += b.y; v[4 * j + 2] += b.z; v[4 * j + 3] += b.w;
+          }
+          if (EPI == WM3_EPI_BIAS_GELU_BF16) {
+#pragma unroll
+            for (int e = 0; e < 64; ++e) v[e] = gelu_erf(v[e]);
+          }
+          if (EPI == WM3_EPI_QKV_ROPE) {
+            const int sec = ep.rope.heads * ep.rope.dhp;
+            if (n < 2 * sec) rope_chunk(ep.rope, row, M, (n % sec) % ep.rope.dhp, v);
+          }
+          uint32_t pk[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) pk[e] = pack_bf16(v[2 * e], v[2 * e + 1]);
+          if (elected) bulk_wait_read<Cfg::STAGING_PER_GROUP - 1>();
+          named_bar_sync(bar_id, 128);
+          const uint32_t st = staging0 + (g * Cfg::STAGING_PER_GROUP + sbuf) * Cfg::STAGING_BYTES;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            st_shared_v4(st + sw128_off(r_in_tile, j), pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        }
+        fence_proxy_async();
+        named_bar_sync(bar_id, 128);
+        if (elected) {
+          const uint32_t st = staging0 + (g * Cfg::STAGING_PER_GROUP + sbuf) * Cfg::STAGING_BYTES;
+          const int P = ep.out_plane_rows;
+          const int p = m0 / P;
+          const int r0 = m0 - p * P;
+          tma_store_3d(&tmOut, st, n, r0, p);
+          if (r0 + GEMM_BM > P && p + 1 < ep.out_planes) tma_store_3d(&tmOut, st, n, r0 - P, p + 1);
+          bulk_commit();
+        }
+        if (Cfg::STAGING_PER_GROUP > 1) sbuf ^= 1;
+        if (EPI == WM3_EPI_BIAS_RESID_F32) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) xa[j] = xb[j];
         }
       }
       tc_fence_before();
@@ -278,6 +298,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }
+    if (elected) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -288,8 +309,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 }
 
 template <int BN, int EPI>
-static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiParams& ep,
-                       cudaStream_t stream) {
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, int M, int N, int K,
+                       const EpiParams& ep, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
   auto kern = gemm_tc_kernel<BN, EPI>;
   static bool attr_done = false;
@@ -300,21 +321,65 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int 
   }
   const int ntiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN);
   const int grid = ntiles < sm_count() ? ntiles : sm_count();
-  kern<<<grid, GEMM_THREADS, Cfg::SMEM, stream>>>(ta, tb, M, N, K, ep);
+  kern<<<grid, GEMM_THREADS, Cfg::SMEM, stream>>>(ta, tb, to, M, N, K, ep);
   return check_launch("gemm_tc_kernel");
 }
 
 template <int BN>
-static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
-                        const EpiParams& ep, cudaStream_t s) {
+static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, int M, int N,
+                        int K, const EpiParams& ep, cudaStream_t s) {
   switch (epi) {
-    case WM3_EPI_F32: return launch_gemm<BN, WM3_EPI_F32>(ta, tb, M, N, K, ep, s);
-    case WM3_EPI_BIAS_BF16: return launch_gemm<BN, WM3_EPI_BIAS_BF16>(ta, tb, M, N, K, ep, s);
-    case WM3_EPI_BIAS_GELU_BF16: return launch_gemm<BN, WM3_EPI_BIAS_GELU_BF16>(ta, tb, M, N, K, ep, s);
-    case WM3_EPI_BIAS_RESID_F32: return launch_gemm<BN, WM3_EPI_BIAS_RESID_F32>(ta, tb, M, N, K, ep, s);
-    case WM3_EPI_QKV_ROPE: return launch_gemm<BN, WM3_EPI_QKV_ROPE>(ta, tb, M, N, K, ep, s);
+    case WM3_EPI_F32: return launch_gemm<BN, WM3_EPI_F32>(ta, tb, to, M, N, K, ep, s);
+    case WM3_EPI_BIAS_BF16: return launch_gemm<BN, WM3_EPI_BIAS_BF16>(ta, tb, to, M, N, K, ep, s);
+    case WM3_EPI_BIAS_GELU_BF16: return launch_gemm<BN, WM3_EPI_BIAS_GELU_BF16>(ta, tb, to, M, N, K, ep, s);
+    case WM3_EPI_BIAS_RESID_F32: return launch_gemm<BN, WM3_EPI_BIAS_RESID_F32>(ta, tb, to, M, N, K, ep, s);
+    case WM3_EPI_QKV_ROPE: return launch_gemm<BN, WM3_EPI_QKV_ROPE>(ta, tb, to, M, N, K, ep, s);
     default: return set_error("wm3_linear: unknown epilogue %d", epi);
   }
+}
+
+static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi, void* out,
+                       int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, int planes, int plane_rows,
+                       long long plane_stride_rows, void* stream) {
+  if (m <= 0 || n <= 0 || k <= 0) return set_error("wm3_linear: bad sizes m=%d n=%d k=%d", m, n, k);
+  const bool f32_out = (epi == WM3_EPI_F32 || epi == WM3_EPI_BIAS_RESID_F32);
+  if ((lda % 8) || (ldb % 8) || (ldo % (f32_out ? 4 : 8)))
+    return set_error("wm3_linear: pitches must be multiples of 8 (bf16) / 4 (f32 out)");
+  if (n % 32) return set_error("wm3_linear: n=%d must be a multiple of 32", n);
+  if (n_valid <= 0 || n_valid > n) return set_error("wm3_linear: n_valid=%d outside (0, %d]", n_valid, n);
+  if ((n_valid * (f32_out ? 4 : 2)) % 16)
+    return set_error("wm3_linear: n_valid=%d rows must span a multiple of 16 bytes (TMA store)", n_valid);
+  if (epi != WM3_EPI_F32 && bias == nullptr) return set_error("wm3_linear: bias required");
+  if (planes < 1 || static_cast<long long>(planes) * plane_rows < m)
+    return set_error("wm3_linear: output planes (%d x %d) do not cover m=%d", planes, plane_rows, m);
+  EpiParams ep{};
+  ep.resid = reinterpret_cast<const float*>(out);
+  ep.ld_resid = ldo;
+  ep.bias = bias;
+  ep.n_valid = n_valid;
+  ep.out_plane_rows = plane_rows;
+  ep.out_planes = planes;
+  if (epi == WM3_EPI_BIAS_RESID_F32 && planes != 1) return set_error("wm3_linear: residual output must be 2D");
+  if (epi == WM3_EPI_QKV_ROPE) {
+    if (rope == nullptr) return set_error("wm3_linear: rope descriptor required");
+    ep.rope = *rope;
+    if (ep.rope.dhp != 64 && ep.rope.dhp != 128) return set_error("wm3_linear: dhp must be 64 or 128");
+  }
+  const int bn = (n >= 256) ? 256 : 128;
+  CUtensorMap ta, tb, to;
+  if (make_tmap_2d_bf16(&ta, a, k, m, lda, GEMM_BK, GEMM_BM)) return -1;
+  if (make_tmap_2d_bf16(&tb, b, k, n, ldb, GEMM_BK, bn)) return -1;
+  {
+    const int cw = f32_out ? 32 : 64;
+    uint64_t dims[3] = {static_cast<uint64_t>(n_valid), static_cast<uint64_t>(plane_rows),
+                        static_cast<uint64_t>(planes)};
+    uint64_t strides[2] = {static_cast<uint64_t>(ldo), static_cast<uint64_t>(plane_stride_rows) * ldo};
+    uint32_t box[3] = {static_cast<uint32_t>(cw), static_cast<uint32_t>(GEMM_BM), 1};
+    if (make_tmap(&to, out, f32_out ? TMAP_F32 : TMAP_BF16, 3, dims, strides, box, nullptr)) return -1;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  return bn == 256 ? dispatch_epi<256>(epi, ta, tb, to, m, n, k, ep, s)
+                   : dispatch_epi<128>(epi, ta, tb, to, m, n, k, ep, s);
 }
 
 }  // namespace wm3
@@ -323,27 +388,12 @@ using namespace wm3;
 
 extern "C" int wm3_linear(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi, void* out,
                           int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, void* stream) {
-  if (m <= 0 || n <= 0 || k <= 0) return set_error("wm3_linear: bad sizes m=%d n=%d k=%d", m, n, k);
-  const bool f32_out = (epi == WM3_EPI_F32 || epi == WM3_EPI_BIAS_RESID_F32);
-  if ((lda % 8) || (ldb % 8) || (ldo % (f32_out ? 4 : 8)))
-    return set_error("wm3_linear: pitches must be multiples of 8 (bf16) / 4 (f32 out)");
-  if (n % 32) return set_error("wm3_linear: n=%d must be a multiple of 32", n);
-  if (epi != WM3_EPI_F32 && bias == nullptr) return set_error("wm3_linear: bias required");
-  EpiParams ep{};
-  ep.out = out;
-  ep.ldo = ldo;
-  ep.n_valid = n_valid;
-  ep.bias = bias;
-  if (epi == WM3_EPI_QKV_ROPE) {
-    if (rope == nullptr) return set_error("wm3_linear: rope descriptor required");
-    ep.rope = *rope;
-    if (ep.rope.dhp != 64 && ep.rope.dhp != 128) return set_error("wm3_linear: dhp must be 64 or 128");
-  }
-  const int bn = (n >= 256) ? 256 : 128;
-  if (epi == WM3_EPI_QKV_ROPE && (bn % ep.rope.dhp)) return set_error("wm3_linear: tile/head mismatch");
-  CUtensorMap ta, tb;
-  if (make_tmap_2d_bf16(&ta, a, k, m, lda, GEMM_BK, GEMM_BM)) return -1;
-  if (make_tmap_2d_bf16(&tb, b, k, n, ldb, GEMM_BK, bn)) return -1;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  return bn == 256 ? dispatch_epi<256>(epi, ta, tb, m, n, k, ep, s) : dispatch_epi<128>(epi, ta, tb, m, n, k, ep, s);
+  return linear_impl(a, lda, b, ldb, m, n, k, epi, out, ldo, n_valid, bias, rope, 1, m, m, stream);
+}
+
+extern "C" int wm3_linear_planes(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi,
+                                 void* out, int ldo, int n_valid, const float* bias, const wm3_rope_t* rope,
+                                 int planes, int plane_rows, long long plane_stride_rows, void* stream) {
+  return linear_impl(a, lda, b, ldb, m, n, k, epi, out, ldo, n_valid, bias, rope, planes, plane_rows,
+                     plane_stride_rows, stream);
 }

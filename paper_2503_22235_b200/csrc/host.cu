@@ -52,10 +52,11 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-int make_tmap_bf16(CUtensorMap* map, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_elems,
-                   const uint32_t* box, const uint32_t* elem_strides) {
+int make_tmap(CUtensorMap* map, const void* ptr, int dtype, int rank, const uint64_t* dims,
+              const uint64_t* strides_elems, const uint32_t* box, const uint32_t* elem_strides) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return set_error("cuTensorMapEncodeTiled unavailable");
+  const uint64_t esz = dtype == TMAP_F32 ? 4 : 2;
   cuuint64_t d[5], st[4];
   cuuint32_t b[5], es[5];
   for (int i = 0; i < rank; ++i) {
@@ -63,15 +64,20 @@ int make_tmap_bf16(CUtensorMap* map, const void* ptr, int rank, const uint64_t* 
     b[i] = box[i];
     es[i] = elem_strides ? elem_strides[i] : 1;
   }
-  for (int i = 0; i + 1 < rank; ++i) st[i] = strides_elems[i] * 2;
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), d, st, b, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  for (int i = 0; i + 1 < rank; ++i) st[i] = strides_elems[i] * esz;
+  CUresult r = fn(map, dtype == TMAP_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank,
+                  const_cast<void*>(ptr), d, st, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
-    return set_error("cuTensorMapEncodeTiled failed (%d): rank %d dims %llu %llu box %u %u", int(r), rank,
-                     (unsigned long long)dims[0], (unsigned long long)(rank > 1 ? dims[1] : 0), box[0],
-                     rank > 1 ? box[1] : 0);
+    return set_error("cuTensorMapEncodeTiled failed (%d): rank %d dims %llu %llu %llu box %u %u", int(r), rank,
+                     (unsigned long long)dims[0], (unsigned long long)(rank > 1 ? dims[1] : 0),
+                     (unsigned long long)(rank > 2 ? dims[2] : 0), box[0], rank > 1 ? box[1] : 0);
   return 0;
+}
+
+int make_tmap_bf16(CUtensorMap* map, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_elems,
+                   const uint32_t* box, const uint32_t* elem_strides) {
+  return make_tmap(map, ptr, TMAP_BF16, rank, dims, strides_elems, box, elem_strides);
 }
 
 int make_tmap_2d_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t pitch_elems,
@@ -79,7 +85,7 @@ int make_tmap_2d_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_
   uint64_t dims[2] = {inner, outer};
   uint64_t strides[1] = {pitch_elems};
   uint32_t box[2] = {box_inner, box_outer};
-  return make_tmap_bf16(map, ptr, 2, dims, strides, box, nullptr);
+  return make_tmap(map, ptr, TMAP_BF16, 2, dims, strides, box, nullptr);
 }
 
 }  // namespace wm3

@@ -16,6 +16,10 @@ int sm_count();
 // OOB elements zero-filled.  Box = (box_inner, box_outer); box_inner * 2 must be 128.
 int make_tmap_2d_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t pitch_elems,
                       uint32_t box_inner, uint32_t box_outer);
+enum { TMAP_BF16 = 0, TMAP_F32 = 1 };
+// General tensor map (SWIZZLE_128B, zero OOB fill), rank <= 5; strides in elements for dims 1..rank-1.
+int make_tmap(CUtensorMap* map, const void* ptr, int dtype, int rank, const uint64_t* dims,
+              const uint64_t* strides_elems, const uint32_t* box, const uint32_t* elem_strides);
 // General bf16 tensor map, rank <= 5; strides in elements for dims 1..rank-1.
 int make_tmap_bf16(CUtensorMap* map, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_elems,
                    const uint32_t* box, const uint32_t* elem_strides);
