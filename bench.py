@@ -177,7 +177,7 @@ def run_gpu(args, world, rank, local):
     t = int(np.prod(EXT))
     params = init_block_params(np.random.default_rng(0), DIM, HEADS, "blk", zero_residual=False)
     bw = CACHE.block(params, "blk", HEADS)
-    ws = CACHE.workspace(t, bw)
+    ws = CACHE.workspace(EXT, WIN, bw)
     rope = CACHE.rope(EXT, DIM // HEADS)
     g = torch.Generator(device="cuda").manual_seed(2 + rank)
     x = torch.randn(t, DIM, device="cuda", generator=g)
@@ -214,16 +214,16 @@ def run_gpu(args, world, rank, local):
 
     # ---- per-kernel breakdown (events around each launch, same stream) ----
     from paper_2503_22235_b200 import _lib, ops
-    names = ["layernorm1", "qkv_rope_gemm", "natten", "oproj_resid_gemm", "layernorm2", "w1_gelu_gemm",
-             "w2_resid_gemm"]
+    names = ["layernorm1", "qkv_rope_gemm", "natten", "oproj_resid_gemm", "layernorm2",
+             "w1_gelu_gemm", "w2_resid_gemm"]
     L = _lib
 
     def launches():
         rs = rope.struct(EXT, 0, bw.heads, bw.dhp)
         return [
             lambda: ops.layernorm_bf16(x, bw.ln1_g, bw.ln1_b, out=ws.hn),
-            lambda: ops.linear(ws.hn, bw.w_qkv, L.WM3_EPI_QKV_ROPE, bias=bw.b_qkv, out=ws.qkv, rope=rs),
-            lambda: ops.natten(ws.qkv, EXT, bw.heads, bw.dhp, bw.dh, WIN, out=ws.ctx),
+            lambda: ops.linear_grid(ws.hn, bw.w_qkv, L.WM3_EPI_QKV_ROPE, bw.b_qkv, ws.qkv, ws.grid, rope=rs),
+            lambda: ops.natten(ws.qkv, ws.grid, bw.heads, bw.dhp, bw.dh, WIN, out=ws.ctx),
             lambda: ops.linear(ws.ctx, bw.w_o, L.WM3_EPI_BIAS_RESID_F32, bias=bw.b_o, out=x, n_valid=bw.hidden),
             lambda: ops.layernorm_bf16(x, bw.ln2_g, bw.ln2_b, out=ws.hn),
             lambda: ops.linear(ws.hn, bw.w_1, L.WM3_EPI_BIAS_GELU_BF16, bias=bw.b_1, out=ws.mid),

@@ -70,17 +70,19 @@ int wm3_layernorm_bf16(const float* x, int ldx, int m, int n, const float* gain,
 int wm3_linear(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi,
                void* out, int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, void* stream);
 
-/* As wm3_linear, but output row r goes to plane r / plane_rows, row r % plane_rows of a buffer whose
- * planes are plane_stride_rows rows apart (latitude-band layout with halo rows between depth planes). */
+/* As wm3_linear, with the m GEMM rows split into `planes` planes of plane_rows rows each; plane p row r
+ * is stored at row row_off + p * plane_stride + r of `out` (M-tiles never straddle planes).  This writes a
+ * latitude band's q/k/v into the K/V grid of wm3_natten_fwd, leaving halo rows between depth planes. */
 int wm3_linear_planes(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi,
                       void* out, int ldo, int n_valid, const float* bias, const wm3_rope_t* rope,
-                      int planes, int plane_rows, long long plane_stride_rows, void* stream);
+                      int planes, int plane_rows, long long plane_stride, int row_off, void* stream);
 
 /* Fused 3D neighborhood attention forward.
- * qkv: bf16 [T][3][heads][dhp] (row pitch ldqkv elements), out: bf16 [T][heads][dhp] (pitch ldo).
- * Token grid (depth, rows, cols) is the local band: rows [row0, row0+rows) of a grid with global row
- * extent rows_global; the band's K/V rows may be extended by halos (halo_lo rows before local row 0
- * and halo_hi after) already present in qkv, i.e. qkv row 0 is global row row0 - halo_lo.
+ * qkv: bf16 K/V grid [depth][rows_ext][cols][ldqkv], token channels [3][heads][dhp]; rows_ext =
+ *      halo_lo + rows + halo_hi: the local band rows [row0, row0 + rows) of a grid with global row extent
+ *      rows_global, plus halo rows received from the neighbouring bands.  Longitude wrap is handled inside
+ *      the kernel (a wrapping key patch is fetched as two TMA boxes).
+ * out: bf16 [depth * rows * cols][ldo] (local token order), channels [heads][dhp].
  * scale = 1/sqrt(dh). */
 int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, int depth, int rows, int cols,
                    int rows_global, int row0, int halo_lo, int halo_hi, int heads, int dhp, int wd,

@@ -61,7 +61,8 @@ def natten_block(x, params: dict, prefix: str, extents, window, heads: int) -> T
     if bw.hidden != shape[1]:
         raise ConfigError(f"parameters {prefix} have width {bw.hidden}, tokens have {shape[1]}")
     from .blocks import block_forward
-    block_forward(xd, bw, CACHE.workspace(shape[0], bw), CACHE.rope(extents, dh), tuple(extents), tuple(window))
+    block_forward(xd, bw, CACHE.workspace(extents, window, bw), CACHE.rope(extents, dh), tuple(extents),
+                  tuple(window))
     return Tensor(device=xd)
 
 
@@ -75,15 +76,16 @@ def attention_weights(x_values, params: dict, prefix: str, extents, window, head
     t, dim = xd.shape
     dh = validate_block_args((t, dim), extents, window, heads)
     bw = CACHE.block(params, prefix, heads)
-    ws = CACHE.workspace(t, bw)
+    ws = CACHE.workspace(extents, window, bw)
     rope = CACHE.rope(extents, dh)
     ops.layernorm_bf16(xd, bw.ln1_g, bw.ln1_b, out=ws.hn)
-    ops.linear(ws.hn, bw.w_qkv, _lib.WM3_EPI_QKV_ROPE, bias=bw.b_qkv, out=ws.qkv,
-               rope=rope.struct(extents, 0, bw.heads, bw.dhp))
+    ops.linear_grid(ws.hn, bw.w_qkv, _lib.WM3_EPI_QKV_ROPE, bw.b_qkv, ws.qkv, ws.grid,
+                    rope=rope.struct(extents, 0, bw.heads, bw.dhp))
     table = ops.neighbor_table(extents, window)
     sec = heads * bw.dhp
-    q = ws.qkv[:, :sec].float().view(t, heads, bw.dhp)
-    k = ws.qkv[:, sec:2 * sec].float().view(t, heads, bw.dhp)
+    qkv = ws.grid.interior(ws.qkv)
+    q = qkv[:, :sec].float().view(t, heads, bw.dhp)
+    k = qkv[:, sec:2 * sec].float().view(t, heads, bw.dhp)
     s = torch.einsum("thd,tkhd->thk", q, k[table]) / math.sqrt(dh)
     return torch.softmax(s, dim=-1).double().cpu().numpy()
 

@@ -201,29 +201,37 @@ class RopeTables:
 
 
 class Workspace:
-    """Scratch activations for one (tokens, block geometry); reused across blocks and steps."""
+    """Scratch activations for one (band geometry, block shape); reused across blocks and steps.
 
-    def __init__(self, tokens: int, bw: BlockWeights, device="cuda", kv_tokens: int | None = None):
+    qkv lives in the padded K/V grid of ops.KVGrid (wrap columns + latitude-band halo rows)."""
+
+    def __init__(self, grid: "ops.KVGrid", bw: BlockWeights, device="cuda"):
+        self.grid = grid
+        tokens = grid.depth * grid.rows * grid.cols
         self.tokens = tokens
         self.hn = torch.empty((tokens, bw.kp), dtype=torch.bfloat16, device=device)
-        self.qkv = torch.empty((kv_tokens or tokens, 3 * bw.heads * bw.dhp), dtype=torch.bfloat16, device=device)
+        self.qkv = torch.zeros((grid.tokens, 3 * bw.heads * bw.dhp), dtype=torch.bfloat16, device=device)
         self.ctx = torch.empty((tokens, bw.heads * bw.dhp), dtype=torch.bfloat16, device=device)
         self.mid = torch.empty((tokens, bw.nm), dtype=torch.bfloat16, device=device)
 
-    def fits(self, tokens: int, bw: BlockWeights) -> bool:
-        return (self.tokens == tokens and self.hn.shape[1] == bw.kp and self.mid.shape[1] == bw.nm
-                and self.qkv.shape[1] == 3 * bw.heads * bw.dhp)
 
+def block_forward(x: torch.Tensor, bw: BlockWeights, ws: Workspace, rope: RopeTables, extents, window,
+                  row0: int = 0, rows_global: int | None = None, halo_exchange=None) -> None:
+    """In-place x (T, hidden) fp32 <- natten_block(x) on the current stream.
 
-def block_forward(x: torch.Tensor, bw: BlockWeights, ws: Workspace, rope: RopeTables, extents, window) -> None:
-    """In-place x (T, hidden) fp32 <- natten_block(x).  7 launches on the current stream."""
-    d, h, w = extents
-    t = d * h * w
+    extents are the local (band) token extents; row0 / rows_global place the band in the global grid
+    (rotary phases and window bumps use global rows).  halo_exchange(qkv, grid), when given, fills the halo
+    rows of the padded K/V grid from the neighbouring bands between the QKV GEMM and the attention kernel.
+    Launches: LN1, QKV+rotary GEMM, NA, O-proj+residual GEMM, LN2, W1+GELU GEMM, W2+residual GEMM.
+    """
     L = _lib
+    g = ws.grid
     ops.layernorm_bf16(x, bw.ln1_g, bw.ln1_b, out=ws.hn)
-    rs = rope.struct(extents, 0, bw.heads, bw.dhp)
-    ops.linear(ws.hn, bw.w_qkv, L.WM3_EPI_QKV_ROPE, bias=bw.b_qkv, out=ws.qkv, rope=rs)
-    ops.natten(ws.qkv, extents, bw.heads, bw.dhp, bw.dh, window, out=ws.ctx)
+    rs = rope.struct(extents, row0, bw.heads, bw.dhp)
+    ops.linear_grid(ws.hn, bw.w_qkv, L.WM3_EPI_QKV_ROPE, bw.b_qkv, ws.qkv, g, rope=rs)
+    if halo_exchange is not None:
+        halo_exchange(ws.qkv, g)
+    ops.natten(ws.qkv, g, bw.heads, bw.dhp, bw.dh, window, out=ws.ctx, rows_global=rows_global, row0=row0)
     ops.linear(ws.ctx, bw.w_o, L.WM3_EPI_BIAS_RESID_F32, bias=bw.b_o, out=x, n_valid=bw.hidden)
     ops.layernorm_bf16(x, bw.ln2_g, bw.ln2_b, out=ws.hn)
     ops.linear(ws.hn, bw.w_1, L.WM3_EPI_BIAS_GELU_BF16, bias=bw.b_1, out=ws.mid)

@@ -23,8 +23,9 @@ struct EpiParams {
   int ld_resid;
   const float* bias;
   int n_valid;
-  int out_plane_rows;  // output rows per plane of the (cols, rows, planes) output map
-  int out_planes;
+  // GEMM rows form `planes` planes of `plane_rows` rows; M-tiles never straddle a plane, so every tile
+  // is one clipped TMA box store at (n, r0, plane) of the (n, row, plane) output map.
+  int plane_rows, planes, tiles_per_plane;
   wm3_rope_t rope;
 };
 
@@ -102,10 +103,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int nm = (M + GEMM_BM - 1) / GEMM_BM;
+  const int nm = ep.planes * ep.tiles_per_plane;
   const int nn = (N + BN - 1) / BN;
   const int ntiles = nm * nn;
   const int nk = (K + GEMM_BK - 1) / GEMM_BK;
+  // tile -> (plane, first row in plane, first GEMM row)
+  auto tile_rows = [&](int tile, int& plane, int& r0) {
+    const int mt = tile / nn;
+    plane = mt / ep.tiles_per_plane;
+    r0 = (mt - plane * ep.tiles_per_plane) * GEMM_BM;
+    return plane * ep.plane_rows + r0;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -135,7 +143,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int m0 = (tile / nn) * GEMM_BM;
+        int plane, r0;
+        const int m0 = tile_rows(tile, plane, r0);
         const int n0 = (tile % nn) * BN;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1);
@@ -188,10 +197,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint32_t aphase = 0;
     int sbuf = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int m0 = (tile / nn) * GEMM_BM;
+      int plane, r0;
+      const int m0 = tile_rows(tile, plane, r0);
       const int n0 = (tile % nn) * BN;
       const int row = m0 + r_in_tile;
-      const bool row_ok = row < M;
+      const bool row_ok = (r0 + r_in_tile < ep.plane_rows) && row < M;
       // residual prefetch of this group's first chunk (overlaps the mainloop wait)
       float4 xa[8], xb[8];
       if (EPI == WM3_EPI_BIAS_RESID_F32) {
@@ -279,11 +289,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         named_bar_sync(bar_id, 128);
         if (elected) {
           const uint32_t st = staging0 + (g * Cfg::STAGING_PER_GROUP + sbuf) * Cfg::STAGING_BYTES;
-          const int P = ep.out_plane_rows;
-          const int p = m0 / P;
-          const int r0 = m0 - p * P;
-          tma_store_3d(&tmOut, st, n, r0, p);
-          if (r0 + GEMM_BM > P && p + 1 < ep.out_planes) tma_store_3d(&tmOut, st, n, r0 - P, p + 1);
+          tma_store_3d(&tmOut, st, n, r0, plane);  // rows past the plane end are clipped
           bulk_commit();
         }
         if (Cfg::STAGING_PER_GROUP > 1) sbuf ^= 1;
@@ -338,9 +344,15 @@ static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, c
   }
 }
 
+struct OutPlanes {
+  int planes, plane_rows;      // GEMM rows = planes x plane_rows (band tokens in order)
+  long long plane_stride;      // destination rows between consecutive planes
+  int row_off;                 // destination row of GEMM row 0
+};
+
 static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi, void* out,
-                       int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, int planes, int plane_rows,
-                       long long plane_stride_rows, void* stream) {
+                       int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, const OutPlanes& op,
+                       void* stream) {
   if (m <= 0 || n <= 0 || k <= 0) return set_error("wm3_linear: bad sizes m=%d n=%d k=%d", m, n, k);
   const bool f32_out = (epi == WM3_EPI_F32 || epi == WM3_EPI_BIAS_RESID_F32);
   if ((lda % 8) || (ldb % 8) || (ldo % (f32_out ? 4 : 8)))
@@ -350,16 +362,18 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
   if ((n_valid * (f32_out ? 4 : 2)) % 16)
     return set_error("wm3_linear: n_valid=%d rows must span a multiple of 16 bytes (TMA store)", n_valid);
   if (epi != WM3_EPI_F32 && bias == nullptr) return set_error("wm3_linear: bias required");
-  if (planes < 1 || static_cast<long long>(planes) * plane_rows < m)
-    return set_error("wm3_linear: output planes (%d x %d) do not cover m=%d", planes, plane_rows, m);
+  if (op.planes < 1 || static_cast<long long>(op.planes) * op.plane_rows != m || op.plane_stride < op.plane_rows)
+    return set_error("wm3_linear: %d planes x %d rows (stride %lld) do not tile m=%d", op.planes, op.plane_rows,
+                     op.plane_stride, m);
+  if (epi == WM3_EPI_BIAS_RESID_F32 && op.planes != 1) return set_error("wm3_linear: residual output must be 2D");
   EpiParams ep{};
   ep.resid = reinterpret_cast<const float*>(out);
   ep.ld_resid = ldo;
   ep.bias = bias;
   ep.n_valid = n_valid;
-  ep.out_plane_rows = plane_rows;
-  ep.out_planes = planes;
-  if (epi == WM3_EPI_BIAS_RESID_F32 && planes != 1) return set_error("wm3_linear: residual output must be 2D");
+  ep.plane_rows = op.plane_rows;
+  ep.planes = op.planes;
+  ep.tiles_per_plane = (op.plane_rows + GEMM_BM - 1) / GEMM_BM;
   if (epi == WM3_EPI_QKV_ROPE) {
     if (rope == nullptr) return set_error("wm3_linear: rope descriptor required");
     ep.rope = *rope;
@@ -371,11 +385,13 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
   if (make_tmap_2d_bf16(&tb, b, k, n, ldb, GEMM_BK, bn)) return -1;
   {
     const int cw = f32_out ? 32 : 64;
-    uint64_t dims[3] = {static_cast<uint64_t>(n_valid), static_cast<uint64_t>(plane_rows),
-                        static_cast<uint64_t>(planes)};
-    uint64_t strides[2] = {static_cast<uint64_t>(ldo), static_cast<uint64_t>(plane_stride_rows) * ldo};
+    const size_t esz = f32_out ? 4 : 2;
+    const char* base = reinterpret_cast<const char*>(out) + static_cast<size_t>(op.row_off) * ldo * esz;
+    uint64_t dims[3] = {static_cast<uint64_t>(n_valid), static_cast<uint64_t>(op.plane_rows),
+                        static_cast<uint64_t>(op.planes)};
+    uint64_t strides[2] = {static_cast<uint64_t>(ldo), static_cast<uint64_t>(op.plane_stride) * ldo};
     uint32_t box[3] = {static_cast<uint32_t>(cw), static_cast<uint32_t>(GEMM_BM), 1};
-    if (make_tmap(&to, out, f32_out ? TMAP_F32 : TMAP_BF16, 3, dims, strides, box, nullptr)) return -1;
+    if (make_tmap(&to, base, f32_out ? TMAP_F32 : TMAP_BF16, 3, dims, strides, box, nullptr)) return -1;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   return bn == 256 ? dispatch_epi<256>(epi, ta, tb, to, m, n, k, ep, s)
@@ -388,12 +404,13 @@ using namespace wm3;
 
 extern "C" int wm3_linear(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi, void* out,
                           int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, void* stream) {
-  return linear_impl(a, lda, b, ldb, m, n, k, epi, out, ldo, n_valid, bias, rope, 1, m, m, stream);
+  const OutPlanes op{1, m, m, 0};
+  return linear_impl(a, lda, b, ldb, m, n, k, epi, out, ldo, n_valid, bias, rope, op, stream);
 }
 
 extern "C" int wm3_linear_planes(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi,
                                  void* out, int ldo, int n_valid, const float* bias, const wm3_rope_t* rope,
-                                 int planes, int plane_rows, long long plane_stride_rows, void* stream) {
-  return linear_impl(a, lda, b, ldb, m, n, k, epi, out, ldo, n_valid, bias, rope, planes, plane_rows,
-                     plane_stride_rows, stream);
+                                 int planes, int plane_rows, long long plane_stride, int row_off, void* stream) {
+  const OutPlanes op{planes, plane_rows, plane_stride, row_off};
+  return linear_impl(a, lda, b, ldb, m, n, k, epi, out, ldo, n_valid, bias, rope, op, stream);
 }

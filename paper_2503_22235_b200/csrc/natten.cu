@@ -24,19 +24,16 @@
 namespace wm3 {
 
 struct NaParams {
-  const __nv_bfloat16* qkv;
-  int ldqkv;
   __nv_bfloat16* out;
   int ldo;
   int depth, rows, cols, rows_global, row0, halo_lo, rows_ext;
   int heads, dhp, wd, wh, ww;
   int TD, TH, TW, ntd, nth, ntw, nitems;
+  int ncp, nrpc;  // key-chunk box: ncp columns x nrpc rows (fixed for every tile)
   float scale_log2;
 };
 
-constexpr int NA_THREADS = 256;
-constexpr int NA_PRODUCER0 = 160;  // warps 5..7
-constexpr int NA_NPRODUCERS = 96;
+constexpr int NA_THREADS = 192;       // warps 0-3 softmax, 4 MMA, 5 TMA producer
 constexpr uint32_t NA_TILE = 32768;  // 128 rows x 256 B
 // smem: Q | K0 V0 | K1 V1 | P
 constexpr uint32_t NA_SMEM = 6 * NA_TILE + 1024 /*align*/ + 256 /*barriers*/;
@@ -44,9 +41,14 @@ constexpr float NA_RESCALE_LOG2 = 8.0f;
 
 struct TileGeo {
   int head, d0, d1, h0, h1, w0, w1;
-  int kd_lo, kr_lo, kr_hi, pc0, ncp, nrpc, nrchunks, nchunks;
+  int kd_lo, kr_lo, kr_hi, pc0, ncp, nrpc, nrchunks, nparts, nchunks;
 };
 
+// Key patch of a tile: depth planes [kd_lo, kd_hi), rows [kr_lo, kr_hi) (global, bumped like grid.py:96-101),
+// columns either the whole circle (pc0 = 0, ncp = W) or the arc [pc0, pc0 + ncp) with pc0 = w0 - hw, which
+// may cross the longitude seam.  A crossing arc is fetched as two TMA boxes of the same shape: part 0 at
+// origin pc0 and part 1 at origin pc0 -/+ W; out-of-range columns of each box are zero-filled by TMA and
+// masked, so together the two parts hold every key of the arc exactly once.
 DEVI TileGeo tile_geo(const NaParams& p, int item) {
   TileGeo g;
   const int ntiles = p.ntd * p.nth * p.ntw;
@@ -63,19 +65,35 @@ DEVI TileGeo tile_geo(const NaParams& p, int item) {
   g.kr_lo = bump_start(g.h0 + p.row0, p.rows_global, p.wh);
   g.kr_hi = bump_start(g.h1 - 1 + p.row0, p.rows_global, p.wh) + p.wh;
   const int hw = (p.ww - 1) / 2;
-  if ((g.w1 - g.w0) + p.ww - 1 >= p.cols) { g.pc0 = 0; g.ncp = p.cols; }
-  else { g.pc0 = g.w0 - hw; g.ncp = (g.w1 - g.w0) + p.ww - 1; }
+  g.ncp = p.ncp;
+  const bool circle = (p.ncp == p.cols);
+  g.pc0 = circle ? 0 : g.w0 - hw;
+  const int arc_end = g.w1 - 1 + (p.ww - 1 - hw);  // last column any query of the tile needs
+  g.nparts = (!circle && (g.pc0 < 0 || arc_end >= p.cols)) ? 2 : 1;
+  g.nrpc = p.nrpc;
   const int nrows_u = g.kr_hi - g.kr_lo;
-  g.nrpc = min(nrows_u, 128 / g.ncp);
   g.nrchunks = (nrows_u + g.nrpc - 1) / g.nrpc;
-  g.nchunks = (kd_hi - g.kd_lo) * g.nrchunks;
+  g.nchunks = (kd_hi - g.kd_lo) * g.nrchunks * g.nparts;
   return g;
 }
 
-DEVI void chunk_geo(const TileGeo& g, int j, int& kd, int& kr0, int& nr) {
-  kd = g.kd_lo + j / g.nrchunks;
-  kr0 = g.kr_lo + (j % g.nrchunks) * g.nrpc;
+// chunk j -> depth plane, first key row, column origin and the patch columns [vlo, vhi) it holds
+DEVI void chunk_geo(const TileGeo& g, int cols, int j, int& kd, int& kr0, int& nr, int& origin, int& vlo,
+                    int& vhi) {
+  const int part = j % g.nparts;
+  const int jr = j / g.nparts;
+  kd = g.kd_lo + jr / g.nrchunks;
+  kr0 = g.kr_lo + (jr % g.nrchunks) * g.nrpc;
   nr = min(g.nrpc, g.kr_hi - kr0);
+  // patch column cc is global column pc0 + cc; part 0 holds those inside [0, W), part 1 the wrapped ones
+  const int in_lo = max(0, -g.pc0), in_hi = min(g.ncp, cols - g.pc0);
+  if (part == 0) {
+    origin = g.pc0; vlo = in_lo; vhi = in_hi;
+  } else if (g.pc0 < 0) {
+    origin = g.pc0 + cols; vlo = 0; vhi = in_lo;
+  } else {
+    origin = g.pc0 - cols; vlo = in_hi; vhi = g.ncp;
+  }
 }
 
 // bits [a, b) of a 64-bit word (a, b clamped to [0, 64])
@@ -87,7 +105,8 @@ DEVI uint64_t bits64(int a, int b) {
   return hi & ~((1ull << a) - 1ull);
 }
 
-__global__ void __launch_bounds__(NA_THREADS, 1) natten_fwd_kernel(NaParams p) {
+__global__ void __launch_bounds__(NA_THREADS, 1)
+    natten_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, NaParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sQ = smem_u32(smem);
@@ -109,10 +128,10 @@ __global__ void __launch_bounds__(NA_THREADS, 1) natten_fwd_kernel(NaParams p) {
   const int lane = tid & 31;
 
   if (tid == 0) {
-    mbar_init(bar_qfull, NA_NPRODUCERS);
+    mbar_init(bar_qfull, 1);
     mbar_init(bar_qempty, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(bar_kvfull(s), NA_NPRODUCERS);
+      mbar_init(bar_kvfull(s), 1);
       mbar_init(bar_kvempty(s), 1);
       mbar_init(bar_sfull(s), 1);
       mbar_init(bar_sempty(s), 4);
@@ -127,6 +146,9 @@ __global__ void __launch_bounds__(NA_THREADS, 1) natten_fwd_kernel(NaParams p) {
     tmem_alloc(smem_u32(tmem_slot), 512);
     tmem_relinquish();
   }
+  // Zero the operand tiles once: rows past a box are never written by TMA and V rows feed P V (0 * NaN).
+  for (uint32_t off = tid * 16u; off < 5 * NA_TILE; off += NA_THREADS * 16u) st_shared_v4(sQ + off, 0, 0, 0, 0);
+  fence_proxy_async();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -134,85 +156,36 @@ __global__ void __launch_bounds__(NA_THREADS, 1) natten_fwd_kernel(NaParams p) {
   const int sec = p.heads * p.dhp;  // columns per q/k/v section
   const int brow0 = p.row0 - p.halo_lo;
 
-  if (tid >= NA_PRODUCER0) {
-    // =============================== producers ===============================
-    const int pt = tid - NA_PRODUCER0;
-    const int cpr = p.dhp >> 3;  // 16-byte chunks per row (8 or 16)
-    const int c16 = pt % cpr;
-    const int rstep = NA_NPRODUCERS / cpr;
-    const int r_first = pt / cpr;
-    int chunk_ctr = 0, tile_ctr = 0;
-    uint32_t pend0 = 0, pend1 = 0;  // barriers whose cp.async group is still in flight (0 = none)
-    auto flush = [&]() {
-      if (pend0 | pend1) {
-        cp_async_wait<0>();
-        fence_proxy_async();
-        if (pend0) mbar_arrive(pend0);
-        if (pend1) mbar_arrive(pend1);
-        pend0 = pend1 = 0;
-      }
-    };
-    auto retire_older = [&](uint32_t newest) {  // all but the newest committed group are complete
-      cp_async_wait<1>();
-      fence_proxy_async();
-      if (pend0) mbar_arrive(pend0);
-      if (pend1) mbar_arrive(pend1);
-      pend0 = newest;
-      pend1 = 0;
-    };
-    for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
-      const TileGeo g = tile_geo(p, item);
-      // ---- Q tile ----
-      flush();
-      mbar_wait(bar_qempty, (tile_ctr & 1) ^ 1);
-      {
-        const __nv_bfloat16* qb = p.qkv + g.head * p.dhp + c16 * 8;
-        const int tq = p.TD * p.TH * p.TW;
-        for (int r = r_first; r < 128; r += rstep) {
-          const int rd = g.d0 + r / (p.TH * p.TW), rh = g.h0 + (r / p.TW) % p.TH, rw = g.w0 + r % p.TW;
-          const bool ok = r < tq && rd < g.d1 && rh < g.h1 && rw < g.w1;
-          const size_t tok = ok ? static_cast<size_t>((rd * p.rows_ext + rh + p.halo_lo) * p.cols + rw) : 0;
-          cp_async_16(sQ + (c16 >> 3) * 16384u + sw128_off(r, c16 & 7), qb + tok * p.ldqkv, ok ? 16u : 0u);
-        }
-      }
-      cp_async_commit();
-      pend1 = pend0;
-      pend0 = bar_qfull;  // newest
-      // ---- K/V chunks ----
-      for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
-        const int slot = chunk_ctr & 1;
-        int kd, kr0, nr;
-        chunk_geo(g, j, kd, kr0, nr);
-        const int nkeys = nr * g.ncp;
-        // The slot frees when PV of chunk c-2 retires, which the MMA thread issues only after S of chunk
-        // c-1, which needs chunk c-1's arrival: publish pending groups before blocking.
-        if (!mbar_try_wait(bar_kvempty(slot), ((chunk_ctr >> 1) & 1) ^ 1)) {
-          flush();
+  if (warp == 5) {
+    // =============================== TMA producer ===============================
+    if (lane == 0) {
+      tma_prefetch(&tmQ);
+      tma_prefetch(&tmKV);
+      const int halves = p.dhp / 64;
+      const uint32_t qbytes = halves * 128u * p.TW * p.TH * p.TD;
+      const uint32_t kvbytes = 2u * halves * 128u * p.ncp * p.nrpc;
+      int chunk_ctr = 0, tile_ctr = 0;
+      for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
+        const TileGeo g = tile_geo(p, item);
+        mbar_wait(bar_qempty, (tile_ctr & 1) ^ 1);
+        mbar_arrive_expect_tx(bar_qfull, qbytes);
+        for (int h = 0; h < halves; ++h)
+          tma_load_4d(sQ + h * 16384u, &tmQ, bar_qfull, g.head * p.dhp + 64 * h, g.w0, g.h0 + p.halo_lo, g.d0);
+        for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
+          const int slot = chunk_ctr & 1;
+          int kd, kr0, nr, origin, vlo, vhi;
+          chunk_geo(g, p.cols, j, kd, kr0, nr, origin, vlo, vhi);
           mbar_wait(bar_kvempty(slot), ((chunk_ctr >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(bar_kvfull(slot), kvbytes);
+          const int c1 = origin, c2 = kr0 - brow0;  // may be negative / past the edge: TMA zero-fills
+          for (int h = 0; h < halves; ++h) {
+            tma_load_4d(sK(slot) + h * 16384u, &tmKV, bar_kvfull(slot), sec + g.head * p.dhp + 64 * h, c1, c2, kd);
+            tma_load_4d(sV(slot) + h * 16384u, &tmKV, bar_kvfull(slot), 2 * sec + g.head * p.dhp + 64 * h, c1, c2,
+                        kd);
+          }
         }
-        const __nv_bfloat16* kb = p.qkv + sec + g.head * p.dhp + c16 * 8;
-        const __nv_bfloat16* vb = kb + sec;
-        const uint32_t dk = sK(slot) + (c16 >> 3) * 16384u;
-        const uint32_t dv = sV(slot) + (c16 >> 3) * 16384u;
-        int rr = r_first / g.ncp, cc = r_first - (r_first / g.ncp) * g.ncp;
-        const int step_r = rstep / g.ncp, step_c = rstep - step_r * g.ncp;
-        const size_t plane_base = static_cast<size_t>(kd) * p.rows_ext;
-        for (int r = r_first; r < 128; r += rstep) {
-          const bool ok = r < nkeys;
-          const size_t tok =
-              ok ? (plane_base + (kr0 + rr - brow0)) * p.cols + wrap_col(g.pc0 + cc, p.cols) : 0;
-          const uint32_t so = sw128_off(r, c16 & 7);
-          cp_async_16(dk + so, kb + tok * p.ldqkv, ok ? 16u : 0u);
-          cp_async_16(dv + so, vb + tok * p.ldqkv, ok ? 16u : 0u);
-          rr += step_r;
-          cc += step_c;
-          if (cc >= g.ncp) { cc -= g.ncp; ++rr; }
-        }
-        cp_async_commit();
-        retire_older(bar_kvfull(slot));
       }
     }
-    flush();
   } else if (warp == 4) {
     // =============================== MMA issuer ===============================
     if (lane == 0) {
@@ -272,23 +245,26 @@ __global__ void __launch_bounds__(NA_THREADS, 1) natten_fwd_kernel(NaParams p) {
       const bool qvalid = tid < p.TD * p.TH * p.TW && qd < g.d1 && qh < g.h1 && qw < g.w1;
       const int q_sd = bump_start(qvalid ? qd : g.d0, p.depth, p.wd);
       const int q_sh = bump_start((qvalid ? qh : g.h0) + p.row0, p.rows_global, p.wh);
-      // window columns inside the patch: [c_lo, c_lo + ww) mod ncp-circle
-      const int c_lo = wrap_col((qvalid ? qw : g.w0) - hw - g.pc0, p.cols);
+      // window columns in patch coordinates: [c_lo, c_lo + ww), taken mod W for a full-circle patch
+      const bool circle = (g.ncp == p.cols);
+      const int c_lo = circle ? wrap_col((qvalid ? qw : g.w0) - hw, p.cols) : (qvalid ? qw : g.w0) - hw - g.pc0;
       float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
         const int slot = chunk_ctr & 1;
-        int kd, kr0, nr;
-        chunk_geo(g, j, kd, kr0, nr);
+        int kd, kr0, nr, origin, vlo, vhi;
+        chunk_geo(g, p.cols, j, kd, kr0, nr, origin, vlo, vhi);
         // ---- validity bitmask over the 128 key columns of this chunk ----
         uint64_t mk0 = 0, mk1 = 0;
         if (qvalid && kd >= q_sd && kd < q_sd + p.wd) {
           const int rlo = max(0, q_sh - kr0), rhi = min(nr, q_sh + p.wh - kr0);
-          const int s1hi = min(c_lo + p.ww, g.ncp);
-          const int s2hi = c_lo + p.ww - g.ncp;  // wrapped part (full-circle patch only)
+          // segment 1: [c_lo, c_lo + ww) clipped to the columns this chunk holds; segment 2: the part of a
+          // full-circle window that wraps past column W - 1
+          const int s1lo = max(c_lo, vlo), s1hi = min(c_lo + p.ww, vhi);
+          const int s2hi = circle ? c_lo + p.ww - g.ncp : 0;
           for (int rr = rlo; rr < rhi; ++rr) {
             const int base = rr * g.ncp;
-            mk0 |= bits64(base + c_lo, base + s1hi);
-            mk1 |= bits64(base + c_lo - 64, base + s1hi - 64);
+            mk0 |= bits64(base + s1lo, base + s1hi);
+            mk1 |= bits64(base + s1lo - 64, base + s1hi - 64);
             if (s2hi > 0) {
               mk0 |= bits64(base, base + s2hi);
               mk1 |= bits64(base - 64, base + s2hi - 64);
@@ -411,21 +387,25 @@ __global__ void natten_windows_kernel(int depth, int rows, int cols, int rows_gl
   }
 }
 
-// Host-side query-tile choice: minimise (#tiles x (#chunks + 1)) over TD x TH x TW <= 128.
-static void choose_tile(int depth, int rows, int cols, int wd, int wh, int ww, int* TD, int* TH, int* TW) {
+// Host-side query-tile choice: minimise (#tiles x (#chunks + 1)) over TD x TH x TW <= 128; also returns
+// the fixed key-chunk box (ncp columns x nrpc rows, <= 128 keys).
+static void choose_tile(int depth, int rows, int cols, int rows_global, int wd, int wh, int ww, int* TD, int* TH,
+                        int* TW, int* NCP, int* NRPC) {
   long best = -1;
   for (int td = 1; td <= depth && td <= 128; ++td)
     for (int th = 1; th <= rows && td * th <= 128; ++th)
       for (int tw = 1; tw <= cols && td * th * tw <= 128; ++tw) {
         const int ncp = (tw + ww - 1 >= cols) ? cols : tw + ww - 1;
         if (ncp > 128) continue;
-        const int nr_u = (th + wh - 1 < rows) ? th + wh - 1 : rows;
+        const int nr_u = (th + wh - 1 < rows_global) ? th + wh - 1 : rows_global;
         const int nd_u = (td + wd - 1 < depth) ? td + wd - 1 : depth;
         const int nrpc = (nr_u < 128 / ncp) ? nr_u : 128 / ncp;
         const int nch = nd_u * ((nr_u + nrpc - 1) / nrpc);
         const long tiles = static_cast<long>((depth + td - 1) / td) * ((rows + th - 1) / th) * ((cols + tw - 1) / tw);
         const long cost = tiles * (nch + 1);
-        if (best < 0 || cost < best) { best = cost; *TD = td; *TH = th; *TW = tw; }
+        if (best < 0 || cost < best) {
+          best = cost; *TD = td; *TH = th; *TW = tw; *NCP = ncp; *NRPC = nrpc;
+        }
       }
 }
 
@@ -450,20 +430,28 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
                        need_hi);
   }
   if ((ldqkv % 8) || (ldo % 8)) return set_error("wm3_natten_fwd: pitches must be multiples of 8");
+  if (ldqkv < 3 * heads * dhp) return set_error("wm3_natten_fwd: ldqkv < 3 * heads * dhp");
   NaParams p{};
-  p.qkv = reinterpret_cast<const __nv_bfloat16*>(qkv);
-  p.ldqkv = ldqkv;
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
   p.ldo = ldo;
   p.depth = depth; p.rows = rows; p.cols = cols; p.rows_global = rows_global; p.row0 = row0;
   p.halo_lo = halo_lo; p.rows_ext = rows + halo_lo + halo_hi;
   p.heads = heads; p.dhp = dhp; p.wd = wd; p.wh = wh; p.ww = ww;
-  choose_tile(depth, rows, cols, wd, wh, ww, &p.TD, &p.TH, &p.TW);
+  choose_tile(depth, rows, cols, rows_global, wd, wh, ww, &p.TD, &p.TH, &p.TW, &p.ncp, &p.nrpc);
   p.ntd = (depth + p.TD - 1) / p.TD;
   p.nth = (rows + p.TH - 1) / p.TH;
   p.ntw = (cols + p.TW - 1) / p.TW;
   p.nitems = p.ntd * p.nth * p.ntw * heads;
   p.scale_log2 = scale * 1.4426950408889634f;
+  const uint64_t wp = cols;
+  const uint64_t dims[4] = {static_cast<uint64_t>(3 * heads * dhp), wp, static_cast<uint64_t>(p.rows_ext),
+                            static_cast<uint64_t>(depth)};
+  const uint64_t strides[3] = {static_cast<uint64_t>(ldqkv), wp * ldqkv, wp * p.rows_ext * ldqkv};
+  const uint32_t qbox[4] = {64, static_cast<uint32_t>(p.TW), static_cast<uint32_t>(p.TH), static_cast<uint32_t>(p.TD)};
+  const uint32_t kvbox[4] = {64, static_cast<uint32_t>(p.ncp), static_cast<uint32_t>(p.nrpc), 1};
+  CUtensorMap tq, tkv;
+  if (make_tmap(&tq, qkv, TMAP_BF16, 4, dims, strides, qbox, nullptr)) return -1;
+  if (make_tmap(&tkv, qkv, TMAP_BF16, 4, dims, strides, kvbox, nullptr)) return -1;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(natten_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, NA_SMEM);
@@ -471,7 +459,7 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
     attr = true;
   }
   const int grid = p.nitems < sm_count() ? p.nitems : sm_count();
-  natten_fwd_kernel<<<grid, NA_THREADS, NA_SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(p);
+  natten_fwd_kernel<<<grid, NA_THREADS, NA_SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(tq, tkv, p);
   return check_launch("natten_fwd_kernel");
 }
 

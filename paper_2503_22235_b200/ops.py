@@ -84,19 +84,68 @@ def ctypes_byref(obj):
     return ctypes.byref(obj)
 
 
-def natten(qkv: torch.Tensor, extents, heads: int, dhp: int, dh: int, window,
-           out: torch.Tensor | None = None, rows_global: int | None = None, row0: int = 0,
-           halo_lo: int = 0, halo_hi: int = 0) -> torch.Tensor:
-    """Fused neighborhood attention over qkv (T_ext, 3*heads*dhp) -> ctx (T, heads*dhp) bf16."""
+class KVGrid:
+    """Geometry of the K/V token grid consumed by the fused attention kernel.
+
+    Tokens live at [depth][halo_lo + rows + halo_hi][cols]: the band's own rows plus latitude-band halo rows
+    received from the neighbouring bands (none on a single GPU).  Longitude wrap needs no padding: the
+    kernel fetches a seam-crossing key patch as two TMA boxes.
+    """
+
+    def __init__(self, extents, window=None, halo_lo: int = 0, halo_hi: int = 0):
+        self.depth, self.rows, self.cols = (int(e) for e in extents)
+        self.halo_lo, self.halo_hi = int(halo_lo), int(halo_hi)
+        self.rows_ext = self.rows + self.halo_lo + self.halo_hi
+
+    @property
+    def tokens(self) -> int:
+        return self.depth * self.rows_ext * self.cols
+
+    def interior(self, buf: torch.Tensor) -> torch.Tensor:
+        """(T, C) copy of the band's own tokens in token order (debug / probes)."""
+        g = buf.view(self.depth, self.rows_ext, self.cols, -1)
+        return g[:, self.halo_lo:self.halo_lo + self.rows].reshape(self.depth * self.rows * self.cols, -1)
+
+
+def linear_grid(a: torch.Tensor, w: torch.Tensor, epi: int, bias: torch.Tensor, out: torch.Tensor, grid: KVGrid,
+                rope: "_lib.RopeT | None" = None) -> torch.Tensor:
+    """linear() whose output rows (band tokens) land in the K/V grid `out` (halo rows left untouched)."""
+    _req(a, torch.bfloat16, "a")
+    _req(w, torch.bfloat16, "w")
+    _req(out, torch.bfloat16, "out")
+    m, k = a.shape
+    n = w.shape[0]
+    rp = None if rope is None else ctypes_byref(rope)
+    plane = grid.rows * grid.cols
+    check(_lib.lib().wm3_linear_planes(ptr(a), a.stride(0), ptr(w), w.stride(0), m, n, k, int(epi), ptr(out),
+                                       out.stride(0), out.shape[1], ptr(bias), rp, grid.depth, plane,
+                                       grid.rows_ext * grid.cols, grid.halo_lo * grid.cols, stream_ptr()),
+          "wm3_linear_planes")
+    return out
+
+
+def natten(qkv: torch.Tensor, grid: KVGrid, heads: int, dhp: int, dh: int, window,
+           out: torch.Tensor | None = None, rows_global: int | None = None, row0: int = 0) -> torch.Tensor:
+    """Fused neighborhood attention over the padded qkv grid -> ctx (T, heads*dhp) bf16, band token order."""
     _req(qkv, torch.bfloat16, "qkv")
-    d, h, w = (int(e) for e in extents)
+    if qkv.shape[0] != grid.tokens:
+        raise RuntimeError(f"qkv has {qkv.shape[0]} rows, padded grid needs {grid.tokens}")
     wd, wh, ww = (int(e) for e in window)
+    d, h, w = grid.depth, grid.rows, grid.cols
     rg = h if rows_global is None else int(rows_global)
     t = d * h * w
     if out is None:
         out = torch.empty((t, heads * dhp), dtype=torch.bfloat16, device=qkv.device)
     _req(out, torch.bfloat16, "out")
     check(_lib.lib().wm3_natten_fwd(ptr(qkv), qkv.stride(0), ptr(out), out.stride(0), d, h, w, rg, int(row0),
-                                    int(halo_lo), int(halo_hi), int(heads), int(dhp), wd, wh, ww,
+                                    grid.halo_lo, grid.halo_hi, int(heads), int(dhp), wd, wh, ww,
                                     float(1.0 / math.sqrt(dh)), stream_ptr()), "wm3_natten_fwd")
     return out
+
+
+def pad_tokens_to_grid(x: torch.Tensor, grid: KVGrid) -> torch.Tensor:
+    """Place token-ordered rows (T, C) into a fresh K/V grid buffer (tests)."""
+    buf = torch.zeros((grid.tokens, x.shape[1]), dtype=x.dtype, device=x.device)
+    g = buf.view(grid.depth, grid.rows_ext, grid.cols, -1)
+    g[:, grid.halo_lo:grid.halo_lo + grid.rows] = x.view(grid.depth, grid.rows, grid.cols, -1)
+    return buf

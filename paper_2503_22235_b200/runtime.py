@@ -13,6 +13,7 @@ import threading
 import torch
 
 from .blocks import BlockWeights, RopeTables, Workspace, prepare_block
+from .ops import KVGrid
 from .params import block_param_names
 
 _lock = threading.Lock()
@@ -51,12 +52,14 @@ class WeightCache:
                 self._ropes[key] = r
             return r
 
-    def workspace(self, tokens: int, bw: BlockWeights, tag: str = "main", kv_tokens: int | None = None) -> Workspace:
-        key = (tag, tokens, bw.kp, bw.nm, bw.heads, bw.dhp, kv_tokens, torch.cuda.current_device())
+    def workspace(self, extents, window, bw: BlockWeights, halo: tuple[int, int] = (0, 0),
+                  tag: str = "main") -> Workspace:
+        key = (tag, tuple(int(e) for e in extents), int(window[2]), tuple(halo), bw.kp, bw.nm, bw.heads, bw.dhp,
+               torch.cuda.current_device())
         with _lock:
             ws = self._ws.get(key)
             if ws is None:
-                ws = Workspace(tokens, bw, kv_tokens=kv_tokens)
+                ws = Workspace(KVGrid(extents, window, *halo), bw)
                 self._ws[key] = ws
             return ws
 

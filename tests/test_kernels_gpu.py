@@ -129,7 +129,8 @@ def test_natten_matches_gather_reference(ext, win, heads, dhp):
     t = int(np.prod(ext))
     g = torch.Generator(device="cuda").manual_seed(t)
     qkv = (torch.randn(t, 3 * heads * dhp, device="cuda", generator=g) * 1.5).to(torch.bfloat16)
-    out = ops().natten(qkv, ext, heads, dhp, dhp, win)
+    grid = ops().KVGrid(ext, win)
+    out = ops().natten(ops().pad_tokens_to_grid(qkv, grid), grid, heads, dhp, dhp, win)
     ref, _ = na_reference(qkv, ext, heads, dhp, dhp, win)
     torch.cuda.synchronize()
     err = (out.float() - ref).abs().max().item()

@@ -12,7 +12,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 t = int(np.prod(EXT))
 params = init_block_params(np.random.default_rng(0), DIM, HEADS, "blk", zero_residual=False)
 bw = CACHE.block(params, "blk", HEADS)
-ws = CACHE.workspace(t, bw)
+ws = CACHE.workspace(EXT, WIN, bw)
 rope = CACHE.rope(EXT, DIM // HEADS)
 x = torch.randn(t, DIM, device="cuda")
 for _ in range(n):
