@@ -220,6 +220,12 @@ DEVI uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 DEVI float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+// 2^x on the SFU (MUFU.EX2); inputs here are <= 8 (lazy-rescaled softmax), -inf -> 0.
+DEVI float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 // SWIZZLE_128B byte offset of 16-byte chunk `c` (0..7) in row `r` of a tile with 128-byte rows.
 DEVI uint32_t sw128_off(uint32_t r, uint32_t c) { return r * 128u + ((c ^ (r & 7u)) << 4); }

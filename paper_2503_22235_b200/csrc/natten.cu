@@ -5,16 +5,16 @@
 // TMEM lane).  The union of the tile's windows is walked as a list of key chunks, each a run of rows of
 // one depth plane x a contiguous (mod W) run of columns, <= 128 keys.
 //
-// Persistent, warp-specialised CTA (one per SM, 256 threads):
-//   warps 5-7   producers: cp.async gathers of the Q tile and of each chunk's K and V head slices into
-//               SWIZZLE_128B tiles (double-buffered K/V slots), completion signalled on mbarriers
-//   warp 4      MMA issuer (one thread): S = Q K^T into one of two TMEM S buffers (M128 N128 K=dhp),
+// Persistent, warp-specialised CTA (one per SM, 320 threads):
+//   warp 9      TMA producer (one thread): the Q tile (4D box TD x TH x TW) and each chunk's K and V head
+//               slices (4D box ncp x nrpc) into SWIZZLE_128B tiles, double-buffered K/V slots, mbarrier tx
+//   warp 8      MMA issuer (one thread): S = Q K^T into one of two TMEM S buffers (M128 N128 K=dhp),
 //               O += P V (M128 N=dhp K=128, V read MN-major), O accumulated in TMEM across chunks;
 //               S_{j+1} is issued before PV_j so the tensor core works while softmax runs
-//   warps 0-3   softmax (one thread per query row): window bitmask built from the same integer formula
-//               as grid.py (bump on depth/rows, wrap on cols), fp32 running max / sum with lazy O
-//               rescaling (only when the max grows by > 2^8), exp2, P (bf16) -> smem; finally O / l ->
-//               bf16 ctx rows.
+//   warps 0-7   softmax (one thread per query row and key-column half, two warps per TMEM lane quarter):
+//               window bitmask built from the same integer formula as grid.py (bump on depth/rows, wrap on
+//               cols), fp32 running max / sum with lazy O rescaling (only when the max grows by > 2^8),
+//               exp2, P (bf16) -> smem; finally O / l -> bf16 ctx rows.
 // The logits never leave the SM.  Output ctx rows are bf16 [T][heads][dhp] = the O-proj GEMM operand.
 #include "common.cuh"
 #include "launch.h"
@@ -33,10 +33,14 @@ struct NaParams {
   float scale_log2;
 };
 
-constexpr int NA_THREADS = 192;       // warps 0-3 softmax, 4 MMA, 5 TMA producer
+// warps 0-7 softmax (warp w: TMEM lanes 32 (w % 4).., key / O columns half w / 4), 8 MMA, 9 TMA producer
+constexpr int NA_SOFTMAX_WARPS = 8;
+constexpr int NA_MMA_WARP = 8;
+constexpr int NA_TMA_WARP = 9;
+constexpr int NA_THREADS = 320;
 constexpr uint32_t NA_TILE = 32768;  // 128 rows x 256 B
-// smem: Q | K0 V0 | K1 V1 | P
-constexpr uint32_t NA_SMEM = 6 * NA_TILE + 1024 /*align*/ + 256 /*barriers*/;
+// smem: Q | K0 V0 | K1 V1 | P | barriers (256 B) | row reductions (2 halves x 128 rows x fp32)
+constexpr uint32_t NA_SMEM = 6 * NA_TILE + 1024 /*align*/ + 256 /*barriers*/ + 3072 /*reductions*/;
 constexpr float NA_RESCALE_LOG2 = 8.0f;
 
 struct TileGeo {
@@ -116,12 +120,14 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * NA_TILE);
   const uint32_t b0 = smem_u32(bars);
   const uint32_t bar_qfull = b0 + 0, bar_qempty = b0 + 8;
-  auto bar_kvfull = [&](int s) { return b0 + 16 + 8 * s; };
-  auto bar_kvempty = [&](int s) { return b0 + 32 + 8 * s; };
+  auto bar_kfull = [&](int s) { return b0 + 16 + 8 * s; };
+  auto bar_kempty = [&](int s) { return b0 + 32 + 8 * s; };
   auto bar_sfull = [&](int s) { return b0 + 48 + 8 * s; };
   auto bar_sempty = [&](int s) { return b0 + 64 + 8 * s; };
   const uint32_t bar_pfull = b0 + 80, bar_pempty = b0 + 88, bar_ofull = b0 + 96, bar_oempty = b0 + 104;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  auto bar_vfull = [&](int s) { return b0 + 112 + 8 * s; };
+  auto bar_vempty = [&](int s) { return b0 + 128 + 8 * s; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -131,18 +137,20 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
     mbar_init(bar_qfull, 1);
     mbar_init(bar_qempty, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(bar_kvfull(s), 1);
-      mbar_init(bar_kvempty(s), 1);
+      mbar_init(bar_kfull(s), 1);
+      mbar_init(bar_kempty(s), 1);
+      mbar_init(bar_vfull(s), 1);
+      mbar_init(bar_vempty(s), 1);
       mbar_init(bar_sfull(s), 1);
-      mbar_init(bar_sempty(s), 4);
+      mbar_init(bar_sempty(s), NA_SOFTMAX_WARPS);
     }
-    mbar_init(bar_pfull, 4);
+    mbar_init(bar_pfull, NA_SOFTMAX_WARPS);
     mbar_init(bar_pempty, 1);
     mbar_init(bar_ofull, 1);
-    mbar_init(bar_oempty, 4);
+    mbar_init(bar_oempty, NA_SOFTMAX_WARPS);
     fence_barrier_init();
   }
-  if (warp == 4) {
+  if (warp == NA_MMA_WARP) {
     tmem_alloc(smem_u32(tmem_slot), 512);
     tmem_relinquish();
   }
@@ -156,15 +164,29 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
   const int sec = p.heads * p.dhp;  // columns per q/k/v section
   const int brow0 = p.row0 - p.halo_lo;
 
-  if (warp == 5) {
+  if (warp == NA_TMA_WARP) {
     // =============================== TMA producer ===============================
+    // K slots free as soon as S = Q K^T retires, V slots only after P V: K loads run one chunk ahead of V
+    // so the next S never waits on a V slot.
     if (lane == 0) {
       tma_prefetch(&tmQ);
       tma_prefetch(&tmKV);
       const int halves = p.dhp / 64;
       const uint32_t qbytes = halves * 128u * p.TW * p.TH * p.TD;
-      const uint32_t kvbytes = 2u * halves * 128u * p.ncp * p.nrpc;
+      const uint32_t kbytes = halves * 128u * p.ncp * p.nrpc;
       int chunk_ctr = 0, tile_ctr = 0;
+      auto load_kv = [&](const TileGeo& g, int j, int c, bool is_v) {
+        const int slot = c & 1;
+        int kd, kr0, nr, origin, vlo, vhi;
+        chunk_geo(g, p.cols, j, kd, kr0, nr, origin, vlo, vhi);
+        const uint32_t full = is_v ? bar_vfull(slot) : bar_kfull(slot);
+        mbar_wait(is_v ? bar_vempty(slot) : bar_kempty(slot), ((c >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(full, kbytes);
+        const int c1 = origin, c2 = kr0 - brow0;  // may be negative / past the edge: TMA zero-fills
+        const uint32_t dst = is_v ? sV(slot) : sK(slot);
+        const int col = (is_v ? 2 : 1) * sec + g.head * p.dhp;
+        for (int h = 0; h < halves; ++h) tma_load_4d(dst + h * 16384u, &tmKV, full, col + 64 * h, c1, c2, kd);
+      };
       for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
         const TileGeo g = tile_geo(p, item);
         mbar_wait(bar_qempty, (tile_ctr & 1) ^ 1);
@@ -172,21 +194,13 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
         for (int h = 0; h < halves; ++h)
           tma_load_4d(sQ + h * 16384u, &tmQ, bar_qfull, g.head * p.dhp + 64 * h, g.w0, g.h0 + p.halo_lo, g.d0);
         for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
-          const int slot = chunk_ctr & 1;
-          int kd, kr0, nr, origin, vlo, vhi;
-          chunk_geo(g, p.cols, j, kd, kr0, nr, origin, vlo, vhi);
-          mbar_wait(bar_kvempty(slot), ((chunk_ctr >> 1) & 1) ^ 1);
-          mbar_arrive_expect_tx(bar_kvfull(slot), kvbytes);
-          const int c1 = origin, c2 = kr0 - brow0;  // may be negative / past the edge: TMA zero-fills
-          for (int h = 0; h < halves; ++h) {
-            tma_load_4d(sK(slot) + h * 16384u, &tmKV, bar_kvfull(slot), sec + g.head * p.dhp + 64 * h, c1, c2, kd);
-            tma_load_4d(sV(slot) + h * 16384u, &tmKV, bar_kvfull(slot), 2 * sec + g.head * p.dhp + 64 * h, c1, c2,
-                        kd);
-          }
+          load_kv(g, j, chunk_ctr, false);
+          if (j > 0) load_kv(g, j - 1, chunk_ctr - 1, true);
         }
+        load_kv(g, g.nchunks - 1, chunk_ctr - 1, true);
       }
     }
-  } else if (warp == 4) {
+  } else if (warp == NA_MMA_WARP) {
     // =============================== MMA issuer ===============================
     if (lane == 0) {
       const uint32_t idesc_s = make_idesc_bf16(128, 128, 0, 0);
@@ -197,6 +211,7 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
       auto issue_pv = [&](int c, bool first, bool last) {
         const int slot = c & 1;
         mbar_wait(bar_pfull, c & 1);
+        mbar_wait(bar_vfull(slot), (c >> 1) & 1);
         if (first) mbar_wait(bar_oempty, (tile_ctr & 1) ^ 1);
         tc_fence_after();
         for (int s = 0; s < 8; ++s) {
@@ -204,17 +219,16 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
           const uint64_t bd = make_sdesc_sw128(sV(slot) + s * 2048u, 16384, 1024);
           umma_bf16_ss(tO, ad, bd, idesc_o, (!first || s > 0) ? 1u : 0u);
         }
-        umma_commit(bar_kvempty(slot));
+        umma_commit(bar_vempty(slot));
         umma_commit(bar_pempty);
         if (last) umma_commit(bar_ofull);
       };
       for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
         const TileGeo g = tile_geo(p, item);
         mbar_wait(bar_qfull, tile_ctr & 1);
-        const int c0 = chunk_ctr;
         for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
           const int slot = chunk_ctr & 1;
-          mbar_wait(bar_kvfull(slot), (chunk_ctr >> 1) & 1);
+          mbar_wait(bar_kfull(slot), (chunk_ctr >> 1) & 1);
           mbar_wait(bar_sempty(slot), ((chunk_ctr >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t tS = tmem + 128 * slot;
@@ -224,25 +238,33 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
                          idesc_s, s > 0 ? 1u : 0u);
           }
           umma_commit(bar_sfull(slot));
+          umma_commit(bar_kempty(slot));
           if (j == g.nchunks - 1) umma_commit(bar_qempty);
           if (j > 0) issue_pv(chunk_ctr - 1, j - 1 == 0, false);
         }
         issue_pv(chunk_ctr - 1, g.nchunks == 1, true);
-        (void)c0;
       }
     }
-  } else if (warp < 4) {
+  } else if (warp < NA_SOFTMAX_WARPS) {
     // =============================== softmax / epilogue ===============================
-    const uint32_t lane_off = static_cast<uint32_t>(32 * warp) << 16;
+    // Warp w owns query rows 32 (w % 4) .. +32 (its TMEM lane quarter) and half h = w / 4 of the key
+    // columns (P region h) and of the O columns; the two warps of a quarter combine row maxima and sums
+    // through shared memory (named barrier 1 + quarter, 64 threads).
+    const int quarter = warp & 3, half = warp >> 2;
+    const int row = 32 * quarter + lane;  // query row in the tile
+    float* red = reinterpret_cast<float*>(smem + 6 * NA_TILE + 256);  // row maxima [chunk parity][half][128]
+    float* red_l = red + 512;                                            // row sums [half][128]
+    const uint32_t lane_off = static_cast<uint32_t>(32 * quarter) << 16;
     const uint32_t tO = tmem + 256;
+    const int ocols = p.dhp / 2;  // O columns handled by this warp
     const int hw = (p.ww - 1) / 2;
     int chunk_ctr = 0, tile_ctr = 0;
     for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
       const TileGeo g = tile_geo(p, item);
-      const int qd = g.d0 + tid / (p.TH * p.TW);
-      const int qh = g.h0 + (tid / p.TW) % p.TH;
-      const int qw = g.w0 + tid % p.TW;
-      const bool qvalid = tid < p.TD * p.TH * p.TW && qd < g.d1 && qh < g.h1 && qw < g.w1;
+      const int qd = g.d0 + row / (p.TH * p.TW);
+      const int qh = g.h0 + (row / p.TW) % p.TH;
+      const int qw = g.w0 + row % p.TW;
+      const bool qvalid = row < p.TD * p.TH * p.TW && qd < g.d1 && qh < g.h1 && qw < g.w1;
       const int q_sd = bump_start(qvalid ? qd : g.d0, p.depth, p.wd);
       const int q_sh = bump_start((qvalid ? qh : g.h0) + p.row0, p.rows_global, p.wh);
       // window columns in patch coordinates: [c_lo, c_lo + ww), taken mod W for a full-circle patch
@@ -253,102 +275,95 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
         const int slot = chunk_ctr & 1;
         int kd, kr0, nr, origin, vlo, vhi;
         chunk_geo(g, p.cols, j, kd, kr0, nr, origin, vlo, vhi);
-        // ---- validity bitmask over the 128 key columns of this chunk ----
-        uint64_t mk0 = 0, mk1 = 0;
+        // ---- validity bits of this warp's 64 key columns [64 half, 64 half + 64) ----
+        uint64_t mk = 0;
         if (qvalid && kd >= q_sd && kd < q_sd + p.wd) {
           const int rlo = max(0, q_sh - kr0), rhi = min(nr, q_sh + p.wh - kr0);
-          // segment 1: [c_lo, c_lo + ww) clipped to the columns this chunk holds; segment 2: the part of a
-          // full-circle window that wraps past column W - 1
           const int s1lo = max(c_lo, vlo), s1hi = min(c_lo + p.ww, vhi);
           const int s2hi = circle ? c_lo + p.ww - g.ncp : 0;
+          const int off = 64 * half;
           for (int rr = rlo; rr < rhi; ++rr) {
-            const int base = rr * g.ncp;
-            mk0 |= bits64(base + s1lo, base + s1hi);
-            mk1 |= bits64(base + s1lo - 64, base + s1hi - 64);
-            if (s2hi > 0) {
-              mk0 |= bits64(base, base + s2hi);
-              mk1 |= bits64(base - 64, base + s2hi - 64);
-            }
+            const int base = rr * g.ncp - off;
+            mk |= bits64(base + s1lo, base + s1hi);
+            if (s2hi > 0) mk |= bits64(base, base + s2hi);
           }
         }
-        // ---- S -> registers ----
+        // ---- S half -> registers ----
         mbar_wait(bar_sfull(slot), (chunk_ctr >> 1) & 1);
         tc_fence_after();
-        uint32_t s[128];
-        {
-          uint32_t* s0 = s;
-          tmem_ld32(tmem + 128 * slot + lane_off + 0, *reinterpret_cast<uint32_t(*)[32]>(s0));
-          tmem_ld32(tmem + 128 * slot + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(s0 + 32));
-          tmem_ld32(tmem + 128 * slot + lane_off + 64, *reinterpret_cast<uint32_t(*)[32]>(s0 + 64));
-          tmem_ld32(tmem + 128 * slot + lane_off + 96, *reinterpret_cast<uint32_t(*)[32]>(s0 + 96));
-        }
+        uint32_t s[64];
+        tmem_ld32(tmem + 128 * slot + lane_off + 64 * half, *reinterpret_cast<uint32_t(*)[32]>(s));
+        tmem_ld32(tmem + 128 * slot + lane_off + 64 * half + 32, *reinterpret_cast<uint32_t(*)[32]>(s + 32));
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_sempty(slot));
-        // ---- masked row max (log2 domain) ----
+        // ---- masked row max (raw scores), combined with the partner warp ----
         float mx = -INFINITY;
 #pragma unroll
-        for (int k = 0; k < 128; ++k) {
-          const uint64_t w = k < 64 ? mk0 : mk1;
-          const bool ok = (w >> (k & 63)) & 1ull;
-          mx = ok ? fmaxf(mx, __uint_as_float(s[k])) : mx;
-        }
+        for (int k = 0; k < 64; ++k) mx = ((mk >> k) & 1ull) ? fmaxf(mx, __uint_as_float(s[k])) : mx;
+        float* rbuf = red + (chunk_ctr & 1) * 256;  // parity buffers: the partner may still read the last one
+        rbuf[half * 128 + row] = mx;
+        named_bar_sync(1 + quarter, 64);
+        mx = fmaxf(mx, rbuf[(half ^ 1) * 128 + row]);
         mx = mx * p.scale_log2;
         float alpha = 1.f;
-        if (mx > m_run + NA_RESCALE_LOG2) {  // lazy rescale (also covers m_run = -inf)
+        if (mx > m_run + NA_RESCALE_LOG2) {  // lazy rescale (also covers m_run = -inf); same in both warps
           alpha = exp2f(m_run - mx);
           m_run = mx;
         }
         const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
         float lsum = 0.f;
-        uint32_t pk[64];
+        uint32_t pk[32];
 #pragma unroll
-        for (int k = 0; k < 128; k += 2) {
-          const uint64_t w = k < 64 ? mk0 : mk1;
-          const bool ok0 = (w >> (k & 63)) & 1ull;
-          const bool ok1 = (w >> ((k + 1) & 63)) & 1ull;
-          const float p0 = ok0 ? exp2f(fmaf(__uint_as_float(s[k]), p.scale_log2, -m_use)) : 0.f;
-          const float p1 = ok1 ? exp2f(fmaf(__uint_as_float(s[k + 1]), p.scale_log2, -m_use)) : 0.f;
+        for (int k = 0; k < 64; k += 2) {
+          float p0 = fast_exp2(fmaf(__uint_as_float(s[k]), p.scale_log2, -m_use));
+          float p1 = fast_exp2(fmaf(__uint_as_float(s[k + 1]), p.scale_log2, -m_use));
+          p0 = ((mk >> k) & 1ull) ? p0 : 0.f;
+          p1 = ((mk >> (k + 1)) & 1ull) ? p1 : 0.f;
           lsum += p0 + p1;
           pk[k >> 1] = pack_bf16(p0, p1);
         }
-        l_run = l_run * alpha + lsum;
-        // ---- P buffer free (previous PV retired) -> rescale O if needed, write P ----
+        l_run = l_run * alpha + lsum;  // this warp's share of the row sum
+        // ---- P buffer free (previous PV retired) -> rescale this warp's O columns, write P region ----
         mbar_wait(bar_pempty, (chunk_ctr & 1) ^ 1);
         tc_fence_after();
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
-          for (int c = 0; c < p.dhp / 32; ++c) {
+          for (int c = 0; c < ocols / 32; ++c) {
             uint32_t r[32];
-            tmem_ld32(tO + lane_off + 32 * c, r);
+            const uint32_t ta = tO + lane_off + half * ocols + 32 * c;
+            tmem_ld32(ta, r);
             tmem_ld_wait();
 #pragma unroll
             for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-            tmem_st32(tO + lane_off + 32 * c, r);
+            tmem_st32(ta, r);
           }
           tmem_st_wait();
         }
+        const uint32_t preg = sP + half * 16384u;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {  // keys [8q, 8q+8) -> region q/8, 16B chunk q%8
-          st_shared_v4(sP + (q >> 3) * 16384u + sw128_off(tid, q & 7), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2],
-                       pk[4 * q + 3]);
-        }
+        for (int q = 0; q < 8; ++q)  // keys [64 half + 8q, +8) -> 16B chunk q of row `row`
+          st_shared_v4(preg + sw128_off(row, q), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
         fence_proxy_async();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_pfull);
       }
-      // ---- epilogue: O / l -> bf16 ctx ----
+      // ---- epilogue: O / l -> bf16 ctx (row sum = both halves) ----
+      red_l[half * 128 + row] = l_run;
+      named_bar_sync(1 + quarter, 64);
+      const float l_tot = l_run + red_l[(half ^ 1) * 128 + row];
       mbar_wait(bar_ofull, tile_ctr & 1);
       tc_fence_after();
-      const float inv_l = (qvalid && l_run > 0.f) ? 1.f / l_run : 0.f;
-      __nv_bfloat16* orow =
-          p.out + (qvalid ? (static_cast<size_t>((qd * p.rows + qh) * p.cols + qw) * p.ldo + g.head * p.dhp) : 0);
+      const float inv_l = (qvalid && l_tot > 0.f) ? 1.f / l_tot : 0.f;
+      __nv_bfloat16* orow = p.out + (qvalid ? (static_cast<size_t>((qd * p.rows + qh) * p.cols + qw) * p.ldo +
+                                                g.head * p.dhp + half * ocols)
+                                             : 0);
 #pragma unroll 1
-      for (int c = 0; c < p.dhp / 32; ++c) {
+      for (int c = 0; c < ocols / 32; ++c) {
         uint32_t r[32];
-        tmem_ld32(tO + lane_off + 32 * c, r);
+        tmem_ld32(tO + lane_off + half * ocols + 32 * c, r);
         tmem_ld_wait();
         if (qvalid) {
           uint4* d4 = reinterpret_cast<uint4*>(orow + 32 * c);
@@ -364,13 +379,14 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
         }
       }
       tc_fence_before();
+      named_bar_sync(1 + quarter, 64);  // partner has read red[] before the next tile overwrites it
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_oempty);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == NA_MMA_WARP) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
