@@ -88,6 +88,32 @@ int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, int depth, in
                    int rows_global, int row0, int halo_lo, int halo_hi, int heads, int dhp, int wd,
                    int wh, int ww, float scale, void* stream);
 
+/* Implicit-GEMM convolutions of the encoder / decoder pyramids (model.py:296-325, autodiff.py:585-764).
+ * Activations are bf16 NHWC with a 1-pixel halo, [imgs][H + 2][W + 2][Cp] (Cp % 64 == 0): zero halo rows,
+ * halo columns = opposite edge (longitude wrap).  Modes:
+ *   WM3_CONV_S1  3x3 stride 1       w: [cout_pad][9][cinp]      (tap = kh * 3 + kw)
+ *   WM3_CONV_S2  3x3 stride 2       w: [cout_pad][9][cinp]
+ *   WM3_CONV_T2  4x4 stride 2 transposed (adjoint geometry), as 4 output-parity classes of 2x2 taps:
+ *                w: [4 = 2a + b][cout_pad][4 = 2tr + tc][cinp] = W[cin][cout][3 - a - 2tr][3 - b - 2tc]
+ * cout_pad = cout rounded up to wm3_conv_bn(cout).  Epilogue: + bias, optional exact GELU, optional
+ * residual (bf16 NHWC, same layout as the output), then one of
+ *   WM3_CONV_OUT_NHWC    bf16 padded NHWC (pitch out_cp), wrap columns written too
+ *   WM3_CONV_OUT_TOKENS  fp32 tokens [img][H][W][cout] (the latent, model.py:350-354)
+ *   WM3_CONV_OUT_FIELD   fp32 NCHW: out[img * img_stride + (c / chan_div) * a_stride + (c % chan_div) * p_stride
+ *                        + h * W + w] (surface / atmos fields with the level unfold of model.py:340-347). */
+enum { WM3_CONV_S1 = 0, WM3_CONV_S2 = 1, WM3_CONV_T2 = 2 };
+enum { WM3_CONV_OUT_NHWC = 0, WM3_CONV_OUT_TOKENS = 1, WM3_CONV_OUT_FIELD = 2 };
+int wm3_conv_bn(int cout);
+int wm3_conv(int mode, const void* in, int imgs, int hin, int win, int cinp, const void* w, int cout,
+             const float* bias, int act_gelu, const void* resid, int resid_cp, int out_kind, void* out, int out_cp,
+             long long img_stride, long long a_stride, long long p_stride, int chan_div, void* stream);
+/* fp32 fields -> padded NHWC: channel c of image i at src[i * img_stride + (c / chan_div) * a_stride
+ * + (c % chan_div) * p_stride + h * W + w] (level fold of model.py:332-337). */
+int wm3_fields_to_nhwc(const float* src, long long img_stride, long long a_stride, long long p_stride, int chan_div,
+                       int imgs, int channels, int h, int w, int cp, void* dst, void* stream);
+/* fp32 tokens [img][H][W][channels] -> padded NHWC (model.py:357-360). */
+int wm3_tokens_to_nhwc(const float* tokens, int imgs, int h, int w, int channels, int cp, void* dst, void* stream);
+
 /* Debug export of the kernel's own window arithmetic: per token, the (start_d, start_h, col_off)
  * it uses; int32 [T][3]. */
 int wm3_natten_windows(int depth, int rows, int cols, int rows_global, int row0, int wd, int wh, int ww,

@@ -63,9 +63,25 @@ def rotary_angles(extents, head_dim: int) -> np.ndarray:
     return ang
 
 
+_ROT: dict = {}
+_NB: dict = {}
+
+
 def rotary_tables(extents, head_dim: int):
-    ang = rotary_angles(extents, head_dim)
-    return np.cos(ang)[:, None, :], np.sin(ang)[:, None, :]
+    """Cached like the reference (attention.py:45)."""
+    key = (tuple(extents), head_dim)
+    if key not in _ROT:
+        ang = rotary_angles(extents, head_dim)
+        _ROT[key] = (np.cos(ang)[:, None, :], np.sin(ang)[:, None, :])
+    return _ROT[key]
+
+
+def _neighborhood(extents, window):
+    """Cached like the reference (grid.py:104)."""
+    key = (tuple(extents), tuple(window))
+    if key not in _NB:
+        _NB[key] = neighborhood(extents, window)
+    return _NB[key]
 
 
 def apply_rotary(x: np.ndarray, cos: np.ndarray, sin: np.ndarray) -> np.ndarray:
@@ -115,7 +131,7 @@ def natten_block(x: np.ndarray, params: dict, prefix: str, extents, window, head
     if dim % heads != 0:
         raise OracleConfigError(f"dim {dim} not divisible by heads {heads}")
     dh = dim // heads
-    table = neighborhood(extents, window)
+    table = _neighborhood(extents, window)
     cos, sin = rotary_tables(extents, dh)
 
     def p(name):
@@ -138,7 +154,7 @@ def attention_weights(x: np.ndarray, params: dict, prefix: str, extents, window,
     """attention.py:187-212 — softmax weights (T, heads, K)."""
     t, dim = x.shape
     dh = dim // heads
-    table = neighborhood(extents, window)
+    table = _neighborhood(extents, window)
     cos, sin = rotary_tables(extents, dh)
 
     def p(name):

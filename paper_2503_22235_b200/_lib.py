@@ -15,6 +15,9 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libwm3.so")
 
+# Tensor-core operand dtype the library is built for (csrc/common.cuh elem_t): fp16 by default.
+ELEM = torch.float16
+
 WM3_EPI_F32 = 0
 WM3_EPI_BIAS_BF16 = 1
 WM3_EPI_BIAS_GELU_BF16 = 2
@@ -24,6 +27,7 @@ WM3_EPI_QKV_ROPE = 4
 _vp = ctypes.c_void_p
 _i = ctypes.c_int
 _f = ctypes.c_float
+_ll = ctypes.c_longlong
 
 
 class RopeT(ctypes.Structure):
@@ -44,7 +48,14 @@ SIGNATURES = {
                           _i, _i, ctypes.c_longlong, _i, _vp],
     "wm3_natten_fwd": [_vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _f, _vp],
     "wm3_natten_windows": [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp],
+    "wm3_conv_bn": [_i],
+    "wm3_conv": [_i, _vp, _i, _i, _i, _i, _vp, _i, _vp, _i, _vp, _i, _i, _vp, _i, _ll, _ll, _ll, _i, _vp],
+    "wm3_fields_to_nhwc": [_vp, _ll, _ll, _ll, _i, _i, _i, _i, _i, _i, _vp, _vp],
+    "wm3_tokens_to_nhwc": [_vp, _i, _i, _i, _i, _i, _vp, _vp],
 }
+
+WM3_CONV_S1, WM3_CONV_S2, WM3_CONV_T2 = 0, 1, 2
+WM3_CONV_OUT_NHWC, WM3_CONV_OUT_TOKENS, WM3_CONV_OUT_FIELD = 0, 1, 2
 
 
 def exported_symbols() -> list[str]:

@@ -137,7 +137,7 @@ def _kmajor_bf16(w_in_out: np.ndarray, n_pad: int, k_pad: int, device) -> torch.
     k, n = w_in_out.shape
     buf = np.zeros((n_pad, k_pad), dtype=np.float32)
     buf[:n, :k] = w_in_out.T
-    return torch.from_numpy(buf).to(device=device, dtype=torch.bfloat16)
+    return torch.from_numpy(buf).to(device=device, dtype=_lib.ELEM)
 
 
 def _vec(v: np.ndarray, n_pad: int, device) -> torch.Tensor:
@@ -209,10 +209,10 @@ class Workspace:
         self.grid = grid
         tokens = grid.depth * grid.rows * grid.cols
         self.tokens = tokens
-        self.hn = torch.empty((tokens, bw.kp), dtype=torch.bfloat16, device=device)
-        self.qkv = torch.zeros((grid.tokens, 3 * bw.heads * bw.dhp), dtype=torch.bfloat16, device=device)
-        self.ctx = torch.empty((tokens, bw.heads * bw.dhp), dtype=torch.bfloat16, device=device)
-        self.mid = torch.empty((tokens, bw.nm), dtype=torch.bfloat16, device=device)
+        self.hn = torch.empty((tokens, bw.kp), dtype=_lib.ELEM, device=device)
+        self.qkv = torch.zeros((grid.tokens, 3 * bw.heads * bw.dhp), dtype=_lib.ELEM, device=device)
+        self.ctx = torch.empty((tokens, bw.heads * bw.dhp), dtype=_lib.ELEM, device=device)
+        self.mid = torch.empty((tokens, bw.nm), dtype=_lib.ELEM, device=device)
 
 
 def block_forward(x: torch.Tensor, bw: BlockWeights, ws: Workspace, rope: RopeTables, extents, window,

@@ -10,6 +10,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 #define DEVI __device__ __forceinline__
@@ -161,11 +162,38 @@ DEVI void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 
-// Instruction descriptor: bf16 x bf16 -> f32, dense.
-__host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, int a_mn_major, int b_mn_major) {
+// Tensor-core operand element type (2 bytes, fp32 accumulation in TMEM).  Default fp16: 11-bit significand,
+// 8x finer rounding than bf16; every operand is range-safe (LayerNorm outputs, GELU / softmax / attention
+// outputs, conv activations of standardised fields), and fp32 stays the residual / latent type.
+// Build with -DWM3_OPERAND_BF16 for bf16 operands.
+#ifdef WM3_OPERAND_BF16
+using elem_t = __nv_bfloat16;
+constexpr uint32_t kElemFmt = 1;  // BF16
+DEVI uint32_t pack_elem(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+DEVI elem_t to_elem(float x) { return __float2bfloat16_rn(x); }
+DEVI float2 unpack_elem2(uint32_t u) {
+  const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&u);
+  return make_float2(__bfloat162float(h.x), __bfloat162float(h.y));
+}
+#else
+using elem_t = __half;
+constexpr uint32_t kElemFmt = 0;  // F16
+DEVI uint32_t pack_elem(float lo, float hi) {
+  __half2 v = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+DEVI elem_t to_elem(float x) { return __float2half_rn(x); }
+DEVI float2 unpack_elem2(uint32_t u) { return __half22float2(*reinterpret_cast<const __half2*>(&u)); }
+#endif
+
+// Instruction descriptor: elem_t x elem_t -> f32, dense.
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, int a_mn_major, int b_mn_major) {
   return (1u << 4)                                  // D format f32
-         | (1u << 7)                                // A format bf16
-         | (1u << 10)                               // B format bf16
+         | (kElemFmt << 7)                          // A format
+         | (kElemFmt << 10)                         // B format
          | (static_cast<uint32_t>(a_mn_major) << 15)
          | (static_cast<uint32_t>(b_mn_major) << 16)
          | (static_cast<uint32_t>(N >> 3) << 17)
@@ -213,12 +241,8 @@ DEVI void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "me
 DEVI void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------------------------
-// small math / packing
+// small math
 // ---------------------------------------------------------------------------------------------
-DEVI uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
 DEVI float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 // 2^x on the SFU (MUFU.EX2); inputs here are <= 8 (lazy-rescaled softmax), -inf -> 0.
 DEVI float fast_exp2(float x) {

@@ -1,0 +1,429 @@
+// K6/K7: implicit-GEMM convolutions of the encoder/decoder pyramids on tcgen05.
+//
+// Reference geometry (model.py:296-325, autodiff.py:585-764): 3x3 convs with rows zero-padded by 1 and
+// columns periodic (centred taps), stride 1 or 2; 4x4 stride-2 transposed convs, the exact adjoint (rows
+// padded (1,1), columns wrapped with c = 1).  All depth planes share the pyramid weights, so the planes are
+// batched as images of one launch.
+//
+// Activation layout: bf16 NHWC with a 1-pixel halo, [img][H + 2][W + 2][Cp]: halo rows are zero (row pad),
+// halo columns hold the opposite edge (longitude wrap), Cp = channels rounded up to 64.  Every tap of every
+// conv is then a plain rectangular TMA box:
+//   3x3 s1      out (r, c) tap (kh, kw) reads padded (r + kh, c + kw)               3D box {64, 128, 1}
+//   3x3 s2      reads padded (2r + kh, 2c + kw): columns viewed as (pair, parity)    4D box {64, 1, 128, 1}
+//   convT s2    output parity class (a, b), taps (tr, tc) in {0,1}^2: out (2r + a, 2c + b) reads padded
+//               (r + a + tr, c + b + tc) with kernel tap (3 - a - 2 tr, 3 - b - 2 tc)
+// GEMM view: M = output pixels of one row (128-pixel tiles), N = Cout, K = taps x Cp (weights pre-arranged
+// [class][Cout_pad][tap][Cp], K-major).  Warp roles as in gemm.cu; the epilogue writes straight from
+// registers (one pixel per thread): bias, optional exact GELU, optional residual (res-block skip), and
+// either the next padded NHWC activation (incl. its wrap columns), fp32 tokens, or fp32 NCHW fields.
+#include "common.cuh"
+#include "launch.h"
+#include "../../include/wm3.h"
+
+namespace wm3 {
+
+constexpr int CV_BM = 128;
+constexpr int CV_BK = 64;
+constexpr int CV_THREADS = 384;
+
+struct ConvParams {
+  int mode;            // WM3_CONV_S1 / S2 / T2
+  int imgs;
+  int hin, win, cinp;  // input extents (unpadded) and padded channel count
+  int hout, wout;      // output extents
+  int rows_t, cols_t;  // GEMM output sub-grid per class: rows x cols (cols tiled by 128)
+  int nclass, ntap, ncb;
+  int cout, cout_pad;  // real output channels, per-class padded N
+  int tiles_per_row, tiles_per_class;
+  // epilogue
+  const float* bias;
+  int act_gelu;
+  const elem_t* resid;  // padded NHWC with the output's spatial extents, or null
+  int resid_cp;
+  int out_kind;
+  void* out;
+  int out_cp;                  // NHWC: padded channel pitch of the output
+  long long img_stride;        // FIELD: elements between images;   TOKENS: unused
+  long long a_stride, p_stride;  // FIELD: channel c -> (c / chan_div) * a_stride + (c % chan_div) * p_stride
+  int chan_div;
+};
+
+template <int BN>
+struct ConvCfg {
+  static constexpr int STAGES = (BN == 256) ? 4 : 5;
+  static constexpr uint32_t A_BYTES = CV_BM * CV_BK * 2;
+  static constexpr uint32_t B_BYTES = BN * CV_BK * 2;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr uint32_t TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
+};
+
+// m-tile -> image, class, output sub-grid row, first column
+DEVI void conv_tile(const ConvParams& p, int mt, int& img, int& cls, int& r, int& c0) {
+  const int per_img = p.nclass * p.tiles_per_class;
+  img = mt / per_img;
+  int rest = mt - img * per_img;
+  cls = rest / p.tiles_per_class;
+  rest -= cls * p.tiles_per_class;
+  r = rest / p.tiles_per_row;
+  c0 = (rest - r * p.tiles_per_row) * CV_BM;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(CV_THREADS, 1)
+    conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, ConvParams p) {
+  using Cfg = ConvCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  const uint32_t bar0 = smem_u32(bars);
+  auto full_bar = [&](int s) { return bar0 + 8u * s; };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
+  auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + a); };
+  auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + 2 + a); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nn = p.cout_pad / BN;
+  const int ntiles = p.imgs * p.nclass * p.tiles_per_class * nn;
+  const int nk = p.ntap * p.ncb;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar(a), 1);
+      mbar_init(tempty_bar(a), 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(smem_u32(tmem_slot), Cfg::TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const int hp = p.hin + 2;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int img, cls, r, c0;
+        conv_tile(p, tile / nn, img, cls, r, c0);
+        const int n0 = (tile % nn) * BN;
+        const int a = cls >> 1, b = cls & 1;
+        for (int kb = 0; kb < nk; ++kb) {
+          const int tap = kb / p.ncb, cb = kb - tap * p.ncb;
+          mbar_wait(empty_bar(stage), phase ^ 1);
+          const uint32_t sa = sbase + stage * Cfg::STAGE_BYTES;
+          const uint32_t sb = sa + Cfg::A_BYTES;
+          mbar_arrive_expect_tx(full_bar(stage), Cfg::STAGE_BYTES);
+          if (p.mode == WM3_CONV_S2) {
+            const int kh = tap / 3, kw = tap - 3 * (tap / 3);
+            tma_load_4d(sa, &tmA, full_bar(stage), cb * CV_BK, kw & 1, c0 + (kw >> 1), img * hp + 2 * r + kh);
+          } else if (p.mode == WM3_CONV_S1) {
+            const int kh = tap / 3, kw = tap - 3 * (tap / 3);
+            tma_load_3d(sa, &tmA, full_bar(stage), cb * CV_BK, c0 + kw, img * hp + r + kh);
+          } else {  // transposed, parity class (a, b), tap (tr, tc)
+            const int tr = tap >> 1, tc = tap & 1;
+            tma_load_3d(sa, &tmA, full_bar(stage), cb * CV_BK, c0 + b + tc, img * hp + r + a + tr);
+          }
+          tma_load_2d(sb, &tmB, full_bar(stage), kb * CV_BK, cls * p.cout_pad + n0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(CV_BM, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        mbar_wait(tempty_bar(acc), aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(full_bar(stage), phase);
+          tc_fence_after();
+          const uint32_t sa = sbase + stage * Cfg::STAGE_BYTES;
+          const uint32_t sb = sa + Cfg::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < CV_BK / 16; ++k)
+            umma_bf16_ss(d_tmem, make_sdesc_sw128(sa + k * 32, 16, 1024), make_sdesc_sw128(sb + k * 32, 16, 1024),
+                         idesc, (kb | k) != 0 ? 1u : 0u);
+          umma_commit(empty_bar(stage));
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(tfull_bar(acc));
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int g = (warp - 4) >> 2;
+    const int q = warp & 3;
+    const int i = 32 * q + lane;  // pixel within the tile
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      int img, cls, r, c0;
+      conv_tile(p, tile / nn, img, cls, r, c0);
+      const int n0 = (tile % nn) * BN;
+      const int col = c0 + i;
+      const bool ok = col < p.cols_t;
+      // output pixel
+      int orow = r, ocol = col;
+      if (p.mode == WM3_CONV_T2) { orow = 2 * r + (cls >> 1); ocol = 2 * col + (cls & 1); }
+      mbar_wait(tfull_bar(acc), aphase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(32 * q) << 16);
+      for (int u = g; u < BN / 32; u += 2) {
+        uint32_t rr[32];
+        tmem_ld32(taddr + 32 * u, rr);
+        tmem_ld_wait();
+        const int n = n0 + 32 * u;
+        if (!ok || n >= p.cout) continue;
+        const int nvalid = min(32, p.cout - n);
+        float v[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(rr[e]) + (e < nvalid ? __ldg(p.bias + n + e) : 0.f);
+        if (p.act_gelu) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = gelu_erf(v[e]);
+        }
+        const size_t pix = (static_cast<size_t>(img) * (p.hout + 2) + orow + 1) * (p.wout + 2) + ocol + 1;
+        if (p.resid != nullptr) {
+          const uint4* rs = reinterpret_cast<const uint4*>(p.resid + pix * p.resid_cp + n);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 w4 = __ldg(rs + j);
+            const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const float2 h2 = unpack_elem2(ws[t]);
+              v[8 * j + 2 * t] += h2.x;
+              v[8 * j + 2 * t + 1] += h2.y;
+            }
+          }
+        }
+        if (p.out_kind == WM3_CONV_OUT_NHWC) {
+          uint4 pk[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            pk[j] = make_uint4(pack_elem(v[8 * j], v[8 * j + 1]), pack_elem(v[8 * j + 2], v[8 * j + 3]),
+                               pack_elem(v[8 * j + 4], v[8 * j + 5]), pack_elem(v[8 * j + 6], v[8 * j + 7]));
+          elem_t* ob = reinterpret_cast<elem_t*>(p.out);
+          uint4* d = reinterpret_cast<uint4*>(ob + pix * p.out_cp + n);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) d[j] = pk[j];
+          // longitude wrap columns of the padded output
+          if (ocol == 0 || ocol == p.wout - 1) {
+            const size_t hp = pix + (ocol == 0 ? p.wout : -static_cast<long long>(p.wout));
+            uint4* d2 = reinterpret_cast<uint4*>(ob + hp * p.out_cp + n);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) d2[j] = pk[j];
+          }
+        } else if (p.out_kind == WM3_CONV_OUT_TOKENS) {
+          // fp32 tokens [img][hout][wout][cout]
+          float* ot = reinterpret_cast<float*>(p.out) +
+                      ((static_cast<size_t>(img) * p.hout + orow) * p.wout + ocol) * p.cout + n;
+          if (nvalid == 32 && (p.cout % 4) == 0) {
+            float4* d4 = reinterpret_cast<float4*>(ot);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          } else {
+            for (int e = 0; e < nvalid; ++e) ot[e] = v[e];
+          }
+        } else {  // fp32 NCHW fields with channel remap (model.py:340-347 level unfold)
+          float* of = reinterpret_cast<float*>(p.out) + static_cast<size_t>(img) * p.img_stride +
+                      static_cast<size_t>(orow) * p.wout + ocol;
+          for (int e = 0; e < nvalid; ++e) {
+            const int c = n + e;
+            of[(c / p.chan_div) * p.a_stride + (c % p.chan_div) * p.p_stride] = v[e];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_bar(acc));
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// layout kernels: fp32 NCHW / tokens -> padded bf16 NHWC (zero halo rows, wrapped halo columns)
+// ---------------------------------------------------------------------------------------------
+// dst[img][h + 1][w + 1][c] = src[img * img_stride + (c / cdiv) * a_stride + (c % cdiv) * p_stride + h * W + w],
+// channels >= C zero; halo columns copied from the opposite edge, halo rows zero.
+__global__ void fields_to_nhwc_kernel(const float* __restrict__ src, long long img_stride, long long a_stride,
+                                      long long p_stride, int cdiv, int imgs, int C, int H, int W, int cp,
+                                      elem_t* __restrict__ dst) {
+  const long long total = static_cast<long long>(imgs) * (H + 2) * (W + 2) * cp;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(idx % cp);
+    long long rest = idx / cp;
+    const int pw = static_cast<int>(rest % (W + 2));
+    rest /= (W + 2);
+    const int ph = static_cast<int>(rest % (H + 2));
+    const int img = static_cast<int>(rest / (H + 2));
+    float v = 0.f;
+    if (c < C && ph >= 1 && ph <= H) {
+      const int h = ph - 1;
+      const int w = pw == 0 ? W - 1 : (pw == W + 1 ? 0 : pw - 1);
+      v = src[img * img_stride + (c / cdiv) * a_stride + (c % cdiv) * p_stride + static_cast<long long>(h) * W + w];
+    }
+    dst[idx] = to_elem(v);
+  }
+}
+
+// tokens fp32 [img][H][W][C] (C = hidden) -> padded bf16 NHWC with cp channels
+__global__ void tokens_to_nhwc_kernel(const float* __restrict__ tok, int imgs, int H, int W, int C, int cp,
+                                      elem_t* __restrict__ dst) {
+  const long long total = static_cast<long long>(imgs) * (H + 2) * (W + 2) * (cp / 2);
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int c2 = static_cast<int>(idx % (cp / 2)) * 2;
+    long long rest = idx / (cp / 2);
+    const int pw = static_cast<int>(rest % (W + 2));
+    rest /= (W + 2);
+    const int ph = static_cast<int>(rest % (H + 2));
+    const int img = static_cast<int>(rest / (H + 2));
+    float a = 0.f, b = 0.f;
+    if (ph >= 1 && ph <= H) {
+      const int h = ph - 1;
+      const int w = pw == 0 ? W - 1 : (pw == W + 1 ? 0 : pw - 1);
+      const float* s = tok + ((static_cast<size_t>(img) * H + h) * W + w) * C;
+      if (c2 < C) a = s[c2];
+      if (c2 + 1 < C) b = s[c2 + 1];
+    }
+    reinterpret_cast<uint32_t*>(dst)[idx] = pack_elem(a, b);
+  }
+}
+
+template <int BN>
+static int launch_conv(const CUtensorMap& ta, const CUtensorMap& tb, const ConvParams& p, cudaStream_t s) {
+  using Cfg = ConvCfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return set_error("cudaFuncSetAttribute(conv): %s", cudaGetErrorString(e));
+    attr = true;
+  }
+  const long long ntiles = static_cast<long long>(p.imgs) * p.nclass * p.tiles_per_class * (p.cout_pad / BN);
+  const int grid = static_cast<int>(ntiles < sm_count() ? ntiles : sm_count());
+  conv_tc_kernel<BN><<<grid, CV_THREADS, Cfg::SMEM, s>>>(ta, tb, p);
+  return check_launch("conv_tc_kernel");
+}
+
+}  // namespace wm3
+
+using namespace wm3;
+
+extern "C" int wm3_conv_bn(int cout) {
+  if (cout <= 128) return 128;
+  if (cout <= 192) return 192;
+  return 256;
+}
+
+extern "C" int wm3_conv(int mode, const void* in, int imgs, int hin, int win, int cinp, const void* w, int cout,
+                        const float* bias, int act_gelu, const void* resid, int resid_cp, int out_kind, void* out,
+                        int out_cp,
+                        long long img_stride, long long a_stride, long long p_stride, int chan_div, void* stream) {
+  if (mode != WM3_CONV_S1 && mode != WM3_CONV_S2 && mode != WM3_CONV_T2) return set_error("wm3_conv: bad mode");
+  if (cinp % 64) return set_error("wm3_conv: padded input channels %d not a multiple of 64", cinp);
+  if ((mode == WM3_CONV_S2 && win % 2) || hin < 1 || win < 1)
+    return set_error("wm3_conv: bad input extents %dx%d", hin, win);
+  ConvParams p{};
+  p.mode = mode;
+  p.imgs = imgs;
+  p.hin = hin; p.win = win; p.cinp = cinp;
+  if (mode == WM3_CONV_S1) { p.hout = hin; p.wout = win; p.nclass = 1; p.ntap = 9; }
+  else if (mode == WM3_CONV_S2) { p.hout = (hin - 1) / 2 + 1; p.wout = win / 2; p.nclass = 1; p.ntap = 9; }
+  else { p.hout = 2 * hin; p.wout = 2 * win; p.nclass = 4; p.ntap = 4; }
+  p.rows_t = (mode == WM3_CONV_T2) ? hin : p.hout;
+  p.cols_t = (mode == WM3_CONV_T2) ? win : p.wout;
+  p.ncb = cinp / 64;
+  p.cout = cout;
+  const int bn = wm3_conv_bn(cout);
+  p.cout_pad = ((cout + bn - 1) / bn) * bn;
+  p.tiles_per_row = (p.cols_t + CV_BM - 1) / CV_BM;
+  p.tiles_per_class = p.rows_t * p.tiles_per_row;
+  p.bias = bias;
+  p.act_gelu = act_gelu;
+  p.resid = reinterpret_cast<const elem_t*>(resid);
+  p.resid_cp = resid_cp;
+  if (resid && (resid_cp % 64 || resid_cp < cout)) return set_error("wm3_conv: bad resid_cp");
+  p.out_kind = out_kind;
+  p.out = out;
+  p.out_cp = out_cp;
+  p.img_stride = img_stride; p.a_stride = a_stride; p.p_stride = p_stride; p.chan_div = chan_div > 0 ? chan_div : 1;
+  if (out_kind == WM3_CONV_OUT_NHWC && (out_cp % 64 || out_cp < cout)) return set_error("wm3_conv: bad out_cp");
+  // A: padded NHWC input, images stacked along rows
+  CUtensorMap ta, tb;
+  const uint64_t wp = win + 2;
+  const uint64_t rows = static_cast<uint64_t>(imgs) * (hin + 2);
+  if (mode == WM3_CONV_S2) {
+    const uint64_t dims[4] = {static_cast<uint64_t>(cinp), 2, wp / 2, rows};
+    const uint64_t strides[3] = {static_cast<uint64_t>(cinp), 2ull * cinp, wp * cinp};
+    const uint32_t box[4] = {64, 1, CV_BM, 1};
+    if (make_tmap(&ta, in, TMAP_BF16, 4, dims, strides, box, nullptr)) return -1;
+  } else {
+    const uint64_t dims[3] = {static_cast<uint64_t>(cinp), wp, rows};
+    const uint64_t strides[2] = {static_cast<uint64_t>(cinp), wp * cinp};
+    const uint32_t box[3] = {64, CV_BM, 1};
+    if (make_tmap(&ta, in, TMAP_BF16, 3, dims, strides, box, nullptr)) return -1;
+  }
+  // B: weights [class][cout_pad][ntap * cinp], K-major
+  const int kdim = p.ntap * cinp;
+  if (make_tmap_2d_bf16(&tb, w, kdim, static_cast<uint64_t>(p.nclass) * p.cout_pad, kdim, CV_BK, bn)) return -1;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (bn == 128) return launch_conv<128>(ta, tb, p, s);
+  if (bn == 192) return launch_conv<192>(ta, tb, p, s);
+  return launch_conv<256>(ta, tb, p, s);
+}
+
+extern "C" int wm3_fields_to_nhwc(const float* src, long long img_stride, long long a_stride, long long p_stride,
+                                  int chan_div, int imgs, int channels, int h, int w, int cp, void* dst,
+                                  void* stream) {
+  if (channels > cp || cp % 64) return set_error("wm3_fields_to_nhwc: bad channel padding");
+  const long long total = static_cast<long long>(imgs) * (h + 2) * (w + 2) * cp;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148LL * 64) blocks = 148LL * 64;
+  fields_to_nhwc_kernel<<<static_cast<int>(blocks), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      src, img_stride, a_stride, p_stride, chan_div > 0 ? chan_div : 1, imgs, channels, h, w, cp,
+      reinterpret_cast<elem_t*>(dst));
+  return check_launch("fields_to_nhwc_kernel");
+}
+
+extern "C" int wm3_tokens_to_nhwc(const float* tokens, int imgs, int h, int w, int channels, int cp, void* dst,
+                                  void* stream) {
+  if (channels > cp || cp % 64) return set_error("wm3_tokens_to_nhwc: bad channel padding");
+  const long long total = static_cast<long long>(imgs) * (h + 2) * (w + 2) * (cp / 2);
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148LL * 64) blocks = 148LL * 64;
+  tokens_to_nhwc_kernel<<<static_cast<int>(blocks), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      tokens, imgs, h, w, channels, cp, reinterpret_cast<elem_t*>(dst));
+  return check_launch("tokens_to_nhwc_kernel");
+}

@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16(GEMM_BM, BN, 0, 0);
+      constexpr uint32_t idesc = make_idesc(GEMM_BM, BN, 0, 0);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           uint32_t pk[32];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) pk[e] = pack_bf16(v[2 * e], v[2 * e + 1]);
+          for (int e = 0; e < 32; ++e) pk[e] = pack_elem(v[2 * e], v[2 * e + 1]);
           if (elected) bulk_wait_read<Cfg::STAGING_PER_GROUP - 1>();
           named_bar_sync(bar_id, 128);
           const uint32_t st = staging0 + (g * Cfg::STAGING_PER_GROUP + sbuf) * Cfg::STAGING_BYTES;

@@ -32,12 +32,12 @@ __global__ void neighbor_table_kernel(int depth, int rows, int cols, int wd, int
 // autodiff.py:400-424: mean, biased variance, eps, gain/bias; one warp per row, fp32 statistics.
 template <int NV>
 __global__ void layernorm_kernel(const float* __restrict__ x, int ldx, int m, int n, const float* __restrict__ gain,
-                                 const float* __restrict__ bias, float eps, __nv_bfloat16* __restrict__ out, int ldo) {
+                                 const float* __restrict__ bias, float eps, elem_t* __restrict__ out, int ldo) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= m) return;
   const float* xr = x + static_cast<size_t>(warp) * ldx;
-  __nv_bfloat16* orow = out + static_cast<size_t>(warp) * ldo;
+  elem_t* orow = out + static_cast<size_t>(warp) * ldo;
   const bool vec = (n % 4 == 0) && (ldx % 4 == 0) && (n <= NV * 128);
   if (vec) {
     float4 v[NV];
@@ -70,8 +70,8 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int ldx, int m, in
         const float4 g = __ldg(reinterpret_cast<const float4*>(gain + c));
         const float4 b = __ldg(reinterpret_cast<const float4*>(bias + c));
         uint2 pk;
-        pk.x = pack_bf16((v[i].x - mu) * inv * g.x + b.x, (v[i].y - mu) * inv * g.y + b.y);
-        pk.y = pack_bf16((v[i].z - mu) * inv * g.z + b.z, (v[i].w - mu) * inv * g.w + b.w);
+        pk.x = pack_elem((v[i].x - mu) * inv * g.x + b.x, (v[i].y - mu) * inv * g.y + b.y);
+        pk.y = pack_elem((v[i].z - mu) * inv * g.z + b.z, (v[i].w - mu) * inv * g.w + b.w);
         *reinterpret_cast<uint2*>(orow + c) = pk;
       }
     }
@@ -84,9 +84,9 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int ldx, int m, in
     for (int c = lane; c < n; c += 32) { const float a = xr[c] - mu; q += a * a; }
     for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
     const float inv = rsqrtf(q / n + eps);
-    for (int c = lane; c < n; c += 32) orow[c] = __float2bfloat16_rn((xr[c] - mu) * inv * gain[c] + bias[c]);
+    for (int c = lane; c < n; c += 32) orow[c] = to_elem((xr[c] - mu) * inv * gain[c] + bias[c]);
   }
-  for (int c = n + lane; c < ldo; c += 32) orow[c] = __float2bfloat16_rn(0.f);
+  for (int c = n + lane; c < ldo; c += 32) orow[c] = to_elem(0.f);
 }
 
 }  // namespace wm3
@@ -114,7 +114,7 @@ extern "C" int wm3_layernorm_bf16(const float* x, int ldx, int m, int n, const f
   const int threads = 256;
   const int blocks = (m * 32 + threads - 1) / threads;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  auto* o = reinterpret_cast<__nv_bfloat16*>(out_bf16);
+  auto* o = reinterpret_cast<elem_t*>(out_bf16);
   if (n <= 256)
     layernorm_kernel<2><<<blocks, threads, 0, s>>>(x, ldx, m, n, gain, bias, eps, o, ldo);
   else if (n <= 1024)

@@ -24,7 +24,7 @@
 namespace wm3 {
 
 struct NaParams {
-  __nv_bfloat16* out;
+  elem_t* out;
   int ldo;
   int depth, rows, cols, rows_global, row0, halo_lo, rows_ext;
   int heads, dhp, wd, wh, ww;
@@ -203,8 +203,8 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
   } else if (warp == NA_MMA_WARP) {
     // =============================== MMA issuer ===============================
     if (lane == 0) {
-      const uint32_t idesc_s = make_idesc_bf16(128, 128, 0, 0);
-      const uint32_t idesc_o = make_idesc_bf16(128, p.dhp, 0, 1);
+      const uint32_t idesc_s = make_idesc(128, 128, 0, 0);
+      const uint32_t idesc_o = make_idesc(128, p.dhp, 0, 1);
       const int kb = p.dhp / 64;
       const uint32_t tO = tmem + 256;
       int chunk_ctr = 0, tile_ctr = 0;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
           p0 = ((mk >> k) & 1ull) ? p0 : 0.f;
           p1 = ((mk >> (k + 1)) & 1ull) ? p1 : 0.f;
           lsum += p0 + p1;
-          pk[k >> 1] = pack_bf16(p0, p1);
+          pk[k >> 1] = pack_elem(p0, p1);
         }
         l_run = l_run * alpha + lsum;  // this warp's share of the row sum
         // ---- P buffer free (previous PV retired) -> rescale this warp's O columns, write P region ----
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
       mbar_wait(bar_ofull, tile_ctr & 1);
       tc_fence_after();
       const float inv_l = (qvalid && l_tot > 0.f) ? 1.f / l_tot : 0.f;
-      __nv_bfloat16* orow = p.out + (qvalid ? (static_cast<size_t>((qd * p.rows + qh) * p.cols + qw) * p.ldo +
+      elem_t* orow = p.out + (qvalid ? (static_cast<size_t>((qd * p.rows + qh) * p.cols + qw) * p.ldo +
                                                 g.head * p.dhp + half * ocols)
                                              : 0);
 #pragma unroll 1
@@ -370,10 +370,10 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             uint4 u;
-            u.x = pack_bf16(__uint_as_float(r[8 * q + 0]) * inv_l, __uint_as_float(r[8 * q + 1]) * inv_l);
-            u.y = pack_bf16(__uint_as_float(r[8 * q + 2]) * inv_l, __uint_as_float(r[8 * q + 3]) * inv_l);
-            u.z = pack_bf16(__uint_as_float(r[8 * q + 4]) * inv_l, __uint_as_float(r[8 * q + 5]) * inv_l);
-            u.w = pack_bf16(__uint_as_float(r[8 * q + 6]) * inv_l, __uint_as_float(r[8 * q + 7]) * inv_l);
+            u.x = pack_elem(__uint_as_float(r[8 * q + 0]) * inv_l, __uint_as_float(r[8 * q + 1]) * inv_l);
+            u.y = pack_elem(__uint_as_float(r[8 * q + 2]) * inv_l, __uint_as_float(r[8 * q + 3]) * inv_l);
+            u.z = pack_elem(__uint_as_float(r[8 * q + 4]) * inv_l, __uint_as_float(r[8 * q + 5]) * inv_l);
+            u.w = pack_elem(__uint_as_float(r[8 * q + 6]) * inv_l, __uint_as_float(r[8 * q + 7]) * inv_l);
             d4[q] = u;
           }
         }
@@ -448,7 +448,7 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
   if ((ldqkv % 8) || (ldo % 8)) return set_error("wm3_natten_fwd: pitches must be multiples of 8");
   if (ldqkv < 3 * heads * dhp) return set_error("wm3_natten_fwd: ldqkv < 3 * heads * dhp");
   NaParams p{};
-  p.out = reinterpret_cast<__nv_bfloat16*>(out);
+  p.out = reinterpret_cast<elem_t*>(out);
   p.ldo = ldo;
   p.depth = depth; p.rows = rows; p.cols = cols; p.rows_global = rows_global; p.row0 = row0;
   p.halo_lo = halo_lo; p.rows_ext = rows + halo_lo + halo_hi;

@@ -1,0 +1,227 @@
+"""Drop-in model API (gridcast/model.py): encode / process / decode on the B200 path.
+
+Same signatures, state types, error behaviour (ConfigError before any launch) and CALL_COUNTS
+instrumentation as the reference (model.py:53-58, 158-183, 363-449).  The latent lives on the device as an
+fp32 (T, hidden) token grid; decoded fields are fp32 device tensors exposed through `.values` (float64
+numpy on first access) so reference callers keep working.
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .blocks import block_forward
+from .config import (DOWNSAMPLE_STAGES, N_STATIC_FIELDS, PRIMARY_SOURCE, GridSpec, ModelConfig,  # noqa: F401
+                     config_from_dict, config_to_dict, desk_config, full_scale_config, load_config, mid_config,
+                     save_config, shape_plan, tiny_config)
+from .errors import ConfigError
+from .grid import desk_grid, quarter_degree_grid, static_fields  # noqa: F401
+from .params import (available_sources, block_param_names, encoder_prefix, init_block_params,  # noqa: F401
+                     init_model_params)
+from .pyramid import DecoderWeights, EncoderWeights, PyramidBuffers, decode_planes, encode_planes
+from .runtime import CACHE
+from .tensor import Tensor, host_values
+
+__all__ = [
+    "ModelConfig", "desk_config", "full_scale_config", "tiny_config", "mid_config", "WeatherState",
+    "DecodedFields", "LatentState", "init_model_params", "encode", "process", "decode", "blend_latents",
+    "encoder_prefix", "available_sources", "shape_plan", "save_config", "load_config", "CALL_COUNTS",
+    "reset_call_counts", "device_model",
+]
+
+CALL_COUNTS = {"encode": 0, "process1": 0, "process6": 0, "decode": 0}
+
+
+def reset_call_counts() -> None:
+    for k in CALL_COUNTS:
+        CALL_COUNTS[k] = 0
+
+
+@dataclass
+class WeatherState:
+    """Gridded fields at one valid time (model.py:158-163): surface (C, H, W), atmos (A, L, H, W)."""
+    valid_time: int
+    surface: object
+    atmos: object
+
+
+@dataclass
+class DecodedFields:
+    """Decoder output (model.py:166-175); surface / atmos are device-backed Tensors."""
+    valid_time: int
+    surface: Tensor
+    atmos: Tensor
+
+    def to_state(self) -> WeatherState:
+        return WeatherState(self.valid_time, self.surface.values.copy(), self.atmos.values.copy())
+
+
+@dataclass
+class LatentState:
+    """Token grid between encoder and decoder (model.py:178-183); tokens (T, hidden) fp32 on the device."""
+    tokens: Tensor
+    valid_time: int
+    extents: tuple
+
+
+# ------------------------------------------------------------------------------------------------
+# device-resident model
+# ------------------------------------------------------------------------------------------------
+class DeviceModel:
+    """Everything the forward needs on the device for one (params, cfg): converted weights (lazily, per
+    encoder source / block / decoder), activation buffers and rotary tables."""
+
+    def __init__(self, params: dict, cfg: ModelConfig):
+        self.params = params
+        self.cfg = cfg
+        self._enc: dict = {}
+        self._dec = None
+        self._bufs = None
+        self._fp = None
+
+    def refresh(self) -> None:
+        fp = tuple(id(getattr(v, "values", v)) for v in self.params.values())
+        if fp != self._fp:
+            self._enc.clear()
+            self._dec = None
+            self._fp = fp
+
+    def encoder(self, prefix: str) -> EncoderWeights:
+        if prefix not in self._enc:
+            self._enc[prefix] = EncoderWeights(self.params, prefix)
+        return self._enc[prefix]
+
+    def decoder(self) -> DecoderWeights:
+        if self._dec is None:
+            self._dec = DecoderWeights(self.params)
+        return self._dec
+
+    def buffers(self) -> PyramidBuffers:
+        if self._bufs is None:
+            self._bufs = PyramidBuffers(self.cfg)
+        return self._bufs
+
+    def run_blocks(self, x: torch.Tensor, prefixes) -> None:
+        cfg = self.cfg
+        ext = cfg.latent_extents
+        rope = CACHE.rope(ext, cfg.head_dim)
+        for pre in prefixes:
+            bw = CACHE.block(self.params, pre, cfg.heads)
+            block_forward(x, bw, CACHE.workspace(ext, cfg.window, bw), rope, ext, cfg.window)
+
+
+_models: dict = {}
+_mlock = threading.Lock()
+
+
+def device_model(params: dict, cfg: ModelConfig) -> DeviceModel:
+    key = (id(params), cfg)
+    with _mlock:
+        hit = _models.get(key)
+        if hit is None or hit.params is not params:
+            hit = DeviceModel(params, cfg)
+            _models[key] = hit
+    hit.refresh()
+    return hit
+
+
+def _to_device(a, shape) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        return a.to("cuda", torch.float32)
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(getattr(a, "values", a), dtype=np.float32))).to("cuda")
+
+
+def _tokens(lat: LatentState) -> torch.Tensor:
+    t = lat.tokens
+    if isinstance(t, Tensor) and t.device is not None:
+        return t.device
+    if isinstance(t, torch.Tensor):
+        return t.to("cuda", torch.float32)
+    return torch.from_numpy(np.ascontiguousarray(host_values(t), dtype=np.float32)).to("cuda")
+
+
+# ------------------------------------------------------------------------------------------------
+# API
+# ------------------------------------------------------------------------------------------------
+def encode(state: WeatherState, params: dict, cfg: ModelConfig, source: str = PRIMARY_SOURCE) -> LatentState:
+    """Lift one gridded state into the latent token grid (model.py:363-390)."""
+    prefix = encoder_prefix(source)
+    if f"{prefix}.stem_sfc.w" not in params:
+        raise ConfigError(f"no encoder for source {source!r}")
+    g = cfg.grid
+    if tuple(state.surface.shape) != (cfg.surface_in, g.rows, g.cols):
+        raise ConfigError(f"surface shape {tuple(state.surface.shape)} != {(cfg.surface_in, g.rows, g.cols)}")
+    if tuple(state.atmos.shape) != (cfg.atmos_vars, cfg.levels, g.rows, g.cols):
+        raise ConfigError(f"atmos shape {tuple(state.atmos.shape)} != "
+                          f"{(cfg.atmos_vars, cfg.levels, g.rows, g.cols)}")
+    CALL_COUNTS["encode"] += 1
+    dm = device_model(params, cfg)
+    bufs = dm.buffers()
+    if not bufs.statics_ready:
+        bufs.sfc_in[cfg.surface_in:] = torch.from_numpy(static_fields(g).astype(np.float32)).to("cuda")
+        bufs.statics_ready = True
+    bufs.sfc_in[:cfg.surface_in].copy_(_to_device(state.surface, None), non_blocking=True)
+    bufs.atm_in.copy_(_to_device(state.atmos, None), non_blocking=True)
+    tokens = torch.empty((cfg.tokens, cfg.hidden), dtype=torch.float32, device="cuda")
+    encode_planes(dm.encoder(prefix), bufs, cfg, tokens)
+    dm.run_blocks(tokens, [f"{prefix}.blk{i}" for i in range(cfg.enc_blocks)])
+    return LatentState(Tensor(device=tokens), state.valid_time, cfg.latent_extents)
+
+
+def _check_processor(params: dict, cfg: ModelConfig, horizon: int) -> None:
+    if horizon not in cfg.horizons:
+        raise ConfigError(f"no {horizon} h processor in config horizons {cfg.horizons}")
+    if f"proc{horizon}.blk0.ln1.gain" not in params:
+        raise ConfigError(f"parameters carry no {horizon} h processor")
+
+
+def process_inplace(x: torch.Tensor, params: dict, cfg: ModelConfig, horizon: int) -> None:
+    """proc_blocks blocks applied in place to a device token buffer (no validation, no counters)."""
+    device_model(params, cfg).run_blocks(x, [f"proc{horizon}.blk{i}" for i in range(cfg.proc_blocks)])
+
+
+def process(lat: LatentState, params: dict, cfg: ModelConfig, horizon: int) -> LatentState:
+    """Advance the latent state by one processor application (model.py:393-405)."""
+    _check_processor(params, cfg, horizon)
+    CALL_COUNTS[f"process{horizon}"] += 1
+    x = _tokens(lat).clone()
+    process_inplace(x, params, cfg, horizon)
+    return LatentState(Tensor(device=x), lat.valid_time + horizon, lat.extents)
+
+
+def decode(lat: LatentState, params: dict, cfg: ModelConfig) -> DecodedFields:
+    """Project the latent token grid back to gridded fields (model.py:408-421)."""
+    CALL_COUNTS["decode"] += 1
+    dm = device_model(params, cfg)
+    x = _tokens(lat).clone()
+    dm.run_blocks(x, [f"dec.blk{i}" for i in range(cfg.dec_blocks)])
+    g = cfg.grid
+    surface = torch.empty((cfg.surface_out, g.rows, g.cols), dtype=torch.float32, device="cuda")
+    atmos = torch.empty((cfg.atmos_vars, cfg.levels, g.rows, g.cols), dtype=torch.float32, device="cuda")
+    decode_planes(dm.decoder(), dm.buffers(), cfg, x, surface, atmos)
+    return DecodedFields(lat.valid_time, Tensor(device=surface), Tensor(device=atmos))
+
+
+def blend_latents(latents: list, weights) -> LatentState:
+    """Convex combination of same-time latent states (model.py:424-449)."""
+    if not latents:
+        raise ConfigError("blend of zero latent states")
+    t0, ext = latents[0].valid_time, latents[0].extents
+    for lt in latents[1:]:
+        if lt.valid_time != t0:
+            raise ConfigError(f"blend of mismatched valid times {t0} and {lt.valid_time}")
+        if tuple(lt.extents) != tuple(ext):
+            raise ConfigError("blend of mismatched latent extents")
+    w = np.asarray(getattr(weights, "values", weights), dtype=np.float64)
+    if w.shape != (len(latents),):
+        raise ConfigError(f"{len(latents)} states but weight shape {w.shape}")
+    if (w < 0).any() or abs(w.sum() - 1.0) > 1e-12:
+        raise ConfigError("blend weights must be nonnegative and sum to 1")
+    out = _tokens(latents[0]) * float(w[0])
+    for wi, lt in zip(w[1:], latents[1:]):
+        out.add_(_tokens(lt), alpha=float(wi))
+    return LatentState(Tensor(device=out), t0, ext)

@@ -50,7 +50,7 @@ def layernorm_bf16(x: torch.Tensor, gain: torch.Tensor, bias: torch.Tensor, ldo:
     m, n = x.shape
     ldo = n if ldo is None else int(ldo)
     if out is None:
-        out = torch.empty((m, ldo), dtype=torch.bfloat16, device=x.device)
+        out = torch.empty((m, ldo), dtype=_lib.ELEM, device=x.device)
     check(_lib.lib().wm3_layernorm_bf16(ptr(x), x.stride(0), m, n, ptr(gain), ptr(bias), float(eps), ptr(out),
                                         out.stride(0), stream_ptr()), "wm3_layernorm_bf16")
     return out
@@ -60,8 +60,8 @@ def linear(a: torch.Tensor, w: torch.Tensor, epi: int, bias: torch.Tensor | None
            out: torch.Tensor | None = None, n_valid: int | None = None,
            rope: "_lib.RopeT | None" = None) -> torch.Tensor:
     """out = epilogue(a @ w.T + bias); a (M, K) bf16, w (N, K) bf16 (weights stored (out, in))."""
-    _req(a, torch.bfloat16, "a")
-    _req(w, torch.bfloat16, "w")
+    _req(a, _lib.ELEM, "a")
+    _req(w, _lib.ELEM, "w")
     m, k = a.shape
     n, k2 = w.shape
     if k2 != k:
@@ -70,8 +70,8 @@ def linear(a: torch.Tensor, w: torch.Tensor, epi: int, bias: torch.Tensor | None
     if out is None:
         if epi == _lib.WM3_EPI_BIAS_RESID_F32:
             raise RuntimeError("residual epilogue needs the fp32 stream as `out`")
-        out = torch.empty((m, n), dtype=torch.float32 if f32_out else torch.bfloat16, device=a.device)
-    _req(out, torch.float32 if f32_out else torch.bfloat16, "out")
+        out = torch.empty((m, n), dtype=torch.float32 if f32_out else _lib.ELEM, device=a.device)
+    _req(out, torch.float32 if f32_out else _lib.ELEM, "out")
     nv = out.shape[1] if n_valid is None else int(n_valid)
     rp = None if rope is None else ctypes_byref(rope)
     check(_lib.lib().wm3_linear(ptr(a), a.stride(0), ptr(w), w.stride(0), m, n, k, int(epi), ptr(out),
@@ -110,9 +110,9 @@ class KVGrid:
 def linear_grid(a: torch.Tensor, w: torch.Tensor, epi: int, bias: torch.Tensor, out: torch.Tensor, grid: KVGrid,
                 rope: "_lib.RopeT | None" = None) -> torch.Tensor:
     """linear() whose output rows (band tokens) land in the K/V grid `out` (halo rows left untouched)."""
-    _req(a, torch.bfloat16, "a")
-    _req(w, torch.bfloat16, "w")
-    _req(out, torch.bfloat16, "out")
+    _req(a, _lib.ELEM, "a")
+    _req(w, _lib.ELEM, "w")
+    _req(out, _lib.ELEM, "out")
     m, k = a.shape
     n = w.shape[0]
     rp = None if rope is None else ctypes_byref(rope)
@@ -127,7 +127,7 @@ def linear_grid(a: torch.Tensor, w: torch.Tensor, epi: int, bias: torch.Tensor, 
 def natten(qkv: torch.Tensor, grid: KVGrid, heads: int, dhp: int, dh: int, window,
            out: torch.Tensor | None = None, rows_global: int | None = None, row0: int = 0) -> torch.Tensor:
     """Fused neighborhood attention over the padded qkv grid -> ctx (T, heads*dhp) bf16, band token order."""
-    _req(qkv, torch.bfloat16, "qkv")
+    _req(qkv, _lib.ELEM, "qkv")
     if qkv.shape[0] != grid.tokens:
         raise RuntimeError(f"qkv has {qkv.shape[0]} rows, padded grid needs {grid.tokens}")
     wd, wh, ww = (int(e) for e in window)
@@ -135,8 +135,8 @@ def natten(qkv: torch.Tensor, grid: KVGrid, heads: int, dhp: int, dh: int, windo
     rg = h if rows_global is None else int(rows_global)
     t = d * h * w
     if out is None:
-        out = torch.empty((t, heads * dhp), dtype=torch.bfloat16, device=qkv.device)
-    _req(out, torch.bfloat16, "out")
+        out = torch.empty((t, heads * dhp), dtype=_lib.ELEM, device=qkv.device)
+    _req(out, _lib.ELEM, "out")
     check(_lib.lib().wm3_natten_fwd(ptr(qkv), qkv.stride(0), ptr(out), out.stride(0), d, h, w, rg, int(row0),
                                     grid.halo_lo, grid.halo_hi, int(heads), int(dhp), wd, wh, ww,
                                     float(1.0 / math.sqrt(dh)), stream_ptr()), "wm3_natten_fwd")

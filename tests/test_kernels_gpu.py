@@ -58,8 +58,8 @@ def test_neighbor_table_band_rows_match_full():
                                    (777, 1024, 4096), (81, 128, 192)])
 def test_gemm_f32(m, n, k):
     g = torch.Generator(device="cuda").manual_seed(m + n + k)
-    a = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
-    w = torch.randn(n, k, device="cuda", generator=g).to(torch.bfloat16)
+    a = torch.randn(m, k, device="cuda", generator=g).to(lib().ELEM)
+    w = torch.randn(n, k, device="cuda", generator=g).to(lib().ELEM)
     out = ops().linear(a, w, lib().WM3_EPI_F32)
     ref = a.float() @ w.float().T
     torch.cuda.synchronize()
@@ -70,8 +70,8 @@ def test_gemm_f32(m, n, k):
 def test_gemm_epilogues():
     m, n, k = 517, 512, 256
     g = torch.Generator(device="cuda").manual_seed(5)
-    a = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
-    w = (torch.randn(n, k, device="cuda", generator=g) / 16).to(torch.bfloat16)
+    a = torch.randn(m, k, device="cuda", generator=g).to(lib().ELEM)
+    w = (torch.randn(n, k, device="cuda", generator=g) / 16).to(lib().ELEM)
     b = torch.randn(n, device="cuda", generator=g)
     ref = a.float() @ w.float().T + b
     L = lib()
@@ -128,7 +128,7 @@ def na_reference(qkv, ext, heads, dhp, dh, win):
 def test_natten_matches_gather_reference(ext, win, heads, dhp):
     t = int(np.prod(ext))
     g = torch.Generator(device="cuda").manual_seed(t)
-    qkv = (torch.randn(t, 3 * heads * dhp, device="cuda", generator=g) * 1.5).to(torch.bfloat16)
+    qkv = (torch.randn(t, 3 * heads * dhp, device="cuda", generator=g) * 1.5).to(lib().ELEM)
     grid = ops().KVGrid(ext, win)
     out = ops().natten(ops().pad_tokens_to_grid(qkv, grid), grid, heads, dhp, dhp, win)
     ref, _ = na_reference(qkv, ext, heads, dhp, dhp, win)
