@@ -1,0 +1,125 @@
+"""CPU: latitude-band sharding host logic with a real 2- and 4-rank gloo process group.
+
+Each rank holds only its band's K/V rows, the HaloExchanger fills the halos from its neighbours, and the
+band-local neighborhood attention (computed here with the float64 oracle on the band + halo rows) must equal
+the global oracle attention rows of that band exactly.
+"""
+
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle.grid import neighborhood
+from paper_2503_22235_b200.bands import HaloExchanger, band_rows, plan_bands
+from paper_2503_22235_b200.ops import KVGrid
+
+
+def test_band_rows_balanced():
+    assert [n for _, n in band_rows(90, 8)] == [12, 11, 11, 11, 11, 11, 11, 12]
+    assert [n for _, n in band_rows(90, 4)] == [23, 22, 22, 23]
+    assert [n for _, n in band_rows(90, 2)] == [45, 45]
+    assert sum(n for _, n in band_rows(17, 3)) == 17
+
+
+def test_plan_bands_halos():
+    bands = plan_bands(90, 7, 8)
+    assert bands[0].halo_lo == 0 and bands[-1].halo_hi == 0
+    assert all(b.halo_lo == 3 for b in bands[1:]) and all(b.halo_hi == 3 for b in bands[:-1])
+    # a pole band's bumped windows stay inside a band of >= 7 rows
+    assert plan_bands(90, 7, 1)[0].halo_lo == 0 and plan_bands(90, 7, 1)[0].halo_hi == 0
+    with pytest.raises(ValueError):
+        plan_bands(9, 7, 4)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _band_attention(q, k, v, ext, win, band, heads):
+    """Oracle NA for the band's queries using only band + halo K/V rows (local buffer indexing)."""
+    d, h, w = ext
+    full_tab = neighborhood(ext, win)  # global indices
+    t = np.arange(d * h * w).reshape(d, h, w)[:, band.row0:band.row0 + band.rows].reshape(-1)
+    gd, gr, gc = np.unravel_index(full_tab[t], (d, h, w))
+    rows_ext = band.rows + band.halo_lo + band.halo_hi
+    lr = gr - (band.row0 - band.halo_lo)
+    assert lr.min() >= 0 and lr.max() < rows_ext, "halo too small for the window reach"
+    local = (gd * rows_ext + lr) * w + gc
+    dh = q.shape[-1] // heads
+    qq = q.reshape(len(t), heads, dh)
+    kk = k.reshape(-1, heads, dh)[local]
+    vv = v.reshape(-1, heads, dh)[local]
+    s = np.einsum("thd,tkhd->thk", qq, kk) / math.sqrt(dh)
+    p = np.exp(s - s.max(-1, keepdims=True))
+    p /= p.sum(-1, keepdims=True)
+    return np.einsum("thk,tkhd->thd", p, vv).reshape(len(t), -1)
+
+
+def _worker(rank, world, port, ext, win, heads, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        d, h, w = ext
+        rng = np.random.default_rng(0)
+        c = 8 * heads
+        q = rng.standard_normal((d * h * w, c))
+        k = rng.standard_normal((d * h * w, c))
+        v = rng.standard_normal((d * h * w, c))
+        bands = plan_bands(h, win[1], world)
+        me = bands[rank]
+        grid = KVGrid((d, me.rows, w), win, me.halo_lo, me.halo_hi)
+        # this rank's K/V grid: only its own rows are filled, halos start as NaN
+        kv = np.concatenate([k, v], axis=1).reshape(d, h, w, -1)
+        buf = torch.full((grid.tokens, 2 * c), float("nan"), dtype=torch.float64)
+        g = buf.view(d, grid.rows_ext, w, -1)
+        g[:, me.halo_lo:me.halo_lo + me.rows] = torch.from_numpy(kv[:, me.row0:me.row0 + me.rows])
+        HaloExchanger(bands, rank)(buf, grid)
+        lo, hi = me.row0 - me.halo_lo, me.row0 + me.rows + me.halo_hi
+        ok_halo = np.array_equal(g.numpy(), kv[:, lo:hi])
+        kb = g.numpy().reshape(-1, 2 * c)
+        qb = q.reshape(d, h, w, c)[:, me.row0:me.row0 + me.rows].reshape(-1, c)
+        got = _band_attention(qb, kb[:, :c], kb[:, c:], ext, win, me, heads)
+        out_q.put((rank, ok_halo, got))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,ext", [(2, (3, 16, 12)), (4, (2, 30, 10))])
+def test_halo_exchange_gloo_band_attention(world, ext):
+    win, heads = (3, 7, 5), 2
+    win = (min(win[0], ext[0]), win[1], win[2])
+    ctx = mp.get_context("spawn")
+    q_out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, ext, win, heads, q_out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict((r, (ok, got)) for r, ok, got in (q_out.get(timeout=120) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # global oracle attention
+    d, h, w = ext
+    rng = np.random.default_rng(0)
+    c = 8 * heads
+    q, k, v = (rng.standard_normal((d * h * w, c)) for _ in range(3))
+    tab = neighborhood(ext, win)
+    dh = c // heads
+    s = np.einsum("thd,tkhd->thk", q.reshape(-1, heads, dh), k.reshape(-1, heads, dh)[tab]) / math.sqrt(dh)
+    p = np.exp(s - s.max(-1, keepdims=True))
+    p /= p.sum(-1, keepdims=True)
+    full = np.einsum("thk,tkhd->thd", p, v.reshape(-1, heads, dh)[tab]).reshape(d, h, w, c)
+    for rank, b in enumerate(plan_bands(h, win[1], world)):
+        ok, got = results[rank]
+        assert ok, f"rank {rank} halo rows differ from the neighbours' rows"
+        np.testing.assert_allclose(got.reshape(d, b.rows, w, c), full[:, b.row0:b.row0 + b.rows], atol=1e-12)

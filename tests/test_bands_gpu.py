@@ -1,0 +1,82 @@
+"""Latitude-band path on one B200: every band of a full-width block is computed with the band kernels (QKV GEMM
+into a halo'd K/V grid with global-row rotary phases, NA with row0/halos) and must reproduce the single-band
+result.  The halo exchange is emulated by device copies between the bands' buffers (the multi-process
+NCCL/gloo exchange itself is covered by tests/test_bands_cpu.py); no kernel ever waits on another."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("world,ext,dim,heads", [(2, (5, 18, 36), 256, 2), (4, (7, 30, 18), 256, 2),
+                                                  (8, (5, 90, 180), 1024, 8)])
+def test_band_block_matches_full(world, ext, dim, heads):
+    from paper_2503_22235_b200 import _lib, ops
+    from paper_2503_22235_b200.bands import gather_bands, local_band_tokens, plan_bands
+    from paper_2503_22235_b200.blocks import RopeTables, Workspace, block_forward
+    from paper_2503_22235_b200.params import init_block_params
+    from paper_2503_22235_b200.runtime import CACHE
+
+    win = (5, 7, 7)
+    d, h, w = ext
+    params = init_block_params(np.random.default_rng(0), dim, heads, "blk", zero_residual=False)
+    bw = CACHE.block(params, "blk", heads)
+    rope = RopeTables(ext, dim // heads)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn(d * h * w, dim, device="cuda", generator=g)
+
+    full = x.clone()
+    block_forward(full, bw, Workspace(ops.KVGrid(ext, win), bw), rope, ext, win)
+
+    bands = plan_bands(h, win[1], world)
+    xs = [local_band_tokens(x, ext, b).clone() for b in bands]
+    wss = [Workspace(ops.KVGrid((d, b.rows, w), win, b.halo_lo, b.halo_hi), bw) for b in bands]
+    # phase 1: LN1 + QKV GEMM of every band into its own K/V grid
+    for b, xb, ws in zip(bands, xs, wss):
+        ops.layernorm_bf16(xb, bw.ln1_g, bw.ln1_b, out=ws.hn)
+        ops.linear_grid(ws.hn, bw.w_qkv, _lib.WM3_EPI_QKV_ROPE, bw.b_qkv, ws.qkv, ws.grid,
+                        rope=rope.struct((d, b.rows, w), b.row0, bw.heads, bw.dhp))
+    # phase 2: halo exchange by copies between neighbouring bands
+    for r, (b, ws) in enumerate(zip(bands, wss)):
+        gme = ws.qkv.view(d, ws.grid.rows_ext, w, -1)
+        if b.halo_lo:
+            up, gup = bands[r - 1], wss[r - 1].qkv.view(d, wss[r - 1].grid.rows_ext, w, -1)
+            s0 = up.halo_lo + up.rows - b.halo_lo
+            gme[:, :b.halo_lo] = gup[:, s0:s0 + b.halo_lo]
+        if b.halo_hi:
+            dn, gdn = bands[r + 1], wss[r + 1].qkv.view(d, wss[r + 1].grid.rows_ext, w, -1)
+            gme[:, b.halo_lo + b.rows:] = gdn[:, dn.halo_lo:dn.halo_lo + b.halo_hi]
+    # phase 3: the rest of the block, per band
+    for b, xb, ws in zip(bands, xs, wss):
+        ops.natten(ws.qkv, ws.grid, bw.heads, bw.dhp, bw.dh, win, out=ws.ctx, rows_global=h, row0=b.row0)
+        ops.linear(ws.ctx, bw.w_o, _lib.WM3_EPI_BIAS_RESID_F32, bias=bw.b_o, out=xb, n_valid=bw.hidden)
+        ops.layernorm_bf16(xb, bw.ln2_g, bw.ln2_b, out=ws.hn)
+        ops.linear(ws.hn, bw.w_1, _lib.WM3_EPI_BIAS_GELU_BF16, bias=bw.b_1, out=ws.mid)
+        ops.linear(ws.mid, bw.w_2, _lib.WM3_EPI_BIAS_RESID_F32, bias=bw.b_2, out=xb, n_valid=bw.hidden)
+    banded = gather_bands(xs, ext, bands)
+    torch.cuda.synchronize()
+    upd_full, upd_band = full - x, banded - x
+    rel = float((upd_band - upd_full).norm() / upd_full.norm())
+    assert rel < 2e-3, rel
+
+
+def test_band_block_forward_with_callback_single_band():
+    """block_forward's halo hook path with a no-op exchanger on a band that needs no halos (world = 1)."""
+    from paper_2503_22235_b200 import ops
+    from paper_2503_22235_b200.blocks import RopeTables, Workspace, block_forward
+    from paper_2503_22235_b200.params import init_block_params
+    from paper_2503_22235_b200.runtime import CACHE
+    ext, win, dim, heads = (5, 18, 36), (5, 7, 7), 256, 2
+    params = init_block_params(np.random.default_rng(1), dim, heads, "blk", zero_residual=False)
+    bw = CACHE.block(params, "blk", heads)
+    rope = RopeTables(ext, dim // heads)
+    x = torch.randn(int(np.prod(ext)), dim, device="cuda")
+    a, b = x.clone(), x.clone()
+    calls = []
+    block_forward(a, bw, Workspace(ops.KVGrid(ext, win), bw), rope, ext, win)
+    block_forward(b, bw, Workspace(ops.KVGrid(ext, win), bw), rope, ext, win, row0=0, rows_global=ext[1],
+                  halo_exchange=lambda buf, grid: calls.append(grid.rows_ext))
+    assert calls == [ext[1]]
+    assert torch.equal(a, b)
