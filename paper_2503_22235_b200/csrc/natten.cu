@@ -7,14 +7,15 @@
 //
 // Persistent, warp-specialised CTA (one per SM, 320 threads):
 //   warp 9      TMA producer (one thread): the Q tile (4D box TD x TH x TW) and each chunk's K and V head
-//               slices (4D box ncp x nrpc) into SWIZZLE_128B tiles, double-buffered K/V slots, mbarrier tx
-//   warp 8      MMA issuer (one thread): S = Q K^T into one of two TMEM S buffers (M128 N128 K=dhp),
-//               O += P V (M128 N=dhp K=128, V read MN-major), O accumulated in TMEM across chunks;
-//               S_{j+1} is issued before PV_j so the tensor core works while softmax runs
+//               slices (4D box ncp x nrpc) into SWIZZLE_128B tiles: 3 K slots (freed by Q K^T), 2 V slots
+//               (freed by P V), K issued one chunk ahead of V; completion via mbarrier transaction counts
+//   warp 8      MMA issuer (one thread): S = Q K^T into one of two TMEM S buffers (M128 N128 K=dhp, both
+//               operands from smem), O += P V with P read from TMEM (M128 N=dhp K=128, V MN-major from its
+//               TMA tile), O accumulated in TMEM across chunks; S_{j+1} is issued before PV_j
 //   warps 0-7   softmax (one thread per query row and key-column half, two warps per TMEM lane quarter):
 //               window bitmask built from the same integer formula as grid.py (bump on depth/rows, wrap on
 //               cols), fp32 running max / sum with lazy O rescaling (only when the max grows by > 2^8),
-//               exp2, P (bf16) -> smem; finally O / l -> bf16 ctx rows.
+//               exp2, P (fp16) -> TMEM (double-buffered); finally O / l -> ctx rows.
 // The logits never leave the SM.  Output ctx rows are bf16 [T][heads][dhp] = the O-proj GEMM operand.
 #include "common.cuh"
 #include "launch.h"
@@ -31,6 +32,7 @@ struct NaParams {
   int TD, TH, TW, ntd, nth, ntw, nitems;
   int ncp, nrpc;  // key-chunk box: ncp columns x nrpc rows (fixed for every tile)
   float scale_log2;
+  int dbg;  // profiling switch (WM3_NA_DEBUG): 1 = skip the softmax arithmetic, 2 = also skip the MMAs
 };
 
 // warps 0-7 softmax (warp w: TMEM lanes 32 (w % 4).., key / O columns half w / 4), 8 MMA, 9 TMA producer
@@ -39,8 +41,13 @@ constexpr int NA_MMA_WARP = 8;
 constexpr int NA_TMA_WARP = 9;
 constexpr int NA_THREADS = 320;
 constexpr uint32_t NA_TILE = 32768;  // 128 rows x 256 B
-// smem: Q | K0 V0 | K1 V1 | P | barriers (256 B) | row reductions (2 halves x 128 rows x fp32)
-constexpr uint32_t NA_SMEM = 6 * NA_TILE + 1024 /*align*/ + 256 /*barriers*/ + 3072 /*reductions*/;
+constexpr int NA_KSLOTS = 3;         // K frees after Q K^T: three slots give the TMA two chunks of lead time
+constexpr int NA_VSLOTS = 2;         // V frees after P V
+// smem: Q | K0 K1 K2 | V0 V1 | barriers (256 B) | row-max / row-sum exchange (2 KB)
+constexpr uint32_t NA_SMEM_BODY = (1 + NA_KSLOTS + NA_VSLOTS) * NA_TILE;
+constexpr uint32_t NA_SMEM = NA_SMEM_BODY + 1024 /*align*/ + 256 /*barriers*/ + 2048 /*exchange*/;
+// TMEM columns: S0 [0,128) S1 [128,256) O [256,384) P0 [384,448) P1 [448,512) (P: fp16 pairs per column)
+constexpr uint32_t NA_TMEM_O = 256, NA_TMEM_P = 384;
 constexpr float NA_RESCALE_LOG2 = 8.0f;
 
 struct TileGeo {
@@ -114,20 +121,20 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sQ = smem_u32(smem);
-  auto sK = [&](int s) { return sQ + NA_TILE * (1 + 2 * s); };
-  auto sV = [&](int s) { return sQ + NA_TILE * (2 + 2 * s); };
-  const uint32_t sP = sQ + 5 * NA_TILE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * NA_TILE);
+  auto sK = [&](int s) { return sQ + NA_TILE * (1 + s); };
+  auto sV = [&](int s) { return sQ + NA_TILE * (1 + NA_KSLOTS + s); };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NA_SMEM_BODY);
   const uint32_t b0 = smem_u32(bars);
   const uint32_t bar_qfull = b0 + 0, bar_qempty = b0 + 8;
-  auto bar_kfull = [&](int s) { return b0 + 16 + 8 * s; };
-  auto bar_kempty = [&](int s) { return b0 + 32 + 8 * s; };
-  auto bar_sfull = [&](int s) { return b0 + 48 + 8 * s; };
-  auto bar_sempty = [&](int s) { return b0 + 64 + 8 * s; };
-  const uint32_t bar_pfull = b0 + 80, bar_pempty = b0 + 88, bar_ofull = b0 + 96, bar_oempty = b0 + 104;
-  auto bar_vfull = [&](int s) { return b0 + 112 + 8 * s; };
-  auto bar_vempty = [&](int s) { return b0 + 128 + 8 * s; };
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  auto bar_kfull = [&](int s) { return b0 + 16 + 8 * s; };   // 3
+  auto bar_kempty = [&](int s) { return b0 + 40 + 8 * s; };  // 3
+  auto bar_vfull = [&](int s) { return b0 + 64 + 8 * s; };   // 2
+  auto bar_vempty = [&](int s) { return b0 + 80 + 8 * s; };  // 2
+  auto bar_sfull = [&](int s) { return b0 + 96 + 8 * s; };   // 2
+  auto bar_sempty = [&](int s) { return b0 + 112 + 8 * s; }; // 2
+  auto bar_pempty = [&](int s) { return b0 + 128 + 8 * s; }; // 2
+  const uint32_t bar_pfull = b0 + 144, bar_ofull = b0 + 152, bar_oempty = b0 + 160;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -136,16 +143,18 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
   if (tid == 0) {
     mbar_init(bar_qfull, 1);
     mbar_init(bar_qempty, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NA_KSLOTS; ++s) {
       mbar_init(bar_kfull(s), 1);
       mbar_init(bar_kempty(s), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(bar_vfull(s), 1);
       mbar_init(bar_vempty(s), 1);
       mbar_init(bar_sfull(s), 1);
       mbar_init(bar_sempty(s), NA_SOFTMAX_WARPS);
+      mbar_init(bar_pempty(s), 1);
     }
     mbar_init(bar_pfull, NA_SOFTMAX_WARPS);
-    mbar_init(bar_pempty, 1);
     mbar_init(bar_ofull, 1);
     mbar_init(bar_oempty, NA_SOFTMAX_WARPS);
     fence_barrier_init();
@@ -155,7 +164,7 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
     tmem_relinquish();
   }
   // Zero the operand tiles once: rows past a box are never written by TMA and V rows feed P V (0 * NaN).
-  for (uint32_t off = tid * 16u; off < 5 * NA_TILE; off += NA_THREADS * 16u) st_shared_v4(sQ + off, 0, 0, 0, 0);
+  for (uint32_t off = tid * 16u; off < NA_SMEM_BODY; off += NA_THREADS * 16u) st_shared_v4(sQ + off, 0, 0, 0, 0);
   fence_proxy_async();
   tc_fence_before();
   __syncthreads();
@@ -166,8 +175,7 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
 
   if (warp == NA_TMA_WARP) {
     // =============================== TMA producer ===============================
-    // K slots free as soon as S = Q K^T retires, V slots only after P V: K loads run one chunk ahead of V
-    // so the next S never waits on a V slot.
+    // K runs one chunk ahead of V (K slots free after Q K^T, V slots only after P V).
     if (lane == 0) {
       tma_prefetch(&tmQ);
       tma_prefetch(&tmKV);
@@ -176,11 +184,12 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
       const uint32_t kbytes = halves * 128u * p.ncp * p.nrpc;
       int chunk_ctr = 0, tile_ctr = 0;
       auto load_kv = [&](const TileGeo& g, int j, int c, bool is_v) {
-        const int slot = c & 1;
+        const int slot = is_v ? (c % NA_VSLOTS) : (c % NA_KSLOTS);
+        const int use = is_v ? (c / NA_VSLOTS) : (c / NA_KSLOTS);
         int kd, kr0, nr, origin, vlo, vhi;
         chunk_geo(g, p.cols, j, kd, kr0, nr, origin, vlo, vhi);
         const uint32_t full = is_v ? bar_vfull(slot) : bar_kfull(slot);
-        mbar_wait(is_v ? bar_vempty(slot) : bar_kempty(slot), ((c >> 1) & 1) ^ 1);
+        mbar_wait(is_v ? bar_vempty(slot) : bar_kempty(slot), (use & 1) ^ 1);
         mbar_arrive_expect_tx(full, kbytes);
         const int c1 = origin, c2 = kr0 - brow0;  // may be negative / past the edge: TMA zero-fills
         const uint32_t dst = is_v ? sV(slot) : sK(slot);
@@ -206,39 +215,39 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
       const uint32_t idesc_s = make_idesc(128, 128, 0, 0);
       const uint32_t idesc_o = make_idesc(128, p.dhp, 0, 1);
       const int kb = p.dhp / 64;
-      const uint32_t tO = tmem + 256;
+      const uint32_t tO = tmem + NA_TMEM_O;
       int chunk_ctr = 0, tile_ctr = 0;
       auto issue_pv = [&](int c, bool first, bool last) {
-        const int slot = c & 1;
+        const int vs = c % NA_VSLOTS, pb = c & 1;
         mbar_wait(bar_pfull, c & 1);
-        mbar_wait(bar_vfull(slot), (c >> 1) & 1);
+        mbar_wait(bar_vfull(vs), (c / NA_VSLOTS) & 1);
         if (first) mbar_wait(bar_oempty, (tile_ctr & 1) ^ 1);
         tc_fence_after();
-        for (int s = 0; s < 8; ++s) {
-          const uint64_t ad = make_sdesc_sw128(sP + (s >> 2) * 16384u + (s & 3) * 32u, 16, 1024);
-          const uint64_t bd = make_sdesc_sw128(sV(slot) + s * 2048u, 16384, 1024);
-          umma_bf16_ss(tO, ad, bd, idesc_o, (!first || s > 0) ? 1u : 0u);
+        // O += P V: A = P from TMEM (fp16 pairs, 8 columns per 16 keys), B = V MN-major from its TMA tile
+        for (int s = 0; s < (p.dbg >= 2 ? 0 : 8); ++s) {
+          const uint64_t bd = make_sdesc_sw128(sV(vs) + s * 2048u, 16384, 1024);
+          umma_f16_ts(tO, tmem + NA_TMEM_P + 64 * pb + 8 * s, bd, idesc_o, (!first || s > 0) ? 1u : 0u);
         }
-        umma_commit(bar_vempty(slot));
-        umma_commit(bar_pempty);
+        umma_commit(bar_vempty(vs));
+        umma_commit(bar_pempty(pb));
         if (last) umma_commit(bar_ofull);
       };
       for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
         const TileGeo g = tile_geo(p, item);
         mbar_wait(bar_qfull, tile_ctr & 1);
         for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
-          const int slot = chunk_ctr & 1;
-          mbar_wait(bar_kfull(slot), (chunk_ctr >> 1) & 1);
-          mbar_wait(bar_sempty(slot), ((chunk_ctr >> 1) & 1) ^ 1);
+          const int ks = chunk_ctr % NA_KSLOTS, ss = chunk_ctr & 1;
+          mbar_wait(bar_kfull(ks), (chunk_ctr / NA_KSLOTS) & 1);
+          mbar_wait(bar_sempty(ss), ((chunk_ctr >> 1) & 1) ^ 1);
           tc_fence_after();
-          const uint32_t tS = tmem + 128 * slot;
-          for (int s = 0; s < kb * 4; ++s) {
+          const uint32_t tS = tmem + 128 * ss;
+          for (int s = 0; s < (p.dbg >= 2 ? 0 : kb * 4); ++s) {
             const uint32_t off = (s >> 2) * 16384u + (s & 3) * 32u;
-            umma_bf16_ss(tS, make_sdesc_sw128(sQ + off, 16, 1024), make_sdesc_sw128(sK(slot) + off, 16, 1024),
+            umma_bf16_ss(tS, make_sdesc_sw128(sQ + off, 16, 1024), make_sdesc_sw128(sK(ks) + off, 16, 1024),
                          idesc_s, s > 0 ? 1u : 0u);
           }
-          umma_commit(bar_sfull(slot));
-          umma_commit(bar_kempty(slot));
+          umma_commit(bar_sfull(ss));
+          umma_commit(bar_kempty(ks));
           if (j == g.nchunks - 1) umma_commit(bar_qempty);
           if (j > 0) issue_pv(chunk_ctr - 1, j - 1 == 0, false);
         }
@@ -248,14 +257,13 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
   } else if (warp < NA_SOFTMAX_WARPS) {
     // =============================== softmax / epilogue ===============================
     // Warp w owns query rows 32 (w % 4) .. +32 (its TMEM lane quarter) and half h = w / 4 of the key
-    // columns (P region h) and of the O columns; the two warps of a quarter combine row maxima and sums
+    // columns (P columns) and of the O columns; the two warps of a quarter combine row maxima and sums
     // through shared memory (named barrier 1 + quarter, 64 threads).
     const int quarter = warp & 3, half = warp >> 2;
     const int row = 32 * quarter + lane;  // query row in the tile
-    float* red = reinterpret_cast<float*>(smem + 6 * NA_TILE + 256);  // row maxima [chunk parity][half][128]
-    float* red_l = red + 512;                                            // row sums [half][128]
+    float* red = reinterpret_cast<float*>(smem + NA_SMEM_BODY + 256);  // [parity][half][128]
     const uint32_t lane_off = static_cast<uint32_t>(32 * quarter) << 16;
-    const uint32_t tO = tmem + 256;
+    const uint32_t tO = tmem + NA_TMEM_O;
     const int ocols = p.dhp / 2;  // O columns handled by this warp
     const int hw = (p.ww - 1) / 2;
     int chunk_ctr = 0, tile_ctr = 0;
@@ -272,7 +280,7 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
       const int c_lo = circle ? wrap_col((qvalid ? qw : g.w0) - hw, p.cols) : (qvalid ? qw : g.w0) - hw - g.pc0;
       float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
-        const int slot = chunk_ctr & 1;
+        const int ss = chunk_ctr & 1, pb = chunk_ctr & 1;
         int kd, kr0, nr, origin, vlo, vhi;
         chunk_geo(g, p.cols, j, kd, kr0, nr, origin, vlo, vhi);
         // ---- validity bits of this warp's 64 key columns [64 half, 64 half + 64) ----
@@ -289,46 +297,64 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
           }
         }
         // ---- S half -> registers ----
-        mbar_wait(bar_sfull(slot), (chunk_ctr >> 1) & 1);
+        mbar_wait(bar_sfull(ss), (chunk_ctr >> 1) & 1);
         tc_fence_after();
         uint32_t s[64];
-        tmem_ld32(tmem + 128 * slot + lane_off + 64 * half, *reinterpret_cast<uint32_t(*)[32]>(s));
-        tmem_ld32(tmem + 128 * slot + lane_off + 64 * half + 32, *reinterpret_cast<uint32_t(*)[32]>(s + 32));
+        tmem_ld32(tmem + 128 * ss + lane_off + 64 * half, *reinterpret_cast<uint32_t(*)[32]>(s));
+        tmem_ld32(tmem + 128 * ss + lane_off + 64 * half + 32, *reinterpret_cast<uint32_t(*)[32]>(s + 32));
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar_sempty(slot));
-        // ---- masked row max (raw scores), combined with the partner warp ----
-        float mx = -INFINITY;
-#pragma unroll
-        for (int k = 0; k < 64; ++k) mx = ((mk >> k) & 1ull) ? fmaxf(mx, __uint_as_float(s[k])) : mx;
-        float* rbuf = red + (chunk_ctr & 1) * 256;  // parity buffers: the partner may still read the last one
-        rbuf[half * 128 + row] = mx;
-        named_bar_sync(1 + quarter, 64);
-        mx = fmaxf(mx, rbuf[(half ^ 1) * 128 + row]);
-        mx = mx * p.scale_log2;
-        float alpha = 1.f;
-        if (mx > m_run + NA_RESCALE_LOG2) {  // lazy rescale (also covers m_run = -inf); same in both warps
-          alpha = exp2f(m_run - mx);
-          m_run = mx;
-        }
-        const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-        float lsum = 0.f;
+        if (lane == 0) mbar_arrive(bar_sempty(ss));
         uint32_t pk[32];
+        float alpha = 1.f, lsum = 0.f;
+        if (p.dbg) {
 #pragma unroll
-        for (int k = 0; k < 64; k += 2) {
-          float p0 = fast_exp2(fmaf(__uint_as_float(s[k]), p.scale_log2, -m_use));
-          float p1 = fast_exp2(fmaf(__uint_as_float(s[k + 1]), p.scale_log2, -m_use));
-          p0 = ((mk >> k) & 1ull) ? p0 : 0.f;
-          p1 = ((mk >> (k + 1)) & 1ull) ? p1 : 0.f;
-          lsum += p0 + p1;
-          pk[k >> 1] = pack_elem(p0, p1);
+          for (int i = 0; i < 32; ++i) pk[i] = 0u;
+        } else {
+          // ---- masked row max (raw scores), combined with the partner warp ----
+          // 8 independent accumulators: a serial 64-long FMNMX / FADD chain would be latency-bound.
+          const uint32_t mlo = static_cast<uint32_t>(mk), mhi = static_cast<uint32_t>(mk >> 32);
+          float mxa[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) mxa[i] = -INFINITY;
+#pragma unroll
+          for (int k = 0; k < 64; ++k) {
+            const bool ok = ((k < 32 ? mlo : mhi) >> (k & 31)) & 1u;
+            mxa[k & 7] = ok ? fmaxf(mxa[k & 7], __uint_as_float(s[k])) : mxa[k & 7];
+          }
+          float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                           fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
+          float* rbuf = red + (chunk_ctr & 1) * 256;  // parity buffers: the partner may still read the last one
+          rbuf[half * 128 + row] = mx;
+          named_bar_sync(1 + quarter, 64);
+          mx = fmaxf(mx, rbuf[(half ^ 1) * 128 + row]);
+          mx = mx * p.scale_log2;
+          if (mx > m_run + NA_RESCALE_LOG2) {  // lazy rescale (also covers m_run = -inf); same in both warps
+            alpha = exp2f(m_run - mx);
+            m_run = mx;
+          }
+          const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+          float lsa[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) lsa[i] = 0.f;
+#pragma unroll
+          for (int k = 0; k < 64; k += 2) {
+            float p0 = fast_exp2(fmaf(__uint_as_float(s[k]), p.scale_log2, -m_use));
+            float p1 = fast_exp2(fmaf(__uint_as_float(s[k + 1]), p.scale_log2, -m_use));
+            p0 = (((k < 32 ? mlo : mhi) >> (k & 31)) & 1u) ? p0 : 0.f;
+            p1 = (((k + 1 < 32 ? mlo : mhi) >> ((k + 1) & 31)) & 1u) ? p1 : 0.f;
+            lsa[(k >> 1) & 7] += p0 + p1;
+            pk[k >> 1] = pack_elem(p0, p1);
+          }
+          lsum = ((lsa[0] + lsa[1]) + (lsa[2] + lsa[3])) + ((lsa[4] + lsa[5]) + (lsa[6] + lsa[7]));
         }
         l_run = l_run * alpha + lsum;  // this warp's share of the row sum
-        // ---- P buffer free (previous PV retired) -> rescale this warp's O columns, write P region ----
-        mbar_wait(bar_pempty, (chunk_ctr & 1) ^ 1);
-        tc_fence_after();
+        // ---- P buffer pb free once P V of chunk c-2 retired; a rescale also needs P V of chunk c-1 ----
+        mbar_wait(bar_pempty(pb), ((chunk_ctr >> 1) & 1) ^ 1);
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+          mbar_wait(bar_pempty(pb ^ 1), ((chunk_ctr - 1) >> 1) & 1);
+          tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < ocols / 32; ++c) {
             uint32_t r[32];
@@ -339,27 +365,25 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
             for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
             tmem_st32(ta, r);
           }
-          tmem_st_wait();
         }
-        const uint32_t preg = sP + half * 16384u;
-#pragma unroll
-        for (int q = 0; q < 8; ++q)  // keys [64 half + 8q, +8) -> 16B chunk q of row `row`
-          st_shared_v4(preg + sw128_off(row, q), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-        fence_proxy_async();
+        tc_fence_after();
+        tmem_st32(tmem + NA_TMEM_P + 64 * pb + 32 * half + lane_off, pk);  // keys [64 half, +64) of my row
+        tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_pfull);
       }
-      // ---- epilogue: O / l -> bf16 ctx (row sum = both halves) ----
-      red_l[half * 128 + row] = l_run;
+      // ---- epilogue: O / l -> ctx (row sum = both halves) ----
+      float* rl = red + ((chunk_ctr) & 1) * 256;  // the parity buffer no warp of this quarter still reads
+      rl[half * 128 + row] = l_run;
       named_bar_sync(1 + quarter, 64);
-      const float l_tot = l_run + red_l[(half ^ 1) * 128 + row];
+      const float l_tot = l_run + rl[(half ^ 1) * 128 + row];
       mbar_wait(bar_ofull, tile_ctr & 1);
       tc_fence_after();
       const float inv_l = (qvalid && l_tot > 0.f) ? 1.f / l_tot : 0.f;
       elem_t* orow = p.out + (qvalid ? (static_cast<size_t>((qd * p.rows + qh) * p.cols + qw) * p.ldo +
-                                                g.head * p.dhp + half * ocols)
-                                             : 0);
+                                        g.head * p.dhp + half * ocols)
+                                     : 0);
 #pragma unroll 1
       for (int c = 0; c < ocols / 32; ++c) {
         uint32_t r[32];
@@ -379,7 +403,7 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
         }
       }
       tc_fence_before();
-      named_bar_sync(1 + quarter, 64);  // partner has read red[] before the next tile overwrites it
+      named_bar_sync(1 + quarter, 64);  // partner has read rl[] before the next tile writes this parity again
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_oempty);
     }
@@ -459,6 +483,10 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
   p.ntw = (cols + p.TW - 1) / p.TW;
   p.nitems = p.ntd * p.nth * p.ntw * heads;
   p.scale_log2 = scale * 1.4426950408889634f;
+  {
+    const char* e = getenv("WM3_NA_DEBUG");
+    p.dbg = e ? atoi(e) : 0;
+  }
   const uint64_t wp = cols;
   const uint64_t dims[4] = {static_cast<uint64_t>(3 * heads * dhp), wp, static_cast<uint64_t>(p.rows_ext),
                             static_cast<uint64_t>(depth)};
