@@ -114,6 +114,9 @@ int wm3_fields_to_nhwc(const float* src, long long img_stride, long long a_strid
 /* fp32 tokens [img][H][W][channels] -> padded NHWC (model.py:357-360). */
 int wm3_tokens_to_nhwc(const float* tokens, int imgs, int h, int w, int channels, int cp, void* dst, void* stream);
 
+/* Profiling aid: cycles for `reps` groups of 8 K=16 MMAs (mode 0 SS, 1 TS, 2 TS with MN-major B), N = n. */
+int wm3_mma_probe(int mode, int n, int reps, int ctas, long long* out_cycles, void* stream);
+
 /* Debug export of the kernel's own window arithmetic: per token, the (start_d, start_h, col_off)
  * it uses; int32 [T][3]. */
 int wm3_natten_windows(int depth, int rows, int cols, int rows_global, int row0, int wd, int wh, int ww,
