@@ -41,15 +41,11 @@ enum {
 /* Rotary description for WM3_EPI_QKV_ROPE (attention.py:48-92).  Output columns are laid out
  * [3][heads][dhp]; within a q/k head, rotation pair j (reference columns j, j + dh/2) sits at the
  * adjacent columns (2j, 2j + 1), j < dh/2 (a permutation shared by q and k leaves q.k unchanged).
- * rope_cos/rope_sin are [3][emax][64] fp32 per-axis tables (axis 0 depth, 1 row, 2 col); pair
- * j < pd uses the depth table, j < pd+pr the row table, else the col table. */
+ * pairs: per GEMM row (token of the local band) 128 fp32 = cos[64] then sin[64] of the rotary phases of
+ * its global (depth, row, col) position (64-aligned rows; pairs >= dh/2 are (1, 0)). */
 typedef struct {
-  const float* rope_cos;
-  const float* rope_sin;
-  int emax;
-  int depth, rows, cols; /* local token-grid extents: token t = (d*rows + r)*cols + c */
-  int row0;              /* global row of local row 0 (latitude band offset) */
-  int heads, dhp, pd, pr;
+  const float* pairs;
+  int heads, dhp;
 } wm3_rope_t;
 
 const char* wm3_last_error(void);

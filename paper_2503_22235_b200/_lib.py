@@ -32,11 +32,7 @@ _ll = ctypes.c_longlong
 
 class RopeT(ctypes.Structure):
     """wm3_rope_t (include/wm3.h)."""
-    _fields_ = [
-        ("rope_cos", _vp), ("rope_sin", _vp), ("emax", _i),
-        ("depth", _i), ("rows", _i), ("cols", _i), ("row0", _i),
-        ("heads", _i), ("dhp", _i), ("pd", _i), ("pr", _i),
-    ]
+    _fields_ = [("pairs", _vp), ("heads", _i), ("dhp", _i)]
 
 
 # name -> argtypes; every function returns int status

@@ -193,11 +193,27 @@ class RopeTables:
         self.sin = torch.from_numpy(sin).to(device)
         self.pd, self.pr, self.emax = pd, pr, emax
         self.extents = tuple(int(e) for e in extents)
+        self._pairs: dict = {}
+
+    def pair_table(self, local_extents, row0: int) -> torch.Tensor:
+        """[T_local][2][64] fp32: (cos, sin) of every rotary pair of each token of the band (global rows)."""
+        d, h, w = (int(e) for e in local_extents)
+        key = (d, h, w, int(row0))
+        tab = self._pairs.get(key)
+        if tab is None:
+            dev = self.cos.device
+            dd = torch.arange(d, device=dev).view(d, 1, 1).expand(d, h, w).reshape(-1)
+            rr = (torch.arange(h, device=dev) + int(row0)).view(1, h, 1).expand(d, h, w).reshape(-1)
+            cc = torch.arange(w, device=dev).view(1, 1, w).expand(d, h, w).reshape(-1)
+            pair = torch.arange(64, device=dev)
+            axis = torch.where(pair < self.pd, 0, torch.where(pair < self.pd + self.pr, 1, 2))
+            coord = torch.stack([dd, rr, cc], 1)[:, axis]                       # (T, 64)
+            tab = torch.stack([self.cos[axis, coord, pair], self.sin[axis, coord, pair]], 1).contiguous()
+            self._pairs[key] = tab
+        return tab
 
     def struct(self, local_extents, row0: int, heads: int, dhp: int) -> _lib.RopeT:
-        d, h, w = local_extents
-        return _lib.RopeT(self.cos.data_ptr(), self.sin.data_ptr(), self.emax, d, h, w, int(row0), heads, dhp,
-                          self.pd, self.pr)
+        return _lib.RopeT(self.pair_table(local_extents, row0).data_ptr(), heads, dhp)
 
 
 class Workspace:

@@ -21,6 +21,7 @@ namespace wm3 {
 struct EpiParams {
   const float* resid;  // fp32 residual stream (read), same buffer the output map writes
   int ld_resid;
+  int resid_v8;  // residual base and pitch 32 B aligned: 256-bit loads
   const float* bias;
   int n_valid;
   // GEMM rows form `planes` planes of `plane_rows` rows; M-tiles never straddle a plane, so every tile
@@ -53,29 +54,48 @@ struct EpiTraits {
   static constexpr int CW = F32 ? 32 : 64;  // columns per staged chunk (128 B rows)
 };
 
-// Rotary on interleaved pairs: columns (2i, 2i+1) of a q/k head hold the reference pair (i, i + dh/2).
-DEVI void rope_chunk(const wm3_rope_t& rp, int row, int M, int col0_in_head, float (&v)[64]) {
-  const int t = row < M ? row : 0;
-  const int c = t % rp.cols;
-  const int rr = (t / rp.cols) % rp.rows + rp.row0;
-  const int d = t / (rp.cols * rp.rows);
-  const float* cd = rp.rope_cos + (0 * rp.emax + d) * 64;
-  const float* ch = rp.rope_cos + (1 * rp.emax + rr) * 64;
-  const float* cw = rp.rope_cos + (2 * rp.emax + c) * 64;
-  const float* sd = rp.rope_sin + (0 * rp.emax + d) * 64;
-  const float* sh = rp.rope_sin + (1 * rp.emax + rr) * 64;
-  const float* sw = rp.rope_sin + (2 * rp.emax + c) * 64;
-  const int pd = rp.pd, pdr = rp.pd + rp.pr;
-  const int i0 = col0_in_head >> 1;
+// 32 residual floats of one row at column n: 256-bit loads when the residual base and pitch are 32 B
+// aligned (else 128-bit), scalar tail at n_valid.
+template <class EP>
+DEVI void load_resid(const EP& ep, int row, bool row_ok, int n, float (&x)[32]) {
+  const float* src = ep.resid + static_cast<size_t>(row) * ep.ld_resid + n;
 #pragma unroll
-  for (int e = 0; e < 32; ++e) {
-    const int i = i0 + e;
-    const float* cp = i < pd ? cd : (i < pdr ? ch : cw);
-    const float* sp = i < pd ? sd : (i < pdr ? sh : sw);
-    const float cs = __ldg(cp + i), sn = __ldg(sp + i);
-    const float x1 = v[2 * e], x2 = v[2 * e + 1];
-    v[2 * e] = x1 * cs - x2 * sn;
-    v[2 * e + 1] = x1 * sn + x2 * cs;
+  for (int j = 0; j < 4; ++j) {
+    float t[8];
+    if (row_ok && n + 8 * j + 8 <= ep.n_valid) {
+      if (ep.resid_v8) {
+        ldg256(src + 8 * j, t);
+      } else {
+        const float4 lo = *reinterpret_cast<const float4*>(src + 8 * j);
+        const float4 hi = *reinterpret_cast<const float4*>(src + 8 * j + 4);
+        t[0] = lo.x; t[1] = lo.y; t[2] = lo.z; t[3] = lo.w; t[4] = hi.x; t[5] = hi.y; t[6] = hi.z; t[7] = hi.w;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) t[e] = (row_ok && n + 8 * j + e < ep.n_valid) ? src[8 * j + e] : 0.f;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) x[8 * j + e] = t[e];
+  }
+}
+
+// Rotary on interleaved pairs: columns (2i, 2i+1) of a q/k head hold the reference pair (i, i + dh/2).
+// The per-token phase table holds cos[64] then sin[64] for token `row`; pairs [i0, i0 + 32) are read with
+// 256-bit loads (every head of a token reuses the same 512 B row, so it stays in L1/L2).
+DEVI void rope_chunk(const wm3_rope_t& rp, int row, int M, int col0_in_head, float (&v)[64]) {
+  const float* tab = rp.pairs + static_cast<size_t>(row < M ? row : 0) * 128 + (col0_in_head >> 1);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float cs[8], sn[8];
+    ldg256(tab + 8 * q, cs);
+    ldg256(tab + 64 + 8 * q, sn);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int k = 8 * q + e;
+      const float x1 = v[2 * k], x2 = v[2 * k + 1];
+      v[2 * k] = x1 * cs[e] - x2 * sn[e];
+      v[2 * k + 1] = x1 * sn[e] + x2 * cs[e];
+    }
   }
 }
 
@@ -203,27 +223,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int row = m0 + r_in_tile;
       const bool row_ok = (r0 + r_in_tile < ep.plane_rows) && row < M;
       // residual prefetch of this group's first chunk (overlaps the mainloop wait)
-      float4 xa[8], xb[8];
-      if (EPI == WM3_EPI_BIAS_RESID_F32) {
-        const float4* src = reinterpret_cast<const float4*>(ep.resid + static_cast<size_t>(row) * ep.ld_resid +
-                                                            n0 + g * CW);
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          xa[j] = (row_ok && n0 + g * CW + 4 * j < ep.n_valid) ? src[j] : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+      float xa[32], xb[32];
+      if (EPI == WM3_EPI_BIAS_RESID_F32) load_resid(ep, row, row_ok, n0 + g * CW, xa);
       mbar_wait(tfull_bar(acc), aphase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(32 * q) << 16);
 #pragma unroll
       for (int u = g; u < NUNITS; u += 2) {
         const int n = n0 + u * CW;
-        if (EPI == WM3_EPI_BIAS_RESID_F32 && u + 2 < NUNITS) {
-          const float4* src =
-              reinterpret_cast<const float4*>(ep.resid + static_cast<size_t>(row) * ep.ld_resid + n + 2 * CW);
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            xb[j] = (row_ok && n + 2 * CW + 4 * j < ep.n_valid) ? src[j] : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        if (EPI == WM3_EPI_BIAS_RESID_F32 && u + 2 < NUNITS) load_resid(ep, row, row_ok, n + 2 * CW, xb);
         if (Tr::F32) {
           uint32_t r[32];
           tmem_ld32(taddr + u * CW, r);
@@ -236,10 +244,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             for (int j = 0; j < 8; ++j) {
               const float4 b = (n + 4 * j < ep.n_valid) ? __ldg(reinterpret_cast<const float4*>(ep.bias + n) + j)
                                                         : make_float4(0.f, 0.f, 0.f, 0.f);
-              v[4 * j + 0] += b.x + xa[j].x;
-              v[4 * j + 1] += b.y + xa[j].y;
-              v[4 * j + 2] += b.z + xa[j].z;
-              v[4 * j + 3] += b.w + xa[j].w;
+              v[4 * j + 0] += b.x + xa[4 * j + 0];
+              v[4 * j + 1] += b.y + xa[4 * j + 1];
+              v[4 * j + 2] += b.z + xa[4 * j + 2];
+              v[4 * j + 3] += b.w + xa[4 * j + 3];
             }
           }
           // staging row: 8 x 16 B chunks of 4 floats
@@ -269,7 +277,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           if (EPI == WM3_EPI_BIAS_GELU_BF16) {
 #pragma unroll
-            for (int e = 0; e < 64; ++e) v[e] = gelu_erf(v[e]);
+            for (int e = 0; e < 64; ++e) v[e] = gelu_fast(v[e]);
           }
           if (EPI == WM3_EPI_QKV_ROPE) {
             const int sec = ep.rope.heads * ep.rope.dhp;
@@ -295,7 +303,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (Cfg::STAGING_PER_GROUP > 1) sbuf ^= 1;
         if (EPI == WM3_EPI_BIAS_RESID_F32) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) xa[j] = xb[j];
+          for (int j = 0; j < 32; ++j) xa[j] = xb[j];
         }
       }
       tc_fence_before();
@@ -366,9 +374,12 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
     return set_error("wm3_linear: %d planes x %d rows (stride %lld) do not tile m=%d", op.planes, op.plane_rows,
                      op.plane_stride, m);
   if (epi == WM3_EPI_BIAS_RESID_F32 && op.planes != 1) return set_error("wm3_linear: residual output must be 2D");
+  if (epi == WM3_EPI_QKV_ROPE && rope != nullptr && (reinterpret_cast<uintptr_t>(rope->pairs) % 32))
+    return set_error("wm3_linear: rope pair table must be 32-byte aligned");
   EpiParams ep{};
   ep.resid = reinterpret_cast<const float*>(out);
   ep.ld_resid = ldo;
+  ep.resid_v8 = (ldo % 8 == 0) && (reinterpret_cast<uintptr_t>(out) % 32 == 0);
   ep.bias = bias;
   ep.n_valid = n_valid;
   ep.plane_rows = op.plane_rows;

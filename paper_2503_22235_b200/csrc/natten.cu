@@ -5,21 +5,18 @@
 // TMEM lane).  The union of the tile's windows is walked as a list of key chunks, each a run of rows of
 // one depth plane x a contiguous (mod W) run of columns, <= 128 keys.
 //
-// Persistent, warp-specialised CTA (one per SM, 576 threads):
-//   warp 17     TMA producer (one thread): the Q tile (4D box TD x TH x TW) and each chunk's K and V head
+// Persistent, warp-specialised CTA (one per SM, 320 threads):
+//   warp 9      TMA producer (one thread): the Q tile (4D box TD x TH x TW) and each chunk's K and V head
 //               slices (4D box ncp x nrpc) into SWIZZLE_128B tiles: 3 K slots (freed by Q K^T), 2 V slots
 //               (freed by P V), K issued one chunk ahead of V; completion via mbarrier transaction counts
-//   warp 16     MMA issuer (one thread): S = Q K^T into one of two TMEM S buffers (M128 N128 K=dhp, both
+//   warp 8      MMA issuer (one thread): S = Q K^T into one of two TMEM S buffers (M128 N128 K=dhp, both
 //               operands from smem), O += P V with P read from TMEM (M128 N=dhp K=128, V MN-major from its
 //               TMA tile), O accumulated in TMEM across chunks; S_{j+1} is issued before PV_j
-//   warps 0-15  softmax (one thread per query row and 32 key columns, four warps per TMEM lane quarter):
+//   warps 0-7   softmax (one thread per query row and key-column half, two warps per TMEM lane quarter):
 //               window bitmask built from the same integer formula as grid.py (bump on depth/rows, wrap on
 //               cols), fp32 running max / sum with lazy O rescaling (only when the max grows by > 2^8),
 //               exp2, P (fp16) -> TMEM (double-buffered); finally O / l -> ctx rows.
 // The logits never leave the SM.  Output ctx rows are bf16 [T][heads][dhp] = the O-proj GEMM operand.
-#include <cstdio>
-#include <cstdlib>
-
 #include "common.cuh"
 #include "launch.h"
 #include "window.cuh"
@@ -36,26 +33,19 @@ struct NaParams {
   int ncp, nrpc;  // key-chunk box: ncp columns x nrpc rows (fixed for every tile)
   float scale_log2;
   int dbg;  // profiling switch (WM3_NA_DEBUG): 1 = skip the softmax arithmetic, 2 = also skip the MMAs
-  long long* trace;  // WM3_NA_TRACE: per-chunk clock64 stamps of CTA 0 (profiling only)
 };
-constexpr int NA_TRACE_CHUNKS = 48, NA_TRACE_EV = 12;
-#define NA_STAMP(c, ev)                                                                                \
-  do {                                                                                                \
-    if (p.trace != nullptr && blockIdx.x == 0 && (c) < NA_TRACE_CHUNKS) p.trace[(c) * NA_TRACE_EV + (ev)] = clock64(); \
-  } while (0)
 
-// warps 0-15 softmax (warp w: TMEM lanes 32 (w % 4).., key columns [32 (w / 4), +32)), 16 MMA, 17 TMA producer
-constexpr int NA_PARTS = 4;  // softmax warps per TMEM lane quarter
-constexpr int NA_SOFTMAX_WARPS = 4 * NA_PARTS;
-constexpr int NA_MMA_WARP = NA_SOFTMAX_WARPS;
-constexpr int NA_TMA_WARP = NA_SOFTMAX_WARPS + 1;
-constexpr int NA_THREADS = 32 * (NA_SOFTMAX_WARPS + 2);
+// warps 0-7 softmax (warp w: TMEM lanes 32 (w % 4).., key / O columns half w / 4), 8 MMA, 9 TMA producer
+constexpr int NA_SOFTMAX_WARPS = 8;
+constexpr int NA_MMA_WARP = 8;
+constexpr int NA_TMA_WARP = 9;
+constexpr int NA_THREADS = 320;
 constexpr uint32_t NA_TILE = 32768;  // 128 rows x 256 B
 constexpr int NA_KSLOTS = 3;         // K frees after Q K^T: three slots give the TMA two chunks of lead time
 constexpr int NA_VSLOTS = 2;         // V frees after P V
 // smem: Q | K0 K1 K2 | V0 V1 | barriers (256 B) | row-max / row-sum exchange (2 KB)
 constexpr uint32_t NA_SMEM_BODY = (1 + NA_KSLOTS + NA_VSLOTS) * NA_TILE;
-constexpr uint32_t NA_SMEM = NA_SMEM_BODY + 1024 /*align*/ + 256 /*barriers*/ + 2 * NA_PARTS * 512 /*exchange*/;
+constexpr uint32_t NA_SMEM = NA_SMEM_BODY + 1024 /*align*/ + 256 /*barriers*/ + 2048 /*exchange*/;
 // TMEM columns: S0 [0,128) S1 [128,256) O [256,384) P0 [384,448) P1 [448,512) (P: fp16 pairs per column)
 constexpr uint32_t NA_TMEM_O = 256, NA_TMEM_P = 384;
 constexpr float NA_RESCALE_LOG2 = 8.0f;
@@ -221,97 +211,60 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
     }
   } else if (warp == NA_MMA_WARP) {
     // =============================== MMA issuer ===============================
-    // A polling scheduler over two in-order streams: S_c = Q K_c^T (needs K_c, a free S buffer, the tile's
-    // Q) and PV_c (needs P_c from softmax, V_c, and for a tile's first chunk the drained O).  Whichever is
-    // ready is issued, so S runs up to two chunks ahead of the softmax, across tile boundaries.
     if (lane == 0) {
       const uint32_t idesc_s = make_idesc(128, 128, 0, 0);
       const uint32_t idesc_o = make_idesc(128, p.dhp, 0, 1);
       const int kb = p.dhp / 64;
       const uint32_t tO = tmem + NA_TMEM_O;
-      struct Cursor {
-        int item, j, c, tile;
-        TileGeo g;
+      int chunk_ctr = 0, tile_ctr = 0;
+      auto issue_pv = [&](int c, bool first, bool last) {
+        const int vs = c % NA_VSLOTS, pb = c & 1;
+        mbar_wait(bar_pfull, c & 1);
+        mbar_wait(bar_vfull(vs), (c / NA_VSLOTS) & 1);
+        if (first) mbar_wait(bar_oempty, (tile_ctr & 1) ^ 1);
+        tc_fence_after();
+        // O += P V: A = P from TMEM (fp16 pairs, 8 columns per 16 keys), B = V MN-major from its TMA tile
+        for (int s = 0; s < (p.dbg >= 2 ? 0 : 8); ++s) {
+          const uint64_t bd = make_sdesc_sw128(sV(vs) + s * 2048u, 16384, 1024);
+          umma_f16_ts(tO, tmem + NA_TMEM_P + 64 * pb + 8 * s, bd, idesc_o, (!first || s > 0) ? 1u : 0u);
+        }
+        umma_commit(bar_vempty(vs));
+        umma_commit(bar_pempty(pb));
+        if (last) umma_commit(bar_ofull);
       };
-      Cursor cs{static_cast<int>(blockIdx.x), 0, 0, 0, TileGeo{}}, cp = cs;
-      if (cs.item < p.nitems) cs.g = cp.g = tile_geo(p, cs.item);
-      auto advance = [&](Cursor& u) {
-        ++u.c;
-        if (++u.j == u.g.nchunks) {
-          u.j = 0;
-          ++u.tile;
-          u.item += gridDim.x;
-          if (u.item < p.nitems) u.g = tile_geo(p, u.item);
-        }
-      };
-      long long t_idle = clock64();
-      while (cp.item < p.nitems) {
-        bool progressed = false;
-        // ---- next S ----
-        if (cs.item < p.nitems && cs.c < cp.c + 2) {
-          const int ks = cs.c % NA_KSLOTS, ss = cs.c & 1;
-          const bool ready = (cs.j != 0 || mbar_test(bar_qfull, cs.tile & 1)) &&
-                             mbar_test(bar_kfull(ks), (cs.c / NA_KSLOTS) & 1) &&
-                             mbar_test(bar_sempty(ss), ((cs.c >> 1) & 1) ^ 1);
-          if (ready) {
-            NA_STAMP(cs.c, 0);
-            tc_fence_after();
-            const uint32_t tS = tmem + 128 * ss;
-            for (int s = 0; s < (p.dbg >= 2 ? 0 : kb * 4); ++s) {
-              const uint32_t off = (s >> 2) * 16384u + (s & 3) * 32u;
-              umma_bf16_ss(tS, make_sdesc_sw128(sQ + off, 16, 1024), make_sdesc_sw128(sK(ks) + off, 16, 1024),
-                           idesc_s, s > 0 ? 1u : 0u);
-            }
-            umma_commit(bar_sfull(ss));
-            umma_commit(bar_kempty(ks));
-            if (cs.j == cs.g.nchunks - 1) umma_commit(bar_qempty);
-            NA_STAMP(cs.c, 1);
-            advance(cs);
-            progressed = true;
+      for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
+        const TileGeo g = tile_geo(p, item);
+        mbar_wait(bar_qfull, tile_ctr & 1);
+        for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
+          const int ks = chunk_ctr % NA_KSLOTS, ss = chunk_ctr & 1;
+          mbar_wait(bar_kfull(ks), (chunk_ctr / NA_KSLOTS) & 1);
+          mbar_wait(bar_sempty(ss), ((chunk_ctr >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t tS = tmem + 128 * ss;
+          for (int s = 0; s < (p.dbg >= 2 ? 0 : kb * 4); ++s) {
+            const uint32_t off = (s >> 2) * 16384u + (s & 3) * 32u;
+            umma_bf16_ss(tS, make_sdesc_sw128(sQ + off, 16, 1024), make_sdesc_sw128(sK(ks) + off, 16, 1024),
+                         idesc_s, s > 0 ? 1u : 0u);
           }
+          umma_commit(bar_sfull(ss));
+          umma_commit(bar_kempty(ks));
+          if (j == g.nchunks - 1) umma_commit(bar_qempty);
+          if (j > 0) issue_pv(chunk_ctr - 1, j - 1 == 0, false);
         }
-        // ---- next PV ----
-        if (cp.c < cs.c) {
-          const int vs = cp.c % NA_VSLOTS, pb = cp.c & 1;
-          const bool first = cp.j == 0, last = cp.j == cp.g.nchunks - 1;
-          const bool ready = mbar_test(bar_pfull, cp.c & 1) && mbar_test(bar_vfull(vs), (cp.c / NA_VSLOTS) & 1) &&
-                             (!first || mbar_test(bar_oempty, (cp.tile & 1) ^ 1));
-          if (ready) {
-            NA_STAMP(cp.c, 2);
-            tc_fence_after();
-            // O += P V: A = P from TMEM (fp16 pairs, 8 columns per 16 keys), B = V MN-major from its TMA tile
-            for (int s = 0; s < (p.dbg >= 2 ? 0 : 8); ++s) {
-              const uint64_t bd = make_sdesc_sw128(sV(vs) + s * 2048u, 16384, 1024);
-              umma_f16_ts(tO, tmem + NA_TMEM_P + 64 * pb + 8 * s, bd, idesc_o, (!first || s > 0) ? 1u : 0u);
-            }
-            umma_commit(bar_vempty(vs));
-            umma_commit(bar_pempty(pb));
-            if (last) umma_commit(bar_ofull);
-            NA_STAMP(cp.c, 3);
-            advance(cp);
-            progressed = true;
-          }
-        }
-        if (progressed) {
-          t_idle = clock64();
-        } else if (clock64() - t_idle > 20000000000LL) {
-          __trap();  // a pipeline bug must not hang the GPU
-        }
+        issue_pv(chunk_ctr - 1, g.nchunks == 1, true);
       }
     }
   } else if (warp < NA_SOFTMAX_WARPS) {
     // =============================== softmax / epilogue ===============================
-    // Warp w owns query rows 32 (w % 4) .. +32 (its TMEM lane quarter) and part p = w / 4 of the key columns
-    // ([32 p, 32 p + 32): S columns, P columns) and of the O columns ([32 p, 32 p + 32) when < dhp).  The
-    // NA_PARTS warps of a quarter (4 per SM sub-partition, for latency hiding) combine row maxima and sums
-    // through shared memory (named barrier 1 + quarter).
-    const int quarter = warp & 3, part = warp >> 2;
+    // Warp w owns query rows 32 (w % 4) .. +32 (its TMEM lane quarter) and half h = w / 4 of the key
+    // columns (P columns) and of the O columns; the two warps of a quarter combine row maxima and sums
+    // through shared memory (named barrier 1 + quarter, 64 threads).
+    const int quarter = warp & 3, half = warp >> 2;
     const int row = 32 * quarter + lane;  // query row in the tile
-    const int nbar = 32 * NA_PARTS;
-    float* red = reinterpret_cast<float*>(smem + NA_SMEM_BODY + 256);  // [parity][part][128]
+    float* red = reinterpret_cast<float*>(smem + NA_SMEM_BODY + 256);  // [parity][half][128]
     const uint32_t lane_off = static_cast<uint32_t>(32 * quarter) << 16;
     const uint32_t tO = tmem + NA_TMEM_O;
-    const bool owns_o = 32 * part < p.dhp;  // O columns [32 part, 32 part + 32)
+    const int ocols = p.dhp / 2;  // O columns handled by this warp
     const int hw = (p.ww - 1) / 2;
     int chunk_ctr = 0, tile_ctr = 0;
     for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
@@ -330,107 +283,114 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
         const int ss = chunk_ctr & 1, pb = chunk_ctr & 1;
         int kd, kr0, nr, origin, vlo, vhi;
         chunk_geo(g, p.cols, j, kd, kr0, nr, origin, vlo, vhi);
-        if (warp == 0 && lane == 0) NA_STAMP(chunk_ctr, 4);
-        // ---- validity bits of this warp's 32 key columns [32 part, 32 part + 32) ----
-        uint32_t mk = 0;
+        // ---- validity bits of this warp's 64 key columns [64 half, 64 half + 64) ----
+        uint64_t mk = 0;
         if (qvalid && kd >= q_sd && kd < q_sd + p.wd) {
           const int rlo = max(0, q_sh - kr0), rhi = min(nr, q_sh + p.wh - kr0);
           const int s1lo = max(c_lo, vlo), s1hi = min(c_lo + p.ww, vhi);
           const int s2hi = circle ? c_lo + p.ww - g.ncp : 0;
-          const int off = 32 * part;
+          const int off = 64 * half;
           for (int rr = rlo; rr < rhi; ++rr) {
             const int base = rr * g.ncp - off;
-            mk |= static_cast<uint32_t>(bits64(base + s1lo, base + s1hi));
-            if (s2hi > 0) mk |= static_cast<uint32_t>(bits64(base, base + s2hi));
+            mk |= bits64(base + s1lo, base + s1hi);
+            if (s2hi > 0) mk |= bits64(base, base + s2hi);
           }
         }
-        // ---- S columns -> registers ----
+        // ---- S half -> registers ----
         mbar_wait(bar_sfull(ss), (chunk_ctr >> 1) & 1);
-        if (warp == 0 && lane == 0) NA_STAMP(chunk_ctr, 5);
         tc_fence_after();
-        uint32_t s[32];
-        tmem_ld32(tmem + 128 * ss + lane_off + 32 * part, s);
+        uint32_t s[64];
+        tmem_ld32(tmem + 128 * ss + lane_off + 64 * half, *reinterpret_cast<uint32_t(*)[32]>(s));
+        tmem_ld32(tmem + 128 * ss + lane_off + 64 * half + 32, *reinterpret_cast<uint32_t(*)[32]>(s + 32));
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_sempty(ss));
-        uint32_t pk[16];
+        uint32_t pk[32];
         float alpha = 1.f, lsum = 0.f;
         if (p.dbg) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) pk[i] = 0u;
+          for (int i = 0; i < 32; ++i) pk[i] = 0u;
         } else {
-          // ---- masked row max (raw scores), combined across the quarter's warps ----
-          float mxa[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+          // ---- masked row max (raw scores), combined with the partner warp ----
+          // 8 independent accumulators: a serial 64-long FMNMX / FADD chain would be latency-bound.
+          const uint32_t mlo = static_cast<uint32_t>(mk), mhi = static_cast<uint32_t>(mk >> 32);
+          float mxa[8];
 #pragma unroll
-          for (int k = 0; k < 32; ++k)
-            mxa[k & 3] = ((mk >> k) & 1u) ? fmaxf(mxa[k & 3], __uint_as_float(s[k])) : mxa[k & 3];
-          float mx = fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3]));
-          float* rbuf = red + (chunk_ctr & 1) * (NA_PARTS * 128);  // parity: a partner may still read the last
-          rbuf[part * 128 + row] = mx;
-          named_bar_sync(1 + quarter, nbar);
+          for (int i = 0; i < 8; ++i) mxa[i] = -INFINITY;
 #pragma unroll
-          for (int q = 0; q < NA_PARTS; ++q) mx = fmaxf(mx, rbuf[q * 128 + row]);
+          for (int k = 0; k < 64; ++k) {
+            const bool ok = ((k < 32 ? mlo : mhi) >> (k & 31)) & 1u;
+            mxa[k & 7] = ok ? fmaxf(mxa[k & 7], __uint_as_float(s[k])) : mxa[k & 7];
+          }
+          float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                           fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
+          float* rbuf = red + (chunk_ctr & 1) * 256;  // parity buffers: the partner may still read the last one
+          rbuf[half * 128 + row] = mx;
+          named_bar_sync(1 + quarter, 64);
+          mx = fmaxf(mx, rbuf[(half ^ 1) * 128 + row]);
           mx = mx * p.scale_log2;
-          if (mx > m_run + NA_RESCALE_LOG2) {  // lazy rescale (also covers m_run = -inf); same in all parts
+          if (mx > m_run + NA_RESCALE_LOG2) {  // lazy rescale (also covers m_run = -inf); same in both warps
             alpha = exp2f(m_run - mx);
             m_run = mx;
           }
           const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-          float lsa[4] = {0.f, 0.f, 0.f, 0.f};
+          float lsa[8];
 #pragma unroll
-          for (int k = 0; k < 32; k += 2) {
+          for (int i = 0; i < 8; ++i) lsa[i] = 0.f;
+#pragma unroll
+          for (int k = 0; k < 64; k += 2) {
             float p0 = fast_exp2(fmaf(__uint_as_float(s[k]), p.scale_log2, -m_use));
             float p1 = fast_exp2(fmaf(__uint_as_float(s[k + 1]), p.scale_log2, -m_use));
-            p0 = ((mk >> k) & 1u) ? p0 : 0.f;
-            p1 = ((mk >> (k + 1)) & 1u) ? p1 : 0.f;
-            lsa[(k >> 1) & 3] += p0 + p1;
+            p0 = (((k < 32 ? mlo : mhi) >> (k & 31)) & 1u) ? p0 : 0.f;
+            p1 = (((k + 1 < 32 ? mlo : mhi) >> ((k + 1) & 31)) & 1u) ? p1 : 0.f;
+            lsa[(k >> 1) & 7] += p0 + p1;
             pk[k >> 1] = pack_elem(p0, p1);
           }
-          lsum = (lsa[0] + lsa[1]) + (lsa[2] + lsa[3]);
+          lsum = ((lsa[0] + lsa[1]) + (lsa[2] + lsa[3])) + ((lsa[4] + lsa[5]) + (lsa[6] + lsa[7]));
         }
-        if (warp == 0 && lane == 0) NA_STAMP(chunk_ctr, 6);
         l_run = l_run * alpha + lsum;  // this warp's share of the row sum
         // ---- P buffer pb free once P V of chunk c-2 retired; a rescale also needs P V of chunk c-1 ----
         mbar_wait(bar_pempty(pb), ((chunk_ctr >> 1) & 1) ^ 1);
-        if (warp == 0 && lane == 0) NA_STAMP(chunk_ctr, 7);
-        if (j > 0 && owns_o && __any_sync(0xffffffffu, alpha != 1.f)) {
+        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
           mbar_wait(bar_pempty(pb ^ 1), ((chunk_ctr - 1) >> 1) & 1);
           tc_fence_after();
-          uint32_t r[32];
-          const uint32_t ta = tO + lane_off + 32 * part;
-          tmem_ld32(ta, r);
-          tmem_ld_wait();
+#pragma unroll 1
+          for (int c = 0; c < ocols / 32; ++c) {
+            uint32_t r[32];
+            const uint32_t ta = tO + lane_off + half * ocols + 32 * c;
+            tmem_ld32(ta, r);
+            tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-          tmem_st32(ta, r);
+            for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+            tmem_st32(ta, r);
+          }
         }
         tc_fence_after();
-        tmem_st16(tmem + NA_TMEM_P + 64 * pb + 16 * part + lane_off, pk);  // keys [32 part, +32) of my row
+        tmem_st32(tmem + NA_TMEM_P + 64 * pb + 32 * half + lane_off, pk);  // keys [64 half, +64) of my row
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_pfull);
-        if (warp == 0 && lane == 0) NA_STAMP(chunk_ctr, 8);
       }
-      // ---- epilogue: O / l -> ctx (row sum over all parts) ----
-      float* rl = red + (chunk_ctr & 1) * (NA_PARTS * 128);  // the parity no warp of this quarter still reads
-      rl[part * 128 + row] = l_run;
-      named_bar_sync(1 + quarter, nbar);
-      float l_tot = 0.f;
-#pragma unroll
-      for (int q = 0; q < NA_PARTS; ++q) l_tot += rl[q * 128 + row];
+      // ---- epilogue: O / l -> ctx (row sum = both halves) ----
+      float* rl = red + ((chunk_ctr) & 1) * 256;  // the parity buffer no warp of this quarter still reads
+      rl[half * 128 + row] = l_run;
+      named_bar_sync(1 + quarter, 64);
+      const float l_tot = l_run + rl[(half ^ 1) * 128 + row];
       mbar_wait(bar_ofull, tile_ctr & 1);
       tc_fence_after();
-      if (owns_o) {
-        const float inv_l = (qvalid && l_tot > 0.f) ? 1.f / l_tot : 0.f;
+      const float inv_l = (qvalid && l_tot > 0.f) ? 1.f / l_tot : 0.f;
+      elem_t* orow = p.out + (qvalid ? (static_cast<size_t>((qd * p.rows + qh) * p.cols + qw) * p.ldo +
+                                        g.head * p.dhp + half * ocols)
+                                     : 0);
+#pragma unroll 1
+      for (int c = 0; c < ocols / 32; ++c) {
         uint32_t r[32];
-        tmem_ld32(tO + lane_off + 32 * part, r);
+        tmem_ld32(tO + lane_off + half * ocols + 32 * c, r);
         tmem_ld_wait();
         if (qvalid) {
-          elem_t* orow =
-              p.out + static_cast<size_t>((qd * p.rows + qh) * p.cols + qw) * p.ldo + g.head * p.dhp + 32 * part;
-          uint4* d4 = reinterpret_cast<uint4*>(orow);
+          uint4* d4 = reinterpret_cast<uint4*>(orow + 32 * c);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             uint4 u;
@@ -443,7 +403,7 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
         }
       }
       tc_fence_before();
-      named_bar_sync(1 + quarter, nbar);  // every part has read rl[] before the next tile reuses this parity
+      named_bar_sync(1 + quarter, 64);  // partner has read rl[] before the next tile writes this parity again
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_oempty);
     }
@@ -543,23 +503,7 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
     attr = true;
   }
   const int grid = p.nitems < sm_count() ? p.nitems : sm_count();
-  const char* tr = getenv("WM3_NA_TRACE");
-  if (tr && atoi(tr)) cudaMalloc(&p.trace, sizeof(long long) * NA_TRACE_CHUNKS * NA_TRACE_EV);
-  if (p.trace) cudaMemset(p.trace, 0, sizeof(long long) * NA_TRACE_CHUNKS * NA_TRACE_EV);
   natten_fwd_kernel<<<grid, NA_THREADS, NA_SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(tq, tkv, p);
-  if (p.trace) {
-    long long h[NA_TRACE_CHUNKS * NA_TRACE_EV];
-    cudaDeviceSynchronize();
-    cudaMemcpy(h, p.trace, sizeof(h), cudaMemcpyDeviceToHost);
-    cudaFree(p.trace);
-    const long long t0 = h[0];
-    fprintf(stderr, "chunk  kfull  S_iss  pfull  PV_iss | sm_start S_rdy exp_done pempty pfull_arr\n");
-    for (int c = 0; c < NA_TRACE_CHUNKS; ++c) {
-      const long long* e = h + c * NA_TRACE_EV;
-      fprintf(stderr, "%4d %7lld %6lld %6lld %6lld | %7lld %6lld %6lld %6lld %6lld\n", c, e[0] - t0, e[1] - t0,
-              e[2] - t0, e[3] - t0, e[4] - t0, e[5] - t0, e[6] - t0, e[7] - t0, e[8] - t0);
-    }
-  }
   return check_launch("natten_fwd_kernel");
 }
 
