@@ -67,7 +67,10 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms while the GPU is under the benchmark load.
+
+    __enter__ returns only once the first sample has been written, so the timed region that follows is
+    covered; the sampler spans the timed block steps, the per-kernel breakdown and the e2e steps."""
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
@@ -83,7 +86,10 @@ class ClockSampler:
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+                 "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.fh, stderr=subprocess.DEVNULL)
+            t0 = time.time()
+            while time.time() - t0 < 5.0 and os.path.getsize(self.path) == 0:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
         return self
@@ -323,8 +329,8 @@ def run_gpu(args, world, rank, local_rank):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
-        ms = timed(step, args.steps, stream, world)
+    clk = ClockSampler(local_rank).__enter__()
+    ms = timed(step, args.steps, stream, world)
     flops = block_flops(int(np.prod(EXT)))
     value = flops * args.steps / (ms / 1e3) / 1e12
 
@@ -346,6 +352,7 @@ def run_gpu(args, world, rank, local_rank):
     e_steps = max(3, min(args.steps, 10))
     e_ms = timed(e2e_step, e_steps, stream, world)
     e2e_value = flops * e_steps / (e_ms / 1e3) / 1e12
+    clk.__exit__(None, None, None)
 
     fc = None
     if world == 1 and not args.no_forecast:

@@ -73,14 +73,15 @@ int wm3_linear_planes(const void* a, int lda, const void* b, int ldb, int m, int
                       void* out, int ldo, int n_valid, const float* bias, const wm3_rope_t* rope,
                       int planes, int plane_rows, long long plane_stride, int row_off, void* stream);
 
-/* Fused 3D neighborhood attention forward.
- * qkv: bf16 K/V grid [depth][rows_ext][cols][ldqkv], token channels [3][heads][dhp]; rows_ext =
+/* Fused 3D neighborhood attention forward, over `batch` independent latents (ensemble members).
+ * qkv: bf16 K/V grid [batch * depth][rows_ext][cols][ldqkv] (member b owns depth planes [b * depth, (b + 1) * depth);
+ *      windows never cross members), token channels [3][heads][dhp]; rows_ext =
  *      halo_lo + rows + halo_hi: the local band rows [row0, row0 + rows) of a grid with global row extent
  *      rows_global, plus halo rows received from the neighbouring bands.  Longitude wrap is handled inside
  *      the kernel (a wrapping key patch is fetched as two TMA boxes).
- * out: bf16 [depth * rows * cols][ldo] (local token order), channels [heads][dhp].
+ * out: bf16 [batch * depth * rows * cols][ldo] (member-major, local token order), channels [heads][dhp].
  * scale = 1/sqrt(dh). */
-int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, int depth, int rows, int cols,
+int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, int batch, int depth, int rows, int cols,
                    int rows_global, int row0, int halo_lo, int halo_hi, int heads, int dhp, int wd,
                    int wh, int ww, float scale, void* stream);
 

@@ -42,7 +42,7 @@ SIGNATURES = {
     "wm3_linear": [_vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, ctypes.POINTER(RopeT), _vp],
     "wm3_linear_planes": [_vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, ctypes.POINTER(RopeT),
                           _i, _i, ctypes.c_longlong, _i, _vp],
-    "wm3_natten_fwd": [_vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _f, _vp],
+    "wm3_natten_fwd": [_vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _f, _vp],
     "wm3_natten_windows": [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp],
     "wm3_conv_bn": [_i],
     "wm3_mma_probe": [_i, _i, _i, _i, _vp, _vp],

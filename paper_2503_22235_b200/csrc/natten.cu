@@ -1,22 +1,27 @@
 // K1: fused 3D neighborhood attention forward on tcgen05 (reference attention.py:173-178,
 // window arithmetic grid.py:96-130).
 //
-// Work item = (query tile, head).  A query tile is a TD x TH x TW box of tokens (<= 128 queries, one per
-// TMEM lane).  The union of the tile's windows is walked as a list of key chunks, each a run of rows of
+// Work item = (query tile, head, member).  A query tile is a TD x TH x TW box of tokens (<= 128 queries, one
+// per TMEM lane).  The union of the tile's windows is walked as a list of key chunks, each a run of rows of
 // one depth plane x a contiguous (mod W) run of columns, <= 128 keys.
 //
-// Persistent, warp-specialised CTA (one per SM, 320 threads):
-//   warp 9      TMA producer (one thread): the Q tile (4D box TD x TH x TW) and each chunk's K and V head
-//               slices (4D box ncp x nrpc) into SWIZZLE_128B tiles: 3 K slots (freed by Q K^T), 2 V slots
-//               (freed by P V), K issued one chunk ahead of V; completion via mbarrier transaction counts
-//   warp 8      MMA issuer (one thread): S = Q K^T into one of two TMEM S buffers (M128 N128 K=dhp, both
-//               operands from smem), O += P V with P read from TMEM (M128 N=dhp K=128, V MN-major from its
-//               TMA tile), O accumulated in TMEM across chunks; S_{j+1} is issued before PV_j
-//   warps 0-7   softmax (one thread per query row and key-column half, two warps per TMEM lane quarter):
-//               window bitmask built from the same integer formula as grid.py (bump on depth/rows, wrap on
-//               cols), fp32 running max / sum with lazy O rescaling (only when the max grows by > 2^8),
-//               exp2, P (fp16) -> TMEM (double-buffered); finally O / l -> ctx rows.
+// Two persistent CTAs per SM (192 threads, 256 TMEM columns and ~100 KB smem each).  Inside a CTA the
+// chunk loop is a strict chain S(c) -> softmax(c) -> P V(c) -> S(c + 1); the second CTA on the SM fills
+// the tensor core while the first one is in softmax (and vice versa), which hides the handshake latencies
+// that a single deeper-pipelined CTA exposes.
+//   warp 5      TMA producer (one thread): the Q tile (4D box TD x TH x TW) and each chunk's K and V head
+//               slices (4D box ncp x nrpc) into SWIZZLE_128B tiles; K(c + 1) streams in while softmax(c)
+//               runs, V(c + 1) while S(c + 1) and softmax(c + 1) run
+//   warp 4      MMA issuer (one thread): S = Q K^T into TMEM columns [0, 128) (M128 N128 K=dhp, both operands
+//               from smem), then O += P V with P (fp16 pairs) read from TMEM columns [0, 64) where softmax
+//               wrote it over S (M128 N=dhp K=128, V MN-major from its TMA tile), O in columns [128, 256)
+//   warps 0-3   softmax (one thread per query row, all 128 key columns of the chunk): window bitmask built
+//               from the same integer formula as grid.py (bump on depth/rows, wrap on cols), fp32 running
+//               max / sum with lazy O rescaling (only when the max grows by > 2^8), exp2, P -> TMEM; at the
+//               end of a tile O / l -> ctx rows.
 // The logits never leave the SM.  Output ctx rows are bf16 [T][heads][dhp] = the O-proj GEMM operand.
+#include <cstdio>
+
 #include "common.cuh"
 #include "launch.h"
 #include "window.cuh"
@@ -27,31 +32,32 @@ namespace wm3 {
 struct NaParams {
   elem_t* out;
   int ldo;
+  int batch;  // ensemble members: the K/V grid holds batch * depth planes, member b at planes [b * depth, ...)
   int depth, rows, cols, rows_global, row0, halo_lo, rows_ext;
   int heads, dhp, wd, wh, ww;
   int TD, TH, TW, ntd, nth, ntw, nitems;
   int ncp, nrpc;  // key-chunk box: ncp columns x nrpc rows (fixed for every tile)
   float scale_log2;
-  int dbg;  // profiling switch (WM3_NA_DEBUG): 1 = skip the softmax arithmetic, 2 = also skip the MMAs
+  long long* trace;  // WM3_NA_TRACE: per-chunk clock64 stamps of CTA 0 (profiling only)
+  int dbg;  // profiling switch (WM3_NA_DEBUG, bit flags): 1 skip softmax arithmetic, 2 skip Q K^T, 4 skip P V, 8 skip K/V loads
 };
 
-// warps 0-7 softmax (warp w: TMEM lanes 32 (w % 4).., key / O columns half w / 4), 8 MMA, 9 TMA producer
-constexpr int NA_SOFTMAX_WARPS = 8;
-constexpr int NA_MMA_WARP = 8;
-constexpr int NA_TMA_WARP = 9;
-constexpr int NA_THREADS = 320;
+constexpr int NA_SOFTMAX_WARPS = 4;
+constexpr int NA_MMA_WARP = 4;
+constexpr int NA_TMA_WARP = 5;
+constexpr int NA_THREADS = 192;
+constexpr int NA_CTAS_PER_SM = 2;
 constexpr uint32_t NA_TILE = 32768;  // 128 rows x 256 B
-constexpr int NA_KSLOTS = 3;         // K frees after Q K^T: three slots give the TMA two chunks of lead time
-constexpr int NA_VSLOTS = 2;         // V frees after P V
-// smem: Q | K0 K1 K2 | V0 V1 | barriers (256 B) | row-max / row-sum exchange (2 KB)
-constexpr uint32_t NA_SMEM_BODY = (1 + NA_KSLOTS + NA_VSLOTS) * NA_TILE;
-constexpr uint32_t NA_SMEM = NA_SMEM_BODY + 1024 /*align*/ + 256 /*barriers*/ + 2048 /*exchange*/;
-// TMEM columns: S0 [0,128) S1 [128,256) O [256,384) P0 [384,448) P1 [448,512) (P: fp16 pairs per column)
-constexpr uint32_t NA_TMEM_O = 256, NA_TMEM_P = 384;
+// smem: Q | K | V | barriers (256 B)
+constexpr uint32_t NA_SMEM_BODY = 3 * NA_TILE;
+constexpr uint32_t NA_SMEM = NA_SMEM_BODY + 1024 /*align*/ + 256 /*barriers*/;
+// TMEM columns (256 per CTA): S / P [0, 128), O [128, 256).  S(c + 1) may overwrite P(c) without a wait
+// because tcgen05.mma ops of one thread execute in issue order and S(c + 1) is issued after P V(c).
+constexpr uint32_t NA_TMEM_COLS = 256, NA_TMEM_O = 128;
 constexpr float NA_RESCALE_LOG2 = 8.0f;
 
 struct TileGeo {
-  int head, d0, d1, h0, h1, w0, w1;
+  int head, b, d0, d1, h0, h1, w0, w1;
   int kd_lo, kr_lo, kr_hi, pc0, ncp, nrpc, nrchunks, nparts, nchunks;
 };
 
@@ -63,8 +69,10 @@ struct TileGeo {
 DEVI TileGeo tile_geo(const NaParams& p, int item) {
   TileGeo g;
   const int ntiles = p.ntd * p.nth * p.ntw;
-  g.head = item / ntiles;
-  const int tile = item - g.head * ntiles;
+  const int hb = item / ntiles;  // head-major, member-minor: concurrent CTAs share a head's K/V in L2
+  g.head = hb / p.batch;
+  g.b = hb - g.head * p.batch;
+  const int tile = item - hb * ntiles;
   const int tw_i = tile % p.ntw;
   const int th_i = (tile / p.ntw) % p.nth;
   const int td_i = tile / (p.ntw * p.nth);
@@ -116,25 +124,40 @@ DEVI uint64_t bits64(int a, int b) {
   return hi & ~((1ull << a) - 1ull);
 }
 
-__global__ void __launch_bounds__(NA_THREADS, 1)
+// m |= bits [a, b) of a 128-bit mask held as 4 words (a, b may lie outside [0, 128)); branch-free
+DEVI void set_bits128(uint32_t (&m)[4], int a, int b) {
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const int lo = min(max(a - 32 * w, 0), 32), hi = min(max(b - 32 * w, 0), 32);
+    m[w] |= __funnelshift_lc(0u, 0xffffffffu, lo) & ~__funnelshift_lc(0u, 0xffffffffu, hi);
+  }
+}
+
+// Window bits of one query over a chunk box of nr x ncp keys (key k = rr * ncp + cc): rows [rlo, rhi),
+// columns [s1lo, s1hi) plus the wrapped run [0, s2hi) of a full-circle patch.  nr is warp-uniform.
+DEVI void window_mask(uint32_t (&m)[4], int nr, int ncp, int rlo, int rhi, int s1lo, int s1hi, int s2hi) {
+  m[0] = m[1] = m[2] = m[3] = 0u;
+  for (int rr = 0; rr < nr; ++rr) {
+    const bool on = rr >= rlo && rr < rhi;
+    const int base = rr * ncp;
+    set_bits128(m, on ? base + s1lo : 0, on ? base + s1hi : 0);
+    set_bits128(m, base, on ? base + s2hi : base);
+  }
+}
+
+__global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
     natten_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, NaParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sQ = smem_u32(smem);
-  auto sK = [&](int s) { return sQ + NA_TILE * (1 + s); };
-  auto sV = [&](int s) { return sQ + NA_TILE * (1 + NA_KSLOTS + s); };
+  const uint32_t sQ = smem_u32(smem), sK = sQ + NA_TILE, sV = sQ + 2 * NA_TILE;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NA_SMEM_BODY);
   const uint32_t b0 = smem_u32(bars);
-  const uint32_t bar_qfull = b0 + 0, bar_qempty = b0 + 8;
-  auto bar_kfull = [&](int s) { return b0 + 16 + 8 * s; };   // 3
-  auto bar_kempty = [&](int s) { return b0 + 40 + 8 * s; };  // 3
-  auto bar_vfull = [&](int s) { return b0 + 64 + 8 * s; };   // 2
-  auto bar_vempty = [&](int s) { return b0 + 80 + 8 * s; };  // 2
-  auto bar_sfull = [&](int s) { return b0 + 96 + 8 * s; };   // 2
-  auto bar_sempty = [&](int s) { return b0 + 112 + 8 * s; }; // 2
-  auto bar_pempty = [&](int s) { return b0 + 128 + 8 * s; }; // 2
-  const uint32_t bar_pfull = b0 + 144, bar_ofull = b0 + 152, bar_oempty = b0 + 160;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
+  // Every barrier completes once per chunk (or tile) and its waiter always observes a phase before the
+  // next one can complete (each completion needs the waiter's own next step), so parity waits never alias.
+  const uint32_t bar_qfull = b0 + 0, bar_qempty = b0 + 8, bar_kfull = b0 + 16, bar_kempty = b0 + 24;
+  const uint32_t bar_vfull = b0 + 32, bar_vempty = b0 + 40, bar_sfull = b0 + 48, bar_pfull = b0 + 56;
+  const uint32_t bar_ofull = b0 + 64, bar_oempty = b0 + 72;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -143,24 +166,18 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
   if (tid == 0) {
     mbar_init(bar_qfull, 1);
     mbar_init(bar_qempty, 1);
-    for (int s = 0; s < NA_KSLOTS; ++s) {
-      mbar_init(bar_kfull(s), 1);
-      mbar_init(bar_kempty(s), 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(bar_vfull(s), 1);
-      mbar_init(bar_vempty(s), 1);
-      mbar_init(bar_sfull(s), 1);
-      mbar_init(bar_sempty(s), NA_SOFTMAX_WARPS);
-      mbar_init(bar_pempty(s), 1);
-    }
+    mbar_init(bar_kfull, 1);
+    mbar_init(bar_kempty, 1);
+    mbar_init(bar_vfull, 1);
+    mbar_init(bar_vempty, 1);
+    mbar_init(bar_sfull, 1);
     mbar_init(bar_pfull, NA_SOFTMAX_WARPS);
     mbar_init(bar_ofull, 1);
     mbar_init(bar_oempty, NA_SOFTMAX_WARPS);
     fence_barrier_init();
   }
   if (warp == NA_MMA_WARP) {
-    tmem_alloc(smem_u32(tmem_slot), 512);
+    tmem_alloc(smem_u32(tmem_slot), NA_TMEM_COLS);
     tmem_relinquish();
   }
   // Zero the operand tiles once: rows past a box are never written by TMA and V rows feed P V (0 * NaN).
@@ -175,7 +192,6 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
 
   if (warp == NA_TMA_WARP) {
     // =============================== TMA producer ===============================
-    // K runs one chunk ahead of V (K slots free after Q K^T, V slots only after P V).
     if (lane == 0) {
       tma_prefetch(&tmQ);
       tma_prefetch(&tmKV);
@@ -184,29 +200,33 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
       const uint32_t kbytes = halves * 128u * p.ncp * p.nrpc;
       int chunk_ctr = 0, tile_ctr = 0;
       auto load_kv = [&](const TileGeo& g, int j, int c, bool is_v) {
-        const int slot = is_v ? (c % NA_VSLOTS) : (c % NA_KSLOTS);
-        const int use = is_v ? (c / NA_VSLOTS) : (c / NA_KSLOTS);
         int kd, kr0, nr, origin, vlo, vhi;
         chunk_geo(g, p.cols, j, kd, kr0, nr, origin, vlo, vhi);
-        const uint32_t full = is_v ? bar_vfull(slot) : bar_kfull(slot);
-        mbar_wait(is_v ? bar_vempty(slot) : bar_kempty(slot), (use & 1) ^ 1);
+        const uint32_t full = is_v ? bar_vfull : bar_kfull;
+        mbar_wait(is_v ? bar_vempty : bar_kempty, (c & 1) ^ 1);
+        if (p.dbg & 8) {
+          mbar_arrive(full);
+          return;
+        }
+        if (!is_v && p.trace && blockIdx.x == 0 && c < 256) p.trace[8 * c + 7] = clock64();
         mbar_arrive_expect_tx(full, kbytes);
         const int c1 = origin, c2 = kr0 - brow0;  // may be negative / past the edge: TMA zero-fills
-        const uint32_t dst = is_v ? sV(slot) : sK(slot);
+        const uint32_t dst = is_v ? sV : sK;
         const int col = (is_v ? 2 : 1) * sec + g.head * p.dhp;
-        for (int h = 0; h < halves; ++h) tma_load_4d(dst + h * 16384u, &tmKV, full, col + 64 * h, c1, c2, kd);
+        for (int h = 0; h < halves; ++h)
+          tma_load_4d(dst + h * 16384u, &tmKV, full, col + 64 * h, c1, c2, g.b * p.depth + kd);
       };
       for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
         const TileGeo g = tile_geo(p, item);
         mbar_wait(bar_qempty, (tile_ctr & 1) ^ 1);
         mbar_arrive_expect_tx(bar_qfull, qbytes);
         for (int h = 0; h < halves; ++h)
-          tma_load_4d(sQ + h * 16384u, &tmQ, bar_qfull, g.head * p.dhp + 64 * h, g.w0, g.h0 + p.halo_lo, g.d0);
+          tma_load_4d(sQ + h * 16384u, &tmQ, bar_qfull, g.head * p.dhp + 64 * h, g.w0, g.h0 + p.halo_lo,
+                      g.b * p.depth + g.d0);
         for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
-          load_kv(g, j, chunk_ctr, false);
-          if (j > 0) load_kv(g, j - 1, chunk_ctr - 1, true);
+          load_kv(g, j, chunk_ctr, false);  // K frees after S(c - 1): streams in during softmax(c - 1)
+          load_kv(g, j, chunk_ctr, true);   // V frees after P V(c - 1)
         }
-        load_kv(g, g.nchunks - 1, chunk_ctr - 1, true);
       }
     }
   } else if (warp == NA_MMA_WARP) {
@@ -215,59 +235,53 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
       const uint32_t idesc_s = make_idesc(128, 128, 0, 0);
       const uint32_t idesc_o = make_idesc(128, p.dhp, 0, 1);
       const int kb = p.dhp / 64;
-      const uint32_t tO = tmem + NA_TMEM_O;
+      const uint32_t tS = tmem, tO = tmem + NA_TMEM_O;
       int chunk_ctr = 0, tile_ctr = 0;
-      auto issue_pv = [&](int c, bool first, bool last) {
-        const int vs = c % NA_VSLOTS, pb = c & 1;
-        mbar_wait(bar_pfull, c & 1);
-        mbar_wait(bar_vfull(vs), (c / NA_VSLOTS) & 1);
-        if (first) mbar_wait(bar_oempty, (tile_ctr & 1) ^ 1);
-        tc_fence_after();
-        // O += P V: A = P from TMEM (fp16 pairs, 8 columns per 16 keys), B = V MN-major from its TMA tile
-        for (int s = 0; s < (p.dbg >= 2 ? 0 : 8); ++s) {
-          const uint64_t bd = make_sdesc_sw128(sV(vs) + s * 2048u, 16384, 1024);
-          umma_f16_ts(tO, tmem + NA_TMEM_P + 64 * pb + 8 * s, bd, idesc_o, (!first || s > 0) ? 1u : 0u);
-        }
-        umma_commit(bar_vempty(vs));
-        umma_commit(bar_pempty(pb));
-        if (last) umma_commit(bar_ofull);
-      };
       for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
         const TileGeo g = tile_geo(p, item);
         mbar_wait(bar_qfull, tile_ctr & 1);
         for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
-          const int ks = chunk_ctr % NA_KSLOTS, ss = chunk_ctr & 1;
-          mbar_wait(bar_kfull(ks), (chunk_ctr / NA_KSLOTS) & 1);
-          mbar_wait(bar_sempty(ss), ((chunk_ctr >> 1) & 1) ^ 1);
+          const uint32_t ph = chunk_ctr & 1;
+          long long* tr = (p.trace && blockIdx.x == 0 && chunk_ctr < 256) ? p.trace + 8 * chunk_ctr : nullptr;
+          mbar_wait(bar_kfull, ph);
+          if (tr) tr[0] = clock64();
           tc_fence_after();
-          const uint32_t tS = tmem + 128 * ss;
-          for (int s = 0; s < (p.dbg >= 2 ? 0 : kb * 4); ++s) {
+          for (int s = 0; s < ((p.dbg & 2) ? 0 : kb * 4); ++s) {
             const uint32_t off = (s >> 2) * 16384u + (s & 3) * 32u;
-            umma_bf16_ss(tS, make_sdesc_sw128(sQ + off, 16, 1024), make_sdesc_sw128(sK(ks) + off, 16, 1024),
-                         idesc_s, s > 0 ? 1u : 0u);
+            umma_bf16_ss(tS, make_sdesc_sw128(sQ + off, 16, 1024), make_sdesc_sw128(sK + off, 16, 1024), idesc_s,
+                         s > 0 ? 1u : 0u);
           }
-          umma_commit(bar_sfull(ss));
-          umma_commit(bar_kempty(ks));
+          umma_commit(bar_sfull);
+          umma_commit(bar_kempty);
           if (j == g.nchunks - 1) umma_commit(bar_qempty);
-          if (j > 0) issue_pv(chunk_ctr - 1, j - 1 == 0, false);
+          if (tr) tr[1] = clock64();
+          // O += P V: A = P from TMEM (fp16 pairs, 8 columns per 16 keys), B = V MN-major from its TMA tile
+          mbar_wait(bar_pfull, ph);
+          if (tr) tr[2] = clock64();
+          mbar_wait(bar_vfull, ph);
+          if (j == 0) mbar_wait(bar_oempty, (tile_ctr & 1) ^ 1);
+          if (tr) tr[3] = clock64();
+          tc_fence_after();
+          for (int s = 0; s < ((p.dbg & 4) ? 0 : 8); ++s) {
+            const uint64_t bd = make_sdesc_sw128(sV + s * 2048u, 16384, 1024);
+            umma_f16_ts(tO, tS + 8 * s, bd, idesc_o, (j > 0 || s > 0) ? 1u : 0u);
+          }
+          umma_commit(bar_vempty);
+          if (j == g.nchunks - 1) umma_commit(bar_ofull);
         }
-        issue_pv(chunk_ctr - 1, g.nchunks == 1, true);
       }
     }
-  } else if (warp < NA_SOFTMAX_WARPS) {
+  } else {
     // =============================== softmax / epilogue ===============================
-    // Warp w owns query rows 32 (w % 4) .. +32 (its TMEM lane quarter) and half h = w / 4 of the key
-    // columns (P columns) and of the O columns; the two warps of a quarter combine row maxima and sums
-    // through shared memory (named barrier 1 + quarter, 64 threads).
-    const int quarter = warp & 3, half = warp >> 2;
-    const int row = 32 * quarter + lane;  // query row in the tile
-    float* red = reinterpret_cast<float*>(smem + NA_SMEM_BODY + 256);  // [parity][half][128]
-    const uint32_t lane_off = static_cast<uint32_t>(32 * quarter) << 16;
-    const uint32_t tO = tmem + NA_TMEM_O;
-    const int ocols = p.dhp / 2;  // O columns handled by this warp
+    // Thread = query row (TMEM lane) of the tile, all 128 key columns of each chunk.
+    const int row = 32 * warp + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(32 * warp) << 16;
+    const uint32_t tS = tmem + lane_off, tO = tmem + NA_TMEM_O + lane_off;
     const int hw = (p.ww - 1) / 2;
+    const size_t member_tokens = static_cast<size_t>(p.depth) * p.rows * p.cols;
     int chunk_ctr = 0, tile_ctr = 0;
     for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
+      if (p.trace && blockIdx.x == 0 && row == 0 && tile_ctr < 32) p.trace[2048 + 8 * tile_ctr + 4] = clock64();
       const TileGeo g = tile_geo(p, item);
       const int qd = g.d0 + row / (p.TH * p.TW);
       const int qh = g.h0 + (row / p.TW) % p.TH;
@@ -278,132 +292,151 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
       // window columns in patch coordinates: [c_lo, c_lo + ww), taken mod W for a full-circle patch
       const bool circle = (g.ncp == p.cols);
       const int c_lo = circle ? wrap_col((qvalid ? qw : g.w0) - hw, p.cols) : (qvalid ? qw : g.w0) - hw - g.pc0;
+      const int s2hi = circle ? c_lo + p.ww - g.ncp : 0;
+      if (p.trace && blockIdx.x == 0 && row == 0 && tile_ctr < 32) p.trace[2048 + 8 * tile_ctr + 3] = clock64();
       float m_run = -INFINITY, l_run = 0.f;
+      // window masks depend on (row chunk, part) only, not on the depth plane: cache one per part
+      int key0 = -1, key1 = -1;
+      uint32_t mc0[4], mc1[4];
       for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
-        const int ss = chunk_ctr & 1, pb = chunk_ctr & 1;
         int kd, kr0, nr, origin, vlo, vhi;
         chunk_geo(g, p.cols, j, kd, kr0, nr, origin, vlo, vhi);
-        // ---- validity bits of this warp's 64 key columns [64 half, 64 half + 64) ----
-        uint64_t mk = 0;
-        if (qvalid && kd >= q_sd && kd < q_sd + p.wd) {
-          const int rlo = max(0, q_sh - kr0), rhi = min(nr, q_sh + p.wh - kr0);
-          const int s1lo = max(c_lo, vlo), s1hi = min(c_lo + p.ww, vhi);
-          const int s2hi = circle ? c_lo + p.ww - g.ncp : 0;
-          const int off = 64 * half;
-          for (int rr = rlo; rr < rhi; ++rr) {
-            const int base = rr * g.ncp - off;
-            mk |= bits64(base + s1lo, base + s1hi);
-            if (s2hi > 0) mk |= bits64(base, base + s2hi);
-          }
+        const int part = j % g.nparts, key = (j / g.nparts) % g.nrchunks;
+        if (part == 0 && key != key0) {
+          window_mask(mc0, nr, g.ncp, max(0, q_sh - kr0), min(nr, q_sh + p.wh - kr0), max(c_lo, vlo),
+                      min(c_lo + p.ww, vhi), s2hi);
+          key0 = key;
+        } else if (part == 1 && key != key1) {
+          window_mask(mc1, nr, g.ncp, max(0, q_sh - kr0), min(nr, q_sh + p.wh - kr0), max(c_lo, vlo),
+                      min(c_lo + p.ww, vhi), s2hi);
+          key1 = key;
         }
-        // ---- S half -> registers ----
-        mbar_wait(bar_sfull(ss), (chunk_ctr >> 1) & 1);
+        const bool dok = !(p.dbg & 16) && qvalid && kd >= q_sd && kd < q_sd + p.wd;
+        uint32_t mw[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) mw[w] = dok ? (part == 0 ? mc0[w] : mc1[w]) : 0u;
+        long long* tr = (p.trace && blockIdx.x == 0 && row == 0 && chunk_ctr < 256) ? p.trace + 8 * chunk_ctr : nullptr;
+        if (tr) tr[4] = clock64();
+        if (tr) tr[7] = clock64();  // (overwrites the producer stamp; mask time = tr[4] of this chunk - tr[7])
+        mbar_wait(bar_sfull, chunk_ctr & 1);
+        if (tr) tr[5] = clock64();
         tc_fence_after();
-        uint32_t s[64];
-        tmem_ld32(tmem + 128 * ss + lane_off + 64 * half, *reinterpret_cast<uint32_t(*)[32]>(s));
-        tmem_ld32(tmem + 128 * ss + lane_off + 64 * half + 32, *reinterpret_cast<uint32_t(*)[32]>(s + 32));
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_sempty(ss));
-        uint32_t pk[32];
-        float alpha = 1.f, lsum = 0.f;
-        if (p.dbg) {
+        // Online softmax in two 64-key halves (64 scores live): masked max, lazy max update, exp2, row sum,
+        // P of keys [64 h, 64 h + 64) -> TMEM columns [32 h, 32 h + 32) (S columns already read).  If the
+        // second half raises the max, the first half's P (fp16, <= 2^8) is rescaled in place.
+        float alpha = 1.f;
+        if (p.dbg & 1) {
+          uint32_t pk[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) pk[i] = 0u;
+          if (!(p.dbg & 32)) {
+            tmem_st32(tS, pk);
+            tmem_st32(tS + 32, pk);
+          }
         } else {
-          // ---- masked row max (raw scores), combined with the partner warp ----
-          // 8 independent accumulators: a serial 64-long FMNMX / FADD chain would be latency-bound.
-          const uint32_t mlo = static_cast<uint32_t>(mk), mhi = static_cast<uint32_t>(mk >> 32);
-          float mxa[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) mxa[i] = -INFINITY;
+          for (int h = 0; h < 2; ++h) {
+            uint32_t x[64];
+            tmem_ld32(tS + 64 * h, *reinterpret_cast<uint32_t(*)[32]>(x));
+            tmem_ld32(tS + 64 * h + 32, *reinterpret_cast<uint32_t(*)[32]>(x + 32));
+            tmem_ld_wait();
+            float mxa[8];
 #pragma unroll
-          for (int k = 0; k < 64; ++k) {
-            const bool ok = ((k < 32 ? mlo : mhi) >> (k & 31)) & 1u;
-            mxa[k & 7] = ok ? fmaxf(mxa[k & 7], __uint_as_float(s[k])) : mxa[k & 7];
+            for (int i = 0; i < 8; ++i) mxa[i] = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < 64; k += 2) {
+              const int kk = 64 * h + k;
+              const float a0 = ((mw[kk >> 5] >> (kk & 31)) & 1u) ? __uint_as_float(x[k]) : -INFINITY;
+              const float a1 = ((mw[kk >> 5] >> ((kk + 1) & 31)) & 1u) ? __uint_as_float(x[k + 1]) : -INFINITY;
+              x[k] = __float_as_uint(a0);
+              x[k + 1] = __float_as_uint(a1);
+              mxa[(k >> 1) & 7] = fmaxf(mxa[(k >> 1) & 7], fmaxf(a0, a1));
+            }
+            const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                                   fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7]))) * p.scale_log2;
+            float a_h = 1.f;
+            if (mx > m_run + NA_RESCALE_LOG2) {  // lazy rescale (also covers m_run = -inf: a_h = 0)
+              a_h = exp2f(m_run - mx);
+              m_run = mx;
+            }
+            const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+            float lsa[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) lsa[i] = 0.f;
+            uint32_t pk[32];
+#pragma unroll
+            for (int k = 0; k < 64; k += 2) {
+              const float p0 = fast_exp2(fmaf(__uint_as_float(x[k]), p.scale_log2, -m_use));  // exp2(-inf) = 0
+              const float p1 = fast_exp2(fmaf(__uint_as_float(x[k + 1]), p.scale_log2, -m_use));
+              lsa[(k >> 1) & 7] += p0 + p1;
+              pk[k >> 1] = pack_elem(p0, p1);
+            }
+            l_run = l_run * a_h + (((lsa[0] + lsa[1]) + (lsa[2] + lsa[3])) + ((lsa[4] + lsa[5]) + (lsa[6] + lsa[7])));
+            alpha *= a_h;
+            if (h == 1 && __any_sync(0xffffffffu, a_h != 1.f)) {  // rare: first half's P to the new max
+              uint32_t q0[32];
+              tmem_st_wait();
+              tmem_ld32(tS, q0);
+              tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) {
+                const float2 f = unpack_elem2(q0[e]);
+                q0[e] = pack_elem(f.x * a_h, f.y * a_h);
+              }
+              tmem_st32(tS, q0);
+            }
+            tmem_st32(tS + 32 * h, pk);
           }
-          float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
-                           fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
-          float* rbuf = red + (chunk_ctr & 1) * 256;  // parity buffers: the partner may still read the last one
-          rbuf[half * 128 + row] = mx;
-          named_bar_sync(1 + quarter, 64);
-          mx = fmaxf(mx, rbuf[(half ^ 1) * 128 + row]);
-          mx = mx * p.scale_log2;
-          if (mx > m_run + NA_RESCALE_LOG2) {  // lazy rescale (also covers m_run = -inf); same in both warps
-            alpha = exp2f(m_run - mx);
-            m_run = mx;
-          }
-          const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-          float lsa[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) lsa[i] = 0.f;
-#pragma unroll
-          for (int k = 0; k < 64; k += 2) {
-            float p0 = fast_exp2(fmaf(__uint_as_float(s[k]), p.scale_log2, -m_use));
-            float p1 = fast_exp2(fmaf(__uint_as_float(s[k + 1]), p.scale_log2, -m_use));
-            p0 = (((k < 32 ? mlo : mhi) >> (k & 31)) & 1u) ? p0 : 0.f;
-            p1 = (((k + 1 < 32 ? mlo : mhi) >> ((k + 1) & 31)) & 1u) ? p1 : 0.f;
-            lsa[(k >> 1) & 7] += p0 + p1;
-            pk[k >> 1] = pack_elem(p0, p1);
-          }
-          lsum = ((lsa[0] + lsa[1]) + (lsa[2] + lsa[3])) + ((lsa[4] + lsa[5]) + (lsa[6] + lsa[7]));
         }
-        l_run = l_run * alpha + lsum;  // this warp's share of the row sum
-        // ---- P buffer pb free once P V of chunk c-2 retired; a rescale also needs P V of chunk c-1 ----
-        mbar_wait(bar_pempty(pb), ((chunk_ctr >> 1) & 1) ^ 1);
+        // ---- rescale O: P V(c - 1) has retired (S(c) was issued after it and has completed) ----
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-          mbar_wait(bar_pempty(pb ^ 1), ((chunk_ctr - 1) >> 1) & 1);
-          tc_fence_after();
 #pragma unroll 1
-          for (int c = 0; c < ocols / 32; ++c) {
+          for (int c = 0; c < p.dhp / 32; ++c) {
             uint32_t r[32];
-            const uint32_t ta = tO + lane_off + half * ocols + 32 * c;
-            tmem_ld32(ta, r);
+            tmem_ld32(tO + 32 * c, r);
             tmem_ld_wait();
 #pragma unroll
             for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-            tmem_st32(ta, r);
+            tmem_st32(tO + 32 * c, r);
           }
         }
-        tc_fence_after();
-        tmem_st32(tmem + NA_TMEM_P + 64 * pb + 32 * half + lane_off, pk);  // keys [64 half, +64) of my row
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
+        if (tr) tr[6] = clock64();
         if (lane == 0) mbar_arrive(bar_pfull);
       }
-      // ---- epilogue: O / l -> ctx (row sum = both halves) ----
-      float* rl = red + ((chunk_ctr) & 1) * 256;  // the parity buffer no warp of this quarter still reads
-      rl[half * 128 + row] = l_run;
-      named_bar_sync(1 + quarter, 64);
-      const float l_tot = l_run + rl[(half ^ 1) * 128 + row];
+      // ---- epilogue: O / l -> ctx ----
+      long long* te = (p.trace && blockIdx.x == 0 && row == 0 && tile_ctr < 32) ? p.trace + 2048 + 8 * tile_ctr : nullptr;
+      if (te) te[0] = clock64();
+      const float inv_l = (qvalid && l_run > 0.f) ? 1.f / l_run : 0.f;
       mbar_wait(bar_ofull, tile_ctr & 1);
+      if (te) te[1] = clock64();
       tc_fence_after();
-      const float inv_l = (qvalid && l_tot > 0.f) ? 1.f / l_tot : 0.f;
-      elem_t* orow = p.out + (qvalid ? (static_cast<size_t>((qd * p.rows + qh) * p.cols + qw) * p.ldo +
-                                        g.head * p.dhp + half * ocols)
-                                     : 0);
-#pragma unroll 1
-      for (int c = 0; c < ocols / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tO + lane_off + half * ocols + 32 * c, r);
-        tmem_ld_wait();
-        if (qvalid) {
-          uint4* d4 = reinterpret_cast<uint4*>(orow + 32 * c);
+      const size_t tok = g.b * member_tokens + static_cast<size_t>((qd * p.rows + qh) * p.cols + qw);
+      elem_t* orow = p.out + (qvalid ? tok * p.ldo + g.head * p.dhp : 0);
+      // all of O's row in one batch of TMEM loads, then 256-bit stores (whole 32-byte sectors)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 u;
-            u.x = pack_elem(__uint_as_float(r[8 * q + 0]) * inv_l, __uint_as_float(r[8 * q + 1]) * inv_l);
-            u.y = pack_elem(__uint_as_float(r[8 * q + 2]) * inv_l, __uint_as_float(r[8 * q + 3]) * inv_l);
-            u.z = pack_elem(__uint_as_float(r[8 * q + 4]) * inv_l, __uint_as_float(r[8 * q + 5]) * inv_l);
-            u.w = pack_elem(__uint_as_float(r[8 * q + 6]) * inv_l, __uint_as_float(r[8 * q + 7]) * inv_l);
-            d4[q] = u;
+      for (int c0 = 0; c0 < 128; c0 += 64) {
+        if (c0 < p.dhp) {
+          uint32_t r[64];
+          tmem_ld32(tO + c0, *reinterpret_cast<uint32_t(*)[32]>(r));
+          tmem_ld32(tO + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+          tmem_ld_wait();
+          if (qvalid) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t u[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                u[e] = pack_elem(__uint_as_float(r[16 * q + 2 * e]) * inv_l, __uint_as_float(r[16 * q + 2 * e + 1]) * inv_l);
+              stg256(orow + c0 + 16 * q, u);
+            }
           }
         }
       }
+      if (te) te[2] = clock64();
       tc_fence_before();
-      named_bar_sync(1 + quarter, 64);  // partner has read rl[] before the next tile writes this parity again
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_oempty);
     }
@@ -412,7 +445,7 @@ __global__ void __launch_bounds__(NA_THREADS, 1)
   __syncthreads();
   if (warp == NA_MMA_WARP) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc(tmem, NA_TMEM_COLS);
   }
 }
 
@@ -453,10 +486,11 @@ static void choose_tile(int depth, int rows, int cols, int rows_global, int wd, 
 
 using namespace wm3;
 
-extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, int depth, int rows, int cols,
+extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, int batch, int depth, int rows, int cols,
                               int rows_global, int row0, int halo_lo, int halo_hi, int heads, int dhp, int wd, int wh,
                               int ww, float scale, void* stream) {
   if (dhp != 64 && dhp != 128) return set_error("wm3_natten_fwd: dhp must be 64 or 128 (got %d)", dhp);
+  if (batch < 1) return set_error("wm3_natten_fwd: batch must be >= 1 (got %d)", batch);
   if (wd > depth || wh > rows_global || ww > cols) return set_error("wm3_natten_fwd: window exceeds extents");
   if (ww > 64) return set_error("wm3_natten_fwd: col window %d > 64 unsupported", ww);
   if (row0 < 0 || row0 + rows > rows_global || halo_lo > row0 || row0 + rows + halo_hi > rows_global)
@@ -469,11 +503,13 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
       return set_error("wm3_natten_fwd: halos (%d,%d) smaller than window reach (%d,%d)", halo_lo, halo_hi, need_lo,
                        need_hi);
   }
-  if ((ldqkv % 8) || (ldo % 8)) return set_error("wm3_natten_fwd: pitches must be multiples of 8");
+  if ((ldqkv % 8) || (ldo % 16)) return set_error("wm3_natten_fwd: ldqkv must be a multiple of 8, ldo of 16");
+  if (reinterpret_cast<uintptr_t>(out) % 32) return set_error("wm3_natten_fwd: out must be 32-byte aligned");
   if (ldqkv < 3 * heads * dhp) return set_error("wm3_natten_fwd: ldqkv < 3 * heads * dhp");
   NaParams p{};
   p.out = reinterpret_cast<elem_t*>(out);
   p.ldo = ldo;
+  p.batch = batch;
   p.depth = depth; p.rows = rows; p.cols = cols; p.rows_global = rows_global; p.row0 = row0;
   p.halo_lo = halo_lo; p.rows_ext = rows + halo_lo + halo_hi;
   p.heads = heads; p.dhp = dhp; p.wd = wd; p.wh = wh; p.ww = ww;
@@ -481,15 +517,20 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
   p.ntd = (depth + p.TD - 1) / p.TD;
   p.nth = (rows + p.TH - 1) / p.TH;
   p.ntw = (cols + p.TW - 1) / p.TW;
-  p.nitems = p.ntd * p.nth * p.ntw * heads;
+  p.nitems = p.ntd * p.nth * p.ntw * heads * batch;
   p.scale_log2 = scale * 1.4426950408889634f;
   {
     const char* e = getenv("WM3_NA_DEBUG");
     p.dbg = e ? atoi(e) : 0;
   }
+  static long long* trace_buf = nullptr;
+  const bool tracing = getenv("WM3_NA_TRACE") != nullptr;
+  if (tracing && trace_buf == nullptr && cudaMalloc(&trace_buf, 512 * 8 * sizeof(long long)) != cudaSuccess)
+    return set_error("wm3_natten_fwd: trace buffer");
+  p.trace = tracing ? trace_buf : nullptr;
   const uint64_t wp = cols;
   const uint64_t dims[4] = {static_cast<uint64_t>(3 * heads * dhp), wp, static_cast<uint64_t>(p.rows_ext),
-                            static_cast<uint64_t>(depth)};
+                            static_cast<uint64_t>(batch) * depth};
   const uint64_t strides[3] = {static_cast<uint64_t>(ldqkv), wp * ldqkv, wp * p.rows_ext * ldqkv};
   const uint32_t qbox[4] = {64, static_cast<uint32_t>(p.TW), static_cast<uint32_t>(p.TH), static_cast<uint32_t>(p.TD)};
   const uint32_t kvbox[4] = {64, static_cast<uint32_t>(p.ncp), static_cast<uint32_t>(p.nrpc), 1};
@@ -502,8 +543,24 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
     if (e != cudaSuccess) return set_error("cudaFuncSetAttribute(natten): %s", cudaGetErrorString(e));
     attr = true;
   }
-  const int grid = p.nitems < sm_count() ? p.nitems : sm_count();
+  const int slots = NA_CTAS_PER_SM * sm_count();
+  const int grid = p.nitems < slots ? p.nitems : slots;
   natten_fwd_kernel<<<grid, NA_THREADS, NA_SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(tq, tkv, p);
+  if (tracing) {  // profiling only: dump CTA 0's chunk timeline (cycles relative to its first stamp)
+    static long long h[512 * 8];
+    cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream));
+    cudaMemcpy(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost);
+    const long long t0 = h[0];
+    for (int c = 0; c < 40; ++c)
+      fprintf(stderr, "chunk %3d kfull %7lld S_done %7lld pfull %7lld pv_go %7lld | sm_wait %7lld sfull %7lld parr %7lld | kload %7lld\n",
+              c, h[8 * c] - t0, h[8 * c + 1] - t0, h[8 * c + 2] - t0, h[8 * c + 3] - t0, h[8 * c + 4] - t0,
+              h[8 * c + 5] - t0, h[8 * c + 6] - t0, h[8 * c + 7] - t0);
+    for (int i = 0; i < 8; ++i) {
+      const long long* e = h + 2048 + 8 * i;
+      fprintf(stderr, "item %2d start %7lld geo_done %7lld | epi %7lld ofull %7lld stored %7lld\n", i, e[4] - t0,
+              e[3] - t0, e[0] - t0, e[1] - t0, e[2] - t0);
+    }
+  }
   return check_launch("natten_fwd_kernel");
 }
 

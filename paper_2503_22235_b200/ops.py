@@ -89,22 +89,28 @@ class KVGrid:
 
     Tokens live at [depth][halo_lo + rows + halo_hi][cols]: the band's own rows plus latitude-band halo rows
     received from the neighbouring bands (none on a single GPU).  Longitude wrap needs no padding: the
-    kernel fetches a seam-crossing key patch as two TMA boxes.
+    kernel fetches a seam-crossing key patch as two TMA boxes.  `batch` latents (ensemble members) are
+    stacked member-major along depth: member b owns planes [b * depth, (b + 1) * depth).
     """
 
-    def __init__(self, extents, window=None, halo_lo: int = 0, halo_hi: int = 0):
+    def __init__(self, extents, window=None, halo_lo: int = 0, halo_hi: int = 0, batch: int = 1):
         self.depth, self.rows, self.cols = (int(e) for e in extents)
         self.halo_lo, self.halo_hi = int(halo_lo), int(halo_hi)
+        self.batch = int(batch)
         self.rows_ext = self.rows + self.halo_lo + self.halo_hi
 
     @property
+    def planes(self) -> int:
+        return self.batch * self.depth
+
+    @property
     def tokens(self) -> int:
-        return self.depth * self.rows_ext * self.cols
+        return self.planes * self.rows_ext * self.cols
 
     def interior(self, buf: torch.Tensor) -> torch.Tensor:
-        """(T, C) copy of the band's own tokens in token order (debug / probes)."""
-        g = buf.view(self.depth, self.rows_ext, self.cols, -1)
-        return g[:, self.halo_lo:self.halo_lo + self.rows].reshape(self.depth * self.rows * self.cols, -1)
+        """(batch * T, C) copy of the band's own tokens in token order (debug / probes)."""
+        g = buf.view(self.planes, self.rows_ext, self.cols, -1)
+        return g[:, self.halo_lo:self.halo_lo + self.rows].reshape(self.planes * self.rows * self.cols, -1)
 
 
 def linear_grid(a: torch.Tensor, w: torch.Tensor, epi: int, bias: torch.Tensor, out: torch.Tensor, grid: KVGrid,
@@ -118,7 +124,7 @@ def linear_grid(a: torch.Tensor, w: torch.Tensor, epi: int, bias: torch.Tensor, 
     rp = None if rope is None else ctypes_byref(rope)
     plane = grid.rows * grid.cols
     check(_lib.lib().wm3_linear_planes(ptr(a), a.stride(0), ptr(w), w.stride(0), m, n, k, int(epi), ptr(out),
-                                       out.stride(0), out.shape[1], ptr(bias), rp, grid.depth, plane,
+                                       out.stride(0), out.shape[1], ptr(bias), rp, grid.planes, plane,
                                        grid.rows_ext * grid.cols, grid.halo_lo * grid.cols, stream_ptr()),
           "wm3_linear_planes")
     return out
@@ -133,11 +139,12 @@ def natten(qkv: torch.Tensor, grid: KVGrid, heads: int, dhp: int, dh: int, windo
     wd, wh, ww = (int(e) for e in window)
     d, h, w = grid.depth, grid.rows, grid.cols
     rg = h if rows_global is None else int(rows_global)
-    t = d * h * w
+    t = grid.batch * d * h * w
     if out is None:
         out = torch.empty((t, heads * dhp), dtype=_lib.ELEM, device=qkv.device)
     _req(out, _lib.ELEM, "out")
-    check(_lib.lib().wm3_natten_fwd(ptr(qkv), qkv.stride(0), ptr(out), out.stride(0), d, h, w, rg, int(row0),
+    check(_lib.lib().wm3_natten_fwd(ptr(qkv), qkv.stride(0), ptr(out), out.stride(0), grid.batch, d, h, w, rg,
+                                    int(row0),
                                     grid.halo_lo, grid.halo_hi, int(heads), int(dhp), wd, wh, ww,
                                     float(1.0 / math.sqrt(dh)), stream_ptr()), "wm3_natten_fwd")
     return out

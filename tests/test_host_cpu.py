@@ -199,7 +199,7 @@ def test_library_reports_errors_without_launching():
     lib = _lib.load_library()
     assert lib.wm3_neighbor_table(2, 5, 8, 3, 3, 3, 0, 5, None, None) != 0
     assert b"exceeds" in lib.wm3_last_error()
-    assert lib.wm3_natten_fwd(None, 768, None, 256, 3, 5, 8, 5, 0, 0, 0, 2, 96, 3, 3, 3, 0.1, None) != 0
+    assert lib.wm3_natten_fwd(None, 768, None, 256, 1, 3, 5, 8, 5, 0, 0, 0, 2, 96, 3, 3, 3, 0.1, None) != 0
     assert b"dhp" in lib.wm3_last_error()
 
 

@@ -138,6 +138,25 @@ def test_natten_matches_gather_reference(ext, win, heads, dhp):
     assert rel < 1e-2 and err < 5e-2, (err, rel)
 
 
+@pytest.mark.parametrize("ext,win,heads,dhp,batch", [
+    ((7, 9, 18), (5, 7, 7), 2, 128, 3), ((3, 5, 10), (3, 3, 3), 2, 64, 2), ((4, 6, 10), (2, 4, 4), 3, 128, 4),
+])
+def test_natten_batched_members_equal_single(ext, win, heads, dhp, batch):
+    """Ensemble batching: member b of one batched launch is bitwise the single-member result on its own data."""
+    t = int(np.prod(ext))
+    g = torch.Generator(device="cuda").manual_seed(7 * t + batch)
+    qkv = (torch.randn(batch, t, 3 * heads * dhp, device="cuda", generator=g) * 1.5).to(lib().ELEM)
+    gb = ops().KVGrid(ext, win, batch=batch)
+    out = ops().natten(qkv.reshape(batch * t, -1).contiguous(), gb, heads, dhp, dhp, win)
+    g1 = ops().KVGrid(ext, win)
+    for b in range(batch):
+        one = ops().natten(qkv[b].contiguous(), g1, heads, dhp, dhp, win)
+        assert torch.equal(out[b * t:(b + 1) * t], one), b
+    ref, _ = na_reference(qkv[batch - 1].contiguous(), ext, heads, dhp, dhp, win)
+    rel = ((out[(batch - 1) * t:].float() - ref).norm() / ref.norm()).item()
+    assert rel < 1e-2, rel
+
+
 def test_natten_windows_bit_exact():
     from oracle.grid import bump_starts
     for ext, win in [((5, 90, 180), (5, 7, 7)), ((7, 9, 18), (5, 7, 7)), ((4, 6, 10), (2, 4, 4))]:
