@@ -42,10 +42,12 @@ enum {
  * [3][heads][dhp]; within a q/k head, rotation pair j (reference columns j, j + dh/2) sits at the
  * adjacent columns (2j, 2j + 1), j < dh/2 (a permutation shared by q and k leaves q.k unchanged).
  * pairs: per GEMM row (token of the local band) 128 fp32 = cos[64] then sin[64] of the rotary phases of
- * its global (depth, row, col) position (64-aligned rows; pairs >= dh/2 are (1, 0)). */
+ * its global (depth, row, col) position (64-aligned rows; pairs >= dh/2 are (1, 0)).  period: tokens per
+ * latent; GEMM row r uses table row r % period, so a batch of ensemble members shares one table. */
 typedef struct {
   const float* pairs;
   int heads, dhp;
+  int period;
 } wm3_rope_t;
 
 const char* wm3_last_error(void);

@@ -32,7 +32,7 @@ _ll = ctypes.c_longlong
 
 class RopeT(ctypes.Structure):
     """wm3_rope_t (include/wm3.h)."""
-    _fields_ = [("pairs", _vp), ("heads", _i), ("dhp", _i)]
+    _fields_ = [("pairs", _vp), ("heads", _i), ("dhp", _i), ("period", _i)]
 
 
 # name -> argtypes; every function returns int status

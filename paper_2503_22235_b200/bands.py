@@ -71,7 +71,7 @@ def plan_bands(rows_global: int, window_rows: int, world: int) -> list[Band]:
 
 
 class HaloExchanger:
-    """Fills the halo rows of a band's K/V grid buffer ([depth][halo_lo + rows + halo_hi][cols][C]) from the
+    """Fills the halo rows of a band's K/V grid buffer ([planes][halo_lo + rows + halo_hi][cols][C]) from the
     neighbouring ranks.  Works on CUDA (NCCL) and CPU (gloo) tensors alike."""
 
     def __init__(self, bands: list[Band], rank: int, group=None):
@@ -81,12 +81,13 @@ class HaloExchanger:
     def __call__(self, buf: torch.Tensor, grid) -> None:
         import torch.distributed as dist
         me = self.me
-        g = buf.view(grid.depth, grid.rows_ext, grid.cols, -1)
+        planes = getattr(grid, "planes", grid.depth)  # batch * depth for an ensemble batch
+        g = buf.view(planes, grid.rows_ext, grid.cols, -1)
         ops = []
         lo0 = me.halo_lo  # buffer row of band row 0
         if me.rank > 0:
             up = self.bands[me.rank - 1]
-            for d in range(grid.depth):
+            for d in range(planes):
                 if up.halo_hi:  # my first rows -> upper neighbour's bottom halo
                     ops.append(dist.P2POp(dist.isend, g[d, lo0:lo0 + up.halo_hi].contiguous(), me.rank - 1,
                                           self.group))
@@ -94,7 +95,7 @@ class HaloExchanger:
                     ops.append(dist.P2POp(dist.irecv, g[d, 0:me.halo_lo], me.rank - 1, self.group))
         if me.rank + 1 < len(self.bands):
             dn = self.bands[me.rank + 1]
-            for d in range(grid.depth):
+            for d in range(planes):
                 if dn.halo_lo:  # my last rows -> lower neighbour's top halo
                     ops.append(dist.P2POp(dist.isend, g[d, lo0 + me.rows - dn.halo_lo:lo0 + me.rows].contiguous(),
                                           me.rank + 1, self.group))

@@ -213,7 +213,8 @@ class RopeTables:
         return tab
 
     def struct(self, local_extents, row0: int, heads: int, dhp: int) -> _lib.RopeT:
-        return _lib.RopeT(self.pair_table(local_extents, row0).data_ptr(), heads, dhp)
+        d, h, w = (int(e) for e in local_extents)
+        return _lib.RopeT(self.pair_table(local_extents, row0).data_ptr(), heads, dhp, d * h * w)
 
 
 class Workspace:
@@ -223,7 +224,7 @@ class Workspace:
 
     def __init__(self, grid: "ops.KVGrid", bw: BlockWeights, device="cuda"):
         self.grid = grid
-        tokens = grid.depth * grid.rows * grid.cols
+        tokens = grid.batch * grid.depth * grid.rows * grid.cols
         self.tokens = tokens
         self.hn = torch.empty((tokens, bw.kp), dtype=_lib.ELEM, device=device)
         self.qkv = torch.zeros((grid.tokens, 3 * bw.heads * bw.dhp), dtype=_lib.ELEM, device=device)
@@ -234,6 +235,9 @@ class Workspace:
 def block_forward(x: torch.Tensor, bw: BlockWeights, ws: Workspace, rope: RopeTables, extents, window,
                   row0: int = 0, rows_global: int | None = None, halo_exchange=None) -> None:
     """In-place x (T, hidden) fp32 <- natten_block(x) on the current stream.
+
+    With a batched workspace (ws.grid.batch = B ensemble members) x is (B * T, hidden), member-major; the
+    members never see each other (per-token ops are row-parallel, attention windows stay in a member).
 
     extents are the local (band) token extents; row0 / rows_global place the band in the global grid
     (rotary phases and window bumps use global rows).  halo_exchange(qkv, grid), when given, fills the halo

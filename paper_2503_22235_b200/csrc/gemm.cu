@@ -83,7 +83,9 @@ DEVI void load_resid(const EP& ep, int row, bool row_ok, int n, float (&x)[32]) 
 // The per-token phase table holds cos[64] then sin[64] for token `row`; pairs [i0, i0 + 32) are read with
 // 256-bit loads (every head of a token reuses the same 512 B row, so it stays in L1/L2).
 DEVI void rope_chunk(const wm3_rope_t& rp, int row, int M, int col0_in_head, float (&v)[64]) {
-  const float* tab = rp.pairs + static_cast<size_t>(row < M ? row : 0) * 128 + (col0_in_head >> 1);
+  int t = row < M ? row : 0;
+  if (rp.period > 0) t %= rp.period;  // ensemble members share the table
+  const float* tab = rp.pairs + static_cast<size_t>(t) * 128 + (col0_in_head >> 1);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     float cs[8], sn[8];

@@ -105,13 +105,14 @@ class DeviceModel:
             self._bufs = PyramidBuffers(self.cfg)
         return self._bufs
 
-    def run_blocks(self, x: torch.Tensor, prefixes) -> None:
+    def run_blocks(self, x: torch.Tensor, prefixes, batch: int = 1) -> None:
+        """Blocks in place on x: (batch * tokens, hidden), `batch` independent latents stacked member-major."""
         cfg = self.cfg
         ext = cfg.latent_extents
         rope = CACHE.rope(ext, cfg.head_dim)
         for pre in prefixes:
             bw = CACHE.block(self.params, pre, cfg.heads)
-            block_forward(x, bw, CACHE.workspace(ext, cfg.window, bw), rope, ext, cfg.window)
+            block_forward(x, bw, CACHE.workspace(ext, cfg.window, bw, batch=batch), rope, ext, cfg.window)
 
 
 _models: dict = {}
@@ -179,9 +180,10 @@ def _check_processor(params: dict, cfg: ModelConfig, horizon: int) -> None:
         raise ConfigError(f"parameters carry no {horizon} h processor")
 
 
-def process_inplace(x: torch.Tensor, params: dict, cfg: ModelConfig, horizon: int) -> None:
-    """proc_blocks blocks applied in place to a device token buffer (no validation, no counters)."""
-    device_model(params, cfg).run_blocks(x, [f"proc{horizon}.blk{i}" for i in range(cfg.proc_blocks)])
+def process_inplace(x: torch.Tensor, params: dict, cfg: ModelConfig, horizon: int, batch: int = 1) -> None:
+    """proc_blocks blocks applied in place to a device token buffer (no validation, no counters); x holds
+    `batch` latents stacked member-major ((batch * tokens, hidden))."""
+    device_model(params, cfg).run_blocks(x, [f"proc{horizon}.blk{i}" for i in range(cfg.proc_blocks)], batch)
 
 
 def process(lat: LatentState, params: dict, cfg: ModelConfig, horizon: int) -> LatentState:

@@ -53,13 +53,13 @@ class WeightCache:
             return r
 
     def workspace(self, extents, window, bw: BlockWeights, halo: tuple[int, int] = (0, 0),
-                  tag: str = "main") -> Workspace:
+                  tag: str = "main", batch: int = 1) -> Workspace:
         key = (tag, tuple(int(e) for e in extents), int(window[2]), tuple(halo), bw.kp, bw.nm, bw.heads, bw.dhp,
-               torch.cuda.current_device())
+               int(batch), torch.cuda.current_device())
         with _lock:
             ws = self._ws.get(key)
             if ws is None:
-                ws = Workspace(KVGrid(extents, window, *halo), bw)
+                ws = Workspace(KVGrid(extents, window, *halo, batch=batch), bw)
                 self._ws[key] = ws
             return ws
 

@@ -114,6 +114,26 @@ def test_forecast_matches_manual_composition_bitwise(setup):
     assert zero.surface.values.tobytes() == enc_dec.surface.values.tobytes()
 
 
+def test_ensemble_rollout_members_bitwise(setup):
+    """Config 5's ensemble batch: every member of one batched rollout equals its own single rollout."""
+    name, cfg, params, host = setup
+    m, r = _pkg()
+    members = r.perturbed_members(_state(cfg, seed=8), 3, scale=0.05)
+    lats = [m.encode(s, params, cfg) for s in members]
+    ens = r.rollout_ensemble(lats, (6, 1), params, cfg)
+    eager = r.rollout_ensemble(lats, (6, 1), params, cfg, graphs=False)
+    for k, lt in enumerate(lats):
+        one = r.rollout(lt, (6, 1), params, cfg)
+        assert ens[k].valid_time == 7
+        assert ens[k].tokens.values.tobytes() == one.tokens.values.tobytes(), k
+        assert eager[k].tokens.values.tobytes() == one.tokens.values.tobytes(), k
+    assert not np.array_equal(ens[0].tokens.values, ens[1].tokens.values)
+    assert r.rollout_ensemble(lats, (), params, cfg)[0] is lats[0]
+    fc = r.forecast_ensemble(members[:2], 6, params, cfg)
+    single = r.forecast(members[1], 6, params, cfg)
+    assert fc[1].surface.values.tobytes() == single.surface.values.tobytes()
+
+
 def test_call_counts_and_plan_rejection(setup):
     name, cfg, params, host = setup
     m, r = _pkg()
