@@ -13,7 +13,7 @@
  *   wm3_layernorm_bf16      autodiff.py:400-424  layernorm, eps 1e-6, biased variance
  *   wm3_linear              attention.py:142-143 _linear = matmul(x, W) + b, with fused epilogues:
  *                             WM3_EPI_BIAS_BF16       (plain linear, bf16 out)
- *                             WM3_EPI_BIAS_GELU_BF16  attention.py:182  gelu(hn2 W1 + b1), exact erf
+ *                             WM3_EPI_BIAS_GELU_BF16  attention.py:182  gelu(hn2 W1 + b1), erf form to 2.5e-5
  *                             WM3_EPI_BIAS_RESID_F32  attention.py:179,183  x += ctx Wo + bo / mid W2 + b2
  *                             WM3_EPI_QKV_ROPE        attention.py:167-171  q,k,v + bias, rotary on q,k
  *                             WM3_EPI_F32             raw fp32 accumulator (tests)

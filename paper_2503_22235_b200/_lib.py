@@ -13,7 +13,7 @@ from functools import lru_cache
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwm3.so")
+LIB_PATH = os.environ.get("WM3_LIB") or os.path.join(_HERE, "libwm3.so")  # WM3_LIB: A/B builds (profiling)
 
 # Tensor-core operand dtype the library is built for (csrc/common.cuh elem_t): fp16 by default.
 ELEM = torch.float16

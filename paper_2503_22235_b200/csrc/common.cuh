@@ -294,6 +294,52 @@ DEVI float gelu_fast(float x) {
   return x * (x >= 0.f ? 1.0f - hq : hq);
 }
 // 256-bit global loads (sm_100: LDG.256): one full 32-byte sector per lane.
+// exact-erf GELU with a single MUFU op: erfc(z) = erfcx(z) exp(-z^2), erfcx by a degree-10 polynomial on
+// [0, 4] (|error| < 3e-5 in Phi, far below the fp16 output rounding); z clamped at 4 (erfc(4) = 1.5e-8)
+DEVI float gelu_poly(float x) {
+  const float z = fminf(fabsf(x) * 0.70710678118654752f, 4.0f);
+  float p = 1.154544167e-05f;
+  p = fmaf(p, z, -2.703333948e-04f);
+  p = fmaf(p, z, 2.808806134e-03f);
+  p = fmaf(p, z, -1.717885046e-02f);
+  p = fmaf(p, z, 6.945530602e-02f);
+  p = fmaf(p, z, -1.989096675e-01f);
+  p = fmaf(p, z, 4.261794687e-01f);
+  p = fmaf(p, z, -7.184812635e-01f);
+  p = fmaf(p, z, 9.914053407e-01f);
+  p = fmaf(p, z, -1.127412286e+00f);
+  p = fmaf(p, z, 9.999727368e-01f);
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-z * z * 1.4426950408889634f));
+  const float hq = 0.5f * p * e;  // erfc(z) / 2
+  return x * (x >= 0.f ? 1.0f - hq : hq);
+}
+// Exact-erf GELU (autodiff.py:372-382) as 0.5 x (1 + tanh(u(x))) with u = x (a + x^2 (b + c x^2)) fitted
+// (minimax on [-6, 6]) to the erf form: |error| <= 2.5e-5 plus tanh.approx's 2^-11 relative error, below the
+// fp16 rounding of the stored activation.  One MUFU op and ~8 issue slots: the W1 epilogue is issue-bound
+// (A/B on B200: 0.57 ms vs 0.66-0.71 ms for the 2-MUFU erfc form and the 1-MUFU erfcx polynomial).
+DEVI float gelu_tanh(float x) {
+  const float xc = fminf(fmaxf(x, -6.0f), 6.0f);  // u is monotone on [-6, 6]; tanh(u(6)) = 1 - 4e-9
+  const float x2 = xc * xc;
+  const float u = xc * fmaf(x2, fmaf(x2, -3.51516786e-4f, 0.037005646f), 0.797507884f);
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+  const float hx = 0.5f * x;
+  return fmaf(hx, t, hx);
+}
+#ifndef WM3_GELU_VARIANT
+#define WM3_GELU_VARIANT 2
+#endif
+DEVI float gelu_epi(float x) {
+#if WM3_GELU_VARIANT == 1
+  return gelu_poly(x);
+#elif WM3_GELU_VARIANT == 2
+  return gelu_tanh(x);
+#else
+  return gelu_fast(x);
+#endif
+}
+
 DEVI void ldg256(const float* p, float (&v)[8]) {
   asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
         for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(rr[e]) + (e < nvalid ? __ldg(p.bias + n + e) : 0.f);
         if (p.act_gelu) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = gelu_fast(v[e]);
+          for (int e = 0; e < 32; ++e) v[e] = gelu_epi(v[e]);
         }
         const size_t pix = (static_cast<size_t>(img) * (p.hout + 2) + orow + 1) * (p.wout + 2) + ocol + 1;
         if (p.resid != nullptr) {

@@ -11,7 +11,7 @@
 //                alternating column chunks: tcgen05.ld -> bias / GELU / rotary / residual in registers ->
 //                SWIZZLE_128B smem staging -> TMA store (coalesced, asynchronous, clipped at the edges).
 // Reference semantics: attention.py:142-143 (_linear), :167-171 (q,k,v + rotary), :179 and :183
-// (residual adds), :182 (exact-erf GELU, autodiff.py:372-382).
+// (residual adds), :182 (erf-form GELU, autodiff.py:372-382; common.cuh gelu_tanh, |err| <= 2.5e-5).
 #include "common.cuh"
 #include "launch.h"
 #include "../../include/wm3.h"
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           if (EPI == WM3_EPI_BIAS_GELU_BF16) {
 #pragma unroll
-            for (int e = 0; e < 64; ++e) v[e] = gelu_fast(v[e]);
+            for (int e = 0; e < 64; ++e) v[e] = gelu_epi(v[e]);
           }
           if (EPI == WM3_EPI_QKV_ROPE) {
             const int sec = ep.rope.heads * ep.rope.dhp;
