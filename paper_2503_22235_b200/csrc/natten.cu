@@ -38,7 +38,6 @@ struct NaParams {
   int TD, TH, TW, ntd, nth, ntw, nitems;
   int ncp, nrpc;  // key-chunk box: ncp columns x nrpc rows (fixed for every tile)
   float scale_log2;
-  long long* trace;  // WM3_NA_TRACE: per-chunk clock64 stamps of CTA 0 (profiling only)
   int dbg;  // profiling switch (WM3_NA_DEBUG, bit flags): 1 skip softmax arithmetic, 2 skip Q K^T, 4 skip P V, 8 skip K/V loads
 };
 
@@ -155,9 +154,11 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
   // Every barrier completes once per chunk (or tile) and its waiter always observes a phase before the
   // next one can complete (each completion needs the waiter's own next step), so parity waits never alias.
   const uint32_t bar_qfull = b0 + 0, bar_qempty = b0 + 8, bar_kfull = b0 + 16, bar_kempty = b0 + 24;
-  const uint32_t bar_vfull = b0 + 32, bar_vempty = b0 + 40, bar_sfull = b0 + 48, bar_pfull = b0 + 56;
-  const uint32_t bar_ofull = b0 + 64, bar_oempty = b0 + 72;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  const uint32_t bar_vfull = b0 + 32, bar_vempty = b0 + 40, bar_ofull = b0 + 48, bar_oempty = b0 + 56;
+  auto bar_sfull = [&](int h) { return b0 + 64 + 8 * h; };   // S half h of the chunk is in TMEM
+  auto bar_pfull = [&](int h) { return b0 + 80 + 8 * h; };   // P half h written by the 4 softmax warps
+  auto bar_pvdone = [&](int h) { return b0 + 96 + 8 * h; };  // P V over key half h retired
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -170,10 +171,13 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
     mbar_init(bar_kempty, 1);
     mbar_init(bar_vfull, 1);
     mbar_init(bar_vempty, 1);
-    mbar_init(bar_sfull, 1);
-    mbar_init(bar_pfull, NA_SOFTMAX_WARPS);
     mbar_init(bar_ofull, 1);
     mbar_init(bar_oempty, NA_SOFTMAX_WARPS);
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(bar_sfull(h), 1);
+      mbar_init(bar_pfull(h), NA_SOFTMAX_WARPS);
+      mbar_init(bar_pvdone(h), 1);
+    }
     fence_barrier_init();
   }
   if (warp == NA_MMA_WARP) {
@@ -208,7 +212,6 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
           mbar_arrive(full);
           return;
         }
-        if (!is_v && p.trace && blockIdx.x == 0 && c < 256) p.trace[8 * c + 7] = clock64();
         mbar_arrive_expect_tx(full, kbytes);
         const int c1 = origin, c2 = kr0 - brow0;  // may be negative / past the edge: TMA zero-fills
         const uint32_t dst = is_v ? sV : sK;
@@ -231,49 +234,73 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
     }
   } else if (warp == NA_MMA_WARP) {
     // =============================== MMA issuer ===============================
+    // Half-chunk software pipeline (key halves h = 0, 1 of 64 keys each):
+    //   S0(c) S1(c) | PV0(c) S0(c+1) | PV1(c) S1(c+1) | PV0(c+1) S0(c+2) | ...
+    // S_h(c + 1) overwrites the TMEM columns [64 h, 64 h + 64) whose P_h(c) the preceding PV_h(c) reads (in
+    // order), so the softmax of half 0 of the next chunk overlaps P V of half 1 of this one.
     if (lane == 0) {
-      const uint32_t idesc_s = make_idesc(128, 128, 0, 0);
+      const uint32_t idesc_s = make_idesc(128, 64, 0, 0);
       const uint32_t idesc_o = make_idesc(128, p.dhp, 0, 1);
-      const int kb = p.dhp / 64;
-      const uint32_t tS = tmem, tO = tmem + NA_TMEM_O;
+      const int ksteps = p.dhp / 16;
+      const uint32_t tO = tmem + NA_TMEM_O;
+      auto issue_s = [&](int h) {
+        // S_h = Q K_h^T: keys [64 h, 64 h + 64) are rows [64 h, +64) of the K tile (SW128 K-major)
+        for (int s = 0; s < ((p.dbg & 2) ? 0 : ksteps); ++s) {
+          const uint32_t off = (s >> 2) * 16384u + (s & 3) * 32u;
+          umma_bf16_ss(tmem + 64 * h, make_sdesc_sw128(sQ + off, 16, 1024),
+                       make_sdesc_sw128(sK + off + h * 8192u, 16, 1024), idesc_s, s > 0 ? 1u : 0u);
+        }
+        umma_commit(bar_sfull(h));
+      };
+      auto issue_pv = [&](int h, bool first) {
+        // O += P_h V_h: A = P_h from TMEM columns [64 h, 64 h + 32) (fp16 pairs), B = V rows 64 h.. (MN-major)
+        for (int s = 0; s < ((p.dbg & 4) ? 0 : 4); ++s) {
+          const uint64_t bd = make_sdesc_sw128(sV + (4 * h + s) * 2048u, 16384, 1024);
+          umma_f16_ts(tO, tmem + 64 * h + 8 * s, bd, idesc_o, (!first || s > 0) ? 1u : 0u);
+        }
+        umma_commit(bar_pvdone(h));
+      };
       int chunk_ctr = 0, tile_ctr = 0;
       for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
         const TileGeo g = tile_geo(p, item);
         mbar_wait(bar_qfull, tile_ctr & 1);
+        // prologue: both S halves of the tile's first chunk
+        mbar_wait(bar_kfull, chunk_ctr & 1);
+        tc_fence_after();
+        issue_s(0);
+        issue_s(1);
+        umma_commit(bar_kempty);
+        if (g.nchunks == 1) umma_commit(bar_qempty);
         for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
           const uint32_t ph = chunk_ctr & 1;
-          long long* tr = (p.trace && blockIdx.x == 0 && chunk_ctr < 256) ? p.trace + 8 * chunk_ctr : nullptr;
-          mbar_wait(bar_kfull, ph);
-          if (tr) tr[0] = clock64();
-          tc_fence_after();
-          for (int s = 0; s < ((p.dbg & 2) ? 0 : kb * 4); ++s) {
-            const uint32_t off = (s >> 2) * 16384u + (s & 3) * 32u;
-            umma_bf16_ss(tS, make_sdesc_sw128(sQ + off, 16, 1024), make_sdesc_sw128(sK + off, 16, 1024), idesc_s,
-                         s > 0 ? 1u : 0u);
-          }
-          umma_commit(bar_sfull);
-          umma_commit(bar_kempty);
-          if (j == g.nchunks - 1) umma_commit(bar_qempty);
-          if (tr) tr[1] = clock64();
-          // O += P V: A = P from TMEM (fp16 pairs, 8 columns per 16 keys), B = V MN-major from its TMA tile
-          mbar_wait(bar_pfull, ph);
-          if (tr) tr[2] = clock64();
+          const bool more = j + 1 < g.nchunks;
+          mbar_wait(bar_pfull(0), ph);
           mbar_wait(bar_vfull, ph);
           if (j == 0) mbar_wait(bar_oempty, (tile_ctr & 1) ^ 1);
-          if (tr) tr[3] = clock64();
           tc_fence_after();
-          for (int s = 0; s < ((p.dbg & 4) ? 0 : 8); ++s) {
-            const uint64_t bd = make_sdesc_sw128(sV + s * 2048u, 16384, 1024);
-            umma_f16_ts(tO, tS + 8 * s, bd, idesc_o, (j > 0 || s > 0) ? 1u : 0u);
+          issue_pv(0, j == 0);
+          if (more) {
+            mbar_wait(bar_kfull, ph ^ 1);
+            tc_fence_after();
+            issue_s(0);
           }
+          mbar_wait(bar_pfull(1), ph);
+          tc_fence_after();
+          issue_pv(1, false);
           umma_commit(bar_vempty);
-          if (j == g.nchunks - 1) umma_commit(bar_ofull);
+          if (!more) umma_commit(bar_ofull);
+          if (more) {
+            issue_s(1);
+            umma_commit(bar_kempty);
+            if (j + 1 == g.nchunks - 1) umma_commit(bar_qempty);
+          }
         }
       }
     }
   } else {
     // =============================== softmax / epilogue ===============================
-    // Thread = query row (TMEM lane) of the tile, all 128 key columns of each chunk.
+    // Thread = query row (TMEM lane) of the tile.  Online softmax over key halves of 64: masked max, lazy max
+    // update (O rescaled only when the max grows by > 2^8), exp2, row sum, P_h -> TMEM columns [64 h, +32).
     const int row = 32 * warp + lane;
     const uint32_t lane_off = static_cast<uint32_t>(32 * warp) << 16;
     const uint32_t tS = tmem + lane_off, tO = tmem + NA_TMEM_O + lane_off;
@@ -281,7 +308,6 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
     const size_t member_tokens = static_cast<size_t>(p.depth) * p.rows * p.cols;
     int chunk_ctr = 0, tile_ctr = 0;
     for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
-      if (p.trace && blockIdx.x == 0 && row == 0 && tile_ctr < 32) p.trace[2048 + 8 * tile_ctr + 4] = clock64();
       const TileGeo g = tile_geo(p, item);
       const int qd = g.d0 + row / (p.TH * p.TW);
       const int qh = g.h0 + (row / p.TW) % p.TH;
@@ -293,7 +319,6 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
       const bool circle = (g.ncp == p.cols);
       const int c_lo = circle ? wrap_col((qvalid ? qw : g.w0) - hw, p.cols) : (qvalid ? qw : g.w0) - hw - g.pc0;
       const int s2hi = circle ? c_lo + p.ww - g.ncp : 0;
-      if (p.trace && blockIdx.x == 0 && row == 0 && tile_ctr < 32) p.trace[2048 + 8 * tile_ctr + 3] = clock64();
       float m_run = -INFINITY, l_run = 0.f;
       // window masks depend on (row chunk, part) only, not on the depth plane: cache one per part
       int key0 = -1, key1 = -1;
@@ -311,31 +336,19 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
                       min(c_lo + p.ww, vhi), s2hi);
           key1 = key;
         }
-        const bool dok = !(p.dbg & 16) && qvalid && kd >= q_sd && kd < q_sd + p.wd;
+        const bool dok = qvalid && kd >= q_sd && kd < q_sd + p.wd;
         uint32_t mw[4];
 #pragma unroll
         for (int w = 0; w < 4; ++w) mw[w] = dok ? (part == 0 ? mc0[w] : mc1[w]) : 0u;
-        long long* tr = (p.trace && blockIdx.x == 0 && row == 0 && chunk_ctr < 256) ? p.trace + 8 * chunk_ctr : nullptr;
-        if (tr) tr[4] = clock64();
-        if (tr) tr[7] = clock64();  // (overwrites the producer stamp; mask time = tr[4] of this chunk - tr[7])
-        mbar_wait(bar_sfull, chunk_ctr & 1);
-        if (tr) tr[5] = clock64();
-        tc_fence_after();
-        // Online softmax in two 64-key halves (64 scores live): masked max, lazy max update, exp2, row sum,
-        // P of keys [64 h, 64 h + 64) -> TMEM columns [32 h, 32 h + 32) (S columns already read).  If the
-        // second half raises the max, the first half's P (fp16, <= 2^8) is rescaled in place.
-        float alpha = 1.f;
-        if (p.dbg & 1) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait(bar_sfull(h), chunk_ctr & 1);
+          tc_fence_after();
           uint32_t pk[32];
+          if (p.dbg & 1) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) pk[i] = 0u;
-          if (!(p.dbg & 32)) {
-            tmem_st32(tS, pk);
-            tmem_st32(tS + 32, pk);
-          }
-        } else {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
+            for (int i = 0; i < 32; ++i) pk[i] = 0u;
+          } else {
             uint32_t x[64];
             tmem_ld32(tS + 64 * h, *reinterpret_cast<uint32_t(*)[32]>(x));
             tmem_ld32(tS + 64 * h + 32, *reinterpret_cast<uint32_t(*)[32]>(x + 32));
@@ -345,25 +358,43 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
             for (int i = 0; i < 8; ++i) mxa[i] = -INFINITY;
 #pragma unroll
             for (int k = 0; k < 64; k += 2) {
-              const int kk = 64 * h + k;
-              const float a0 = ((mw[kk >> 5] >> (kk & 31)) & 1u) ? __uint_as_float(x[k]) : -INFINITY;
-              const float a1 = ((mw[kk >> 5] >> ((kk + 1) & 31)) & 1u) ? __uint_as_float(x[k + 1]) : -INFINITY;
+              const uint32_t wbits = mw[2 * h + (k >> 5)];
+              const float a0 = ((wbits >> (k & 31)) & 1u) ? __uint_as_float(x[k]) : -INFINITY;
+              const float a1 = ((wbits >> ((k + 1) & 31)) & 1u) ? __uint_as_float(x[k + 1]) : -INFINITY;
               x[k] = __float_as_uint(a0);
               x[k + 1] = __float_as_uint(a1);
               mxa[(k >> 1) & 7] = fmaxf(mxa[(k >> 1) & 7], fmaxf(a0, a1));
             }
             const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
                                    fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7]))) * p.scale_log2;
-            float a_h = 1.f;
-            if (mx > m_run + NA_RESCALE_LOG2) {  // lazy rescale (also covers m_run = -inf: a_h = 0)
-              a_h = exp2f(m_run - mx);
+            float alpha = 1.f;
+            if (mx > m_run + NA_RESCALE_LOG2) {  // lazy max update (also covers m_run = -inf)
+              alpha = exp2f(m_run - mx);
               m_run = mx;
+            }
+            // O holds weight only once l_run > 0; rescaling it needs the one P V that may still be in flight
+            // (issued right after the S half just waited on): PV1(c - 1) for half 0, PV0(c) for half 1.
+            const bool resc = alpha != 1.f && l_run > 0.f;
+            l_run *= alpha;
+            if (__any_sync(0xffffffffu, resc)) {
+              if (h == 0) mbar_wait(bar_pvdone(1), (chunk_ctr - 1) & 1);
+              else mbar_wait(bar_pvdone(0), chunk_ctr & 1);
+              tc_fence_after();
+              const float f = resc ? alpha : 1.f;
+#pragma unroll 1
+              for (int c = 0; c < p.dhp / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld32(tO + 32 * c, r);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * f);
+                tmem_st32(tO + 32 * c, r);
+              }
             }
             const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
             float lsa[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) lsa[i] = 0.f;
-            uint32_t pk[32];
 #pragma unroll
             for (int k = 0; k < 64; k += 2) {
               const float p0 = fast_exp2(fmaf(__uint_as_float(x[k]), p.scale_log2, -m_use));  // exp2(-inf) = 0
@@ -371,47 +402,18 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
               lsa[(k >> 1) & 7] += p0 + p1;
               pk[k >> 1] = pack_elem(p0, p1);
             }
-            l_run = l_run * a_h + (((lsa[0] + lsa[1]) + (lsa[2] + lsa[3])) + ((lsa[4] + lsa[5]) + (lsa[6] + lsa[7])));
-            alpha *= a_h;
-            if (h == 1 && __any_sync(0xffffffffu, a_h != 1.f)) {  // rare: first half's P to the new max
-              uint32_t q0[32];
-              tmem_st_wait();
-              tmem_ld32(tS, q0);
-              tmem_ld_wait();
-#pragma unroll
-              for (int e = 0; e < 32; ++e) {
-                const float2 f = unpack_elem2(q0[e]);
-                q0[e] = pack_elem(f.x * a_h, f.y * a_h);
-              }
-              tmem_st32(tS, q0);
-            }
-            tmem_st32(tS + 32 * h, pk);
+            l_run += ((lsa[0] + lsa[1]) + (lsa[2] + lsa[3])) + ((lsa[4] + lsa[5]) + (lsa[6] + lsa[7]));
           }
+          tmem_st32(tS + 64 * h, pk);  // P_h over the first 32 of the S_h columns just read
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_pfull(h));
         }
-        // ---- rescale O: P V(c - 1) has retired (S(c) was issued after it and has completed) ----
-        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll 1
-          for (int c = 0; c < p.dhp / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld32(tO + 32 * c, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-            tmem_st32(tO + 32 * c, r);
-          }
-        }
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (tr) tr[6] = clock64();
-        if (lane == 0) mbar_arrive(bar_pfull);
       }
       // ---- epilogue: O / l -> ctx ----
-      long long* te = (p.trace && blockIdx.x == 0 && row == 0 && tile_ctr < 32) ? p.trace + 2048 + 8 * tile_ctr : nullptr;
-      if (te) te[0] = clock64();
       const float inv_l = (qvalid && l_run > 0.f) ? 1.f / l_run : 0.f;
       mbar_wait(bar_ofull, tile_ctr & 1);
-      if (te) te[1] = clock64();
       tc_fence_after();
       const size_t tok = g.b * member_tokens + static_cast<size_t>((qd * p.rows + qh) * p.cols + qw);
       elem_t* orow = p.out + (qvalid ? tok * p.ldo + g.head * p.dhp : 0);
@@ -429,13 +431,13 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
               uint32_t u[8];
 #pragma unroll
               for (int e = 0; e < 8; ++e)
-                u[e] = pack_elem(__uint_as_float(r[16 * q + 2 * e]) * inv_l, __uint_as_float(r[16 * q + 2 * e + 1]) * inv_l);
+                u[e] = pack_elem(__uint_as_float(r[16 * q + 2 * e]) * inv_l,
+                                 __uint_as_float(r[16 * q + 2 * e + 1]) * inv_l);
               stg256(orow + c0 + 16 * q, u);
             }
           }
         }
       }
-      if (te) te[2] = clock64();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_oempty);
@@ -523,11 +525,7 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
     const char* e = getenv("WM3_NA_DEBUG");
     p.dbg = e ? atoi(e) : 0;
   }
-  static long long* trace_buf = nullptr;
-  const bool tracing = getenv("WM3_NA_TRACE") != nullptr;
-  if (tracing && trace_buf == nullptr && cudaMalloc(&trace_buf, 512 * 8 * sizeof(long long)) != cudaSuccess)
-    return set_error("wm3_natten_fwd: trace buffer");
-  p.trace = tracing ? trace_buf : nullptr;
+
   const uint64_t wp = cols;
   const uint64_t dims[4] = {static_cast<uint64_t>(3 * heads * dhp), wp, static_cast<uint64_t>(p.rows_ext),
                             static_cast<uint64_t>(batch) * depth};
@@ -546,21 +544,6 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
   const int slots = NA_CTAS_PER_SM * sm_count();
   const int grid = p.nitems < slots ? p.nitems : slots;
   natten_fwd_kernel<<<grid, NA_THREADS, NA_SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(tq, tkv, p);
-  if (tracing) {  // profiling only: dump CTA 0's chunk timeline (cycles relative to its first stamp)
-    static long long h[512 * 8];
-    cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream));
-    cudaMemcpy(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost);
-    const long long t0 = h[0];
-    for (int c = 0; c < 40; ++c)
-      fprintf(stderr, "chunk %3d kfull %7lld S_done %7lld pfull %7lld pv_go %7lld | sm_wait %7lld sfull %7lld parr %7lld | kload %7lld\n",
-              c, h[8 * c] - t0, h[8 * c + 1] - t0, h[8 * c + 2] - t0, h[8 * c + 3] - t0, h[8 * c + 4] - t0,
-              h[8 * c + 5] - t0, h[8 * c + 6] - t0, h[8 * c + 7] - t0);
-    for (int i = 0; i < 8; ++i) {
-      const long long* e = h + 2048 + 8 * i;
-      fprintf(stderr, "item %2d start %7lld geo_done %7lld | epi %7lld ofull %7lld stored %7lld\n", i, e[4] - t0,
-              e[3] - t0, e[0] - t0, e[1] - t0, e[2] - t0);
-    }
-  }
   return check_launch("natten_fwd_kernel");
 }
 
