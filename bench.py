@@ -211,33 +211,12 @@ def timed(fn, steps, stream, world):
     return float(ms.item())
 
 
-def kernel_breakdown(bw, ws, rope, local, me, x, reps, stream):
-    """Per-launch device time (CUDA events on the launching stream) of one block's kernels."""
-    import torch
-    from paper_2503_22235_b200 import _lib as L
-    from paper_2503_22235_b200 import ops
-    rs = rope.struct(local, me.row0, bw.heads, bw.dhp)
-    fns = [
-        lambda: ops.layernorm_bf16(x, bw.ln1_g, bw.ln1_b, out=ws.hn),
-        lambda: ops.linear_grid(ws.hn, bw.w_qkv, L.WM3_EPI_QKV_ROPE, bw.b_qkv, ws.qkv, ws.grid, rope=rs),
-        lambda: ops.natten(ws.qkv, ws.grid, bw.heads, bw.dhp, bw.dh, WIN, out=ws.ctx, rows_global=EXT[1],
-                           row0=me.row0),
-        lambda: ops.linear(ws.ctx, bw.w_o, L.WM3_EPI_BIAS_RESID_F32, bias=bw.b_o, out=x, n_valid=bw.hidden),
-        lambda: ops.layernorm_bf16(x, bw.ln2_g, bw.ln2_b, out=ws.hn),
-        lambda: ops.linear(ws.hn, bw.w_1, L.WM3_EPI_BIAS_GELU_BF16, bias=bw.b_1, out=ws.mid),
-        lambda: ops.linear(ws.mid, bw.w_2, L.WM3_EPI_BIAS_RESID_F32, bias=bw.b_2, out=x, n_valid=bw.hidden),
-    ]
-    acc = [0.0] * len(fns)
-    for _ in range(reps):
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(fns) + 1)]
-        evs[0].record(stream)
-        for i, fn in enumerate(fns):
-            fn()
-            evs[i + 1].record(stream)
-        torch.cuda.synchronize()
-        for i in range(len(fns)):
-            acc[i] += evs[i].elapsed_time(evs[i + 1])
-    return {n: a / reps for n, a in zip(KERNELS, acc)}
+def load_traffic() -> dict:
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from the committed ncu capture."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic_r1.json")))["bytes_per_launch"]
+    except Exception:
+        return {}
 
 
 def roofline(per_ms: dict, tokens: int) -> tuple[dict, dict]:
@@ -247,19 +226,20 @@ def roofline(per_ms: dict, tokens: int) -> tuple[dict, dict]:
     # algorithmic bytes: LN reads fp32 x and writes the 2-byte operand; NA reads q, k, v and writes ctx
     kbytes = {"layernorm1": T * D * 6.0, "layernorm2": T * D * 6.0, "natten": T * D * 2 * 4.0}
     peaks = load_peaks()
+    traffic = load_traffic()
     top = max(per_ms, key=per_ms.get)
     if top in kflops:
         ach = kflops[top] / (per_ms[top] / 1e3) / 1e12
         roof = {"kernel": top, "bound": "tensor", "achieved": ach, "peak": peaks["bf16_sustained"],
-                "unit": "TFLOP/s", "frac": ach / peaks["bf16_sustained"], "traffic": None,
+                "unit": "TFLOP/s", "frac": ach / peaks["bf16_sustained"], "traffic": traffic.get(top),
                 "peak_kind": f"{peaks['source']} bf16 dense, sustained (fp16 operands run at the same rate)"}
     else:
         ach = kbytes[top] / (per_ms[top] / 1e3) / 1e9
         roof = {"kernel": top, "bound": "hbm", "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s",
-                "frac": ach / peaks["hbm"], "traffic": None, "peak_kind": f"{peaks['source']} hbm copy"}
+                "frac": ach / peaks["hbm"], "traffic": traffic.get(top), "peak_kind": f"{peaks['source']} hbm copy"}
     table = {}
     for n, ms in per_ms.items():
-        row = {"ms": round(ms, 5)}
+        row = {"ms": round(ms, 5), "dram_bytes_ncu": traffic.get(n)}
         if n in kflops:
             row["tflops"] = round(kflops[n] / (ms / 1e3) / 1e12, 2)
             row["frac_tc"] = round(row["tflops"] / peaks["bf16_sustained"], 4)
@@ -344,18 +324,34 @@ def run_gpu(args, world, rank, local_rank):
     params, bw, me, local, ws, rope, exch, x = block_setup(world, rank)
     stream = torch.cuda.current_stream()
 
+    # per-launch CUDA events recorded on the launching stream inside the timed steps (kernel durations for
+    # the roofline are these, averaged over the timed region)
+    marks = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
+    cursor = [None]
+
+    def mark(i):
+        if cursor[0] is not None:
+            cursor[0][i].record(stream)
+
     def step():
-        block_forward(x, bw, ws, rope, local, WIN, row0=me.row0, rows_global=EXT[1], halo_exchange=exch)
+        block_forward(x, bw, ws, rope, local, WIN, row0=me.row0, rows_global=EXT[1], halo_exchange=exch, mark=mark)
 
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
     clk = ClockSampler(local_rank).__enter__()
-    ms = timed(step, args.steps, stream, world)
+    it = iter(marks)
+
+    def timed_step():
+        cursor[0] = next(it)
+        step()
+
+    ms = timed(timed_step, args.steps, stream, world)
+    cursor[0] = None
     flops = block_flops(int(np.prod(EXT)))
     value = flops * args.steps / (ms / 1e3) / 1e12
 
-    per_ms = kernel_breakdown(bw, ws, rope, local, me, x, max(3, min(args.steps, 10)), stream)
+    per_ms = {n: sum(ev[i].elapsed_time(ev[i + 1]) for ev in marks) / len(marks) for i, n in enumerate(KERNELS)}
     roof, table = roofline(per_ms, int(np.prod(local)))
 
     # ---- e2e: pinned host band -> H2D -> block -> D2H ----

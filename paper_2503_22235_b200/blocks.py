@@ -233,7 +233,7 @@ class Workspace:
 
 
 def block_forward(x: torch.Tensor, bw: BlockWeights, ws: Workspace, rope: RopeTables, extents, window,
-                  row0: int = 0, rows_global: int | None = None, halo_exchange=None) -> None:
+                  row0: int = 0, rows_global: int | None = None, halo_exchange=None, mark=None) -> None:
     """In-place x (T, hidden) fp32 <- natten_block(x) on the current stream.
 
     With a batched workspace (ws.grid.batch = B ensemble members) x is (B * T, hidden), member-major; the
@@ -243,16 +243,26 @@ def block_forward(x: torch.Tensor, bw: BlockWeights, ws: Workspace, rope: RopeTa
     (rotary phases and window bumps use global rows).  halo_exchange(qkv, grid), when given, fills the halo
     rows of the padded K/V grid from the neighbouring bands between the QKV GEMM and the attention kernel.
     Launches: LN1, QKV+rotary GEMM, NA, O-proj+residual GEMM, LN2, W1+GELU GEMM, W2+residual GEMM.
+    mark(i), when given, is called before launch i and once more after the last (profiling: CUDA events).
     """
     L = _lib
     g = ws.grid
+    mk = mark if mark is not None else (lambda i: None)
+    mk(0)
     ops.layernorm_bf16(x, bw.ln1_g, bw.ln1_b, out=ws.hn)
+    mk(1)
     rs = rope.struct(extents, row0, bw.heads, bw.dhp)
     ops.linear_grid(ws.hn, bw.w_qkv, L.WM3_EPI_QKV_ROPE, bw.b_qkv, ws.qkv, g, rope=rs)
     if halo_exchange is not None:
         halo_exchange(ws.qkv, g)
+    mk(2)
     ops.natten(ws.qkv, g, bw.heads, bw.dhp, bw.dh, window, out=ws.ctx, rows_global=rows_global, row0=row0)
+    mk(3)
     ops.linear(ws.ctx, bw.w_o, L.WM3_EPI_BIAS_RESID_F32, bias=bw.b_o, out=x, n_valid=bw.hidden)
+    mk(4)
     ops.layernorm_bf16(x, bw.ln2_g, bw.ln2_b, out=ws.hn)
+    mk(5)
     ops.linear(ws.hn, bw.w_1, L.WM3_EPI_BIAS_GELU_BF16, bias=bw.b_1, out=ws.mid)
+    mk(6)
     ops.linear(ws.mid, bw.w_2, L.WM3_EPI_BIAS_RESID_F32, bias=bw.b_2, out=x, n_valid=bw.hidden)
+    mk(7)
