@@ -76,6 +76,11 @@ DEVI bool mbar_test(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Programmatic dependent launch (launch.h launch_pdl): let the next kernel on the stream be scheduled, and
+// wait until the previous kernels have completed and their memory is visible.  No-ops without PDL.
+DEVI void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+DEVI void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Bounded wait: a pipeline bug traps (kernel error) instead of hanging the box.
 DEVI void mbar_wait(uint32_t bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;

@@ -72,6 +72,7 @@ DEVI void conv_tile(const ConvParams& p, int mt, int& img, int& cls, int& r, int
 template <int BN>
 __global__ void __launch_bounds__(CV_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, ConvParams p) {
+  griddep_launch_dependents();  // PDL: the next kernel may start its prologue
   using Cfg = ConvCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -112,6 +113,7 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();  // PDL: inputs are complete from here on
 
   if (warp == 0) {
     if (lane == 0) {
@@ -279,6 +281,8 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
 __global__ void fields_to_nhwc_kernel(const float* __restrict__ src, long long img_stride, long long a_stride,
                                       long long p_stride, int cdiv, int imgs, int C, int H, int W, int cp,
                                       elem_t* __restrict__ dst) {
+  griddep_launch_dependents();  // PDL: the next kernel may start its prologue
+  griddep_wait();
   const long long total = static_cast<long long>(imgs) * (H + 2) * (W + 2) * cp;
   for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -301,6 +305,8 @@ __global__ void fields_to_nhwc_kernel(const float* __restrict__ src, long long i
 // tokens fp32 [img][H][W][C] (C = hidden) -> padded bf16 NHWC with cp channels
 __global__ void tokens_to_nhwc_kernel(const float* __restrict__ tok, int imgs, int H, int W, int C, int cp,
                                       elem_t* __restrict__ dst) {
+  griddep_launch_dependents();  // PDL: the next kernel may start its prologue
+  griddep_wait();
   const long long total = static_cast<long long>(imgs) * (H + 2) * (W + 2) * (cp / 2);
   for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -333,7 +339,7 @@ static int launch_conv(const CUtensorMap& ta, const CUtensorMap& tb, const ConvP
   }
   const long long ntiles = static_cast<long long>(p.imgs) * p.nclass * p.tiles_per_class * (p.cout_pad / BN);
   const int grid = static_cast<int>(ntiles < sm_count() ? ntiles : sm_count());
-  conv_tc_kernel<BN><<<grid, CV_THREADS, Cfg::SMEM, s>>>(ta, tb, p);
+  if (launch_pdl(conv_tc_kernel<BN>, dim3(grid), dim3(CV_THREADS), Cfg::SMEM, s, ta, tb, p)) return -1;
   return check_launch("conv_tc_kernel");
 }
 
@@ -411,9 +417,10 @@ extern "C" int wm3_fields_to_nhwc(const float* src, long long img_stride, long l
   const long long total = static_cast<long long>(imgs) * (h + 2) * (w + 2) * cp;
   long long blocks = (total + 255) / 256;
   if (blocks > 148LL * 64) blocks = 148LL * 64;
-  fields_to_nhwc_kernel<<<static_cast<int>(blocks), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      src, img_stride, a_stride, p_stride, chan_div > 0 ? chan_div : 1, imgs, channels, h, w, cp,
-      reinterpret_cast<elem_t*>(dst));
+  if (launch_pdl(fields_to_nhwc_kernel, dim3(static_cast<int>(blocks)), dim3(256), 0,
+                 reinterpret_cast<cudaStream_t>(stream), src, img_stride, a_stride, p_stride,
+                 chan_div > 0 ? chan_div : 1, imgs, channels, h, w, cp, reinterpret_cast<elem_t*>(dst)))
+    return -1;
   return check_launch("fields_to_nhwc_kernel");
 }
 
@@ -423,7 +430,9 @@ extern "C" int wm3_tokens_to_nhwc(const float* tokens, int imgs, int h, int w, i
   const long long total = static_cast<long long>(imgs) * (h + 2) * (w + 2) * (cp / 2);
   long long blocks = (total + 255) / 256;
   if (blocks > 148LL * 64) blocks = 148LL * 64;
-  tokens_to_nhwc_kernel<<<static_cast<int>(blocks), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      tokens, imgs, h, w, channels, cp, reinterpret_cast<elem_t*>(dst));
+  if (launch_pdl(tokens_to_nhwc_kernel, dim3(static_cast<int>(blocks)), dim3(256), 0,
+                 reinterpret_cast<cudaStream_t>(stream), tokens, imgs, h, w, channels, cp,
+                 reinterpret_cast<elem_t*>(dst)))
+    return -1;
   return check_launch("tokens_to_nhwc_kernel");
 }

@@ -105,6 +105,7 @@ template <int BN, int EPI>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmOut, int M, int N, int K, EpiParams ep) {
+  griddep_launch_dependents();  // PDL: the next kernel may start its prologue
   using Cfg = GemmCfg<BN>;
   using Tr = EpiTraits<EPI>;
   constexpr int STAGES = Cfg::STAGES;
@@ -159,6 +160,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();  // PDL: inputs (A, residual) are complete from here on
 
   if (warp == 0) {
     if (lane == 0) {
@@ -337,7 +339,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUten
   }
   const int ntiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN);
   const int grid = ntiles < sm_count() ? ntiles : sm_count();
-  kern<<<grid, GEMM_THREADS, Cfg::SMEM, stream>>>(ta, tb, to, M, N, K, ep);
+  if (launch_pdl(kern, dim3(grid), dim3(GEMM_THREADS), Cfg::SMEM, stream, ta, tb, to, M, N, K, ep)) return -1;
   return check_launch("gemm_tc_kernel");
 }
 

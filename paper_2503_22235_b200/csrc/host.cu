@@ -1,5 +1,6 @@
 // C-ABI plumbing: error reporting, device properties, TMA descriptor encoding.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <mutex>
 
@@ -22,6 +23,16 @@ int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error("%s launch failed: %s", what, cudaGetErrorString(e));
   return 0;
+}
+
+bool pdl_enabled() {
+  // Off by default: measured on B200 the CUDA-graph rollout ran 4.5 % slower with PDL (2.80 vs 2.68 ms per
+  // block, alternating A/B, tools/rollout_time.py) and the eager block step was unchanged.  WM3_PDL=1 enables.
+  static const bool on = [] {
+    const char* e = getenv("WM3_PDL");
+    return e && atoi(e) != 0;
+  }();
+  return on;
 }
 
 int sm_count() {

@@ -24,4 +24,26 @@ int make_tmap(CUtensorMap* map, const void* ptr, int dtype, int rank, const uint
 int make_tmap_bf16(CUtensorMap* map, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_elems,
                    const uint32_t* box, const uint32_t* elem_strides);
 
+// Launch with programmatic dependent launch (PDL): the kernel may be scheduled while the previous kernel on
+// the stream drains; it must execute griddep_wait() (common.cuh) before touching memory the previous kernels
+// produce or consume.  Every wm3 kernel does, right after its prologue (barriers, TMEM, tensor-map prefetch),
+// so the prologue and launch latency overlap the predecessor's tail.  Opt-in (WM3_PDL=1): see host.cu.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess) return set_error("launch: %s", cudaGetErrorString(e));
+  return 0;
+}
+
 }  // namespace wm3

@@ -33,6 +33,8 @@ __global__ void neighbor_table_kernel(int depth, int rows, int cols, int wd, int
 template <int NV>
 __global__ void layernorm_kernel(const float* __restrict__ x, int ldx, int m, int n, const float* __restrict__ gain,
                                  const float* __restrict__ bias, float eps, elem_t* __restrict__ out, int ldo) {
+  griddep_launch_dependents();  // PDL: the next kernel may start its prologue
+  griddep_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= m) return;
@@ -115,11 +117,7 @@ extern "C" int wm3_layernorm_bf16(const float* x, int ldx, int m, int n, const f
   const int blocks = (m * 32 + threads - 1) / threads;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   auto* o = reinterpret_cast<elem_t*>(out_bf16);
-  if (n <= 256)
-    layernorm_kernel<2><<<blocks, threads, 0, s>>>(x, ldx, m, n, gain, bias, eps, o, ldo);
-  else if (n <= 1024)
-    layernorm_kernel<8><<<blocks, threads, 0, s>>>(x, ldx, m, n, gain, bias, eps, o, ldo);
-  else
-    layernorm_kernel<16><<<blocks, threads, 0, s>>>(x, ldx, m, n, gain, bias, eps, o, ldo);
+  auto kern = (n <= 256) ? layernorm_kernel<2> : (n <= 1024) ? layernorm_kernel<8> : layernorm_kernel<16>;
+  if (launch_pdl(kern, dim3(blocks), dim3(threads), 0, s, x, ldx, m, n, gain, bias, eps, o, ldo)) return -1;
   return check_launch("layernorm_kernel");
 }

@@ -146,6 +146,7 @@ DEVI void window_mask(uint32_t (&m)[4], int nr, int ncp, int rlo, int rhi, int s
 
 __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
     natten_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, NaParams p) {
+  griddep_launch_dependents();  // PDL: the next kernel may start its prologue
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sQ = smem_u32(smem), sK = sQ + NA_TILE, sV = sQ + 2 * NA_TILE;
@@ -191,6 +192,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // PDL: q/k/v are complete from here on
   const int sec = p.heads * p.dhp;  // columns per q/k/v section
   const int brow0 = p.row0 - p.halo_lo;
 
@@ -543,7 +545,9 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
   }
   const int slots = NA_CTAS_PER_SM * sm_count();
   const int grid = p.nitems < slots ? p.nitems : slots;
-  natten_fwd_kernel<<<grid, NA_THREADS, NA_SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(tq, tkv, p);
+  if (launch_pdl(natten_fwd_kernel, dim3(grid), dim3(NA_THREADS), NA_SMEM, reinterpret_cast<cudaStream_t>(stream), tq,
+                 tkv, p))
+    return -1;
   return check_launch("natten_fwd_kernel");
 }
 
