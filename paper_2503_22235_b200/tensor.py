@@ -55,5 +55,9 @@ class Tensor:
 
 
 def host_values(t) -> np.ndarray:
-    """float64 numpy view of a parameter given as our Tensor, a reference Tensor (.values) or an array."""
-    return np.asarray(getattr(t, "values", t), dtype=np.float64)
+    """float64 numpy view of a parameter given as our Tensor, a reference Tensor (.values), a torch tensor
+    (e.g. from serialization.load_params_device) or an array."""
+    v = getattr(t, "values", t)
+    if isinstance(v, torch.Tensor):
+        return v.detach().to("cpu", torch.float64).numpy()
+    return np.asarray(v, dtype=np.float64)

@@ -1,0 +1,62 @@
+"""`forecast` CLI on the B200 path vs the reference CLI's own outputs (tests/golden/cli, reference-generated).
+
+Tolerance as the model tests: per-variable relative L2 <= 1e-2 after a 13 h (6, 6, 1) forecast
+and a 2-source blended 7 h forecast; --offload bitwise equal to the plain run (reference test_cli.py:128-139).
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2503_22235_b200.cli import main
+from paper_2503_22235_b200.serialization import load_params_file
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "cli")
+BASE = ["forecast", "--config", os.path.join(GOLD, "tiny.cfg"), "--params", os.path.join(GOLD, "params.lmtw"),
+        "--init", os.path.join(GOLD, "data.wmd3")]
+
+
+def _per_var_rel(got, ref):
+    out = {}
+    for i in range(ref["surface"].shape[0]):
+        out[f"sfc{i}"] = np.linalg.norm(got["surface"][i] - ref["surface"][i]) / np.linalg.norm(ref["surface"][i])
+    for a in range(ref["atmos"].shape[0]):
+        for lev in range(ref["atmos"].shape[1]):
+            r = ref["atmos"][a, lev]
+            out[f"atm{a}.lev{lev}"] = np.linalg.norm(got["atmos"][a, lev] - r) / np.linalg.norm(r)
+    return out
+
+
+@pytest.mark.parametrize("extra,ref_name", [
+    (["--init-hour", "0", "--dt", "13"], "fc_primary.lmtw"),
+    (["--init-hour", "4", "--dt", "7", "--source", "primary", "--source", "op1"], "fc_blend.lmtw"),
+])
+def test_forecast_matches_reference_cli(tmp_path, extra, ref_name):
+    out = tmp_path / "fc.lmtw"
+    assert main(BASE + extra + ["--out", str(out)]) == 0
+    got, ref = load_params_file(out), load_params_file(os.path.join(GOLD, ref_name))
+    assert set(got) == {"surface", "atmos", "valid_time"}
+    assert got["surface"].shape == ref["surface"].shape and got["atmos"].shape == ref["atmos"].shape
+    assert float(got["valid_time"]) == float(ref["valid_time"])
+    rel = _per_var_rel(got, ref)
+    worst = max(rel, key=rel.get)
+    assert rel[worst] < 1e-2, (worst, rel[worst])
+    man = json.loads(open(str(out) + ".manifest.json").read())
+    assert man["outputs"] == [str(out)] and man["config"]["rows"] == 24 and man["seed"] is None
+
+
+def test_offload_flag_matches_plain_bitwise(tmp_path):
+    a, b = tmp_path / "a.lmtw", tmp_path / "b.lmtw"
+    args = BASE + ["--init-hour", "0", "--dt", "13"]
+    assert main(args + ["--out", str(a)]) == 0
+    assert main(args + ["--out", str(b), "--offload"]) == 0
+    assert a.read_bytes() == b.read_bytes()
+
+
+def test_out_dir_env(tmp_path, monkeypatch):
+    monkeypatch.setenv("GRIDCAST_OUT_DIR", str(tmp_path))
+    assert main(BASE + ["--dt", "1", "--out", "rel/fc.lmtw"]) == 0
+    assert (tmp_path / "rel" / "fc.lmtw").exists()
