@@ -113,6 +113,16 @@ int wm3_fields_to_nhwc(const float* src, long long img_stride, long long a_strid
 /* fp32 tokens [img][H][W][channels] -> padded NHWC (model.py:357-360). */
 int wm3_tokens_to_nhwc(const float* tokens, int imgs, int h, int w, int channels, int cp, void* dst, void* stream);
 
+/* Verification metrics (evaluation.py:37-190), float64 accumulation, deterministic order.
+ * Fields are [imgs][rows][cols] of dtype 0 = float32 or 1 = float64; with k > 1 the field is the mean of k
+ * ensemble members spaced member_stride elements apart (the leading-k ensemble mean of ensemble_curve).
+ *   wm3_sq_err_rows:  partial[t * rows + r] = w_rows[r] * sum_c (a - b)^2 (latitude_rmse, evaluation.py:37-52)
+ *   wm3_zonal_power:  out[img][r][m], m <= cols / 2, mean-square zonal power (zonal_power, evaluation.py:59-75) */
+int wm3_sq_err_rows(int dtype, const void* a, long long member_stride, int k, const void* b, const double* w_rows,
+                    int times, int rows, int cols, double* partial, void* stream);
+int wm3_zonal_power(int dtype, const void* field, long long member_stride, int k, int imgs, int rows, int cols,
+                    double* out, void* stream);
+
 /* Profiling aid: cycles for `reps` groups of 8 K=16 MMAs (mode 0 SS, 1 TS, 2 TS with MN-major B), N = n. */
 int wm3_mma_probe(int mode, int n, int reps, int ctas, long long* out_cycles, void* stream);
 

@@ -49,6 +49,8 @@ SIGNATURES = {
     "wm3_conv": [_i, _vp, _i, _i, _i, _i, _vp, _i, _vp, _i, _vp, _i, _i, _vp, _i, _ll, _ll, _ll, _i, _vp],
     "wm3_fields_to_nhwc": [_vp, _ll, _ll, _ll, _i, _i, _i, _i, _i, _i, _vp, _vp],
     "wm3_tokens_to_nhwc": [_vp, _i, _i, _i, _i, _i, _vp, _vp],
+    "wm3_sq_err_rows": [_i, _vp, _ll, _i, _vp, _vp, _i, _i, _i, _vp, _vp],
+    "wm3_zonal_power": [_i, _vp, _ll, _i, _i, _i, _i, _vp, _vp],
 }
 
 WM3_CONV_S1, WM3_CONV_S2, WM3_CONV_T2 = 0, 1, 2

@@ -9,8 +9,10 @@ GRIDCAST_OUT_DIR prepended to relative output paths, exit code 0 / 1 (one line "
 stderr, category io | config | data | compute) / 2 (usage).  `--offload` selects the reference's activation
 offload engine for the latent chain; the inference forward keeps no activations, so it is accepted and the
 output is bitwise identical (the reference's own test_cli.py:128-139 property).  Validation (sources, dt cap)
-runs before any device work.  The other reference subcommands (gen-data, train, evaluate, scorecard,
-bench-offload, verify) are not part of the forecast hot path and are not provided.
+runs before any device work.  `evaluate` (cli.py:235-276) scores a forecast file against the truth planes of a
+WMD3 dataset with the device metrics (evaluation.py: every plane's RMSE and blur in one launch each) and
+`scorecard` (cli.py:279-300) compares two evaluation reports.  The other reference subcommands (gen-data,
+train, bench-offload, verify) are not part of the forecast path and are not provided.
 """
 
 from __future__ import annotations
@@ -120,6 +122,67 @@ def _cmd_forecast(args, argv) -> int:
     return 0
 
 
+def _load_forecast_fields(path):
+    blobs = load_params_file(path)
+    for key in ("surface", "atmos", "valid_time"):
+        if key not in blobs:
+            raise DataError(f"forecast file lacks {key!r}")
+    return blobs["surface"], blobs["atmos"], int(blobs["valid_time"])
+
+
+def _cmd_evaluate(args, argv) -> int:
+    from .evaluation import plane_scores
+
+    t0 = time.time()
+    sfc, atm, valid_time = _load_forecast_fields(args.forecast)
+    ds = load_dataset_file(args.truth)
+    true_sfc, true_atm = ds.truth_fields(ds.index_at(valid_time))
+    if sfc.shape != true_sfc.shape or atm.shape != true_atm.shape:
+        raise DataError(f"forecast shapes {sfc.shape}/{atm.shape} do not match truth "
+                        f"{true_sfc.shape}/{true_atm.shape}")
+    names = [f"sfc{i}" for i in range(sfc.shape[0])]
+    names += [f"atm{a}.lev{lev}" for a in range(atm.shape[0]) for lev in range(atm.shape[1])]
+    h, w = ds.grid.rows, ds.grid.cols
+    pred = np.concatenate([sfc, atm.reshape(-1, h, w)])
+    true = np.concatenate([true_sfc, true_atm.reshape(-1, h, w)])
+    rmse_v, blur_v = plane_scores(pred, true, ds.grid, args.wavelength_km)
+    doc = {"valid_time": valid_time, "wavelength_km": args.wavelength_km, "rmse": dict(zip(names, rmse_v)),
+           "blur": dict(zip(names, blur_v))}
+    out = _resolve_out(args.out)
+    os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
+    with open(out, "w") as f:
+        json.dump(doc, f, indent=2, sort_keys=True)
+        f.write("\n")
+    write_manifest(out, argv, {"wavelength_km": args.wavelength_km}, None, [out], time.time() - t0)
+    print(f"evaluated {len(names)} planes at hour {valid_time}; mean rmse {float(np.mean(rmse_v)):.6f} -> {out}")
+    return 0
+
+
+def _cmd_scorecard(args, argv) -> int:
+    from .evaluation import scorecard
+
+    t0 = time.time()
+    docs = []
+    for name, path in (("a", args.a), ("b", args.b)):
+        with open(path) as f:
+            doc = json.load(f)
+        if "rmse" not in doc:
+            raise DataError(f"file {name} is not an evaluation report")
+        docs.append(doc)
+    pct = scorecard(docs[0]["rmse"], docs[1]["rmse"])
+    width = max(len(k) for k in pct)
+    for k in sorted(pct):
+        print(f"{k:<{width}}  {docs[0]['rmse'][k]:12.6f}  {docs[1]['rmse'][k]:12.6f}  {pct[k]:+8.3f}%")
+    if args.out:
+        out = _resolve_out(args.out)
+        os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
+        with open(out, "w") as f:
+            json.dump({"percent_vs_baseline": pct}, f, indent=2, sort_keys=True)
+            f.write("\n")
+        write_manifest(out, argv, {}, None, [out], time.time() - t0)
+    return 0
+
+
 def build_parser() -> argparse.ArgumentParser:
     p = argparse.ArgumentParser(prog="paper_2503_22235_b200", description=__doc__.split("\n\n")[0])
     p.add_argument("--version", action="version", version=f"%(prog)s {__version__}")
@@ -135,10 +198,19 @@ def build_parser() -> argparse.ArgumentParser:
     f.add_argument("--offload", action="store_true", help="accepted for compatibility; identical output")
     f.add_argument("--budget-bytes", type=int, default=1 << 28)
     f.add_argument("--lookahead", type=int, default=2)
+    e = sub.add_parser("evaluate", help="score a forecast file against truth")
+    e.add_argument("--forecast", required=True)
+    e.add_argument("--truth", required=True, help="WMD3 dataset file")
+    e.add_argument("--wavelength-km", type=float, default=2000.0)
+    e.add_argument("--out", required=True)
+    sc = sub.add_parser("scorecard", help="percent RMSE change of a versus b")
+    sc.add_argument("--a", required=True, help="evaluation JSON")
+    sc.add_argument("--b", required=True, help="baseline evaluation JSON")
+    sc.add_argument("--out")
     return p
 
 
-_HANDLERS = {"forecast": _cmd_forecast}
+_HANDLERS = {"forecast": _cmd_forecast, "evaluate": _cmd_evaluate, "scorecard": _cmd_scorecard}
 
 
 def _categorize(exc: BaseException) -> str:

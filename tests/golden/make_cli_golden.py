@@ -10,6 +10,7 @@ Writes tests/golden/cli/:
     data.wmd3           reference CLI `gen-data --hours 18 --seed 3 --sources 2`
     fc_primary.lmtw     reference CLI `forecast --init-hour 0 --dt 13`
     fc_blend.lmtw       reference CLI `forecast --init-hour 4 --dt 7 --source primary --source op1`
+    eval_primary.json   reference CLI `evaluate --forecast fc_primary.lmtw --truth data.wmd3 --wavelength-km 12000`
 """
 import os
 import sys
@@ -39,6 +40,8 @@ def run():
     assert main(base + ["--init-hour", "0", "--dt", "13", "--out", os.path.join(HERE, "fc_primary.lmtw")]) == 0
     assert main(base + ["--init-hour", "4", "--dt", "7", "--source", "primary", "--source", "op1",
                         "--out", os.path.join(HERE, "fc_blend.lmtw")]) == 0
+    assert main(["evaluate", "--forecast", os.path.join(HERE, "fc_primary.lmtw"), "--truth", data,
+                 "--wavelength-km", "12000", "--out", os.path.join(HERE, "eval_primary.json")]) == 0
     for f in os.listdir(HERE):  # manifests carry host paths and timings: not fixtures
         if f.endswith(".manifest.json"):
             os.remove(os.path.join(HERE, f))

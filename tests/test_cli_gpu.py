@@ -60,3 +60,22 @@ def test_out_dir_env(tmp_path, monkeypatch):
     monkeypatch.setenv("GRIDCAST_OUT_DIR", str(tmp_path))
     assert main(BASE + ["--dt", "1", "--out", "rel/fc.lmtw"]) == 0
     assert (tmp_path / "rel" / "fc.lmtw").exists()
+
+
+def test_evaluate_and_scorecard_match_reference(tmp_path):
+    ev = tmp_path / "eval.json"
+    assert main(["evaluate", "--forecast", os.path.join(GOLD, "fc_primary.lmtw"), "--truth",
+                 os.path.join(GOLD, "data.wmd3"), "--wavelength-km", "12000", "--out", str(ev)]) == 0
+    got = json.loads(ev.read_text())
+    ref = json.loads(open(os.path.join(GOLD, "eval_primary.json")).read())
+    assert got["valid_time"] == ref["valid_time"] == 13 and len(got["rmse"]) == 3 + 8
+    for k in ref["rmse"]:
+        assert abs(got["rmse"][k] - ref["rmse"][k]) <= 1e-10 * ref["rmse"][k], k
+        if ref["blur"][k] is None:
+            assert got["blur"][k] is None
+        else:
+            assert abs(got["blur"][k] - ref["blur"][k]) <= 1e-8 * ref["blur"][k], k
+    sc = tmp_path / "sc.json"
+    assert main(["scorecard", "--a", str(ev), "--b", os.path.join(GOLD, "eval_primary.json"), "--out", str(sc)]) == 0
+    pct = json.loads(sc.read_text())["percent_vs_baseline"]
+    assert all(abs(v) < 1e-6 for v in pct.values())
