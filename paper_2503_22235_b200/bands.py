@@ -116,3 +116,120 @@ def local_band_tokens(x_global: torch.Tensor, extents, band: Band) -> torch.Tens
 def gather_bands(parts: list[torch.Tensor], extents, bands: list[Band]) -> torch.Tensor:
     d, h, w = extents
     return torch.cat([p.view(d, b.rows, w, -1) for p, b in zip(parts, bands)], dim=1).reshape(d * h * w, -1)
+
+
+# ------------------------------------------------------------------------------------------------
+# banded latent processor / rollout
+# ------------------------------------------------------------------------------------------------
+def copy_halos(bands: list[Band], workspaces: list) -> None:
+    """In-process halo fill between the K/V grids of several bands held by one process (device copies);
+    the same rows HaloExchanger moves between ranks."""
+    for r, (b, ws) in enumerate(zip(bands, workspaces)):
+        g = ws.grid
+        me = ws.qkv.view(g.planes, g.rows_ext, g.cols, -1)
+        if b.halo_lo:
+            up, gu = bands[r - 1], workspaces[r - 1].grid
+            src = workspaces[r - 1].qkv.view(gu.planes, gu.rows_ext, gu.cols, -1)
+            s0 = up.halo_lo + up.rows - b.halo_lo
+            me[:, :b.halo_lo] = src[:, s0:s0 + b.halo_lo]
+        if b.halo_hi:
+            dn, gd = bands[r + 1], workspaces[r + 1].grid
+            src = workspaces[r + 1].qkv.view(gd.planes, gd.rows_ext, gd.cols, -1)
+            me[:, b.halo_lo + b.rows:] = src[:, dn.halo_lo:dn.halo_lo + b.halo_hi]
+
+
+class BandedProcessor:
+    """Processor blocks over latitude bands: for each block, LN1 + QKV (into each band's halo'd K/V grid)
+    for every held band, the halo exchange, then attention and the rest of the block per band.
+
+    `held` are the bands this process computes: its own band under torch.distributed (exchange =
+    HaloExchanger over NCCL / gloo), or every band when one process emulates the split on one GPU
+    (exchange = copy_halos).  Kernels never wait on one another either way."""
+
+    def __init__(self, params: dict, cfg, bands: list[Band], held: list[int], exchanger=None):
+        from .runtime import CACHE
+        self.params, self.cfg, self.bands = params, cfg, bands
+        self.held = [bands[i] for i in held]
+        self.exchanger = exchanger
+        d, h, w = cfg.latent_extents
+        self.rope = CACHE.rope(cfg.latent_extents, cfg.head_dim)
+        self.local = [(d, b.rows, w) for b in self.held]
+
+    def _ws(self, bw):
+        from .runtime import CACHE
+        # one workspace per band (tagged by rank): bands of equal shape must not share K/V grids
+        return [CACHE.workspace(ext, self.cfg.window, bw, halo=(b.halo_lo, b.halo_hi), tag=f"band{b.rank}")
+                for ext, b in zip(self.local, self.held)]
+
+    def process(self, xs: list[torch.Tensor], horizon: int) -> None:
+        """In place on the held bands' token buffers xs[i] ((d * rows_i * w, hidden) fp32, band order)."""
+        from . import _lib, ops
+        from .runtime import CACHE
+        cfg = self.cfg
+        h = cfg.latent_extents[1]
+        for i in range(cfg.proc_blocks):
+            bw = CACHE.block(self.params, f"proc{horizon}.blk{i}", cfg.heads)
+            wss = self._ws(bw)
+            for b, ext, xb, ws in zip(self.held, self.local, xs, wss):
+                ops.layernorm_bf16(xb, bw.ln1_g, bw.ln1_b, out=ws.hn)
+                ops.linear_grid(ws.hn, bw.w_qkv, _lib.WM3_EPI_QKV_ROPE, bw.b_qkv, ws.qkv, ws.grid,
+                                rope=self.rope.struct(ext, b.row0, bw.heads, bw.dhp))
+            if self.exchanger is not None:
+                for ws in wss:
+                    self.exchanger(ws.qkv, ws.grid)
+            else:
+                copy_halos(self.held, wss)
+            for b, xb, ws in zip(self.held, xs, wss):
+                ops.natten(ws.qkv, ws.grid, bw.heads, bw.dhp, bw.dh, cfg.window, out=ws.ctx, rows_global=h,
+                           row0=b.row0)
+                ops.linear(ws.ctx, bw.w_o, _lib.WM3_EPI_BIAS_RESID_F32, bias=bw.b_o, out=xb, n_valid=bw.hidden)
+                ops.layernorm_bf16(xb, bw.ln2_g, bw.ln2_b, out=ws.hn)
+                ops.linear(ws.hn, bw.w_1, _lib.WM3_EPI_BIAS_GELU_BF16, bias=bw.b_1, out=ws.mid)
+                ops.linear(ws.mid, bw.w_2, _lib.WM3_EPI_BIAS_RESID_F32, bias=bw.b_2, out=xb, n_valid=bw.hidden)
+
+
+def rollout_banded(lat, plan, params: dict, cfg, world: int | None = None, group=None):
+    """rollout() with the latent split into latitude bands.
+
+    Under an initialised torch.distributed group of size N > 1 (and world None): rank r keeps band r, halos
+    move over the group (NCCL over NVLink on B200), and the bands are all-gathered at the end so every rank
+    returns the full latent.  With `world` given and no group, one process emulates `world` bands on its GPU
+    (the same kernels and halo rows; used to verify the split on one device).  Validation as rollout()."""
+    import torch.distributed as dist
+
+    from .model import CALL_COUNTS, LatentState, _tokens
+    from .rollout import _check_plan, plan_hours
+    from .tensor import Tensor
+
+    plan = _check_plan(plan, params, cfg)
+    if not plan:
+        return lat
+    from .model import device_model
+    device_model(params, cfg)
+    d, h, w = cfg.latent_extents
+    x = _tokens(lat)
+    distributed = world is None and dist.is_available() and dist.is_initialized() and \
+        dist.get_world_size(group) > 1
+    n = dist.get_world_size(group) if distributed else int(world or 1)
+    bands = plan_bands(h, cfg.window[1], n)
+    if distributed:
+        rank = dist.get_rank(group)
+        proc = BandedProcessor(params, cfg, bands, [rank], HaloExchanger(bands, rank, group))
+        xs = [local_band_tokens(x, cfg.latent_extents, bands[rank]).clone()]
+    else:
+        proc = BandedProcessor(params, cfg, bands, list(range(n)))
+        xs = [local_band_tokens(x, cfg.latent_extents, b).clone() for b in bands]
+    for hz in plan:
+        proc.process(xs, hz)
+        CALL_COUNTS[f"process{hz}"] += 1
+    if distributed:
+        # variable band sizes: pad to the largest band for all_gather, then trim
+        hidden = x.shape[1]
+        mx = max(b.rows for b in bands) * d * w
+        buf = torch.zeros((mx, hidden), dtype=x.dtype, device=x.device)
+        buf[:xs[0].shape[0]] = xs[0]
+        parts = [torch.empty_like(buf) for _ in bands]
+        dist.all_gather(parts, buf, group=group)
+        xs = [p[:d * b.rows * w] for p, b in zip(parts, bands)]
+    full = gather_bands(xs, cfg.latent_extents, bands)
+    return LatentState(Tensor(device=full), lat.valid_time + plan_hours(plan), tuple(lat.extents))

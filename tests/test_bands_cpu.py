@@ -123,3 +123,60 @@ def test_halo_exchange_gloo_band_attention(world, ext):
         ok, got = results[rank]
         assert ok, f"rank {rank} halo rows differ from the neighbours' rows"
         np.testing.assert_allclose(got.reshape(d, b.rows, w, c), full[:, b.row0:b.row0 + b.rows], atol=1e-12)
+
+
+class _FakeProcessor:
+    """Stands in for BandedProcessor (whose kernels need a GPU): adds (global row + 1) * horizon to every token
+    of each held band, so the test checks the sharding, the band bookkeeping and the all-gather."""
+
+    def __init__(self, params, cfg, bands, held, exchanger=None):
+        self.held = [bands[i] for i in held]
+        self.ext = cfg.latent_extents
+
+    def process(self, xs, horizon):
+        d, h, w = self.ext
+        for b, x in zip(self.held, xs):
+            rows = torch.arange(b.row0, b.row0 + b.rows, dtype=x.dtype).view(1, -1, 1, 1)
+            x.view(d, b.rows, w, -1).add_((rows + 1.0) * horizon)
+
+
+def _rollout_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2503_22235_b200.bands as B
+        import paper_2503_22235_b200.model as M
+        from paper_2503_22235_b200.tensor import Tensor
+        cfg = M.mid_config()
+        B.BandedProcessor = _FakeProcessor
+        M._tokens = lambda lat: lat.tokens.device  # CPU tensor stands in for the device latent
+        M.device_model = lambda params, cfg: None
+        params = {f"proc{h}.blk0.ln1.gain": None for h in cfg.horizons}
+        x = torch.from_numpy(np.random.default_rng(3).standard_normal((cfg.tokens, 4)))
+        lat = M.LatentState(Tensor(device=x.clone()), 5, cfg.latent_extents)
+        out = B.rollout_banded(lat, (6, 1, 1), params, cfg)
+        out_q.put((rank, out.valid_time, out.tokens.device.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_rollout_banded_gloo_sharding_and_gather():
+    import paper_2503_22235_b200.model as M
+    cfg = M.mid_config()
+    world = 2
+    ctx = mp.get_context("spawn")
+    q_out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rollout_worker, args=(r, world, port, q_out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q_out.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    d, h, w = cfg.latent_extents
+    x = np.random.default_rng(3).standard_normal((cfg.tokens, 4))
+    want = x.reshape(d, h, w, 4) + (np.arange(h) + 1.0).reshape(1, h, 1, 1) * 8
+    for rank, vt, got in res:
+        assert vt == 5 + 8
+        np.testing.assert_allclose(got.reshape(d, h, w, 4), want, rtol=0, atol=1e-12)

@@ -80,3 +80,26 @@ def test_band_block_forward_with_callback_single_band():
                   halo_exchange=lambda buf, grid: calls.append(grid.rows_ext))
     assert calls == [ext[1]]
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("name,world", [("desk", 2), ("mid", 2)])
+def test_banded_rollout_matches_single_gpu(name, world):
+    """rollout_banded: the latent split into `world` latitude bands (emulated on this GPU: same kernels and
+    halo rows as the NCCL path) reproduces the single-GPU mixed-horizon rollout."""
+    import paper_2503_22235_b200.model as m
+    import paper_2503_22235_b200.rollout as r
+    from paper_2503_22235_b200.bands import rollout_banded
+    cfg = {"desk": m.desk_config, "mid": m.mid_config}[name]()
+    params = m.init_model_params(cfg, seed=7, zero_residual=False)
+    rng = np.random.default_rng(4)
+    g = cfg.grid
+    st = m.WeatherState(0, rng.standard_normal((cfg.surface_in, g.rows, g.cols)),
+                        rng.standard_normal((cfg.atmos_vars, cfg.levels, g.rows, g.cols)))
+    lat = m.encode(st, params, cfg)
+    one = r.rollout(lat, (6, 1), params, cfg)
+    banded = rollout_banded(lat, (6, 1), params, cfg, world=world)
+    assert banded.valid_time == 7 and tuple(banded.extents) == tuple(lat.extents)
+    x0, a, b = lat.tokens.values, one.tokens.values, banded.tokens.values
+    rel = np.linalg.norm((b - x0) - (a - x0)) / np.linalg.norm(a - x0)
+    assert rel < 2e-3, rel
+    assert rollout_banded(lat, (), params, cfg, world=world) is lat
