@@ -226,23 +226,33 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int n0 = (tile % nn) * BN;
       const int row = m0 + r_in_tile;
       const bool row_ok = (r0 + r_in_tile < ep.plane_rows) && row < M;
-      // residual prefetch of this group's first chunk (overlaps the mainloop wait)
-      float xa[32], xb[32];
-      if (EPI == WM3_EPI_BIAS_RESID_F32) load_resid(ep, row, row_ok, n0 + g * CW, xa);
+      // residual prefetch, RESID_DEPTH chunks of this group ahead: the first ones overlap the mainloop wait
+      // (the residual epilogue is HBM-latency bound: more bytes in flight per thread)
+#ifndef WM3_RESID_DEPTH
+#define WM3_RESID_DEPTH 1  // deeper prefetch spills registers and measured slower (A/B: depth 1 0.25 ms, 2 0.28 ms O-proj)
+#endif
+      constexpr int RESID_DEPTH = WM3_RESID_DEPTH;
+      float xr[RESID_DEPTH + 1][32];
+      if (EPI == WM3_EPI_BIAS_RESID_F32) {
+#pragma unroll
+        for (int i = 0; i < RESID_DEPTH; ++i)
+          if (g + 2 * i < NUNITS) load_resid(ep, row, row_ok, n0 + (g + 2 * i) * CW, xr[i]);
+      }
       mbar_wait(tfull_bar(acc), aphase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(32 * q) << 16);
 #pragma unroll
       for (int u = g; u < NUNITS; u += 2) {
         const int n = n0 + u * CW;
-        if (EPI == WM3_EPI_BIAS_RESID_F32 && u + 2 < NUNITS) load_resid(ep, row, row_ok, n + 2 * CW, xb);
+        const int it = (u - g) >> 1;  // compile-time after unrolling
+        float(&xa)[32] = xr[it % (RESID_DEPTH + 1)];
+        if (EPI == WM3_EPI_BIAS_RESID_F32 && u + 2 * RESID_DEPTH < NUNITS)
+          load_resid(ep, row, row_ok, n + 2 * RESID_DEPTH * CW, xr[(it + RESID_DEPTH) % (RESID_DEPTH + 1)]);
         if (Tr::F32) {
           uint32_t r[32];
           tmem_ld32(taddr + u * CW, r);
           tmem_ld_wait();
-          float v[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
+          float* v = reinterpret_cast<float*>(r);  // accumulate in place: no extra 32-register copy
           if (EPI == WM3_EPI_BIAS_RESID_F32) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -305,10 +315,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           bulk_commit();
         }
         if (Cfg::STAGING_PER_GROUP > 1) sbuf ^= 1;
-        if (EPI == WM3_EPI_BIAS_RESID_F32) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) xa[j] = xb[j];
-        }
       }
       tc_fence_before();
       __syncwarp();
