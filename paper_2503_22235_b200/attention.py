@@ -17,7 +17,7 @@ from .blocks import rope_axis_tables
 from .errors import ConfigError
 from .params import block_param_names, init_block_params  # noqa: F401  (re-exported API)
 from .runtime import CACHE
-from .tensor import Tensor
+from .tensor import Tensor, host_array
 
 __all__ = ["natten_block", "attention_weights", "rotary_tables", "apply_rotary", "init_block_params",
            "block_param_names", "to_device_f32", "validate_block_args"]
@@ -30,7 +30,7 @@ def to_device_f32(x) -> torch.Tensor:
     elif isinstance(x, torch.Tensor):
         src = x
     else:
-        src = torch.from_numpy(np.ascontiguousarray(np.asarray(getattr(x, "values", x), dtype=np.float32)))
+        src = torch.from_numpy(np.ascontiguousarray(host_array(x, np.float32)))
     return src.to(device="cuda", dtype=torch.float32, copy=True).contiguous()
 
 
@@ -107,9 +107,7 @@ def rotary_tables(extents, head_dim: int):
 
 def apply_rotary(x, cos, sin):
     """Rotate feature pairs (j, j + dh/2) of x (T, heads, dh) by per-token phases (attention.py:87-92)."""
-    xv = np.asarray(getattr(x, "values", x))
-    cv = np.asarray(getattr(cos, "values", cos))
-    sv = np.asarray(getattr(sin, "values", sin))
+    xv, cv, sv = host_array(x), host_array(cos), host_array(sin)
     half = xv.shape[-1] // 2
     a, b = xv[..., :half], xv[..., half:]
     return Tensor(np.concatenate([a * cv - b * sv, a * sv + b * cv], axis=-1))

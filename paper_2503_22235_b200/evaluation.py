@@ -21,6 +21,7 @@ from . import _lib
 from ._lib import check, ptr, stream_ptr
 from .errors import ConfigError, DataError
 from .grid import GridSpec, latitude_weights, row_circumference_km
+from .tensor import host_array
 
 __all__ = ["BLUR_UNBOUNDED", "DEFAULT_SUBSET_SIZES", "latitude_rmse", "zonal_power", "power_at_wavelength",
            "blur_index", "subset_sizes", "ensemble_curve", "scorecard", "plane_scores"]
@@ -35,7 +36,7 @@ def _device(x) -> torch.Tensor:
     if isinstance(dev, torch.Tensor):  # our Tensor wrapper with a device buffer
         x = dev
     elif not isinstance(x, torch.Tensor):
-        x = torch.from_numpy(np.ascontiguousarray(np.asarray(getattr(x, "values", x), dtype=np.float64)))
+        x = torch.from_numpy(np.ascontiguousarray(host_array(x, np.float64)))
     if x.dtype not in (torch.float32, torch.float64):
         x = x.to(torch.float64)
     return x.to("cuda").contiguous()

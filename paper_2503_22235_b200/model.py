@@ -24,7 +24,7 @@ from .params import (available_sources, block_param_names, encoder_prefix, init_
                      init_model_params)
 from .pyramid import DecoderWeights, EncoderWeights, PyramidBuffers, decode_planes, encode_planes
 from .runtime import CACHE
-from .tensor import Tensor, host_values
+from .tensor import Tensor, host_array, host_values, payload
 
 __all__ = [
     "ModelConfig", "desk_config", "full_scale_config", "tiny_config", "mid_config", "WeatherState",
@@ -59,6 +59,17 @@ class DecodedFields:
     def to_state(self) -> WeatherState:
         return WeatherState(self.valid_time, self.surface.values.copy(), self.atmos.values.copy())
 
+    def to_host(self, out=None):
+        """(surface, atmos) as float32 host tensors in page-locked memory (one DMA each, no float64 widening).
+        Pass `out` = a previous result to reuse its pinned buffers (steady-state: no host allocation)."""
+        if out is None:
+            out = tuple(torch.empty(t.device.shape, dtype=torch.float32, pin_memory=True)
+                        for t in (self.surface, self.atmos))
+        for host, t in zip(out, (self.surface, self.atmos)):
+            host.copy_(t.device, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return out
+
 
 @dataclass
 class LatentState:
@@ -84,7 +95,7 @@ class DeviceModel:
         self._fp = None
 
     def refresh(self) -> None:
-        fp = tuple(id(getattr(v, "values", v)) for v in self.params.values())
+        fp = tuple(id(payload(v)) for v in self.params.values())
         if fp != self._fp:
             self._enc.clear()
             self._dec = None
@@ -133,7 +144,7 @@ def device_model(params: dict, cfg: ModelConfig) -> DeviceModel:
 def _to_device(a, shape) -> torch.Tensor:
     if isinstance(a, torch.Tensor):
         return a.to("cuda", torch.float32)
-    return torch.from_numpy(np.ascontiguousarray(np.asarray(getattr(a, "values", a), dtype=np.float32))).to("cuda")
+    return torch.from_numpy(np.ascontiguousarray(host_array(a, np.float32))).to("cuda")
 
 
 def _tokens(lat: LatentState) -> torch.Tensor:
@@ -218,7 +229,7 @@ def blend_latents(latents: list, weights) -> LatentState:
             raise ConfigError(f"blend of mismatched valid times {t0} and {lt.valid_time}")
         if tuple(lt.extents) != tuple(ext):
             raise ConfigError("blend of mismatched latent extents")
-    w = np.asarray(getattr(weights, "values", weights), dtype=np.float64)
+    w = host_array(weights, np.float64)
     if w.shape != (len(latents),):
         raise ConfigError(f"{len(latents)} states but weight shape {w.shape}")
     if (w < 0).any() or abs(w.sum() - 1.0) > 1e-12:

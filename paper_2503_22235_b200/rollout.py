@@ -171,8 +171,8 @@ def perturbed_members(state: WeatherState, members: int, scale: float = 0.01, se
     """Ensemble initial states: member m = state + N(0, scale) from default_rng(seed + m), in the style of
     the reference's perturbed sources (synthdata.py:186-193)."""
     import numpy as np
-    sfc = np.asarray(getattr(state.surface, "values", state.surface))
-    atm = np.asarray(getattr(state.atmos, "values", state.atmos))
+    from .tensor import host_array
+    sfc, atm = host_array(state.surface), host_array(state.atmos)
     out = []
     for m in range(members):
         rng = np.random.default_rng(seed + m)

@@ -15,12 +15,13 @@ import torch
 from .blocks import BlockWeights, RopeTables, Workspace, prepare_block
 from .ops import KVGrid
 from .params import block_param_names
+from .tensor import payload
 
 _lock = threading.Lock()
 
 
 def _fingerprint(params: dict, names) -> tuple:
-    return tuple(id(getattr(params[n], "values", params[n])) for n in names if n in params)
+    return tuple(id(payload(params[n])) for n in names if n in params)
 
 
 class WeightCache:
@@ -38,7 +39,7 @@ class WeightCache:
             if hit is not None and hit[0] == fp:
                 return hit[2]
         bw = prepare_block(params, prefix, heads)
-        keep = [getattr(params[n], "values", params[n]) for n in names]
+        keep = [payload(params[n]) for n in names]
         with _lock:
             self._blocks[key] = (fp, keep, bw)
         return bw

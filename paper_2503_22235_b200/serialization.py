@@ -32,9 +32,8 @@ class ContainerError(ValueError):
 
 
 def _as_f64(v) -> np.ndarray:
-    a = getattr(v, "values", v)
-    if hasattr(a, "detach"):  # torch tensor (e.g. device-backed values)
-        a = a.detach().double().cpu().numpy()
+    from .tensor import host_array
+    a = host_array(v)
     # np.array keeps rank 0 as rank 0 (np.ascontiguousarray would promote it to rank 1)
     return np.array(a, dtype=np.float64, order="C", copy=None)
 

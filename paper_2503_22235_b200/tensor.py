@@ -54,10 +54,23 @@ class Tensor:
         return f"Tensor(shape={self.shape}, {where})"
 
 
+def payload(x):
+    """The array object behind x: a torch tensor as is (torch.Tensor.values is a sparse-tensor method, not
+    data), else x.values for our / the reference's Tensor, else x itself."""
+    if isinstance(x, torch.Tensor):
+        return x
+    return getattr(x, "values", x)
+
+
+def host_array(x, dtype=None) -> np.ndarray:
+    """numpy view / copy of x (torch CPU or CUDA tensor, Tensor with .values, or array-like)."""
+    v = payload(x)
+    if isinstance(v, torch.Tensor):
+        v = v.detach().cpu().numpy()
+    return np.asarray(v, dtype=dtype)
+
+
 def host_values(t) -> np.ndarray:
     """float64 numpy view of a parameter given as our Tensor, a reference Tensor (.values), a torch tensor
     (e.g. from serialization.load_params_device) or an array."""
-    v = getattr(t, "values", t)
-    if isinstance(v, torch.Tensor):
-        return v.detach().to("cpu", torch.float64).numpy()
-    return np.asarray(v, dtype=np.float64)
+    return host_array(t, np.float64)
