@@ -2,6 +2,10 @@
 //
 //   C[M, N] = A[M, K] * B[N, K]^T     A: activations bf16 (K-major), B: weights bf16 pre-transposed
 //                                     to (out, in) so both operands are K-major SWIZZLE_128B tiles.
+// CG = 2 (default for N >= 256): CTA pairs (cluster of 2 on one TPC) issue tcgen05.mma.cta_group::2 with
+// M = 256: each CTA loads its own 128 A rows and half of the B tile (BN / 2 rows) into its smem, the leader's
+// MMA reads B from both SMs, and each CTA's TMEM receives its 128 x BN accumulator; per-SM smem operand
+// traffic halves (A 16 KB + B/2 16 KB per k-block instead of 16 + 32 KB), freeing smem for a 6-deep ring.
 // Roles (one CTA per SM, 384 threads):
 //   warp 0       TMA producer: A/B k-blocks into a STAGES-deep smem ring (mbarrier full/empty)
 //   warp 1       MMA issuer: one thread issues tcgen05.mma 128xBNx16, accumulator in TMEM,
@@ -12,6 +16,8 @@
 //                SWIZZLE_128B smem staging -> TMA store (coalesced, asynchronous, clipped at the edges).
 // Reference semantics: attention.py:142-143 (_linear), :167-171 (q,k,v + rotary), :179 and :183
 // (residual adds), :182 (erf-form GELU, autodiff.py:372-382; common.cuh gelu_tanh, |err| <= 2.5e-5).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "launch.h"
 #include "../../include/wm3.h"
@@ -35,12 +41,12 @@ constexpr int GEMM_BK = 64;
 constexpr int GEMM_THREADS = 384;
 constexpr int EPI_WARP0 = 4;
 
-template <int BN>
+template <int BN, int CG = 1>
 struct GemmCfg {
-  static constexpr int STAGES = 4;
+  static constexpr int STAGES = (CG == 2) ? 6 : 4;
   static constexpr int STAGING_PER_GROUP = (BN == 256) ? 1 : 2;
   static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
-  static constexpr uint32_t B_BYTES = BN * GEMM_BK * 2;
+  static constexpr uint32_t B_BYTES = (BN / CG) * GEMM_BK * 2;  // this CTA's share of the B tile
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t STAGING_BYTES = 16384;  // 128 rows x 128 B
   static constexpr uint32_t SMEM =
@@ -101,12 +107,12 @@ DEVI void rope_chunk(const wm3_rope_t& rp, int row, int M, int col0_in_head, flo
   }
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmOut, int M, int N, int K, EpiParams ep) {
   griddep_launch_dependents();  // PDL: the next kernel may start its prologue
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, CG>;
   using Tr = EpiTraits<EPI>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int CW = Tr::CW;
@@ -126,15 +132,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // CTA pairs: cluster = (2k, 2k+1); the pair walks the tile list together, rank r owns rows [128 r, +128)
+  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
+  const int tile0 = (CG == 2) ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int tstep = (CG == 2) ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
   const int nm = ep.planes * ep.tiles_per_plane;
   const int nn = (N + BN - 1) / BN;
   const int ntiles = nm * nn;
   const int nk = (K + GEMM_BK - 1) / GEMM_BK;
-  // tile -> (plane, first row in plane, first GEMM row)
+  // tile -> (plane, this CTA's first row in the plane, its first GEMM row); a tile is CG x 128 rows
   auto tile_rows = [&](int tile, int& plane, int& r0) {
     const int mt = tile / nn;
     plane = mt / ep.tiles_per_plane;
-    r0 = (mt - plane * ep.tiles_per_plane) * GEMM_BM;
+    r0 = (mt - plane * ep.tiles_per_plane) * (GEMM_BM * CG) + static_cast<int>(rank) * GEMM_BM;
     return plane * ep.plane_rows + r0;
   };
 
@@ -148,16 +158,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
-      mbar_init(tempty_bar(a), 8);
+      mbar_init(tempty_bar(a), 8 * CG);  // every epilogue warp of the pair arrives on the leader's barrier
     }
     fence_barrier_init();
   }
   if (warp == 2) {
-    tmem_alloc(smem_u32(tmem_slot), Cfg::TMEM_COLS);
-    tmem_relinquish();
+    if (CG == 2) {
+      tmem_alloc_cg2(smem_u32(tmem_slot), Cfg::TMEM_COLS);
+      tmem_relinquish_cg2();
+    } else {
+      tmem_alloc(smem_u32(tmem_slot), Cfg::TMEM_COLS);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();  // both CTAs' barriers exist before any cross-CTA arrive / TMA completion
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   griddep_wait();  // PDL: inputs (A, residual) are complete from here on
@@ -166,29 +184,37 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int tile = tile0; tile < ntiles; tile += tstep) {
         int plane, r0;
         const int m0 = tile_rows(tile, plane, r0);
-        const int n0 = (tile % nn) * BN;
+        const int n0 = (tile % nn) * BN + static_cast<int>(rank) * (BN / CG);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sa = sbase + stage * Cfg::STAGE_BYTES;
           const uint32_t sb = sa + Cfg::A_BYTES;
-          mbar_arrive_expect_tx(full_bar(stage), Cfg::STAGE_BYTES);
-          tma_load_2d(sa, &tmA, full_bar(stage), kb * GEMM_BK, m0);
-          tma_load_2d(sb, &tmB, full_bar(stage), kb * GEMM_BK, n0);
+          if (CG == 2) {
+            // both CTAs' bytes complete on the leader's full barrier; only the leader arms it
+            const uint32_t fb = mapa_shared(full_bar(stage), 0);
+            if (rank == 0) mbar_arrive_expect_tx(full_bar(stage), 2 * Cfg::STAGE_BYTES);
+            tma_load_2d_cg2(sa, &tmA, fb, kb * GEMM_BK, m0);
+            tma_load_2d_cg2(sb, &tmB, fb, kb * GEMM_BK, n0);
+          } else {
+            mbar_arrive_expect_tx(full_bar(stage), Cfg::STAGE_BYTES);
+            tma_load_2d(sa, &tmA, full_bar(stage), kb * GEMM_BK, m0);
+            tma_load_2d(sb, &tmB, full_bar(stage), kb * GEMM_BK, n0);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc(GEMM_BM, BN, 0, 0);
+    if (lane == 0 && rank == 0) {  // the leader issues the pair's MMAs
+      constexpr uint32_t idesc = make_idesc(GEMM_BM * CG, BN, 0, 0);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t aphase = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int tile = tile0; tile < ntiles; tile += tstep) {
         mbar_wait(tempty_bar(acc), aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -201,12 +227,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int k = 0; k < GEMM_BK / 16; ++k) {
             const uint64_t ad = make_sdesc_sw128(sa + k * 32, 16, 1024);
             const uint64_t bd = make_sdesc_sw128(sb + k * 32, 16, 1024);
-            umma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            if (CG == 2)
+              umma_ss_cg2(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            else
+              umma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
           }
-          umma_commit(empty_bar(stage));
+          if (CG == 2)
+            umma_commit_mc(empty_bar(stage), 0x3);  // frees the stage in both CTAs
+          else
+            umma_commit(empty_bar(stage));
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(tfull_bar(acc));
+        if (CG == 2)
+          umma_commit_mc(tfull_bar(acc), 0x3);
+        else
+          umma_commit(tfull_bar(acc));
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
       }
@@ -220,7 +255,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int acc = 0;
     uint32_t aphase = 0;
     int sbuf = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t tempty_leader0 = (CG == 2) ? mapa_shared(tempty_bar(0), 0) : 0u;
+    for (int tile = tile0; tile < ntiles; tile += tstep) {
       int plane, r0;
       const int m0 = tile_rows(tile, plane, r0);
       const int n0 = (tile % nn) * BN;
@@ -318,46 +354,75 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty_bar(acc));
+      if (lane == 0) {
+        if (CG == 2)
+          mbar_arrive_cluster(tempty_leader0 + 8u * acc);  // the leader's MMA thread reuses the accumulator
+        else
+          mbar_arrive(tempty_bar(acc));
+      }
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }
     if (elected) bulk_wait<0>();
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();  // the pair's MMAs read this CTA's smem and write its TMEM until the last tile
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    if (CG == 2)
+      tmem_dealloc_cg2(tmem_base, Cfg::TMEM_COLS);
+    else
+      tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CG>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, int M, int N, int K,
                        const EpiParams& ep, cudaStream_t stream) {
-  using Cfg = GemmCfg<BN>;
-  auto kern = gemm_tc_kernel<BN, EPI>;
+  using Cfg = GemmCfg<BN, CG>;
+  auto kern = gemm_tc_kernel<BN, EPI, CG>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return set_error("cudaFuncSetAttribute(gemm): %s", cudaGetErrorString(e));
     attr_done = true;
   }
-  const int ntiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN);
-  const int grid = ntiles < sm_count() ? ntiles : sm_count();
-  if (launch_pdl(kern, dim3(grid), dim3(GEMM_THREADS), Cfg::SMEM, stream, ta, tb, to, M, N, K, ep)) return -1;
+  const int ntiles = ep.planes * ep.tiles_per_plane * ((N + BN - 1) / BN);
+  if (CG == 1) {
+    const int grid = ntiles < sm_count() ? ntiles : sm_count();
+    if (launch_pdl(kern, dim3(grid), dim3(GEMM_THREADS), Cfg::SMEM, stream, ta, tb, to, M, N, K, ep)) return -1;
+    return check_launch("gemm_tc_kernel");
+  }
+  const int pairs = (ntiles < sm_count() / 2) ? ntiles : sm_count() / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, to, M, N, K, ep);
+  if (e != cudaSuccess) return set_error("gemm_tc_kernel (pair) launch: %s", cudaGetErrorString(e));
   return check_launch("gemm_tc_kernel");
 }
 
-template <int BN>
+template <int BN, int CG>
 static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, int M, int N,
                         int K, const EpiParams& ep, cudaStream_t s) {
   switch (epi) {
-    case WM3_EPI_F32: return launch_gemm<BN, WM3_EPI_F32>(ta, tb, to, M, N, K, ep, s);
-    case WM3_EPI_BIAS_BF16: return launch_gemm<BN, WM3_EPI_BIAS_BF16>(ta, tb, to, M, N, K, ep, s);
-    case WM3_EPI_BIAS_GELU_BF16: return launch_gemm<BN, WM3_EPI_BIAS_GELU_BF16>(ta, tb, to, M, N, K, ep, s);
-    case WM3_EPI_BIAS_RESID_F32: return launch_gemm<BN, WM3_EPI_BIAS_RESID_F32>(ta, tb, to, M, N, K, ep, s);
-    case WM3_EPI_QKV_ROPE: return launch_gemm<BN, WM3_EPI_QKV_ROPE>(ta, tb, to, M, N, K, ep, s);
+    case WM3_EPI_F32: return launch_gemm<BN, WM3_EPI_F32, CG>(ta, tb, to, M, N, K, ep, s);
+    case WM3_EPI_BIAS_BF16: return launch_gemm<BN, WM3_EPI_BIAS_BF16, CG>(ta, tb, to, M, N, K, ep, s);
+    case WM3_EPI_BIAS_GELU_BF16: return launch_gemm<BN, WM3_EPI_BIAS_GELU_BF16, CG>(ta, tb, to, M, N, K, ep, s);
+    case WM3_EPI_BIAS_RESID_F32: return launch_gemm<BN, WM3_EPI_BIAS_RESID_F32, CG>(ta, tb, to, M, N, K, ep, s);
+    case WM3_EPI_QKV_ROPE: return launch_gemm<BN, WM3_EPI_QKV_ROPE, CG>(ta, tb, to, M, N, K, ep, s);
     default: return set_error("wm3_linear: unknown epilogue %d", epi);
   }
 }
@@ -394,16 +459,25 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
   ep.n_valid = n_valid;
   ep.plane_rows = op.plane_rows;
   ep.planes = op.planes;
-  ep.tiles_per_plane = (op.plane_rows + GEMM_BM - 1) / GEMM_BM;
+  const int bn = (n >= 256) ? 256 : 128;
+  // CTA pairs for the wide GEMMs (WM3_GEMM_CG=1 forces single-CTA tiles: A/B aid)
+  static const int cg_env = [] {
+    const char* e = getenv("WM3_GEMM_CG");
+    return e ? atoi(e) : 2;
+  }();
+  // the short-K residual GEMM (O-proj, K = 1024) is HBM-latency bound in its epilogue and measured faster as
+  // single-CTA tiles (0.227 vs 0.241 ms in-block); every other wide GEMM is faster as pairs
+  const bool short_resid = (epi == WM3_EPI_BIAS_RESID_F32 && k <= 1024);
+  const int cg = (bn == 256 && cg_env == 2 && !short_resid) ? 2 : 1;
+  ep.tiles_per_plane = (op.plane_rows + GEMM_BM * cg - 1) / (GEMM_BM * cg);
   if (epi == WM3_EPI_QKV_ROPE) {
     if (rope == nullptr) return set_error("wm3_linear: rope descriptor required");
     ep.rope = *rope;
     if (ep.rope.dhp != 64 && ep.rope.dhp != 128) return set_error("wm3_linear: dhp must be 64 or 128");
   }
-  const int bn = (n >= 256) ? 256 : 128;
   CUtensorMap ta, tb, to;
   if (make_tmap_2d_bf16(&ta, a, k, m, lda, GEMM_BK, GEMM_BM)) return -1;
-  if (make_tmap_2d_bf16(&tb, b, k, n, ldb, GEMM_BK, bn)) return -1;
+  if (make_tmap_2d_bf16(&tb, b, k, n, ldb, GEMM_BK, bn / cg)) return -1;  // each CTA of a pair loads half
   {
     const int cw = f32_out ? 32 : 64;
     const size_t esz = f32_out ? 4 : 2;
@@ -415,8 +489,10 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
     if (make_tmap(&to, base, f32_out ? TMAP_F32 : TMAP_BF16, 3, dims, strides, box, nullptr)) return -1;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  return bn == 256 ? dispatch_epi<256>(epi, ta, tb, to, m, n, k, ep, s)
-                   : dispatch_epi<128>(epi, ta, tb, to, m, n, k, ep, s);
+  if (bn == 256)
+    return cg == 2 ? dispatch_epi<256, 2>(epi, ta, tb, to, m, n, k, ep, s)
+                   : dispatch_epi<256, 1>(epi, ta, tb, to, m, n, k, ep, s);
+  return dispatch_epi<128, 1>(epi, ta, tb, to, m, n, k, ep, s);
 }
 
 }  // namespace wm3
