@@ -41,10 +41,14 @@ constexpr int GEMM_BK = 64;
 constexpr int GEMM_THREADS = 384;
 constexpr int EPI_WARP0 = 4;
 
+#ifndef WM3_PAIR_STAGING
+#define WM3_PAIR_STAGING 1
+#endif
 template <int BN, int CG = 1>
 struct GemmCfg {
-  static constexpr int STAGES = (CG == 2) ? 6 : 4;
-  static constexpr int STAGING_PER_GROUP = (BN == 256) ? 1 : 2;
+  // CTA pairs free 16 KB per stage: 6 stages, or 5 stages with double-buffered epilogue staging
+  static constexpr int STAGES = (CG == 2) ? (WM3_PAIR_STAGING == 2 ? 5 : 6) : 4;
+  static constexpr int STAGING_PER_GROUP = (BN == 256) ? ((CG == 2) ? WM3_PAIR_STAGING : 1) : 2;
   static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
   static constexpr uint32_t B_BYTES = (BN / CG) * GEMM_BK * 2;  // this CTA's share of the B tile
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
