@@ -388,22 +388,38 @@ def run_gpu(args, world, rank, local_rank):
     x_host.copy_(x.cpu())
     y_host = torch.empty_like(x_host).pin_memory()
     xd = torch.empty_like(x)
+    e_steps = max(3, min(args.steps, 10))
     if world == 1:
-        # the public operator (attention.natten_block, reference signature): host tokens in, new tensor out
-        from paper_2503_22235_b200.attention import natten_block
-
-        def e2e_step():
-            out = natten_block(x_host, params, "blk", EXT, WIN, HEADS)
-            y_host.copy_(out.device, non_blocking=True)
+        # the public serving operator (attention.NattenBlockStream): page-locked host batches in and out, the
+        # uploads / downloads of neighbouring batches overlapped with the block on separate CUDA streams
+        from paper_2503_22235_b200.attention import NattenBlockStream
+        runner = NattenBlockStream(params, "blk", EXT, WIN, HEADS, DIM)
+        hin = [x_host, torch.empty_like(x_host).pin_memory()]
+        hin[1].copy_(x_host)
+        hout = [y_host, torch.empty_like(y_host).pin_memory()]
+        for i in range(2):
+            runner.submit(hin[i], hout[i])
+        runner.synchronize()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(runner.s_in)
+        for i in range(e_steps):
+            runner.submit(hin[i & 1], hout[i & 1])
+        e1.record(runner.s_out)
+        runner.synchronize()
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1)
+        e2e_api = ("attention.NattenBlockStream: page-locked host batches, H2D / block / D2H on three CUDA "
+                   "streams, neighbouring batches' transfers overlapped")
     else:
         def e2e_step():
             xd.copy_(x_host, non_blocking=True)
             block_forward(xd, bw, ws, rope, local, WIN, row0=me.row0, rows_global=EXT[1], halo_exchange=exch)
             y_host.copy_(xd, non_blocking=True)
 
-    e2e_step()
-    e_steps = max(3, min(args.steps, 10))
-    e_ms = timed(e2e_step, e_steps, stream, world)
+        e2e_step()
+        e_ms = timed(e2e_step, e_steps, stream, world)
+        e2e_api = "band block_forward with pinned host copies of the band"
     e2e_value = flops * e_steps / (e_ms / 1e3) / 1e12
     clk.__exit__(None, None, None)
 
@@ -429,8 +445,7 @@ def run_gpu(args, world, rank, local_rank):
                        "band_rows_rank0": me.rows},
             "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": int(x.numel() * 4),
                     "d2h_bytes_per_step": int(x.numel() * 4), "ms_per_step": e_ms / e_steps,
-                    "api": ("attention.natten_block(pinned fp32 host tokens) -> pinned host copy" if world == 1
-                            else "band block_forward with pinned host copies of the band")},
+                    "api": e2e_api},
             "gpu_launches": 7 * args.steps,
             "roofline": roof,
             "kernels": table,

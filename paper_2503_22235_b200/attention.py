@@ -19,8 +19,8 @@ from .params import block_param_names, init_block_params  # noqa: F401  (re-expo
 from .runtime import CACHE
 from .tensor import Tensor, host_array
 
-__all__ = ["natten_block", "attention_weights", "rotary_tables", "apply_rotary", "init_block_params",
-           "block_param_names", "to_device_f32", "validate_block_args"]
+__all__ = ["natten_block", "NattenBlockStream", "attention_weights", "rotary_tables", "apply_rotary",
+           "init_block_params", "block_param_names", "to_device_f32", "validate_block_args"]
 
 
 def to_device_f32(x) -> torch.Tensor:
@@ -64,6 +64,55 @@ def natten_block(x, params: dict, prefix: str, extents, window, heads: int) -> T
     block_forward(xd, bw, CACHE.workspace(extents, window, bw), CACHE.rope(extents, dh), tuple(extents),
                   tuple(window))
     return Tensor(device=xd)
+
+
+class NattenBlockStream:
+    """natten_block over a stream of host token batches, with the transfers overlapped (serving path).
+
+    `submit(host_in, host_out)` takes page-locked float32 (T, dim) host tensors and returns at once: the batch is
+    copied host->device on one CUDA stream, the block runs on a second, the result is copied device->host on a
+    third, so batch i+1's upload and batch i-1's download run under batch i's compute (both PCIe directions at
+    once).  Two device buffers alternate; `synchronize()` waits for everything submitted.  Each batch's result
+    equals natten_block(host_in, ...) bitwise (same kernels, same inputs)."""
+
+    def __init__(self, params: dict, prefix: str, extents, window, heads: int, dim: int):
+        t = int(np.prod(extents))
+        self.dh = validate_block_args((t, dim), extents, window, heads)
+        self.extents, self.window = tuple(int(e) for e in extents), tuple(int(e) for e in window)
+        self.bw = CACHE.block(params, prefix, heads)
+        self.ws = CACHE.workspace(self.extents, self.window, self.bw, tag="stream")
+        self.rope = CACHE.rope(self.extents, self.dh)
+        self.buf = [torch.empty((t, dim), dtype=torch.float32, device="cuda") for _ in range(2)]
+        self.s_in, self.s_run, self.s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        self.uploaded = [torch.cuda.Event() for _ in range(2)]
+        self.computed = [torch.cuda.Event() for _ in range(2)]
+        self.downloaded = [None, None]
+        self.i = 0
+
+    def submit(self, host_in: torch.Tensor, host_out: torch.Tensor) -> None:
+        from .blocks import block_forward
+        b = self.i & 1
+        self.i += 1
+        dev = self.buf[b]
+        with torch.cuda.stream(self.s_in):
+            if self.downloaded[b] is not None:  # the download of the batch that last used this buffer
+                self.s_in.wait_event(self.downloaded[b])
+            dev.copy_(host_in, non_blocking=True)
+            self.uploaded[b].record(self.s_in)
+        with torch.cuda.stream(self.s_run):
+            self.s_run.wait_event(self.uploaded[b])
+            block_forward(dev, self.bw, self.ws, self.rope, self.extents, self.window)
+            self.computed[b].record(self.s_run)
+        with torch.cuda.stream(self.s_out):
+            self.s_out.wait_event(self.computed[b])
+            host_out.copy_(dev, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.s_out)
+            self.downloaded[b] = ev
+
+    def synchronize(self) -> None:
+        for s in (self.s_in, self.s_run, self.s_out):
+            s.synchronize()
 
 
 def attention_weights(x_values, params: dict, prefix: str, extents, window, heads: int) -> np.ndarray:

@@ -100,3 +100,22 @@ def test_block_errors_before_launch():
         _api().natten_block(x, params, "blk", (2, 7, 10), (1, 3, 3), 5)
     with pytest.raises(ConfigError):
         _api().natten_block(x[:100], params, "blk", (2, 7, 10), (1, 3, 3), 4)
+
+
+def test_natten_block_stream_matches_operator():
+    """The overlapped serving path returns, per batch, exactly natten_block's result."""
+    import torch
+    from paper_2503_22235_b200.attention import NattenBlockStream, natten_block
+    from paper_2503_22235_b200.params import init_block_params
+    ext, win, dim, heads = (5, 18, 36), (5, 7, 7), 256, 2
+    params = init_block_params(np.random.default_rng(3), dim, heads, "blk", zero_residual=False)
+    t = int(np.prod(ext))
+    xs = [torch.randn(t, dim).pin_memory() for _ in range(3)]
+    outs = [torch.empty(t, dim).pin_memory() for _ in range(3)]
+    runner = NattenBlockStream(params, "blk", ext, win, heads, dim)
+    for xi, oi in zip(xs, outs):
+        runner.submit(xi, oi)
+    runner.synchronize()
+    for xi, oi in zip(xs, outs):
+        ref = natten_block(xi, params, "blk", ext, win, heads).device.cpu()
+        assert torch.equal(oi, ref)
