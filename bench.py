@@ -331,12 +331,25 @@ def run_forecast(args, world: int = 1) -> dict:
         torch.cuda.synchronize()
         ens_s = time.perf_counter() - t0
         spread = float(np.std([h[0][0].numpy().mean() for h in hosts]))
+        # device verification of the ensemble (evaluation.ensemble_curve on the decoded fields in HBM):
+        # leading-k ensemble-mean RMSE / blur of surface variable 0 against the unperturbed forecast
+        from paper_2503_22235_b200 import evaluation as EV
+        ctrl = forecast(state, dt, params, cfg)
+        members_dev = torch.stack([o.surface.device[0] for o in outs])[:, None]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        curve = EV.ensemble_curve(members_dev, ctrl.surface.device[0][None], cfg.grid, wavelength_km=2000.0)
+        torch.cuda.synchronize()
+        t_curve = time.perf_counter() - t0
         res["ensemble"] = {"members": args.ensemble, "seconds": round(ens_s, 4),
                            "seconds_per_member": round(ens_s / args.ensemble, 4),
                            "block_tflop": round(tf_blocks * args.ensemble, 1),
                            "outputs_finite": bool(all(np.isfinite(a.numpy()).all() and np.isfinite(b.numpy()).all()
                                                       for a, b in hosts)),
                            "member_spread_sfc0_mean": spread,
+                           "curve_vs_control_sfc0": [{k: (round(v, 6) if isinstance(v, float) else v)
+                                                      for k, v in r.items()} for r in curve],
+                           "curve_seconds": round(t_curve, 4),
                            "note": "perturbed_members(scale=0.01); batched rollout_ensemble; host fields in/out"}
     return res
 
