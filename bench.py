@@ -43,6 +43,9 @@ WIN = (5, 7, 7)
 DIM, HEADS = 1024, 8
 SAMPLE_EXT = (5, 18, 36)
 METRIC = "3D NATTEN block TFLOP/s"
+# N > 1: WM3_FUSED_HALO=1 moves the K/V halo rows in the QKV GEMM epilogue over peer memory (bands.PeerHalo)
+# for the banded forecast; default is the NCCL point-to-point exchange (bands.HaloExchanger)
+FUSED_HALO = os.environ.get("WM3_FUSED_HALO", "0") == "1"
 KERNELS = ["layernorm1", "qkv_rope_gemm", "natten", "oproj_resid_gemm", "layernorm2", "w1_gelu_gemm",
            "w2_resid_gemm"]
 
@@ -267,7 +270,7 @@ def run_forecast(args, world: int = 1) -> dict:
         if world == 1:
             return R.forecast(state, dt, params, cfg)
         lat = M.encode(state, params, cfg)
-        lat = rollout_banded(lat, R.greedy_plan(dt, cfg.max_dt), params, cfg)
+        lat = rollout_banded(lat, R.greedy_plan(dt, cfg.max_dt), params, cfg, fused=FUSED_HALO)
         return M.decode(lat, params, cfg)
 
     def sync_max(sec: float) -> float:
@@ -454,7 +457,9 @@ def run_gpu(args, world, rank, local_rank):
                        "tokens": int(np.prod(EXT)), "block_tflop": round(flops / 1e12, 4), "residual": "fp32",
                        "operands": "fp16 tensor-core operands, fp32 accumulate / residual / softmax",
                        "l2": "inputs larger than L2 (332 MB fp32 latent), no flush",
-                       "parallelism": f"latitude bands x{world} (NCCL halo)" if world > 1 else "single GPU",
+                       "parallelism": (f"latitude bands x{world} ("
+                                       + ("fused QKV-epilogue peer-memory halo" if FUSED_HALO else "NCCL halo")
+                                       + ")") if world > 1 else "single GPU",
                        "band_rows_rank0": me.rows},
             "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": int(x.numel() * 4),
                     "d2h_bytes_per_step": int(x.numel() * 4), "ms_per_step": e_ms / e_steps,

@@ -75,6 +75,33 @@ int wm3_linear_planes(const void* a, int lda, const void* b, int ldb, int m, int
                       void* out, int ldo, int n_valid, const float* bias, const wm3_rope_t* rope,
                       int planes, int plane_rows, long long plane_stride, int row_off, void* stream);
 
+/* Fused halo exchange for latitude bands (the QKV GEMM epilogue stores a band's boundary K/V rows straight
+ * into the neighbouring ranks' K/V grids over NVLink peer memory; no separate collective).
+ * For GEMM plane p and plane-row r (band row * cols + col) with column block n >= col_lo:
+ *   r <  n_up           -> up[(p * up_plane_stride + up_row_off + r) * ld + n]
+ *   r >= plane_rows - n_dn -> dn[(p * dn_plane_stride + dn_row_off + r - (plane_rows - n_dn)) * ld + n]
+ * up / dn may be null (no neighbour).  Pointers are peer-mapped device addresses (CUDA IPC); the stores are
+ * followed by a system-scope fence in the kernel, and wm3_halo_signal / wm3_halo_wait order them against the
+ * neighbours' attention kernels (monotonic epoch flags, one int32 per direction and purpose). */
+typedef struct {
+  void* up;
+  void* dn;
+  int n_up, n_dn;                  /* plane-rows sent to each neighbour */
+  long long up_plane_stride, dn_plane_stride;
+  long long up_row_off, dn_row_off;
+  int ld;                          /* destination row pitch (elements) */
+  int col_lo;                      /* first column sent (K and V sections only) */
+} wm3_halo_t;
+
+int wm3_linear_planes_halo(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi, void* out,
+                           int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, int planes,
+                           int plane_rows, long long plane_stride, int row_off, const wm3_halo_t* halo,
+                           void* stream);
+/* Release-store `epoch` to each non-null peer flag (system scope), after a system fence. */
+int wm3_halo_signal(int* peer_flag_a, int* peer_flag_b, int epoch, void* stream);
+/* Spin (acquire, system scope) until each of the n local flags is >= epoch; traps after ~10 s. */
+int wm3_halo_wait(const int* flags, int n, int epoch, void* stream);
+
 /* Fused 3D neighborhood attention forward, over `batch` independent latents (ensemble members).
  * qkv: bf16 K/V grid [batch * depth][rows_ext][cols][ldqkv] (member b owns depth planes [b * depth, (b + 1) * depth);
  *      windows never cross members), token channels [3][heads][dhp]; rows_ext =

@@ -35,6 +35,12 @@ class RopeT(ctypes.Structure):
     _fields_ = [("pairs", _vp), ("heads", _i), ("dhp", _i), ("period", _i)]
 
 
+class HaloT(ctypes.Structure):
+    """wm3_halo_t (include/wm3.h)."""
+    _fields_ = [("up", _vp), ("dn", _vp), ("n_up", _i), ("n_dn", _i), ("up_plane_stride", _ll),
+                ("dn_plane_stride", _ll), ("up_row_off", _ll), ("dn_row_off", _ll), ("ld", _i), ("col_lo", _i)]
+
+
 # name -> argtypes; every function returns int status
 SIGNATURES = {
     "wm3_neighbor_table": [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp],
@@ -42,6 +48,10 @@ SIGNATURES = {
     "wm3_linear": [_vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, ctypes.POINTER(RopeT), _vp],
     "wm3_linear_planes": [_vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, ctypes.POINTER(RopeT),
                           _i, _i, ctypes.c_longlong, _i, _vp],
+    "wm3_linear_planes_halo": [_vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, ctypes.POINTER(RopeT),
+                               _i, _i, ctypes.c_longlong, _i, ctypes.POINTER(HaloT), _vp],
+    "wm3_halo_signal": [_vp, _vp, _i, _vp],
+    "wm3_halo_wait": [_vp, _i, _i, _vp],
     "wm3_natten_fwd": [_vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _f, _vp],
     "wm3_natten_windows": [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp],
     "wm3_conv_bn": [_i],

@@ -138,6 +138,108 @@ def copy_halos(bands: list[Band], workspaces: list) -> None:
             me[:, b.halo_lo + b.rows:] = src[:, dn.halo_lo:dn.halo_lo + b.halo_hi]
 
 
+def halo_descriptor(me: int, bands: list[Band], grids: list, qkv_ptrs: list, cols: int, sec: int):
+    """wm3_halo_t for band `me`: its first halo_hi[up] rows go to the bottom halo of the band above, its last
+    halo_lo[down] rows to the top halo of the band below (same rows HaloExchanger / copy_halos move).
+    grids[i] / qkv_ptrs[i]: K/V grid geometry and device (or peer-mapped) address of band i; sec = first
+    column of the K section (q is not needed by neighbours)."""
+    from . import _lib
+    h = _lib.HaloT()
+    h.ld = grids[me].qkv_ld
+    h.col_lo = sec
+    if me > 0 and bands[me - 1].halo_hi:
+        up, gu = bands[me - 1], grids[me - 1]
+        h.up = qkv_ptrs[me - 1]
+        h.n_up = up.halo_hi * cols
+        h.up_plane_stride = gu.rows_ext * cols
+        h.up_row_off = (up.halo_lo + up.rows) * cols
+    if me + 1 < len(bands) and bands[me + 1].halo_lo:
+        dn, gd = bands[me + 1], grids[me + 1]
+        h.dn = qkv_ptrs[me + 1]
+        h.n_dn = dn.halo_lo * cols
+        h.dn_plane_stride = gd.rows_ext * cols
+        h.dn_row_off = 0
+    return h
+
+
+class PeerHalo:
+    """Fused halo exchange across ranks: every rank's K/V grid and a 4-word epoch-flag block are shared with its
+    neighbours through CUDA IPC (torch's CUDA tensor reductions, handles exchanged over the process group), the
+    QKV epilogue writes boundary rows straight into the neighbours' grids over NVLink, and per block:
+        wait  consumed(e-1) from both neighbours   (their attention no longer reads the halo rows we overwrite)
+        QKV GEMM with peer stores  -> signal ready(e) to both neighbours -> wait ready(e) from both
+        attention -> signal consumed(e) to both neighbours
+    Flags (int32, monotonic epochs) in each rank's block: [ready_from_up, ready_from_dn, consumed_from_up,
+    consumed_from_dn]; a missing neighbour's flags start at INT32_MAX so its waits pass."""
+
+    def __init__(self, bands: list[Band], rank: int, qkv: torch.Tensor, grid, group=None):
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.bands, self.rank = bands, rank
+        n = len(bands)
+        big = 2 ** 31 - 1
+        self.flags = torch.zeros(4, dtype=torch.int32, device=qkv.device)
+        if rank == 0:
+            self.flags[0] = big
+            self.flags[2] = big
+        if rank == n - 1:
+            self.flags[1] = big
+            self.flags[3] = big
+        torch.cuda.synchronize()
+        mine = (reduce_tensor(qkv), reduce_tensor(self.flags),
+                {"rows_ext": grid.rows_ext, "qkv_ld": qkv.stride(0)})
+        allv = [None] * n
+        dist.all_gather_object(allv, mine, group=group)
+        self.peer_qkv, self.peer_flags, self.geo = {}, {}, {}
+        for r in (rank - 1, rank + 1):
+            if 0 <= r < n:
+                fq, aq = allv[r][0]
+                ff, af = allv[r][1]
+                self.peer_qkv[r] = fq(*aq)      # peer-mapped views (keep the objects alive)
+                self.peer_flags[r] = ff(*af)
+                self.geo[r] = allv[r][2]
+        self.epoch = 0
+        self.qkv_ld = qkv.stride(0)
+
+    def descriptor(self, grid, cols: int, sec: int):
+        """wm3_halo_t pointing at the neighbours' peer-mapped K/V grids."""
+        class _G:
+            def __init__(self, rows_ext, qkv_ld):
+                self.rows_ext, self.qkv_ld = rows_ext, qkv_ld
+        grids = [None] * len(self.bands)
+        ptrs = [None] * len(self.bands)
+        for r, t in self.peer_qkv.items():
+            grids[r] = _G(self.geo[r]["rows_ext"], self.geo[r]["qkv_ld"])
+            ptrs[r] = t.data_ptr()
+        grids[self.rank] = _G(grid.rows_ext, self.qkv_ld)
+        return halo_descriptor(self.rank, self.bands, grids, ptrs, cols, sec)
+
+    def _signal(self, idx_in_up: int, idx_in_dn: int, epoch: int) -> None:
+        from . import _lib
+        up = self.peer_flags.get(self.rank - 1)
+        dn = self.peer_flags.get(self.rank + 1)
+        a = None if up is None else up.data_ptr() + 4 * idx_in_up
+        b = None if dn is None else dn.data_ptr() + 4 * idx_in_dn
+        _lib.check(_lib.lib().wm3_halo_signal(a, b, int(epoch), _lib.stream_ptr()), "wm3_halo_signal")
+
+    def _wait(self, first: int, epoch: int) -> None:
+        from . import _lib
+        _lib.check(_lib.lib().wm3_halo_wait(self.flags.data_ptr() + 4 * first, 2, int(epoch), _lib.stream_ptr()),
+                   "wm3_halo_wait")
+
+    def before_qkv(self) -> None:
+        self.epoch += 1
+        self._wait(2, self.epoch - 1)          # consumed flags of the previous block
+
+    def after_qkv(self) -> None:
+        # my rows are in the band above's "ready_from_dn" slot and the band below's "ready_from_up" slot
+        self._signal(1, 0, self.epoch)
+        self._wait(0, self.epoch)
+
+    def after_attention(self) -> None:
+        self._signal(3, 2, self.epoch)
+
+
 class BandedProcessor:
     """Processor blocks over latitude bands: for each block, LN1 + QKV (into each band's halo'd K/V grid)
     for every held band, the halo exchange, then attention and the rest of the block per band.
@@ -146,11 +248,15 @@ class BandedProcessor:
     HaloExchanger over NCCL / gloo), or every band when one process emulates the split on one GPU
     (exchange = copy_halos).  Kernels never wait on one another either way."""
 
-    def __init__(self, params: dict, cfg, bands: list[Band], held: list[int], exchanger=None):
+    def __init__(self, params: dict, cfg, bands: list[Band], held: list[int], exchanger=None, fused: bool = False):
+        """fused: halo rows travel in the QKV GEMM epilogue (peer stores) instead of a separate exchange —
+        between the held bands' own grids when emulating, through PeerHalo (`exchanger`) across ranks."""
         from .runtime import CACHE
         self.params, self.cfg, self.bands = params, cfg, bands
         self.held = [bands[i] for i in held]
+        self.held_idx = list(held)
         self.exchanger = exchanger
+        self.fused = fused
         d, h, w = cfg.latent_extents
         self.rope = CACHE.rope(cfg.latent_extents, cfg.head_dim)
         self.local = [(d, b.rows, w) for b in self.held]
@@ -167,14 +273,37 @@ class BandedProcessor:
         from .runtime import CACHE
         cfg = self.cfg
         h = cfg.latent_extents[1]
+        cols = cfg.latent_extents[2]
         for i in range(cfg.proc_blocks):
             bw = CACHE.block(self.params, f"proc{horizon}.blk{i}", cfg.heads)
             wss = self._ws(bw)
-            for b, ext, xb, ws in zip(self.held, self.local, xs, wss):
+            sec = bw.heads * bw.dhp
+            peer = self.exchanger if (self.fused and isinstance(self.exchanger, PeerHalo)) else None
+            if peer is not None:
+                peer.before_qkv()
+            for j, (b, ext, xb, ws) in enumerate(zip(self.held, self.local, xs, wss)):
                 ops.layernorm_bf16(xb, bw.ln1_g, bw.ln1_b, out=ws.hn)
+                halo = None
+                if self.fused:
+                    if peer is not None:
+                        halo = peer.descriptor(ws.grid, cols, sec)
+                    else:  # emulation: the neighbours are the other held bands' grids on this GPU
+                        class _G:
+                            pass
+                        grids = []
+                        for w_ in wss:
+                            g_ = _G()
+                            g_.rows_ext, g_.qkv_ld = w_.grid.rows_ext, w_.qkv.stride(0)
+                            grids.append(g_)
+                        halo = halo_descriptor(self.held_idx[j], self.held, grids,
+                                               [w_.qkv.data_ptr() for w_ in wss], cols, sec)
                 ops.linear_grid(ws.hn, bw.w_qkv, _lib.WM3_EPI_QKV_ROPE, bw.b_qkv, ws.qkv, ws.grid,
-                                rope=self.rope.struct(ext, b.row0, bw.heads, bw.dhp))
-            if self.exchanger is not None:
+                                rope=self.rope.struct(ext, b.row0, bw.heads, bw.dhp), halo=halo)
+            if peer is not None:
+                peer.after_qkv()
+            elif self.fused:
+                pass  # emulation: stream order already puts every band's halo stores before any attention
+            elif self.exchanger is not None:
                 for ws in wss:
                     self.exchanger(ws.qkv, ws.grid)
             else:
@@ -182,19 +311,23 @@ class BandedProcessor:
             for b, xb, ws in zip(self.held, xs, wss):
                 ops.natten(ws.qkv, ws.grid, bw.heads, bw.dhp, bw.dh, cfg.window, out=ws.ctx, rows_global=h,
                            row0=b.row0)
+                if peer is not None:
+                    peer.after_attention()  # neighbours may overwrite our halo rows for the next block
                 ops.linear(ws.ctx, bw.w_o, _lib.WM3_EPI_BIAS_RESID_F32, bias=bw.b_o, out=xb, n_valid=bw.hidden)
                 ops.layernorm_bf16(xb, bw.ln2_g, bw.ln2_b, out=ws.hn)
                 ops.linear(ws.hn, bw.w_1, _lib.WM3_EPI_BIAS_GELU_BF16, bias=bw.b_1, out=ws.mid)
                 ops.linear(ws.mid, bw.w_2, _lib.WM3_EPI_BIAS_RESID_F32, bias=bw.b_2, out=xb, n_valid=bw.hidden)
 
 
-def rollout_banded(lat, plan, params: dict, cfg, world: int | None = None, group=None):
+def rollout_banded(lat, plan, params: dict, cfg, world: int | None = None, group=None, fused: bool = False):
     """rollout() with the latent split into latitude bands.
 
     Under an initialised torch.distributed group of size N > 1 (and world None): rank r keeps band r, halos
     move over the group (NCCL over NVLink on B200), and the bands are all-gathered at the end so every rank
     returns the full latent.  With `world` given and no group, one process emulates `world` bands on its GPU
-    (the same kernels and halo rows; used to verify the split on one device).  Validation as rollout()."""
+    (the same kernels and halo rows; used to verify the split on one device).  fused=True moves the halo rows
+    in the QKV GEMM epilogue (peer stores into the neighbours' K/V grids, PeerHalo epoch flags across ranks)
+    instead of a separate exchange.  Validation as rollout()."""
     import torch.distributed as dist
 
     from .model import CALL_COUNTS, LatentState, _tokens
@@ -214,10 +347,18 @@ def rollout_banded(lat, plan, params: dict, cfg, world: int | None = None, group
     bands = plan_bands(h, cfg.window[1], n)
     if distributed:
         rank = dist.get_rank(group)
-        proc = BandedProcessor(params, cfg, bands, [rank], HaloExchanger(bands, rank, group))
+        if fused:
+            from .runtime import CACHE
+            me = bands[rank]
+            bw0 = CACHE.block(params, f"proc{plan[0]}.blk0", cfg.heads)
+            ws0 = CACHE.workspace((d, me.rows, w), cfg.window, bw0, halo=(me.halo_lo, me.halo_hi), tag=f"band{rank}")
+            exch = PeerHalo(bands, rank, ws0.qkv, ws0.grid, group)
+        else:
+            exch = HaloExchanger(bands, rank, group)
+        proc = BandedProcessor(params, cfg, bands, [rank], exch, fused=fused)
         xs = [local_band_tokens(x, cfg.latent_extents, bands[rank]).clone()]
     else:
-        proc = BandedProcessor(params, cfg, bands, list(range(n)))
+        proc = BandedProcessor(params, cfg, bands, list(range(n)), fused=fused)
         xs = [local_band_tokens(x, cfg.latent_extents, b).clone() for b in bands]
     for hz in plan:
         proc.process(xs, hz)

@@ -34,6 +34,8 @@ struct EpiParams {
   // is one clipped TMA box store at (n, r0, plane) of the (n, row, plane) output map.
   int plane_rows, planes, tiles_per_plane;
   wm3_rope_t rope;
+  wm3_halo_t halo;  // QKV epilogue: boundary rows also stored into the neighbours' K/V grids (peer memory)
+  int has_halo;
 };
 
 constexpr int GEMM_BM = 128;
@@ -265,7 +267,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int m0 = tile_rows(tile, plane, r0);
       const int n0 = (tile % nn) * BN;
       const int row = m0 + r_in_tile;
-      const bool row_ok = (r0 + r_in_tile < ep.plane_rows) && row < M;
+      const int prow = r0 + r_in_tile;  // row within the plane
+      const bool row_ok = (prow < ep.plane_rows) && row < M;
       // residual prefetch, RESID_DEPTH chunks of this group ahead: the first ones overlap the mainloop wait
       // (the residual epilogue is HBM-latency bound: more bytes in flight per thread)
 #ifndef WM3_RESID_DEPTH
@@ -340,6 +343,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           uint32_t pk[32];
 #pragma unroll
           for (int e = 0; e < 32; ++e) pk[e] = pack_elem(v[2 * e], v[2 * e + 1]);
+          if (EPI == WM3_EPI_QKV_ROPE && ep.has_halo && row_ok && n >= ep.halo.col_lo) {
+            // fused halo exchange: this row's 64 columns also go to a neighbour's K/V grid over NVLink
+            const int r = prow;
+            elem_t* dst = nullptr;
+            if (ep.halo.up != nullptr && r < ep.halo.n_up)
+              dst = static_cast<elem_t*>(ep.halo.up) +
+                    (plane * ep.halo.up_plane_stride + ep.halo.up_row_off + r) * ep.halo.ld + n;
+            else if (ep.halo.dn != nullptr && r >= ep.plane_rows - ep.halo.n_dn)
+              dst = static_cast<elem_t*>(ep.halo.dn) +
+                    (plane * ep.halo.dn_plane_stride + ep.halo.dn_row_off + (r - (ep.plane_rows - ep.halo.n_dn))) *
+                        ep.halo.ld + n;
+            if (dst != nullptr) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                uint32_t w[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) w[e] = pk[8 * q + e];
+                stg256(dst + 16 * q, w);
+              }
+            }
+          }
           if (elected) bulk_wait_read<Cfg::STAGING_PER_GROUP - 1>();
           named_bar_sync(bar_id, 128);
           const uint32_t st = staging0 + (g * Cfg::STAGING_PER_GROUP + sbuf) * Cfg::STAGING_BYTES;
@@ -368,6 +392,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (acc == 0) aphase ^= 1;
     }
     if (elected) bulk_wait<0>();
+    if (EPI == WM3_EPI_QKV_ROPE && ep.has_halo) __threadfence_system();  // peer halo rows visible system-wide
   }
   tc_fence_before();
   if (CG == 2)
@@ -439,7 +464,7 @@ struct OutPlanes {
 
 static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi, void* out,
                        int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, const OutPlanes& op,
-                       void* stream) {
+                       void* stream, const wm3_halo_t* halo = nullptr) {
   if (m <= 0 || n <= 0 || k <= 0) return set_error("wm3_linear: bad sizes m=%d n=%d k=%d", m, n, k);
   const bool f32_out = (epi == WM3_EPI_F32 || epi == WM3_EPI_BIAS_RESID_F32);
   if ((lda % 8) || (ldb % 8) || (ldo % (f32_out ? 4 : 8)))
@@ -474,6 +499,15 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
   const bool short_resid = (epi == WM3_EPI_BIAS_RESID_F32 && k <= 1024);
   const int cg = (bn == 256 && cg_env == 2 && !short_resid) ? 2 : 1;
   ep.tiles_per_plane = (op.plane_rows + GEMM_BM * cg - 1) / (GEMM_BM * cg);
+  if (halo != nullptr) {
+    if (epi != WM3_EPI_QKV_ROPE) return set_error("wm3_linear: halo stores need the QKV epilogue");
+    if ((halo->ld % 16) || (halo->col_lo % 64) || halo->n_up < 0 || halo->n_dn < 0 ||
+        halo->n_up > op.plane_rows || halo->n_dn > op.plane_rows ||
+        (reinterpret_cast<uintptr_t>(halo->up) % 32) || (reinterpret_cast<uintptr_t>(halo->dn) % 32))
+      return set_error("wm3_linear: bad halo descriptor (ld %% 16, col_lo %% 64, row counts, 32 B alignment)");
+    ep.halo = *halo;
+    ep.has_halo = 1;
+  }
   if (epi == WM3_EPI_QKV_ROPE) {
     if (rope == nullptr) return set_error("wm3_linear: rope descriptor required");
     ep.rope = *rope;
@@ -514,4 +548,44 @@ extern "C" int wm3_linear_planes(const void* a, int lda, const void* b, int ldb,
                                  int planes, int plane_rows, long long plane_stride, int row_off, void* stream) {
   const OutPlanes op{planes, plane_rows, plane_stride, row_off};
   return linear_impl(a, lda, b, ldb, m, n, k, epi, out, ldo, n_valid, bias, rope, op, stream);
+}
+
+extern "C" int wm3_linear_planes_halo(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi,
+                                      void* out, int ldo, int n_valid, const float* bias, const wm3_rope_t* rope,
+                                      int planes, int plane_rows, long long plane_stride, int row_off,
+                                      const wm3_halo_t* halo, void* stream) {
+  const OutPlanes op{planes, plane_rows, plane_stride, row_off};
+  return linear_impl(a, lda, b, ldb, m, n, k, epi, out, ldo, n_valid, bias, rope, op, stream, halo);
+}
+
+namespace wm3 {
+__global__ void halo_signal_kernel(int* a, int* b, int epoch) {
+  __threadfence_system();
+  if (a != nullptr) asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(a), "r"(epoch) : "memory");
+  if (b != nullptr) asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(b), "r"(epoch) : "memory");
+}
+__global__ void halo_wait_kernel(const int* flags, int n, int epoch) {
+  const long long t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+    int v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(flags + i) : "memory");
+      if (v >= epoch) break;
+      __nanosleep(200);
+      if (clock64() - t0 > 20000000000LL) __trap();  // ~10 s: a neighbour never signalled
+    }
+  }
+  __threadfence_system();
+}
+}  // namespace wm3
+
+extern "C" int wm3_halo_signal(int* peer_flag_a, int* peer_flag_b, int epoch, void* stream) {
+  halo_signal_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(peer_flag_a, peer_flag_b, epoch);
+  return check_launch("halo_signal_kernel");
+}
+
+extern "C" int wm3_halo_wait(const int* flags, int n, int epoch, void* stream) {
+  if (n <= 0) return 0;
+  halo_wait_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(flags, n, epoch);
+  return check_launch("halo_wait_kernel");
 }

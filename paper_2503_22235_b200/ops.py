@@ -114,8 +114,10 @@ class KVGrid:
 
 
 def linear_grid(a: torch.Tensor, w: torch.Tensor, epi: int, bias: torch.Tensor, out: torch.Tensor, grid: KVGrid,
-                rope: "_lib.RopeT | None" = None) -> torch.Tensor:
-    """linear() whose output rows (band tokens) land in the K/V grid `out` (halo rows left untouched)."""
+                rope: "_lib.RopeT | None" = None, halo: "_lib.HaloT | None" = None) -> torch.Tensor:
+    """linear() whose output rows (band tokens) land in the K/V grid `out` (halo rows left untouched).  With
+    `halo` (wm3_halo_t), the QKV epilogue also stores the band's boundary K/V rows into the neighbouring bands'
+    grids (fused halo exchange over peer memory)."""
     _req(a, _lib.ELEM, "a")
     _req(w, _lib.ELEM, "w")
     _req(out, _lib.ELEM, "out")
@@ -123,10 +125,12 @@ def linear_grid(a: torch.Tensor, w: torch.Tensor, epi: int, bias: torch.Tensor, 
     n = w.shape[0]
     rp = None if rope is None else ctypes_byref(rope)
     plane = grid.rows * grid.cols
-    check(_lib.lib().wm3_linear_planes(ptr(a), a.stride(0), ptr(w), w.stride(0), m, n, k, int(epi), ptr(out),
-                                       out.stride(0), out.shape[1], ptr(bias), rp, grid.planes, plane,
-                                       grid.rows_ext * grid.cols, grid.halo_lo * grid.cols, stream_ptr()),
-          "wm3_linear_planes")
+    args = (ptr(a), a.stride(0), ptr(w), w.stride(0), m, n, k, int(epi), ptr(out), out.stride(0), out.shape[1],
+            ptr(bias), rp, grid.planes, plane, grid.rows_ext * grid.cols, grid.halo_lo * grid.cols)
+    if halo is None:
+        check(_lib.lib().wm3_linear_planes(*args, stream_ptr()), "wm3_linear_planes")
+    else:
+        check(_lib.lib().wm3_linear_planes_halo(*args, ctypes_byref(halo), stream_ptr()), "wm3_linear_planes_halo")
     return out
 
 

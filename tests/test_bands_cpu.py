@@ -129,7 +129,7 @@ class _FakeProcessor:
     """Stands in for BandedProcessor (whose kernels need a GPU): adds (global row + 1) * horizon to every token
     of each held band, so the test checks the sharding, the band bookkeeping and the all-gather."""
 
-    def __init__(self, params, cfg, bands, held, exchanger=None):
+    def __init__(self, params, cfg, bands, held, exchanger=None, fused=False):
         self.held = [bands[i] for i in held]
         self.ext = cfg.latent_extents
 

@@ -103,3 +103,34 @@ def test_banded_rollout_matches_single_gpu(name, world):
     rel = np.linalg.norm((b - x0) - (a - x0)) / np.linalg.norm(a - x0)
     assert rel < 2e-3, rel
     assert rollout_banded(lat, (), params, cfg, world=world) is lat
+
+
+@pytest.mark.parametrize("name,world", [("desk", 2), ("mid", 2)])
+def test_fused_halo_epilogue_matches_exchange(name, world):
+    """Halo rows written by the QKV GEMM epilogue straight into the neighbouring bands' K/V grids (the fused
+    compute + exchange path; here the "peer" grids are the other bands' buffers on this GPU) give bitwise the
+    same rollout as the separate halo copy."""
+    import paper_2503_22235_b200.model as m
+    from paper_2503_22235_b200.bands import rollout_banded
+    cfg = {"desk": m.desk_config, "mid": m.mid_config}[name]()
+    params = m.init_model_params(cfg, seed=9, zero_residual=False)
+    rng = np.random.default_rng(5)
+    g = cfg.grid
+    st = m.WeatherState(0, rng.standard_normal((cfg.surface_in, g.rows, g.cols)),
+                        rng.standard_normal((cfg.atmos_vars, cfg.levels, g.rows, g.cols)))
+    lat = m.encode(st, params, cfg)
+    copied = rollout_banded(lat, (6, 1), params, cfg, world=world)
+    fused = rollout_banded(lat, (6, 1), params, cfg, world=world, fused=True)
+    assert fused.tokens.values.tobytes() == copied.tokens.values.tobytes()
+
+
+def test_halo_flag_kernels_self_signal():
+    """wm3_halo_signal / wm3_halo_wait on this GPU's own flag words (a rank signalling itself: no cross-kernel
+    waiting): release stores land, acquire waits pass once the epoch is reached."""
+    from paper_2503_22235_b200 import _lib
+    flags = torch.zeros(4, dtype=torch.int32, device="cuda")
+    s = _lib.stream_ptr()
+    _lib.check(_lib.lib().wm3_halo_signal(flags.data_ptr() + 4, flags.data_ptr() + 8, 3, s), "signal")
+    _lib.check(_lib.lib().wm3_halo_wait(flags.data_ptr() + 4, 2, 3, s), "wait")
+    torch.cuda.synchronize()
+    assert flags.tolist() == [0, 3, 3, 0]
