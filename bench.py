@@ -318,21 +318,27 @@ def run_forecast(args, world: int = 1) -> dict:
                      f"{world} latitude bands, NCCL halo exchange per block (bands.rollout_banded)",
            "note": "page-locked host float32 fields in, page-locked host float32 fields out "
                    "(DecodedFields.to_host); H2D/D2H inside the timed region"}
-    if args.ensemble > 1 and world == 1:
-        # config 5's ensemble: perturbed members, per-member encode / decode, one batched latent rollout
+    if args.ensemble > 1:
+        # config 5's ensemble: perturbed members, per-member encode / decode, one batched latent rollout; with
+        # N ranks the members are sharded round-robin (independent replicas, no communication), time = max
         del out, s_host, a_host
-        states = [M.WeatherState(st.valid_time, torch.from_numpy(st.surface).pin_memory(),
-                                 torch.from_numpy(st.atmos).pin_memory())
-                  for st in R.perturbed_members(state, args.ensemble, scale=0.01)]
+        rank = dist.get_rank() if world > 1 else 0
+        mine = [m for m in range(args.ensemble) if m % world == rank]
+        all_states = R.perturbed_members(state, args.ensemble, scale=0.01)
+        states = [M.WeatherState(all_states[m].valid_time, torch.from_numpy(all_states[m].surface).pin_memory(),
+                                 torch.from_numpy(all_states[m].atmos).pin_memory()) for m in mine]
+        del all_states
         outs = R.forecast_ensemble(states, dt, params, cfg)   # first call: buffers, graph capture
         bufs = [o.to_host() for o in outs]                      # pinned output buffers, reused below
         del outs
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         outs = R.forecast_ensemble(states, dt, params, cfg)
         hosts = [o.to_host(b) for o, b in zip(outs, bufs)]
         torch.cuda.synchronize()
-        ens_s = time.perf_counter() - t0
+        ens_s = sync_max(time.perf_counter() - t0)
         spread = float(np.std([h[0][0].numpy().mean() for h in hosts]))
         # device verification of the ensemble (evaluation.ensemble_curve on the decoded fields in HBM):
         # leading-k ensemble-mean RMSE / blur of surface variable 0 against the unperturbed forecast
@@ -344,7 +350,8 @@ def run_forecast(args, world: int = 1) -> dict:
         curve = EV.ensemble_curve(members_dev, ctrl.surface.device[0][None], cfg.grid, wavelength_km=2000.0)
         torch.cuda.synchronize()
         t_curve = time.perf_counter() - t0
-        res["ensemble"] = {"members": args.ensemble, "seconds": round(ens_s, 4),
+        res["ensemble"] = {"members": args.ensemble, "gpus": world, "members_per_gpu": len(mine),
+                           "seconds": round(ens_s, 4),
                            "seconds_per_member": round(ens_s / args.ensemble, 4),
                            "block_tflop": round(tf_blocks * args.ensemble, 1),
                            "outputs_finite": bool(all(np.isfinite(a.numpy()).all() and np.isfinite(b.numpy()).all()
@@ -353,7 +360,8 @@ def run_forecast(args, world: int = 1) -> dict:
                            "curve_vs_control_sfc0": [{k: (round(v, 6) if isinstance(v, float) else v)
                                                       for k, v in r.items()} for r in curve],
                            "curve_seconds": round(t_curve, 4),
-                           "note": "perturbed_members(scale=0.01); batched rollout_ensemble; host fields in/out"}
+                           "note": "perturbed_members(scale=0.01); batched rollout_ensemble; host fields in/out; "
+                                   "curve over this rank's members"}
     return res
 
 
