@@ -6,8 +6,9 @@ wavelength and averaged over the rows whose resolvable range covers the target, 
 leading-k ensemble-mean curves, percent-change scorecards.
 
 The heavy parts run in libwm3.so (csrc/metrics.cu: float64 accumulation, fixed reduction order): the weighted
-squared error per (time, row) and the per-row zonal power spectra, each optionally of the mean of the
-leading k ensemble members computed on the fly.  Inputs may be numpy arrays (copied to the device once) or
+squared error per (time, row) and, for rows up to 256 columns, the per-row zonal power spectra by direct DFT,
+each optionally of the mean of the leading k ensemble members computed on the fly; wider rows (the 1440-column
+0.25 deg grid) take their spectra from cuFFT in float64 (torch.fft.rfft).  Inputs may be numpy arrays (copied to the device once) or
 CUDA tensors (used in place: decoded forecasts and ensemble members are scored without leaving HBM); only a
 (times x rows) or (rows x bins) float64 array comes back to the host.
 """
@@ -80,10 +81,22 @@ def latitude_rmse(pred, truth, spec: GridSpec) -> float:
     return _rmse_from(p[None], 1, g, spec)
 
 
+# Rows wider than this use cuFFT (torch.fft, float64: O(W log W)); narrower ones the direct-DFT kernel of
+# csrc/metrics.cu (O(W^2) but one launch and exact twiddles).  At 1440 columns the direct DFT is ~100x the work.
+DFT_MAX_COLS = 256
+
+
 def _zonal_power_dev(fields: torch.Tensor, k: int, spec: GridSpec) -> torch.Tensor:
     """(imgs, rows, cols//2 + 1) float64 power of fields (imgs, rows, cols), or of the leading-k member mean
     when fields is (n, imgs, rows, cols) and k > 1."""
     imgs = fields.shape[-3]
+    if spec.cols > DFT_MAX_COLS:
+        f = fields[:k].double().mean(dim=0) if fields.dim() == 4 else fields.double()
+        coef = torch.fft.rfft(f, dim=-1)
+        pw = (coef.real * coef.real + coef.imag * coef.imag) / float(spec.cols * spec.cols)
+        last = pw.shape[-1] - 1 if spec.cols % 2 == 0 else pw.shape[-1]
+        pw[..., 1:last] *= 2.0
+        return pw.contiguous()
     out = torch.empty((imgs, spec.rows, spec.cols // 2 + 1), dtype=torch.float64, device="cuda")
     stride = fields[0].numel() if k > 1 else 0
     check(_lib.lib().wm3_zonal_power(_dtype_code(fields), ptr(fields), stride, int(k), imgs, spec.rows, spec.cols,
@@ -99,34 +112,47 @@ def zonal_power(field, spec: GridSpec) -> np.ndarray:
     return _zonal_power_dev(f[None], 1, spec)[0].cpu().numpy()
 
 
-def _interp_rows(p: np.ndarray, spec: GridSpec, wavelength_km: float) -> float:
-    """Power at one wavelength from a (rows, bins) spectrum: log-wavelength interpolation per row, rows whose
-    resolvable range misses the target left out, cos-latitude weighted mean (evaluation.py:78-107)."""
+def _interp_plan(spec: GridSpec, n_wave: int, wavelength_km: float):
+    """Per-row interpolation plan for power_at_wavelength (evaluation.py:78-107): bracketing wavenumbers lo / hi
+    of circumference / wavelength, the weight t of hi (linear in log(lambda) = log(circumference) - log(m), which
+    is exactly np.interp on the reversed arrays), and the row weights (cos latitude, 0 for rows whose resolvable
+    range misses the target)."""
     if wavelength_km <= 0:
         raise ConfigError("wavelength must be positive")
-    n_wave = p.shape[1] - 1
     if n_wave < 1:
         raise ConfigError("grid too narrow for any zonal wave")
     circ = row_circumference_km(spec)
-    weights = latitude_weights(spec)
-    m = np.arange(1, n_wave + 1, dtype=np.float64)
-    x = np.log(wavelength_km)
-    acc, wsum = 0.0, 0.0
-    for r in range(spec.rows):
-        lam = circ[r] / m  # decreasing in m
-        if not (lam[-1] <= wavelength_km <= lam[0]):
-            continue
-        acc += weights[r] * float(np.interp(x, np.log(lam[::-1]), p[r, 1:][::-1]))
-        wsum += weights[r]
-    if wsum == 0.0:
+    ok = (circ / n_wave <= wavelength_km) & (wavelength_km <= circ)  # lam[-1] <= target <= lam[0]
+    if not ok.any():
         raise ConfigError(f"wavelength {wavelength_km} km outside every row's resolvable range")
-    return acc / wsum
+    lo = np.clip(np.floor(circ / wavelength_km), 1, n_wave).astype(np.int64)
+    hi = np.minimum(lo + 1, n_wave)
+    xl, xh = np.log(circ / lo), np.log(circ / hi)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t = np.where(hi > lo, (np.log(wavelength_km) - xl) / (xh - xl), 0.0)
+    wr = np.where(ok, latitude_weights(spec), 0.0)
+    return lo, hi, t, wr / wr.sum()
+
+
+def _interp_rows(p, spec: GridSpec, wavelength_km: float):
+    """Power at one wavelength from (..., rows, bins) spectra (numpy or CUDA tensor), vectorised over rows and
+    leading planes; a float for 2D input, an array over the leading dimensions otherwise."""
+    lo, hi, t, wr = _interp_plan(spec, p.shape[-1] - 1, wavelength_km)
+    rows = np.arange(spec.rows)
+    if isinstance(p, torch.Tensor):  # on the device: only the per-plane values come back
+        dev = p.device
+        rows_t, lo_t, hi_t = (torch.from_numpy(a).to(dev) for a in (rows, lo, hi))
+        t_t, w_t = torch.from_numpy(t).to(dev), torch.from_numpy(wr).to(dev)
+        plo, phi = p[..., rows_t, lo_t], p[..., rows_t, hi_t]
+        return ((plo + (phi - plo) * t_t) * w_t).sum(dim=-1).cpu().numpy()
+    plo, phi = p[..., rows, lo], p[..., rows, hi]
+    return ((plo + (phi - plo) * t) * wr).sum(axis=-1)
 
 
 def power_at_wavelength(field, spec: GridSpec, wavelength_km: float) -> float:
     if wavelength_km <= 0:
         raise ConfigError("wavelength must be positive")
-    return _interp_rows(zonal_power(field, spec), spec, wavelength_km)
+    return float(_interp_rows(zonal_power(field, spec), spec, wavelength_km))
 
 
 def _blur_from_powers(pf: float, pt: float) -> float:
@@ -174,10 +200,10 @@ def ensemble_curve(members, truth, spec: GridSpec, sizes=None, wavelength_km=Non
         row = {"size": k, "rmse": _rmse_from(m, k, t, spec)}
         if wavelength_km is not None:
             if truth_power is None:
-                truth_power = _zonal_power_dev(t, 1, spec).cpu().numpy()
-            mean_power = _zonal_power_dev(m, k, spec).cpu().numpy()
-            blurs = [_blur_from_powers(_interp_rows(mean_power[i], spec, wavelength_km),
-                                       _interp_rows(truth_power[i], spec, wavelength_km)) for i in range(t.shape[0])]
+                truth_power = _zonal_power_dev(t, 1, spec)
+            mean_power = _zonal_power_dev(m, k, spec)
+            wm, wt = _interp_rows(mean_power, spec, wavelength_km), _interp_rows(truth_power, spec, wavelength_km)
+            blurs = [_blur_from_powers(float(wm[i]), float(wt[i])) for i in range(t.shape[0])]
             row["blur"] = float(np.mean(blurs))
         rows.append(row)
     return rows
@@ -198,10 +224,11 @@ def plane_scores(pred, truth, spec: GridSpec, wavelength_km: float):
     check(_lib.lib().wm3_sq_err_rows(_dtype_code(p), ptr(p), 0, 1, ptr(g), ptr(_weights(spec)), n, spec.rows,
                                      spec.cols, ptr(partial), stream_ptr()), "wm3_sq_err_rows")
     rmse = np.sqrt(partial.cpu().numpy().sum(axis=1) / (spec.rows * spec.cols))
-    pp, pt = _zonal_power_dev(p, 1, spec).cpu().numpy(), _zonal_power_dev(g, 1, spec).cpu().numpy()
+    wf = _interp_rows(_zonal_power_dev(p, 1, spec), spec, wavelength_km)
+    wt = _interp_rows(_zonal_power_dev(g, 1, spec), spec, wavelength_km)
     blur = []
     for i in range(n):
-        b = _blur_from_powers(_interp_rows(pp[i], spec, wavelength_km), _interp_rows(pt[i], spec, wavelength_km))
+        b = _blur_from_powers(float(wf[i]), float(wt[i]))
         blur.append(None if not np.isfinite(b) else b)
     return [float(v) for v in rmse], blur
 

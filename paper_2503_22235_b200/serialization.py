@@ -109,30 +109,34 @@ def load_params_file(path) -> dict[str, np.ndarray]:
 
 
 def load_params_device(path, dtype=None, device: str = "cuda") -> dict:
-    """Memory-map an LMTW file and stream every tensor to the device (float64 payload -> `dtype`, default fp32).
+    """Stream an LMTW file to the device (float64 payload -> `dtype`, default fp32): name -> torch tensor.
 
-    Returns name -> torch tensor on `device`.  The host never materialises a copy of the payload: each
-    tensor is a zero-copy float64 view of the mapping, copied H2D and narrowed on the GPU."""
-    import warnings
-
+    The file is read once with readinto() into one page-locked host buffer (no intermediate Python bytes or
+    per-tensor numpy copies), the header index is parsed from it, every payload is copied host -> device
+    asynchronously from that buffer, and narrowed to `dtype` on the GPU."""
     import torch
     dtype = torch.float32 if dtype is None else dtype
-
-    def to_device(mm, off: int, shape) -> "torch.Tensor":
-        n = int(np.prod(shape, dtype=np.int64)) if shape else 1
-        host = np.frombuffer(mm, dtype="<f8", count=n, offset=off).reshape(shape)
-        with warnings.catch_warnings():  # read-only mapping: torch warns about non-writable arrays
-            warnings.simplefilter("ignore", UserWarning)
-            return torch.from_numpy(host).to(device=device, dtype=dtype, copy=True)
-
     with open(path, "rb") as f:
-        mm = mmap.mmap(f.fileno(), 0, access=mmap.ACCESS_READ) if f.seek(0, 2) else None
-    if mm is None:
-        raise ContainerError("truncated container: empty file")
-    try:
-        out = {name: to_device(mm, off, shape) for name, shape, off in index_params(mm)}
-        if device != "cpu":
-            torch.cuda.synchronize()
-        return out
-    finally:
-        mm.close()
+        size = f.seek(0, 2)
+        if size == 0:
+            raise ContainerError("truncated container: empty file")
+        f.seek(0)
+        host = torch.empty(size, dtype=torch.uint8, pin_memory=(device != "cpu"))
+        view = memoryview(host.numpy())
+        got = 0
+        while got < size:
+            k = f.readinto(view[got:])
+            if not k:
+                raise ContainerError("truncated container: short read")
+            got += k
+    entries = index_params(view)
+    out = {}
+    for name, shape, off in entries:
+        n = int(np.prod(shape, dtype=np.int64)) if shape else 1
+        raw = host[off:off + 8 * n]  # payloads are not 8-byte aligned in the file: move bytes, view on arrival
+        dev = torch.empty(8 * n, dtype=torch.uint8, device=device)
+        dev.copy_(raw, non_blocking=True)
+        out[name] = dev.view(torch.float64).to(dtype).view(shape)
+    if device != "cpu":
+        torch.cuda.synchronize()
+    return out
