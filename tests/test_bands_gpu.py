@@ -134,3 +134,26 @@ def test_halo_flag_kernels_self_signal():
     _lib.check(_lib.lib().wm3_halo_wait(flags.data_ptr() + 4, 2, 3, s), "wait")
     torch.cuda.synchronize()
     assert flags.tolist() == [0, 3, 3, 0]
+
+
+def test_banded_forecast_full_scale_bands_8():
+    """The bench's N = 8 forecast path (encode -> rollout_banded -> decode) at full latent scale, with the eight
+    latitude bands emulated on this GPU: decoded fields match the single-GPU forecast to fp16 round-off."""
+    import paper_2503_22235_b200.model as m
+    import paper_2503_22235_b200.rollout as r
+    from paper_2503_22235_b200.bands import rollout_banded
+    cfg = m.full_scale_config()
+    params = m.init_model_params(cfg, seed=0, zero_residual=False)
+    g = cfg.grid
+    rng = np.random.default_rng(1)
+    st = m.WeatherState(0, torch.from_numpy(rng.standard_normal((cfg.surface_in, g.rows, g.cols)).astype(np.float32)).cuda(),
+                        torch.from_numpy(rng.standard_normal((cfg.atmos_vars, cfg.levels, g.rows, g.cols))
+                                         .astype(np.float32)).cuda())
+    lat = m.encode(st, params, cfg)
+    one = m.decode(r.rollout(lat, (6, 1), params, cfg), params, cfg)
+    banded = m.decode(rollout_banded(lat, (6, 1), params, cfg, world=8), params, cfg)
+    a, b = one.surface.device, banded.surface.device
+    rel = float((a - b).norm() / a.norm())
+    assert rel < 5e-3, rel
+    a, b = one.atmos.device, banded.atmos.device
+    assert float((a - b).norm() / a.norm()) < 5e-3
