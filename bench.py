@@ -449,7 +449,12 @@ def run_gpu(args, world, rank, local_rank):
 
     fc = None
     if not args.no_forecast:
-        fc = run_forecast(args, world)
+        try:
+            fc = run_forecast(args, world)
+        except Exception as exc:  # keep the block measurement if the (secondary) forecast leg fails
+            import traceback
+            traceback.print_exc(file=sys.stderr)
+            fc = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     if rank == 0:
         cpu = None
