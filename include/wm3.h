@@ -18,6 +18,7 @@
  *                             WM3_EPI_QKV_ROPE        attention.py:167-171  q,k,v + bias, rotary on q,k
  *                             WM3_EPI_F32             raw fp32 accumulator (tests)
  *   wm3_natten_fwd          attention.py:173-178 gather + q k^T/sqrt(dh) + softmax + @V, fused
+ *   wm3_block_fwd           attention.py:146-184 the whole block (7 launches) in one call
  *   wm3_conv3x3             model.py:296-301 + autodiff.py:677-713  row zero pad, col wrap, stride 1/2
  *   wm3_convT4x4s2          model.py:317-325 + autodiff.py:716-764  exact adjoint geometry
  */
@@ -101,6 +102,41 @@ int wm3_linear_planes_halo(const void* a, int lda, const void* b, int ldb, int m
 int wm3_halo_signal(int* peer_flag_a, int* peer_flag_b, int epoch, void* stream);
 /* Spin (acquire, system scope) until each of the n local flags is >= epoch; traps after ~10 s. */
 int wm3_halo_wait(const int* flags, int n, int epoch, void* stream);
+
+/* One processor block (attention.py:146-184) as library calls: x (T, hidden) fp32 in place, T = batch * depth *
+ * rows * cols band tokens.  Weights in the device layout the Python layer prepares (blocks.prepare_block:
+ * K-major fp16, q/k rotary pairs interleaved, heads padded to dhp); workspace buffers: hn (T, kp), the K/V grid
+ * qkv ([batch * depth][halo_lo + rows + halo_hi][cols][3 * heads * dhp]), ctx (T, heads * dhp), mid (T, nm). */
+typedef struct {
+  const float *ln1_g, *ln1_b;
+  const void* w_qkv;
+  const float* b_qkv;
+  const void* w_o;
+  const float* b_o;
+  const float *ln2_g, *ln2_b;
+  const void* w_1;
+  const float* b_1;
+  const void* w_2;
+  const float* b_2;
+  int hidden, heads, dh, dhp, kp, np, nm;
+} wm3_block_weights_t;
+typedef struct {
+  void *hn, *qkv, *ctx, *mid;
+} wm3_block_ws_t;
+typedef struct {
+  int batch, depth, rows, cols;    /* local band extents (batch = ensemble members) */
+  int rows_global, row0, halo_lo, halo_hi;
+  int wd, wh, ww;                  /* attention window */
+} wm3_block_geom_t;
+/* LN1 + QKV (+rotary) into the K/V grid; with halo != NULL the epilogue also fills the neighbours' halos. */
+int wm3_block_qkv(const float* x, const wm3_block_weights_t* w, const wm3_block_ws_t* ws, const wm3_block_geom_t* g,
+                  const wm3_rope_t* rope, const wm3_halo_t* halo, void* stream);
+/* NA -> O-proj + residual -> LN2 -> W1 + GELU -> W2 + residual (halo rows of the K/V grid must be filled). */
+int wm3_block_rest(float* x, const wm3_block_weights_t* w, const wm3_block_ws_t* ws, const wm3_block_geom_t* g,
+                   void* stream);
+/* Both halves (a band without halos, or halos filled by the fused epilogue). */
+int wm3_block_fwd(float* x, const wm3_block_weights_t* w, const wm3_block_ws_t* ws, const wm3_block_geom_t* g,
+                  const wm3_rope_t* rope, void* stream);
 
 /* Fused 3D neighborhood attention forward, over `batch` independent latents (ensemble members).
  * qkv: bf16 K/V grid [batch * depth][rows_ext][cols][ldqkv] (member b owns depth planes [b * depth, (b + 1) * depth);

@@ -41,6 +41,24 @@ class HaloT(ctypes.Structure):
                 ("dn_plane_stride", _ll), ("up_row_off", _ll), ("dn_row_off", _ll), ("ld", _i), ("col_lo", _i)]
 
 
+class BlockWeightsT(ctypes.Structure):
+    """wm3_block_weights_t (include/wm3.h)."""
+    _fields_ = [("ln1_g", _vp), ("ln1_b", _vp), ("w_qkv", _vp), ("b_qkv", _vp), ("w_o", _vp), ("b_o", _vp),
+                ("ln2_g", _vp), ("ln2_b", _vp), ("w_1", _vp), ("b_1", _vp), ("w_2", _vp), ("b_2", _vp),
+                ("hidden", _i), ("heads", _i), ("dh", _i), ("dhp", _i), ("kp", _i), ("np", _i), ("nm", _i)]
+
+
+class BlockWsT(ctypes.Structure):
+    """wm3_block_ws_t."""
+    _fields_ = [("hn", _vp), ("qkv", _vp), ("ctx", _vp), ("mid", _vp)]
+
+
+class BlockGeomT(ctypes.Structure):
+    """wm3_block_geom_t."""
+    _fields_ = [("batch", _i), ("depth", _i), ("rows", _i), ("cols", _i), ("rows_global", _i), ("row0", _i),
+                ("halo_lo", _i), ("halo_hi", _i), ("wd", _i), ("wh", _i), ("ww", _i)]
+
+
 # name -> argtypes; every function returns int status
 SIGNATURES = {
     "wm3_neighbor_table": [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp],
@@ -52,6 +70,11 @@ SIGNATURES = {
                                _i, _i, ctypes.c_longlong, _i, ctypes.POINTER(HaloT), _vp],
     "wm3_halo_signal": [_vp, _vp, _i, _vp],
     "wm3_halo_wait": [_vp, _i, _i, _vp],
+    "wm3_block_qkv": [_vp, ctypes.POINTER(BlockWeightsT), ctypes.POINTER(BlockWsT), ctypes.POINTER(BlockGeomT),
+                      ctypes.POINTER(RopeT), ctypes.POINTER(HaloT), _vp],
+    "wm3_block_rest": [_vp, ctypes.POINTER(BlockWeightsT), ctypes.POINTER(BlockWsT), ctypes.POINTER(BlockGeomT), _vp],
+    "wm3_block_fwd": [_vp, ctypes.POINTER(BlockWeightsT), ctypes.POINTER(BlockWsT), ctypes.POINTER(BlockGeomT),
+                      ctypes.POINTER(RopeT), _vp],
     "wm3_natten_fwd": [_vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _f, _vp],
     "wm3_natten_windows": [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp],
     "wm3_conv_bn": [_i],

@@ -81,6 +81,7 @@ def rope_axis_tables(extents, head_dim: int):
 # ------------------------------------------------------------------------------------------------
 @dataclass
 class BlockWeights:
+    """Device layout of one block's parameters (see prepare_block)."""
     hidden: int
     heads: int
     dh: int
@@ -100,6 +101,17 @@ class BlockWeights:
     b_1: torch.Tensor
     w_2: torch.Tensor
     b_2: torch.Tensor
+
+    def native(self) -> "_lib.BlockWeightsT":
+        """wm3_block_weights_t view of these tensors (cached; the tensors stay owned by this object)."""
+        nat = self.__dict__.get("_native")
+        if nat is None:
+            nat = _lib.BlockWeightsT(*(t.data_ptr() for t in (self.ln1_g, self.ln1_b, self.w_qkv, self.b_qkv, self.w_o,
+                                                              self.b_o, self.ln2_g, self.ln2_b, self.w_1, self.b_1,
+                                                              self.w_2, self.b_2)),
+                                     self.hidden, self.heads, self.dh, self.dhp, self.kp, self.np_, self.nm)
+            self.__dict__["_native"] = nat
+        return nat
 
 
 def _qk_perm(heads: int, dh: int, dhp: int) -> np.ndarray:
@@ -230,6 +242,11 @@ class Workspace:
         self.qkv = torch.zeros((grid.tokens, 3 * bw.heads * bw.dhp), dtype=_lib.ELEM, device=device)
         self.ctx = torch.empty((tokens, bw.heads * bw.dhp), dtype=_lib.ELEM, device=device)
         self.mid = torch.empty((tokens, bw.nm), dtype=_lib.ELEM, device=device)
+        self._native = _lib.BlockWsT(self.hn.data_ptr(), self.qkv.data_ptr(), self.ctx.data_ptr(),
+                                     self.mid.data_ptr())
+
+    def native(self) -> "_lib.BlockWsT":
+        return self._native
 
 
 def block_forward(x: torch.Tensor, bw: BlockWeights, ws: Workspace, rope: RopeTables, extents, window,
@@ -247,6 +264,16 @@ def block_forward(x: torch.Tensor, bw: BlockWeights, ws: Workspace, rope: RopeTa
     """
     L = _lib
     g = ws.grid
+    if mark is None and halo_exchange is None:
+        # the whole block in one library call (wm3_block_fwd: the 7 launches are issued by the C++ host code)
+        import ctypes
+        rs = rope.struct(extents, row0, bw.heads, bw.dhp)
+        d, h, w = (int(e) for e in extents)
+        geom = L.BlockGeomT(g.batch, d, h, w, int(rows_global if rows_global is not None else h), int(row0),
+                            g.halo_lo, g.halo_hi, *(int(v) for v in window))
+        L.check(L.lib().wm3_block_fwd(x.data_ptr(), ctypes.byref(bw.native()), ctypes.byref(ws.native()),
+                                      ctypes.byref(geom), ctypes.byref(rs), L.stream_ptr()), "wm3_block_fwd")
+        return
     mk = mark if mark is not None else (lambda i: None)
     mk(0)
     ops.layernorm_bf16(x, bw.ln1_g, bw.ln1_b, out=ws.hn)

@@ -119,3 +119,21 @@ def test_natten_block_stream_matches_operator():
     for xi, oi in zip(xs, outs):
         ref = natten_block(xi, params, "blk", ext, win, heads).device.cpu()
         assert torch.equal(oi, ref)
+
+
+def test_native_block_call_equals_composed_launches():
+    """wm3_block_fwd (the 7 launches issued by the library's C++ host code) is bitwise the Python-composed chain."""
+    import torch
+    from paper_2503_22235_b200 import ops
+    from paper_2503_22235_b200.blocks import RopeTables, Workspace, block_forward
+    from paper_2503_22235_b200.params import init_block_params
+    from paper_2503_22235_b200.runtime import CACHE
+    ext, win, dim, heads = (5, 18, 36), (5, 7, 7), 256, 2
+    params = init_block_params(np.random.default_rng(4), dim, heads, "blk", zero_residual=False)
+    bw = CACHE.block(params, "blk", heads)
+    rope = RopeTables(ext, dim // heads)
+    x = torch.randn(int(np.prod(ext)), dim, device="cuda")
+    a, b = x.clone(), x.clone()
+    block_forward(a, bw, Workspace(ops.KVGrid(ext, win), bw), rope, ext, win)                    # native
+    block_forward(b, bw, Workspace(ops.KVGrid(ext, win), bw), rope, ext, win, mark=lambda i: None)  # composed
+    assert torch.equal(a, b)
