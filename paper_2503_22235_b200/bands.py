@@ -269,7 +269,9 @@ class BandedProcessor:
 
     def process(self, xs: list[torch.Tensor], horizon: int) -> None:
         """In place on the held bands' token buffers xs[i] ((d * rows_i * w, hidden) fp32, band order)."""
-        from . import _lib, ops
+        import ctypes
+
+        from . import _lib
         from .runtime import CACHE
         cfg = self.cfg
         h = cfg.latent_extents[1]
@@ -281,8 +283,9 @@ class BandedProcessor:
             peer = self.exchanger if (self.fused and isinstance(self.exchanger, PeerHalo)) else None
             if peer is not None:
                 peer.before_qkv()
+            geoms = [_lib.BlockGeomT(1, ext[0], ext[1], ext[2], h, b.row0, b.halo_lo, b.halo_hi, *cfg.window)
+                     for b, ext in zip(self.held, self.local)]
             for j, (b, ext, xb, ws) in enumerate(zip(self.held, self.local, xs, wss)):
-                ops.layernorm_bf16(xb, bw.ln1_g, bw.ln1_b, out=ws.hn)
                 halo = None
                 if self.fused:
                     if peer is not None:
@@ -297,8 +300,12 @@ class BandedProcessor:
                             grids.append(g_)
                         halo = halo_descriptor(self.held_idx[j], self.held, grids,
                                                [w_.qkv.data_ptr() for w_ in wss], cols, sec)
-                ops.linear_grid(ws.hn, bw.w_qkv, _lib.WM3_EPI_QKV_ROPE, bw.b_qkv, ws.qkv, ws.grid,
-                                rope=self.rope.struct(ext, b.row0, bw.heads, bw.dhp), halo=halo)
+                # LN1 + QKV (+rotary, + fused halo stores) in one library call
+                rs = self.rope.struct(ext, b.row0, bw.heads, bw.dhp)
+                _lib.check(_lib.lib().wm3_block_qkv(xb.data_ptr(), ctypes.byref(bw.native()), ctypes.byref(ws.native()),
+                                                    ctypes.byref(geoms[j]), ctypes.byref(rs),
+                                                    None if halo is None else ctypes.byref(halo), _lib.stream_ptr()),
+                           "wm3_block_qkv")
             if peer is not None:
                 peer.after_qkv()
             elif self.fused:
@@ -308,15 +315,12 @@ class BandedProcessor:
                     self.exchanger(ws.qkv, ws.grid)
             else:
                 copy_halos(self.held, wss)
-            for b, xb, ws in zip(self.held, xs, wss):
-                ops.natten(ws.qkv, ws.grid, bw.heads, bw.dhp, bw.dh, cfg.window, out=ws.ctx, rows_global=h,
-                           row0=b.row0)
+            for j, (b, xb, ws) in enumerate(zip(self.held, xs, wss)):
+                # attention -> O-proj -> LN2 -> MLP in one library call
+                _lib.check(_lib.lib().wm3_block_rest(xb.data_ptr(), ctypes.byref(bw.native()), ctypes.byref(ws.native()),
+                                                     ctypes.byref(geoms[j]), _lib.stream_ptr()), "wm3_block_rest")
                 if peer is not None:
                     peer.after_attention()  # neighbours may overwrite our halo rows for the next block
-                ops.linear(ws.ctx, bw.w_o, _lib.WM3_EPI_BIAS_RESID_F32, bias=bw.b_o, out=xb, n_valid=bw.hidden)
-                ops.layernorm_bf16(xb, bw.ln2_g, bw.ln2_b, out=ws.hn)
-                ops.linear(ws.hn, bw.w_1, _lib.WM3_EPI_BIAS_GELU_BF16, bias=bw.b_1, out=ws.mid)
-                ops.linear(ws.mid, bw.w_2, _lib.WM3_EPI_BIAS_RESID_F32, bias=bw.b_2, out=xb, n_valid=bw.hidden)
 
 
 def rollout_banded(lat, plan, params: dict, cfg, world: int | None = None, group=None, fused: bool = False):
