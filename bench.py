@@ -258,20 +258,19 @@ def roofline(per_ms: dict, tokens: int) -> tuple[dict, dict]:
 
 def run_forecast(args, world: int = 1) -> dict:
     """14-day 0.25 deg forecast through the public API, host fields in -> host fields out.  With N > 1 ranks
-    the latent rollout is split into latitude bands (bands.rollout_banded: NCCL halo exchange per block,
-    all-gather at the end); encode / decode run replicated on every rank; time = max over ranks."""
+    the whole forecast is split (bands.forecast_banded): encoder / decoder pyramids by depth plane with
+    all-gathers of the token planes and fields, every latent block on latitude bands with the NCCL halo
+    exchange per block; time = max over ranks."""
     import torch
     import torch.distributed as dist
     from paper_2503_22235_b200 import model as M
     from paper_2503_22235_b200 import rollout as R
-    from paper_2503_22235_b200.bands import rollout_banded
+    from paper_2503_22235_b200.bands import forecast_banded
 
     def forecast(state, dt, params, cfg):
         if world == 1:
             return R.forecast(state, dt, params, cfg)
-        lat = M.encode(state, params, cfg)
-        lat = rollout_banded(lat, R.greedy_plan(dt, cfg.max_dt), params, cfg, fused=FUSED_HALO)
-        return M.decode(lat, params, cfg)
+        return forecast_banded(state, dt, params, cfg, fused=FUSED_HALO)
 
     def sync_max(sec: float) -> float:
         if world == 1:
@@ -315,7 +314,8 @@ def run_forecast(args, world: int = 1) -> dict:
            "block_tflop": round(tf_blocks, 1), "processor_steps": len(plan), "outputs_finite": finite,
            "paper_rtx4090_seconds": 12.0, "gpus": world,
            "latent": "single GPU, CUDA-graph replays" if world == 1 else
-                     f"{world} latitude bands, NCCL halo exchange per block (bands.rollout_banded)",
+                     f"{world} ranks: pyramids by depth plane, blocks on latitude bands with NCCL halo "
+                     "exchange per block (bands.forecast_banded)",
            "note": "page-locked host float32 fields in, page-locked host float32 fields out "
                    "(DecodedFields.to_host); H2D/D2H inside the timed region"}
     if args.ensemble > 1:

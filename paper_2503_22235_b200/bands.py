@@ -269,6 +269,10 @@ class BandedProcessor:
 
     def process(self, xs: list[torch.Tensor], horizon: int) -> None:
         """In place on the held bands' token buffers xs[i] ((d * rows_i * w, hidden) fp32, band order)."""
+        self.run(xs, [f"proc{horizon}.blk{i}" for i in range(self.cfg.proc_blocks)])
+
+    def run(self, xs: list[torch.Tensor], prefixes) -> None:
+        """The blocks named by `prefixes` (encoder, processor or decoder blocks) in order, in place on xs."""
         import ctypes
 
         from . import _lib
@@ -276,8 +280,8 @@ class BandedProcessor:
         cfg = self.cfg
         h = cfg.latent_extents[1]
         cols = cfg.latent_extents[2]
-        for i in range(cfg.proc_blocks):
-            bw = CACHE.block(self.params, f"proc{horizon}.blk{i}", cfg.heads)
+        for prefix in prefixes:
+            bw = CACHE.block(self.params, prefix, cfg.heads)
             wss = self._ws(bw)
             sec = bw.heads * bw.dhp
             peer = self.exchanger if (self.fused and isinstance(self.exchanger, PeerHalo)) else None
@@ -323,6 +327,60 @@ class BandedProcessor:
                     peer.after_attention()  # neighbours may overwrite our halo rows for the next block
 
 
+def plane_ranges(depth: int, world: int) -> list[tuple[int, int]]:
+    """Depth planes [lo, hi) per rank for the encoder / decoder pyramids: contiguous, sizes differing by at
+    most one; with more ranks than planes the extra ranks get an empty range (they only run latent bands)."""
+    if depth < 1 or world < 1:
+        raise ValueError(f"cannot split {depth} planes over {world} ranks")
+    base, extra = divmod(depth, world)
+    out, lo = [], 0
+    for r in range(world):
+        n = base + (1 if r < extra else 0)
+        out.append((lo, lo + n))
+        lo += n
+    return out
+
+
+def _banded_setup(params: dict, cfg, world, group, fused: bool, first_prefix: str):
+    """(processor, bands, rank, world, distributed) for a banded run; see rollout_banded."""
+    import torch.distributed as dist
+
+    from .model import device_model
+    device_model(params, cfg)
+    d, h, w = cfg.latent_extents
+    distributed = world is None and dist.is_available() and dist.is_initialized() and \
+        dist.get_world_size(group) > 1
+    n = dist.get_world_size(group) if distributed else int(world or 1)
+    bands = plan_bands(h, cfg.window[1], n)
+    if not distributed:
+        return BandedProcessor(params, cfg, bands, list(range(n)), fused=fused), bands, 0, n, False
+    rank = dist.get_rank(group)
+    if fused:
+        from .runtime import CACHE
+        me = bands[rank]
+        bw0 = CACHE.block(params, first_prefix, cfg.heads)
+        ws0 = CACHE.workspace((d, me.rows, w), cfg.window, bw0, halo=(me.halo_lo, me.halo_hi), tag=f"band{rank}")
+        exch = PeerHalo(bands, rank, ws0.qkv, ws0.grid, group)
+    else:
+        exch = HaloExchanger(bands, rank, group)
+    return BandedProcessor(params, cfg, bands, [rank], exch, fused=fused), bands, rank, n, True
+
+
+def _gather_latent(xs: list[torch.Tensor], bands: list[Band], extents, distributed: bool, group) -> torch.Tensor:
+    """The full latent from the bands (all-gather across ranks, padded to the largest band)."""
+    import torch.distributed as dist
+    d, _, w = extents
+    if distributed:
+        hidden = xs[0].shape[1]
+        mx = max(b.rows for b in bands) * d * w
+        buf = torch.zeros((mx, hidden), dtype=xs[0].dtype, device=xs[0].device)
+        buf[:xs[0].shape[0]] = xs[0]
+        parts = [torch.empty_like(buf) for _ in bands]
+        dist.all_gather(parts, buf, group=group)
+        xs = [p[:d * b.rows * w] for p, b in zip(parts, bands)]
+    return gather_bands(xs, extents, bands)
+
+
 def rollout_banded(lat, plan, params: dict, cfg, world: int | None = None, group=None, fused: bool = False):
     """rollout() with the latent split into latitude bands.
 
@@ -332,8 +390,6 @@ def rollout_banded(lat, plan, params: dict, cfg, world: int | None = None, group
     (the same kernels and halo rows; used to verify the split on one device).  fused=True moves the halo rows
     in the QKV GEMM epilogue (peer stores into the neighbours' K/V grids, PeerHalo epoch flags across ranks)
     instead of a separate exchange.  Validation as rollout()."""
-    import torch.distributed as dist
-
     from .model import CALL_COUNTS, LatentState, _tokens
     from .rollout import _check_plan, plan_hours
     from .tensor import Tensor
@@ -341,40 +397,132 @@ def rollout_banded(lat, plan, params: dict, cfg, world: int | None = None, group
     plan = _check_plan(plan, params, cfg)
     if not plan:
         return lat
-    from .model import device_model
-    device_model(params, cfg)
-    d, h, w = cfg.latent_extents
+    proc, bands, rank, n, distributed = _banded_setup(params, cfg, world, group, fused, f"proc{plan[0]}.blk0")
     x = _tokens(lat)
-    distributed = world is None and dist.is_available() and dist.is_initialized() and \
-        dist.get_world_size(group) > 1
-    n = dist.get_world_size(group) if distributed else int(world or 1)
-    bands = plan_bands(h, cfg.window[1], n)
-    if distributed:
-        rank = dist.get_rank(group)
-        if fused:
-            from .runtime import CACHE
-            me = bands[rank]
-            bw0 = CACHE.block(params, f"proc{plan[0]}.blk0", cfg.heads)
-            ws0 = CACHE.workspace((d, me.rows, w), cfg.window, bw0, halo=(me.halo_lo, me.halo_hi), tag=f"band{rank}")
-            exch = PeerHalo(bands, rank, ws0.qkv, ws0.grid, group)
-        else:
-            exch = HaloExchanger(bands, rank, group)
-        proc = BandedProcessor(params, cfg, bands, [rank], exch, fused=fused)
-        xs = [local_band_tokens(x, cfg.latent_extents, bands[rank]).clone()]
-    else:
-        proc = BandedProcessor(params, cfg, bands, list(range(n)), fused=fused)
-        xs = [local_band_tokens(x, cfg.latent_extents, b).clone() for b in bands]
+    held = [bands[rank]] if distributed else bands
+    xs = [local_band_tokens(x, cfg.latent_extents, b).clone() for b in held]
     for hz in plan:
         proc.process(xs, hz)
         CALL_COUNTS[f"process{hz}"] += 1
-    if distributed:
-        # variable band sizes: pad to the largest band for all_gather, then trim
-        hidden = x.shape[1]
-        mx = max(b.rows for b in bands) * d * w
-        buf = torch.zeros((mx, hidden), dtype=x.dtype, device=x.device)
-        buf[:xs[0].shape[0]] = xs[0]
-        parts = [torch.empty_like(buf) for _ in bands]
-        dist.all_gather(parts, buf, group=group)
-        xs = [p[:d * b.rows * w] for p, b in zip(parts, bands)]
-    full = gather_bands(xs, cfg.latent_extents, bands)
+    full = _gather_latent(xs, bands, cfg.latent_extents, distributed, group)
     return LatentState(Tensor(device=full), lat.valid_time + plan_hours(plan), tuple(lat.extents))
+
+
+def _all_gather_var(local: torch.Tensor, sizes: list[int], group) -> list[torch.Tensor]:
+    """all_gather of 1-D/2-D row blocks of per-rank `sizes` rows (padded to the largest)."""
+    import torch.distributed as dist
+    mx = max(max(sizes), 1)
+    buf = torch.zeros((mx,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    buf[:local.shape[0]] = local
+    parts = [torch.empty_like(buf) for _ in sizes]
+    dist.all_gather(parts, buf, group=group)
+    return [p[:k] for p, k in zip(parts, sizes)]
+
+
+def gather_plane_tokens(tokens: torch.Tensor, ranges: list[tuple[int, int]], rank: int, plane_tokens: int,
+                        group=None) -> None:
+    """In place: every rank's encoded planes (rows [lo * plane_tokens, hi * plane_tokens) of `tokens`, ranges[r]
+    for rank r) copied into every other rank's `tokens` (one all-gather)."""
+    lo, hi = ranges[rank]
+    pt = plane_tokens
+    parts = _all_gather_var(tokens[lo * pt:hi * pt], [(b - a) * pt for a, b in ranges], group)
+    for r, ((a, b), part) in enumerate(zip(ranges, parts)):
+        if b > a and r != rank:
+            tokens[a * pt:b * pt] = part
+
+
+def _plane_levels(a: int, b: int, level_patch: int) -> tuple[int, int]:
+    """Atmosphere levels [l0, l1) decoded from depth planes [a, b) (plane 0 = surface, p = level group p-1)."""
+    return (max(a, 1) - 1) * level_patch, max(b - 1, 0) * level_patch
+
+
+def gather_plane_fields(surface: torch.Tensor, atmos: torch.Tensor, ranges: list[tuple[int, int]], rank: int,
+                        level_patch: int, group=None) -> None:
+    """In place: the decoded fields of every rank's planes (surface from the rank holding plane 0, atmosphere
+    levels of its level groups, all variables) copied into every rank's (surface, atmos) (one all-gather of
+    packed [surface | atmos[:, l0:l1]] chunks)."""
+    a_vars, _, rows, cols = atmos.shape
+
+    def count(a, b):
+        l0, l1 = _plane_levels(a, b, level_patch)
+        return (surface.numel() if a == 0 and b > 0 else 0) + a_vars * max(l1 - l0, 0) * rows * cols
+
+    lo, hi = ranges[rank]
+    l0, l1 = _plane_levels(lo, hi, level_patch)
+    chunks = ([surface.reshape(-1)] if lo == 0 and hi > 0 else []) + \
+        ([atmos[:, l0:l1].reshape(-1)] if l1 > l0 else [])
+    local = torch.cat(chunks) if chunks else surface.new_empty(0)
+    parts = _all_gather_var(local, [count(a, b) for a, b in ranges], group)
+    for r, ((a, b), part) in enumerate(zip(ranges, parts)):
+        if b <= a or r == rank:
+            continue
+        off = 0
+        if a == 0:
+            surface.view(-1).copy_(part[:surface.numel()])
+            off = surface.numel()
+        m0, m1 = _plane_levels(a, b, level_patch)
+        if m1 > m0:
+            atmos[:, m0:m1] = part[off:].view(a_vars, m1 - m0, rows, cols)
+
+
+def forecast_banded(state, dt: int, params: dict, cfg, world: int | None = None, group=None, fused: bool = False,
+                    source: str = "primary"):
+    """forecast() (rollout.py:84-91) with every stage split across ranks.
+
+    The encoder and decoder pyramids treat the depth planes independently, so each rank convolves only its
+    planes (`plane_ranges`: surface and level groups) and the latent tokens / decoded fields are all-gathered
+    by plane; the encoder, processor and decoder blocks run on latitude bands with the per-block halo exchange
+    (`BandedProcessor`, as rollout_banded).  Every rank returns the full DecodedFields.  `world` without a
+    group emulates the split in one process (plane ranges and bands one after another on one GPU).
+    Validation as forecast(), before any launch."""
+    from .model import CALL_COUNTS, DecodedFields, stage_inputs
+    from .pyramid import decode_planes, encode_planes
+    from .rollout import _check_plan, greedy_plan, plan_hours
+    from .tensor import Tensor
+
+    plan = _check_plan(greedy_plan(dt, cfg.max_dt), params, cfg)
+    dm, prefix = stage_inputs(state, params, cfg, source)
+    enc_p = [f"{prefix}.blk{i}" for i in range(cfg.enc_blocks)]
+    dec_p = [f"dec.blk{i}" for i in range(cfg.dec_blocks)]
+    first = (enc_p + [f"proc{hz}.blk0" for hz in plan] + dec_p + [None])[0]
+    fused = fused and first is not None
+    proc, bands, rank, n, distributed = _banded_setup(params, cfg, world, group, fused, first)
+    d, h, w = cfg.latent_extents
+    g = cfg.grid
+    pt = h * w  # tokens per depth plane
+    ranges = plane_ranges(d, n)
+    mine = [ranges[rank]] if distributed else ranges
+    bufs = dm.buffers()
+
+    # encoder pyramid by planes -> all-gather the token planes
+    tokens = torch.empty((cfg.tokens, cfg.hidden), dtype=torch.float32, device="cuda")
+    enc = dm.encoder(prefix)
+    for lo, hi in mine:
+        if hi > lo:
+            encode_planes(enc, bufs, cfg, tokens, (lo, hi))
+    if distributed:
+        gather_plane_tokens(tokens, ranges, rank, pt, group)
+
+    # latent blocks by latitude bands
+    held = [bands[rank]] if distributed else bands
+    xs = [local_band_tokens(tokens, cfg.latent_extents, b).clone() for b in held]
+    del tokens
+    proc.run(xs, enc_p)
+    for hz in plan:
+        proc.process(xs, hz)
+        CALL_COUNTS[f"process{hz}"] += 1
+    proc.run(xs, dec_p)
+    CALL_COUNTS["decode"] += 1
+    full = _gather_latent(xs, bands, cfg.latent_extents, distributed, group)
+    del xs
+
+    # decoder pyramid by planes -> all-gather the fields
+    surface = torch.empty((cfg.surface_out, g.rows, g.cols), dtype=torch.float32, device="cuda")
+    atmos = torch.empty((cfg.atmos_vars, cfg.levels, g.rows, g.cols), dtype=torch.float32, device="cuda")
+    dec = dm.decoder()
+    for lo, hi in mine:
+        if hi > lo:
+            decode_planes(dec, bufs, cfg, full, surface, atmos, (lo, hi))
+    if distributed:
+        gather_plane_fields(surface, atmos, ranges, rank, cfg.level_patch, group)
+    return DecodedFields(state.valid_time + plan_hours(plan), Tensor(device=surface), Tensor(device=atmos))

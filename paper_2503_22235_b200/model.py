@@ -159,8 +159,9 @@ def _tokens(lat: LatentState) -> torch.Tensor:
 # ------------------------------------------------------------------------------------------------
 # API
 # ------------------------------------------------------------------------------------------------
-def encode(state: WeatherState, params: dict, cfg: ModelConfig, source: str = PRIMARY_SOURCE) -> LatentState:
-    """Lift one gridded state into the latent token grid (model.py:363-390)."""
+def stage_inputs(state: WeatherState, params: dict, cfg: ModelConfig, source: str = PRIMARY_SOURCE):
+    """encode()'s validation (ConfigError before any launch) and the host->device copy of the state into the
+    pyramid input buffers; returns (device model, encoder weight prefix)."""
     prefix = encoder_prefix(source)
     if f"{prefix}.stem_sfc.w" not in params:
         raise ConfigError(f"no encoder for source {source!r}")
@@ -178,6 +179,13 @@ def encode(state: WeatherState, params: dict, cfg: ModelConfig, source: str = PR
         bufs.statics_ready = True
     bufs.sfc_in[:cfg.surface_in].copy_(_to_device(state.surface, None), non_blocking=True)
     bufs.atm_in.copy_(_to_device(state.atmos, None), non_blocking=True)
+    return dm, prefix
+
+
+def encode(state: WeatherState, params: dict, cfg: ModelConfig, source: str = PRIMARY_SOURCE) -> LatentState:
+    """Lift one gridded state into the latent token grid (model.py:363-390)."""
+    dm, prefix = stage_inputs(state, params, cfg, source)
+    bufs = dm.buffers()
     tokens = torch.empty((cfg.tokens, cfg.hidden), dtype=torch.float32, device="cuda")
     encode_planes(dm.encoder(prefix), bufs, cfg, tokens)
     dm.run_blocks(tokens, [f"{prefix}.blk{i}" for i in range(cfg.enc_blocks)])

@@ -167,81 +167,106 @@ class PyramidBuffers:
         return b
 
 
-def _res_block(ws: StageW, bufs: PyramidBuffers, level: int, x_idx: int, imgs: int, h: int, w: int, c: int) -> int:
-    """Two res blocks x + conv2(gelu(conv1(x))) (model.py:304-306) with ping-pong buffers; returns result idx."""
+def _res_block(ws: StageW, bufs: PyramidBuffers, level: int, x_idx: int, imgs: int, h: int, w: int, c: int,
+               lo: int = 0) -> int:
+    """Two res blocks x + conv2(gelu(conv1(x))) (model.py:304-306) with ping-pong buffers on images
+    [lo, lo + imgs); returns result idx."""
     for conv1, conv2 in ws.res:
         t_idx, y_idx = [k for k in range(3) if k != x_idx][:2]
-        x = bufs.buf(level, x_idx, c)
-        t = bufs.buf(level, t_idx, c)
-        y = bufs.buf(level, y_idx, c)
+        x = bufs.buf(level, x_idx, c)[lo:lo + imgs]
+        t = bufs.buf(level, t_idx, c)[lo:lo + imgs]
+        y = bufs.buf(level, y_idx, c)[lo:lo + imgs]
         run_conv(conv1, x, imgs, h, w, t, gelu=True)
         run_conv(conv2, t, imgs, h, w, y, resid=x)
         x_idx = y_idx
     return x_idx
 
 
-def encode_planes(ew: EncoderWeights, bufs: PyramidBuffers, cfg: ModelConfig, tokens_out: torch.Tensor) -> None:
-    """bufs.sfc_in / atm_in (device fp32) -> latent tokens (D*h*w, hidden) fp32."""
+def encode_planes(ew: EncoderWeights, bufs: PyramidBuffers, cfg: ModelConfig, tokens_out: torch.Tensor,
+                  planes: tuple[int, int] | None = None) -> None:
+    """bufs.sfc_in / atm_in (device fp32) -> latent tokens (D*h*w, hidden) fp32.
+
+    planes = (lo, hi) encodes only depth planes [lo, hi) (plane 0 = surface, p >= 1 = atmosphere level group
+    p - 1) into their token rows: the planes share the pyramid weights and never interact before the encoder
+    blocks, so the split is exact (bands.forecast_banded runs one range per rank)."""
     g = cfg.grid
     hh, ww = g.rows, g.cols
     d = cfg.depth_planes
-    grp = cfg.levels // cfg.level_patch
+    lo, hi = (0, d) if planes is None else (int(planes[0]), int(planes[1]))
+    if not 0 <= lo < hi <= d:
+        raise ConfigError(f"plane range {planes} outside [0, {d})")
+    n = hi - lo
     csfc = cfg.surface_in + N_STATIC_FIELDS
     catm = cfg.atmos_vars * cfg.level_patch
     hw = hh * ww
-    fields_to_nhwc(bufs.sfc_in, 1, csfc, hh, ww, bufs.in_sfc, 0, hw, 0, 1)
-    fields_to_nhwc(bufs.atm_in, grp, catm, hh, ww, bufs.in_atm, cfg.level_patch * hw, cfg.levels * hw, hw,
-                   cfg.level_patch)
     x0 = bufs.buf(0, 0, cfg.stem_channels)
-    run_conv(ew.stem_sfc, bufs.in_sfc, 1, hh, ww, x0[0:1])
-    run_conv(ew.stem_atm, bufs.in_atm, grp, hh, ww, x0[1:])
+    if lo == 0:
+        fields_to_nhwc(bufs.sfc_in, 1, csfc, hh, ww, bufs.in_sfc, 0, hw, 0, 1)
+        run_conv(ew.stem_sfc, bufs.in_sfc, 1, hh, ww, x0[0:1])
+    a0 = max(lo, 1)
+    if hi > a0:  # atmosphere level groups a0 - 1 .. hi - 2
+        fields_to_nhwc(bufs.atm_in.view(-1)[(a0 - 1) * cfg.level_patch * hw:], hi - a0, catm, hh, ww,
+                       bufs.in_atm[a0 - 1:hi - 1], cfg.level_patch * hw, cfg.levels * hw, hw, cfg.level_patch)
+        run_conv(ew.stem_atm, bufs.in_atm[a0 - 1:hi - 1], hi - a0, hh, ww, x0[a0:hi])
     x_idx, c = 0, cfg.stem_channels
     for i, st in enumerate(ew.stages):
         h2, w2 = hh >> (i + 1), ww >> (i + 1)
         c_out = cfg.stage_channels[i]
         last = i == DOWNSAMPLE_STAGES - 1
-        y = bufs.buf(i + 1, 0, c_out)
-        run_conv(st.resample, bufs.buf(i, x_idx, c), d, h2 * 2, w2 * 2, y)
+        y = bufs.buf(i + 1, 0, c_out)[lo:hi]
+        run_conv(st.resample, bufs.buf(i, x_idx, c)[lo:hi], n, h2 * 2, w2 * 2, y)
         x_idx = 0
         if not last:
-            x_idx = _res_block(st, bufs, i + 1, x_idx, d, h2, w2, c_out)
+            x_idx = _res_block(st, bufs, i + 1, x_idx, n, h2, w2, c_out, lo)
         else:
             # final res block writes the fp32 token grid directly (model.py:350-354)
             conv1, conv2 = st.res[0]
-            t, z = bufs.buf(i + 1, 1, c_out), bufs.buf(i + 1, 2, c_out)
-            run_conv(conv1, y, d, h2, w2, t, gelu=True)
-            run_conv(conv2, t, d, h2, w2, z, resid=y)
+            t, z = bufs.buf(i + 1, 1, c_out)[lo:hi], bufs.buf(i + 1, 2, c_out)[lo:hi]
+            run_conv(conv1, y, n, h2, w2, t, gelu=True)
+            run_conv(conv2, t, n, h2, w2, z, resid=y)
             conv1, conv2 = st.res[1]
-            run_conv(conv1, z, d, h2, w2, t, gelu=True)
-            run_conv(conv2, t, d, h2, w2, tokens_out, resid=z, kind=_lib.WM3_CONV_OUT_TOKENS)
+            run_conv(conv1, z, n, h2, w2, t, gelu=True)
+            run_conv(conv2, t, n, h2, w2, tokens_out[lo * h2 * w2:hi * h2 * w2], resid=z,
+                     kind=_lib.WM3_CONV_OUT_TOKENS)
             # residual add for the token output happens in-kernel from the padded skip buffer
         c = c_out
 
 
 def decode_planes(dw: DecoderWeights, bufs: PyramidBuffers, cfg: ModelConfig, tokens: torch.Tensor,
-                  surface_out: torch.Tensor, atmos_out: torch.Tensor) -> None:
-    """latent tokens (fp32) -> surface (surface_out, H, W) and atmos (A, L, H, W) fp32 fields."""
+                  surface_out: torch.Tensor, atmos_out: torch.Tensor, planes: tuple[int, int] | None = None) -> None:
+    """latent tokens (fp32) -> surface (surface_out, H, W) and atmos (A, L, H, W) fp32 fields.
+
+    planes = (lo, hi): only depth planes [lo, hi) (surface if lo == 0, atmosphere levels of groups lo-1..hi-2)
+    are decoded; the up-pyramid treats planes independently, so the split is exact."""
     g = cfg.grid
     d, h, w = cfg.latent_extents
+    lo, hi = (0, d) if planes is None else (int(planes[0]), int(planes[1]))
+    if not 0 <= lo < hi <= d:
+        raise ConfigError(f"plane range {planes} outside [0, {d})")
+    n = hi - lo
     lvl = DOWNSAMPLE_STAGES
-    x = bufs.buf(lvl, 0, cfg.hidden)
-    tokens_to_nhwc(tokens, d, h, w, x)
+    x = bufs.buf(lvl, 0, cfg.hidden)[lo:hi]
+    tokens_to_nhwc(tokens[lo * h * w:hi * h * w], n, h, w, x)
     chans = [cfg.hidden] + list(cfg.stage_channels[-2::-1]) + [cfg.stem_channels]
     x_idx = 0
     for i, st in enumerate(dw.stages):
-        src = bufs.buf(lvl - i, x_idx, chans[i])
+        src = bufs.buf(lvl - i, x_idx, chans[i])[lo:hi]
         lvl_out = lvl - i - 1
         ho, wo = g.rows >> lvl_out, g.cols >> lvl_out
-        y = bufs.buf(lvl_out, 0, chans[i + 1])
-        run_conv(st.resample, src, d, ho // 2, wo // 2, y)
-        x_idx = _res_block(st, bufs, lvl_out, 0, d, ho, wo, chans[i + 1])
+        y = bufs.buf(lvl_out, 0, chans[i + 1])[lo:hi]
+        run_conv(st.resample, src, n, ho // 2, wo // 2, y)
+        x_idx = _res_block(st, bufs, lvl_out, 0, n, ho, wo, chans[i + 1], lo)
     full = bufs.buf(0, x_idx, cfg.stem_channels)
     hh, ww = g.rows, g.cols
-    run_conv(dw.head_sfc, full[0:1], 1, hh, ww, surface_out, kind=_lib.WM3_CONV_OUT_FIELD, img_stride=0,
-             a_stride=hh * ww, p_stride=0, chan_div=1)
+    if lo == 0:
+        run_conv(dw.head_sfc, full[0:1], 1, hh, ww, surface_out, kind=_lib.WM3_CONV_OUT_FIELD, img_stride=0,
+                 a_stride=hh * ww, p_stride=0, chan_div=1)
     p = cfg.level_patch
-    run_conv(dw.head_atm, full[1:], d - 1, hh, ww, atmos_out, kind=_lib.WM3_CONV_OUT_FIELD, img_stride=p * hh * ww,
-             a_stride=cfg.levels * hh * ww, p_stride=hh * ww, chan_div=p)
+    a0 = max(lo, 1)
+    if hi > a0:  # level groups a0 - 1 .. hi - 2 -> levels [(a0 - 1) p, (hi - 1) p)
+        dst = atmos_out.view(-1)[(a0 - 1) * p * hh * ww:]
+        run_conv(dw.head_atm, full[a0:hi], hi - a0, hh, ww, dst, kind=_lib.WM3_CONV_OUT_FIELD,
+                 img_stride=p * hh * ww, a_stride=cfg.levels * hh * ww, p_stride=hh * ww, chan_div=p)
 
 
 def check_grid(cfg: ModelConfig) -> None:

@@ -180,3 +180,59 @@ def test_rollout_banded_gloo_sharding_and_gather():
     for rank, vt, got in res:
         assert vt == 5 + 8
         np.testing.assert_allclose(got.reshape(d, h, w, 4), want, rtol=0, atol=1e-12)
+
+
+def _planes_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2503_22235_b200.bands as B
+        d, pt, hidden, p, a_vars, rows, cols = 5, 6, 3, 2, 3, 4, 5
+        rng = np.random.default_rng(11)
+        tok_full = torch.from_numpy(rng.standard_normal((d * pt, hidden)))
+        sfc_full = torch.from_numpy(rng.standard_normal((2, rows, cols)))
+        atm_full = torch.from_numpy(rng.standard_normal((a_vars, (d - 1) * p, rows, cols)))
+        ranges = B.plane_ranges(d, world)
+        lo, hi = ranges[rank]
+        # each rank holds only its own planes; everything else is garbage before the gathers
+        tokens = torch.full_like(tok_full, float("nan"))
+        tokens[lo * pt:hi * pt] = tok_full[lo * pt:hi * pt]
+        sfc = torch.full_like(sfc_full, float("nan"))
+        atm = torch.full_like(atm_full, float("nan"))
+        if lo == 0 and hi > 0:
+            sfc.copy_(sfc_full)
+        l0, l1 = B._plane_levels(lo, hi, p)
+        atm[:, l0:l1] = atm_full[:, l0:l1]
+        B.gather_plane_tokens(tokens, ranges, rank, pt)
+        B.gather_plane_fields(sfc, atm, ranges, rank, p)
+        ok = (torch.equal(tokens, tok_full) and torch.equal(sfc, sfc_full) and torch.equal(atm, atm_full))
+        out_q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 7])
+def test_plane_gathers_gloo(world):
+    """forecast_banded's encoder-token and decoded-field all-gathers by depth plane (surface + level groups),
+    including ranks that hold no plane (world > depth)."""
+    ctx = mp.get_context("spawn")
+    q_out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_planes_worker, args=(r, world, port, q_out)) for r in range(world)]
+    for p_ in procs:
+        p_.start()
+    res = [q_out.get(timeout=120) for _ in range(world)]
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    assert all(ok for _, ok in res), res
+
+
+def test_plane_ranges():
+    from paper_2503_22235_b200.bands import plane_ranges
+    assert plane_ranges(5, 1) == [(0, 5)]
+    assert plane_ranges(5, 2) == [(0, 3), (3, 5)]
+    assert plane_ranges(5, 8)[4:] == [(4, 5), (5, 5), (5, 5), (5, 5)]
+    for world in range(1, 10):
+        r = plane_ranges(5, world)
+        assert r[0][0] == 0 and r[-1][1] == 5 and all(a[1] == b[0] for a, b in zip(r, r[1:]))

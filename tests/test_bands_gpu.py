@@ -137,11 +137,12 @@ def test_halo_flag_kernels_self_signal():
 
 
 def test_banded_forecast_full_scale_bands_8():
-    """The bench's N = 8 forecast path (encode -> rollout_banded -> decode) at full latent scale, with the eight
-    latitude bands emulated on this GPU: decoded fields match the single-GPU forecast to fp16 round-off."""
+    """The bench's N = 8 forecast path (bands.forecast_banded: encoder / decoder pyramids split by depth plane,
+    every latent block on latitude bands) at full scale, with the eight ranks emulated on this GPU: decoded
+    fields match the single-GPU forecast to fp16 round-off."""
     import paper_2503_22235_b200.model as m
     import paper_2503_22235_b200.rollout as r
-    from paper_2503_22235_b200.bands import rollout_banded
+    from paper_2503_22235_b200.bands import forecast_banded
     cfg = m.full_scale_config()
     params = m.init_model_params(cfg, seed=0, zero_residual=False)
     g = cfg.grid
@@ -149,11 +150,71 @@ def test_banded_forecast_full_scale_bands_8():
     st = m.WeatherState(0, torch.from_numpy(rng.standard_normal((cfg.surface_in, g.rows, g.cols)).astype(np.float32)).cuda(),
                         torch.from_numpy(rng.standard_normal((cfg.atmos_vars, cfg.levels, g.rows, g.cols))
                                          .astype(np.float32)).cuda())
-    lat = m.encode(st, params, cfg)
-    one = m.decode(r.rollout(lat, (6, 1), params, cfg), params, cfg)
-    banded = m.decode(rollout_banded(lat, (6, 1), params, cfg, world=8), params, cfg)
+    one = r.forecast(st, 7, params, cfg)
+    banded = forecast_banded(st, 7, params, cfg, world=8)
+    assert banded.valid_time == one.valid_time == 7
     a, b = one.surface.device, banded.surface.device
     rel = float((a - b).norm() / a.norm())
     assert rel < 5e-3, rel
     a, b = one.atmos.device, banded.atmos.device
     assert float((a - b).norm() / a.norm()) < 5e-3
+
+
+@pytest.mark.parametrize("name", ["desk", "mid"])
+def test_pyramid_plane_ranges_bitwise(name):
+    """encode_planes / decode_planes over plane ranges (the per-rank split of forecast_banded) write exactly
+    the bytes the all-plane launches write: the pyramid never mixes depth planes."""
+    import paper_2503_22235_b200.model as m
+    from paper_2503_22235_b200.bands import plane_ranges
+    from paper_2503_22235_b200.pyramid import decode_planes, encode_planes
+    cfg = {"desk": m.desk_config, "mid": m.mid_config}[name]()
+    params = m.init_model_params(cfg, seed=3, zero_residual=False)
+    rng = np.random.default_rng(8)
+    g = cfg.grid
+    st = m.WeatherState(0, rng.standard_normal((cfg.surface_in, g.rows, g.cols)),
+                        rng.standard_normal((cfg.atmos_vars, cfg.levels, g.rows, g.cols)))
+    dm, prefix = m.stage_inputs(st, params, cfg)
+    bufs, enc = dm.buffers(), dm.encoder(prefix)
+    full = torch.empty((cfg.tokens, cfg.hidden), device="cuda")
+    encode_planes(enc, bufs, cfg, full)
+    d = cfg.depth_planes
+    sfc_full = torch.empty((cfg.surface_out, g.rows, g.cols), device="cuda")
+    atm_full = torch.empty((cfg.atmos_vars, cfg.levels, g.rows, g.cols), device="cuda")
+    decode_planes(dm.decoder(), bufs, cfg, full, sfc_full, atm_full)
+    for world in (2, 3, d):
+        split = torch.full_like(full, float("nan"))
+        sfc = torch.full_like(sfc_full, float("nan"))
+        atm = torch.full_like(atm_full, float("nan"))
+        for lo, hi in plane_ranges(d, world):
+            encode_planes(enc, bufs, cfg, split, (lo, hi))
+        for lo, hi in reversed(plane_ranges(d, world)):
+            decode_planes(dm.decoder(), bufs, cfg, full, sfc, atm, (lo, hi))
+        torch.cuda.synchronize()
+        assert torch.equal(split, full), world
+        assert torch.equal(sfc, sfc_full) and torch.equal(atm, atm_full), world
+    with pytest.raises(m.ConfigError):
+        encode_planes(enc, bufs, cfg, full, (2, 2))
+
+
+@pytest.mark.parametrize("name,world", [("desk", 3), ("mid", 2)])
+def test_forecast_banded_matches_forecast(name, world):
+    """forecast_banded (plane-split pyramids + banded encoder / processor / decoder blocks, ranks emulated on
+    this GPU) reproduces forecast() to fp16 round-off; validation matches forecast()."""
+    import paper_2503_22235_b200.model as m
+    import paper_2503_22235_b200.rollout as r
+    from paper_2503_22235_b200.bands import forecast_banded
+    cfg = {"desk": m.desk_config, "mid": m.mid_config}[name]()
+    params = m.init_model_params(cfg, seed=7, zero_residual=False)
+    rng = np.random.default_rng(4)
+    g = cfg.grid
+    st = m.WeatherState(2, rng.standard_normal((cfg.surface_in, g.rows, g.cols)),
+                        rng.standard_normal((cfg.atmos_vars, cfg.levels, g.rows, g.cols)))
+    for dt in (0, 13):
+        one = r.forecast(st, dt, params, cfg)
+        banded = forecast_banded(st, dt, params, cfg, world=world)
+        assert banded.valid_time == one.valid_time == 2 + dt
+        for a, b in ((one.surface.device, banded.surface.device), (one.atmos.device, banded.atmos.device)):
+            rel = float((a - b).norm() / a.norm())
+            assert rel < 5e-3, (dt, rel)
+    with pytest.raises(m.ConfigError):
+        forecast_banded(st, cfg.max_dt + 1, params, cfg, world=world)
