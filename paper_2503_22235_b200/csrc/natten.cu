@@ -41,15 +41,23 @@ struct NaParams {
   int dbg;  // profiling switch (WM3_NA_DEBUG, bit flags): 1 skip softmax arithmetic, 2 skip Q K^T, 4 skip P V, 8 skip K/V loads
 };
 
-constexpr int NA_SOFTMAX_WARPS = 4;
-constexpr int NA_MMA_WARP = 4;
-constexpr int NA_TMA_WARP = 5;
-constexpr int NA_THREADS = 192;
+#ifndef WM3_NA_SPLIT
+#define WM3_NA_SPLIT 1
+#endif
+// Softmax threads per query row: each handles 64 / NA_SPLIT of the 64 columns of an S half (the partner
+// threads of a row sit in warps w and w + 4, which see the same TMEM lanes) and they exchange the row max
+// through shared memory, which halves the per-half softmax chain.
+constexpr int NA_SPLIT = WM3_NA_SPLIT;
+constexpr int NA_SOFTMAX_WARPS = 4 * NA_SPLIT;
+constexpr int NA_MMA_WARP = NA_SOFTMAX_WARPS;
+constexpr int NA_TMA_WARP = NA_SOFTMAX_WARPS + 1;
+constexpr int NA_THREADS = 32 * (NA_SOFTMAX_WARPS + 2);
 constexpr int NA_CTAS_PER_SM = 2;
 constexpr uint32_t NA_TILE = 32768;  // 128 rows x 256 B
-// smem: Q | K | V | barriers (256 B)
+// smem: Q | K | V | barriers (256 B) | row-max / row-sum exchange (2 halves + 1) x NA_SPLIT x 128 floats
 constexpr uint32_t NA_SMEM_BODY = 3 * NA_TILE;
-constexpr uint32_t NA_SMEM = NA_SMEM_BODY + 1024 /*align*/ + 256 /*barriers*/;
+constexpr uint32_t NA_RED_BYTES = 3 * NA_SPLIT * 128 * 4;
+constexpr uint32_t NA_SMEM = NA_SMEM_BODY + 1024 /*align*/ + 256 /*barriers*/ + NA_RED_BYTES;
 // TMEM columns (256 per CTA): S / P [0, 128), O [128, 256).  S(c + 1) may overwrite P(c) without a wait
 // because tcgen05.mma ops of one thread execute in issue order and S(c + 1) is issued after P V(c).
 constexpr uint32_t NA_TMEM_COLS = 256, NA_TMEM_O = 128;
@@ -160,6 +168,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
   auto bar_pfull = [&](int h) { return b0 + 80 + 8 * h; };   // P half h written by the 4 softmax warps
   auto bar_pvdone = [&](int h) { return b0 + 96 + 8 * h; };  // P V over key half h retired
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  float* red = reinterpret_cast<float*>(smem + NA_SMEM_BODY + 256);  // [3][NA_SPLIT][128]
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -301,13 +310,17 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
     }
   } else {
     // =============================== softmax / epilogue ===============================
-    // Thread = query row (TMEM lane) of the tile.  Online softmax over key halves of 64: masked max, lazy max
-    // update (O rescaled only when the max grows by > 2^8), exp2, row sum, P_h -> TMEM columns [64 h, +32).
-    const int row = 32 * warp + lane;
-    const uint32_t lane_off = static_cast<uint32_t>(32 * warp) << 16;
+    // Thread = (query row = TMEM lane, column sub-range) of the tile.  Online softmax over key halves of 64:
+    // masked max (combined across the row's NA_SPLIT threads), lazy max update (O rescaled only when the max
+    // grows by > 2^8), exp2, partial row sum, P_h -> TMEM columns [64 h, +32).
+    constexpr int CW = 64 / NA_SPLIT;  // S columns per thread per half
+    const int g4 = warp & 3, sub = warp >> 2;
+    const int row = 32 * g4 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(32 * g4) << 16;
     const uint32_t tS = tmem + lane_off, tO = tmem + NA_TMEM_O + lane_off;
     const int hw = (p.ww - 1) / 2;
     const size_t member_tokens = static_cast<size_t>(p.depth) * p.rows * p.cols;
+    const int ocols = p.dhp / NA_SPLIT, oc0 = sub * ocols;  // O columns this thread rescales / stores
     int chunk_ctr = 0, tile_ctr = 0;
     for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
       const TileGeo g = tile_geo(p, item);
@@ -322,61 +335,83 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
       const int c_lo = circle ? wrap_col((qvalid ? qw : g.w0) - hw, p.cols) : (qvalid ? qw : g.w0) - hw - g.pc0;
       const int s2hi = circle ? c_lo + p.ww - g.ncp : 0;
       float m_run = -INFINITY, l_run = 0.f;
-      // window masks depend on (row chunk, part) only, not on the depth plane: cache one per part
+      // window masks depend on (row chunk, part) only, not on the depth plane: cache one per part, keeping
+      // only the MWN words of this thread's columns (word h * CW / 32 + i = columns CW * sub + 32 i of half h)
+      constexpr int MWN = 4 / NA_SPLIT;
       int key0 = -1, key1 = -1;
-      uint32_t mc0[4], mc1[4];
+      uint32_t mc0[MWN], mc1[MWN];
+      auto own_words = [&](const uint32_t (&m)[4], uint32_t (&o)[MWN]) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int i = 0; i < CW / 32; ++i) o[h * (CW / 32) + i] = sub ? m[2 * h + i + CW / 32] : m[2 * h + i];
+      };
       for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
         int kd, kr0, nr, origin, vlo, vhi;
         chunk_geo(g, p.cols, j, kd, kr0, nr, origin, vlo, vhi);
         const int part = j % g.nparts, key = (j / g.nparts) % g.nrchunks;
-        if (part == 0 && key != key0) {
-          window_mask(mc0, nr, g.ncp, max(0, q_sh - kr0), min(nr, q_sh + p.wh - kr0), max(c_lo, vlo),
+        if ((part == 0 && key != key0) || (part == 1 && key != key1)) {
+          uint32_t m4[4];
+          window_mask(m4, nr, g.ncp, max(0, q_sh - kr0), min(nr, q_sh + p.wh - kr0), max(c_lo, vlo),
                       min(c_lo + p.ww, vhi), s2hi);
-          key0 = key;
-        } else if (part == 1 && key != key1) {
-          window_mask(mc1, nr, g.ncp, max(0, q_sh - kr0), min(nr, q_sh + p.wh - kr0), max(c_lo, vlo),
-                      min(c_lo + p.ww, vhi), s2hi);
-          key1 = key;
+          if (part == 0) {
+            own_words(m4, mc0);
+            key0 = key;
+          } else {
+            own_words(m4, mc1);
+            key1 = key;
+          }
         }
         const bool dok = qvalid && kd >= q_sd && kd < q_sd + p.wd;
-        uint32_t mw[4];
+        uint32_t mw[MWN];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) mw[w] = dok ? (part == 0 ? mc0[w] : mc1[w]) : 0u;
+        for (int w = 0; w < MWN; ++w) mw[w] = dok ? (part == 0 ? mc0[w] : mc1[w]) : 0u;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           mbar_wait(bar_sfull(h), chunk_ctr & 1);
           tc_fence_after();
-          uint32_t pk[32];
+          uint32_t pk[CW / 2];
           if (p.dbg & 1) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) pk[i] = 0u;
+            for (int i = 0; i < CW / 2; ++i) pk[i] = 0u;
           } else {
-            uint32_t x[64];
-            tmem_ld32(tS + 64 * h, *reinterpret_cast<uint32_t(*)[32]>(x));
-            tmem_ld32(tS + 64 * h + 32, *reinterpret_cast<uint32_t(*)[32]>(x + 32));
+            uint32_t x[CW];
+            const uint32_t scol = tS + 64 * h + CW * sub;
+#pragma unroll
+            for (int i = 0; i < CW / 32; ++i)
+              tmem_ld32(scol + 32 * i, *reinterpret_cast<uint32_t(*)[32]>(x + 32 * i));
             tmem_ld_wait();
             float mxa[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) mxa[i] = -INFINITY;
 #pragma unroll
-            for (int k = 0; k < 64; k += 2) {
-              const uint32_t wbits = mw[2 * h + (k >> 5)];
+            for (int k = 0; k < CW; k += 2) {
+              const uint32_t wbits = mw[h * (CW / 32) + (k >> 5)];
               const float a0 = ((wbits >> (k & 31)) & 1u) ? __uint_as_float(x[k]) : -INFINITY;
               const float a1 = ((wbits >> ((k + 1) & 31)) & 1u) ? __uint_as_float(x[k + 1]) : -INFINITY;
               x[k] = __float_as_uint(a0);
               x[k + 1] = __float_as_uint(a1);
               mxa[(k >> 1) & 7] = fmaxf(mxa[(k >> 1) & 7], fmaxf(a0, a1));
             }
-            const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
-                                   fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7]))) * p.scale_log2;
+            float mxl = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                              fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
+            if (NA_SPLIT > 1) {
+              // the barrier also orders the partners' S loads before either overwrites S with P
+              red[(h * NA_SPLIT + sub) * 128 + row] = mxl;
+              named_bar_sync(1 + g4, 32 * NA_SPLIT);
+#pragma unroll
+              for (int o = 1; o < NA_SPLIT; ++o) mxl = fmaxf(mxl, red[(h * NA_SPLIT + (sub ^ o)) * 128 + row]);
+            }
+            const float mx = mxl * p.scale_log2;
+            const bool had = m_run != -INFINITY;  // O already holds weight of this row
             float alpha = 1.f;
             if (mx > m_run + NA_RESCALE_LOG2) {  // lazy max update (also covers m_run = -inf)
               alpha = exp2f(m_run - mx);
               m_run = mx;
             }
-            // O holds weight only once l_run > 0; rescaling it needs the one P V that may still be in flight
-            // (issued right after the S half just waited on): PV1(c - 1) for half 0, PV0(c) for half 1.
-            const bool resc = alpha != 1.f && l_run > 0.f;
+            // rescaling O needs the one P V that may still be in flight (issued right after the S half just
+            // waited on): PV1(c - 1) for half 0, PV0(c) for half 1.  The row's threads agree on `resc`.
+            const bool resc = alpha != 1.f && had;
             l_run *= alpha;
             if (__any_sync(0xffffffffu, resc)) {
               if (h == 0) mbar_wait(bar_pvdone(1), (chunk_ctr - 1) & 1);
@@ -384,13 +419,13 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
               tc_fence_after();
               const float f = resc ? alpha : 1.f;
 #pragma unroll 1
-              for (int c = 0; c < p.dhp / 32; ++c) {
+              for (int c = oc0; c < oc0 + ocols; c += 32) {
                 uint32_t r[32];
-                tmem_ld32(tO + 32 * c, r);
+                tmem_ld32(tO + c, r);
                 tmem_ld_wait();
 #pragma unroll
                 for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * f);
-                tmem_st32(tO + 32 * c, r);
+                tmem_st32(tO + c, r);
               }
             }
             const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
@@ -398,7 +433,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
 #pragma unroll
             for (int i = 0; i < 8; ++i) lsa[i] = 0.f;
 #pragma unroll
-            for (int k = 0; k < 64; k += 2) {
+            for (int k = 0; k < CW; k += 2) {
               const float p0 = fast_exp2(fmaf(__uint_as_float(x[k]), p.scale_log2, -m_use));  // exp2(-inf) = 0
               const float p1 = fast_exp2(fmaf(__uint_as_float(x[k + 1]), p.scale_log2, -m_use));
               lsa[(k >> 1) & 7] += p0 + p1;
@@ -406,7 +441,9 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
             }
             l_run += ((lsa[0] + lsa[1]) + (lsa[2] + lsa[3])) + ((lsa[4] + lsa[5]) + (lsa[6] + lsa[7]));
           }
-          tmem_st32(tS + 64 * h, pk);  // P_h over the first 32 of the S_h columns just read
+          // P_h (fp16 pairs) over S_h columns [64 h, 64 h + 32): this thread's keys -> CW / 2 columns
+          if constexpr (CW == 64) tmem_st32(tS + 64 * h, *reinterpret_cast<uint32_t(*)[32]>(pk));
+          else tmem_st16(tS + 64 * h + (CW / 2) * sub, *reinterpret_cast<uint32_t(*)[16]>(pk));
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
@@ -414,29 +451,33 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
         }
       }
       // ---- epilogue: O / l -> ctx ----
+      if (NA_SPLIT > 1) {
+        red[(2 * NA_SPLIT + sub) * 128 + row] = l_run;
+        named_bar_sync(1 + g4, 32 * NA_SPLIT);
+        float lt = l_run;
+#pragma unroll
+        for (int o = 1; o < NA_SPLIT; ++o) lt += red[(2 * NA_SPLIT + (sub ^ o)) * 128 + row];
+        l_run = lt;
+      }
       const float inv_l = (qvalid && l_run > 0.f) ? 1.f / l_run : 0.f;
       mbar_wait(bar_ofull, tile_ctr & 1);
       tc_fence_after();
       const size_t tok = g.b * member_tokens + static_cast<size_t>((qd * p.rows + qh) * p.cols + qw);
       elem_t* orow = p.out + (qvalid ? tok * p.ldo + g.head * p.dhp : 0);
-      // all of O's row in one batch of TMEM loads, then 256-bit stores (whole 32-byte sectors)
+      // this thread's O columns in batches of 32 TMEM columns, then 256-bit stores (whole 32-byte sectors)
+#pragma unroll 1
+      for (int c0 = oc0; c0 < oc0 + ocols; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tO + c0, r);
+        tmem_ld_wait();
+        if (qvalid) {
 #pragma unroll
-      for (int c0 = 0; c0 < 128; c0 += 64) {
-        if (c0 < p.dhp) {
-          uint32_t r[64];
-          tmem_ld32(tO + c0, *reinterpret_cast<uint32_t(*)[32]>(r));
-          tmem_ld32(tO + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
-          tmem_ld_wait();
-          if (qvalid) {
+          for (int q = 0; q < 2; ++q) {
+            uint32_t u[8];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint32_t u[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e)
-                u[e] = pack_elem(__uint_as_float(r[16 * q + 2 * e]) * inv_l,
-                                 __uint_as_float(r[16 * q + 2 * e + 1]) * inv_l);
-              stg256(orow + c0 + 16 * q, u);
-            }
+            for (int e = 0; e < 8; ++e)
+              u[e] = pack_elem(__uint_as_float(r[16 * q + 2 * e]) * inv_l, __uint_as_float(r[16 * q + 2 * e + 1]) * inv_l);
+            stg256(orow + c0 + 16 * q, u);
           }
         }
       }
