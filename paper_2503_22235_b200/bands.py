@@ -493,9 +493,10 @@ def forecast_banded(state, dt: int, params: dict, cfg, world: int | None = None,
     ranges = plane_ranges(d, n)
     mine = [ranges[rank]] if distributed else ranges
     bufs = dm.buffers()
+    dev = bufs.sfc_in.device
 
     # encoder pyramid by planes -> all-gather the token planes
-    tokens = torch.empty((cfg.tokens, cfg.hidden), dtype=torch.float32, device="cuda")
+    tokens = torch.empty((cfg.tokens, cfg.hidden), dtype=torch.float32, device=dev)
     enc = dm.encoder(prefix)
     for lo, hi in mine:
         if hi > lo:
@@ -517,8 +518,8 @@ def forecast_banded(state, dt: int, params: dict, cfg, world: int | None = None,
     del xs
 
     # decoder pyramid by planes -> all-gather the fields
-    surface = torch.empty((cfg.surface_out, g.rows, g.cols), dtype=torch.float32, device="cuda")
-    atmos = torch.empty((cfg.atmos_vars, cfg.levels, g.rows, g.cols), dtype=torch.float32, device="cuda")
+    surface = torch.empty((cfg.surface_out, g.rows, g.cols), dtype=torch.float32, device=dev)
+    atmos = torch.empty((cfg.atmos_vars, cfg.levels, g.rows, g.cols), dtype=torch.float32, device=dev)
     dec = dm.decoder()
     for lo, hi in mine:
         if hi > lo:

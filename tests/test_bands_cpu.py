@@ -236,3 +236,102 @@ def test_plane_ranges():
     for world in range(1, 10):
         r = plane_ranges(5, world)
         assert r[0][0] == 0 and r[-1][1] == 5 and all(a[1] == b[0] for a, b in zip(r, r[1:]))
+
+
+class _FakeBlocks(_FakeProcessor):
+    def run(self, xs, prefixes):
+        d, h, w = self.ext
+        for b, x in zip(self.held, xs):
+            rows = torch.arange(b.row0, b.row0 + b.rows, dtype=x.dtype).view(1, -1, 1, 1)
+            x.view(d, b.rows, w, -1).add_((rows + 1.0) * 0.5 * len(prefixes))
+
+
+def _fake_pyramid(cfg):
+    """CPU stand-ins for the pyramid launches: encode writes fixed per-plane token values, decode writes
+    per-plane sums of the (gathered) latent into the plane's surface / atmosphere levels."""
+    d, h, w = cfg.latent_extents
+    pt = h * w
+    base = torch.from_numpy(np.random.default_rng(5).standard_normal((d, pt, cfg.hidden)))
+
+    def encode_planes(enc, bufs, cfg_, tokens, planes):
+        lo, hi = planes
+        tokens.view(d, pt, -1)[lo:hi] = base[lo:hi].to(tokens.dtype)
+
+    def decode_planes(dec, bufs, cfg_, full, surface, atmos, planes):
+        lo, hi = planes
+        x = full.view(d, pt, -1)
+        p = cfg.level_patch
+        if lo == 0:
+            surface.copy_(x[0].sum() + torch.arange(surface.numel(), dtype=surface.dtype).view(surface.shape))
+        for plane in range(max(lo, 1), hi):
+            for lev in range((plane - 1) * p, plane * p):
+                atmos[:, lev] = x[plane].sum() + lev + 100 * torch.arange(atmos.shape[0], dtype=atmos.dtype
+                                                                          ).view(-1, 1, 1)
+    return base, encode_planes, decode_planes
+
+
+def _forecast_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2503_22235_b200.bands as B
+        import paper_2503_22235_b200.model as M
+        import paper_2503_22235_b200.pyramid as P
+        cfg = M.mid_config()
+        g = cfg.grid
+        _, P.encode_planes, P.decode_planes = _fake_pyramid(cfg)
+        B.BandedProcessor = _FakeBlocks
+        M.device_model = lambda params, cfg: None
+
+        class _DM:
+            def buffers(self):
+                class _B:
+                    sfc_in = torch.zeros(1, dtype=torch.float32)
+                return _B()
+
+            def encoder(self, prefix):
+                return None
+
+            def decoder(self):
+                return None
+
+        M.stage_inputs = lambda state, params, cfg, source="primary": (_DM(), "enc")
+        params = {f"proc{h}.blk0.ln1.gain": None for h in cfg.horizons}
+        st = M.WeatherState(3, np.zeros((cfg.surface_in, g.rows, g.cols)),
+                            np.zeros((cfg.atmos_vars, cfg.levels, g.rows, g.cols)))
+        out = B.forecast_banded(st, 13, params, cfg)
+        out_q.put((rank, out.valid_time, out.surface.device.numpy(), out.atmos.device.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_forecast_banded_gloo_plumbing():
+    """forecast_banded's distributed branch (the bench's N > 1 forecast) under a real gloo group, with CPU
+    stand-ins for the kernels: plane-split encode -> token all-gather -> banded encoder / processor / decoder
+    blocks -> band all-gather -> plane-split decode -> field all-gather; every rank returns the full fields."""
+    import paper_2503_22235_b200.model as M
+    cfg = M.mid_config()
+    world = 2  # mid: 9 latent rows, 7 depth planes -> planes (0, 4), (4, 7)
+    ctx = mp.get_context("spawn")
+    q_out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_forecast_worker, args=(r, world, port, q_out)) for r in range(world)]
+    for p_ in procs:
+        p_.start()
+    res = [q_out.get(timeout=180) for _ in range(world)]
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    # expected: tokens = base + (row + 1) * (0.5 * enc_blocks + 13 + 0.5 * dec_blocks), decoded by the fake
+    d, h, w = cfg.latent_extents
+    base, _, dec = _fake_pyramid(cfg)
+    x = base.view(d, h, w, -1).double() + (torch.arange(h, dtype=torch.float64).view(1, -1, 1, 1) + 1.0) * \
+        (0.5 * cfg.enc_blocks + 13 + 0.5 * cfg.dec_blocks)
+    g = cfg.grid
+    sfc = torch.zeros((cfg.surface_out, g.rows, g.cols), dtype=torch.float32)
+    atm = torch.zeros((cfg.atmos_vars, cfg.levels, g.rows, g.cols), dtype=torch.float32)
+    dec(None, None, cfg, x.float().reshape(d * h * w, -1), sfc, atm, (0, d))
+    for rank, vt, s, a in res:
+        assert vt == 3 + 13
+        np.testing.assert_allclose(s, sfc.numpy(), rtol=1e-5)
+        np.testing.assert_allclose(a, atm.numpy(), rtol=1e-5)
