@@ -138,6 +138,13 @@ def copy_halos(bands: list[Band], workspaces: list) -> None:
             me[:, b.halo_lo + b.rows:] = src[:, dn.halo_lo:dn.halo_lo + b.halo_hi]
 
 
+@dataclass(frozen=True)
+class GridGeo:
+    """What a neighbour needs to know about a band's K/V grid to store halo rows into it."""
+    rows_ext: int
+    qkv_ld: int
+
+
 def halo_descriptor(me: int, bands: list[Band], grids: list, qkv_ptrs: list, cols: int, sec: int):
     """wm3_halo_t for band `me`: its first halo_hi[up] rows go to the bottom halo of the band above, its last
     halo_lo[down] rows to the top halo of the band below (same rows HaloExchanger / copy_halos move).
@@ -203,15 +210,12 @@ class PeerHalo:
 
     def descriptor(self, grid, cols: int, sec: int):
         """wm3_halo_t pointing at the neighbours' peer-mapped K/V grids."""
-        class _G:
-            def __init__(self, rows_ext, qkv_ld):
-                self.rows_ext, self.qkv_ld = rows_ext, qkv_ld
         grids = [None] * len(self.bands)
         ptrs = [None] * len(self.bands)
         for r, t in self.peer_qkv.items():
-            grids[r] = _G(self.geo[r]["rows_ext"], self.geo[r]["qkv_ld"])
+            grids[r] = GridGeo(self.geo[r]["rows_ext"], self.geo[r]["qkv_ld"])
             ptrs[r] = t.data_ptr()
-        grids[self.rank] = _G(grid.rows_ext, self.qkv_ld)
+        grids[self.rank] = GridGeo(grid.rows_ext, self.qkv_ld)
         return halo_descriptor(self.rank, self.bands, grids, ptrs, cols, sec)
 
     def _signal(self, idx_in_up: int, idx_in_dn: int, epoch: int) -> None:
@@ -289,20 +293,14 @@ class BandedProcessor:
                 peer.before_qkv()
             geoms = [_lib.BlockGeomT(1, ext[0], ext[1], ext[2], h, b.row0, b.halo_lo, b.halo_hi, *cfg.window)
                      for b, ext in zip(self.held, self.local)]
+            local_grids = [GridGeo(w_.grid.rows_ext, w_.qkv.stride(0)) for w_ in wss]
             for j, (b, ext, xb, ws) in enumerate(zip(self.held, self.local, xs, wss)):
                 halo = None
                 if self.fused:
                     if peer is not None:
                         halo = peer.descriptor(ws.grid, cols, sec)
                     else:  # emulation: the neighbours are the other held bands' grids on this GPU
-                        class _G:
-                            pass
-                        grids = []
-                        for w_ in wss:
-                            g_ = _G()
-                            g_.rows_ext, g_.qkv_ld = w_.grid.rows_ext, w_.qkv.stride(0)
-                            grids.append(g_)
-                        halo = halo_descriptor(self.held_idx[j], self.held, grids,
+                        halo = halo_descriptor(self.held_idx[j], self.held, local_grids,
                                                [w_.qkv.data_ptr() for w_ in wss], cols, sec)
                 # LN1 + QKV (+rotary, + fused halo stores) in one library call
                 rs = self.rope.struct(ext, b.row0, bw.heads, bw.dhp)
