@@ -42,13 +42,20 @@ enum {
 /* Rotary description for WM3_EPI_QKV_ROPE (attention.py:48-92).  Output columns are laid out
  * [3][heads][dhp]; within a q/k head, rotation pair j (reference columns j, j + dh/2) sits at the
  * adjacent columns (2j, 2j + 1), j < dh/2 (a permutation shared by q and k leaves q.k unchanged).
- * pairs: per GEMM row (token of the local band) 128 fp32 = cos[64] then sin[64] of the rotary phases of
- * its global (depth, row, col) position (64-aligned rows; pairs >= dh/2 are (1, 0)).  period: tokens per
- * latent; GEMM row r uses table row r % period, so a batch of ensemble members shares one table. */
+ * The phases factor by axis: pairs j < split (depth, then row pairs) depend on the token's (depth plane,
+ * global row) only, pairs j >= split (column pairs) on its column only.
+ *   dr:  [depth * rows][128] fp32, row d * rows + h = cos[64] then sin[64] of band row h of plane d
+ *        (32-byte aligned; entries of column pairs and of pairs >= dh/2 are (1, 0));
+ *   col: [2][64][cols] fp32, pair-major cos then sin of every column (entries of pairs < split are (1, 0)).
+ * rows, cols: the band's token extents; period = depth * rows * cols tokens per latent: GEMM row r is token
+ * r % period, so a batch of ensemble members shares the tables. */
 typedef struct {
-  const float* pairs;
+  const float* dr;
+  const float* col;
   int heads, dhp;
+  int rows, cols;
   int period;
+  int split;
 } wm3_rope_t;
 
 const char* wm3_last_error(void);

@@ -32,7 +32,8 @@ _ll = ctypes.c_longlong
 
 class RopeT(ctypes.Structure):
     """wm3_rope_t (include/wm3.h)."""
-    _fields_ = [("pairs", _vp), ("heads", _i), ("dhp", _i), ("period", _i)]
+    _fields_ = [("dr", _vp), ("col", _vp), ("heads", _i), ("dhp", _i), ("rows", _i), ("cols", _i),
+                ("period", _i), ("split", _i)]
 
 
 class HaloT(ctypes.Structure):

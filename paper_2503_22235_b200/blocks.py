@@ -205,28 +205,41 @@ class RopeTables:
         self.sin = torch.from_numpy(sin).to(device)
         self.pd, self.pr, self.emax = pd, pr, emax
         self.extents = tuple(int(e) for e in extents)
-        self._pairs: dict = {}
+        self._bands: dict = {}
 
-    def pair_table(self, local_extents, row0: int) -> torch.Tensor:
-        """[T_local][2][64] fp32: (cos, sin) of every rotary pair of each token of the band (global rows)."""
+    def band_tables(self, local_extents, row0: int):
+        """(dr, col) device tables of wm3_rope_t for a band of `local_extents` starting at global row row0:
+        dr [d * rows][2][64] (depth / row pairs of each (plane, band row); column pairs (1, 0)) and col
+        [2][64][cols] pair-major (column pairs of each column; other pairs (1, 0))."""
         d, h, w = (int(e) for e in local_extents)
         key = (d, h, w, int(row0))
-        tab = self._pairs.get(key)
-        if tab is None:
+        hit = self._bands.get(key)
+        if hit is None:
             dev = self.cos.device
-            dd = torch.arange(d, device=dev).view(d, 1, 1).expand(d, h, w).reshape(-1)
-            rr = (torch.arange(h, device=dev) + int(row0)).view(1, h, 1).expand(d, h, w).reshape(-1)
-            cc = torch.arange(w, device=dev).view(1, 1, w).expand(d, h, w).reshape(-1)
             pair = torch.arange(64, device=dev)
-            axis = torch.where(pair < self.pd, 0, torch.where(pair < self.pd + self.pr, 1, 2))
-            coord = torch.stack([dd, rr, cc], 1)[:, axis]                       # (T, 64)
-            tab = torch.stack([self.cos[axis, coord, pair], self.sin[axis, coord, pair]], 1).contiguous()
-            self._pairs[key] = tab
-        return tab
+            split = self.pd + self.pr
+            dd = torch.arange(d, device=dev).view(d, 1).expand(d, h).reshape(-1)
+            rr = (torch.arange(h, device=dev) + int(row0)).view(1, h).expand(d, h).reshape(-1)
+            axis = torch.where(pair < self.pd, 0, torch.where(pair < split, 1, 2))           # (64,)
+            coord = torch.where(axis == 0, dd[:, None], rr[:, None])                          # (d*h, 64)
+            coord = torch.where(axis[None, :] == 2, 0, coord)
+            ax = axis.clamp(max=1).expand_as(coord)
+            is_col = (axis == 2)[None, :]
+            c_dr = torch.where(is_col, 1.0, self.cos[ax, coord, pair.expand_as(coord)])
+            s_dr = torch.where(is_col, 0.0, self.sin[ax, coord, pair.expand_as(coord)])
+            dr = torch.stack([c_dr, s_dr], 1).contiguous()                                    # (d*h, 2, 64)
+            cc = torch.arange(w, device=dev)
+            c_col = torch.where(is_col.T, self.cos[2][cc][:, pair].T, 1.0)                    # (64, w)
+            s_col = torch.where(is_col.T, self.sin[2][cc][:, pair].T, 0.0)
+            col = torch.stack([c_col, s_col], 0).contiguous()                                  # (2, 64, w)
+            hit = (dr, col, split)
+            self._bands[key] = hit
+        return hit
 
     def struct(self, local_extents, row0: int, heads: int, dhp: int) -> _lib.RopeT:
         d, h, w = (int(e) for e in local_extents)
-        return _lib.RopeT(self.pair_table(local_extents, row0).data_ptr(), heads, dhp, d * h * w)
+        dr, col, split = self.band_tables(local_extents, row0)
+        return _lib.RopeT(dr.data_ptr(), col.data_ptr(), heads, dhp, h, w, d * h * w, split)
 
 
 class Workspace:

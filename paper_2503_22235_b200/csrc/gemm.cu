@@ -92,17 +92,51 @@ DEVI void load_resid(const EP& ep, int row, bool row_ok, int n, float (&x)[32]) 
 }
 
 // Rotary on interleaved pairs: columns (2i, 2i+1) of a q/k head hold the reference pair (i, i + dh/2).
-// The per-token phase table holds cos[64] then sin[64] for token `row`; pairs [i0, i0 + 32) are read with
-// 256-bit loads (every head of a token reuses the same 512 B row, so it stays in L1/L2).
+// Token `row` -> (depth plane d, band row h, column w).  Depth / row pairs come from the dr table row of (d, h),
+// which the 32 tokens of a warp (consecutive columns) share: 256-bit broadcast loads.  Column pair k (k = 1,
+// 2, ... from `split`) has phase k * alpha_w (attention.py:76-78: integer wavenumbers), so its (cos, sin) is
+// e^{i alpha_w} raised step by step from the first column pair of the chunk: two coalesced loads per chunk
+// instead of one per pair (|error| <= ~1e-6, far below the fp16 output rounding).  (A per-token table made
+// every lane read its own 512 B row: 32 sectors per load, 0.07 ms of the QKV GEMM.)
 DEVI void rope_chunk(const wm3_rope_t& rp, int row, int M, int col0_in_head, float (&v)[64]) {
   int t = row < M ? row : 0;
-  if (rp.period > 0) t %= rp.period;  // ensemble members share the table
-  const float* tab = rp.pairs + static_cast<size_t>(t) * 128 + (col0_in_head >> 1);
+  if (rp.period > 0) t %= rp.period;  // ensemble members share the tables
+  const int rc = rp.rows * rp.cols;
+  const int d = t / rc;
+  const int rem = t - d * rc;
+  const int h = rem / rp.cols;
+  const int w = rem - h * rp.cols;
+  const int p0 = col0_in_head >> 1;  // first pair of this 64-column chunk
+  const float* dr = rp.dr + static_cast<size_t>(d * rp.rows + h) * 128 + p0;
+  const float* col_c = rp.col + w;
+  const float* col_s = rp.col + static_cast<size_t>(64) * rp.cols + w;
+  float cr = 1.f, ci = 0.f, er = 1.f, ei = 0.f;  // current e^{i k alpha}, step e^{i alpha}
+  if (p0 + 32 > rp.split) {
+    const int pc0 = max(p0, rp.split);
+    cr = __ldg(col_c + static_cast<size_t>(pc0) * rp.cols);
+    ci = __ldg(col_s + static_cast<size_t>(pc0) * rp.cols);
+    er = __ldg(col_c + static_cast<size_t>(rp.split) * rp.cols);
+    ei = __ldg(col_s + static_cast<size_t>(rp.split) * rp.cols);
+  }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
+    const int pa = p0 + 8 * q;  // first pair of this vector (warp-uniform branches)
     float cs[8], sn[8];
-    ldg256(tab + 8 * q, cs);
-    ldg256(tab + 64 + 8 * q, sn);
+    if (pa < rp.split) {
+      ldg256(dr + 8 * q, cs);
+      ldg256(dr + 64 + 8 * q, sn);
+    }
+    if (pa + 8 > rp.split) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (pa + e >= rp.split) {
+          cs[e] = cr;
+          sn[e] = ci;
+          const float nr = cr * er - ci * ei;
+          ci = fmaf(cr, ei, ci * er);
+          cr = nr;
+        }
+    }
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const int k = 8 * q + e;
@@ -478,8 +512,14 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
     return set_error("wm3_linear: %d planes x %d rows (stride %lld) do not tile m=%d", op.planes, op.plane_rows,
                      op.plane_stride, m);
   if (epi == WM3_EPI_BIAS_RESID_F32 && op.planes != 1) return set_error("wm3_linear: residual output must be 2D");
-  if (epi == WM3_EPI_QKV_ROPE && rope != nullptr && (reinterpret_cast<uintptr_t>(rope->pairs) % 32))
-    return set_error("wm3_linear: rope pair table must be 32-byte aligned");
+  if (epi == WM3_EPI_QKV_ROPE && rope != nullptr) {
+    if (reinterpret_cast<uintptr_t>(rope->dr) % 32 || rope->col == nullptr)
+      return set_error("wm3_linear: rope dr table must be 32-byte aligned and the column table given");
+    if (rope->rows < 1 || rope->cols < 1 || rope->split < 0 || rope->split > 64 ||
+        (rope->period > 0 && rope->period % (rope->rows * rope->cols)))
+      return set_error("wm3_linear: bad rope geometry (rows %d cols %d period %d split %d)", rope->rows, rope->cols,
+                       rope->period, rope->split);
+  }
   EpiParams ep{};
   ep.resid = reinterpret_cast<const float*>(out);
   ep.ld_resid = ldo;
