@@ -400,6 +400,24 @@ DEVI float gelu_epi(float x) {
 #endif
 }
 
+// gelu_tanh of two fp32 values straight to a packed fp16 pair, in f16x2 arithmetic (half the instructions of
+// two scalar gelu_tanh + pack): x clamped to [-6, 6] for the polynomial (u monotone there, |u| = 10 at the
+// ends, where tanh has saturated), tanh.approx.f16x2, 0.5 x (1 + t).  The error stays at the level of the
+// scalar form (tanh.approx's ~2^-11 plus one fp16 rounding), below the fp16 storage of the result.
+DEVI uint32_t gelu_tanh_h2(float a, float b) {
+  const __half2 x = __floats2half2_rn(a, b);
+  const __half2 xc = __hmin2(__hmax2(x, __float2half2_rn(-6.0f)), __float2half2_rn(6.0f));
+  const __half2 x2 = __hmul2(xc, xc);
+  __half2 p = __hfma2(x2, __float2half2_rn(-3.51516786e-4f), __float2half2_rn(0.037005646f));
+  p = __hfma2(x2, p, __float2half2_rn(0.797507884f));
+  const __half2 u = __hmul2(xc, p);
+  uint32_t ub = *reinterpret_cast<const uint32_t*>(&u), tb;
+  asm("tanh.approx.f16x2 %0, %1;" : "=r"(tb) : "r"(ub));
+  const __half2 t = *reinterpret_cast<const __half2*>(&tb);
+  const __half2 y = __hmul2(x, __hfma2(t, __float2half2_rn(0.5f), __float2half2_rn(0.5f)));
+  return *reinterpret_cast<const uint32_t*>(&y);
+}
+
 DEVI void ldg256(const float* p, float (&v)[8]) {
   asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])

@@ -366,7 +366,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                                                       : make_float4(0.f, 0.f, 0.f, 0.f);
             v[4 * j + 0] += b.x; v[4 * j + 1] += b.y; v[4 * j + 2] += b.z; v[4 * j + 3] += b.w;
           }
-          if (EPI == WM3_EPI_BIAS_GELU_BF16) {
+#if !defined(WM3_OPERAND_BF16) && WM3_GELU_VARIANT == 2
+          constexpr bool gelu_h2 = (EPI == WM3_EPI_BIAS_GELU_BF16);  // f16x2 GELU straight to packed pairs
+#else
+          constexpr bool gelu_h2 = false;
+#endif
+          if (EPI == WM3_EPI_BIAS_GELU_BF16 && !gelu_h2) {
 #pragma unroll
             for (int e = 0; e < 64; ++e) v[e] = gelu_epi(v[e]);
           }
@@ -376,7 +381,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           uint32_t pk[32];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) pk[e] = pack_elem(v[2 * e], v[2 * e + 1]);
+          for (int e = 0; e < 32; ++e)
+            pk[e] = gelu_h2 ? gelu_tanh_h2(v[2 * e], v[2 * e + 1]) : pack_elem(v[2 * e], v[2 * e + 1]);
           if (EPI == WM3_EPI_QKV_ROPE && ep.has_halo && row_ok && n >= ep.halo.col_lo) {
             // fused halo exchange: this row's 64 columns also go to a neighbour's K/V grid over NVLink
             const int r = prow;
