@@ -442,6 +442,9 @@ DEVI float fast_exp2(float x) {
 }
 
 // SWIZZLE_128B byte offset of 16-byte chunk `c` (0..7) in row `r` of a tile with 128-byte rows.
+DEVI void ld_shared_v4(uint32_t addr, float& a, float& b, float& c, float& d) {
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(addr));
+}
 DEVI uint32_t sw128_off(uint32_t r, uint32_t c) { return r * 128u + ((c ^ (r & 7u)) << 4); }
 
 }  // namespace wm3

@@ -46,17 +46,26 @@ constexpr int EPI_WARP0 = 4;
 #ifndef WM3_PAIR_STAGING
 #define WM3_PAIR_STAGING 1
 #endif
-template <int BN, int CG = 1>
+#ifndef WM3_RESID_TMA
+#define WM3_RESID_TMA 1
+#endif
+template <int BN, int CG = 1, int EPI = 0>
 struct GemmCfg {
+  // Residual epilogue: the fp32 residual chunks stream into RSLOTS smem slots by TMA (warp 3), ahead of the
+  // epilogue, instead of per-thread global loads (the O-proj epilogue was HBM-latency bound); one mainloop
+  // stage gives up its smem for them.
+  static constexpr bool RESID_TMA = (EPI == WM3_EPI_BIAS_RESID_F32) && WM3_RESID_TMA;
+  static constexpr int RSLOTS = RESID_TMA ? (CG == 2 ? 2 : 3) : 0;
   // CTA pairs free 16 KB per stage: 6 stages, or 5 stages with double-buffered epilogue staging
-  static constexpr int STAGES = (CG == 2) ? (WM3_PAIR_STAGING == 2 ? 5 : 6) : 4;
+  static constexpr int STAGES = (CG == 2) ? ((WM3_PAIR_STAGING == 2 || RESID_TMA) ? 5 : 6) : (RESID_TMA ? 3 : 4);
   static constexpr int STAGING_PER_GROUP = (BN == 256) ? ((CG == 2) ? WM3_PAIR_STAGING : 1) : 2;
   static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
   static constexpr uint32_t B_BYTES = (BN / CG) * GEMM_BK * 2;  // this CTA's share of the B tile
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t STAGING_BYTES = 16384;  // 128 rows x 128 B
-  static constexpr uint32_t SMEM =
-      STAGES * STAGE_BYTES + 2 * STAGING_PER_GROUP * STAGING_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t RSLOT_BYTES = 16384;    // 128 rows x 32 fp32
+  static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 2 * STAGING_PER_GROUP * STAGING_BYTES +
+                                   RSLOTS * RSLOT_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = 2 * BN;
 };
 
@@ -152,23 +161,28 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmOut, int M, int N, int K, EpiParams ep) {
   griddep_launch_dependents();  // PDL: the next kernel may start its prologue
-  using Cfg = GemmCfg<BN, CG>;
+  using Cfg = GemmCfg<BN, CG, EPI>;
   using Tr = EpiTraits<EPI>;
   constexpr int STAGES = Cfg::STAGES;
+  constexpr int RSLOTS = Cfg::RSLOTS;
   constexpr int CW = Tr::CW;
   constexpr int NUNITS = BN / CW;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
   const uint32_t staging0 = sbase + STAGES * Cfg::STAGE_BYTES;
-  uint64_t* bars =
-      reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + 2 * Cfg::STAGING_PER_GROUP * Cfg::STAGING_BYTES);
+  const uint32_t rslot0 = staging0 + 2 * Cfg::STAGING_PER_GROUP * Cfg::STAGING_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES +
+                                               2 * Cfg::STAGING_PER_GROUP * Cfg::STAGING_BYTES +
+                                               RSLOTS * Cfg::RSLOT_BYTES);
   const uint32_t bar0 = smem_u32(bars);
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
   auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + a); };
   auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + 2 + a); };
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  auto rfull_bar = [&](int r) { return bar0 + 8u * (2 * STAGES + 4 + r); };
+  auto rempty_bar = [&](int r) { return bar0 + 8u * (2 * STAGES + 4 + RSLOTS + r); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4 + 2 * RSLOTS);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -199,6 +213,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
       mbar_init(tempty_bar(a), 8 * CG);  // every epilogue warp of the pair arrives on the leader's barrier
+    }
+    for (int r = 0; r < RSLOTS; ++r) {
+      mbar_init(rfull_bar(r), 1);
+      mbar_init(rempty_bar(r), 4);  // the 4 warps of the epilogue group that consumes the chunk
     }
     fence_barrier_init();
   }
@@ -286,6 +304,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (acc == 0) aphase ^= 1;
       }
     }
+  } else if (Cfg::RESID_TMA && warp == 3) {
+    // residual producer: chunk c of this CTA (tile-major, column units in order) -> slot c % RSLOTS
+    if (lane == 0) {
+      int c = 0;
+      for (int tile = tile0; tile < ntiles; tile += tstep) {
+        int plane, r0;
+        tile_rows(tile, plane, r0);
+        const int n0 = (tile % nn) * BN;
+        for (int u = 0; u < NUNITS; ++u, ++c) {
+          const int slot = c % RSLOTS;
+          mbar_wait(rempty_bar(slot), ((c / RSLOTS) & 1) ^ 1);
+          mbar_arrive_expect_tx(rfull_bar(slot), Cfg::RSLOT_BYTES);
+          tma_load_3d(rslot0 + slot * Cfg::RSLOT_BYTES, &tmOut, rfull_bar(slot), n0 + u * CW, r0, plane);
+        }
+      }
+    }
   } else if (warp >= EPI_WARP0) {
     const int g = (warp - EPI_WARP0) >> 2;  // epilogue group
     const int q = warp & 3;                  // TMEM lane quarter
@@ -296,7 +330,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint32_t aphase = 0;
     int sbuf = 0;
     const uint32_t tempty_leader0 = (CG == 2) ? mapa_shared(tempty_bar(0), 0) : 0u;
-    for (int tile = tile0; tile < ntiles; tile += tstep) {
+    int tile_it = 0;
+    for (int tile = tile0; tile < ntiles; tile += tstep, ++tile_it) {
       int plane, r0;
       const int m0 = tile_rows(tile, plane, r0);
       const int n0 = (tile % nn) * BN;
@@ -310,7 +345,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #endif
       constexpr int RESID_DEPTH = WM3_RESID_DEPTH;
       float xr[RESID_DEPTH + 1][32];
-      if (EPI == WM3_EPI_BIAS_RESID_F32) {
+      if (EPI == WM3_EPI_BIAS_RESID_F32 && !Cfg::RESID_TMA) {
 #pragma unroll
         for (int i = 0; i < RESID_DEPTH; ++i)
           if (g + 2 * i < NUNITS) load_resid(ep, row, row_ok, n0 + (g + 2 * i) * CW, xr[i]);
@@ -323,8 +358,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int n = n0 + u * CW;
         const int it = (u - g) >> 1;  // compile-time after unrolling
         float(&xa)[32] = xr[it % (RESID_DEPTH + 1)];
-        if (EPI == WM3_EPI_BIAS_RESID_F32 && u + 2 * RESID_DEPTH < NUNITS)
+        if (EPI == WM3_EPI_BIAS_RESID_F32 && !Cfg::RESID_TMA && u + 2 * RESID_DEPTH < NUNITS)
           load_resid(ep, row, row_ok, n + 2 * RESID_DEPTH * CW, xr[(it + RESID_DEPTH) % (RESID_DEPTH + 1)]);
+        if (Cfg::RESID_TMA) {
+          // this unit's residual chunk from its smem slot (SWIZZLE_128B rows, as the TMA box landed)
+          const int c = tile_it * NUNITS + u;
+          const int slot = c % (RSLOTS > 0 ? RSLOTS : 1);
+          mbar_wait(rfull_bar(slot), (c / (RSLOTS > 0 ? RSLOTS : 1)) & 1);
+          const uint32_t rb = rslot0 + slot * Cfg::RSLOT_BYTES;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            ld_shared_v4(rb + sw128_off(r_in_tile, j), xa[4 * j], xa[4 * j + 1], xa[4 * j + 2], xa[4 * j + 3]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(rempty_bar(slot));
+        }
         if (Tr::F32) {
           uint32_t r[32];
           tmem_ld32(taddr + u * CW, r);
@@ -451,7 +498,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 template <int BN, int EPI, int CG>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, int M, int N, int K,
                        const EpiParams& ep, cudaStream_t stream) {
-  using Cfg = GemmCfg<BN, CG>;
+  using Cfg = GemmCfg<BN, CG, EPI>;
   auto kern = gemm_tc_kernel<BN, EPI, CG>;
   static bool attr_done = false;
   if (!attr_done) {
@@ -540,10 +587,10 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
     const char* e = getenv("WM3_GEMM_CG");
     return e ? atoi(e) : 2;
   }();
-  // the short-K residual GEMM (O-proj, K = 1024) is HBM-latency bound in its epilogue and measured faster as
-  // single-CTA tiles (0.227 vs 0.241 ms in-block); every other wide GEMM is faster as pairs
-  const bool short_resid = (epi == WM3_EPI_BIAS_RESID_F32 && k <= 1024);
-  const int cg = (bn == 256 && cg_env == 2 && !short_resid) ? 2 : 1;
+  // every wide GEMM runs as CTA pairs; the short-K residual GEMM (O-proj, K = 1024) was faster as single-CTA
+  // tiles while its residual came through per-thread loads, and is faster as pairs since the residual streams
+  // in by TMA (0.195 vs 0.204 ms isolated)
+  const int cg = (bn == 256 && cg_env == 2) ? 2 : 1;
   ep.tiles_per_plane = (op.plane_rows + GEMM_BM * cg - 1) / (GEMM_BM * cg);
   if (halo != nullptr) {
     if (epi != WM3_EPI_QKV_ROPE) return set_error("wm3_linear: halo stores need the QKV epilogue");
