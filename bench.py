@@ -412,7 +412,7 @@ def run_gpu(args, world, rank, local_rank):
     x_host.copy_(x.cpu())
     y_host = torch.empty_like(x_host).pin_memory()
     xd = torch.empty_like(x)
-    e_steps = max(3, min(args.steps, 10))
+    e_steps = max(3, min(args.steps, 20))
     if world == 1:
         # the public serving operator (attention.NattenBlockStream): page-locked host batches in and out, the
         # uploads / downloads of neighbouring batches overlapped with the block on separate CUDA streams

@@ -72,8 +72,12 @@ class NattenBlockStream:
     `submit(host_in, host_out)` takes page-locked float32 (T, dim) host tensors and returns at once: the batch is
     copied host->device on one CUDA stream, the block runs on a second, the result is copied device->host on a
     third, so batch i+1's upload and batch i-1's download run under batch i's compute (both PCIe directions at
-    once).  Two device buffers alternate; `synchronize()` waits for everything submitted.  Each batch's result
-    equals natten_block(host_in, ...) bitwise (same kernels, same inputs)."""
+    once).  Three device buffers rotate, so an upload never waits for the download of the batch just before
+    (with two, upload i+1 waits for download i-1 and the period is (up + compute + down) / 2 instead of the
+    transfer time); `synchronize()` waits for everything submitted.  Each batch's result equals
+    natten_block(host_in, ...) bitwise (same kernels, same inputs)."""
+
+    NBUF = 3
 
     def __init__(self, params: dict, prefix: str, extents, window, heads: int, dim: int):
         t = int(np.prod(extents))
@@ -82,16 +86,16 @@ class NattenBlockStream:
         self.bw = CACHE.block(params, prefix, heads)
         self.ws = CACHE.workspace(self.extents, self.window, self.bw, tag="stream")
         self.rope = CACHE.rope(self.extents, self.dh)
-        self.buf = [torch.empty((t, dim), dtype=torch.float32, device="cuda") for _ in range(2)]
+        self.buf = [torch.empty((t, dim), dtype=torch.float32, device="cuda") for _ in range(self.NBUF)]
         self.s_in, self.s_run, self.s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-        self.uploaded = [torch.cuda.Event() for _ in range(2)]
-        self.computed = [torch.cuda.Event() for _ in range(2)]
-        self.downloaded = [None, None]
+        self.uploaded = [torch.cuda.Event() for _ in range(self.NBUF)]
+        self.computed = [torch.cuda.Event() for _ in range(self.NBUF)]
+        self.downloaded = [None] * self.NBUF
         self.i = 0
 
     def submit(self, host_in: torch.Tensor, host_out: torch.Tensor) -> None:
         from .blocks import block_forward
-        b = self.i & 1
+        b = self.i % self.NBUF
         self.i += 1
         dev = self.buf[b]
         with torch.cuda.stream(self.s_in):
