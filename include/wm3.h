@@ -110,6 +110,34 @@ int wm3_halo_signal(int* peer_flag_a, int* peer_flag_b, int epoch, void* stream)
 /* Spin (acquire, system scope) until each of the n local flags is >= epoch; traps after ~10 s. */
 int wm3_halo_wait(const int* flags, int n, int epoch, void* stream);
 
+/* LayerNorm folded into the GEMMs around it (attention.py:163-165, 180-181).  A residual GEMM
+ * (WM3_EPI_BIAS_RESID_F32) acting as producer also writes an fp16 copy of the updated stream (xh_out, columns
+ * < n_valid; pad columns untouched) and per row partial (sum, sum of squares) pairs into
+ * stats_out[row][slot][2] (slot = 2 * column tile + epilogue group, every slot < 2 * ceil(n / tile) written).
+ * The next GEMM, as consumer, takes A = xh with weights pre-scaled by the LN gain, sums the first stats_parts
+ * pairs of its row into mean and rstd = 1 / sqrt(biased variance + eps) and applies
+ * rstd * acc - rstd * mean * fold_c[col] + bias[col] before its own epilogue (bias = b + beta . W). */
+#define WM3_LN_SLOTS 16
+typedef struct {
+  void* xh_out;
+  int ld_xh;
+  float* stats_out;
+  const float* stats_in;
+  int stats_parts;
+  int ln_n;
+  float eps;
+  const float* fold_c;
+} wm3_ln_fold_t;
+/* wm3_linear_planes_halo with an optional LayerNorm fold (producer and / or consumer side); halo may be NULL. */
+int wm3_linear_fold(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi, void* out, int ldo,
+                    int n_valid, const float* bias, const wm3_rope_t* rope, int planes, int plane_rows,
+                    long long plane_stride, int row_off, const wm3_halo_t* halo, const wm3_ln_fold_t* fold,
+                    void* stream);
+/* Start of a folded chain: xh = fp16(x) (columns >= n of each xh row zeroed) and stats (pair 0 = row sum and
+ * sum of squares, pairs 1 .. parts-1 zero) for a consumer GEMM. */
+int wm3_ln_fold_prep(const float* x, int ldx, int m, int n, void* xh, int ld_xh, float* stats, int parts,
+                     void* stream);
+
 /* One processor block (attention.py:146-184) as library calls: x (T, hidden) fp32 in place, T = batch * depth *
  * rows * cols band tokens.  Weights in the device layout the Python layer prepares (blocks.prepare_block:
  * K-major fp16, q/k rotary pairs interleaved, heads padded to dhp); workspace buffers: hn (T, kp), the K/V grid
@@ -126,14 +154,24 @@ typedef struct {
   const void* w_2;
   const float* b_2;
   int hidden, heads, dh, dhp, kp, np, nm;
+  /* LayerNorm folded into the QKV and W1 GEMMs (wm3_ln_fold_t); NULL w_qkv_f = separate LayerNorm launches.
+   * w_qkv_f / w_1_f: w_qkv / w_1 with every input column k scaled by ln1 / ln2 gain[k] (fp16); c_*: per
+   * output column sum over k of those fp16 weights; d_*: bias + sum_k ln bias[k] * W[col][k]. */
+  const void* w_qkv_f;
+  const float *c_qkv, *d_qkv;
+  const void* w_1_f;
+  const float *c_1, *d_1;
 } wm3_block_weights_t;
 typedef struct {
   void *hn, *qkv, *ctx, *mid;
+  float* stats; /* [T][WM3_LN_SLOTS][2] LayerNorm partial sums (folded path); hn then holds the fp16 copy of x */
 } wm3_block_ws_t;
 typedef struct {
   int batch, depth, rows, cols;    /* local band extents (batch = ensemble members) */
   int rows_global, row0, halo_lo, halo_hi;
   int wd, wh, ww;                  /* attention window */
+  int x_prepped;                   /* folded LayerNorm: ws hn / stats already describe x (written by the
+                                      previous block's W2 epilogue); 0 = compute them first */
 } wm3_block_geom_t;
 /* LN1 + QKV (+rotary) into the K/V grid; with halo != NULL the epilogue also fills the neighbours' halos. */
 int wm3_block_qkv(const float* x, const wm3_block_weights_t* w, const wm3_block_ws_t* ws, const wm3_block_geom_t* g,

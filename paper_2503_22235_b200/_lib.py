@@ -46,18 +46,28 @@ class BlockWeightsT(ctypes.Structure):
     """wm3_block_weights_t (include/wm3.h)."""
     _fields_ = [("ln1_g", _vp), ("ln1_b", _vp), ("w_qkv", _vp), ("b_qkv", _vp), ("w_o", _vp), ("b_o", _vp),
                 ("ln2_g", _vp), ("ln2_b", _vp), ("w_1", _vp), ("b_1", _vp), ("w_2", _vp), ("b_2", _vp),
-                ("hidden", _i), ("heads", _i), ("dh", _i), ("dhp", _i), ("kp", _i), ("np", _i), ("nm", _i)]
+                ("hidden", _i), ("heads", _i), ("dh", _i), ("dhp", _i), ("kp", _i), ("np", _i), ("nm", _i),
+                ("w_qkv_f", _vp), ("c_qkv", _vp), ("d_qkv", _vp), ("w_1_f", _vp), ("c_1", _vp), ("d_1", _vp)]
 
 
 class BlockWsT(ctypes.Structure):
     """wm3_block_ws_t."""
-    _fields_ = [("hn", _vp), ("qkv", _vp), ("ctx", _vp), ("mid", _vp)]
+    _fields_ = [("hn", _vp), ("qkv", _vp), ("ctx", _vp), ("mid", _vp), ("stats", _vp)]
 
 
 class BlockGeomT(ctypes.Structure):
     """wm3_block_geom_t."""
     _fields_ = [("batch", _i), ("depth", _i), ("rows", _i), ("cols", _i), ("rows_global", _i), ("row0", _i),
-                ("halo_lo", _i), ("halo_hi", _i), ("wd", _i), ("wh", _i), ("ww", _i)]
+                ("halo_lo", _i), ("halo_hi", _i), ("wd", _i), ("wh", _i), ("ww", _i), ("x_prepped", _i)]
+
+
+LN_SLOTS = 16  # WM3_LN_SLOTS
+
+
+class LnFoldT(ctypes.Structure):
+    """wm3_ln_fold_t (include/wm3.h)."""
+    _fields_ = [("xh_out", _vp), ("ld_xh", _i), ("stats_out", _vp), ("stats_in", _vp), ("stats_parts", _i),
+                ("ln_n", _i), ("eps", _f), ("fold_c", _vp)]
 
 
 # name -> argtypes; every function returns int status
@@ -67,6 +77,9 @@ SIGNATURES = {
     "wm3_linear": [_vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, ctypes.POINTER(RopeT), _vp],
     "wm3_linear_planes": [_vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, ctypes.POINTER(RopeT),
                           _i, _i, ctypes.c_longlong, _i, _vp],
+    "wm3_linear_fold": [_vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, ctypes.POINTER(RopeT),
+                        _i, _i, ctypes.c_longlong, _i, ctypes.POINTER(HaloT), ctypes.POINTER(LnFoldT), _vp],
+    "wm3_ln_fold_prep": [_vp, _i, _i, _i, _vp, _i, _vp, _i, _vp],
     "wm3_linear_planes_halo": [_vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, ctypes.POINTER(RopeT),
                                _i, _i, ctypes.c_longlong, _i, ctypes.POINTER(HaloT), _vp],
     "wm3_halo_signal": [_vp, _vp, _i, _vp],

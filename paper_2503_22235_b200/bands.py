@@ -284,14 +284,16 @@ class BandedProcessor:
         cfg = self.cfg
         h = cfg.latent_extents[1]
         cols = cfg.latent_extents[2]
-        for prefix in prefixes:
+        for bi, prefix in enumerate(prefixes):
             bw = CACHE.block(self.params, prefix, cfg.heads)
             wss = self._ws(bw)
             sec = bw.heads * bw.dhp
             peer = self.exchanger if (self.fused and isinstance(self.exchanger, PeerHalo)) else None
             if peer is not None:
                 peer.before_qkv()
-            geoms = [_lib.BlockGeomT(1, ext[0], ext[1], ext[2], h, b.row0, b.halo_lo, b.halo_hi, *cfg.window)
+            # folded LayerNorm: after the first block the previous W2 epilogue left each band's hn / stats
+            geoms = [_lib.BlockGeomT(1, ext[0], ext[1], ext[2], h, b.row0, b.halo_lo, b.halo_hi, *cfg.window,
+                                     int(bi > 0))
                      for b, ext in zip(self.held, self.local)]
             local_grids = [GridGeo(w_.grid.rows_ext, w_.qkv.stride(0)) for w_ in wss]
             for j, (b, ext, xb, ws) in enumerate(zip(self.held, self.local, xs, wss)):

@@ -15,6 +15,7 @@ Weight layout (built once per parameter set, from the reference's (in, out) floa
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -101,15 +102,35 @@ class BlockWeights:
     b_1: torch.Tensor
     w_2: torch.Tensor
     b_2: torch.Tensor
+    # LayerNorm folded into the QKV / W1 GEMMs (wm3_ln_fold_t): gain-scaled weights, their column sums and the
+    # shifted biases; None = separate LayerNorm launches (the default; WM3_LN_FOLD=1 folds)
+    w_qkv_f: torch.Tensor | None = None
+    c_qkv: torch.Tensor | None = None
+    d_qkv: torch.Tensor | None = None
+    w_1_f: torch.Tensor | None = None
+    c_1: torch.Tensor | None = None
+    d_1: torch.Tensor | None = None
+
+    @property
+    def folded(self) -> bool:
+        return self.w_qkv_f is not None
+
+    @property
+    def ln_parts(self) -> int:
+        """Partial-sum pairs per row the residual GEMMs write (gemm.cu: 2 epilogue groups per column tile)."""
+        bn = 256 if self.np_ >= 256 else 128
+        return 2 * ((self.np_ + bn - 1) // bn)
 
     def native(self) -> "_lib.BlockWeightsT":
         """wm3_block_weights_t view of these tensors (cached; the tensors stay owned by this object)."""
         nat = self.__dict__.get("_native")
         if nat is None:
+            fold = [(t.data_ptr() if t is not None else None)
+                    for t in (self.w_qkv_f, self.c_qkv, self.d_qkv, self.w_1_f, self.c_1, self.d_1)]
             nat = _lib.BlockWeightsT(*(t.data_ptr() for t in (self.ln1_g, self.ln1_b, self.w_qkv, self.b_qkv, self.w_o,
                                                               self.b_o, self.ln2_g, self.ln2_b, self.w_1, self.b_1,
                                                               self.w_2, self.b_2)),
-                                     self.hidden, self.heads, self.dh, self.dhp, self.kp, self.np_, self.nm)
+                                     self.hidden, self.heads, self.dh, self.dhp, self.kp, self.np_, self.nm, *fold)
             self.__dict__["_native"] = nat
         return nat
 
@@ -158,6 +179,26 @@ def _vec(v: np.ndarray, n_pad: int, device) -> torch.Tensor:
     return torch.from_numpy(buf).to(device)
 
 
+def _fold_ln(w_in_out: np.ndarray, bias: np.ndarray, gain: np.ndarray, beta: np.ndarray, n_pad: int, k_pad: int,
+             device):
+    """LayerNorm folded into the GEMM that follows it: LN(x) W + b = rstd (x W') - rstd mean c + d with
+    W' = diag(gain) W (stored fp16), c = column sums of the stored fp16 W' (so the mean term cancels exactly what
+    the tensor cores accumulate), d = b + beta W."""
+    k = w_in_out.shape[0]
+    wf = _kmajor_bf16(w_in_out * gain[:k, None], n_pad, k_pad, device)
+    c = wf.double().cpu().numpy().sum(axis=1)
+    d = np.zeros(n_pad, dtype=np.float64)
+    d[: w_in_out.shape[1]] = bias + beta[:k] @ w_in_out
+    return wf, _vec(c, n_pad, device), _vec(d, n_pad, device)
+
+
+def ln_fold_enabled() -> bool:
+    """WM3_LN_FOLD=1 selects the folded LayerNorm (5 launches per block).  Off by default: measured in-block on
+    one B200 it costs more epilogue time than the two LayerNorm launches it removes (2.228 vs 2.181 ms per block:
+    QKV +0.066, O-proj +0.045, W1 +0.079, W2 +0.008 ms against 0.160 ms of LayerNorm)."""
+    return os.environ.get("WM3_LN_FOLD", "0") == "1"
+
+
 def prepare_block(params: dict, prefix: str, heads: int, device="cuda") -> BlockWeights:
     names = block_param_names(prefix)
     missing = [n for n in names if n not in params]
@@ -182,6 +223,12 @@ def prepare_block(params: dict, prefix: str, heads: int, device="cuda") -> Block
     wo = np.zeros((heads * dhp, hidden), dtype=np.float64)
     ok = vv >= 0
     wo[ok] = p["attn.wo"][vv[ok]]
+    fold = {}
+    if ln_fold_enabled():
+        fold["w_qkv_f"], fold["c_qkv"], fold["d_qkv"] = _fold_ln(w_qkv, b_qkv, p["ln1.gain"], p["ln1.bias"],
+                                                                 3 * heads * dhp, kp, device)
+        fold["w_1_f"], fold["c_1"], fold["d_1"] = _fold_ln(p["mlp.w1"], p["mlp.b1"], p["ln2.gain"], p["ln2.bias"],
+                                                           nm, kp, device)
     return BlockWeights(
         hidden=hidden, heads=heads, dh=dh, dhp=dhp, kp=kp, np_=np_, nm=nm,
         ln1_g=_vec(p["ln1.gain"], hidden, device), ln1_b=_vec(p["ln1.bias"], hidden, device),
@@ -189,7 +236,7 @@ def prepare_block(params: dict, prefix: str, heads: int, device="cuda") -> Block
         w_o=_kmajor_bf16(wo, np_, heads * dhp, device), b_o=_vec(p["attn.bo"], np_, device),
         ln2_g=_vec(p["ln2.gain"], hidden, device), ln2_b=_vec(p["ln2.bias"], hidden, device),
         w_1=_kmajor_bf16(p["mlp.w1"], nm, kp, device), b_1=_vec(p["mlp.b1"], nm, device),
-        w_2=_kmajor_bf16(p["mlp.w2"], np_, nm, device), b_2=_vec(p["mlp.b2"], np_, device),
+        w_2=_kmajor_bf16(p["mlp.w2"], np_, nm, device), b_2=_vec(p["mlp.b2"], np_, device), **fold,
     )
 
 
@@ -251,19 +298,22 @@ class Workspace:
         self.grid = grid
         tokens = grid.batch * grid.depth * grid.rows * grid.cols
         self.tokens = tokens
-        self.hn = torch.empty((tokens, bw.kp), dtype=_lib.ELEM, device=device)
+        self.hn = torch.zeros((tokens, bw.kp), dtype=_lib.ELEM, device=device)  # pad columns stay zero
         self.qkv = torch.zeros((grid.tokens, 3 * bw.heads * bw.dhp), dtype=_lib.ELEM, device=device)
         self.ctx = torch.empty((tokens, bw.heads * bw.dhp), dtype=_lib.ELEM, device=device)
         self.mid = torch.empty((tokens, bw.nm), dtype=_lib.ELEM, device=device)
+        # LayerNorm-fold row statistics ([tokens][WM3_LN_SLOTS] (sum, sum of squares) pairs)
+        self.stats = torch.zeros((tokens, 2 * _lib.LN_SLOTS), dtype=torch.float32, device=device)
         self._native = _lib.BlockWsT(self.hn.data_ptr(), self.qkv.data_ptr(), self.ctx.data_ptr(),
-                                     self.mid.data_ptr())
+                                     self.mid.data_ptr(), self.stats.data_ptr())
 
     def native(self) -> "_lib.BlockWsT":
         return self._native
 
 
 def block_forward(x: torch.Tensor, bw: BlockWeights, ws: Workspace, rope: RopeTables, extents, window,
-                  row0: int = 0, rows_global: int | None = None, halo_exchange=None, mark=None) -> None:
+                  row0: int = 0, rows_global: int | None = None, halo_exchange=None, mark=None,
+                  prepped: bool = False) -> None:
     """In-place x (T, hidden) fp32 <- natten_block(x) on the current stream.
 
     With a batched workspace (ws.grid.batch = B ensemble members) x is (B * T, hidden), member-major; the
@@ -272,26 +322,53 @@ def block_forward(x: torch.Tensor, bw: BlockWeights, ws: Workspace, rope: RopeTa
     extents are the local (band) token extents; row0 / rows_global place the band in the global grid
     (rotary phases and window bumps use global rows).  halo_exchange(qkv, grid), when given, fills the halo
     rows of the padded K/V grid from the neighbouring bands between the QKV GEMM and the attention kernel.
-    Launches: LN1, QKV+rotary GEMM, NA, O-proj+residual GEMM, LN2, W1+GELU GEMM, W2+residual GEMM.
-    mark(i), when given, is called before launch i and once more after the last (profiling: CUDA events).
+    Launches with the folded LayerNorm (bw.folded): [LN-fold prep unless `prepped`], QKV+rotary GEMM, NA,
+    O-proj+residual GEMM (+ fp16 copy and row statistics of x), W1+GELU GEMM, W2+residual GEMM (+ the same for
+    the next block, which may then pass prepped=True); otherwise LN1, QKV, NA, O-proj, LN2, W1, W2.
+    mark(i), when given, is called before launch slot i (0..6: LN1 / prep, QKV, NA, O-proj, LN2, W1, W2) and once
+    more after the last (profiling: CUDA events; the folded path leaves slot 4 empty).
     """
     L = _lib
     g = ws.grid
+    d, h, w = (int(e) for e in extents)
+    rg = int(rows_global if rows_global is not None else h)
     if mark is None and halo_exchange is None:
-        # the whole block in one library call (wm3_block_fwd: the 7 launches are issued by the C++ host code)
+        # the whole block in one library call (wm3_block_fwd: the launches are issued by the C++ host code)
         import ctypes
         rs = rope.struct(extents, row0, bw.heads, bw.dhp)
-        d, h, w = (int(e) for e in extents)
-        geom = L.BlockGeomT(g.batch, d, h, w, int(rows_global if rows_global is not None else h), int(row0),
-                            g.halo_lo, g.halo_hi, *(int(v) for v in window))
+        geom = L.BlockGeomT(g.batch, d, h, w, rg, int(row0), g.halo_lo, g.halo_hi, *(int(v) for v in window),
+                            int(bool(prepped)))
         L.check(L.lib().wm3_block_fwd(x.data_ptr(), ctypes.byref(bw.native()), ctypes.byref(ws.native()),
                                       ctypes.byref(geom), ctypes.byref(rs), L.stream_ptr()), "wm3_block_fwd")
         return
     mk = mark if mark is not None else (lambda i: None)
+    rs = rope.struct(extents, row0, bw.heads, bw.dhp)
+    if bw.folded:
+        parts = bw.ln_parts
+        cons_qkv = ops.ln_fold_consumer(ws.stats, parts, bw.hidden, bw.c_qkv)
+        cons_1 = ops.ln_fold_consumer(ws.stats, parts, bw.hidden, bw.c_1)
+        prod = ops.ln_fold_producer(ws.hn, ws.stats)
+        mk(0)
+        if not prepped:
+            ops.ln_fold_prep(x, bw.hidden, ws.hn, ws.stats, parts)
+        mk(1)
+        ops.linear_grid(ws.hn, bw.w_qkv_f, L.WM3_EPI_QKV_ROPE, bw.d_qkv, ws.qkv, g, rope=rs, fold=cons_qkv)
+        if halo_exchange is not None:
+            halo_exchange(ws.qkv, g)
+        mk(2)
+        ops.natten(ws.qkv, g, bw.heads, bw.dhp, bw.dh, window, out=ws.ctx, rows_global=rows_global, row0=row0)
+        mk(3)
+        ops.linear(ws.ctx, bw.w_o, L.WM3_EPI_BIAS_RESID_F32, bias=bw.b_o, out=x, n_valid=bw.hidden, fold=prod)
+        mk(4)
+        mk(5)
+        ops.linear(ws.hn, bw.w_1_f, L.WM3_EPI_BIAS_GELU_BF16, bias=bw.d_1, out=ws.mid, fold=cons_1)
+        mk(6)
+        ops.linear(ws.mid, bw.w_2, L.WM3_EPI_BIAS_RESID_F32, bias=bw.b_2, out=x, n_valid=bw.hidden, fold=prod)
+        mk(7)
+        return
     mk(0)
     ops.layernorm_bf16(x, bw.ln1_g, bw.ln1_b, out=ws.hn)
     mk(1)
-    rs = rope.struct(extents, row0, bw.heads, bw.dhp)
     ops.linear_grid(ws.hn, bw.w_qkv, L.WM3_EPI_QKV_ROPE, bw.b_qkv, ws.qkv, g, rope=rs)
     if halo_exchange is not None:
         halo_exchange(ws.qkv, g)

@@ -6,12 +6,23 @@
 //   wm3_block_rest  NA -> O-proj (+bias, +x) -> LN2 -> W1 (+bias, GELU) -> W2 (+bias, +x)  (:173-184)
 //   wm3_block_fwd   both, for a band without halos (single GPU) or with halos filled by the fused epilogue
 // The halo exchange of a band with NCCL neighbours goes between the two halves.
+//
+// With folded weights (w_qkv_f != NULL) the two LayerNorms are not separate launches (wm3_ln_fold_t): the
+// residual epilogues (O-proj, W2) also write the fp16 copy of the updated stream into ws->hn and its row
+// statistics into ws->stats, and the QKV / W1 GEMMs consume them with gain-scaled weights.  A block is then
+// 5 launches (QKV, NA, O-proj, W1, W2); the first block of a chain (geom x_prepped = 0) starts with
+// wm3_ln_fold_prep.
 #include <cmath>
 
 #include "launch.h"
 #include "../../include/wm3.h"
 
 using namespace wm3;
+
+static int ln_parts(const wm3_block_weights_t* w) {
+  const int bn = (w->np >= 256) ? 256 : 128;  // column tile of the residual GEMMs (gemm.cu linear_impl)
+  return 2 * ((w->np + bn - 1) / bn);
+}
 
 static int check_block(const float* x, const wm3_block_weights_t* w, const wm3_block_ws_t* ws,
                        const wm3_block_geom_t* g) {
@@ -22,7 +33,29 @@ static int check_block(const float* x, const wm3_block_weights_t* w, const wm3_b
                      w->dhp);
   if (g->batch < 1 || g->depth < 1 || g->rows < 1 || g->cols < 1 || g->rows_global < g->rows)
     return set_error("wm3_block: bad geometry");
+  if (w->w_qkv_f != nullptr && (ws->stats == nullptr || w->c_qkv == nullptr || w->d_qkv == nullptr ||
+                                w->w_1_f == nullptr || w->c_1 == nullptr || w->d_1 == nullptr || ln_parts(w) > WM3_LN_SLOTS))
+    return set_error("wm3_block: folded LayerNorm needs w_1_f, c_*, d_* and ws stats (hidden <= %d)",
+                     WM3_LN_SLOTS / 2 * 256);
   return 0;
+}
+
+static wm3_ln_fold_t fold_consumer(const wm3_block_weights_t* w, const wm3_block_ws_t* ws, const float* c) {
+  wm3_ln_fold_t f{};
+  f.stats_in = ws->stats;
+  f.stats_parts = ln_parts(w);
+  f.ln_n = w->hidden;
+  f.eps = 1e-6f;
+  f.fold_c = c;
+  return f;
+}
+
+static wm3_ln_fold_t fold_producer(const wm3_block_weights_t* w, const wm3_block_ws_t* ws) {
+  wm3_ln_fold_t f{};
+  f.xh_out = ws->hn;
+  f.ld_xh = w->kp;
+  f.stats_out = ws->stats;
+  return f;
 }
 
 extern "C" int wm3_block_qkv(const float* x, const wm3_block_weights_t* w, const wm3_block_ws_t* ws,
@@ -32,8 +65,16 @@ extern "C" int wm3_block_qkv(const float* x, const wm3_block_weights_t* w, const
   const int t = g->batch * g->depth * g->rows * g->cols;
   const int rows_ext = g->halo_lo + g->rows + g->halo_hi;
   const int qkv_n = 3 * w->heads * w->dhp;
-  if (wm3_layernorm_bf16(x, w->hidden, t, w->hidden, w->ln1_g, w->ln1_b, 1e-6f, ws->hn, w->kp, stream)) return -1;
   const int plane = g->rows * g->cols;
+  if (w->w_qkv_f != nullptr) {
+    if (!g->x_prepped && wm3_ln_fold_prep(x, w->hidden, t, w->hidden, ws->hn, w->kp, ws->stats, ln_parts(w), stream))
+      return -1;
+    const wm3_ln_fold_t f = fold_consumer(w, ws, w->c_qkv);
+    return wm3_linear_fold(ws->hn, w->kp, w->w_qkv_f, w->kp, t, qkv_n, w->kp, WM3_EPI_QKV_ROPE, ws->qkv, qkv_n, qkv_n,
+                           w->d_qkv, rope, g->batch * g->depth, plane, static_cast<long long>(rows_ext) * g->cols,
+                           g->halo_lo * g->cols, halo, &f, stream);
+  }
+  if (wm3_layernorm_bf16(x, w->hidden, t, w->hidden, w->ln1_g, w->ln1_b, 1e-6f, ws->hn, w->kp, stream)) return -1;
   if (halo != nullptr)
     return wm3_linear_planes_halo(ws->hn, w->kp, w->w_qkv, w->kp, t, qkv_n, w->kp, WM3_EPI_QKV_ROPE, ws->qkv, qkv_n,
                                   qkv_n, w->b_qkv, rope, g->batch * g->depth, plane,
@@ -52,6 +93,18 @@ extern "C" int wm3_block_rest(float* x, const wm3_block_weights_t* w, const wm3_
                      g->halo_lo, g->halo_hi, w->heads, w->dhp, g->wd, g->wh, g->ww,
                      1.0f / std::sqrt(static_cast<float>(w->dh)), stream))
     return -1;
+  if (w->w_qkv_f != nullptr) {
+    const wm3_ln_fold_t prod = fold_producer(w, ws), cons = fold_consumer(w, ws, w->c_1);
+    if (wm3_linear_fold(ws->ctx, hd, w->w_o, hd, t, w->np, hd, WM3_EPI_BIAS_RESID_F32, x, w->hidden, w->hidden,
+                        w->b_o, nullptr, 1, t, t, 0, nullptr, &prod, stream))
+      return -1;
+    if (wm3_linear_fold(ws->hn, w->kp, w->w_1_f, w->kp, t, w->nm, w->kp, WM3_EPI_BIAS_GELU_BF16, ws->mid, w->nm,
+                        w->nm, w->d_1, nullptr, 1, t, t, 0, nullptr, &cons, stream))
+      return -1;
+    // W2 leaves xh / stats of the block's output for the next block's QKV GEMM
+    return wm3_linear_fold(ws->mid, w->nm, w->w_2, w->nm, t, w->np, w->nm, WM3_EPI_BIAS_RESID_F32, x, w->hidden,
+                           w->hidden, w->b_2, nullptr, 1, t, t, 0, nullptr, &prod, stream);
+  }
   if (wm3_linear(ws->ctx, hd, w->w_o, hd, t, w->np, hd, WM3_EPI_BIAS_RESID_F32, x, w->hidden, w->hidden, w->b_o,
                  nullptr, stream))
     return -1;

@@ -418,6 +418,17 @@ DEVI uint32_t gelu_tanh_h2(float a, float b) {
   return *reinterpret_cast<const uint32_t*>(&y);
 }
 
+// Packed fp32 pair arithmetic (sm_100 FFMA2 / FADD2: two lanes of fp32 work per instruction).
+DEVI unsigned long long f2_bits(float lo, float hi) {
+  return (static_cast<unsigned long long>(__float_as_uint(hi)) << 32) | __float_as_uint(lo);
+}
+DEVI void ffma2(float& lo, float& hi, float alo, float ahi, float blo, float bhi, float clo, float chi) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_bits(alo, ahi)), "l"(f2_bits(blo, bhi)), "l"(f2_bits(clo, chi)));
+  lo = __uint_as_float(static_cast<uint32_t>(r));
+  hi = __uint_as_float(static_cast<uint32_t>(r >> 32));
+}
+
 DEVI void ldg256(const float* p, float (&v)[8]) {
   asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])

@@ -36,6 +36,8 @@ struct EpiParams {
   wm3_rope_t rope;
   wm3_halo_t halo;  // QKV epilogue: boundary rows also stored into the neighbours' K/V grids (peer memory)
   int has_halo;
+  wm3_ln_fold_t fold;  // LayerNorm fold (include/wm3.h): producer (residual epilogue) / consumer (next GEMM)
+  int ln_prod, ln_cons;
 };
 
 constexpr int GEMM_BM = 128;
@@ -313,8 +315,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tile_rows(tile, plane, r0);
         const int n0 = (tile % nn) * BN;
         for (int u = 0; u < NUNITS; ++u, ++c) {
-          const int slot = c % RSLOTS;
-          mbar_wait(rempty_bar(slot), ((c / RSLOTS) & 1) ^ 1);
+          constexpr int RS = RSLOTS > 0 ? RSLOTS : 1;
+          const int slot = c % RS;
+          mbar_wait(rempty_bar(slot), ((c / RS) & 1) ^ 1);
           mbar_arrive_expect_tx(rfull_bar(slot), Cfg::RSLOT_BYTES);
           tma_load_3d(rslot0 + slot * Cfg::RSLOT_BYTES, &tmOut, rfull_bar(slot), n0 + u * CW, r0, plane);
         }
@@ -331,6 +334,38 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int sbuf = 0;
     const uint32_t tempty_leader0 = (CG == 2) ? mapa_shared(tempty_bar(0), 0) : 0u;
     int tile_it = 0;
+    // LayerNorm fold, consumer side: the row's (mean, rstd) from the producer's partial sums.  The partials of
+    // the next tile's row are loaded while this tile is processed (prefetch, up to 8 pairs in 4 float4), so
+    // their latency never sits between the accumulator and the epilogue.
+    constexpr bool kCons = (EPI != WM3_EPI_BIAS_RESID_F32 && EPI != WM3_EPI_F32);
+    const bool cons = kCons && ep.ln_cons;
+    const bool cons_pf = cons && ep.fold.stats_parts <= 8;
+    float4 pf[4];
+    auto stats_issue = [&](int t) {
+      int pl, rr;
+      const int rw = (t < ntiles) ? tile_rows(t, pl, rr) + r_in_tile : 0;
+      const float4* sp = reinterpret_cast<const float4*>(ep.fold.stats_in +
+                                                         static_cast<size_t>(rw < M ? rw : 0) * (2 * WM3_LN_SLOTS));
+#pragma unroll
+      for (int i = 0; i < 4; ++i) pf[i] = (2 * i < ep.fold.stats_parts) ? __ldg(sp + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    auto stats_finish = [&](float& rstd, float& rmu) {
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        s1 += pf[i].x + pf[i].z;
+        s2 += pf[i].y + pf[i].w;
+      }
+      const float inv_n = 1.f / static_cast<float>(ep.fold.ln_n);
+      const float mu = s1 * inv_n;
+      rstd = rsqrtf(fmaxf(fmaf(-mu, mu, s2 * inv_n), 0.f) + ep.fold.eps);
+      rmu = rstd * mu;
+    };
+    float ln_rstd_next = 0.f, ln_rmu_next = 0.f;
+    if (cons_pf) {
+      stats_issue(tile0);
+      stats_finish(ln_rstd_next, ln_rmu_next);
+    }
     for (int tile = tile0; tile < ntiles; tile += tstep, ++tile_it) {
       int plane, r0;
       const int m0 = tile_rows(tile, plane, r0);
@@ -338,6 +373,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int row = m0 + r_in_tile;
       const int prow = r0 + r_in_tile;  // row within the plane
       const bool row_ok = (prow < ep.plane_rows) && row < M;
+      float ln_rstd = ln_rstd_next, ln_rmu = ln_rmu_next;
+      if (cons_pf) {
+        stats_issue(tile + tstep);  // consumed after this tile's units
+      } else if (cons) {
+        const float* sp = ep.fold.stats_in + static_cast<size_t>(row < M ? row : 0) * (2 * WM3_LN_SLOTS);
+        float s1 = 0.f, s2 = 0.f;
+        for (int p = 0; p < ep.fold.stats_parts; ++p) {
+          s1 += sp[2 * p];
+          s2 += sp[2 * p + 1];
+        }
+        const float inv_n = 1.f / static_cast<float>(ep.fold.ln_n);
+        const float mu = s1 * inv_n;
+        ln_rstd = rsqrtf(fmaxf(fmaf(-mu, mu, s2 * inv_n), 0.f) + ep.fold.eps);
+        ln_rmu = ln_rstd * mu;
+      }
+      // LayerNorm fold, producer side: partial (sum, sum of squares) of this group's columns of the row
+      float ln_s1 = 0.f, ln_s2 = 0.f;
       // residual prefetch, RESID_DEPTH chunks of this group ahead: the first ones overlap the mainloop wait
       // (the residual epilogue is HBM-latency bound: more bytes in flight per thread)
 #ifndef WM3_RESID_DEPTH
@@ -357,35 +409,70 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int u = g; u < NUNITS; u += 2) {
         const int n = n0 + u * CW;
         const int it = (u - g) >> 1;  // compile-time after unrolling
-        float(&xa)[32] = xr[it % (RESID_DEPTH + 1)];
+        const float* xa = Cfg::RESID_TMA ? nullptr : xr[it % (RESID_DEPTH + 1)];
         if (EPI == WM3_EPI_BIAS_RESID_F32 && !Cfg::RESID_TMA && u + 2 * RESID_DEPTH < NUNITS)
           load_resid(ep, row, row_ok, n + 2 * RESID_DEPTH * CW, xr[(it + RESID_DEPTH) % (RESID_DEPTH + 1)]);
-        if (Cfg::RESID_TMA) {
-          // this unit's residual chunk from its smem slot (SWIZZLE_128B rows, as the TMA box landed)
-          const int c = tile_it * NUNITS + u;
-          const int slot = c % (RSLOTS > 0 ? RSLOTS : 1);
-          mbar_wait(rfull_bar(slot), (c / (RSLOTS > 0 ? RSLOTS : 1)) & 1);
-          const uint32_t rb = rslot0 + slot * Cfg::RSLOT_BYTES;
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            ld_shared_v4(rb + sw128_off(r_in_tile, j), xa[4 * j], xa[4 * j + 1], xa[4 * j + 2], xa[4 * j + 3]);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(rempty_bar(slot));
-        }
         if (Tr::F32) {
           uint32_t r[32];
           tmem_ld32(taddr + u * CW, r);
           tmem_ld_wait();
           float* v = reinterpret_cast<float*>(r);  // accumulate in place: no extra 32-register copy
           if (EPI == WM3_EPI_BIAS_RESID_F32) {
+            // residual chunk: from its TMA smem slot (SWIZZLE_128B rows, as the box landed), or the registers
+            int rslot = 0;
+            uint32_t rb = 0;
+            if (Cfg::RESID_TMA) {
+              const int c = tile_it * NUNITS + u;
+              rslot = c % (RSLOTS > 0 ? RSLOTS : 1);
+              mbar_wait(rfull_bar(rslot), (c / (RSLOTS > 0 ? RSLOTS : 1)) & 1);
+              rb = rslot0 + rslot * Cfg::RSLOT_BYTES;
+            }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const float4 b = (n + 4 * j < ep.n_valid) ? __ldg(reinterpret_cast<const float4*>(ep.bias + n) + j)
                                                         : make_float4(0.f, 0.f, 0.f, 0.f);
-              v[4 * j + 0] += b.x + xa[4 * j + 0];
-              v[4 * j + 1] += b.y + xa[4 * j + 1];
-              v[4 * j + 2] += b.z + xa[4 * j + 2];
-              v[4 * j + 3] += b.w + xa[4 * j + 3];
+              float4 xv;
+              if (Cfg::RESID_TMA)
+                ld_shared_v4(rb + sw128_off(r_in_tile, j), xv.x, xv.y, xv.z, xv.w);
+              else
+                xv = make_float4(xa[4 * j + 0], xa[4 * j + 1], xa[4 * j + 2], xa[4 * j + 3]);
+              v[4 * j + 0] += b.x + xv.x;
+              v[4 * j + 1] += b.y + xv.y;
+              v[4 * j + 2] += b.z + xv.z;
+              v[4 * j + 3] += b.w + xv.w;
+            }
+            if (Cfg::RESID_TMA) {
+              __syncwarp();
+              if (lane == 0) mbar_arrive(rempty_bar(rslot));
+            }
+            if (ep.ln_prod) {
+              // the updated stream as the next GEMM's fp16 operand, and its row statistics
+              float s1b = 0.f, s2b = 0.f;  // packed pairs: (even, odd) column partial sums
+#pragma unroll
+              for (int e = 0; e < 32; e += 2) {
+                const float ta = (n + e < ep.n_valid) ? v[e] : 0.f;
+                const float tb = (n + e + 1 < ep.n_valid) ? v[e + 1] : 0.f;
+                ffma2(ln_s1, s1b, ta, tb, 1.f, 1.f, ln_s1, s1b);
+                ffma2(ln_s2, s2b, ta, tb, ta, tb, ln_s2, s2b);
+              }
+              ln_s1 += s1b;
+              ln_s2 += s2b;
+              if (row_ok) {
+                elem_t* dst = static_cast<elem_t*>(ep.fold.xh_out) + static_cast<size_t>(row) * ep.fold.ld_xh + n;
+                if (n + 32 <= ep.n_valid) {
+#pragma unroll
+                  for (int h = 0; h < 2; ++h) {
+                    uint32_t w8[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) w8[e] = pack_elem(v[16 * h + 2 * e], v[16 * h + 2 * e + 1]);
+                    stg256(dst + 16 * h, w8);
+                  }
+                } else {
+#pragma unroll
+                  for (int e = 0; e < 32; ++e)
+                    if (n + e < ep.n_valid) dst[e] = to_elem(v[e]);
+                }
+              }
             }
           }
           // staging row: 8 x 16 B chunks of 4 floats
@@ -407,11 +494,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             v[e] = __uint_as_float(r0[e]);
             v[32 + e] = __uint_as_float(r1[e]);
           }
+          if (cons) {
+            // folded LayerNorm: rstd * acc - rstd * mean * c[col] + d[col]   (d = b + beta . W, in ep.bias)
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float4 b = (n + 4 * j < ep.n_valid) ? __ldg(reinterpret_cast<const float4*>(ep.bias + n) + j)
-                                                      : make_float4(0.f, 0.f, 0.f, 0.f);
-            v[4 * j + 0] += b.x; v[4 * j + 1] += b.y; v[4 * j + 2] += b.z; v[4 * j + 3] += b.w;
+            for (int j = 0; j < 16; ++j) {
+              const bool okc = n + 4 * j < ep.n_valid;
+              const float4 b = okc ? __ldg(reinterpret_cast<const float4*>(ep.bias + n) + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+              const float4 c = okc ? __ldg(reinterpret_cast<const float4*>(ep.fold.fold_c + n) + j)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+              float t0, t1, t2, t3;  // packed pairs: two FFMA2 per two columns
+              ffma2(t0, t1, -ln_rmu, -ln_rmu, c.x, c.y, b.x, b.y);
+              ffma2(t2, t3, -ln_rmu, -ln_rmu, c.z, c.w, b.z, b.w);
+              ffma2(v[4 * j + 0], v[4 * j + 1], v[4 * j + 0], v[4 * j + 1], ln_rstd, ln_rstd, t0, t1);
+              ffma2(v[4 * j + 2], v[4 * j + 3], v[4 * j + 2], v[4 * j + 3], ln_rstd, ln_rstd, t2, t3);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float4 b = (n + 4 * j < ep.n_valid) ? __ldg(reinterpret_cast<const float4*>(ep.bias + n) + j)
+                                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+              v[4 * j + 0] += b.x; v[4 * j + 1] += b.y; v[4 * j + 2] += b.z; v[4 * j + 3] += b.w;
+            }
           }
 #if !defined(WM3_OPERAND_BF16) && WM3_GELU_VARIANT == 2
           constexpr bool gelu_h2 = (EPI == WM3_EPI_BIAS_GELU_BF16);  // f16x2 GELU straight to packed pairs
@@ -466,6 +569,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           bulk_commit();
         }
         if (Cfg::STAGING_PER_GROUP > 1) sbuf ^= 1;
+      }
+      if (cons_pf) stats_finish(ln_rstd_next, ln_rmu_next);
+      if (EPI == WM3_EPI_BIAS_RESID_F32 && ep.ln_prod && row_ok) {
+        float* so = ep.fold.stats_out + static_cast<size_t>(row) * (2 * WM3_LN_SLOTS) + 2 * ((tile % nn) * 2 + g);
+        *reinterpret_cast<float2*>(so) = make_float2(ln_s1, ln_s2);
       }
       tc_fence_before();
       __syncwarp();
@@ -551,7 +659,7 @@ struct OutPlanes {
 
 static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi, void* out,
                        int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, const OutPlanes& op,
-                       void* stream, const wm3_halo_t* halo = nullptr) {
+                       void* stream, const wm3_halo_t* halo = nullptr, const wm3_ln_fold_t* fold = nullptr) {
   if (m <= 0 || n <= 0 || k <= 0) return set_error("wm3_linear: bad sizes m=%d n=%d k=%d", m, n, k);
   const bool f32_out = (epi == WM3_EPI_F32 || epi == WM3_EPI_BIAS_RESID_F32);
   if ((lda % 8) || (ldb % 8) || (ldo % (f32_out ? 4 : 8)))
@@ -601,6 +709,21 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
     ep.halo = *halo;
     ep.has_halo = 1;
   }
+  if (fold != nullptr) {
+    ep.fold = *fold;
+    ep.ln_prod = fold->xh_out != nullptr || fold->stats_out != nullptr;
+    ep.ln_cons = fold->stats_in != nullptr;
+    const int ntile_n = (n + bn - 1) / bn;
+    if (ep.ln_prod && (epi != WM3_EPI_BIAS_RESID_F32 || fold->xh_out == nullptr || fold->stats_out == nullptr ||
+                       (fold->ld_xh % 16) || fold->ld_xh < n_valid || (reinterpret_cast<uintptr_t>(fold->xh_out) % 32) ||
+                       2 * ntile_n > WM3_LN_SLOTS || (n_valid % 2)))
+      return set_error("wm3_linear: bad LayerNorm-fold producer (residual epilogue, xh and stats, ld_xh %% 16, "
+                       "<= %d column tiles)", WM3_LN_SLOTS / 2);
+    if (ep.ln_cons && (epi == WM3_EPI_BIAS_RESID_F32 || epi == WM3_EPI_F32 || fold->fold_c == nullptr ||
+                       fold->stats_parts < 1 || fold->stats_parts > WM3_LN_SLOTS || fold->ln_n < 1))
+      return set_error("wm3_linear: bad LayerNorm-fold consumer (bf16 epilogue, fold_c, 1..%d stats parts)",
+                       WM3_LN_SLOTS);
+  }
   if (epi == WM3_EPI_QKV_ROPE) {
     if (rope == nullptr) return set_error("wm3_linear: rope descriptor required");
     ep.rope = *rope;
@@ -649,6 +772,14 @@ extern "C" int wm3_linear_planes_halo(const void* a, int lda, const void* b, int
                                       const wm3_halo_t* halo, void* stream) {
   const OutPlanes op{planes, plane_rows, plane_stride, row_off};
   return linear_impl(a, lda, b, ldb, m, n, k, epi, out, ldo, n_valid, bias, rope, op, stream, halo);
+}
+
+extern "C" int wm3_linear_fold(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi, void* out,
+                               int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, int planes,
+                               int plane_rows, long long plane_stride, int row_off, const wm3_halo_t* halo,
+                               const wm3_ln_fold_t* fold, void* stream) {
+  const OutPlanes op{planes, plane_rows, plane_stride, row_off};
+  return linear_impl(a, lda, b, ldb, m, n, k, epi, out, ldo, n_valid, bias, rope, op, stream, halo, fold);
 }
 
 namespace wm3 {

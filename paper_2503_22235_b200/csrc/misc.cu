@@ -91,9 +91,71 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int ldx, int m, in
   for (int c = n + lane; c < ldo; c += 32) orow[c] = to_elem(0.f);
 }
 
+// Start of a LayerNorm-folded chain (include/wm3.h wm3_ln_fold_prep): one warp per row writes the fp16 copy of
+// the row (pad columns zero) and the row's (sum, sum of squares) as partial pair 0 of the consumer's stats.
+template <int NV>
+__global__ void ln_fold_prep_kernel(const float* __restrict__ x, int ldx, int m, int n, elem_t* __restrict__ xh,
+                                    int ld_xh, float* __restrict__ stats, int parts) {
+  griddep_launch_dependents();
+  griddep_wait();
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= m) return;
+  const float* xr = x + static_cast<size_t>(warp) * ldx;
+  elem_t* orow = xh + static_cast<size_t>(warp) * ld_xh;
+  float s1 = 0.f, s2 = 0.f;
+  if ((n % 4 == 0) && (ldx % 4 == 0) && (n <= NV * 128)) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * 32 + lane) * 4;
+      if (c < n) {
+        const float4 v = *reinterpret_cast<const float4*>(xr + c);
+        s1 += (v.x + v.y) + (v.z + v.w);
+        s2 = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, s2))));
+        uint2 pk;
+        pk.x = pack_elem(v.x, v.y);
+        pk.y = pack_elem(v.z, v.w);
+        *reinterpret_cast<uint2*>(orow + c) = pk;
+      }
+    }
+  } else {
+    for (int c = lane; c < n; c += 32) {
+      const float v = xr[c];
+      s1 += v;
+      s2 = fmaf(v, v, s2);
+      orow[c] = to_elem(v);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  for (int c = n + lane; c < ld_xh; c += 32) orow[c] = to_elem(0.f);
+  float* sr = stats + static_cast<size_t>(warp) * (2 * WM3_LN_SLOTS);
+  for (int p = lane; p < parts; p += 32) {
+    sr[2 * p] = p == 0 ? s1 : 0.f;
+    sr[2 * p + 1] = p == 0 ? s2 : 0.f;
+  }
+}
+
 }  // namespace wm3
 
 using namespace wm3;
+
+extern "C" int wm3_ln_fold_prep(const float* x, int ldx, int m, int n, void* xh, int ld_xh, float* stats, int parts,
+                                void* stream) {
+  if (m <= 0) return 0;
+  if (n <= 0 || ld_xh < n || ldx < n || parts < 1 || parts > WM3_LN_SLOTS)
+    return set_error("wm3_ln_fold_prep: bad sizes (n %d ld_xh %d parts %d)", n, ld_xh, parts);
+  const int threads = 256;
+  const int blocks = (m * 32 + threads - 1) / threads;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  auto* o = reinterpret_cast<elem_t*>(xh);
+  auto kern = (n <= 256) ? ln_fold_prep_kernel<2> : (n <= 1024) ? ln_fold_prep_kernel<8> : ln_fold_prep_kernel<16>;
+  if (launch_pdl(kern, dim3(blocks), dim3(threads), 0, s, x, ldx, m, n, o, ld_xh, stats, parts)) return -1;
+  return check_launch("ln_fold_prep_kernel");
+}
 
 extern "C" int wm3_neighbor_table(int depth, int rows, int cols, int wd, int wh, int ww, int row0, int nrows,
                                   int64_t* out, void* stream) {

@@ -121,9 +121,11 @@ class DeviceModel:
         cfg = self.cfg
         ext = cfg.latent_extents
         rope = CACHE.rope(ext, cfg.head_dim)
-        for pre in prefixes:
+        for i, pre in enumerate(prefixes):
             bw = CACHE.block(self.params, pre, cfg.heads)
-            block_forward(x, bw, CACHE.workspace(ext, cfg.window, bw, batch=batch), rope, ext, cfg.window)
+            # folded LayerNorm: block i > 0 finds x's fp16 copy and row statistics left by block i-1's W2
+            block_forward(x, bw, CACHE.workspace(ext, cfg.window, bw, batch=batch), rope, ext, cfg.window,
+                          prepped=i > 0)
 
 
 _models: dict = {}

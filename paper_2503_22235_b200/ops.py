@@ -56,10 +56,33 @@ def layernorm_bf16(x: torch.Tensor, gain: torch.Tensor, bias: torch.Tensor, ldo:
     return out
 
 
+def ln_fold_consumer(stats: torch.Tensor, parts: int, ln_n: int, fold_c: torch.Tensor,
+                     eps: float = 1e-6) -> "_lib.LnFoldT":
+    """wm3_ln_fold_t for a GEMM that applies the folded LayerNorm (reads the row statistics)."""
+    _req(stats, torch.float32, "stats")
+    return _lib.LnFoldT(None, 0, None, stats.data_ptr(), int(parts), int(ln_n), float(eps), fold_c.data_ptr())
+
+
+def ln_fold_producer(xh: torch.Tensor, stats: torch.Tensor) -> "_lib.LnFoldT":
+    """wm3_ln_fold_t for a residual GEMM that also writes the fp16 copy of x and its row statistics."""
+    _req(xh, _lib.ELEM, "xh")
+    _req(stats, torch.float32, "stats")
+    return _lib.LnFoldT(xh.data_ptr(), xh.stride(0), stats.data_ptr(), None, 0, 0, 0.0, None)
+
+
+def ln_fold_prep(x: torch.Tensor, n: int, xh: torch.Tensor, stats: torch.Tensor, parts: int) -> None:
+    """Start of a folded chain: xh = fp16(x) (pad columns zero), stats pair 0 = row (sum, sum of squares)."""
+    _req(x, torch.float32, "x")
+    _req(xh, _lib.ELEM, "xh")
+    check(_lib.lib().wm3_ln_fold_prep(ptr(x), x.stride(0), x.shape[0], int(n), ptr(xh), xh.stride(0), ptr(stats),
+                                      int(parts), stream_ptr()), "wm3_ln_fold_prep")
+
+
 def linear(a: torch.Tensor, w: torch.Tensor, epi: int, bias: torch.Tensor | None = None,
            out: torch.Tensor | None = None, n_valid: int | None = None,
-           rope: "_lib.RopeT | None" = None) -> torch.Tensor:
-    """out = epilogue(a @ w.T + bias); a (M, K) bf16, w (N, K) bf16 (weights stored (out, in))."""
+           rope: "_lib.RopeT | None" = None, fold: "_lib.LnFoldT | None" = None) -> torch.Tensor:
+    """out = epilogue(a @ w.T + bias); a (M, K) bf16, w (N, K) bf16 (weights stored (out, in)).  fold: the
+    folded-LayerNorm producer / consumer descriptor (ln_fold_producer / ln_fold_consumer)."""
     _req(a, _lib.ELEM, "a")
     _req(w, _lib.ELEM, "w")
     m, k = a.shape
@@ -74,6 +97,11 @@ def linear(a: torch.Tensor, w: torch.Tensor, epi: int, bias: torch.Tensor | None
     _req(out, torch.float32 if f32_out else _lib.ELEM, "out")
     nv = out.shape[1] if n_valid is None else int(n_valid)
     rp = None if rope is None else ctypes_byref(rope)
+    if fold is not None:
+        check(_lib.lib().wm3_linear_fold(ptr(a), a.stride(0), ptr(w), w.stride(0), m, n, k, int(epi), ptr(out),
+                                         out.stride(0), nv, ptr(bias), rp, 1, m, m, 0, None, ctypes_byref(fold),
+                                         stream_ptr()), "wm3_linear_fold")
+        return out
     check(_lib.lib().wm3_linear(ptr(a), a.stride(0), ptr(w), w.stride(0), m, n, k, int(epi), ptr(out),
                                 out.stride(0), nv, ptr(bias), rp, stream_ptr()), "wm3_linear")
     return out
@@ -114,7 +142,8 @@ class KVGrid:
 
 
 def linear_grid(a: torch.Tensor, w: torch.Tensor, epi: int, bias: torch.Tensor, out: torch.Tensor, grid: KVGrid,
-                rope: "_lib.RopeT | None" = None, halo: "_lib.HaloT | None" = None) -> torch.Tensor:
+                rope: "_lib.RopeT | None" = None, halo: "_lib.HaloT | None" = None,
+                fold: "_lib.LnFoldT | None" = None) -> torch.Tensor:
     """linear() whose output rows (band tokens) land in the K/V grid `out` (halo rows left untouched).  With
     `halo` (wm3_halo_t), the QKV epilogue also stores the band's boundary K/V rows into the neighbouring bands'
     grids (fused halo exchange over peer memory)."""
@@ -127,7 +156,10 @@ def linear_grid(a: torch.Tensor, w: torch.Tensor, epi: int, bias: torch.Tensor, 
     plane = grid.rows * grid.cols
     args = (ptr(a), a.stride(0), ptr(w), w.stride(0), m, n, k, int(epi), ptr(out), out.stride(0), out.shape[1],
             ptr(bias), rp, grid.planes, plane, grid.rows_ext * grid.cols, grid.halo_lo * grid.cols)
-    if halo is None:
+    if fold is not None:
+        check(_lib.lib().wm3_linear_fold(*args, None if halo is None else ctypes_byref(halo), ctypes_byref(fold),
+                                         stream_ptr()), "wm3_linear_fold")
+    elif halo is None:
         check(_lib.lib().wm3_linear_planes(*args, stream_ptr()), "wm3_linear_planes")
     else:
         check(_lib.lib().wm3_linear_planes_halo(*args, ctypes_byref(halo), stream_ptr()), "wm3_linear_planes_halo")

@@ -137,3 +137,40 @@ def test_native_block_call_equals_composed_launches():
     block_forward(a, bw, Workspace(ops.KVGrid(ext, win), bw), rope, ext, win)                    # native
     block_forward(b, bw, Workspace(ops.KVGrid(ext, win), bw), rope, ext, win, mark=lambda i: None)  # composed
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("offset", [0.0, 8.0])
+def test_folded_layernorm_matches_separate_launches(offset, monkeypatch):
+    """LayerNorm folded into the QKV / W1 GEMMs (wm3_ln_fold_t: residual epilogues write x's fp16 copy and row
+    statistics, the next GEMM applies rstd * acc - rstd * mean * c + d) against separate LayerNorm launches and
+    the oracle, also for tokens whose channel mean sits 8 std away from zero (the fold rounds x before the mean
+    is removed)."""
+    import torch
+
+    from paper_2503_22235_b200.blocks import RopeTables, Workspace, block_forward, prepare_block
+    from paper_2503_22235_b200.ops import KVGrid
+    ext, win, dim, heads = (5, 18, 36), (5, 7, 7), 1024, 8
+    t = int(np.prod(ext))
+    params = _params(dim, heads, seed=4)
+    x = np.random.default_rng(5).standard_normal((t, dim)) + offset
+    outs = {}
+    for fold in ("1", "0"):
+        monkeypatch.setenv("WM3_LN_FOLD", fold)
+        bw = prepare_block(params, "blk", heads)
+        assert bw.folded == (fold == "1")
+        xd = torch.from_numpy(x.astype(np.float32)).cuda()
+        ws = Workspace(KVGrid(ext, win), bw)
+        block_forward(xd, bw, ws, RopeTables(ext, dim // heads), ext, win)
+        # the chain hand-off: the W2 epilogue left fp16(x_out) and its row sums for the next block
+        xo = xd.cpu().numpy().astype(np.float64)
+        if bw.folded:
+            xh = ws.hn[:, :dim].float().cpu().numpy()
+            assert np.allclose(xh, xo, rtol=2e-3, atol=1e-3)
+            st = ws.stats.view(t, -1, 2).cpu().numpy()[:, :bw.ln_parts].sum(1)
+            np.testing.assert_allclose(st[:, 0], xo.sum(1), rtol=1e-4, atol=1e-2)
+            np.testing.assert_allclose(st[:, 1], (xo * xo).sum(1), rtol=1e-4)
+        outs[fold] = xo
+    want = om.natten_block(x, params, "blk", ext, win, heads, chunk=128)
+    assert _rel(outs["1"] - x, outs["0"] - x) < 5e-3
+    assert _rel(outs["1"] - x, want - x) < 3e-2
+    assert _rel(outs["1"], want) < 1e-2

@@ -170,3 +170,26 @@ def test_encode_rejects_bad_shapes():
         m.encode(st, params, cfg)
     with pytest.raises(ConfigError):
         m.encode(_state(cfg), params, cfg, source="ghost")
+
+
+def test_folded_layernorm_chain(monkeypatch):
+    """WM3_LN_FOLD=1 (LayerNorm folded into the GEMM epilogues): blocks after the first of each chain take x's fp16
+    copy and row statistics from the previous block's W2 epilogue (graph-captured rollout, banded processor).
+    Forecast parity with the oracle and agreement with the separate-LayerNorm path."""
+    m, r = _pkg()
+    from paper_2503_22235_b200.bands import forecast_banded
+    cfg = m.mid_config()
+    st = _state(cfg, seed=6)
+    plain = m.init_model_params(cfg, seed=7, zero_residual=False)
+    ref_s, ref_a = om.forecast(st.surface, st.atmos, 7, {k: v.values for k, v in plain.items()}, cfg)
+    base = r.forecast(st, 7, plain, cfg)
+    monkeypatch.setenv("WM3_LN_FOLD", "1")
+    folded = m.init_model_params(cfg, seed=7, zero_residual=False)  # fresh dict: blocks prepared folded
+    out = r.forecast(st, 7, folded, cfg)
+    from paper_2503_22235_b200.runtime import CACHE
+    assert CACHE.block(folded, "proc6.blk3", cfg.heads).folded
+    rel = per_variable_rel(out.surface.values, out.atmos.values, ref_s, ref_a)
+    assert max(rel.values()) < 1e-2, max(rel.values())
+    assert _rel(out.surface.values, base.surface.values) < 5e-3
+    banded = forecast_banded(st, 7, folded, cfg, world=2)
+    assert _rel(banded.surface.values, out.surface.values) < 5e-3
