@@ -62,8 +62,9 @@ def test_band_block_matches_full(world, ext, dim, heads, monkeypatch):
     torch.cuda.synchronize()
     upd_full, upd_band = full - x, banded - x
     rel = float((upd_band - upd_full).norm() / upd_full.norm())
-    # the attention kernel's key-chunk order depends on the band height: measured 2.3e-3 at 8 bands
-    assert rel < 3e-3, rel
+    # the attention kernel's key-chunk order depends on the band height, so the fp32 summation order differs:
+    # measured 2.3e-3 - 3.6e-3 at 8 bands across builds (the oracle tolerance for the update is 3e-2)
+    assert rel < 5e-3, rel
 
 
 def test_band_block_forward_with_callback_single_band():
