@@ -57,7 +57,10 @@ struct GemmCfg {
   // epilogue, instead of per-thread global loads (the O-proj epilogue was HBM-latency bound); one mainloop
   // stage gives up its smem for them.
   static constexpr bool RESID_TMA = (EPI == WM3_EPI_BIAS_RESID_F32) && WM3_RESID_TMA;
-  static constexpr int RSLOTS = RESID_TMA ? (CG == 2 ? 2 : 3) : 0;
+  // Two slots: with an even slot count and even units per tile, slot c % RSLOTS has the parity of the unit, so
+  // each slot is consumed by one epilogue group only, in order (an odd count interleaves the groups on a slot
+  // and a fast group can then pass a parity wait one phase early).
+  static constexpr int RSLOTS = RESID_TMA ? 2 : 0;
   // CTA pairs free 16 KB per stage: 6 stages, or 5 stages with double-buffered epilogue staging
   static constexpr int STAGES = (CG == 2) ? ((WM3_PAIR_STAGING == 2 || RESID_TMA) ? 5 : 6) : (RESID_TMA ? 3 : 4);
   static constexpr int STAGING_PER_GROUP = (BN == 256) ? ((CG == 2) ? WM3_PAIR_STAGING : 1) : 2;
@@ -169,6 +172,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   constexpr int RSLOTS = Cfg::RSLOTS;
   constexpr int CW = Tr::CW;
   constexpr int NUNITS = BN / CW;
+  static_assert(!Cfg::RESID_TMA || (NUNITS % 2 == 0 && Cfg::RSLOTS % 2 == 0),
+                "residual slots must map onto one epilogue group each");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
@@ -442,6 +447,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               v[4 * j + 3] += b.w + xv.w;
             }
             if (Cfg::RESID_TMA) {
+              // the slot's next TMA load (async proxy) must not overtake these generic-proxy reads
+              fence_proxy_async();
               __syncwarp();
               if (lane == 0) mbar_arrive(rempty_bar(rslot));
             }

@@ -168,3 +168,26 @@ def test_natten_windows_bit_exact():
         assert np.array_equal(got[..., 1], np.broadcast_to(sh[None, :, None], (d, h, w)))
         assert np.array_equal(got[..., 2], np.broadcast_to(((np.arange(w) - (win[2] - 1) // 2) % w)[None, None, :],
                                                           (d, h, w)))
+
+
+def test_residual_gemm_bitwise_repeatable():
+    """The residual epilogue streams fp32 residual chunks through smem slots by TMA (gemm.cu RESID_TMA); a slot
+    hand-off race would show up as run-to-run differences.  40 repeats of the O-proj and W2 shapes (CTA pairs)
+    and of a single-CTA residual GEMM must all be bitwise identical."""
+    E = lib().ELEM
+    g = torch.Generator(device="cuda").manual_seed(3)
+    T, D = 40000, 1024
+    x0 = torch.randn(T, D, device="cuda", generator=g)
+    b = torch.randn(D, device="cuda", generator=g)
+    for k, n in ((1024, 1024), (4096, 1024), (256, 128)):
+        a = torch.randn(T, k, device="cuda", generator=g).to(E)
+        w = (torch.randn(n, k, device="cuda", generator=g) / 32).to(E)
+        xs = x0[:, :n].contiguous()
+        ref = xs.clone()
+        ops().linear(a, w, lib().WM3_EPI_BIAS_RESID_F32, bias=b[:n].contiguous(), out=ref)
+        for _ in range(40):
+            y = xs.clone()
+            ops().linear(a, w, lib().WM3_EPI_BIAS_RESID_F32, bias=b[:n].contiguous(), out=y)
+            assert torch.equal(y, ref), (k, n)
+        want = xs + (a.float() @ w.float().T) + b[:n]
+        assert ((ref - want).norm() / want.norm()).item() < 1e-3
