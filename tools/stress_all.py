@@ -55,3 +55,18 @@ stress("encode", lambda: [m.encode(st, p, cfg).tokens.device], 20)
 lat = m.encode(st, p, cfg)
 stress("decode", lambda: (lambda d: [d.surface.device, d.atmos.device])(m.decode(lat, p, cfg)), 20)
 print("mismatches", bad)
+
+# latitude bands (emulated ranks): separate copy and fused epilogue halo paths
+from paper_2503_22235_b200.bands import rollout_banded
+import paper_2503_22235_b200.rollout as R
+cfg = m.mid_config()
+pm = m.init_model_params(cfg, seed=7, zero_residual=False)
+rng = np.random.default_rng(4)
+stm = m.WeatherState(0, rng.standard_normal((cfg.surface_in, cfg.grid.rows, cfg.grid.cols)),
+                     rng.standard_normal((cfg.atmos_vars, cfg.levels, cfg.grid.rows, cfg.grid.cols)))
+latm = m.encode(stm, pm, cfg)
+bad.clear()
+stress("bands2", lambda: [rollout_banded(latm, (6, 1), pm, cfg, world=2).tokens.device], 30)
+stress("bands2_fused", lambda: [rollout_banded(latm, (6, 1), pm, cfg, world=2, fused=True).tokens.device], 30)
+stress("rollout_graph", lambda: [R.rollout(latm, (6, 6, 1), pm, cfg).tokens.device], 30)
+print("mismatches", bad)
