@@ -369,9 +369,16 @@ def run_gpu(args, world, rank, local_rank):
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local_rank)
+    # WM3_DIST_BACKEND=gloo: host-staged exchanges, for multi-process smoke runs of the N > 1 path on fewer GPUs
+    # than ranks (ranks then share devices round-robin; no kernel ever waits on another rank's kernel)
+    backend = os.environ.get("WM3_DIST_BACKEND", "nccl")
+    device = local_rank % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(device)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group(backend)
     from paper_2503_22235_b200.blocks import block_forward
 
     params, bw, me, local, ws, rope, exch, x = block_setup(world, rank)
@@ -399,7 +406,7 @@ def run_gpu(args, world, rank, local_rank):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
-    clk = ClockSampler(local_rank).__enter__()
+    clk = ClockSampler(device).__enter__()
     it = iter(marks)
 
     def timed_step():
@@ -481,7 +488,8 @@ def run_gpu(args, world, rank, local_rank):
                        "operands": "fp16 tensor-core operands, fp32 accumulate / residual / softmax",
                        "l2": "inputs larger than L2 (332 MB fp32 latent), no flush",
                        "parallelism": (f"latitude bands x{world} ("
-                                       + ("fused QKV-epilogue peer-memory halo" if FUSED_HALO else "NCCL halo")
+                                       + ("fused QKV-epilogue peer-memory halo" if FUSED_HALO else
+                                          f"{os.environ.get('WM3_DIST_BACKEND', 'nccl').upper()} halo")
                                        + ")") if world > 1 else "single GPU",
                        "band_rows_rank0": me.rows,
                        "layernorm": ("folded into the GEMM epilogues: O-proj / W2 write x's fp16 copy and row "

@@ -83,28 +83,41 @@ class HaloExchanger:
         me = self.me
         planes = getattr(grid, "planes", grid.depth)  # batch * depth for an ensemble batch
         g = buf.view(planes, grid.rows_ext, grid.cols, -1)
-        ops = []
+        # gloo moves host memory only: CUDA rows are staged through the host (the multi-process smoke runs of
+        # the N > 1 bench path on one device); NCCL sends / receives the device rows directly
+        stage = buf.is_cuda and dist.get_backend(self.group) == "gloo"
+        ops, post = [], []
+
+        def send(rows, peer):
+            ops.append(dist.P2POp(dist.isend, rows.cpu() if stage else rows.contiguous(), peer, self.group))
+
+        def recv(rows, peer):
+            if stage:
+                tmp = torch.empty(rows.shape, dtype=rows.dtype)
+                post.append((rows, tmp))
+                rows = tmp
+            ops.append(dist.P2POp(dist.irecv, rows, peer, self.group))
+
         lo0 = me.halo_lo  # buffer row of band row 0
         if me.rank > 0:
             up = self.bands[me.rank - 1]
             for d in range(planes):
                 if up.halo_hi:  # my first rows -> upper neighbour's bottom halo
-                    ops.append(dist.P2POp(dist.isend, g[d, lo0:lo0 + up.halo_hi].contiguous(), me.rank - 1,
-                                          self.group))
+                    send(g[d, lo0:lo0 + up.halo_hi], me.rank - 1)
                 if me.halo_lo:
-                    ops.append(dist.P2POp(dist.irecv, g[d, 0:me.halo_lo], me.rank - 1, self.group))
+                    recv(g[d, 0:me.halo_lo], me.rank - 1)
         if me.rank + 1 < len(self.bands):
             dn = self.bands[me.rank + 1]
             for d in range(planes):
                 if dn.halo_lo:  # my last rows -> lower neighbour's top halo
-                    ops.append(dist.P2POp(dist.isend, g[d, lo0 + me.rows - dn.halo_lo:lo0 + me.rows].contiguous(),
-                                          me.rank + 1, self.group))
+                    send(g[d, lo0 + me.rows - dn.halo_lo:lo0 + me.rows], me.rank + 1)
                 if me.halo_hi:
-                    ops.append(dist.P2POp(dist.irecv, g[d, lo0 + me.rows:lo0 + me.rows + me.halo_hi],
-                                          me.rank + 1, self.group))
+                    recv(g[d, lo0 + me.rows:lo0 + me.rows + me.halo_hi], me.rank + 1)
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        for rows, tmp in post:
+            rows.copy_(tmp)
 
 
 def local_band_tokens(x_global: torch.Tensor, extents, band: Band) -> torch.Tensor:
