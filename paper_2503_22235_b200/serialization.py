@@ -15,7 +15,6 @@ a 3 GB host copy plus per-tensor conversion with one streaming pass.
 
 from __future__ import annotations
 
-import mmap
 import struct
 
 import numpy as np
