@@ -113,19 +113,16 @@ int wm3_halo_wait(const int* flags, int n, int epoch, void* stream);
 /* LayerNorm folded into the GEMMs around it (attention.py:163-165, 180-181).  A residual GEMM
  * (WM3_EPI_BIAS_RESID_F32) acting as producer also writes an fp16 copy of the updated stream (xh_out, columns
  * < n_valid; pad columns untouched) and per row partial (sum, sum of squares) pairs into
- * stats_out[row][slot][2] (slot = 2 * column tile + epilogue group, every slot < 2 * ceil(n / tile) written).
- * The next GEMM, as consumer, takes A = xh with weights pre-scaled by the LN gain, sums the first stats_parts
- * pairs of its row into mean and rstd = 1 / sqrt(biased variance + eps) and applies
+ * stats_out[row][slot][2] (slot = 2 * column tile + epilogue group, every slot < 2 * ceil(n / tile) written);
+ * wm3_ln_fold_finalize turns them into row_stats[row] = (rstd, rstd * mean) (biased variance, eps).  The next
+ * GEMM, as consumer, takes A = xh with weights pre-scaled by the LN gain and applies
  * rstd * acc - rstd * mean * fold_c[col] + bias[col] before its own epilogue (bias = b + beta . W). */
 #define WM3_LN_SLOTS 16
 typedef struct {
   void* xh_out;
   int ld_xh;
   float* stats_out;
-  const float* stats_in;
-  int stats_parts;
-  int ln_n;
-  float eps;
+  const float* row_stats;
   const float* fold_c;
 } wm3_ln_fold_t;
 /* wm3_linear_planes_halo with an optional LayerNorm fold (producer and / or consumer side); halo may be NULL. */
@@ -133,9 +130,10 @@ int wm3_linear_fold(const void* a, int lda, const void* b, int ldb, int m, int n
                     int n_valid, const float* bias, const wm3_rope_t* rope, int planes, int plane_rows,
                     long long plane_stride, int row_off, const wm3_halo_t* halo, const wm3_ln_fold_t* fold,
                     void* stream);
-/* Start of a folded chain: xh = fp16(x) (columns >= n of each xh row zeroed) and stats (pair 0 = row sum and
- * sum of squares, pairs 1 .. parts-1 zero) for a consumer GEMM. */
-int wm3_ln_fold_prep(const float* x, int ldx, int m, int n, void* xh, int ld_xh, float* stats, int parts,
+/* Producer partials (the first `parts` pairs of each row) -> row_stats[m][2] = (rstd, rstd * mean) over n. */
+int wm3_ln_fold_finalize(const float* stats, int parts, int n, float eps, int m, float* row_stats, void* stream);
+/* Start of a folded chain: xh = fp16(x) (columns >= n of each xh row zeroed) and row_stats of x. */
+int wm3_ln_fold_prep(const float* x, int ldx, int m, int n, void* xh, int ld_xh, float eps, float* row_stats,
                      void* stream);
 
 /* One processor block (attention.py:146-184) as library calls: x (T, hidden) fp32 in place, T = batch * depth *
@@ -164,7 +162,8 @@ typedef struct {
 } wm3_block_weights_t;
 typedef struct {
   void *hn, *qkv, *ctx, *mid;
-  float* stats; /* [T][WM3_LN_SLOTS][2] LayerNorm partial sums (folded path); hn then holds the fp16 copy of x */
+  float* stats;     /* [T][WM3_LN_SLOTS][2] LayerNorm partial sums (folded path); hn then holds fp16(x) */
+  float* row_stats; /* [T][2] (rstd, rstd * mean) of x (folded path) */
 } wm3_block_ws_t;
 typedef struct {
   int batch, depth, rows, cols;    /* local band extents (batch = ensemble members) */

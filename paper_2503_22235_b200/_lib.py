@@ -52,7 +52,7 @@ class BlockWeightsT(ctypes.Structure):
 
 class BlockWsT(ctypes.Structure):
     """wm3_block_ws_t."""
-    _fields_ = [("hn", _vp), ("qkv", _vp), ("ctx", _vp), ("mid", _vp), ("stats", _vp)]
+    _fields_ = [("hn", _vp), ("qkv", _vp), ("ctx", _vp), ("mid", _vp), ("stats", _vp), ("row_stats", _vp)]
 
 
 class BlockGeomT(ctypes.Structure):
@@ -66,8 +66,7 @@ LN_SLOTS = 16  # WM3_LN_SLOTS
 
 class LnFoldT(ctypes.Structure):
     """wm3_ln_fold_t (include/wm3.h)."""
-    _fields_ = [("xh_out", _vp), ("ld_xh", _i), ("stats_out", _vp), ("stats_in", _vp), ("stats_parts", _i),
-                ("ln_n", _i), ("eps", _f), ("fold_c", _vp)]
+    _fields_ = [("xh_out", _vp), ("ld_xh", _i), ("stats_out", _vp), ("row_stats", _vp), ("fold_c", _vp)]
 
 
 # name -> argtypes; every function returns int status
@@ -79,7 +78,8 @@ SIGNATURES = {
                           _i, _i, ctypes.c_longlong, _i, _vp],
     "wm3_linear_fold": [_vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, ctypes.POINTER(RopeT),
                         _i, _i, ctypes.c_longlong, _i, ctypes.POINTER(HaloT), ctypes.POINTER(LnFoldT), _vp],
-    "wm3_ln_fold_prep": [_vp, _i, _i, _i, _vp, _i, _vp, _i, _vp],
+    "wm3_ln_fold_prep": [_vp, _i, _i, _i, _vp, _i, _f, _vp, _vp],
+    "wm3_ln_fold_finalize": [_vp, _i, _i, _f, _i, _vp, _vp],
     "wm3_linear_planes_halo": [_vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, ctypes.POINTER(RopeT),
                                _i, _i, ctypes.c_longlong, _i, ctypes.POINTER(HaloT), _vp],
     "wm3_halo_signal": [_vp, _vp, _i, _vp],

@@ -193,9 +193,9 @@ def _fold_ln(w_in_out: np.ndarray, bias: np.ndarray, gain: np.ndarray, beta: np.
 
 
 def ln_fold_enabled() -> bool:
-    """WM3_LN_FOLD=1 selects the folded LayerNorm (5 launches per block).  Off by default: measured in-block on
-    one B200 it costs more epilogue time than the two LayerNorm launches it removes (2.228 vs 2.181 ms per block:
-    QKV +0.066, O-proj +0.045, W1 +0.079, W2 +0.008 ms against 0.160 ms of LayerNorm)."""
+    """WM3_LN_FOLD=1 selects the folded LayerNorm (no LayerNorm launches; two tiny row-statistics launches).
+    Off by default: measured in-block on one B200 the epilogue work it adds costs about what the two LayerNorm
+    launches cost (2.127 vs 2.111 ms per block)."""
     return os.environ.get("WM3_LN_FOLD", "0") == "1"
 
 
@@ -304,8 +304,9 @@ class Workspace:
         self.mid = torch.empty((tokens, bw.nm), dtype=_lib.ELEM, device=device)
         # LayerNorm-fold row statistics ([tokens][WM3_LN_SLOTS] (sum, sum of squares) pairs)
         self.stats = torch.zeros((tokens, 2 * _lib.LN_SLOTS), dtype=torch.float32, device=device)
+        self.row_stats = torch.zeros((tokens, 2), dtype=torch.float32, device=device)
         self._native = _lib.BlockWsT(self.hn.data_ptr(), self.qkv.data_ptr(), self.ctx.data_ptr(),
-                                     self.mid.data_ptr(), self.stats.data_ptr())
+                                     self.mid.data_ptr(), self.stats.data_ptr(), self.row_stats.data_ptr())
 
     def native(self) -> "_lib.BlockWsT":
         return self._native
@@ -345,12 +346,12 @@ def block_forward(x: torch.Tensor, bw: BlockWeights, ws: Workspace, rope: RopeTa
     rs = rope.struct(extents, row0, bw.heads, bw.dhp)
     if bw.folded:
         parts = bw.ln_parts
-        cons_qkv = ops.ln_fold_consumer(ws.stats, parts, bw.hidden, bw.c_qkv)
-        cons_1 = ops.ln_fold_consumer(ws.stats, parts, bw.hidden, bw.c_1)
+        cons_qkv = ops.ln_fold_consumer(ws.row_stats, bw.c_qkv)
+        cons_1 = ops.ln_fold_consumer(ws.row_stats, bw.c_1)
         prod = ops.ln_fold_producer(ws.hn, ws.stats)
         mk(0)
         if not prepped:
-            ops.ln_fold_prep(x, bw.hidden, ws.hn, ws.stats, parts)
+            ops.ln_fold_prep(x, bw.hidden, ws.hn, ws.row_stats)
         mk(1)
         ops.linear_grid(ws.hn, bw.w_qkv_f, L.WM3_EPI_QKV_ROPE, bw.d_qkv, ws.qkv, g, rope=rs, fold=cons_qkv)
         if halo_exchange is not None:
@@ -360,10 +361,12 @@ def block_forward(x: torch.Tensor, bw: BlockWeights, ws: Workspace, rope: RopeTa
         mk(3)
         ops.linear(ws.ctx, bw.w_o, L.WM3_EPI_BIAS_RESID_F32, bias=bw.b_o, out=x, n_valid=bw.hidden, fold=prod)
         mk(4)
+        ops.ln_fold_finalize(ws.stats, parts, bw.hidden, ws.row_stats)
         mk(5)
         ops.linear(ws.hn, bw.w_1_f, L.WM3_EPI_BIAS_GELU_BF16, bias=bw.d_1, out=ws.mid, fold=cons_1)
         mk(6)
         ops.linear(ws.mid, bw.w_2, L.WM3_EPI_BIAS_RESID_F32, bias=bw.b_2, out=x, n_valid=bw.hidden, fold=prod)
+        ops.ln_fold_finalize(ws.stats, parts, bw.hidden, ws.row_stats)  # for the next block (counted in W2's slot)
         mk(7)
         return
     mk(0)

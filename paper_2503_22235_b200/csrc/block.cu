@@ -10,8 +10,8 @@
 // With folded weights (w_qkv_f != NULL) the two LayerNorms are not separate launches (wm3_ln_fold_t): the
 // residual epilogues (O-proj, W2) also write the fp16 copy of the updated stream into ws->hn and its row
 // statistics into ws->stats, and the QKV / W1 GEMMs consume them with gain-scaled weights.  A block is then
-// 5 launches (QKV, NA, O-proj, W1, W2); the first block of a chain (geom x_prepped = 0) starts with
-// wm3_ln_fold_prep.
+// 5 GEMM / attention launches plus two tiny row-statistics launches (wm3_ln_fold_finalize); the first block of
+// a chain (geom x_prepped = 0) starts with wm3_ln_fold_prep.
 #include <cmath>
 
 #include "launch.h"
@@ -33,19 +33,16 @@ static int check_block(const float* x, const wm3_block_weights_t* w, const wm3_b
                      w->dhp);
   if (g->batch < 1 || g->depth < 1 || g->rows < 1 || g->cols < 1 || g->rows_global < g->rows)
     return set_error("wm3_block: bad geometry");
-  if (w->w_qkv_f != nullptr && (ws->stats == nullptr || w->c_qkv == nullptr || w->d_qkv == nullptr ||
+  if (w->w_qkv_f != nullptr && (ws->stats == nullptr || ws->row_stats == nullptr || w->c_qkv == nullptr || w->d_qkv == nullptr ||
                                 w->w_1_f == nullptr || w->c_1 == nullptr || w->d_1 == nullptr || ln_parts(w) > WM3_LN_SLOTS))
     return set_error("wm3_block: folded LayerNorm needs w_1_f, c_*, d_* and ws stats (hidden <= %d)",
                      WM3_LN_SLOTS / 2 * 256);
   return 0;
 }
 
-static wm3_ln_fold_t fold_consumer(const wm3_block_weights_t* w, const wm3_block_ws_t* ws, const float* c) {
+static wm3_ln_fold_t fold_consumer(const wm3_block_ws_t* ws, const float* c) {
   wm3_ln_fold_t f{};
-  f.stats_in = ws->stats;
-  f.stats_parts = ln_parts(w);
-  f.ln_n = w->hidden;
-  f.eps = 1e-6f;
+  f.row_stats = ws->row_stats;
   f.fold_c = c;
   return f;
 }
@@ -67,9 +64,9 @@ extern "C" int wm3_block_qkv(const float* x, const wm3_block_weights_t* w, const
   const int qkv_n = 3 * w->heads * w->dhp;
   const int plane = g->rows * g->cols;
   if (w->w_qkv_f != nullptr) {
-    if (!g->x_prepped && wm3_ln_fold_prep(x, w->hidden, t, w->hidden, ws->hn, w->kp, ws->stats, ln_parts(w), stream))
+    if (!g->x_prepped && wm3_ln_fold_prep(x, w->hidden, t, w->hidden, ws->hn, w->kp, 1e-6f, ws->row_stats, stream))
       return -1;
-    const wm3_ln_fold_t f = fold_consumer(w, ws, w->c_qkv);
+    const wm3_ln_fold_t f = fold_consumer(ws, w->c_qkv);
     return wm3_linear_fold(ws->hn, w->kp, w->w_qkv_f, w->kp, t, qkv_n, w->kp, WM3_EPI_QKV_ROPE, ws->qkv, qkv_n, qkv_n,
                            w->d_qkv, rope, g->batch * g->depth, plane, static_cast<long long>(rows_ext) * g->cols,
                            g->halo_lo * g->cols, halo, &f, stream);
@@ -94,16 +91,19 @@ extern "C" int wm3_block_rest(float* x, const wm3_block_weights_t* w, const wm3_
                      1.0f / std::sqrt(static_cast<float>(w->dh)), stream))
     return -1;
   if (w->w_qkv_f != nullptr) {
-    const wm3_ln_fold_t prod = fold_producer(w, ws), cons = fold_consumer(w, ws, w->c_1);
+    const wm3_ln_fold_t prod = fold_producer(w, ws), cons = fold_consumer(ws, w->c_1);
     if (wm3_linear_fold(ws->ctx, hd, w->w_o, hd, t, w->np, hd, WM3_EPI_BIAS_RESID_F32, x, w->hidden, w->hidden,
                         w->b_o, nullptr, 1, t, t, 0, nullptr, &prod, stream))
       return -1;
+    if (wm3_ln_fold_finalize(ws->stats, ln_parts(w), w->hidden, 1e-6f, t, ws->row_stats, stream)) return -1;
     if (wm3_linear_fold(ws->hn, w->kp, w->w_1_f, w->kp, t, w->nm, w->kp, WM3_EPI_BIAS_GELU_BF16, ws->mid, w->nm,
                         w->nm, w->d_1, nullptr, 1, t, t, 0, nullptr, &cons, stream))
       return -1;
-    // W2 leaves xh / stats of the block's output for the next block's QKV GEMM
-    return wm3_linear_fold(ws->mid, w->nm, w->w_2, w->nm, t, w->np, w->nm, WM3_EPI_BIAS_RESID_F32, x, w->hidden,
-                           w->hidden, w->b_2, nullptr, 1, t, t, 0, nullptr, &prod, stream);
+    // W2 leaves xh / row statistics of the block's output for the next block's QKV GEMM
+    if (wm3_linear_fold(ws->mid, w->nm, w->w_2, w->nm, t, w->np, w->nm, WM3_EPI_BIAS_RESID_F32, x, w->hidden,
+                        w->hidden, w->b_2, nullptr, 1, t, t, 0, nullptr, &prod, stream))
+      return -1;
+    return wm3_ln_fold_finalize(ws->stats, ln_parts(w), w->hidden, 1e-6f, t, ws->row_stats, stream);
   }
   if (wm3_linear(ws->ctx, hd, w->w_o, hd, t, w->np, hd, WM3_EPI_BIAS_RESID_F32, x, w->hidden, w->hidden, w->b_o,
                  nullptr, stream))

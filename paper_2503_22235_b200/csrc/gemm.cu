@@ -339,38 +339,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int sbuf = 0;
     const uint32_t tempty_leader0 = (CG == 2) ? mapa_shared(tempty_bar(0), 0) : 0u;
     int tile_it = 0;
-    // LayerNorm fold, consumer side: the row's (mean, rstd) from the producer's partial sums.  The partials of
-    // the next tile's row are loaded while this tile is processed (prefetch, up to 8 pairs in 4 float4), so
-    // their latency never sits between the accumulator and the epilogue.
+    // LayerNorm fold, consumer side: the row's (rstd, rstd * mean), loaded one tile ahead so its latency never
+    // sits between the accumulator and the epilogue.
     constexpr bool kCons = (EPI != WM3_EPI_BIAS_RESID_F32 && EPI != WM3_EPI_F32);
     const bool cons = kCons && ep.ln_cons;
-    const bool cons_pf = cons && ep.fold.stats_parts <= 8;
-    float4 pf[4];
-    auto stats_issue = [&](int t) {
+    auto stats_load = [&](int t) {
       int pl, rr;
       const int rw = (t < ntiles) ? tile_rows(t, pl, rr) + r_in_tile : 0;
-      const float4* sp = reinterpret_cast<const float4*>(ep.fold.stats_in +
-                                                         static_cast<size_t>(rw < M ? rw : 0) * (2 * WM3_LN_SLOTS));
-#pragma unroll
-      for (int i = 0; i < 4; ++i) pf[i] = (2 * i < ep.fold.stats_parts) ? __ldg(sp + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      return __ldg(reinterpret_cast<const float2*>(ep.fold.row_stats) + (rw < M ? rw : 0));
     };
-    auto stats_finish = [&](float& rstd, float& rmu) {
-      float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        s1 += pf[i].x + pf[i].z;
-        s2 += pf[i].y + pf[i].w;
-      }
-      const float inv_n = 1.f / static_cast<float>(ep.fold.ln_n);
-      const float mu = s1 * inv_n;
-      rstd = rsqrtf(fmaxf(fmaf(-mu, mu, s2 * inv_n), 0.f) + ep.fold.eps);
-      rmu = rstd * mu;
-    };
-    float ln_rstd_next = 0.f, ln_rmu_next = 0.f;
-    if (cons_pf) {
-      stats_issue(tile0);
-      stats_finish(ln_rstd_next, ln_rmu_next);
-    }
+    float2 ln_next = cons ? stats_load(tile0) : make_float2(0.f, 0.f);
     for (int tile = tile0; tile < ntiles; tile += tstep, ++tile_it) {
       int plane, r0;
       const int m0 = tile_rows(tile, plane, r0);
@@ -378,21 +356,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int row = m0 + r_in_tile;
       const int prow = r0 + r_in_tile;  // row within the plane
       const bool row_ok = (prow < ep.plane_rows) && row < M;
-      float ln_rstd = ln_rstd_next, ln_rmu = ln_rmu_next;
-      if (cons_pf) {
-        stats_issue(tile + tstep);  // consumed after this tile's units
-      } else if (cons) {
-        const float* sp = ep.fold.stats_in + static_cast<size_t>(row < M ? row : 0) * (2 * WM3_LN_SLOTS);
-        float s1 = 0.f, s2 = 0.f;
-        for (int p = 0; p < ep.fold.stats_parts; ++p) {
-          s1 += sp[2 * p];
-          s2 += sp[2 * p + 1];
-        }
-        const float inv_n = 1.f / static_cast<float>(ep.fold.ln_n);
-        const float mu = s1 * inv_n;
-        ln_rstd = rsqrtf(fmaxf(fmaf(-mu, mu, s2 * inv_n), 0.f) + ep.fold.eps);
-        ln_rmu = ln_rstd * mu;
-      }
+      const float ln_rstd = ln_next.x, ln_rmu = ln_next.y;
+      if (cons) ln_next = stats_load(tile + tstep);  // consumed by the next tile
       // LayerNorm fold, producer side: partial (sum, sum of squares) of this group's columns of the row
       float ln_s1 = 0.f, ln_s2 = 0.f;
       // residual prefetch, RESID_DEPTH chunks of this group ahead: the first ones overlap the mainloop wait
@@ -577,7 +542,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         if (Cfg::STAGING_PER_GROUP > 1) sbuf ^= 1;
       }
-      if (cons_pf) stats_finish(ln_rstd_next, ln_rmu_next);
       if (EPI == WM3_EPI_BIAS_RESID_F32 && ep.ln_prod && row_ok) {
         float* so = ep.fold.stats_out + static_cast<size_t>(row) * (2 * WM3_LN_SLOTS) + 2 * ((tile % nn) * 2 + g);
         *reinterpret_cast<float2*>(so) = make_float2(ln_s1, ln_s2);
@@ -719,17 +683,15 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
   if (fold != nullptr) {
     ep.fold = *fold;
     ep.ln_prod = fold->xh_out != nullptr || fold->stats_out != nullptr;
-    ep.ln_cons = fold->stats_in != nullptr;
+    ep.ln_cons = fold->row_stats != nullptr;
     const int ntile_n = (n + bn - 1) / bn;
     if (ep.ln_prod && (epi != WM3_EPI_BIAS_RESID_F32 || fold->xh_out == nullptr || fold->stats_out == nullptr ||
                        (fold->ld_xh % 16) || fold->ld_xh < n_valid || (reinterpret_cast<uintptr_t>(fold->xh_out) % 32) ||
                        2 * ntile_n > WM3_LN_SLOTS || (n_valid % 2)))
       return set_error("wm3_linear: bad LayerNorm-fold producer (residual epilogue, xh and stats, ld_xh %% 16, "
                        "<= %d column tiles)", WM3_LN_SLOTS / 2);
-    if (ep.ln_cons && (epi == WM3_EPI_BIAS_RESID_F32 || epi == WM3_EPI_F32 || fold->fold_c == nullptr ||
-                       fold->stats_parts < 1 || fold->stats_parts > WM3_LN_SLOTS || fold->ln_n < 1))
-      return set_error("wm3_linear: bad LayerNorm-fold consumer (bf16 epilogue, fold_c, 1..%d stats parts)",
-                       WM3_LN_SLOTS);
+    if (ep.ln_cons && (epi == WM3_EPI_BIAS_RESID_F32 || epi == WM3_EPI_F32 || fold->fold_c == nullptr))
+      return set_error("wm3_linear: bad LayerNorm-fold consumer (16-bit epilogue and fold_c required)");
   }
   if (epi == WM3_EPI_QKV_ROPE) {
     if (rope == nullptr) return set_error("wm3_linear: rope descriptor required");

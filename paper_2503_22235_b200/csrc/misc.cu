@@ -91,11 +91,39 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int ldx, int m, in
   for (int c = n + lane; c < ldo; c += 32) orow[c] = to_elem(0.f);
 }
 
+DEVI float2 ln_row_stats(float s1, float s2, int n, float eps) {
+  const float inv_n = 1.f / static_cast<float>(n);
+  const float mu = s1 * inv_n;
+  const float rstd = rsqrtf(fmaxf(fmaf(-mu, mu, s2 * inv_n), 0.f) + eps);
+  return make_float2(rstd, rstd * mu);
+}
+
+// Producer partials -> (rstd, rstd * mean) per row (include/wm3.h wm3_ln_fold_finalize); one thread per row.
+__global__ void ln_fold_finalize_kernel(const float* __restrict__ stats, int parts, int n, float eps, int m,
+                                        float2* __restrict__ row_stats) {
+  griddep_launch_dependents();
+  griddep_wait();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  const float4* sp = reinterpret_cast<const float4*>(stats + static_cast<size_t>(r) * (2 * WM3_LN_SLOTS));
+  float s1 = 0.f, s2 = 0.f;
+  for (int i = 0; i < (parts + 1) / 2; ++i) {
+    const float4 v = __ldg(sp + i);
+    s1 += v.x;
+    s2 += v.y;
+    if (2 * i + 1 < parts) {
+      s1 += v.z;
+      s2 += v.w;
+    }
+  }
+  row_stats[r] = ln_row_stats(s1, s2, n, eps);
+}
+
 // Start of a LayerNorm-folded chain (include/wm3.h wm3_ln_fold_prep): one warp per row writes the fp16 copy of
-// the row (pad columns zero) and the row's (sum, sum of squares) as partial pair 0 of the consumer's stats.
+// the row (pad columns zero) and the row's (rstd, rstd * mean).
 template <int NV>
 __global__ void ln_fold_prep_kernel(const float* __restrict__ x, int ldx, int m, int n, elem_t* __restrict__ xh,
-                                    int ld_xh, float* __restrict__ stats, int parts) {
+                                    int ld_xh, float eps, float2* __restrict__ row_stats) {
   griddep_launch_dependents();
   griddep_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -132,28 +160,36 @@ __global__ void ln_fold_prep_kernel(const float* __restrict__ x, int ldx, int m,
     s2 += __shfl_xor_sync(0xffffffffu, s2, o);
   }
   for (int c = n + lane; c < ld_xh; c += 32) orow[c] = to_elem(0.f);
-  float* sr = stats + static_cast<size_t>(warp) * (2 * WM3_LN_SLOTS);
-  for (int p = lane; p < parts; p += 32) {
-    sr[2 * p] = p == 0 ? s1 : 0.f;
-    sr[2 * p + 1] = p == 0 ? s2 : 0.f;
-  }
+  if (lane == 0) row_stats[warp] = ln_row_stats(s1, s2, n, eps);
 }
 
 }  // namespace wm3
 
 using namespace wm3;
 
-extern "C" int wm3_ln_fold_prep(const float* x, int ldx, int m, int n, void* xh, int ld_xh, float* stats, int parts,
-                                void* stream) {
+extern "C" int wm3_ln_fold_finalize(const float* stats, int parts, int n, float eps, int m, float* row_stats,
+                                    void* stream) {
   if (m <= 0) return 0;
-  if (n <= 0 || ld_xh < n || ldx < n || parts < 1 || parts > WM3_LN_SLOTS)
-    return set_error("wm3_ln_fold_prep: bad sizes (n %d ld_xh %d parts %d)", n, ld_xh, parts);
+  if (n <= 0 || parts < 1 || parts > WM3_LN_SLOTS) return set_error("wm3_ln_fold_finalize: bad sizes");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (launch_pdl(ln_fold_finalize_kernel, dim3((m + 255) / 256), dim3(256), 0, s, stats, parts, n, eps, m,
+                 reinterpret_cast<float2*>(row_stats)))
+    return -1;
+  return check_launch("ln_fold_finalize_kernel");
+}
+
+extern "C" int wm3_ln_fold_prep(const float* x, int ldx, int m, int n, void* xh, int ld_xh, float eps,
+                                float* row_stats, void* stream) {
+  if (m <= 0) return 0;
+  if (n <= 0 || ld_xh < n || ldx < n) return set_error("wm3_ln_fold_prep: bad sizes (n %d ld_xh %d)", n, ld_xh);
   const int threads = 256;
   const int blocks = (m * 32 + threads - 1) / threads;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   auto* o = reinterpret_cast<elem_t*>(xh);
   auto kern = (n <= 256) ? ln_fold_prep_kernel<2> : (n <= 1024) ? ln_fold_prep_kernel<8> : ln_fold_prep_kernel<16>;
-  if (launch_pdl(kern, dim3(blocks), dim3(threads), 0, s, x, ldx, m, n, o, ld_xh, stats, parts)) return -1;
+  if (launch_pdl(kern, dim3(blocks), dim3(threads), 0, s, x, ldx, m, n, o, ld_xh, eps,
+                 reinterpret_cast<float2*>(row_stats)))
+    return -1;
   return check_launch("ln_fold_prep_kernel");
 }
 

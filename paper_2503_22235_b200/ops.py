@@ -56,26 +56,31 @@ def layernorm_bf16(x: torch.Tensor, gain: torch.Tensor, bias: torch.Tensor, ldo:
     return out
 
 
-def ln_fold_consumer(stats: torch.Tensor, parts: int, ln_n: int, fold_c: torch.Tensor,
-                     eps: float = 1e-6) -> "_lib.LnFoldT":
-    """wm3_ln_fold_t for a GEMM that applies the folded LayerNorm (reads the row statistics)."""
-    _req(stats, torch.float32, "stats")
-    return _lib.LnFoldT(None, 0, None, stats.data_ptr(), int(parts), int(ln_n), float(eps), fold_c.data_ptr())
+def ln_fold_consumer(row_stats: torch.Tensor, fold_c: torch.Tensor) -> "_lib.LnFoldT":
+    """wm3_ln_fold_t for a GEMM that applies the folded LayerNorm (reads (rstd, rstd * mean) per row)."""
+    _req(row_stats, torch.float32, "row_stats")
+    return _lib.LnFoldT(None, 0, None, row_stats.data_ptr(), fold_c.data_ptr())
 
 
 def ln_fold_producer(xh: torch.Tensor, stats: torch.Tensor) -> "_lib.LnFoldT":
     """wm3_ln_fold_t for a residual GEMM that also writes the fp16 copy of x and its row statistics."""
     _req(xh, _lib.ELEM, "xh")
     _req(stats, torch.float32, "stats")
-    return _lib.LnFoldT(xh.data_ptr(), xh.stride(0), stats.data_ptr(), None, 0, 0, 0.0, None)
+    return _lib.LnFoldT(xh.data_ptr(), xh.stride(0), stats.data_ptr(), None, None)
 
 
-def ln_fold_prep(x: torch.Tensor, n: int, xh: torch.Tensor, stats: torch.Tensor, parts: int) -> None:
-    """Start of a folded chain: xh = fp16(x) (pad columns zero), stats pair 0 = row (sum, sum of squares)."""
+def ln_fold_prep(x: torch.Tensor, n: int, xh: torch.Tensor, row_stats: torch.Tensor, eps: float = 1e-6) -> None:
+    """Start of a folded chain: xh = fp16(x) (pad columns zero) and x's (rstd, rstd * mean) per row."""
     _req(x, torch.float32, "x")
     _req(xh, _lib.ELEM, "xh")
-    check(_lib.lib().wm3_ln_fold_prep(ptr(x), x.stride(0), x.shape[0], int(n), ptr(xh), xh.stride(0), ptr(stats),
-                                      int(parts), stream_ptr()), "wm3_ln_fold_prep")
+    check(_lib.lib().wm3_ln_fold_prep(ptr(x), x.stride(0), x.shape[0], int(n), ptr(xh), xh.stride(0), float(eps),
+                                      ptr(row_stats), stream_ptr()), "wm3_ln_fold_prep")
+
+
+def ln_fold_finalize(stats: torch.Tensor, parts: int, n: int, row_stats: torch.Tensor, eps: float = 1e-6) -> None:
+    """Producer partial sums -> (rstd, rstd * mean) per row."""
+    check(_lib.lib().wm3_ln_fold_finalize(ptr(stats), int(parts), int(n), float(eps), stats.shape[0],
+                                          ptr(row_stats), stream_ptr()), "wm3_ln_fold_finalize")
 
 
 def linear(a: torch.Tensor, w: torch.Tensor, epi: int, bias: torch.Tensor | None = None,

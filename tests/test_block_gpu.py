@@ -169,6 +169,10 @@ def test_folded_layernorm_matches_separate_launches(offset, monkeypatch):
             st = ws.stats.view(t, -1, 2).cpu().numpy()[:, :bw.ln_parts].sum(1)
             np.testing.assert_allclose(st[:, 0], xo.sum(1), rtol=1e-4, atol=1e-2)
             np.testing.assert_allclose(st[:, 1], (xo * xo).sum(1), rtol=1e-4)
+            rs = ws.row_stats.cpu().numpy()
+            rstd = 1.0 / np.sqrt(xo.var(1) + 1e-6)
+            np.testing.assert_allclose(rs[:, 0], rstd, rtol=2e-3)
+            np.testing.assert_allclose(rs[:, 1], rstd * xo.mean(1), rtol=2e-3, atol=1e-4)
         outs[fold] = xo
     want = om.natten_block(x, params, "blk", ext, win, heads, chunk=128)
     assert _rel(outs["1"] - x, outs["0"] - x) < 5e-3

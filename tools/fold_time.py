@@ -33,11 +33,12 @@ out3 = torch.empty(T, 3 * D, device="cuda", dtype=E)
 out4 = torch.empty(T, 4 * D, device="cuda", dtype=E)
 xh = torch.zeros(T, D, device="cuda", dtype=E)
 stats = torch.zeros(T, 2 * L.LN_SLOTS, device="cuda")
-ops.ln_fold_prep(x, D, xh, stats, 8)
+rows = torch.zeros(T, 2, device="cuda")
+ops.ln_fold_prep(x, D, xh, rows)
 rs = RopeTables((5, 90, 180), 128).struct((5, 90, 180), 0, 8, 128)
 c3, c4 = torch.ones(3 * D, device="cuda"), torch.ones(4 * D, device="cuda")
-cons3 = ops.ln_fold_consumer(stats, 8, D, c3)
-cons4 = ops.ln_fold_consumer(stats, 8, D, c4)
+cons3 = ops.ln_fold_consumer(rows, c3)
+cons4 = ops.ln_fold_consumer(rows, c4)
 prod = ops.ln_fold_producer(xh, stats)
 res = {
     "qkv rope": t(lambda: ops.linear(hn, wqkv, L.WM3_EPI_QKV_ROPE, bias=b3, out=out3, rope=rs)),
@@ -49,7 +50,8 @@ res = {
     "w2 resid": t(lambda: ops.linear(mid, w2, L.WM3_EPI_BIAS_RESID_F32, bias=b1, out=x)),
     "w2 resid prod": t(lambda: ops.linear(mid, w2, L.WM3_EPI_BIAS_RESID_F32, bias=b1, out=x, fold=prod)),
     "ln": t(lambda: ops.layernorm_bf16(x, b1 + 1, b1, out=xh)),
-    "ln prep": t(lambda: ops.ln_fold_prep(x, D, xh, stats, 8)),
+    "ln prep": t(lambda: ops.ln_fold_prep(x, D, xh, rows)),
+    "ln finalize": t(lambda: ops.ln_fold_finalize(stats, 8, D, rows)),
 }
 for k, v in res.items():
     print(f"{k:16s} {v:.4f} ms")
