@@ -559,6 +559,18 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
   p.halo_lo = halo_lo; p.rows_ext = rows + halo_lo + halo_hi;
   p.heads = heads; p.dhp = dhp; p.wd = wd; p.wh = wh; p.ww = ww;
   choose_tile(depth, rows, cols, rows_global, wd, wh, ww, &p.TD, &p.TH, &p.TW, &p.ncp, &p.nrpc);
+  if (const char* e = getenv("WM3_NA_TILE")) {  // A/B aid: "TD,TH,TW" (key box derived as in choose_tile)
+    int td, th, tw;
+    if (sscanf(e, "%d,%d,%d", &td, &th, &tw) == 3 && td >= 1 && th >= 1 && tw >= 1 && td <= depth && th <= rows &&
+        tw <= cols && td * th * tw <= 128) {
+      const int ncp = (tw + ww - 1 >= cols) ? cols : tw + ww - 1;
+      const int nr_u = (th + wh - 1 < rows_global) ? th + wh - 1 : rows_global;
+      if (ncp <= 128) {
+        p.TD = td; p.TH = th; p.TW = tw; p.ncp = ncp;
+        p.nrpc = (nr_u < 128 / ncp) ? nr_u : 128 / ncp;
+      }
+    }
+  }
   p.ntd = (depth + p.TD - 1) / p.TD;
   p.nth = (rows + p.TH - 1) / p.TH;
   p.ntw = (cols + p.TW - 1) / p.TW;
