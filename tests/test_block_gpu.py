@@ -178,3 +178,27 @@ def test_folded_layernorm_matches_separate_launches(offset, monkeypatch):
     assert _rel(outs["1"] - x, outs["0"] - x) < 5e-3
     assert _rel(outs["1"] - x, want - x) < 3e-2
     assert _rel(outs["1"], want) < 1e-2
+
+
+@pytest.mark.parametrize("ext,win", [((7, 9, 18), (5, 7, 7)), ((4, 6, 10), (2, 4, 4))])
+def test_locality_bitwise(ext, win):
+    """Reference test_attention.py test_locality_radius, made exact: perturbing one token changes a block's
+    output only at the tokens whose (bumped / wrapped) window contains it, and the rest of the output is bitwise
+    unchanged (every per-token op is row-local, and the attention kernel's masks exclude everything else)."""
+    from oracle.grid import neighborhood
+    dim, heads = 256, 2
+    t = int(np.prod(ext))
+    params = _params(dim, heads, seed=11)
+    x = np.random.default_rng(3).standard_normal((t, dim))
+    base = _api().natten_block(x, params, "blk", ext, win, heads).values
+    table = neighborhood(ext, win)
+    for p in (0, t // 2 + 3, t - 1):
+        xp = x.copy()
+        xp[p] += np.random.default_rng(p).standard_normal(dim)  # not a constant shift: LayerNorm would remove it
+        out = _api().natten_block(xp, params, "blk", ext, win, heads).values
+        affected = np.zeros(t, dtype=bool)
+        affected[np.any(table == p, axis=1)] = True
+        affected[p] = True
+        changed = np.any(out != base, axis=1)
+        assert not np.any(changed & ~affected), np.nonzero(changed & ~affected)[0][:10]
+        assert changed[affected].mean() > 0.9
