@@ -8,9 +8,9 @@ rows of the neighbouring bands that its bumped windows reach: `halo` rows above 
 global row indices, so a band computes exactly the rows of the global block.
 
 Halo exchange after the QKV GEMM: rank r sends its first `halo_hi[r-1]` band rows to r-1 and its last
-`halo_lo[r+1]` rows to r+1, per depth plane, via torch.distributed point-to-point (NCCL over NVLink on B200,
-gloo in the CPU tests).  Only the exchanged rows cross the link: 3 x 180 tokens x 6 KB x 5 planes ~= 16.6 MB
-per neighbour per block at full scale.
+`halo_lo[r+1]` rows to r+1 (those rows of every depth plane packed into one message per neighbour) via
+torch.distributed point-to-point (NCCL over NVLink on B200, gloo in the CPU tests).  Only the exchanged rows
+cross the link: 3 x 180 tokens x 6 KB x 5 planes ~= 16.6 MB per neighbour per block at full scale.
 """
 
 from __future__ import annotations
@@ -83,8 +83,10 @@ class HaloExchanger:
         me = self.me
         planes = getattr(grid, "planes", grid.depth)  # batch * depth for an ensemble batch
         g = buf.view(planes, grid.rows_ext, grid.cols, -1)
-        # gloo moves host memory only: CUDA rows are staged through the host (the multi-process smoke runs of
-        # the N > 1 bench path on one device); NCCL sends / receives the device rows directly
+        # One message per neighbour and direction: the halo rows of every depth plane are packed into one
+        # contiguous buffer (a strided copy) instead of one send per plane, so a block costs at most two sends
+        # and two receives.  gloo moves host memory only: CUDA rows are staged through the host (multi-process
+        # smoke runs of the N > 1 bench path on one device); NCCL sends / receives device buffers.
         stage = buf.is_cuda and dist.get_backend(self.group) == "gloo"
         ops, post = [], []
 
@@ -92,32 +94,28 @@ class HaloExchanger:
             ops.append(dist.P2POp(dist.isend, rows.cpu() if stage else rows.contiguous(), peer, self.group))
 
         def recv(rows, peer):
-            if stage:
-                tmp = torch.empty(rows.shape, dtype=rows.dtype)
-                post.append((rows, tmp))
-                rows = tmp
-            ops.append(dist.P2POp(dist.irecv, rows, peer, self.group))
+            tmp = torch.empty(rows.shape, dtype=rows.dtype, device="cpu" if stage else rows.device)
+            post.append((rows, tmp))
+            ops.append(dist.P2POp(dist.irecv, tmp, peer, self.group))
 
         lo0 = me.halo_lo  # buffer row of band row 0
         if me.rank > 0:
             up = self.bands[me.rank - 1]
-            for d in range(planes):
-                if up.halo_hi:  # my first rows -> upper neighbour's bottom halo
-                    send(g[d, lo0:lo0 + up.halo_hi], me.rank - 1)
-                if me.halo_lo:
-                    recv(g[d, 0:me.halo_lo], me.rank - 1)
+            if up.halo_hi:  # my first rows -> upper neighbour's bottom halo
+                send(g[:, lo0:lo0 + up.halo_hi], me.rank - 1)
+            if me.halo_lo:
+                recv(g[:, 0:me.halo_lo], me.rank - 1)
         if me.rank + 1 < len(self.bands):
             dn = self.bands[me.rank + 1]
-            for d in range(planes):
-                if dn.halo_lo:  # my last rows -> lower neighbour's top halo
-                    send(g[d, lo0 + me.rows - dn.halo_lo:lo0 + me.rows], me.rank + 1)
-                if me.halo_hi:
-                    recv(g[d, lo0 + me.rows:lo0 + me.rows + me.halo_hi], me.rank + 1)
+            if dn.halo_lo:  # my last rows -> lower neighbour's top halo
+                send(g[:, lo0 + me.rows - dn.halo_lo:lo0 + me.rows], me.rank + 1)
+            if me.halo_hi:
+                recv(g[:, lo0 + me.rows:lo0 + me.rows + me.halo_hi], me.rank + 1)
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
         for rows, tmp in post:
-            rows.copy_(tmp)
+            rows.copy_(tmp, non_blocking=not stage)
 
 
 def local_band_tokens(x_global: torch.Tensor, extents, band: Band) -> torch.Tensor:
