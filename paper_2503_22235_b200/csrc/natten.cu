@@ -29,6 +29,27 @@
 
 namespace wm3 {
 
+// Event trace of one CTA (WM3_NA_TRACE builds only): (event, counter, clock) triples for a timeline of the
+// hand-off chain.  Events: 0/1 softmax sfull wait begin/end, 2 softmax P arrive, 3/4 MMA pfull wait
+// begin/end, 5/6 MMA vfull wait, 7/8 MMA kfull wait, 9 MMA issue done, 10/11 TMA empty wait, 12/13 ofull wait.
+#ifdef WM3_NA_TRACE
+constexpr int NA_TRACE_MAX = 1 << 16;
+__device__ long long g_na_trace[NA_TRACE_MAX][3];
+__device__ int g_na_trace_n;
+DEVI void na_ev(int e, int c) {
+  if (blockIdx.x != 0) return;
+  const int i = atomicAdd(&g_na_trace_n, 1);
+  if (i < NA_TRACE_MAX) {
+    g_na_trace[i][0] = e;
+    g_na_trace[i][1] = c;
+    g_na_trace[i][2] = clock64();
+  }
+}
+#define NA_EV(e, c) na_ev(e, c)
+#else
+#define NA_EV(e, c)
+#endif
+
 struct NaParams {
   elem_t* out;
   int ldo;
@@ -218,7 +239,9 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
         int kd, kr0, nr, origin, vlo, vhi;
         chunk_geo(g, p.cols, j, kd, kr0, nr, origin, vlo, vhi);
         const uint32_t full = is_v ? bar_vfull : bar_kfull;
+        NA_EV(10, c);
         mbar_wait(is_v ? bar_vempty : bar_kempty, (c & 1) ^ 1);
+        NA_EV(11, c);
         if (p.dbg & 8) {
           mbar_arrive(full);
           return;
@@ -285,17 +308,24 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
         for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
           const uint32_t ph = chunk_ctr & 1;
           const bool more = j + 1 < g.nchunks;
+          NA_EV(3, 2 * chunk_ctr);
           mbar_wait(bar_pfull(0), ph);
+          NA_EV(4, 2 * chunk_ctr);
           mbar_wait(bar_vfull, ph);
+          NA_EV(6, chunk_ctr);
           if (j == 0) mbar_wait(bar_oempty, (tile_ctr & 1) ^ 1);
           tc_fence_after();
           issue_pv(0, j == 0);
           if (more) {
+            NA_EV(7, chunk_ctr);
             mbar_wait(bar_kfull, ph ^ 1);
+            NA_EV(8, chunk_ctr);
             tc_fence_after();
             issue_s(0);
           }
+          NA_EV(3, 2 * chunk_ctr + 1);
           mbar_wait(bar_pfull(1), ph);
+          NA_EV(4, 2 * chunk_ctr + 1);
           tc_fence_after();
           issue_pv(1, false);
           umma_commit(bar_vempty);
@@ -368,7 +398,9 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
         for (int w = 0; w < MWN; ++w) mw[w] = dok ? (part == 0 ? mc0[w] : mc1[w]) : 0u;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
+          if (threadIdx.x == 0) NA_EV(0, 2 * chunk_ctr + h);
           mbar_wait(bar_sfull(h), chunk_ctr & 1);
+          if (threadIdx.x == 0) NA_EV(1, 2 * chunk_ctr + h);
           tc_fence_after();
           uint32_t pk[CW / 2];
           if (p.dbg & 1) {
@@ -448,6 +480,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(bar_pfull(h));
+          if (threadIdx.x == 0) NA_EV(2, 2 * chunk_ctr + h);
         }
       }
       // ---- epilogue: O / l -> ctx ----
@@ -460,7 +493,9 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
         l_run = lt;
       }
       const float inv_l = (qvalid && l_run > 0.f) ? 1.f / l_run : 0.f;
+      if (threadIdx.x == 0) NA_EV(12, tile_ctr);
       mbar_wait(bar_ofull, tile_ctr & 1);
+      if (threadIdx.x == 0) NA_EV(13, tile_ctr);
       tc_fence_after();
       const size_t tok = g.b * member_tokens + static_cast<size_t>((qd * p.rows + qh) * p.cols + qw);
       elem_t* orow = p.out + (qvalid ? tok * p.ldo + g.head * p.dhp : 0);
@@ -614,3 +649,16 @@ extern "C" int wm3_natten_windows(int depth, int rows, int cols, int rows_global
                                                                                     row0, wd, wh, ww, out);
   return check_launch("natten_windows_kernel");
 }
+
+#ifdef WM3_NA_TRACE
+extern "C" int wm3_na_trace(long long* out, int max_events) {
+  int n = 0;
+  cudaMemcpyFromSymbol(&n, wm3::g_na_trace_n, sizeof(int));
+  n = n < max_events ? n : max_events;
+  n = n < wm3::NA_TRACE_MAX ? n : wm3::NA_TRACE_MAX;
+  cudaMemcpyFromSymbol(out, wm3::g_na_trace, static_cast<size_t>(n) * 3 * sizeof(long long));
+  const int zero = 0;
+  cudaMemcpyToSymbol(wm3::g_na_trace_n, &zero, sizeof(int));
+  return n;
+}
+#endif
