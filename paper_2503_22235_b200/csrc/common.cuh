@@ -429,6 +429,13 @@ DEVI void ffma2(float& lo, float& hi, float alo, float ahi, float blo, float bhi
   hi = __uint_as_float(static_cast<uint32_t>(r >> 32));
 }
 
+DEVI void fadd2(float& lo, float& hi, float alo, float ahi, float blo, float bhi) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(alo, ahi)), "l"(f2_bits(blo, bhi)));
+  lo = __uint_as_float(static_cast<uint32_t>(r));
+  hi = __uint_as_float(static_cast<uint32_t>(r >> 32));
+}
+
 DEVI void ldg256(const float* p, float (&v)[8]) {
   asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])

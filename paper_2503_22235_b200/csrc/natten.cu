@@ -461,14 +461,18 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
               }
             }
             const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+            // packed fp32 pairs (FFMA2 / FADD2): scale-and-shift and row sums issue one instruction per two keys
             float lsa[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) lsa[i] = 0.f;
 #pragma unroll
             for (int k = 0; k < CW; k += 2) {
-              const float p0 = fast_exp2(fmaf(__uint_as_float(x[k]), p.scale_log2, -m_use));  // exp2(-inf) = 0
-              const float p1 = fast_exp2(fmaf(__uint_as_float(x[k + 1]), p.scale_log2, -m_use));
-              lsa[(k >> 1) & 7] += p0 + p1;
+              float e0, e1;  // exp2(-inf) = 0
+              ffma2(e0, e1, __uint_as_float(x[k]), __uint_as_float(x[k + 1]), p.scale_log2, p.scale_log2, -m_use,
+                    -m_use);
+              const float p0 = fast_exp2(e0), p1 = fast_exp2(e1);
+              const int a = (k >> 1) & 3;
+              fadd2(lsa[2 * a], lsa[2 * a + 1], lsa[2 * a], lsa[2 * a + 1], p0, p1);
               pk[k >> 1] = pack_elem(p0, p1);
             }
             l_run += ((lsa[0] + lsa[1]) + (lsa[2] + lsa[3])) + ((lsa[4] + lsa[5]) + (lsa[6] + lsa[7]));
