@@ -140,6 +140,12 @@ DEVI void tma_store_4d(const CUtensorMap* m, uint32_t src, int c0, int c1, int c
                "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                : "memory");
 }
+// plain (non-tensor) bulk copy global -> shared, completing `bytes` on an mbarrier
+DEVI void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
 DEVI void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 DEVI void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
@@ -460,6 +466,9 @@ DEVI float fast_exp2(float x) {
 }
 
 // SWIZZLE_128B byte offset of 16-byte chunk `c` (0..7) in row `r` of a tile with 128-byte rows.
+DEVI void ld_shared_v4u(uint32_t addr, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(addr));
+}
 DEVI void ld_shared_v4(uint32_t addr, float& a, float& b, float& c, float& d) {
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(addr));
 }

@@ -21,6 +21,9 @@
 //               end of a tile O / l -> ctx rows.
 // The logits never leave the SM.  Output ctx rows are bf16 [T][heads][dhp] = the O-proj GEMM operand.
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "common.cuh"
 #include "launch.h"
@@ -59,6 +62,8 @@ struct NaParams {
   int TD, TH, TW, ntd, nth, ntw, nitems;
   int ncp, nrpc;  // key-chunk box: ncp columns x nrpc rows (fixed for every tile)
   float scale_log2;
+  const uint8_t* bias_table;  // BIAS: [tile][maxch] B_x images (4 KB each), built once per geometry
+  int maxch;
   int dbg;  // profiling switch (WM3_NA_DEBUG, bit flags): 1 skip softmax arithmetic, 2 skip Q K^T, 4 skip P V, 8 skip K/V loads
 };
 
@@ -76,8 +81,17 @@ constexpr int NA_THREADS = 32 * (NA_SOFTMAX_WARPS + 2);
 constexpr int NA_CTAS_PER_SM = 2;
 constexpr uint32_t NA_TILE = 32768;  // 128 rows x 256 B
 // smem: Q | K | V | barriers (256 B) | row-max / row-sum exchange (2 halves + 1) x NA_SPLIT x 128 floats
-constexpr uint32_t NA_SMEM_BODY = 3 * NA_TILE;
-constexpr uint32_t NA_RED_BYTES = 3 * NA_SPLIT * 128 * 4;
+// Window mask as one extra K = 16 step of Q K^T (kernel template BIAS): A_x = one-hot query classes (tile
+// depth / row / column position, 128 x 16, built once per CTA), B_x = the chunk's key bias (0, or NA_MASKED
+// where a class's window misses the key), fp16 in the no-swizzle K-major core-matrix layout (4 KB each).  The
+// B_x images of every (tile, chunk) are precomputed once per geometry (natten_bias_table_kernel) and loaded
+// with the chunk's K by one bulk copy.  The softmax then needs no per-element mask: a masked logit is ~-3e4
+// and never wins the row max; a query whose first key half is entirely masked accumulates garbage that the
+// lazy rescale multiplies by exp2(-huge) = 0 as soon as its first real key arrives.
+constexpr uint32_t NA_XTRA = 8192;  // A_x and the B_x slot (loaded with K, same lifetime)
+constexpr float NA_MASKED = -30000.f;
+constexpr uint32_t NA_SMEM_BODY = 3 * NA_TILE + NA_XTRA;
+constexpr uint32_t NA_RED_BYTES = NA_SPLIT > 1 ? 3 * NA_SPLIT * 128 * 4 : 0;  // (2 CTAs per SM must fit)
 constexpr uint32_t NA_SMEM = NA_SMEM_BODY + 1024 /*align*/ + 256 /*barriers*/ + NA_RED_BYTES;
 // TMEM columns (256 per CTA): S / P [0, 128), O [128, 256).  S(c + 1) may overwrite P(c) without a wait
 // because tcgen05.mma ops of one thread execute in issue order and S(c + 1) is issued after P V(c).
@@ -173,12 +187,72 @@ DEVI void window_mask(uint32_t (&m)[4], int nr, int ncp, int rlo, int rhi, int s
   }
 }
 
+// smem descriptor of a K-major operand in the no-swizzle core-matrix layout: core matrix (8 rows x 16 B) at
+// (row / 8) * 256 + (k / 8) * 128 (LBO = 128 B between K-adjacent cores, SBO = 256 B between row groups)
+DEVI uint64_t make_sdesc_interleave(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((128u >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((256u >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  return d;  // layout type 0: SWIZZLE_NONE
+}
+DEVI uint32_t xtra_off(int r, int kc) { return (r >> 3) * 256u + kc * 128u + (r & 7) * 16u; }
+
+// Row `k` of the B_x image of chunk j of tile g: per query class (tile depth td, row th, column tw) 0 if the
+// class's window (grid.py bump / wrap, the same formulas as window_mask) holds key k, else NA_MASKED; padding
+// keys are masked through their row classes.
+DEVI void bx_row(const NaParams& p, const TileGeo& g, int j, int k, uint32_t (&u)[8]) {
+  int kd, kr0, nr, origin, vlo, vhi;
+  chunk_geo(g, p.cols, j, kd, kr0, nr, origin, vlo, vhi);
+  const int rr = k / g.ncp, cc = k - rr * g.ncp;
+  const bool key_ok = rr < nr;
+  const int kr = kr0 + rr;
+  const int hw = (p.ww - 1) / 2;
+  const bool circle = (g.ncp == p.cols);
+  const uint32_t masked = __half_as_ushort(__float2half(NA_MASKED));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) u[i] = 0u;  // fp16 0 = open
+#pragma unroll
+  for (int cl = 0; cl < 16; ++cl) {
+    bool ok = true;
+    if (cl < p.TD) {
+      const int sd = bump_start(min(g.d0 + cl, p.depth - 1), p.depth, p.wd);
+      ok = kd >= sd && kd < sd + p.wd;
+    } else if (cl < p.TD + p.TH) {
+      const int sh = bump_start(min(g.h0 + cl - p.TD, p.rows - 1) + p.row0, p.rows_global, p.wh);
+      ok = key_ok && kr >= sh && kr < sh + p.wh;
+    } else if (cl < p.TD + p.TH + p.TW) {
+      const int qw = min(g.w0 + cl - p.TD - p.TH, p.cols - 1);
+      const int c_lo = circle ? wrap_col(qw - hw, p.cols) : qw - hw - g.pc0;
+      const int s2hi = circle ? c_lo + p.ww - g.ncp : 0;
+      ok = (cc >= max(c_lo, vlo) && cc < min(c_lo + p.ww, vhi)) || cc < s2hi;
+    }
+    if (!ok) u[cl >> 1] |= masked << (16 * (cl & 1));
+  }
+}
+
+// One block per (tile, chunk slot), one thread per key: the B_x images of every chunk of every tile, in the
+// no-swizzle core-matrix layout the MMA descriptor reads (copied into shared memory with one bulk copy).
+__global__ void natten_bias_table_kernel(NaParams p, uint8_t* table) {
+  const int tile = blockIdx.x / p.maxch, j = blockIdx.x % p.maxch;
+  const TileGeo g = tile_geo(p, tile);  // item = tile: head 0, member 0 (the geometry is head-independent)
+  if (j >= g.nchunks) return;
+  uint32_t u[8];
+  bx_row(p, g, j, threadIdx.x, u);
+  uint8_t* img = table + static_cast<size_t>(blockIdx.x) * 4096;
+  *reinterpret_cast<uint4*>(img + xtra_off(threadIdx.x, 0)) = make_uint4(u[0], u[1], u[2], u[3]);
+  *reinterpret_cast<uint4*>(img + xtra_off(threadIdx.x, 1)) = make_uint4(u[4], u[5], u[6], u[7]);
+}
+
+template <bool BIAS>
 __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
     natten_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, NaParams p) {
   griddep_launch_dependents();  // PDL: the next kernel may start its prologue
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sQ = smem_u32(smem), sK = sQ + NA_TILE, sV = sQ + 2 * NA_TILE;
+  const uint32_t sXA = sQ + 3 * NA_TILE, sXB = sXA + 4096;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NA_SMEM_BODY);
   const uint32_t b0 = smem_u32(bars);
   // Every barrier completes once per chunk (or tile) and its waiter always observes a phase before the
@@ -217,6 +291,19 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
   }
   // Zero the operand tiles once: rows past a box are never written by TMA and V rows feed P V (0 * NaN).
   for (uint32_t off = tid * 16u; off < NA_SMEM_BODY; off += NA_THREADS * 16u) st_shared_v4(sQ + off, 0, 0, 0, 0);
+  if (BIAS && tid < 128) {
+    __syncwarp();
+    // A_x row `tid`: ones at the query's tile depth / row / column class (td-major lanes)
+    uint32_t u[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    if (tid < p.TD * p.TH * p.TW) {
+      const uint32_t one = __half_as_ushort(__float2half(1.f));
+      const int c3[3] = {tid / (p.TH * p.TW), p.TD + (tid / p.TW) % p.TH, p.TD + p.TH + tid % p.TW};
+      for (int i = 0; i < 3; ++i) u[c3[i] >> 1] |= one << (16 * (c3[i] & 1));
+    }
+    st_shared_v4(sXA + xtra_off(tid, 0), u[0], u[1], u[2], u[3]);
+    st_shared_v4(sXA + xtra_off(tid, 1), u[4], u[5], u[6], u[7]);
+
+  }
   fence_proxy_async();
   tc_fence_before();
   __syncthreads();
@@ -235,7 +322,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
       const uint32_t qbytes = halves * 128u * p.TW * p.TH * p.TD;
       const uint32_t kbytes = halves * 128u * p.ncp * p.nrpc;
       int chunk_ctr = 0, tile_ctr = 0;
-      auto load_kv = [&](const TileGeo& g, int j, int c, bool is_v) {
+      auto load_kv = [&](const TileGeo& g, int item, int j, int c, bool is_v) {
         int kd, kr0, nr, origin, vlo, vhi;
         chunk_geo(g, p.cols, j, kd, kr0, nr, origin, vlo, vhi);
         const uint32_t full = is_v ? bar_vfull : bar_kfull;
@@ -246,12 +333,17 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
           mbar_arrive(full);
           return;
         }
-        mbar_arrive_expect_tx(full, kbytes);
+        const bool with_bx = BIAS && !is_v;  // the chunk's key-bias image rides with K (same slot lifetime)
+        mbar_arrive_expect_tx(full, kbytes + (with_bx ? 4096u : 0u));
         const int c1 = origin, c2 = kr0 - brow0;  // may be negative / past the edge: TMA zero-fills
         const uint32_t dst = is_v ? sV : sK;
         const int col = (is_v ? 2 : 1) * sec + g.head * p.dhp;
         for (int h = 0; h < halves; ++h)
           tma_load_4d(dst + h * 16384u, &tmKV, full, col + 64 * h, c1, c2, g.b * p.depth + kd);
+        if (with_bx) {
+          const int tile = item % (p.ntd * p.nth * p.ntw);
+          bulk_load(sXB, p.bias_table + (static_cast<size_t>(tile) * p.maxch + j) * 4096, 4096u, full);
+        }
       };
       for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
         const TileGeo g = tile_geo(p, item);
@@ -261,8 +353,8 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
           tma_load_4d(sQ + h * 16384u, &tmQ, bar_qfull, g.head * p.dhp + 64 * h, g.w0, g.h0 + p.halo_lo,
                       g.b * p.depth + g.d0);
         for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
-          load_kv(g, j, chunk_ctr, false);  // K frees after S(c - 1): streams in during softmax(c - 1)
-          load_kv(g, j, chunk_ctr, true);   // V frees after P V(c - 1)
+          load_kv(g, item, j, chunk_ctr, false);  // K frees after S(c - 1): streams in during softmax(c - 1)
+          load_kv(g, item, j, chunk_ctr, true);   // V frees after P V(c - 1)
         }
       }
     }
@@ -277,13 +369,16 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
       const uint32_t idesc_o = make_idesc(128, p.dhp, 0, 1);
       const int ksteps = p.dhp / 16;
       const uint32_t tO = tmem + NA_TMEM_O;
-      auto issue_s = [&](int h) {
+      auto issue_s = [&](int h, int c) {  // c: the chunk's running index (B_x buffer parity)
         // S_h = Q K_h^T: keys [64 h, 64 h + 64) are rows [64 h, +64) of the K tile (SW128 K-major)
         for (int s = 0; s < ((p.dbg & 2) ? 0 : ksteps); ++s) {
           const uint32_t off = (s >> 2) * 16384u + (s & 3) * 32u;
           umma_bf16_ss(tmem + 64 * h, make_sdesc_sw128(sQ + off, 16, 1024),
                        make_sdesc_sw128(sK + off + h * 8192u, 16, 1024), idesc_s, s > 0 ? 1u : 0u);
         }
+        if (BIAS)  // + window mask: one-hot query classes x key bias (keys 64 h ..)
+          umma_bf16_ss(tmem + 64 * h, make_sdesc_interleave(sXA),
+                       make_sdesc_interleave(sXB + h * 2048u), idesc_s, (p.dbg & 2) ? 0u : 1u);
         umma_commit(bar_sfull(h));
       };
       auto issue_pv = [&](int h, bool first) {
@@ -301,8 +396,8 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
         // prologue: both S halves of the tile's first chunk
         mbar_wait(bar_kfull, chunk_ctr & 1);
         tc_fence_after();
-        issue_s(0);
-        issue_s(1);
+        issue_s(0, chunk_ctr);
+        issue_s(1, chunk_ctr);
         umma_commit(bar_kempty);
         if (g.nchunks == 1) umma_commit(bar_qempty);
         for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
@@ -321,7 +416,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
             mbar_wait(bar_kfull, ph ^ 1);
             NA_EV(8, chunk_ctr);
             tc_fence_after();
-            issue_s(0);
+            issue_s(0, chunk_ctr + 1);
           }
           NA_EV(3, 2 * chunk_ctr + 1);
           mbar_wait(bar_pfull(1), ph);
@@ -331,7 +426,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
           umma_commit(bar_vempty);
           if (!more) umma_commit(bar_ofull);
           if (more) {
-            issue_s(1);
+            issue_s(1, chunk_ctr + 1);
             umma_commit(bar_kempty);
             if (j + 1 == g.nchunks - 1) umma_commit(bar_qempty);
           }
@@ -380,7 +475,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
         int kd, kr0, nr, origin, vlo, vhi;
         chunk_geo(g, p.cols, j, kd, kr0, nr, origin, vlo, vhi);
         const int part = j % g.nparts, key = (j / g.nparts) % g.nrchunks;
-        if ((part == 0 && key != key0) || (part == 1 && key != key1)) {
+        if (!BIAS && ((part == 0 && key != key0) || (part == 1 && key != key1))) {
           uint32_t m4[4];
           window_mask(m4, nr, g.ncp, max(0, q_sh - kr0), min(nr, q_sh + p.wh - kr0), max(c_lo, vlo),
                       min(c_lo + p.ww, vhi), s2hi);
@@ -395,7 +490,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
         const bool dok = qvalid && kd >= q_sd && kd < q_sd + p.wd;
         uint32_t mw[MWN];
 #pragma unroll
-        for (int w = 0; w < MWN; ++w) mw[w] = dok ? (part == 0 ? mc0[w] : mc1[w]) : 0u;
+        for (int w = 0; w < MWN; ++w) mw[w] = BIAS ? 0xffffffffu : (dok ? (part == 0 ? mc0[w] : mc1[w]) : 0u);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (threadIdx.x == 0) NA_EV(0, 2 * chunk_ctr + h);
@@ -631,13 +726,54 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
   if (make_tmap(&tkv, qkv, TMAP_BF16, 4, dims, strides, kvbox, nullptr)) return -1;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(natten_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, NA_SMEM);
-    if (e != cudaSuccess) return set_error("cudaFuncSetAttribute(natten): %s", cudaGetErrorString(e));
+    for (auto kern : {natten_fwd_kernel<true>, natten_fwd_kernel<false>}) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, NA_SMEM);
+      if (e != cudaSuccess) return set_error("cudaFuncSetAttribute(natten): %s", cudaGetErrorString(e));
+    }
     attr = true;
+  }
+  // window mask in the MMA when the tile's query classes fit the extra K = 16 step (WM3_NA_BIAS=0: softmax mask)
+  static const bool bias_env = [] {
+    const char* e = getenv("WM3_NA_BIAS");
+    return !(e && e[0] == '0');
+  }();
+  const bool bias = bias_env && p.TD + p.TH + p.TW <= 16;
+  if (bias) {
+    // B_x images of every (tile, chunk): built once per geometry on this stream, kept for the process (a few
+    // tens of MB at full scale, shared by every head, member, block and step)
+    const int ntiles = p.ntd * p.nth * p.ntw;
+    p.maxch = p.wd + p.TD - 1;  // depth planes of a tile's key patch ...
+    p.maxch = (p.maxch < depth ? p.maxch : depth) * ((p.wh + p.TH - 1 + p.nrpc - 1) / p.nrpc) * 2;  // x row chunks x parts
+    struct Key {
+      int dev, depth, rows, cols, rows_global, row0, wd, wh, ww, TD, TH, TW, ncp, nrpc;
+      bool operator<(const Key& o) const {
+        return std::tie(dev, depth, rows, cols, rows_global, row0, wd, wh, ww, TD, TH, TW, ncp, nrpc) <
+               std::tie(o.dev, o.depth, o.rows, o.cols, o.rows_global, o.row0, o.wd, o.wh, o.ww, o.TD, o.TH, o.TW,
+                        o.ncp, o.nrpc);
+      }
+    };
+    static std::map<Key, uint8_t*> tables;
+    static std::mutex mu;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const Key key{dev, depth, rows, cols, rows_global, row0, wd, wh, ww, p.TD, p.TH, p.TW, p.ncp, p.nrpc};
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = tables.find(key);
+    if (it == tables.end()) {
+      uint8_t* t = nullptr;
+      const size_t bytes = static_cast<size_t>(ntiles) * p.maxch * 4096;
+      if (cudaMalloc(&t, bytes) != cudaSuccess) return set_error("wm3_natten_fwd: bias table allocation failed");
+      cudaMemsetAsync(t, 0, bytes, reinterpret_cast<cudaStream_t>(stream));
+      natten_bias_table_kernel<<<ntiles * p.maxch, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p, t);
+      if (check_launch("natten_bias_table_kernel")) return -1;
+      it = tables.emplace(key, t).first;
+    }
+    p.bias_table = it->second;
   }
   const int slots = NA_CTAS_PER_SM * sm_count();
   const int grid = p.nitems < slots ? p.nitems : slots;
-  if (launch_pdl(natten_fwd_kernel, dim3(grid), dim3(NA_THREADS), NA_SMEM, reinterpret_cast<cudaStream_t>(stream), tq,
+  if (launch_pdl(bias ? natten_fwd_kernel<true> : natten_fwd_kernel<false>, dim3(grid), dim3(NA_THREADS), NA_SMEM,
+                 reinterpret_cast<cudaStream_t>(stream), tq,
                  tkv, p))
     return -1;
   return check_launch("natten_fwd_kernel");
