@@ -189,7 +189,8 @@ int wm3_block_fwd(float* x, const wm3_block_weights_t* w, const wm3_block_ws_t* 
  *      rows_global, plus halo rows received from the neighbouring bands.  Longitude wrap is handled inside
  *      the kernel (a wrapping key patch is fetched as two TMA boxes).
  * out: bf16 [batch * depth * rows * cols][ldo] (member-major, local token order), channels [heads][dhp].
- * scale = 1/sqrt(dh). */
+ * scale = 1/sqrt(dh).  The window mask is applied inside the QK^T MMA from key-bias images that the library
+ * builds once per device and geometry (on `stream`, at first use) and caches for the process. */
 int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, int batch, int depth, int rows, int cols,
                    int rows_global, int row0, int halo_lo, int halo_hi, int heads, int dhp, int wd,
                    int wh, int ww, float scale, void* stream);
