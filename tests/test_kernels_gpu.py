@@ -191,3 +191,22 @@ def test_residual_gemm_bitwise_repeatable():
             assert torch.equal(y, ref), (k, n)
         want = xs + (a.float() @ w.float().T) + b[:n]
         assert ((ref - want).norm() / want.norm()).item() < 1e-3
+
+
+@pytest.mark.parametrize("tile", ["5,5,5", "1,2,40", "3,6,7", "1,1,64"])
+def test_natten_both_mask_paths_match_reference(tile, monkeypatch):
+    """The attention window mask runs inside the QK^T MMA (one-hot query classes x precomputed key bias) when a
+    tile's depth + row + column classes fit in 16, else in the softmax; force tile shapes on both sides of that
+    limit (WM3_NA_TILE) and check each against the fp32 gather reference on the same fp16 inputs."""
+    monkeypatch.setenv("WM3_NA_TILE", tile)
+    ext, win, heads, dhp = (5, 18, 72), (5, 7, 7), 2, 128
+    t = int(np.prod(ext))
+    g = torch.Generator(device="cuda").manual_seed(17)
+    qkv = (torch.randn(t, 3 * heads * dhp, device="cuda", generator=g) * 1.5).to(lib().ELEM)
+    grid = ops().KVGrid(ext, win)
+    out = ops().natten(ops().pad_tokens_to_grid(qkv, grid), grid, heads, dhp, dhp, win)
+    ref, _ = na_reference(qkv, ext, heads, dhp, dhp, win)
+    torch.cuda.synchronize()
+    err = (out.float() - ref).abs().max().item()
+    rel = ((out.float() - ref).norm() / ref.norm()).item()
+    assert rel < 1e-2 and err < 5e-2, (tile, err, rel)
