@@ -760,12 +760,20 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
     std::lock_guard<std::mutex> lock(mu);
     auto it = tables.find(key);
     if (it == tables.end()) {
+      cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(s, &cap);
+      if (cap != cudaStreamCaptureStatusNone)
+        return set_error("wm3_natten_fwd: first call for this geometry inside a CUDA graph capture; run it once "
+                         "eagerly first (the window-mask images are built then)");
       uint8_t* t = nullptr;
       const size_t bytes = static_cast<size_t>(ntiles) * p.maxch * 4096;
       if (cudaMalloc(&t, bytes) != cudaSuccess) return set_error("wm3_natten_fwd: bias table allocation failed");
-      cudaMemsetAsync(t, 0, bytes, reinterpret_cast<cudaStream_t>(stream));
-      natten_bias_table_kernel<<<ntiles * p.maxch, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p, t);
+      cudaMemsetAsync(t, 0, bytes, s);
+      natten_bias_table_kernel<<<ntiles * p.maxch, 128, 0, s>>>(p, t);
       if (check_launch("natten_bias_table_kernel")) return -1;
+      // one-time: the images must be complete before any stream (not only this one) uses them
+      if (cudaStreamSynchronize(s) != cudaSuccess) return set_error("wm3_natten_fwd: bias table build failed");
       it = tables.emplace(key, t).first;
     }
     p.bias_table = it->second;
