@@ -401,15 +401,15 @@ def rollout_banded(lat, plan, params: dict, cfg, world: int | None = None, group
     (the same kernels and halo rows; used to verify the split on one device).  fused=True moves the halo rows
     in the QKV GEMM epilogue (peer stores into the neighbours' K/V grids, PeerHalo epoch flags across ranks)
     instead of a separate exchange.  Validation as rollout()."""
-    from .model import CALL_COUNTS, LatentState, _tokens
+    from .model import CALL_COUNTS, LatentState, latent_tokens
     from .rollout import _check_plan, plan_hours
     from .tensor import Tensor
 
     plan = _check_plan(plan, params, cfg)
     if not plan:
         return lat
+    x = latent_tokens(lat, cfg)
     proc, bands, rank, n, distributed = _banded_setup(params, cfg, world, group, fused, f"proc{plan[0]}.blk0")
-    x = _tokens(lat)
     held = [bands[rank]] if distributed else bands
     xs = [local_band_tokens(x, cfg.latent_extents, b).clone() for b in held]
     for hz in plan:

@@ -60,6 +60,7 @@ struct NaParams {
   int depth, rows, cols, rows_global, row0, halo_lo, rows_ext;
   int heads, dhp, wd, wh, ww;
   int TD, TH, TW, ntd, nth, ntw, nitems;
+  int th_first;   // first global row tile the band touches (tiles are aligned to global rows, see tile_geo)
   int ncp, nrpc;  // key-chunk box: ncp columns x nrpc rows (fixed for every tile)
   float scale_log2;
   const uint8_t* bias_table;  // BIAS: [tile][maxch] B_x images (4 KB each), built once per geometry
@@ -119,12 +120,16 @@ DEVI TileGeo tile_geo(const NaParams& p, int item) {
   const int th_i = (tile / p.ntw) % p.nth;
   const int td_i = tile / (p.ntw * p.nth);
   g.d0 = td_i * p.TD; g.d1 = min(g.d0 + p.TD, p.depth);
-  g.h0 = th_i * p.TH; g.h1 = min(g.h0 + p.TH, p.rows);
+  // Rows are GLOBAL and the row tiles are aligned to multiples of TH of the global grid, whatever the band:
+  // a query then sees the same key chunks, in the same order and slot positions, whether its band is the
+  // whole latent or one of N latitude bands, so N-band results are bitwise the single-GPU ones.  Tile rows
+  // outside the band are not stored; key rows outside the band's grid are zero-filled by TMA and masked.
+  g.h0 = (p.th_first + th_i) * p.TH; g.h1 = min(g.h0 + p.TH, p.rows_global);
   g.w0 = tw_i * p.TW; g.w1 = min(g.w0 + p.TW, p.cols);
   g.kd_lo = bump_start(g.d0, p.depth, p.wd);
   const int kd_hi = bump_start(g.d1 - 1, p.depth, p.wd) + p.wd;
-  g.kr_lo = bump_start(g.h0 + p.row0, p.rows_global, p.wh);
-  g.kr_hi = bump_start(g.h1 - 1 + p.row0, p.rows_global, p.wh) + p.wh;
+  g.kr_lo = bump_start(g.h0, p.rows_global, p.wh);
+  g.kr_hi = bump_start(g.h1 - 1, p.rows_global, p.wh) + p.wh;
   const int hw = (p.ww - 1) / 2;
   g.ncp = p.ncp;
   const bool circle = (p.ncp == p.cols);
@@ -220,7 +225,7 @@ DEVI void bx_row(const NaParams& p, const TileGeo& g, int j, int k, uint32_t (&u
       const int sd = bump_start(min(g.d0 + cl, p.depth - 1), p.depth, p.wd);
       ok = kd >= sd && kd < sd + p.wd;
     } else if (cl < p.TD + p.TH) {
-      const int sh = bump_start(min(g.h0 + cl - p.TD, p.rows - 1) + p.row0, p.rows_global, p.wh);
+      const int sh = bump_start(min(g.h0 + cl - p.TD, p.rows_global - 1), p.rows_global, p.wh);
       ok = key_ok && kr >= sh && kr < sh + p.wh;
     } else if (cl < p.TD + p.TH + p.TW) {
       const int qw = min(g.w0 + cl - p.TD - p.TH, p.cols - 1);
@@ -350,7 +355,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
         mbar_wait(bar_qempty, (tile_ctr & 1) ^ 1);
         mbar_arrive_expect_tx(bar_qfull, qbytes);
         for (int h = 0; h < halves; ++h)
-          tma_load_4d(sQ + h * 16384u, &tmQ, bar_qfull, g.head * p.dhp + 64 * h, g.w0, g.h0 + p.halo_lo,
+          tma_load_4d(sQ + h * 16384u, &tmQ, bar_qfull, g.head * p.dhp + 64 * h, g.w0, g.h0 - brow0,
                       g.b * p.depth + g.d0);
         for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
           load_kv(g, item, j, chunk_ctr, false);  // K frees after S(c - 1): streams in during softmax(c - 1)
@@ -450,11 +455,12 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
     for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
       const TileGeo g = tile_geo(p, item);
       const int qd = g.d0 + row / (p.TH * p.TW);
-      const int qh = g.h0 + (row / p.TW) % p.TH;
+      const int qh = g.h0 + (row / p.TW) % p.TH;  // global row
       const int qw = g.w0 + row % p.TW;
-      const bool qvalid = row < p.TD * p.TH * p.TW && qd < g.d1 && qh < g.h1 && qw < g.w1;
+      const bool qvalid = row < p.TD * p.TH * p.TW && qd < g.d1 && qh < g.h1 && qh >= p.row0 &&
+                          qh < p.row0 + p.rows && qw < g.w1;
       const int q_sd = bump_start(qvalid ? qd : g.d0, p.depth, p.wd);
-      const int q_sh = bump_start((qvalid ? qh : g.h0) + p.row0, p.rows_global, p.wh);
+      const int q_sh = bump_start(qvalid ? qh : g.h0, p.rows_global, p.wh);
       // window columns in patch coordinates: [c_lo, c_lo + ww), taken mod W for a full-circle patch
       const bool circle = (g.ncp == p.cols);
       const int c_lo = circle ? wrap_col((qvalid ? qw : g.w0) - hw, p.cols) : (qvalid ? qw : g.w0) - hw - g.pc0;
@@ -596,7 +602,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
       mbar_wait(bar_ofull, tile_ctr & 1);
       if (threadIdx.x == 0) NA_EV(13, tile_ctr);
       tc_fence_after();
-      const size_t tok = g.b * member_tokens + static_cast<size_t>((qd * p.rows + qh) * p.cols + qw);
+      const size_t tok = g.b * member_tokens + static_cast<size_t>((qd * p.rows + (qh - p.row0)) * p.cols + qw);
       elem_t* orow = p.out + (qvalid ? tok * p.ldo + g.head * p.dhp : 0);
       // this thread's O columns in batches of 32 TMEM columns, then 256-bit stores (whole 32-byte sectors)
 #pragma unroll 1
@@ -641,8 +647,9 @@ __global__ void natten_windows_kernel(int depth, int rows, int cols, int rows_gl
 
 // Host-side query-tile choice: minimise (#tiles x (#chunks + 1)) over TD x TH x TW <= 128; also returns
 // the fixed key-chunk box (ncp columns x nrpc rows, <= 128 keys).
-static void choose_tile(int depth, int rows, int cols, int rows_global, int wd, int wh, int ww, int* TD, int* TH,
-                        int* TW, int* NCP, int* NRPC) {
+static void choose_tile(int depth, int cols, int rows_global, int wd, int wh, int ww, int* TD, int* TH, int* TW,
+                        int* NCP, int* NRPC) {
+  const int rows = rows_global;  // the tile shape depends on the global grid only (band-invariant results)
   long best = -1;
   for (int td = 1; td <= depth && td <= 128; ++td)
     for (int th = 1; th <= rows && td * th <= 128; ++th)
@@ -692,10 +699,10 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
   p.depth = depth; p.rows = rows; p.cols = cols; p.rows_global = rows_global; p.row0 = row0;
   p.halo_lo = halo_lo; p.rows_ext = rows + halo_lo + halo_hi;
   p.heads = heads; p.dhp = dhp; p.wd = wd; p.wh = wh; p.ww = ww;
-  choose_tile(depth, rows, cols, rows_global, wd, wh, ww, &p.TD, &p.TH, &p.TW, &p.ncp, &p.nrpc);
+  choose_tile(depth, cols, rows_global, wd, wh, ww, &p.TD, &p.TH, &p.TW, &p.ncp, &p.nrpc);
   if (const char* e = getenv("WM3_NA_TILE")) {  // A/B aid: "TD,TH,TW" (key box derived as in choose_tile)
     int td, th, tw;
-    if (sscanf(e, "%d,%d,%d", &td, &th, &tw) == 3 && td >= 1 && th >= 1 && tw >= 1 && td <= depth && th <= rows &&
+    if (sscanf(e, "%d,%d,%d", &td, &th, &tw) == 3 && td >= 1 && th >= 1 && tw >= 1 && td <= depth && th <= rows_global &&
         tw <= cols && td * th * tw <= 128) {
       const int ncp = (tw + ww - 1 >= cols) ? cols : tw + ww - 1;
       const int nr_u = (th + wh - 1 < rows_global) ? th + wh - 1 : rows_global;
@@ -706,7 +713,8 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
     }
   }
   p.ntd = (depth + p.TD - 1) / p.TD;
-  p.nth = (rows + p.TH - 1) / p.TH;
+  p.th_first = row0 / p.TH;
+  p.nth = (row0 + rows - 1) / p.TH - p.th_first + 1;
   p.ntw = (cols + p.TW - 1) / p.TW;
   p.nitems = p.ntd * p.nth * p.ntw * heads * batch;
   p.scale_log2 = scale * 1.4426950408889634f;

@@ -24,7 +24,7 @@ from .params import (available_sources, block_param_names, encoder_prefix, init_
                      init_model_params)
 from .pyramid import DecoderWeights, EncoderWeights, PyramidBuffers, decode_planes, encode_planes
 from .runtime import CACHE
-from .tensor import Tensor, host_array, host_values, payload
+from .tensor import Tensor, content_tag, host_array, host_values
 
 __all__ = [
     "ModelConfig", "desk_config", "full_scale_config", "tiny_config", "mid_config", "WeatherState",
@@ -95,7 +95,7 @@ class DeviceModel:
         self._fp = None
 
     def refresh(self) -> None:
-        fp = tuple(id(payload(v)) for v in self.params.values())
+        fp = tuple(content_tag(v) for v in self.params.values())
         if fp != self._fp:
             self._enc.clear()
             self._dec = None
@@ -158,6 +158,33 @@ def _tokens(lat: LatentState) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(host_values(t), dtype=np.float32)).to("cuda")
 
 
+def check_latent(lat: LatentState, cfg: ModelConfig) -> None:
+    """The latent must be the configuration's token grid: the kernels take their sizes from cfg, so a
+    mismatched latent would read / write out of bounds.  ConfigError before any launch, as the reference's
+    natten_block check (attention.py:150-151) would raise inside its first block."""
+    ext = tuple(int(e) for e in lat.extents)
+    if ext != tuple(cfg.latent_extents):
+        raise ConfigError(f"latent extents {ext} != config latent extents {tuple(cfg.latent_extents)}")
+    shape = tuple(lat.tokens.shape)
+    if shape != (cfg.tokens, cfg.hidden):
+        raise ConfigError(f"latent tokens {shape} != (prod of extents {ext}, hidden) = {(cfg.tokens, cfg.hidden)}")
+
+
+def latent_tokens(lat: LatentState, cfg: ModelConfig) -> torch.Tensor:
+    """Validated (check_latent) contiguous fp32 device tokens of a latent (no copy when already so)."""
+    check_latent(lat, cfg)
+    return _tokens(lat).to(torch.float32).contiguous()
+
+
+def check_token_buffer(x: torch.Tensor, cfg: ModelConfig, batch: int = 1) -> None:
+    """A device token buffer the blocks run in place on: (batch * tokens, hidden) contiguous fp32 CUDA."""
+    want = (int(batch) * cfg.tokens, cfg.hidden)
+    if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.float32 or not x.is_contiguous():
+        raise ConfigError("token buffer must be a contiguous float32 CUDA tensor")
+    if tuple(x.shape) != want:
+        raise ConfigError(f"token buffer {tuple(x.shape)} != {want}")
+
+
 # ------------------------------------------------------------------------------------------------
 # API
 # ------------------------------------------------------------------------------------------------
@@ -204,23 +231,24 @@ def _check_processor(params: dict, cfg: ModelConfig, horizon: int) -> None:
 def process_inplace(x: torch.Tensor, params: dict, cfg: ModelConfig, horizon: int, batch: int = 1) -> None:
     """proc_blocks blocks applied in place to a device token buffer (no validation, no counters); x holds
     `batch` latents stacked member-major ((batch * tokens, hidden))."""
+    check_token_buffer(x, cfg, batch)
     device_model(params, cfg).run_blocks(x, [f"proc{horizon}.blk{i}" for i in range(cfg.proc_blocks)], batch)
 
 
 def process(lat: LatentState, params: dict, cfg: ModelConfig, horizon: int) -> LatentState:
     """Advance the latent state by one processor application (model.py:393-405)."""
     _check_processor(params, cfg, horizon)
+    x = latent_tokens(lat, cfg).clone()
     CALL_COUNTS[f"process{horizon}"] += 1
-    x = _tokens(lat).clone()
     process_inplace(x, params, cfg, horizon)
     return LatentState(Tensor(device=x), lat.valid_time + horizon, lat.extents)
 
 
 def decode(lat: LatentState, params: dict, cfg: ModelConfig) -> DecodedFields:
     """Project the latent token grid back to gridded fields (model.py:408-421)."""
+    x = latent_tokens(lat, cfg).clone()
     CALL_COUNTS["decode"] += 1
     dm = device_model(params, cfg)
-    x = _tokens(lat).clone()
     dm.run_blocks(x, [f"dec.blk{i}" for i in range(cfg.dec_blocks)])
     g = cfg.grid
     surface = torch.empty((cfg.surface_out, g.rows, g.cols), dtype=torch.float32, device="cuda")

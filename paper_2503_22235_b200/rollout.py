@@ -19,7 +19,7 @@ import torch
 
 from .errors import ConfigError
 from .model import (CALL_COUNTS, PRIMARY_SOURCE, DecodedFields, LatentState, ModelConfig, WeatherState,
-                    _check_processor, _tokens, decode, encode, process_inplace)
+                    _check_processor, check_latent, decode, encode, latent_tokens, process_inplace)
 from .tensor import Tensor
 
 __all__ = ["greedy_plan", "plan_hours", "rollout", "forecast", "rollout_ensemble", "forecast_ensemble",
@@ -97,19 +97,20 @@ def rollout(lat: LatentState, plan, params: dict, cfg: ModelConfig, engine=None,
     plan = _check_plan(plan, params, cfg)
     if not plan:
         return lat
+    x0 = latent_tokens(lat, cfg)
     use_graphs = (len(plan) > 1) if graphs is None else graphs
     if use_graphs:
         from .model import device_model
         device_model(params, cfg)  # refresh converted weights if the caller changed parameters
         st = _rollout_state(params, cfg)
         steps = {h: st.graph(h) for h in sorted(set(plan))}
-        st.buf.copy_(_tokens(lat))
+        st.buf.copy_(x0)
         for h in plan:
             steps[h].replay()
             CALL_COUNTS[f"process{h}"] += 1
         x = st.buf.clone()
     else:
-        x = _tokens(lat).clone()
+        x = x0.clone()
         for h in plan:
             CALL_COUNTS[f"process{h}"] += 1
             process_inplace(x, params, cfg, h)
@@ -135,8 +136,7 @@ def rollout_ensemble(latents, plan, params: dict, cfg: ModelConfig, graphs: bool
     if not latents:
         raise ConfigError("ensemble of zero members")
     for lt in latents:
-        if tuple(lt.extents) != tuple(cfg.latent_extents):
-            raise ConfigError(f"member latent extents {tuple(lt.extents)} != {tuple(cfg.latent_extents)}")
+        check_latent(lt, cfg)
     if not plan:
         return latents
     from .model import device_model
@@ -145,7 +145,7 @@ def rollout_ensemble(latents, plan, params: dict, cfg: ModelConfig, graphs: bool
     st = _rollout_state(params, cfg, n)
     steps = {h: st.graph(h) for h in sorted(set(plan))} if graphs else {}  # capture warm-up runs on st.buf
     for m, lt in enumerate(latents):
-        st.buf[m * t:(m + 1) * t].copy_(_tokens(lt))
+        st.buf[m * t:(m + 1) * t].copy_(latent_tokens(lt, cfg))
     if graphs:
         for h in plan:
             steps[h].replay()

@@ -3,7 +3,9 @@
 The reference recomputes nothing across calls except its neighbor/rotary caches (grid.py:104,
 attention.py:45).  Here every weight is converted once (float64 host -> bf16/fp32 device, re-laid out for
 the kernels) and reused until the caller's parameter arrays change: the cache key of a block is the
-identity of its 16 host arrays, and the arrays are held so their ids cannot be recycled.
+identity and a content sample of its 16 host arrays (tensor.content_tag: the reference's optimizer and
+checkpoint reload update arrays in place), and the arrays are held so their ids cannot be recycled.
+`invalidate_params()` drops every converted weight, workspace and captured rollout graph explicitly.
 """
 
 from __future__ import annotations
@@ -15,13 +17,13 @@ import torch
 from .blocks import BlockWeights, RopeTables, Workspace, prepare_block
 from .ops import KVGrid
 from .params import block_param_names
-from .tensor import payload
+from .tensor import content_tag, payload
 
 _lock = threading.Lock()
 
 
 def _fingerprint(params: dict, names) -> tuple:
-    return tuple(id(payload(params[n])) for n in names if n in params)
+    return tuple(content_tag(params[n]) for n in names if n in params)
 
 
 class WeightCache:
@@ -72,3 +74,15 @@ class WeightCache:
 
 
 CACHE = WeightCache()
+
+
+def invalidate_params() -> None:
+    """Forget every device copy of parameters: converted block weights, workspaces, rotary tables, encoder /
+    decoder weights (model.device_model) and the captured rollout graphs.  The next call re-converts from the
+    caller's current arrays.  Needed only after a sparse in-place write into a large parameter array, which
+    the content sample of tensor.content_tag may miss."""
+    CACHE.clear()
+    from . import model, rollout
+    with model._mlock:
+        model._models.clear()
+    rollout._ROLLOUTS.clear()

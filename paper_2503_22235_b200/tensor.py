@@ -8,6 +8,8 @@ as float64, on first access.  `.device` exposes the torch tensor without a copy.
 
 from __future__ import annotations
 
+import zlib
+
 import numpy as np
 import torch
 
@@ -74,3 +76,26 @@ def host_values(t) -> np.ndarray:
     """float64 numpy view of a parameter given as our Tensor, a reference Tensor (.values), a torch tensor
     (e.g. from serialization.load_params_device) or an array."""
     return host_array(t, np.float64)
+
+
+# at most this many elements of a host parameter array are hashed per content check
+TAG_SAMPLES = 2048
+
+
+def content_tag(x) -> tuple:
+    """Cheap identity-and-content fingerprint of a parameter, for the device weight caches.
+
+    The reference updates parameters in place (training.py:144, `p.values -= ...`; an `np.copyto` checkpoint
+    reload does the same), which keeps the array's identity.  The tag therefore combines the identity with a
+    content sample: for a host array, a CRC of up to TAG_SAMPLES evenly strided elements (every element of a
+    vector of that size or less); for a torch tensor, torch's in-place version counter and its storage
+    address.  A dense update (any optimizer step, any reload) changes the sample; a sparse in-place write to
+    a large array may not — call runtime.invalidate_params() after one."""
+    v = payload(x)
+    if isinstance(v, torch.Tensor):
+        return (id(v), v._version, v.data_ptr())
+    a = np.asarray(v)
+    flat = a.reshape(-1)
+    step = max(1, flat.size // TAG_SAMPLES)
+    sample = np.ascontiguousarray(flat[::step])
+    return (id(v), flat.size, zlib.crc32(sample.view(np.uint8)))
