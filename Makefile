@@ -16,7 +16,12 @@ build/%.o: $(PKG)/csrc/%.cu $(HDRS)
 $(PKG)/libwm3.so: $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart_static -lrt -ldl -lpthread
 
-clean:
-	rm -rf build $(PKG)/libwm3.so
+# profiling aid outside the public ABI (tools/mma_probe.py)
+probe: tools/libmma_probe.so
+tools/libmma_probe.so: tools/csrc/mma_probe.cu $(PKG)/libwm3.so
+	$(NVCC) $(NVFLAGS) -shared -o $@ $< $(PKG)/libwm3.so -lcuda
 
-.PHONY: all clean
+clean:
+	rm -rf build $(PKG)/libwm3.so tools/libmma_probe.so
+
+.PHONY: all clean probe

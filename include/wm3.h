@@ -8,19 +8,28 @@
  * before any of these are called; a nonzero status here is a launch/device fault
  * ("compute" category in the reference CLI, gridcast/cli.py:456-463).
  *
+ * Operand type.  Every `void*` tensor-core operand below (GEMM A / B, LayerNorm outputs, the q/k/v grid, ctx,
+ * MLP activations, conv activations and weights) is a 16-bit float of ONE type for the whole library, chosen at
+ * build time: IEEE fp16 in the default build (measured 8-10x lower forecast error than bf16),
+ * bf16 when built with -DWM3_OPERAND_BF16.  wm3_operand_dtype() reports it; bind it before feeding data.
+ * Names carrying "bf16" (wm3_layernorm_bf16, WM3_EPI_BIAS_BF16, WM3_EPI_BIAS_GELU_BF16) are historical and
+ * mean "the 16-bit operand type".  Accumulation is fp32 (TMEM); the residual stream / latent is fp32.
+ *
  * Reference interfaces replaced (paths relative to the reference package pkg/src/gridcast):
  *   wm3_neighbor_table      grid.py:96-130       bump_starts + neighborhood (bit-exact int64 export)
- *   wm3_layernorm_bf16      autodiff.py:400-424  layernorm, eps 1e-6, biased variance
+ *   wm3_layernorm_bf16      autodiff.py:400-424  layernorm, eps 1e-6, biased variance (16-bit operand out)
  *   wm3_linear              attention.py:142-143 _linear = matmul(x, W) + b, with fused epilogues:
- *                             WM3_EPI_BIAS_BF16       (plain linear, bf16 out)
+ *                             WM3_EPI_BIAS_BF16       (plain linear, 16-bit operand out)
  *                             WM3_EPI_BIAS_GELU_BF16  attention.py:182  gelu(hn2 W1 + b1), erf form to 2.5e-5
  *                             WM3_EPI_BIAS_RESID_F32  attention.py:179,183  x += ctx Wo + bo / mid W2 + b2
  *                             WM3_EPI_QKV_ROPE        attention.py:167-171  q,k,v + bias, rotary on q,k
  *                             WM3_EPI_F32             raw fp32 accumulator (tests)
  *   wm3_natten_fwd          attention.py:173-178 gather + q k^T/sqrt(dh) + softmax + @V, fused
  *   wm3_block_fwd           attention.py:146-184 the whole block (7 launches) in one call
- *   wm3_conv3x3             model.py:296-301 + autodiff.py:677-713  row zero pad, col wrap, stride 1/2
- *   wm3_convT4x4s2          model.py:317-325 + autodiff.py:716-764  exact adjoint geometry
+ *   wm3_conv  WM3_CONV_S1/S2  model.py:296-301 + autodiff.py:677-713  3x3, row zero pad, col wrap, stride 1/2
+ *   wm3_conv  WM3_CONV_T2     model.py:317-325 + autodiff.py:716-764  4x4 stride-2 transposed (exact adjoint)
+ *   wm3_fields_to_nhwc / wm3_tokens_to_nhwc   model.py:332-337, 350-360  relayouts feeding the pyramids
+ *   wm3_sq_err_rows / wm3_zonal_power          evaluation.py:37-75         verification metrics
  */
 #ifndef WM3_H
 #define WM3_H
@@ -61,18 +70,21 @@ typedef struct {
 const char* wm3_last_error(void);
 int wm3_version(void);
 int wm3_sm_count(void);
+/* The 16-bit operand type of this build: WM3_DTYPE_F16 (default) or WM3_DTYPE_BF16 (-DWM3_OPERAND_BF16). */
+enum { WM3_DTYPE_F16 = 1, WM3_DTYPE_BF16 = 2 };
+int wm3_operand_dtype(void);
 
 /* (T, K) int64 neighbor table of a (depth,rows,cols) box; rows [row0, row0+nrows) of a grid with
  * global extent `rows`.  Row-major K order kd*wh*ww + kh*ww + kw (grid.py:124-127). */
 int wm3_neighbor_table(int depth, int rows, int cols, int wd, int wh, int ww, int row0, int nrows,
                        int64_t* out, void* stream);
 
-/* out[m, 0:ldo] = bf16(layernorm(x[m, 0:n]) * gain + bias), zero in [n, ldo). */
+/* out[m, 0:ldo] = operand(layernorm(x[m, 0:n]) * gain + bias), zero in [n, ldo) (operand = wm3_operand_dtype). */
 int wm3_layernorm_bf16(const float* x, int ldx, int m, int n, const float* gain, const float* bias,
                        float eps, void* out_bf16, int ldo, void* stream);
 
-/* C[M, N] = A[M, K] (bf16, row pitch lda) * B[N, K]^T (bf16, row pitch ldb) + epilogue.
- * out: bf16 or f32 depending on epi; ldo in elements; n_valid columns are stored. */
+/* C[M, N] = A[M, K] (16-bit operand, row pitch lda) * B[N, K]^T (16-bit operand, row pitch ldb) + epilogue.
+ * out: 16-bit operand or f32 depending on epi; ldo in elements; n_valid columns are stored. */
 int wm3_linear(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi,
                void* out, int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, void* stream);
 
@@ -183,12 +195,12 @@ int wm3_block_fwd(float* x, const wm3_block_weights_t* w, const wm3_block_ws_t* 
                   const wm3_rope_t* rope, void* stream);
 
 /* Fused 3D neighborhood attention forward, over `batch` independent latents (ensemble members).
- * qkv: bf16 K/V grid [batch * depth][rows_ext][cols][ldqkv] (member b owns depth planes [b * depth, (b + 1) * depth);
+ * qkv: 16-bit operand K/V grid [batch * depth][rows_ext][cols][ldqkv] (member b owns depth planes [b * depth, (b + 1) * depth);
  *      windows never cross members), token channels [3][heads][dhp]; rows_ext =
  *      halo_lo + rows + halo_hi: the local band rows [row0, row0 + rows) of a grid with global row extent
  *      rows_global, plus halo rows received from the neighbouring bands.  Longitude wrap is handled inside
  *      the kernel (a wrapping key patch is fetched as two TMA boxes).
- * out: bf16 [batch * depth * rows * cols][ldo] (member-major, local token order), channels [heads][dhp].
+ * out: 16-bit operand [batch * depth * rows * cols][ldo] (member-major, local token order), channels [heads][dhp].
  * scale = 1/sqrt(dh).  The window mask is applied inside the QK^T MMA from key-bias images that the library
  * builds once per device and geometry (on `stream`, at first use) and caches for the process. */
 int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, int batch, int depth, int rows, int cols,
@@ -196,15 +208,15 @@ int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, int batch, in
                    int wh, int ww, float scale, void* stream);
 
 /* Implicit-GEMM convolutions of the encoder / decoder pyramids (model.py:296-325, autodiff.py:585-764).
- * Activations are bf16 NHWC with a 1-pixel halo, [imgs][H + 2][W + 2][Cp] (Cp % 64 == 0): zero halo rows,
+ * Activations are 16-bit operand NHWC with a 1-pixel halo, [imgs][H + 2][W + 2][Cp] (Cp % 64 == 0): zero halo rows,
  * halo columns = opposite edge (longitude wrap).  Modes:
  *   WM3_CONV_S1  3x3 stride 1       w: [cout_pad][9][cinp]      (tap = kh * 3 + kw)
  *   WM3_CONV_S2  3x3 stride 2       w: [cout_pad][9][cinp]
  *   WM3_CONV_T2  4x4 stride 2 transposed (adjoint geometry), as 4 output-parity classes of 2x2 taps:
  *                w: [4 = 2a + b][cout_pad][4 = 2tr + tc][cinp] = W[cin][cout][3 - a - 2tr][3 - b - 2tc]
  * cout_pad = cout rounded up to wm3_conv_bn(cout).  Epilogue: + bias, optional exact GELU, optional
- * residual (bf16 NHWC, same layout as the output), then one of
- *   WM3_CONV_OUT_NHWC    bf16 padded NHWC (pitch out_cp), wrap columns written too
+ * residual (16-bit NHWC, same layout as the output), then one of
+ *   WM3_CONV_OUT_NHWC    16-bit padded NHWC (pitch out_cp), wrap columns written too
  *   WM3_CONV_OUT_TOKENS  fp32 tokens [img][H][W][cout] (the latent, model.py:350-354)
  *   WM3_CONV_OUT_FIELD   fp32 NCHW: out[img * img_stride + (c / chan_div) * a_stride + (c % chan_div) * p_stride
  *                        + h * W + w] (surface / atmos fields with the level unfold of model.py:340-347). */
@@ -230,9 +242,6 @@ int wm3_sq_err_rows(int dtype, const void* a, long long member_stride, int k, co
                     int times, int rows, int cols, double* partial, void* stream);
 int wm3_zonal_power(int dtype, const void* field, long long member_stride, int k, int imgs, int rows, int cols,
                     double* out, void* stream);
-
-/* Profiling aid: cycles for `reps` groups of 8 K=16 MMAs (mode 0 SS, 1 TS, 2 TS with MN-major B), N = n. */
-int wm3_mma_probe(int mode, int n, int reps, int ctas, long long* out_cycles, void* stream);
 
 /* Debug export of the kernel's own window arithmetic: per token, the (start_d, start_h, col_off)
  * it uses; int32 [T][3]. */

@@ -15,8 +15,10 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("WM3_LIB") or os.path.join(_HERE, "libwm3.so")  # WM3_LIB: A/B builds (profiling)
 
-# Tensor-core operand dtype the library is built for (csrc/common.cuh elem_t): fp16 by default.
+# Tensor-core operand dtype the library is built for (csrc/common.cuh elem_t): fp16 by default.  load_library()
+# checks it against the library's own wm3_operand_dtype() and refuses a mismatched build.
 ELEM = torch.float16
+WM3_DTYPE_F16, WM3_DTYPE_BF16 = 1, 2
 
 WM3_EPI_F32 = 0
 WM3_EPI_BIAS_BF16 = 1
@@ -92,7 +94,6 @@ SIGNATURES = {
     "wm3_natten_fwd": [_vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _f, _vp],
     "wm3_natten_windows": [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp],
     "wm3_conv_bn": [_i],
-    "wm3_mma_probe": [_i, _i, _i, _i, _vp, _vp],
     "wm3_conv": [_i, _vp, _i, _i, _i, _i, _vp, _i, _vp, _i, _vp, _i, _i, _vp, _i, _ll, _ll, _ll, _i, _vp],
     "wm3_fields_to_nhwc": [_vp, _ll, _ll, _ll, _i, _i, _i, _i, _i, _i, _vp, _vp],
     "wm3_tokens_to_nhwc": [_vp, _i, _i, _i, _i, _i, _vp, _vp],
@@ -106,7 +107,7 @@ WM3_CONV_OUT_NHWC, WM3_CONV_OUT_TOKENS, WM3_CONV_OUT_FIELD = 0, 1, 2
 
 def exported_symbols() -> list[str]:
     """Every symbol include/wm3.h declares (checked against the .so by the CPU test suite)."""
-    return ["wm3_last_error", "wm3_version", "wm3_sm_count"] + list(SIGNATURES)
+    return ["wm3_last_error", "wm3_version", "wm3_sm_count", "wm3_operand_dtype"] + list(SIGNATURES)
 
 
 @lru_cache(maxsize=1)
@@ -119,6 +120,12 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.wm3_last_error.argtypes = []
     lib.wm3_version.restype = _i
     lib.wm3_sm_count.restype = _i
+    lib.wm3_operand_dtype.restype = _i
+    lib.wm3_operand_dtype.argtypes = []
+    want = {torch.float16: WM3_DTYPE_F16, torch.bfloat16: WM3_DTYPE_BF16}[ELEM]
+    if lib.wm3_operand_dtype() != want:
+        raise RuntimeError(f"{path} is built for operand dtype {lib.wm3_operand_dtype()}, the host layer expects "
+                           f"{want} ({ELEM}); rebuild with the matching WM3_OPERAND_BF16 setting")
     for name, argt in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = argt

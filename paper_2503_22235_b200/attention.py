@@ -53,16 +53,51 @@ def validate_block_args(shape, extents, window, heads: int) -> int:
     return dh
 
 
-def natten_block(x, params: dict, prefix: str, extents, window, heads: int) -> Tensor:
+def _foreign_tensor(x) -> bool:
+    """x is a tensor of another package with the reference's surface (gridcast.autodiff.Tensor: `.values`
+    plus the tape), not ours, not a torch tensor, not a plain array."""
+    return (not isinstance(x, (Tensor, torch.Tensor, np.ndarray)) and hasattr(x, "values")
+            and hasattr(type(x), "reshape"))
+
+
+def _no_backward(grad_out, saved, add):
+    raise NotImplementedError("backward through the B200 natten_block is not supported (forward-only path); "
+                              "train with the reference block (integration.uninstall)")
+
+
+def _wrap_foreign(x, values: np.ndarray, params: dict, prefix: str):
+    """The block output as the caller's tensor class.  For the reference's Tensor it goes through the
+    reference's own recorder (autodiff.py:288-291), so grad mode and requires_grad propagate exactly as for
+    the reference block; the recorded rule raises on backward instead of silently dropping the gradient."""
+    import sys
+    record = getattr(sys.modules.get(type(x).__module__), "_record", None)
+    if record is None:
+        return type(x)(values)
+    parents = [x] + [params[n] for n in block_param_names(prefix) if n in params]
+    return record("natten_block_b200", values, parents, [], _no_backward)
+
+
+def natten_block(x, params: dict, prefix: str, extents, window, heads: int):
+    """One pre-norm neighborhood attention block (attention.py:146-184) on the B200.
+
+    Returns our Tensor (device-backed) for our / torch / numpy inputs.  Given the reference's own Tensor
+    (the operator-level seam: `gridcast.model.natten_block = natten_block`), it returns a
+    tensor of the caller's class built from the float64 result, so the reference's encode / process / decode
+    keep applying their own ops (`tokens.reshape(...)`, model.py:357-360) to it.  The B200 block is forward
+    only: it is recorded on the reference's tape like the reference block, and a backward sweep that reaches
+    it raises NotImplementedError instead of silently cutting the gradient."""
     shape = tuple(x.shape)
     dh = validate_block_args(shape, extents, window, heads)
-    xd = to_device_f32(x)
+    foreign = _foreign_tensor(x)
     bw = CACHE.block(params, prefix, heads)
     if bw.hidden != shape[1]:
         raise ConfigError(f"parameters {prefix} have width {bw.hidden}, tokens have {shape[1]}")
+    xd = to_device_f32(x)
     from .blocks import block_forward
     block_forward(xd, bw, CACHE.workspace(extents, window, bw), CACHE.rope(extents, dh), tuple(extents),
                   tuple(window))
+    if foreign:
+        return _wrap_foreign(x, xd.to("cpu", torch.float64).numpy(), params, prefix)
     return Tensor(device=xd)
 
 
@@ -84,7 +119,10 @@ class NattenBlockStream:
         self.dh = validate_block_args((t, dim), extents, window, heads)
         self.extents, self.window = tuple(int(e) for e in extents), tuple(int(e) for e in window)
         self.bw = CACHE.block(params, prefix, heads)
-        self.ws = CACHE.workspace(self.extents, self.window, self.bw, tag="stream")
+        # a private workspace: two streams (e.g. a pipeline of two blocks) run concurrently on their own
+        # s_run streams and must not share the q/k/v / ctx / MLP buffers
+        from .blocks import Workspace
+        self.ws = Workspace(ops.KVGrid(self.extents, self.window), self.bw)
         self.rope = CACHE.rope(self.extents, self.dh)
         self.buf = [torch.empty((t, dim), dtype=torch.float32, device="cuda") for _ in range(self.NBUF)]
         self.s_in, self.s_run, self.s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
@@ -92,6 +130,9 @@ class NattenBlockStream:
         self.computed = [torch.cuda.Event() for _ in range(self.NBUF)]
         self.downloaded = [None] * self.NBUF
         self.i = 0
+        # weight conversion, workspace zero-fill and rotary tables were queued on the creating stream: finish
+        # them before s_run (which only waits on uploads) can read them
+        torch.cuda.current_stream().synchronize()
 
     def submit(self, host_in: torch.Tensor, host_out: torch.Tensor) -> None:
         from .blocks import block_forward

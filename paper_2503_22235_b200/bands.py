@@ -19,6 +19,7 @@ from dataclasses import dataclass
 
 import torch
 
+from .config import as_config
 from .grid import bump_starts
 
 
@@ -401,6 +402,7 @@ def rollout_banded(lat, plan, params: dict, cfg, world: int | None = None, group
     (the same kernels and halo rows; used to verify the split on one device).  fused=True moves the halo rows
     in the QKV GEMM epilogue (peer stores into the neighbours' K/V grids, PeerHalo epoch flags across ranks)
     instead of a separate exchange.  Validation as rollout()."""
+    cfg = as_config(cfg)
     from .model import CALL_COUNTS, LatentState, latent_tokens
     from .rollout import _check_plan, plan_hours
     from .tensor import Tensor
@@ -486,6 +488,7 @@ def forecast_banded(state, dt: int, params: dict, cfg, world: int | None = None,
     (`BandedProcessor`, as rollout_banded).  Every rank returns the full DecodedFields.  `world` without a
     group emulates the split in one process (plane ranges and bands one after another on one GPU).
     Validation as forecast(), before any launch."""
+    cfg = as_config(cfg)
     from .model import CALL_COUNTS, DecodedFields, stage_inputs
     from .pyramid import decode_planes, encode_planes
     from .rollout import _check_plan, greedy_plan, plan_hours

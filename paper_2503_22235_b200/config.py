@@ -176,6 +176,23 @@ def config_from_dict(d: dict) -> ModelConfig:
     return ModelConfig(grid=grid, **rest)
 
 
+_FOREIGN: dict = {}
+
+
+def as_config(cfg) -> ModelConfig:
+    """Our ModelConfig for `cfg`: itself, or the field-for-field equal copy of another package's config (the
+    reference's gridcast.model.ModelConfig has the same fields but not every derived property used here, e.g.
+    head_dim), built once per distinct config.  Validation as ModelConfig (ConfigError)."""
+    if isinstance(cfg, ModelConfig):
+        return cfg
+    hit = _FOREIGN.get(cfg)
+    if hit is None:
+        d = {k: getattr(cfg.grid, k) for k in _GRID_KEYS}
+        d.update({k: getattr(cfg, k) for k in _KEY_TYPES if k not in _GRID_KEYS})
+        hit = _FOREIGN[cfg] = config_from_dict(d)
+    return hit
+
+
 def _fmt(v) -> str:
     if isinstance(v, bool):
         return "true" if v else "false"

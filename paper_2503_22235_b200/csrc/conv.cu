@@ -331,12 +331,7 @@ __global__ void tokens_to_nhwc_kernel(const float* __restrict__ tok, int imgs, i
 template <int BN>
 static int launch_conv(const CUtensorMap& ta, const CUtensorMap& tb, const ConvParams& p, cudaStream_t s) {
   using Cfg = ConvCfg<BN>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-    if (e != cudaSuccess) return set_error("cudaFuncSetAttribute(conv): %s", cudaGetErrorString(e));
-    attr = true;
-  }
+  if (ensure_smem_attr(reinterpret_cast<const void*>(conv_tc_kernel<BN>), Cfg::SMEM, "conv")) return -1;
   const long long ntiles = static_cast<long long>(p.imgs) * p.nclass * p.tiles_per_class * (p.cout_pad / BN);
   const int grid = static_cast<int>(ntiles < sm_count() ? ntiles : sm_count());
   if (launch_pdl(conv_tc_kernel<BN>, dim3(grid), dim3(CV_THREADS), Cfg::SMEM, s, ta, tb, p)) return -1;

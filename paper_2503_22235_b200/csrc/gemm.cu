@@ -579,12 +579,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUten
                        const EpiParams& ep, cudaStream_t stream) {
   using Cfg = GemmCfg<BN, CG, EPI>;
   auto kern = gemm_tc_kernel<BN, EPI, CG>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-    if (e != cudaSuccess) return set_error("cudaFuncSetAttribute(gemm): %s", cudaGetErrorString(e));
-    attr_done = true;
-  }
+  if (ensure_smem_attr(reinterpret_cast<const void*>(kern), Cfg::SMEM, "gemm")) return -1;
   const int ntiles = ep.planes * ep.tiles_per_plane * ((N + BN - 1) / BN);
   if (CG == 1) {
     const int grid = ntiles < sm_count() ? ntiles : sm_count();

@@ -3,6 +3,8 @@
 #include <cstdlib>
 #include <cstdio>
 #include <mutex>
+#include <set>
+#include <utility>
 
 #include "launch.h"
 #include "../../include/wm3.h"
@@ -36,14 +38,33 @@ bool pdl_enabled() {
 }
 
 int sm_count() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  // per device (a process may drive several GPUs); cached per (thread, device)
+  static thread_local int cached_dev = -1, n = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev) {
+    n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    cached_dev = dev;
   }
   return n;
+}
+
+int ensure_smem_attr(const void* func, int bytes, const char* what) {
+  // cudaFuncSetAttribute applies to the current device only: remember (device, kernel, size) triples, under a
+  // lock so concurrent host threads (one per GPU) stay correct
+  static std::mutex mu;
+  static std::set<std::pair<std::pair<int, const void*>, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_pair(std::make_pair(dev, func), bytes);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(key)) return 0;
+  const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return set_error("cudaFuncSetAttribute(%s): %s", what, cudaGetErrorString(e));
+  done.insert(key);
+  return 0;
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -102,5 +123,5 @@ int make_tmap_2d_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_
 }  // namespace wm3
 
 extern "C" const char* wm3_last_error(void) { return wm3::g_err; }
-extern "C" int wm3_version(void) { return 1; }
+extern "C" int wm3_version(void) { return 2; }
 extern "C" int wm3_sm_count(void) { return wm3::sm_count(); }

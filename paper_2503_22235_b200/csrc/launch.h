@@ -11,6 +11,8 @@ int set_error(const char* fmt, ...);
 // cudaGetLastError after a launch; returns 0 or -1 (with message).
 int check_launch(const char* what);
 int sm_count();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel, size); thread-safe.
+int ensure_smem_attr(const void* func, int bytes, const char* what);
 
 // 2D bf16 tensor map (inner = contiguous extent, outer = rows, pitch in elements), SWIZZLE_128B,
 // OOB elements zero-filled.  Box = (box_inner, box_outer); box_inner * 2 must be 128.

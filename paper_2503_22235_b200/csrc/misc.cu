@@ -219,3 +219,5 @@ extern "C" int wm3_layernorm_bf16(const float* x, int ldx, int m, int n, const f
   if (launch_pdl(kern, dim3(blocks), dim3(threads), 0, s, x, ldx, m, n, gain, bias, eps, o, ldo)) return -1;
   return check_launch("layernorm_kernel");
 }
+
+extern "C" int wm3_operand_dtype(void) { return wm3::kElemFmt == 0 ? WM3_DTYPE_F16 : WM3_DTYPE_BF16; }

@@ -215,7 +215,7 @@ DEVI void bx_row(const NaParams& p, const TileGeo& g, int j, int k, uint32_t (&u
   const int kr = kr0 + rr;
   const int hw = (p.ww - 1) / 2;
   const bool circle = (g.ncp == p.cols);
-  const uint32_t masked = __half_as_ushort(__float2half(NA_MASKED));
+  const uint32_t masked = pack_elem(NA_MASKED, 0.f) & 0xffffu;  // operand encoding (kElemFmt) of the bias
 #pragma unroll
   for (int i = 0; i < 8; ++i) u[i] = 0u;  // fp16 0 = open
 #pragma unroll
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
     // A_x row `tid`: ones at the query's tile depth / row / column class (td-major lanes)
     uint32_t u[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
     if (tid < p.TD * p.TH * p.TW) {
-      const uint32_t one = __half_as_ushort(__float2half(1.f));
+      const uint32_t one = pack_elem(1.f, 0.f) & 0xffffu;
       const int c3[3] = {tid / (p.TH * p.TW), p.TD + (tid / p.TW) % p.TH, p.TD + p.TH + tid % p.TW};
       for (int i = 0; i < 3; ++i) u[c3[i] >> 1] |= one << (16 * (c3[i] & 1));
     }
@@ -732,14 +732,8 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
   CUtensorMap tq, tkv;
   if (make_tmap(&tq, qkv, TMAP_BF16, 4, dims, strides, qbox, nullptr)) return -1;
   if (make_tmap(&tkv, qkv, TMAP_BF16, 4, dims, strides, kvbox, nullptr)) return -1;
-  static bool attr = false;
-  if (!attr) {
-    for (auto kern : {natten_fwd_kernel<true>, natten_fwd_kernel<false>}) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, NA_SMEM);
-      if (e != cudaSuccess) return set_error("cudaFuncSetAttribute(natten): %s", cudaGetErrorString(e));
-    }
-    attr = true;
-  }
+  for (auto kern : {natten_fwd_kernel<true>, natten_fwd_kernel<false>})
+    if (ensure_smem_attr(reinterpret_cast<const void*>(kern), NA_SMEM, "natten")) return -1;
   // window mask in the MMA when the tile's query classes fit the extra K = 16 step (WM3_NA_BIAS=0: softmax mask)
   static const bool bias_env = [] {
     const char* e = getenv("WM3_NA_BIAS");
@@ -770,7 +764,12 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
     if (it == tables.end()) {
       cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
       cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-      cudaStreamIsCapturing(s, &cap);
+      const cudaError_t ce = cudaStreamIsCapturing(s, &cap);
+      if (ce != cudaSuccess) {  // e.g. the legacy stream during another thread's global-mode capture
+        cudaGetLastError();
+        return set_error("wm3_natten_fwd: cannot build the window-mask images now (%s); run this geometry once "
+                         "eagerly first", cudaGetErrorString(ce));
+      }
       if (cap != cudaStreamCaptureStatusNone)
         return set_error("wm3_natten_fwd: first call for this geometry inside a CUDA graph capture; run it once "
                          "eagerly first (the window-mask images are built then)");
@@ -779,9 +778,15 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
       if (cudaMalloc(&t, bytes) != cudaSuccess) return set_error("wm3_natten_fwd: bias table allocation failed");
       cudaMemsetAsync(t, 0, bytes, s);
       natten_bias_table_kernel<<<ntiles * p.maxch, 128, 0, s>>>(p, t);
-      if (check_launch("natten_bias_table_kernel")) return -1;
+      if (check_launch("natten_bias_table_kernel")) {
+        cudaFree(t);
+        return -1;
+      }
       // one-time: the images must be complete before any stream (not only this one) uses them
-      if (cudaStreamSynchronize(s) != cudaSuccess) return set_error("wm3_natten_fwd: bias table build failed");
+      if (cudaStreamSynchronize(s) != cudaSuccess) {
+        cudaFree(t);
+        return set_error("wm3_natten_fwd: bias table build failed");
+      }
       it = tables.emplace(key, t).first;
     }
     p.bias_table = it->second;

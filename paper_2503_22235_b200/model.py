@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from .blocks import block_forward
-from .config import (DOWNSAMPLE_STAGES, N_STATIC_FIELDS, PRIMARY_SOURCE, GridSpec, ModelConfig,  # noqa: F401
+from .config import (DOWNSAMPLE_STAGES, as_config, N_STATIC_FIELDS, PRIMARY_SOURCE, GridSpec, ModelConfig,  # noqa: F401
                      config_from_dict, config_to_dict, desk_config, full_scale_config, load_config, mid_config,
                      save_config, shape_plan, tiny_config)
 from .errors import ConfigError
@@ -191,6 +191,7 @@ def check_token_buffer(x: torch.Tensor, cfg: ModelConfig, batch: int = 1) -> Non
 def stage_inputs(state: WeatherState, params: dict, cfg: ModelConfig, source: str = PRIMARY_SOURCE):
     """encode()'s validation (ConfigError before any launch) and the host->device copy of the state into the
     pyramid input buffers; returns (device model, encoder weight prefix)."""
+    cfg = as_config(cfg)
     prefix = encoder_prefix(source)
     if f"{prefix}.stem_sfc.w" not in params:
         raise ConfigError(f"no encoder for source {source!r}")
@@ -213,6 +214,7 @@ def stage_inputs(state: WeatherState, params: dict, cfg: ModelConfig, source: st
 
 def encode(state: WeatherState, params: dict, cfg: ModelConfig, source: str = PRIMARY_SOURCE) -> LatentState:
     """Lift one gridded state into the latent token grid (model.py:363-390)."""
+    cfg = as_config(cfg)
     dm, prefix = stage_inputs(state, params, cfg, source)
     bufs = dm.buffers()
     tokens = torch.empty((cfg.tokens, cfg.hidden), dtype=torch.float32, device="cuda")
@@ -231,12 +233,14 @@ def _check_processor(params: dict, cfg: ModelConfig, horizon: int) -> None:
 def process_inplace(x: torch.Tensor, params: dict, cfg: ModelConfig, horizon: int, batch: int = 1) -> None:
     """proc_blocks blocks applied in place to a device token buffer (no validation, no counters); x holds
     `batch` latents stacked member-major ((batch * tokens, hidden))."""
+    cfg = as_config(cfg)
     check_token_buffer(x, cfg, batch)
     device_model(params, cfg).run_blocks(x, [f"proc{horizon}.blk{i}" for i in range(cfg.proc_blocks)], batch)
 
 
 def process(lat: LatentState, params: dict, cfg: ModelConfig, horizon: int) -> LatentState:
     """Advance the latent state by one processor application (model.py:393-405)."""
+    cfg = as_config(cfg)
     _check_processor(params, cfg, horizon)
     x = latent_tokens(lat, cfg).clone()
     CALL_COUNTS[f"process{horizon}"] += 1
@@ -246,6 +250,7 @@ def process(lat: LatentState, params: dict, cfg: ModelConfig, horizon: int) -> L
 
 def decode(lat: LatentState, params: dict, cfg: ModelConfig) -> DecodedFields:
     """Project the latent token grid back to gridded fields (model.py:408-421)."""
+    cfg = as_config(cfg)
     x = latent_tokens(lat, cfg).clone()
     CALL_COUNTS["decode"] += 1
     dm = device_model(params, cfg)

@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import torch
 
+from .config import as_config
 from .errors import ConfigError
 from .model import (CALL_COUNTS, PRIMARY_SOURCE, DecodedFields, LatentState, ModelConfig, WeatherState,
                     _check_processor, check_latent, decode, encode, latent_tokens, process_inplace)
@@ -94,6 +95,7 @@ def _check_plan(plan, params: dict, cfg: ModelConfig) -> tuple:
 def rollout(lat: LatentState, plan, params: dict, cfg: ModelConfig, engine=None,
             graphs: bool | None = None) -> LatentState:
     """Apply the plan's processors in sequence, entirely in latent space (rollout.py:56-81)."""
+    cfg = as_config(cfg)
     plan = _check_plan(plan, params, cfg)
     if not plan:
         return lat
@@ -120,6 +122,7 @@ def rollout(lat: LatentState, plan, params: dict, cfg: ModelConfig, engine=None,
 def forecast(state: WeatherState, dt: int, params: dict, cfg: ModelConfig, source: str = PRIMARY_SOURCE,
              engine=None) -> DecodedFields:
     """encode -> greedy latent rollout -> decode (rollout.py:84-91)."""
+    cfg = as_config(cfg)
     plan = greedy_plan(dt, cfg.max_dt)
     lat = encode(state, params, cfg, source=source)
     lat = rollout(lat, plan, params, cfg, engine=engine)
@@ -131,6 +134,7 @@ def rollout_ensemble(latents, plan, params: dict, cfg: ModelConfig, graphs: bool
 
     Validation as rollout() (before any launch); an empty plan returns the input objects.  Member m's output
     equals rollout(latents[m], plan, ...) bitwise."""
+    cfg = as_config(cfg)
     latents = list(latents)
     plan = _check_plan(plan, params, cfg)
     if not latents:
@@ -161,6 +165,7 @@ def rollout_ensemble(latents, plan, params: dict, cfg: ModelConfig, graphs: bool
 
 def forecast_ensemble(states, dt: int, params: dict, cfg: ModelConfig, source: str = PRIMARY_SOURCE) -> list:
     """forecast() of every member: per-member encode, one batched greedy rollout, per-member decode."""
+    cfg = as_config(cfg)
     plan = greedy_plan(dt, cfg.max_dt)
     lats = [encode(s, params, cfg, source=source) for s in states]
     lats = rollout_ensemble(lats, plan, params, cfg)

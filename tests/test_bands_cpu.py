@@ -149,7 +149,7 @@ def _rollout_worker(rank, world, port, out_q):
         from paper_2503_22235_b200.tensor import Tensor
         cfg = M.mid_config()
         B.BandedProcessor = _FakeProcessor
-        M._tokens = lambda lat: lat.tokens.device  # CPU tensor stands in for the device latent
+        M.latent_tokens = lambda lat, cfg: lat.tokens.device  # CPU tensor stands in for the device latent
         M.device_model = lambda params, cfg: None
         params = {f"proc{h}.blk0.ln1.gain": None for h in cfg.horizons}
         x = torch.from_numpy(np.random.default_rng(3).standard_normal((cfg.tokens, 4)))

@@ -215,3 +215,77 @@ def test_product_path_refuses_to_run_without_gpu():
 
 def test_block_flops_formula():
     assert math.isclose(om.block_flops(81000, 1024, 245), 2.119716864e12)
+
+
+def test_operand_dtype_export_matches_host_layer():
+    """The header's operand-type query: the host layer's ELEM must be the library's build type."""
+    import torch
+    from paper_2503_22235_b200 import _lib
+    lib = _lib.load_library()  # refuses a mismatched build
+    assert lib.wm3_operand_dtype() == {torch.float16: 1, torch.bfloat16: 2}[_lib.ELEM]
+
+
+# ------------------------------------------------------------------------------------------------
+# latent validation before any launch (ADVICE r1: a mismatched latent must not reach the kernels)
+# ------------------------------------------------------------------------------------------------
+def _lat(tokens, extents, vt=0):
+    from paper_2503_22235_b200.model import LatentState
+    from paper_2503_22235_b200.tensor import Tensor
+    return LatentState(Tensor(tokens), vt, extents)
+
+
+@pytest.mark.parametrize("shape,extents", [((150, 64), (3, 5, 10)), ((149, 48), (3, 5, 10)),
+                                           ((150, 48), (3, 10, 5)), ((300, 48), (3, 10, 10))])
+def test_mismatched_latent_rejected_before_launch(shape, extents):
+    """process / rollout / decode / rollout_ensemble / rollout_banded raise ConfigError (attention.py:150-151
+    style) for a latent whose token count, width or extents differ from the config's, before touching the
+    device (this runs with no GPU: reaching a launch would raise RuntimeError instead)."""
+    import paper_2503_22235_b200.model as M
+    import paper_2503_22235_b200.rollout as R
+    from paper_2503_22235_b200.bands import rollout_banded
+    cfg = M.desk_config()
+    assert cfg.latent_extents == (3, 5, 10) and cfg.hidden == 48
+    params = {f"proc{h}.blk0.ln1.gain": None for h in cfg.horizons}
+    lat = _lat(np.zeros(shape), extents)
+    with pytest.raises(ConfigError):
+        M.process(lat, params, cfg, 6)
+    with pytest.raises(ConfigError):
+        R.rollout(lat, (6, 1), params, cfg)
+    with pytest.raises(ConfigError):
+        M.decode(lat, params, cfg)
+    with pytest.raises(ConfigError):
+        R.rollout_ensemble([lat], (6,), params, cfg)
+    with pytest.raises(ConfigError):
+        rollout_banded(lat, (6,), params, cfg, world=1)
+    assert R.rollout(lat, (), params, cfg) is lat  # empty plan: the same object, no validation (rollout.py:66-67)
+
+
+def test_process_inplace_rejects_bad_buffer():
+    import torch
+    import paper_2503_22235_b200.model as M
+    cfg = M.desk_config()
+    for x in (torch.zeros(cfg.tokens, cfg.hidden), torch.zeros(cfg.tokens, cfg.hidden, dtype=torch.float64),
+              np.zeros((cfg.tokens, cfg.hidden))):
+        with pytest.raises(ConfigError):
+            M.process_inplace(x, {}, cfg, 6)
+
+
+def test_content_tag_sees_in_place_updates():
+    """The device weight caches key on tensor.content_tag: the reference's in-place optimizer step
+    (training.py:144) and np.copyto reloads change it; reads do not."""
+    import torch
+    from paper_2503_22235_b200.tensor import Tensor, content_tag
+    rng = np.random.default_rng(0)
+    for shape in ((7,), (1024, 4096), (3, 1000, 7)):
+        p = Tensor(rng.standard_normal(shape))
+        t0 = content_tag(p)
+        assert content_tag(p) == t0
+        p.values -= 1e-3 * rng.standard_normal(shape)  # in place: same array object
+        t1 = content_tag(p)
+        assert t1 != t0 and t1[0] == t0[0]
+        np.copyto(p.values, rng.standard_normal(shape))
+        assert content_tag(p) != t1
+    t = torch.zeros(10)
+    a = content_tag(t)
+    t.add_(1.0)
+    assert content_tag(t) != a

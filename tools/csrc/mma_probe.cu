@@ -1,8 +1,7 @@
 // Micro-benchmark of tcgen05.mma issue/execution rates for the shapes the kernels use (profiling aid; not on
 // the forecast path).  One CTA per SM; one thread issues `reps` groups of 8 K=16 MMAs and waits for each group.
-#include "common.cuh"
-#include "launch.h"
-#include "../../include/wm3.h"
+#include "../../paper_2503_22235_b200/csrc/common.cuh"
+#include "../../paper_2503_22235_b200/csrc/launch.h"
 
 namespace wm3 {
 
@@ -66,7 +65,7 @@ __global__ void __launch_bounds__(128, 1) mma_probe_kernel(int mode, int n, int 
 
 using namespace wm3;
 
-extern "C" int wm3_mma_probe(int mode, int n, int reps, int ctas, long long* out_cycles, void* stream) {
+extern "C" int mma_probe(int mode, int n, int reps, int ctas, long long* out_cycles, void* stream) {
   const int smem = 98304 + 1024;
   static bool attr = false;
   if (!attr) {
