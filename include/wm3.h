@@ -227,9 +227,11 @@ int wm3_conv(int mode, const void* in, int imgs, int hin, int win, int cinp, con
              const float* bias, int act_gelu, const void* resid, int resid_cp, int out_kind, void* out, int out_cp,
              long long img_stride, long long a_stride, long long p_stride, int chan_div, void* stream);
 /* fp32 fields -> padded NHWC: channel c of image i at src[i * img_stride + (c / chan_div) * a_stride
- * + (c % chan_div) * p_stride + h * W + w] (level fold of model.py:332-337). */
+ * + (c % chan_div) * p_stride + h * W + w] (level fold of model.py:332-337).  If `overflow` is non-null, *overflow
+ * is OR-ed with 1 when any input value is outside the operand type's finite range (|x| > 65504 for fp16) or is
+ * not finite; the caller zeroes it first and checks it after the launch. */
 int wm3_fields_to_nhwc(const float* src, long long img_stride, long long a_stride, long long p_stride, int chan_div,
-                       int imgs, int channels, int h, int w, int cp, void* dst, void* stream);
+                       int imgs, int channels, int h, int w, int cp, void* dst, int* overflow, void* stream);
 /* fp32 tokens [img][H][W][channels] -> padded NHWC (model.py:357-360). */
 int wm3_tokens_to_nhwc(const float* tokens, int imgs, int h, int w, int channels, int cp, void* dst, void* stream);
 

@@ -95,7 +95,7 @@ SIGNATURES = {
     "wm3_natten_windows": [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp],
     "wm3_conv_bn": [_i],
     "wm3_conv": [_i, _vp, _i, _i, _i, _i, _vp, _i, _vp, _i, _vp, _i, _i, _vp, _i, _ll, _ll, _ll, _i, _vp],
-    "wm3_fields_to_nhwc": [_vp, _ll, _ll, _ll, _i, _i, _i, _i, _i, _i, _vp, _vp],
+    "wm3_fields_to_nhwc": [_vp, _ll, _ll, _ll, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp],
     "wm3_tokens_to_nhwc": [_vp, _i, _i, _i, _i, _i, _vp, _vp],
     "wm3_sq_err_rows": [_i, _vp, _ll, _i, _vp, _vp, _i, _i, _i, _vp, _vp],
     "wm3_zonal_power": [_i, _vp, _ll, _i, _i, _i, _i, _vp, _vp],

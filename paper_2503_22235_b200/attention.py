@@ -161,27 +161,39 @@ class NattenBlockStream:
 
 
 def attention_weights(x_values, params: dict, prefix: str, extents, window, heads: int) -> np.ndarray:
-    """Softmax weights (T, heads, K) for inspection (attention.py:187-212).
+    """Softmax weights (T, heads, K) for inspection (attention.py:187-212), produced by the fused attention
+    kernel itself.
 
-    q and k come from the same fused LN + QKV/rotary kernels as the block; the probe then evaluates the
-    scores on the neighbor table exported by the window kernel.
-    """
+    q and k come from the block's own LN + QKV/rotary kernels.  The probabilities are read out of the NA kernel
+    by feeding it one-hot values: in pass r, V of token r * dhp + j is the unit vector e_j (every head) and
+    every other token's V is 0, so the kernel's normalised output row of query t is exactly its softmax weight
+    on each key of that token range (its own masked online softmax, fp32 statistics, operand-rounded output).
+    ceil(T / dhp) passes cover every key; the weights are then gathered in window order with the kernel's
+    neighbor table (grid.py:124-127 K order)."""
     xd = to_device_f32(x_values)
     t, dim = xd.shape
     dh = validate_block_args((t, dim), extents, window, heads)
+    extents, window = tuple(int(e) for e in extents), tuple(int(e) for e in window)
     bw = CACHE.block(params, prefix, heads)
     ws = CACHE.workspace(extents, window, bw)
     rope = CACHE.rope(extents, dh)
     ops.layernorm_bf16(xd, bw.ln1_g, bw.ln1_b, out=ws.hn)
     ops.linear_grid(ws.hn, bw.w_qkv, _lib.WM3_EPI_QKV_ROPE, bw.b_qkv, ws.qkv, ws.grid,
                     rope=rope.struct(extents, 0, bw.heads, bw.dhp))
-    table = ops.neighbor_table(extents, window)
-    sec = heads * bw.dhp
-    qkv = ws.grid.interior(ws.qkv)
-    q = qkv[:, :sec].float().view(t, heads, bw.dhp)
-    k = qkv[:, sec:2 * sec].float().view(t, heads, bw.dhp)
-    s = torch.einsum("thd,tkhd->thk", q, k[table]) / math.sqrt(dh)
-    return torch.softmax(s, dim=-1).double().cpu().numpy()
+    dhp, sec = bw.dhp, heads * bw.dhp
+    qkv = ws.qkv.clone()  # single band, no halos: grid rows are tokens
+    v = qkv[:, 2 * sec:].view(t, heads, dhp)
+    full = torch.empty((t, heads, t), dtype=torch.float32, device=xd.device)
+    for r0 in range(0, t, dhp):
+        n = min(dhp, t - r0)
+        v.zero_()
+        idx = torch.arange(n, device=xd.device)
+        v[r0 + idx, :, idx] = 1.0
+        out = ops.natten(qkv, ws.grid, heads, dhp, dh, window).view(t, heads, dhp)
+        full[:, :, r0:r0 + n] = out[:, :, :n].float()
+    table = ops.neighbor_table(extents, window)  # (T, K)
+    probs = torch.gather(full, 2, table.unsqueeze(1).expand(t, heads, table.shape[1]))
+    return probs.double().cpu().numpy()
 
 
 def rotary_tables(extents, head_dim: int):

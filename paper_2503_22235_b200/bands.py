@@ -490,7 +490,7 @@ def forecast_banded(state, dt: int, params: dict, cfg, world: int | None = None,
     Validation as forecast(), before any launch."""
     cfg = as_config(cfg)
     from .model import CALL_COUNTS, DecodedFields, stage_inputs
-    from .pyramid import decode_planes, encode_planes
+    from .pyramid import check_input_range, decode_planes, encode_planes
     from .rollout import _check_plan, greedy_plan, plan_hours
     from .tensor import Tensor
 
@@ -515,6 +515,7 @@ def forecast_banded(state, dt: int, params: dict, cfg, world: int | None = None,
     for lo, hi in mine:
         if hi > lo:
             encode_planes(enc, bufs, cfg, tokens, (lo, hi))
+            check_input_range(bufs)
     if distributed:
         gather_plane_tokens(tokens, ranges, rank, pt, group)
 

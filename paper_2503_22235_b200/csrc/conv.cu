@@ -278,28 +278,53 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
 // ---------------------------------------------------------------------------------------------
 // dst[img][h + 1][w + 1][c] = src[img * img_stride + (c / cdiv) * a_stride + (c % cdiv) * p_stride + h * W + w],
 // channels >= C zero; halo columns copied from the opposite edge, halo rows zero.
-__global__ void fields_to_nhwc_kernel(const float* __restrict__ src, long long img_stride, long long a_stride,
-                                      long long p_stride, int cdiv, int imgs, int C, int H, int W, int cp,
-                                      elem_t* __restrict__ dst) {
+// Tiled transpose: a block owns one padded row of one image and 32 padded columns; it reads each channel's 32
+// columns as one coalesced 128-byte run of the NCHW plane into shared memory, then writes the 32 NHWC pixels
+// (32 x cp contiguous operand elements) with consecutive threads on consecutive element pairs.  Values outside
+// the operand's finite range (|x| > 65504 for fp16, or non-finite) set *overflow (when non-null), so the host
+// can refuse the input instead of silently convolving infinities.
+constexpr int F2N_W = 32, F2N_THREADS = 256;
+__global__ void __launch_bounds__(F2N_THREADS) fields_to_nhwc_kernel(
+    const float* __restrict__ src, long long img_stride, long long a_stride, long long p_stride, int cdiv, int imgs,
+    int C, int H, int W, int cp, elem_t* __restrict__ dst, int* __restrict__ overflow) {
   griddep_launch_dependents();  // PDL: the next kernel may start its prologue
   griddep_wait();
-  const long long total = static_cast<long long>(imgs) * (H + 2) * (W + 2) * cp;
-  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int c = static_cast<int>(idx % cp);
-    long long rest = idx / cp;
-    const int pw = static_cast<int>(rest % (W + 2));
-    rest /= (W + 2);
-    const int ph = static_cast<int>(rest % (H + 2));
-    const int img = static_cast<int>(rest / (H + 2));
-    float v = 0.f;
-    if (c < C && ph >= 1 && ph <= H) {
-      const int h = ph - 1;
-      const int w = pw == 0 ? W - 1 : (pw == W + 1 ? 0 : pw - 1);
-      v = src[img * img_stride + (c / cdiv) * a_stride + (c % cdiv) * p_stride + static_cast<long long>(h) * W + w];
-    }
-    dst[idx] = to_elem(v);
+  __shared__ float tile[F2N_W][64 + 1];
+  const int ntw = (W + 2 + F2N_W - 1) / F2N_W;
+  const int pw0 = (blockIdx.x % ntw) * F2N_W;
+  const int ph = (blockIdx.x / ntw) % (H + 2);
+  const int img = blockIdx.x / (ntw * (H + 2));
+  const int tid = threadIdx.x, lane = tid & 31, ty = tid >> 5;
+  const int npix = min(F2N_W, W + 2 - pw0);
+  uint32_t* out = reinterpret_cast<uint32_t*>(dst + ((static_cast<size_t>(img) * (H + 2) + ph) * (W + 2) + pw0) * cp);
+  if (ph == 0 || ph == H + 1) {  // zero halo row
+    for (int e = tid; e < npix * cp / 2; e += F2N_THREADS) out[e] = 0u;
+    return;
   }
+  const int h = ph - 1;
+  const int pw = pw0 + lane;
+  const int wsrc = pw == 0 ? W - 1 : (pw == W + 1 ? 0 : pw - 1);
+  const float maxf = (kElemFmt == 0) ? 65504.f : 3.0e38f;
+  bool bad = false;
+  for (int cc = 0; cc < cp; cc += 64) {
+    for (int cl = ty; cl < 64; cl += F2N_THREADS / 32) {
+      const int c = cc + cl;
+      float v = 0.f;
+      if (c < C && lane < npix) {
+        v = __ldg(src + img * img_stride + (c / cdiv) * a_stride + (c % cdiv) * p_stride +
+                  static_cast<long long>(h) * W + wsrc);
+        bad |= !(fabsf(v) <= maxf);
+      }
+      tile[lane][cl] = v;
+    }
+    __syncthreads();
+    for (int e = tid; e < npix * 32; e += F2N_THREADS) {
+      const int wl = e >> 5, c2 = (e & 31) * 2;
+      out[(wl * cp + cc + c2) >> 1] = pack_elem(tile[wl][c2], tile[wl][c2 + 1]);
+    }
+    __syncthreads();
+  }
+  if (overflow != nullptr && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(overflow, 1);
 }
 
 // tokens fp32 [img][H][W][C] (C = hidden) -> padded bf16 NHWC with cp channels
@@ -407,14 +432,13 @@ extern "C" int wm3_conv(int mode, const void* in, int imgs, int hin, int win, in
 
 extern "C" int wm3_fields_to_nhwc(const float* src, long long img_stride, long long a_stride, long long p_stride,
                                   int chan_div, int imgs, int channels, int h, int w, int cp, void* dst,
-                                  void* stream) {
+                                  int* overflow, void* stream) {
   if (channels > cp || cp % 64) return set_error("wm3_fields_to_nhwc: bad channel padding");
-  const long long total = static_cast<long long>(imgs) * (h + 2) * (w + 2) * cp;
-  long long blocks = (total + 255) / 256;
-  if (blocks > 148LL * 64) blocks = 148LL * 64;
-  if (launch_pdl(fields_to_nhwc_kernel, dim3(static_cast<int>(blocks)), dim3(256), 0,
+  const long long blocks = static_cast<long long>(imgs) * (h + 2) * ((w + 2 + F2N_W - 1) / F2N_W);
+  if (blocks > 0x7fffffffLL) return set_error("wm3_fields_to_nhwc: too many images");
+  if (launch_pdl(fields_to_nhwc_kernel, dim3(static_cast<int>(blocks)), dim3(F2N_THREADS), 0,
                  reinterpret_cast<cudaStream_t>(stream), src, img_stride, a_stride, p_stride,
-                 chan_div > 0 ? chan_div : 1, imgs, channels, h, w, cp, reinterpret_cast<elem_t*>(dst)))
+                 chan_div > 0 ? chan_div : 1, imgs, channels, h, w, cp, reinterpret_cast<elem_t*>(dst), overflow))
     return -1;
   return check_launch("fields_to_nhwc_kernel");
 }

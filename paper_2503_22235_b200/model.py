@@ -22,7 +22,8 @@ from .errors import ConfigError
 from .grid import desk_grid, quarter_degree_grid, static_fields  # noqa: F401
 from .params import (available_sources, block_param_names, encoder_prefix, init_block_params,  # noqa: F401
                      init_model_params)
-from .pyramid import DecoderWeights, EncoderWeights, PyramidBuffers, decode_planes, encode_planes
+from .pyramid import (DecoderWeights, EncoderWeights, PyramidBuffers, check_input_range, decode_planes,
+                      encode_planes)
 from .runtime import CACHE
 from .tensor import Tensor, content_tag, host_array, host_values
 
@@ -219,6 +220,7 @@ def encode(state: WeatherState, params: dict, cfg: ModelConfig, source: str = PR
     bufs = dm.buffers()
     tokens = torch.empty((cfg.tokens, cfg.hidden), dtype=torch.float32, device="cuda")
     encode_planes(dm.encoder(prefix), bufs, cfg, tokens)
+    check_input_range(bufs)
     dm.run_blocks(tokens, [f"{prefix}.blk{i}" for i in range(cfg.enc_blocks)])
     return LatentState(Tensor(device=tokens), state.valid_time, cfg.latent_extents)
 

@@ -93,9 +93,20 @@ def run_conv(cw: ConvW, x: torch.Tensor, imgs: int, h: int, w: int, out: torch.T
 
 
 def fields_to_nhwc(src: torch.Tensor, imgs: int, channels: int, h: int, w: int, dst: torch.Tensor,
-                   img_stride: int, a_stride: int, p_stride: int, chan_div: int) -> None:
+                   img_stride: int, a_stride: int, p_stride: int, chan_div: int,
+                   overflow: torch.Tensor | None = None) -> None:
     check(_lib.lib().wm3_fields_to_nhwc(ptr(src), img_stride, a_stride, p_stride, chan_div, imgs, channels, h, w,
-                                        dst.shape[-1], ptr(dst), stream_ptr()), "wm3_fields_to_nhwc")
+                                        dst.shape[-1], ptr(dst), ptr(overflow), stream_ptr()), "wm3_fields_to_nhwc")
+
+
+def check_input_range(bufs: "PyramidBuffers") -> None:
+    """Raise ConfigError if the last encode_planes saw an input value the 16-bit operand type cannot hold
+    (|x| > 65504 for fp16, or a non-finite value): the reference accepts any float64 magnitude, the B200 path
+    refuses instead of convolving infinities.  One device->host read of a flag (synchronises the stream)."""
+    if int(bufs.overflow.item()):
+        lim = "65504 (fp16 operands)" if _lib.ELEM == torch.float16 else "the bf16 range"
+        raise ConfigError(f"input fields hold values beyond {lim} or non-finite values; standardise the fields "
+                          f"before encoding")
 
 
 def tokens_to_nhwc(tokens: torch.Tensor, imgs: int, h: int, w: int, dst: torch.Tensor) -> None:
@@ -159,6 +170,7 @@ class PyramidBuffers:
         self.in_sfc = nhwc(1, g.rows, g.cols, cfg.surface_in + N_STATIC_FIELDS, device)
         self.in_atm = nhwc(cfg.levels // cfg.level_patch, g.rows, g.cols, cfg.atmos_vars * cfg.level_patch, device)
         self.statics_ready = False
+        self.overflow = torch.zeros(1, dtype=torch.int32, device=device)  # fields_to_nhwc range flag
 
     def buf(self, level: int, k: int, c: int) -> torch.Tensor:
         b = self.levels[level][2][k]
@@ -200,13 +212,15 @@ def encode_planes(ew: EncoderWeights, bufs: PyramidBuffers, cfg: ModelConfig, to
     catm = cfg.atmos_vars * cfg.level_patch
     hw = hh * ww
     x0 = bufs.buf(0, 0, cfg.stem_channels)
+    bufs.overflow.zero_()
     if lo == 0:
-        fields_to_nhwc(bufs.sfc_in, 1, csfc, hh, ww, bufs.in_sfc, 0, hw, 0, 1)
+        fields_to_nhwc(bufs.sfc_in, 1, csfc, hh, ww, bufs.in_sfc, 0, hw, 0, 1, bufs.overflow)
         run_conv(ew.stem_sfc, bufs.in_sfc, 1, hh, ww, x0[0:1])
     a0 = max(lo, 1)
     if hi > a0:  # atmosphere level groups a0 - 1 .. hi - 2
         fields_to_nhwc(bufs.atm_in.view(-1)[(a0 - 1) * cfg.level_patch * hw:], hi - a0, catm, hh, ww,
-                       bufs.in_atm[a0 - 1:hi - 1], cfg.level_patch * hw, cfg.levels * hw, hw, cfg.level_patch)
+                       bufs.in_atm[a0 - 1:hi - 1], cfg.level_patch * hw, cfg.levels * hw, hw, cfg.level_patch,
+                       bufs.overflow)
         run_conv(ew.stem_atm, bufs.in_atm[a0 - 1:hi - 1], hi - a0, hh, ww, x0[a0:hi])
     x_idx, c = 0, cfg.stem_channels
     for i, st in enumerate(ew.stages):

@@ -85,9 +85,37 @@ def test_attention_weights_probe():
     got = _api().attention_weights(x, params, "blk", ext, win, heads)
     want = om.attention_weights(x, params, "blk", ext, win, heads)
     assert got.shape == (t, heads, 9)
-    np.testing.assert_allclose(got.sum(-1), 1.0, atol=1e-5)
+    np.testing.assert_allclose(got.sum(-1), 1.0, atol=2e-3)
     assert (got > 0).all()
-    assert np.abs(got - want).max() < 2e-2
+    assert np.abs(got - want).max() < 5e-3
+
+
+def _golden():
+    import json
+    import os
+    d = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    return json.load(open(os.path.join(d, "golden.json"))), np.load(os.path.join(d, "golden.npz"))
+
+
+@pytest.mark.parametrize("tag", ["b_2x7x10", "b_desk", "b_even", "b_mid"])
+def test_kernel_softmax_probabilities_match_reference(tag):
+    """The NA kernel's own softmax probabilities (read out with one-hot values, attention.attention_weights) vs
+    the reference's attention_weights (attention.py:187-212) stored by tests/golden/make_golden.py: every
+    window slot of every query and head, including bumped / wrapped / even windows."""
+    meta, arr = _golden()
+    case = next(c for c in meta["blocks"] if c["tag"] == tag)
+    if f"{tag}_attn" not in arr:
+        pytest.skip("no reference attention weights stored for this shape")
+    from paper_2503_22235_b200.params import init_block_params
+    ext, win, dim, heads = tuple(case["extents"]), tuple(case["window"]), case["dim"], case["heads"]
+    params = init_block_params(np.random.default_rng(case["param_seed"]), dim, heads, "blk", zero_residual=False)
+    x = np.random.default_rng(case["x_seed"]).standard_normal((int(np.prod(ext)), dim))
+    got = _api().attention_weights(x, params, "blk", ext, win, heads)
+    want = arr[f"{tag}_attn"].reshape(got.shape)
+    err = np.abs(got - want).max()
+    print(f"kernel P vs reference {tag}: max abs {err:.2e}, row-sum error {np.abs(got.sum(-1) - 1).max():.2e}")
+    assert err < 5e-3, err
+    assert np.abs(got.sum(-1) - 1.0).max() < 2e-3
 
 
 def test_block_errors_before_launch():
@@ -201,4 +229,4 @@ def test_locality_bitwise(ext, win):
         affected[p] = True
         changed = np.any(out != base, axis=1)
         assert not np.any(changed & ~affected), np.nonzero(changed & ~affected)[0][:10]
-        assert changed[affected].mean() > 0.9
+        assert changed[affected].all(), np.nonzero(affected & ~changed)[0][:10]

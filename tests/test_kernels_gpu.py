@@ -36,6 +36,22 @@ def test_neighbor_table_bit_exact(ext, win):
     assert np.array_equal(got, want)
 
 
+def test_neighbor_table_all_golden_cases():
+    """Every neighbor-table case the reference generated (tests/golden/make_golden.py: the 40-case sweep of the
+    reference's tests/test_grid.py:107-120 incl. even windows, plus the named shapes): sha256 of the int64 table
+    and token 0's neighbors, from the GPU kernel."""
+    import hashlib
+    import json
+    import os
+    meta = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden.json")))
+    assert len(meta["neighborhood"]) == 50
+    for case in meta["neighborhood"]:
+        got = ops().neighbor_table(tuple(case["extents"]), tuple(case["window"])).cpu().numpy()
+        assert list(got.shape) == case["shape"], case
+        assert hashlib.sha256(got.astype("<i8").tobytes()).hexdigest() == case["sha256"], case
+        assert got[0, :len(case["row0"])].tolist() == case["row0"], case
+
+
 def test_neighbor_table_full_scale_checksum():
     import hashlib
     got = ops().neighbor_table((5, 90, 180), (5, 7, 7)).cpu().numpy()
@@ -75,11 +91,16 @@ def test_gemm_epilogues():
     b = torch.randn(n, device="cuda", generator=g)
     ref = a.float() @ w.float().T + b
     L = lib()
+    # 16-bit outputs: one rounding of the fp32 result (2^-11 relative for fp16, 2^-8 for bf16) + accumulation
+    ulp = 2.0 ** -10 if L.ELEM == torch.float16 else 2.0 ** -7
     o1 = ops().linear(a, w, L.WM3_EPI_BIAS_BF16, bias=b)
-    assert (o1.float() - ref).abs().max().item() < 3e-2
+    assert ((o1.float() - ref).abs() <= ulp * ref.abs() + 2e-3).all()
     o2 = ops().linear(a, w, L.WM3_EPI_BIAS_GELU_BF16, bias=b)
     gel = 0.5 * ref * (1 + torch.erf(ref / math.sqrt(2)))
-    assert (o2.float() - gel).abs().max().item() < 3e-2
+    # + the fitted erf form (|err| <= 2.5e-5) and tanh.approx (2^-11 relative)
+    d = (o2.float() - gel).abs()
+    print(f"GELU epilogue: max abs {d.max().item():.2e}")
+    assert (d <= ulp * gel.abs() + 3e-3).all()
     x = torch.randn(m, n, device="cuda", generator=g)
     x0 = x.clone()
     ops().linear(a, w, L.WM3_EPI_BIAS_RESID_F32, bias=b, out=x)
@@ -135,7 +156,9 @@ def test_natten_matches_gather_reference(ext, win, heads, dhp):
     torch.cuda.synchronize()
     err = (out.float() - ref).abs().max().item()
     rel = ((out.float() - ref).norm() / ref.norm()).item()
-    assert rel < 1e-2 and err < 5e-2, (err, rel)
+    print(f"NA vs fp32 gather {ext} {win}: rel L2 {rel:.2e} max abs {err:.2e}")
+    # expected: fp16 P and output rounding, ~3e-4 relative; one wrong key per query (weight ~1/K) would be >1e-2
+    assert rel < 2e-3 and err < 1e-2, (err, rel)
 
 
 @pytest.mark.parametrize("ext,win,heads,dhp,batch", [
@@ -154,7 +177,7 @@ def test_natten_batched_members_equal_single(ext, win, heads, dhp, batch):
         assert torch.equal(out[b * t:(b + 1) * t], one), b
     ref, _ = na_reference(qkv[batch - 1].contiguous(), ext, heads, dhp, dhp, win)
     rel = ((out[(batch - 1) * t:].float() - ref).norm() / ref.norm()).item()
-    assert rel < 1e-2, rel
+    assert rel < 2e-3, rel
 
 
 def test_natten_windows_bit_exact():
@@ -209,4 +232,5 @@ def test_natten_both_mask_paths_match_reference(tile, monkeypatch):
     torch.cuda.synchronize()
     err = (out.float() - ref).abs().max().item()
     rel = ((out.float() - ref).norm() / ref.norm()).item()
-    assert rel < 1e-2 and err < 5e-2, (tile, err, rel)
+    print(f"NA tile {tile}: rel L2 {rel:.2e} max abs {err:.2e}")
+    assert rel < 2e-3 and err < 1e-2, (tile, err, rel)

@@ -193,3 +193,35 @@ def test_folded_layernorm_chain(monkeypatch):
     assert _rel(out.surface.values, base.surface.values) < 5e-3
     banded = forecast_banded(st, 7, folded, cfg, world=2)
     assert _rel(banded.surface.values, out.surface.values) < 5e-3
+
+
+@pytest.mark.parametrize("scale", [1e3, 1e5, float("nan")])
+def test_input_range_guard(scale):
+    """fp16 operands hold |x| <= 65504: inputs scaled by 1e3 (max ~5e3) still forecast within the one-step
+    tolerance of the float64 oracle on the same scaled input; 1e5 (beyond the fp16 range) and non-finite
+    inputs raise ConfigError from encode instead of convolving infinities (the reference accepts any float64
+    magnitude, fields_to_nhwc sets a device flag that encode checks)."""
+    m, r = _pkg()
+    from paper_2503_22235_b200.errors import ConfigError
+    cfg = m.desk_config()
+    params = m.init_model_params(cfg, seed=7, zero_residual=False)
+    st = _state(cfg, seed=9)
+    if np.isnan(scale):
+        st.atmos = st.atmos.copy()
+        st.atmos[1, 2, 3, 4] = np.nan
+    else:
+        st = m.WeatherState(0, st.surface * scale, st.atmos * scale)
+    if np.isnan(scale) or scale > 65504 / 8:
+        with pytest.raises(ConfigError):
+            m.encode(st, params, cfg)
+        with pytest.raises(ConfigError):
+            r.forecast(st, 6, params, cfg)
+        return
+    out = r.forecast(st, 6, params, cfg)
+    host = {k: v.values for k, v in params.items()}
+    ref_s, ref_a = om.forecast(st.surface, st.atmos, 6, host, cfg)
+    rel = per_variable_rel(out.surface.values, out.atmos.values, ref_s, ref_a)
+    worst = max(rel, key=rel.get)
+    print(f"inputs x{scale:g}: worst per-variable rel L2 {rel[worst]:.2e} ({worst})")
+    assert np.isfinite(out.surface.values).all() and np.isfinite(out.atmos.values).all()
+    assert rel[worst] < 1e-2, (worst, rel[worst])
