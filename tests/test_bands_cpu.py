@@ -287,6 +287,7 @@ def _forecast_worker(rank, world, port, out_q):
             def buffers(self):
                 class _B:
                     sfc_in = torch.zeros(1, dtype=torch.float32)
+                    overflow = torch.zeros(1, dtype=torch.int32)  # fields_to_nhwc range flag, never set here
                 return _B()
 
             def encoder(self, prefix):
