@@ -256,6 +256,94 @@ def roofline(per_ms: dict, tokens: int) -> tuple[dict, dict]:
     return roof, table
 
 
+def measure_config3(state, params, cfg, reps: int = 3) -> dict:
+    """BASELINE configs[2]: full 0.25 deg encode -> one 6 h processor application -> decode through the public API
+    (host page-locked fields in, host fields out), each part timed with CUDA events on the launching stream
+    (min over `reps`), plus every encoder / decoder conv launch timed individually (pyramid.CONV_HOOK events) with
+    its algorithmic FLOPs and fraction of the sustained tensor peak."""
+    import torch
+    from paper_2503_22235_b200 import model as M
+    from paper_2503_22235_b200 import pyramid as P
+    from paper_2503_22235_b200.config import conv_flops
+    peaks = load_peaks()
+    stream = torch.cuda.current_stream()
+    lat = M.encode(state, params, cfg)
+    lat6 = M.process(lat, params, cfg, 6)
+    dec = M.decode(lat6, params, cfg)
+    host = dec.to_host()
+    torch.cuda.synchronize()
+
+    def ev_time(fn):
+        best = None
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out = fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        return best, out
+
+    t_enc, lat = ev_time(lambda: M.encode(state, params, cfg))
+    t_proc, lat6 = ev_time(lambda: M.process(lat, params, cfg, 6))
+    t_dec, _ = ev_time(lambda: M.decode(lat6, params, cfg).to_host(host))
+    cf = conv_flops(cfg)
+    bf = block_flops(cfg.tokens)
+    fl = {"encode": cf["encode_conv"] + cfg.enc_blocks * bf, "process6": cfg.proc_blocks * bf,
+          "decode": cf["decode_conv"] + cfg.dec_blocks * bf}
+    parts = {}
+    for name, ms in (("encode", t_enc), ("process6", t_proc), ("decode", t_dec)):
+        tf = fl[name] / (ms / 1e3) / 1e12
+        parts[name] = {"ms": round(ms, 3), "tflop": round(fl[name] / 1e12, 3), "tflops": round(tf, 1),
+                       "frac_tc": round(tf / peaks["bf16_sustained"], 3)}
+    total_ms = t_enc + t_proc + t_dec
+    total_tf = sum(fl.values())
+
+    # per-conv launch times (one extra encode + decode with events around every conv launch)
+    layers, pending = [], []
+
+    def hook(cw, imgs, h, w, phase):
+        if phase == "begin":
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(stream)
+            pending.append((cw, imgs, h, w, ev))
+        else:
+            cw_, imgs_, h_, w_, e0 = pending.pop()
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(stream)
+            layers.append((cw_, imgs_, h_, w_, e0, e1))
+
+    P.CONV_HOOK = hook
+    try:
+        lat = M.encode(state, params, cfg)
+        n_enc = len(layers)
+        M.decode(lat, params, cfg)
+        torch.cuda.synchronize()
+    finally:
+        P.CONV_HOOK = None
+    rows = []
+    mode_name = {0: "3x3s1", 1: "3x3s2", 2: "4x4s2T"}
+    for i, (cw, imgs, h, w, e0, e1) in enumerate(layers):
+        ms = e0.elapsed_time(e1)
+        f = P.conv_layer_flops(cw, imgs, h, w)
+        ho, wo = (h, w) if cw.mode == 0 else ((h // 2, w // 2) if cw.mode == 1 else (2 * h, 2 * w))
+        tf = f / (ms / 1e3) / 1e12
+        rows.append({"part": "encode" if i < n_enc else "decode", "conv": mode_name[cw.mode], "imgs": imgs,
+                     "out_hw": [ho, wo], "cin": cw.cin, "cout": cw.cout, "ms": round(ms, 4),
+                     "gflop": round(f / 1e9, 1), "tflops": round(tf, 1),
+                     "frac_tc": round(tf / peaks["bf16_sustained"], 3)})
+    conv_ms = {p_: sum(r["ms"] for r in rows if r["part"] == p_) for p_ in ("encode", "decode")}
+    return {"workload": "full_scale_config encode -> process(6) -> decode, 720x1440, host fields in / out",
+            "parts": parts, "total_ms": round(total_ms, 3), "total_tflop": round(total_tf / 1e12, 2),
+            "total_tflops": round(total_tf / (total_ms / 1e3) / 1e12, 1),
+            "ideal_ms_sustained": round(total_tf / (peaks["bf16_sustained"] * 1e12) * 1e3, 2),
+            "conv_tflops": {p_: round(cf[f"{p_}_conv"] / (conv_ms[p_] / 1e3) / 1e12, 1) for p_ in conv_ms},
+            "conv_ms": {p_: round(v, 3) for p_, v in conv_ms.items()},
+            "conv_layers": rows}
+
+
 def run_forecast(args, world: int = 1) -> dict:
     """14-day 0.25 deg forecast through the public API, host fields in -> host fields out.  With N > 1 ranks
     the whole forecast is split (bands.forecast_banded): encoder / decoder pyramids by depth plane with
@@ -318,6 +406,11 @@ def run_forecast(args, world: int = 1) -> dict:
                      "exchange per block (bands.forecast_banded)",
            "note": "page-locked host float32 fields in, page-locked host float32 fields out "
                    "(DecodedFields.to_host); H2D/D2H inside the timed region"}
+    if world == 1:
+        try:
+            res["config3"] = measure_config3(state, params, cfg)
+        except Exception as exc:
+            res["config3"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if args.ensemble > 1:
         # config 5's ensemble: perturbed members, per-member encode / decode, one batched latent rollout; with
         # N ranks the members are sharded round-robin (independent replicas, no communication), time = max

@@ -190,6 +190,13 @@ int wm3_block_qkv(const float* x, const wm3_block_weights_t* w, const wm3_block_
 /* NA -> O-proj + residual -> LN2 -> W1 + GELU -> W2 + residual (halo rows of the K/V grid must be filled). */
 int wm3_block_rest(float* x, const wm3_block_weights_t* w, const wm3_block_ws_t* ws, const wm3_block_geom_t* g,
                    void* stream);
+/* The two halves of wm3_block_rest, for overlapping the halo exchange with attention: NA of the global query
+ * rows [q_lo, q_lo + q_rows) of the band into ws->ctx (wm3_natten_fwd_rows; rows whose windows stay inside the
+ * band need no halo), then everything after NA once every row's ctx is written. */
+int wm3_block_na_rows(const wm3_block_weights_t* w, const wm3_block_ws_t* ws, const wm3_block_geom_t* g, int q_lo,
+                      int q_rows, void* stream);
+int wm3_block_out(float* x, const wm3_block_weights_t* w, const wm3_block_ws_t* ws, const wm3_block_geom_t* g,
+                  void* stream);
 /* Both halves (a band without halos, or halos filled by the fused epilogue). */
 int wm3_block_fwd(float* x, const wm3_block_weights_t* w, const wm3_block_ws_t* ws, const wm3_block_geom_t* g,
                   const wm3_rope_t* rope, void* stream);
@@ -206,6 +213,13 @@ int wm3_block_fwd(float* x, const wm3_block_weights_t* w, const wm3_block_ws_t* 
 int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, int batch, int depth, int rows, int cols,
                    int rows_global, int row0, int halo_lo, int halo_hi, int heads, int dhp, int wd,
                    int wh, int ww, float scale, void* stream);
+/* wm3_natten_fwd restricted to the queries of global rows [q_lo, q_lo + q_rows) (inside the band); other rows of
+ * `out` are untouched.  Query tiles are aligned to global rows and a query's key chunks do not depend on the
+ * launch, so any split of the band's rows over several launches writes bitwise the bytes of one launch (and of
+ * the single-GPU launch): rows whose windows stay inside the band can run while the halo rows are in flight. */
+int wm3_natten_fwd_rows(const void* qkv, int ldqkv, void* out, int ldo, int batch, int depth, int rows, int cols,
+                        int rows_global, int row0, int halo_lo, int halo_hi, int heads, int dhp, int wd, int wh,
+                        int ww, float scale, int q_lo, int q_rows, void* stream);
 
 /* Implicit-GEMM convolutions of the encoder / decoder pyramids (model.py:296-325, autodiff.py:585-764).
  * Activations are 16-bit operand NHWC with a 1-pixel halo, [imgs][H + 2][W + 2][Cp] (Cp % 64 == 0): zero halo rows,

@@ -89,9 +89,13 @@ SIGNATURES = {
     "wm3_block_qkv": [_vp, ctypes.POINTER(BlockWeightsT), ctypes.POINTER(BlockWsT), ctypes.POINTER(BlockGeomT),
                       ctypes.POINTER(RopeT), ctypes.POINTER(HaloT), _vp],
     "wm3_block_rest": [_vp, ctypes.POINTER(BlockWeightsT), ctypes.POINTER(BlockWsT), ctypes.POINTER(BlockGeomT), _vp],
+    "wm3_block_na_rows": [ctypes.POINTER(BlockWeightsT), ctypes.POINTER(BlockWsT), ctypes.POINTER(BlockGeomT), _i, _i,
+                          _vp],
+    "wm3_block_out": [_vp, ctypes.POINTER(BlockWeightsT), ctypes.POINTER(BlockWsT), ctypes.POINTER(BlockGeomT), _vp],
     "wm3_block_fwd": [_vp, ctypes.POINTER(BlockWeightsT), ctypes.POINTER(BlockWsT), ctypes.POINTER(BlockGeomT),
                       ctypes.POINTER(RopeT), _vp],
     "wm3_natten_fwd": [_vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _f, _vp],
+    "wm3_natten_fwd_rows": [_vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _f, _i, _i, _vp],
     "wm3_natten_windows": [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp],
     "wm3_conv_bn": [_i],
     "wm3_conv": [_i, _vp, _i, _i, _i, _i, _vp, _i, _vp, _i, _vp, _i, _i, _vp, _i, _ll, _ll, _ll, _i, _vp],

@@ -71,19 +71,37 @@ def plan_bands(rows_global: int, window_rows: int, world: int) -> list[Band]:
     return bands
 
 
-class HaloExchanger:
-    """Fills the halo rows of a band's K/V grid buffer ([planes][halo_lo + rows + halo_hi][cols][C]) from the
-    neighbouring ranks.  Works on CUDA (NCCL) and CPU (gloo) tensors alike."""
+def interior_rows(band: Band, rows_global: int, window_rows: int) -> tuple[int, int]:
+    """Global query rows [a, b) of `band` whose bumped windows (grid.py:96-101) stay inside the band's own rows:
+    their attention needs no halo row, so it can run while the halo exchange is in flight (empty: a == b)."""
+    starts = bump_starts(rows_global, window_rows)
+    rows = [r for r in range(band.row0, band.row0 + band.rows)
+            if starts[r] >= band.row0 and starts[r] + window_rows <= band.row0 + band.rows]
+    return (rows[0], rows[-1] + 1) if rows else (band.row0, band.row0)
 
-    def __init__(self, bands: list[Band], rank: int, group=None):
+
+class HaloExchanger:
+    """Fills the halo rows of a band's K/V grid buffer ([planes][halo_lo + rows + halo_hi][cols][3 * sec]) from the
+    neighbouring ranks.  Only the K and V sections (columns [sec, 3 * sec)) travel: a neighbour's attention reads
+    keys and values of halo rows, never their queries.  Works on CUDA (NCCL) and CPU (gloo) tensors alike.
+
+    start() posts the sends / receives and returns at once (NCCL: the transfers run on NCCL's stream, ordered after
+    the work already queued on the current stream, i.e. the QKV GEMM); wait(handle) makes the current stream wait
+    for them (NCCL: a stream dependency, no host block) and copies the received rows into the halo.  Work queued
+    between the two — the attention of the band's interior rows — overlaps the exchange.  __call__ = both."""
+
+    def __init__(self, bands: list[Band], rank: int, group=None, sec: int | None = None):
         self.bands, self.rank, self.group = bands, rank, group
         self.me = bands[rank]
+        self.sec = sec  # first K column (heads * dhp); None: deduced as a third of the row width
 
-    def __call__(self, buf: torch.Tensor, grid) -> None:
+    def start(self, buf: torch.Tensor, grid):
         import torch.distributed as dist
         me = self.me
         planes = getattr(grid, "planes", grid.depth)  # batch * depth for an ensemble batch
         g = buf.view(planes, grid.rows_ext, grid.cols, -1)
+        c0 = self.sec if self.sec is not None else g.shape[-1] // 3
+        g = g[..., c0:]  # K and V sections
         # One message per neighbour and direction: the halo rows of every depth plane are packed into one
         # contiguous buffer (a strided copy) instead of one send per plane, so a block costs at most two sends
         # and two receives.  gloo moves host memory only: CUDA rows are staged through the host (multi-process
@@ -112,11 +130,33 @@ class HaloExchanger:
                 send(g[:, lo0 + me.rows - dn.halo_lo:lo0 + me.rows], me.rank + 1)
             if me.halo_hi:
                 recv(g[:, lo0 + me.rows:lo0 + me.rows + me.halo_hi], me.rank + 1)
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+        return reqs, post, stage
+
+    def wait(self, handle) -> None:
+        reqs, post, stage = handle
+        for req in reqs:
+            req.wait()
         for rows, tmp in post:
             rows.copy_(tmp, non_blocking=not stage)
+
+    def __call__(self, buf: torch.Tensor, grid) -> None:
+        self.wait(self.start(buf, grid))
+
+
+class CopyExchanger:
+    """HaloExchanger's interface over the bands one process holds (the N-rank emulation on one GPU): start()
+    copies the neighbouring bands' boundary rows (copy_halos, device copies on the current stream)."""
+
+    def __init__(self, bands: list[Band], workspaces: list):
+        self.bands, self.workspaces = bands, workspaces
+
+    def start(self, buf=None, grid=None):
+        copy_halos(self.bands, self.workspaces)
+        return None
+
+    def wait(self, handle) -> None:
+        return None
 
 
 def local_band_tokens(x_global: torch.Tensor, extents, band: Band) -> torch.Tensor:
@@ -262,7 +302,16 @@ class BandedProcessor:
 
     `held` are the bands this process computes: its own band under torch.distributed (exchange =
     HaloExchanger over NCCL / gloo), or every band when one process emulates the split on one GPU
-    (exchange = copy_halos).  Kernels never wait on one another either way."""
+    (exchange = copy_halos).  Kernels never wait on one another either way.
+
+    With a separate exchange (not fused) the attention is split by query rows (wm3_block_na_rows): the rows
+    whose windows stay inside the band run between starting the exchange and waiting for it, the boundary rows
+    after; attention query tiles are aligned to global rows, so the split changes no bit of the result.
+
+    graphs(): the blocks of each processor horizon captured once as a CUDA graph over processor-owned band
+    buffers (`buffers()`), replayed per step — on by default for the one-GPU emulation; for the NCCL exchange
+    opt-in (WM3_BAND_GRAPHS=1: NCCL point-to-point inside stream capture, not exercised on more than one GPU
+    here); never for PeerHalo, whose epoch flags are host-side counters."""
 
     def __init__(self, params: dict, cfg, bands: list[Band], held: list[int], exchanger=None, fused: bool = False):
         """fused: halo rows travel in the QKV GEMM epilogue (peer stores) instead of a separate exchange —
@@ -276,6 +325,10 @@ class BandedProcessor:
         d, h, w = cfg.latent_extents
         self.rope = CACHE.rope(cfg.latent_extents, cfg.head_dim)
         self.local = [(d, b.rows, w) for b in self.held]
+        self.interior = [interior_rows(b, h, cfg.window[1]) for b in self.held]
+        self._bufs = None
+        self._graphs: dict = {}
+        self.timing = None  # optional callback(name) between phases (bench: CUDA events per phase)
 
     def _ws(self, bw):
         from .runtime import CACHE
@@ -287,6 +340,43 @@ class BandedProcessor:
         """In place on the held bands' token buffers xs[i] ((d * rows_i * w, hidden) fp32, band order)."""
         self.run(xs, [f"proc{horizon}.blk{i}" for i in range(self.cfg.proc_blocks)])
 
+    # ---------------- CUDA graphs over processor-owned buffers ----------------
+    def graphs_supported(self) -> bool:
+        import os
+        if isinstance(self.exchanger, PeerHalo):
+            return False
+        if isinstance(self.exchanger, HaloExchanger):
+            return os.environ.get("WM3_BAND_GRAPHS", "0") == "1"
+        return True
+
+    def buffers(self) -> list[torch.Tensor]:
+        """The held bands' token buffers the captured graphs run on (allocated once)."""
+        if self._bufs is None:
+            d, _, w = self.cfg.latent_extents
+            self._bufs = [torch.zeros((d * b.rows * w, self.cfg.hidden), dtype=torch.float32, device="cuda")
+                          for b in self.held]
+        return self._bufs
+
+    def graph(self, horizon: int):
+        """The captured processor step of `horizon` over buffers() (warm-up and capture on the buffers'
+        current content: call before loading the latent)."""
+        g = self._graphs.get(horizon)
+        if g is None:
+            from .runtime import CACHE
+            bufs = self.buffers()
+            self.process(bufs, horizon)  # warm-up outside capture: weights, workspaces, kernel attributes
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.process(bufs, horizon)
+            # the graph holds raw device pointers: keep the captured weights alive with it
+            self._keep = getattr(self, "_keep", []) + [CACHE.block(self.params, f"proc{horizon}.blk{i}",
+                                                                   self.cfg.heads)
+                                                       for i in range(self.cfg.proc_blocks)]
+            self._graphs[horizon] = g
+        return g
+
+    # ---------------- the blocks ----------------
     def run(self, xs: list[torch.Tensor], prefixes) -> None:
         """The blocks named by `prefixes` (encoder, processor or decoder blocks) in order, in place on xs."""
         import ctypes
@@ -296,6 +386,7 @@ class BandedProcessor:
         cfg = self.cfg
         h = cfg.latent_extents[1]
         cols = cfg.latent_extents[2]
+        mark = self.timing if self.timing is not None else (lambda name: None)
         for bi, prefix in enumerate(prefixes):
             bw = CACHE.block(self.params, prefix, cfg.heads)
             wss = self._ws(bw)
@@ -308,6 +399,7 @@ class BandedProcessor:
                                      int(bi > 0))
                      for b, ext in zip(self.held, self.local)]
             local_grids = [GridGeo(w_.grid.rows_ext, w_.qkv.stride(0)) for w_ in wss]
+            mark("qkv")
             for j, (b, ext, xb, ws) in enumerate(zip(self.held, self.local, xs, wss)):
                 halo = None
                 if self.fused:
@@ -322,21 +414,46 @@ class BandedProcessor:
                                                     ctypes.byref(geoms[j]), ctypes.byref(rs),
                                                     None if halo is None else ctypes.byref(halo), _lib.stream_ptr()),
                            "wm3_block_qkv")
-            if peer is not None:
-                peer.after_qkv()
-            elif self.fused:
-                pass  # emulation: stream order already puts every band's halo stores before any attention
-            elif self.exchanger is not None:
-                for ws in wss:
-                    self.exchanger(ws.qkv, ws.grid)
+
+            def na_rows(j, lo, hi):
+                if hi > lo:
+                    _lib.check(_lib.lib().wm3_block_na_rows(ctypes.byref(bw.native()), ctypes.byref(wss[j].native()),
+                                                            ctypes.byref(geoms[j]), int(lo), int(hi - lo),
+                                                            _lib.stream_ptr()), "wm3_block_na_rows")
+
+            if self.fused:
+                if peer is not None:
+                    peer.after_qkv()
+                # emulation: stream order already puts every band's halo stores before any attention
+                mark("na")
+                for j, b in enumerate(self.held):
+                    na_rows(j, b.row0, b.row0 + b.rows)
             else:
-                copy_halos(self.held, wss)
-            for j, (b, xb, ws) in enumerate(zip(self.held, xs, wss)):
-                # attention -> O-proj -> LN2 -> MLP in one library call
-                _lib.check(_lib.lib().wm3_block_rest(xb.data_ptr(), ctypes.byref(bw.native()), ctypes.byref(ws.native()),
-                                                     ctypes.byref(geoms[j]), _lib.stream_ptr()), "wm3_block_rest")
+                exch = self.exchanger if self.exchanger is not None else CopyExchanger(self.held, wss)
+                mark("exchange_start")
+                handles = [exch.start(ws.qkv, ws.grid) for ws in wss] if self.exchanger is not None \
+                    else [exch.start()]
+                mark("na_interior")  # attention of rows that need no halo, overlapping the exchange
+                for j, (a, z) in enumerate(self.interior):
+                    na_rows(j, a, z)
+                mark("exchange_wait")
+                for hd in handles:
+                    exch.wait(hd)
+                mark("na_boundary")
+                for j, (b, (a, z)) in enumerate(zip(self.held, self.interior)):
+                    if z > a:
+                        na_rows(j, b.row0, a)
+                        na_rows(j, z, b.row0 + b.rows)
+                    else:
+                        na_rows(j, b.row0, b.row0 + b.rows)
+            mark("out")
+            for j, (xb, ws) in enumerate(zip(xs, wss)):
+                # O-proj -> LN2 -> MLP in one library call
+                _lib.check(_lib.lib().wm3_block_out(xb.data_ptr(), ctypes.byref(bw.native()), ctypes.byref(ws.native()),
+                                                    ctypes.byref(geoms[j]), _lib.stream_ptr()), "wm3_block_out")
                 if peer is not None:
                     peer.after_attention()  # neighbours may overwrite our halo rows for the next block
+            mark("end")
 
 
 def plane_ranges(depth: int, world: int) -> list[tuple[int, int]]:
@@ -353,29 +470,42 @@ def plane_ranges(depth: int, world: int) -> list[tuple[int, int]]:
     return out
 
 
+_PROCS: dict = {}
+
+
 def _banded_setup(params: dict, cfg, world, group, fused: bool, first_prefix: str):
-    """(processor, bands, rank, world, distributed) for a banded run; see rollout_banded."""
+    """(processor, bands, rank, world, distributed) for a banded run; see rollout_banded.  Processors (with
+    their exchangers, peer mappings and captured graphs) are cached per (params, cfg, split) and rebuilt when
+    the parameters' content tags change (as the single-GPU rollout graphs)."""
     import torch.distributed as dist
 
     from .model import device_model
-    device_model(params, cfg)
+    fp = getattr(device_model(params, cfg), "_fp", None)
     d, h, w = cfg.latent_extents
     distributed = world is None and dist.is_available() and dist.is_initialized() and \
         dist.get_world_size(group) > 1
     n = dist.get_world_size(group) if distributed else int(world or 1)
+    rank = dist.get_rank(group) if distributed else 0
+    dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
+    key = (id(params), cfg, n, bool(fused), distributed, rank, id(group), dev)
+    hit = _PROCS.get(key)
+    if hit is not None and hit[0] is params and hit[1] == fp:
+        return hit[2], hit[3], rank, n, distributed
     bands = plan_bands(h, cfg.window[1], n)
     if not distributed:
-        return BandedProcessor(params, cfg, bands, list(range(n)), fused=fused), bands, 0, n, False
-    rank = dist.get_rank(group)
-    if fused:
-        from .runtime import CACHE
-        me = bands[rank]
-        bw0 = CACHE.block(params, first_prefix, cfg.heads)
-        ws0 = CACHE.workspace((d, me.rows, w), cfg.window, bw0, halo=(me.halo_lo, me.halo_hi), tag=f"band{rank}")
-        exch = PeerHalo(bands, rank, ws0.qkv, ws0.grid, group)
+        proc = BandedProcessor(params, cfg, bands, list(range(n)), fused=fused)
     else:
-        exch = HaloExchanger(bands, rank, group)
-    return BandedProcessor(params, cfg, bands, [rank], exch, fused=fused), bands, rank, n, True
+        if fused:
+            from .runtime import CACHE
+            me = bands[rank]
+            bw0 = CACHE.block(params, first_prefix, cfg.heads)
+            ws0 = CACHE.workspace((d, me.rows, w), cfg.window, bw0, halo=(me.halo_lo, me.halo_hi), tag=f"band{rank}")
+            exch = PeerHalo(bands, rank, ws0.qkv, ws0.grid, group)
+        else:
+            exch = HaloExchanger(bands, rank, group)
+        proc = BandedProcessor(params, cfg, bands, [rank], exch, fused=fused)
+    _PROCS[key] = (params, fp, proc, bands)
+    return proc, bands, rank, n, distributed
 
 
 def _gather_latent(xs: list[torch.Tensor], bands: list[Band], extents, distributed: bool, group) -> torch.Tensor:
@@ -393,7 +523,8 @@ def _gather_latent(xs: list[torch.Tensor], bands: list[Band], extents, distribut
     return gather_bands(xs, extents, bands)
 
 
-def rollout_banded(lat, plan, params: dict, cfg, world: int | None = None, group=None, fused: bool = False):
+def rollout_banded(lat, plan, params: dict, cfg, world: int | None = None, group=None, fused: bool = False,
+                   graphs: bool | None = None):
     """rollout() with the latent split into latitude bands.
 
     Under an initialised torch.distributed group of size N > 1 (and world None): rank r keeps band r, halos
@@ -401,7 +532,9 @@ def rollout_banded(lat, plan, params: dict, cfg, world: int | None = None, group
     returns the full latent.  With `world` given and no group, one process emulates `world` bands on its GPU
     (the same kernels and halo rows; used to verify the split on one device).  fused=True moves the halo rows
     in the QKV GEMM epilogue (peer stores into the neighbours' K/V grids, PeerHalo epoch flags across ranks)
-    instead of a separate exchange.  Validation as rollout()."""
+    instead of a separate exchange.  graphs (default: plans of more than one step, where the split supports it,
+    BandedProcessor.graphs_supported): each horizon's step replayed as a CUDA graph, bitwise the eager result.
+    Validation as rollout()."""
     cfg = as_config(cfg)
     from .model import CALL_COUNTS, LatentState, latent_tokens
     from .rollout import _check_plan, plan_hours
@@ -413,10 +546,20 @@ def rollout_banded(lat, plan, params: dict, cfg, world: int | None = None, group
     x = latent_tokens(lat, cfg)
     proc, bands, rank, n, distributed = _banded_setup(params, cfg, world, group, fused, f"proc{plan[0]}.blk0")
     held = [bands[rank]] if distributed else bands
-    xs = [local_band_tokens(x, cfg.latent_extents, b).clone() for b in held]
-    for hz in plan:
-        proc.process(xs, hz)
-        CALL_COUNTS[f"process{hz}"] += 1
+    use_graphs = (len(plan) > 1 if graphs is None else bool(graphs)) and proc.graphs_supported()
+    if use_graphs:
+        steps = {hz: proc.graph(hz) for hz in sorted(set(plan))}  # warm-up / capture before the latent loads
+        xs = proc.buffers()
+        for xb, b in zip(xs, held):
+            xb.copy_(local_band_tokens(x, cfg.latent_extents, b))
+        for hz in plan:
+            steps[hz].replay()
+            CALL_COUNTS[f"process{hz}"] += 1
+    else:
+        xs = [local_band_tokens(x, cfg.latent_extents, b).clone() for b in held]
+        for hz in plan:
+            proc.process(xs, hz)
+            CALL_COUNTS[f"process{hz}"] += 1
     full = _gather_latent(xs, bands, cfg.latent_extents, distributed, group)
     return LatentState(Tensor(device=full), lat.valid_time + plan_hours(plan), tuple(lat.extents))
 
@@ -521,11 +664,21 @@ def forecast_banded(state, dt: int, params: dict, cfg, world: int | None = None,
 
     # latent blocks by latitude bands
     held = [bands[rank]] if distributed else bands
-    xs = [local_band_tokens(tokens, cfg.latent_extents, b).clone() for b in held]
+    steps = {}
+    if len(plan) > 1 and proc.graphs_supported():
+        steps = {hz: proc.graph(hz) for hz in sorted(set(plan))}  # capture before the latent loads
+        xs = proc.buffers()
+        for xb, b in zip(xs, held):
+            xb.copy_(local_band_tokens(tokens, cfg.latent_extents, b))
+    else:
+        xs = [local_band_tokens(tokens, cfg.latent_extents, b).clone() for b in held]
     del tokens
     proc.run(xs, enc_p)
     for hz in plan:
-        proc.process(xs, hz)
+        if steps:
+            steps[hz].replay()
+        else:
+            proc.process(xs, hz)
         CALL_COUNTS[f"process{hz}"] += 1
     proc.run(xs, dec_p)
     CALL_COUNTS["decode"] += 1

@@ -288,3 +288,27 @@ def shape_plan(cfg: ModelConfig) -> dict:
         "atmos_output": (cfg.atmos_vars, cfg.levels, g.rows, g.cols),
         "param_elements": n,
     }
+
+
+def conv_flops(cfg: ModelConfig) -> dict:
+    """Algorithmic FLOPs (2 x multiply-adds) of the encoder and decoder pyramids of one forecast, all depth planes
+    (model.py:296-325, 363-421): 3x3 convs 2 * P_out * Cout * 9 * Cin; the stride-2 transposed 4x4 conv
+    2 * P_out * Cout * 4 * Cin (each output pixel sees 2 x 2 taps); heads 192 -> surface_out (plane 0) and
+    -> atmos_vars * level_patch (level-group planes)."""
+    g = cfg.grid
+    groups = cfg.levels // cfg.level_patch
+    planes = 1 + groups
+    enc = 2.0 * g.rows * g.cols * cfg.stem_channels * 9 * ((cfg.surface_in + N_STATIC_FIELDS)
+                                                           + groups * cfg.atmos_vars * cfg.level_patch)
+    r, c, ci = g.rows, g.cols, cfg.stem_channels
+    for ch in cfg.stage_channels:
+        r, c = r // 2, c // 2
+        enc += planes * 2.0 * r * c * ch * 9 * (ci + 4 * ch)  # stride-2 down + two res blocks (2 convs each)
+        ci = ch
+    dec = 0.0
+    chans = [cfg.hidden] + list(cfg.stage_channels[-2::-1]) + [cfg.stem_channels]
+    for i in range(DOWNSAMPLE_STAGES):
+        r, c = r * 2, c * 2
+        dec += planes * 2.0 * r * c * chans[i + 1] * (4 * chans[i] + 4 * 9 * chans[i + 1])
+    dec += 2.0 * g.rows * g.cols * 9 * cfg.stem_channels * (cfg.surface_out + groups * cfg.atmos_vars * cfg.level_patch)
+    return {"encode_conv": enc, "decode_conv": dec}

@@ -81,15 +81,27 @@ extern "C" int wm3_block_qkv(const float* x, const wm3_block_weights_t* w, const
                            g->halo_lo * g->cols, stream);
 }
 
+extern "C" int wm3_block_na_rows(const wm3_block_weights_t* w, const wm3_block_ws_t* ws, const wm3_block_geom_t* g,
+                                 int q_lo, int q_rows, void* stream) {
+  if (w == nullptr || ws == nullptr || g == nullptr) return set_error("wm3_block_na_rows: null argument");
+  const int hd = w->heads * w->dhp;
+  return wm3_natten_fwd_rows(ws->qkv, 3 * hd, ws->ctx, hd, g->batch, g->depth, g->rows, g->cols, g->rows_global,
+                             g->row0, g->halo_lo, g->halo_hi, w->heads, w->dhp, g->wd, g->wh, g->ww,
+                             1.0f / std::sqrt(static_cast<float>(w->dh)), q_lo, q_rows, stream);
+}
+
 extern "C" int wm3_block_rest(float* x, const wm3_block_weights_t* w, const wm3_block_ws_t* ws,
                               const wm3_block_geom_t* g, void* stream) {
   if (check_block(x, w, ws, g)) return -1;
+  if (wm3_block_na_rows(w, ws, g, g->row0, g->rows, stream)) return -1;
+  return wm3_block_out(x, w, ws, g, stream);
+}
+
+extern "C" int wm3_block_out(float* x, const wm3_block_weights_t* w, const wm3_block_ws_t* ws,
+                             const wm3_block_geom_t* g, void* stream) {
+  if (check_block(x, w, ws, g)) return -1;
   const int t = g->batch * g->depth * g->rows * g->cols;
   const int hd = w->heads * w->dhp;
-  if (wm3_natten_fwd(ws->qkv, 3 * hd, ws->ctx, hd, g->batch, g->depth, g->rows, g->cols, g->rows_global, g->row0,
-                     g->halo_lo, g->halo_hi, w->heads, w->dhp, g->wd, g->wh, g->ww,
-                     1.0f / std::sqrt(static_cast<float>(w->dh)), stream))
-    return -1;
   if (w->w_qkv_f != nullptr) {
     const wm3_ln_fold_t prod = fold_producer(w, ws), cons = fold_consumer(ws, w->c_1);
     if (wm3_linear_fold(ws->ctx, hd, w->w_o, hd, t, w->np, hd, WM3_EPI_BIAS_RESID_F32, x, w->hidden, w->hidden,

@@ -60,7 +60,8 @@ struct NaParams {
   int depth, rows, cols, rows_global, row0, halo_lo, rows_ext;
   int heads, dhp, wd, wh, ww;
   int TD, TH, TW, ntd, nth, ntw, nitems;
-  int th_first;   // first global row tile the band touches (tiles are aligned to global rows, see tile_geo)
+  int th_first;   // first global row tile the launch touches (tiles are aligned to global rows, see tile_geo)
+  int q_lo, q_hi;  // global query rows this launch computes and stores: [q_lo, q_hi) within the band
   int ncp, nrpc;  // key-chunk box: ncp columns x nrpc rows (fixed for every tile)
   float scale_log2;
   const uint8_t* bias_table;  // BIAS: [tile][maxch] B_x images (4 KB each), built once per geometry
@@ -457,8 +458,8 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
       const int qd = g.d0 + row / (p.TH * p.TW);
       const int qh = g.h0 + (row / p.TW) % p.TH;  // global row
       const int qw = g.w0 + row % p.TW;
-      const bool qvalid = row < p.TD * p.TH * p.TW && qd < g.d1 && qh < g.h1 && qh >= p.row0 &&
-                          qh < p.row0 + p.rows && qw < g.w1;
+      const bool qvalid = row < p.TD * p.TH * p.TW && qd < g.d1 && qh < g.h1 && qh >= p.q_lo &&
+                          qh < p.q_hi && qw < g.w1;
       const int q_sd = bump_start(qvalid ? qd : g.d0, p.depth, p.wd);
       const int q_sh = bump_start(qvalid ? qh : g.h0, p.rows_global, p.wh);
       // window columns in patch coordinates: [c_lo, c_lo + ww), taken mod W for a full-circle patch
@@ -672,15 +673,18 @@ static void choose_tile(int depth, int cols, int rows_global, int wd, int wh, in
 
 using namespace wm3;
 
-extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, int batch, int depth, int rows, int cols,
-                              int rows_global, int row0, int halo_lo, int halo_hi, int heads, int dhp, int wd, int wh,
-                              int ww, float scale, void* stream) {
+static int natten_launch(const void* qkv, int ldqkv, void* out, int ldo, int batch, int depth, int rows, int cols,
+                         int rows_global, int row0, int halo_lo, int halo_hi, int heads, int dhp, int wd, int wh,
+                         int ww, float scale, int q_lo, int q_rows, void* stream) {
   if (dhp != 64 && dhp != 128) return set_error("wm3_natten_fwd: dhp must be 64 or 128 (got %d)", dhp);
   if (batch < 1) return set_error("wm3_natten_fwd: batch must be >= 1 (got %d)", batch);
   if (wd > depth || wh > rows_global || ww > cols) return set_error("wm3_natten_fwd: window exceeds extents");
   if (ww > 64) return set_error("wm3_natten_fwd: col window %d > 64 unsupported", ww);
   if (row0 < 0 || row0 + rows > rows_global || halo_lo > row0 || row0 + rows + halo_hi > rows_global)
     return set_error("wm3_natten_fwd: bad band rows");
+  if (q_rows < 1 || q_lo < row0 || q_lo + q_rows > row0 + rows)
+    return set_error("wm3_natten_fwd: query rows [%d, %d) outside the band [%d, %d)", q_lo, q_lo + q_rows, row0,
+                     row0 + rows);
   // the halo must cover every window that reaches outside the band
   if (rows < rows_global) {
     const int need_lo = row0 - bump_start(row0, rows_global, wh);
@@ -713,8 +717,10 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
     }
   }
   p.ntd = (depth + p.TD - 1) / p.TD;
-  p.th_first = row0 / p.TH;
-  p.nth = (row0 + rows - 1) / p.TH - p.th_first + 1;
+  p.q_lo = q_lo;
+  p.q_hi = q_lo + q_rows;
+  p.th_first = q_lo / p.TH;
+  p.nth = (p.q_hi - 1) / p.TH - p.th_first + 1;
   p.ntw = (cols + p.TW - 1) / p.TW;
   p.nitems = p.ntd * p.nth * p.ntw * heads * batch;
   p.scale_log2 = scale * 1.4426950408889634f;
@@ -747,18 +753,19 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
     p.maxch = p.wd + p.TD - 1;  // depth planes of a tile's key patch ...
     p.maxch = (p.maxch < depth ? p.maxch : depth) * ((p.wh + p.TH - 1 + p.nrpc - 1) / p.nrpc) * 2;  // x row chunks x parts
     struct Key {
-      int dev, depth, rows, cols, rows_global, row0, wd, wh, ww, TD, TH, TW, ncp, nrpc;
+      // the images depend on the launch's global tile rows only (not on the band or its halos)
+      int dev, depth, cols, rows_global, th_first, nth, wd, wh, ww, TD, TH, TW, ncp, nrpc;
       bool operator<(const Key& o) const {
-        return std::tie(dev, depth, rows, cols, rows_global, row0, wd, wh, ww, TD, TH, TW, ncp, nrpc) <
-               std::tie(o.dev, o.depth, o.rows, o.cols, o.rows_global, o.row0, o.wd, o.wh, o.ww, o.TD, o.TH, o.TW,
-                        o.ncp, o.nrpc);
+        return std::tie(dev, depth, cols, rows_global, th_first, nth, wd, wh, ww, TD, TH, TW, ncp, nrpc) <
+               std::tie(o.dev, o.depth, o.cols, o.rows_global, o.th_first, o.nth, o.wd, o.wh, o.ww, o.TD, o.TH,
+                        o.TW, o.ncp, o.nrpc);
       }
     };
     static std::map<Key, uint8_t*> tables;
     static std::mutex mu;
     int dev = 0;
     cudaGetDevice(&dev);
-    const Key key{dev, depth, rows, cols, rows_global, row0, wd, wh, ww, p.TD, p.TH, p.TW, p.ncp, p.nrpc};
+    const Key key{dev, depth, cols, rows_global, p.th_first, p.nth, wd, wh, ww, p.TD, p.TH, p.TW, p.ncp, p.nrpc};
     std::lock_guard<std::mutex> lock(mu);
     auto it = tables.find(key);
     if (it == tables.end()) {
@@ -798,6 +805,20 @@ extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, in
                  tkv, p))
     return -1;
   return check_launch("natten_fwd_kernel");
+}
+
+extern "C" int wm3_natten_fwd(const void* qkv, int ldqkv, void* out, int ldo, int batch, int depth, int rows, int cols,
+                              int rows_global, int row0, int halo_lo, int halo_hi, int heads, int dhp, int wd, int wh,
+                              int ww, float scale, void* stream) {
+  return natten_launch(qkv, ldqkv, out, ldo, batch, depth, rows, cols, rows_global, row0, halo_lo, halo_hi, heads,
+                       dhp, wd, wh, ww, scale, row0, rows, stream);
+}
+
+extern "C" int wm3_natten_fwd_rows(const void* qkv, int ldqkv, void* out, int ldo, int batch, int depth, int rows,
+                                   int cols, int rows_global, int row0, int halo_lo, int halo_hi, int heads, int dhp,
+                                   int wd, int wh, int ww, float scale, int q_lo, int q_rows, void* stream) {
+  return natten_launch(qkv, ldqkv, out, ldo, batch, depth, rows, cols, rows_global, row0, halo_lo, halo_hi, heads,
+                       dhp, wd, wh, ww, scale, q_lo, q_rows, stream);
 }
 
 extern "C" int wm3_natten_windows(int depth, int rows, int cols, int rows_global, int row0, int wd, int wh, int ww,

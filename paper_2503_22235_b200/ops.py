@@ -172,8 +172,10 @@ def linear_grid(a: torch.Tensor, w: torch.Tensor, epi: int, bias: torch.Tensor, 
 
 
 def natten(qkv: torch.Tensor, grid: KVGrid, heads: int, dhp: int, dh: int, window,
-           out: torch.Tensor | None = None, rows_global: int | None = None, row0: int = 0) -> torch.Tensor:
-    """Fused neighborhood attention over the padded qkv grid -> ctx (T, heads*dhp) bf16, band token order."""
+           out: torch.Tensor | None = None, rows_global: int | None = None, row0: int = 0,
+           q_rows: tuple[int, int] | None = None) -> torch.Tensor:
+    """Fused neighborhood attention over the padded qkv grid -> ctx (T, heads*dhp) bf16, band token order.
+    q_rows = (lo, hi): only the queries of global rows [lo, hi) (wm3_natten_fwd_rows; other rows untouched)."""
     _req(qkv, _lib.ELEM, "qkv")
     if qkv.shape[0] != grid.tokens:
         raise RuntimeError(f"qkv has {qkv.shape[0]} rows, padded grid needs {grid.tokens}")
@@ -184,6 +186,13 @@ def natten(qkv: torch.Tensor, grid: KVGrid, heads: int, dhp: int, dh: int, windo
     if out is None:
         out = torch.empty((t, heads * dhp), dtype=_lib.ELEM, device=qkv.device)
     _req(out, _lib.ELEM, "out")
+    if q_rows is not None:
+        lo, hi = int(q_rows[0]), int(q_rows[1])
+        check(_lib.lib().wm3_natten_fwd_rows(ptr(qkv), qkv.stride(0), ptr(out), out.stride(0), grid.batch, d, h, w, rg,
+                                             int(row0), grid.halo_lo, grid.halo_hi, int(heads), int(dhp), wd, wh, ww,
+                                             float(1.0 / math.sqrt(dh)), lo, hi - lo, stream_ptr()),
+              "wm3_natten_fwd_rows")
+        return out
     check(_lib.lib().wm3_natten_fwd(ptr(qkv), qkv.stride(0), ptr(out), out.stride(0), grid.batch, d, h, w, rg,
                                     int(row0),
                                     grid.halo_lo, grid.halo_hi, int(heads), int(dhp), wd, wh, ww,

@@ -78,6 +78,20 @@ def nhwc(imgs: int, h: int, w: int, c: int, device="cuda") -> torch.Tensor:
     return torch.zeros((imgs, h + 2, w + 2, cpad(c)), dtype=_lib.ELEM, device=device)
 
 
+# Measurement hook (bench.py / tools/encdec_roofline.py): when set, called as hook(cw, imgs, h, w, phase) with
+# phase "begin" / "end" around every conv launch on the current stream (e.g. to record CUDA events).
+CONV_HOOK = None
+
+
+def conv_layer_flops(cw: ConvW, imgs: int, h: int, w: int) -> float:
+    """Algorithmic FLOPs of one run_conv call (h, w = input extents as passed to run_conv)."""
+    if cw.mode == _lib.WM3_CONV_S1:
+        return 2.0 * imgs * h * w * cw.cout * 9 * cw.cin
+    if cw.mode == _lib.WM3_CONV_S2:
+        return 2.0 * imgs * (h // 2) * (w // 2) * cw.cout * 9 * cw.cin
+    return 2.0 * imgs * (2 * h) * (2 * w) * cw.cout * 4 * cw.cin
+
+
 def run_conv(cw: ConvW, x: torch.Tensor, imgs: int, h: int, w: int, out: torch.Tensor, *, gelu: bool = False,
              resid: torch.Tensor | None = None, kind: int = _lib.WM3_CONV_OUT_NHWC, img_stride: int = 0,
              a_stride: int = 0, p_stride: int = 0, chan_div: int = 1) -> torch.Tensor:
@@ -86,9 +100,13 @@ def run_conv(cw: ConvW, x: torch.Tensor, imgs: int, h: int, w: int, out: torch.T
         raise RuntimeError(f"conv input has {x.shape[-1]} channels, weights expect {cw.cinp}")
     out_cp = out.shape[-1] if kind == _lib.WM3_CONV_OUT_NHWC else 0
     resid_cp = resid.shape[-1] if resid is not None else 0
+    if CONV_HOOK is not None:
+        CONV_HOOK(cw, imgs, h, w, "begin")
     check(_lib.lib().wm3_conv(cw.mode, ptr(x), imgs, h, w, cw.cinp, ptr(cw.w), cw.cout, ptr(cw.b), int(gelu),
                               ptr(resid), resid_cp, kind, ptr(out), out_cp, img_stride, a_stride, p_stride,
                               chan_div, stream_ptr()), "wm3_conv")
+    if CONV_HOOK is not None:
+        CONV_HOOK(cw, imgs, h, w, "end")
     return out
 
 

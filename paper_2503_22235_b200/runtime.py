@@ -82,7 +82,8 @@ def invalidate_params() -> None:
     caller's current arrays.  Needed only after a sparse in-place write into a large parameter array, which
     the content sample of tensor.content_tag may miss."""
     CACHE.clear()
-    from . import model, rollout
+    from . import bands, model, rollout
     with model._mlock:
         model._models.clear()
     rollout._ROLLOUTS.clear()
+    bands._PROCS.clear()

@@ -66,6 +66,10 @@ def _band_attention(q, k, v, ext, win, band, heads):
 
 
 def _worker(rank, world, port, ext, win, heads, out_q):
+    """Overlapped exchange as BandedProcessor runs it: start() -> attention of the band's interior rows (whose
+    windows need no halo: the halo rows are still NaN here, so any use would poison the result) -> wait() ->
+    attention of the boundary rows.  Only the K and V sections travel (the Q columns of halo rows stay NaN)."""
+    from paper_2503_22235_b200.bands import interior_rows
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -78,18 +82,34 @@ def _worker(rank, world, port, ext, win, heads, out_q):
         bands = plan_bands(h, win[1], world)
         me = bands[rank]
         grid = KVGrid((d, me.rows, w), win, me.halo_lo, me.halo_hi)
-        # this rank's K/V grid: only its own rows are filled, halos start as NaN
-        kv = np.concatenate([k, v], axis=1).reshape(d, h, w, -1)
-        buf = torch.full((grid.tokens, 2 * c), float("nan"), dtype=torch.float64)
+        # this rank's q/k/v grid: only its own rows are filled, halos start as NaN
+        qkv = np.concatenate([q, k, v], axis=1).reshape(d, h, w, -1)
+        buf = torch.full((grid.tokens, 3 * c), float("nan"), dtype=torch.float64)
         g = buf.view(d, grid.rows_ext, w, -1)
-        g[:, me.halo_lo:me.halo_lo + me.rows] = torch.from_numpy(kv[:, me.row0:me.row0 + me.rows])
-        HaloExchanger(bands, rank)(buf, grid)
+        g[:, me.halo_lo:me.halo_lo + me.rows] = torch.from_numpy(qkv[:, me.row0:me.row0 + me.rows])
+        exch = HaloExchanger(bands, rank, sec=c)
+        handle = exch.start(buf, grid)
+        a, z = interior_rows(me, h, win[1])
+
+        def attend(rows_lo, rows_hi):
+            kb = g.numpy().reshape(-1, 3 * c)
+            out = _band_attention(np.zeros((d * me.rows * w, c)) + q.reshape(d, h, w, c)[
+                :, me.row0:me.row0 + me.rows].reshape(-1, c), kb[:, c:2 * c], kb[:, 2 * c:], ext, win, me, heads)
+            out = out.reshape(d, me.rows, w, c)
+            return out[:, rows_lo - me.row0:rows_hi - me.row0]
+
+        interior = attend(a, z)  # before wait(): halo rows are NaN
+        exch.wait(handle)
+        full = attend(me.row0, me.row0 + me.rows)
+        got = full.copy()
+        got[:, a - me.row0:z - me.row0] = interior
         lo, hi = me.row0 - me.halo_lo, me.row0 + me.rows + me.halo_hi
-        ok_halo = np.array_equal(g.numpy(), kv[:, lo:hi])
-        kb = g.numpy().reshape(-1, 2 * c)
-        qb = q.reshape(d, h, w, c)[:, me.row0:me.row0 + me.rows].reshape(-1, c)
-        got = _band_attention(qb, kb[:, :c], kb[:, c:], ext, win, me, heads)
-        out_q.put((rank, ok_halo, got))
+        gn = g.numpy()
+        own = slice(me.halo_lo, me.halo_lo + me.rows)
+        ok_halo = (np.array_equal(gn[..., c:], qkv[:, lo:hi, :, c:])              # K / V halo rows filled
+                   and np.array_equal(gn[:, own], qkv[:, me.row0:me.row0 + me.rows])
+                   and np.isnan(np.delete(gn[..., :c], np.arange(own.start, own.stop), axis=1)).all())  # Q not sent
+        out_q.put((rank, ok_halo and np.isfinite(interior).all(), got.reshape(-1, c)))
     finally:
         dist.destroy_process_group()
 
@@ -132,6 +152,9 @@ class _FakeProcessor:
     def __init__(self, params, cfg, bands, held, exchanger=None, fused=False):
         self.held = [bands[i] for i in held]
         self.ext = cfg.latent_extents
+
+    def graphs_supported(self):
+        return False
 
     def process(self, xs, horizon):
         d, h, w = self.ext

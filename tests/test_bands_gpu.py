@@ -275,3 +275,49 @@ def test_forecast_banded_matches_forecast(name, world):
         assert torch.equal(one.atmos.device, banded.atmos.device), dt
     with pytest.raises(m.ConfigError):
         forecast_banded(st, cfg.max_dt + 1, params, cfg, world=world)
+
+
+def test_natten_row_split_bitwise():
+    """wm3_natten_fwd_rows: the band's query rows computed in several launches (interior rows first, as while
+    the halo exchange is in flight, then the boundary rows) write bitwise the bytes of one launch."""
+    from paper_2503_22235_b200 import _lib, ops
+    from paper_2503_22235_b200.bands import interior_rows, plan_bands
+    ext, win, heads, dhp = (5, 90, 180), (5, 7, 7), 8, 128
+    d, h, w = ext
+    C = 3 * heads * dhp
+    g = torch.Generator(device="cuda").manual_seed(5)
+    qkv = (torch.randn(d * h * w, C, device="cuda", generator=g) * 1.5).to(_lib.ELEM)
+    g3 = qkv.view(d, h, w, C)
+    for b in plan_bands(h, win[1], 8)[:3] + [plan_bands(h, win[1], 1)[0]]:
+        grid = ops.KVGrid((d, b.rows, w), win, b.halo_lo, b.halo_hi)
+        buf = g3[:, b.row0 - b.halo_lo:b.row0 + b.rows + b.halo_hi].reshape(-1, C).contiguous()
+        one = ops.natten(buf, grid, heads, dhp, dhp, win, rows_global=h, row0=b.row0)
+        a, z = interior_rows(b, h, win[1])
+        split = torch.full_like(one, float("nan"))
+        for lo, hi in ((a, z), (b.row0, a), (z, b.row0 + b.rows)):
+            if hi > lo:
+                ops.natten(buf, grid, heads, dhp, dhp, win, out=split, rows_global=h, row0=b.row0, q_rows=(lo, hi))
+        assert torch.equal(split, one), b
+
+
+@pytest.mark.parametrize("name,world", [("mid", 2), ("desk", 2)])
+def test_banded_rollout_graphs_bitwise(name, world):
+    """rollout_banded with every horizon's step captured as a CUDA graph (processor-owned band buffers, the
+    overlapped interior / boundary attention and the halo copies inside the graph) is bitwise the eager banded
+    rollout and the single-GPU rollout; a second call replays the cached graphs."""
+    import paper_2503_22235_b200.model as m
+    import paper_2503_22235_b200.rollout as r
+    from paper_2503_22235_b200.bands import rollout_banded
+    cfg = {"desk": m.desk_config, "mid": m.mid_config}[name]()
+    params = m.init_model_params(cfg, seed=11, zero_residual=False)
+    rng = np.random.default_rng(6)
+    g = cfg.grid
+    st = m.WeatherState(0, rng.standard_normal((cfg.surface_in, g.rows, g.cols)),
+                        rng.standard_normal((cfg.atmos_vars, cfg.levels, g.rows, g.cols)))
+    lat = m.encode(st, params, cfg)
+    plan = (6, 6, 1)
+    one = r.rollout(lat, plan, params, cfg).tokens.device
+    eager = rollout_banded(lat, plan, params, cfg, world=world, graphs=False).tokens.device
+    graphed = rollout_banded(lat, plan, params, cfg, world=world, graphs=True).tokens.device
+    again = rollout_banded(lat, plan, params, cfg, world=world, graphs=True).tokens.device
+    assert torch.equal(eager, one) and torch.equal(graphed, one) and torch.equal(again, one)
