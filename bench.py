@@ -222,15 +222,18 @@ def load_traffic() -> dict:
         return {}
 
 
-def roofline(per_ms: dict, tokens: int) -> tuple[dict, dict]:
+def roofline(per_ms: dict, tokens: int, traffic: bool = True) -> tuple[dict, dict]:
+    """traffic=False (N > 1: band-sized kernels): no ncu DRAM bytes — the committed capture is of the
+    full-domain kernels and does not describe a band's launch."""
     T, D, K = tokens, DIM, int(np.prod(WIN))
     kflops = {"qkv_rope_gemm": 6.0 * T * D * D, "oproj_resid_gemm": 2.0 * T * D * D, "w1_gelu_gemm": 8.0 * T * D * D,
-              "w2_resid_gemm": 8.0 * T * D * D, "natten": 4.0 * T * K * D}
+              "w2_resid_gemm": 8.0 * T * D * D, "natten": 4.0 * T * K * D,
+              "qkv": 6.0 * T * D * D, "out": 18.0 * T * D * D}
     # algorithmic bytes: LN reads fp32 x and writes the 2-byte operand; NA reads q, k, v and writes ctx
     kbytes = {"layernorm1": T * D * 6.0, "layernorm2": T * D * 6.0, "natten": T * D * 2 * 4.0}
     peaks = load_peaks()
-    traffic = load_traffic()
-    top = max(per_ms, key=per_ms.get)
+    traffic = load_traffic() if traffic else {}
+    top = max((n for n in per_ms if n in kflops or n in kbytes), key=per_ms.get)
     if top in kflops:
         ach = kflops[top] / (per_ms[top] / 1e3) / 1e12
         roof = {"kernel": top, "bound": "tensor", "achieved": ach, "peak": peaks["bf16_sustained"],
@@ -469,6 +472,9 @@ def run_gpu(args, world, rank, local_rank):
     torch.cuda.set_device(device)
     if world > 1:
         if backend == "nccl":
+            # communicator lines in the log (ranks, NVLS / NVLink transport) for the scaling run
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", device))
         else:
             dist.init_process_group(backend)
@@ -476,6 +482,24 @@ def run_gpu(args, world, rank, local_rank):
 
     params, bw, me, local, ws, rope, exch, x = block_setup(world, rank)
     stream = torch.cuda.current_stream()
+    if world > 1:
+        # the banded block as the forecast runs it: BandedProcessor (attention split by query rows, the interior
+        # rows overlapping the NCCL halo exchange), with CUDA events between its phases
+        from paper_2503_22235_b200.bands import BandedProcessor, plan_bands
+        from paper_2503_22235_b200.model import full_scale_config
+        cfg = full_scale_config()
+        assert cfg.latent_extents == EXT and cfg.window == WIN and cfg.hidden == DIM and cfg.heads == HEADS
+        bands = plan_bands(EXT[1], WIN[1], world)
+        proc = BandedProcessor(params, cfg, bands, [rank], exch)
+        xs = [x]
+        phases = ["qkv", "exchange_start", "na_interior", "exchange_wait", "na_boundary", "out", "end"]
+        pmarks = []
+
+        def pmark(name):
+            if pmarks and name in pmarks[-1]:
+                pmarks[-1][name].record(stream)
+
+        proc.timing = pmark
 
     # per-launch CUDA events recorded on the launching stream inside the timed steps (kernel durations for
     # the roofline are these, averaged over the timed region)
@@ -492,6 +516,9 @@ def run_gpu(args, world, rank, local_rank):
     prepped = [False]
 
     def step():
+        if world > 1:
+            proc.run(xs, ["blk"])
+            return
         block_forward(x, bw, ws, rope, local, WIN, row0=me.row0, rows_global=EXT[1], halo_exchange=exch, mark=mark,
                       prepped=prepped[0])
         prepped[0] = bw.folded
@@ -504,6 +531,8 @@ def run_gpu(args, world, rank, local_rank):
 
     def timed_step():
         cursor[0] = next(it)
+        if world > 1:
+            pmarks.append({n: torch.cuda.Event(enable_timing=True) for n in phases})
         step()
 
     ms = timed(timed_step, args.steps, stream, world)
@@ -511,12 +540,21 @@ def run_gpu(args, world, rank, local_rank):
     flops = block_flops(int(np.prod(EXT)))
     value = flops * args.steps / (ms / 1e3) / 1e12
 
-    per_ms = {n: sum(ev[i].elapsed_time(ev[i + 1]) for ev in marks) / len(marks) for i, n in enumerate(KERNELS)}
-    if bw.folded:  # LN1 / LN2 folded into the GEMM epilogues: slot 0 is empty once chained, slot 4 the statistics
+    if world > 1:
+        # per-phase device time of the banded block (mean over the timed steps); "exchange_wait" is the part of
+        # the halo exchange not hidden behind the interior-row attention
+        per_ms = {n: sum(pm[n].elapsed_time(pm[phases[i + 1]]) for pm in pmarks) / len(pmarks)
+                  for i, n in enumerate(phases[:-1])}
+        per_ms["natten"] = per_ms.pop("na_interior") + per_ms.pop("na_boundary")
+    else:
+        per_ms = {n: sum(ev[i].elapsed_time(ev[i + 1]) for ev in marks) / len(marks) for i, n in enumerate(KERNELS)}
+    if bw.folded and world == 1:  # LN1 / LN2 folded into the GEMM epilogues: slot 0 is empty once chained, slot 4 the statistics
         per_ms.pop("layernorm1")
         per_ms["ln_fold_finalize"] = per_ms.pop("layernorm2")
-    roof, table = roofline(per_ms, int(np.prod(local)))
+    roof, table = roofline(per_ms, int(np.prod(local)), traffic=(world == 1))
 
+    if world > 1:
+        proc.timing = None
     # ---- e2e: pinned host band -> H2D -> block -> D2H ----
     x_host = torch.empty(x.shape, dtype=torch.float32).pin_memory()
     x_host.copy_(x.cpu())
@@ -548,12 +586,12 @@ def run_gpu(args, world, rank, local_rank):
     else:
         def e2e_step():
             xd.copy_(x_host, non_blocking=True)
-            block_forward(xd, bw, ws, rope, local, WIN, row0=me.row0, rows_global=EXT[1], halo_exchange=exch)
+            proc.run([xd], ["blk"])
             y_host.copy_(xd, non_blocking=True)
 
         e2e_step()
         e_ms = timed(e2e_step, e_steps, stream, world)
-        e2e_api = "band block_forward with pinned host copies of the band"
+        e2e_api = "BandedProcessor block (overlapped halo exchange) with pinned host copies of the band"
     e2e_value = flops * e_steps / (e_ms / 1e3) / 1e12
     clk.__exit__(None, None, None)
 
@@ -566,6 +604,11 @@ def run_gpu(args, world, rank, local_rank):
             traceback.print_exc(file=sys.stderr)
             fc = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
+    n_launch = 7
+    if world > 1:  # LN1, QKV, O-proj, LN2, W1, W2 + the attention launches of the row split
+        from paper_2503_22235_b200.bands import interior_rows
+        a_, z_ = interior_rows(me, EXT[1], WIN[1])
+        n_launch = 6 + ((z_ > a_) + (a_ > me.row0) + (z_ < me.row0 + me.rows) if z_ > a_ else 1)
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu:
@@ -591,7 +634,7 @@ def run_gpu(args, world, rank, local_rank):
             "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": int(x.numel() * 4),
                     "d2h_bytes_per_step": int(x.numel() * 4), "ms_per_step": e_ms / e_steps,
                     "api": e2e_api},
-            "gpu_launches": 7 * args.steps,
+            "gpu_launches": n_launch * args.steps,
             "roofline": roof,
             "kernels": table,
             "forecast_14d": fc,

@@ -50,7 +50,7 @@ struct ConvParams {
 
 template <int BN>
 struct ConvCfg {
-  static constexpr int STAGES = (BN == 256) ? 4 : 5;
+  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 64 ? 8 : 5);
   static constexpr uint32_t A_BYTES = CV_BM * CV_BK * 2;
   static constexpr uint32_t B_BYTES = BN * CV_BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -290,6 +290,7 @@ __global__ void __launch_bounds__(F2N_THREADS) fields_to_nhwc_kernel(
   griddep_launch_dependents();  // PDL: the next kernel may start its prologue
   griddep_wait();
   __shared__ float tile[F2N_W][64 + 1];
+  __shared__ long long coff[64];  // source offset of each channel of the current 64-channel chunk (-1: pad)
   const int ntw = (W + 2 + F2N_W - 1) / F2N_W;
   const int pw0 = (blockIdx.x % ntw) * F2N_W;
   const int ph = (blockIdx.x / ntw) % (H + 2);
@@ -306,13 +307,19 @@ __global__ void __launch_bounds__(F2N_THREADS) fields_to_nhwc_kernel(
   const int wsrc = pw == 0 ? W - 1 : (pw == W + 1 ? 0 : pw - 1);
   const float maxf = (kElemFmt == 0) ? 65504.f : 3.0e38f;
   bool bad = false;
+  const float* base = src + img * img_stride + static_cast<long long>(h) * W + wsrc;
   for (int cc = 0; cc < cp; cc += 64) {
+    if (tid < 64) {
+      const int c = cc + tid;
+      coff[tid] = c < C ? (c / cdiv) * a_stride + (c % cdiv) * p_stride : -1;
+    }
+    __syncthreads();
+#pragma unroll 4
     for (int cl = ty; cl < 64; cl += F2N_THREADS / 32) {
-      const int c = cc + cl;
+      const long long off = coff[cl];
       float v = 0.f;
-      if (c < C && lane < npix) {
-        v = __ldg(src + img * img_stride + (c / cdiv) * a_stride + (c % cdiv) * p_stride +
-                  static_cast<long long>(h) * W + wsrc);
+      if (off >= 0 && lane < npix) {
+        v = __ldg(base + off);
         bad |= !(fabsf(v) <= maxf);
       }
       tile[lane][cl] = v;
@@ -368,6 +375,7 @@ static int launch_conv(const CUtensorMap& ta, const CUtensorMap& tb, const ConvP
 using namespace wm3;
 
 extern "C" int wm3_conv_bn(int cout) {
+  if (cout <= 64) return 64;  // decoder heads (17 / 35 channels): half the MMA columns of a 128 tile
   if (cout <= 128) return 128;
   if (cout <= 192) return 192;
   return 256;
@@ -425,6 +433,7 @@ extern "C" int wm3_conv(int mode, const void* in, int imgs, int hin, int win, in
   const int kdim = p.ntap * cinp;
   if (make_tmap_2d_bf16(&tb, w, kdim, static_cast<uint64_t>(p.nclass) * p.cout_pad, kdim, CV_BK, bn)) return -1;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (bn == 64) return launch_conv<64>(ta, tb, p, s);
   if (bn == 128) return launch_conv<128>(ta, tb, p, s);
   if (bn == 192) return launch_conv<192>(ta, tb, p, s);
   return launch_conv<256>(ta, tb, p, s);

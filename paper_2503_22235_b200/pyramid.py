@@ -25,7 +25,8 @@ def cpad(c: int) -> int:
 
 
 def conv_bn(cout: int) -> int:
-    return 128 if cout <= 128 else (192 if cout <= 192 else 256)
+    """N tile of the conv kernel for `cout` output channels (csrc/conv.cu wm3_conv_bn)."""
+    return 64 if cout <= 64 else (128 if cout <= 128 else (192 if cout <= 192 else 256))
 
 
 @dataclass

@@ -176,7 +176,7 @@ def test_conv_weight_layouts_reproduce_reference_convs():
                     acc += np.einsum("co,chw->ohw", wt[:, :, 3 - a - 2 * tr, 3 - bb - 2 * tc], tap)
             y[:, a::2, bb::2] = acc
     np.testing.assert_allclose(y, om.conv_transpose4x4s2(x, wt, bt, (2 * h, 2 * w)), atol=1e-12)
-    assert P.conv_bn(17) == 128 and P.conv_bn(192) == 192 and P.conv_bn(1024) == 256
+    assert P.conv_bn(17) == 64 and P.conv_bn(100) == 128 and P.conv_bn(192) == 192 and P.conv_bn(1024) == 256
 
 
 # ------------------------------------------------------------------------------------------------

@@ -1,6 +1,7 @@
 """One warm-up full-scale encode + decode, then a second one for ncu to capture (profiles/r2_encdec.md):
-    ncu --set full -k regex:"conv_tc|fields_to_nhwc|tokens_to_nhwc" -s 39 -c 39 python tools/prof_encdec_ncu.py
-(39 = 2 fields_to_nhwc + 17 convs per encode, 1 tokens_to_nhwc + 19 convs per decode)."""
+    ncu --set full -k regex:"conv_tc|fields_to_nhwc|tokens_to_nhwc" -s 37 -c 37 python tools/prof_encdec_ncu.py
+(37 = 2 fields_to_nhwc + 17 convs per encode, 1 tokens_to_nhwc + 17 convs per decode; the round-2 capture used
+-s 39 and so starts at the atmosphere fields_to_nhwc of the second pass)."""
 import os
 import sys
 
