@@ -259,6 +259,39 @@ int wm3_sq_err_rows(int dtype, const void* a, long long member_stride, int k, co
 int wm3_zonal_power(int dtype, const void* field, long long member_stride, int k, int imgs, int rows, int cols,
                     double* out, void* stream);
 
+/* Reverse mode of one processor block (autodiff.py backward rules; orchestrated by
+ * paper_2503_22235_b200/backward.py, which runs the weight / input gradient GEMMs on wm3_linear).  Deterministic
+ * (fixed summation orders), so recomputed segments reproduce their gradients bitwise.  Gradient tensors are fp32;
+ * before a GEMM they are cast to the 16-bit operand with a power-of-two scale 2^(14 - ceil(log2 max|g|)) held on
+ * the device (amax_bits = the float bits of max|g|, written by wm3_bw_amax), and every consumer of a GEMM result
+ * divides it back out (NULL amax_bits = scale 1).
+ *   wm3_bw_amax       *amax_bits = bits of max |x| over rows x cols (pitch ld)
+ *   wm3_bw_cast       dst = operand(src * scale), row-major [rows][ldd] or transposed [cols][ldd] (zero padded);
+ *                     src fp32 (src_f32 = 1) or 16-bit operand
+ *   wm3_bw_colsum     out[c] = sum_r src[r][c] (* src2[r][c]) / scale, fixed order (partial: ceil(rows/256) * cols)
+ *   wm3_bw_gelu       out = g / scale * gelu'(a + bias) (exact-erf GELU, autodiff.py:372-382)
+ *   wm3_bw_layernorm  gx = LayerNorm-backward(x, gamma, g / scale) (+ add); gxh = g / scale * xhat; gsc = g / scale
+ *                     (autodiff.py:400-424: mean, biased variance, eps)
+ *   wm3_bw_natten     attention backward over the neighbor table nbr [T][K] (grid.py K order) of the 16-bit qkv
+ *                     [T][3][heads][dhp] (rotated q, k): the q gradient per query, the k / v gradients per key from
+ *                     the inverse neighbor list (inv_off [T + 1], inv_ent [(t, k)] sorted by t); P, dS
+ *                     [T][heads][K] and work [T][heads][2K] scratch; gout [T][3][heads][dhp] fp32
+ *   wm3_bw_rope       in place on the q / k sections of gout: the transpose of the rotary rotation (cos / sin
+ *                     [T][dhp / 2] of the interleaved pairs) */
+int wm3_bw_amax(const float* x, int rows, int cols, int ld, unsigned* amax_bits, void* stream);
+int wm3_bw_cast(const void* src, int src_f32, int rows, int cols, int lds, void* dst, int ldd, int transpose,
+                const unsigned* amax_bits, void* stream);
+int wm3_bw_colsum(const float* src, const float* src2, int rows, int cols, int ld, const unsigned* amax_bits,
+                  float* partial, float* out, void* stream);
+int wm3_bw_gelu(const float* g, int ldg, const float* a, int lda, const float* bias, int rows, int cols,
+                const unsigned* amax_bits, float* out, int ldo, void* stream);
+int wm3_bw_layernorm(const float* x, int ldx, int rows, int n, float eps, const float* gamma, const float* g, int ldg,
+                     const unsigned* amax_bits, const float* add, float* gx, float* gxh, float* gsc, void* stream);
+int wm3_bw_natten(const void* qkv, int ldq, const int64_t* nbr, const int* inv_off, const int* inv_ent, int T, int K,
+                  int heads, int dhp, float scale, const float* gctx, int ldc, const unsigned* amax_bits, float* P,
+                  float* dS, float* work, float* gout, int ldg, void* stream);
+int wm3_bw_rope(float* g, int ldg, int T, int heads, int dhp, const float* cos_t, const float* sin_t, void* stream);
+
 /* Debug export of the kernel's own window arithmetic: per token, the (start_d, start_h, col_off)
  * it uses; int32 [T][3]. */
 int wm3_natten_windows(int depth, int rows, int cols, int rows_global, int row0, int wd, int wh, int ww,

@@ -102,6 +102,13 @@ SIGNATURES = {
     "wm3_fields_to_nhwc": [_vp, _ll, _ll, _ll, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp],
     "wm3_tokens_to_nhwc": [_vp, _i, _i, _i, _i, _i, _vp, _vp],
     "wm3_sq_err_rows": [_i, _vp, _ll, _i, _vp, _vp, _i, _i, _i, _vp, _vp],
+    "wm3_bw_amax": [_vp, _i, _i, _i, _vp, _vp],
+    "wm3_bw_cast": [_vp, _i, _i, _i, _i, _vp, _i, _i, _vp, _vp],
+    "wm3_bw_colsum": [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp],
+    "wm3_bw_gelu": [_vp, _i, _vp, _i, _vp, _i, _i, _vp, _vp, _i, _vp],
+    "wm3_bw_layernorm": [_vp, _i, _i, _i, _f, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp],
+    "wm3_bw_natten": [_vp, _i, _vp, _vp, _vp, _i, _i, _i, _i, _f, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp],
+    "wm3_bw_rope": [_vp, _i, _i, _i, _i, _vp, _vp, _vp],
     "wm3_zonal_power": [_i, _vp, _ll, _i, _i, _i, _i, _vp, _vp],
 }
 

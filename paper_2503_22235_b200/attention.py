@@ -60,21 +60,29 @@ def _foreign_tensor(x) -> bool:
             and hasattr(type(x), "reshape"))
 
 
-def _no_backward(grad_out, saved, add):
-    raise NotImplementedError("backward through the B200 natten_block is not supported (forward-only path); "
-                              "train with the reference block (integration.uninstall)")
-
-
-def _wrap_foreign(x, values: np.ndarray, params: dict, prefix: str):
+def _wrap_foreign(x, values: np.ndarray, params: dict, prefix: str, extents, window, heads: int):
     """The block output as the caller's tensor class.  For the reference's Tensor it goes through the
     reference's own recorder (autodiff.py:288-291), so grad mode and requires_grad propagate exactly as for
-    the reference block; the recorded rule raises on backward instead of silently dropping the gradient."""
+    the reference block.  The recorded rule is the B200 block VJP (backward.block_vjp: the block input is the
+    one saved array, the intermediates are recomputed on the device), accumulating the input and every
+    parameter gradient through the reference's own accumulator."""
     import sys
     record = getattr(sys.modules.get(type(x).__module__), "_record", None)
     if record is None:
         return type(x)(values)
-    parents = [x] + [params[n] for n in block_param_names(prefix) if n in params]
-    return record("natten_block_b200", values, parents, [], _no_backward)
+    names = [n for n in block_param_names(prefix) if n in params]
+    parents = [x] + [params[n] for n in names]
+    ext, win = tuple(int(e) for e in extents), tuple(int(w) for w in window)
+
+    def rule(g, saved, add):
+        from .backward import block_vjp
+        (xv,) = saved
+        gx, grads = block_vjp(xv, params, prefix, ext, win, heads, g)
+        add(x, gx)
+        for n in names:
+            add(params[n], grads[n])
+
+    return record("natten_block_b200", values, parents, [x.values], rule)
 
 
 def natten_block(x, params: dict, prefix: str, extents, window, heads: int):
@@ -83,9 +91,10 @@ def natten_block(x, params: dict, prefix: str, extents, window, heads: int):
     Returns our Tensor (device-backed) for our / torch / numpy inputs.  Given the reference's own Tensor
     (the operator-level seam: `gridcast.model.natten_block = natten_block`), it returns a
     tensor of the caller's class built from the float64 result, so the reference's encode / process / decode
-    keep applying their own ops (`tokens.reshape(...)`, model.py:357-360) to it.  The B200 block is forward
-    only: it is recorded on the reference's tape like the reference block, and a backward sweep that reaches
-    it raises NotImplementedError instead of silently cutting the gradient."""
+    keep applying their own ops (`tokens.reshape(...)`, model.py:357-360) to it.  It is recorded on the
+    reference's tape like the reference block, with the B200 block VJP as its backward rule (backward.py), so
+    the reference's training, checkpointing and offload engine run the block forward and backward on the
+    device."""
     shape = tuple(x.shape)
     dh = validate_block_args(shape, extents, window, heads)
     foreign = _foreign_tensor(x)
@@ -97,7 +106,7 @@ def natten_block(x, params: dict, prefix: str, extents, window, heads: int):
     block_forward(xd, bw, CACHE.workspace(extents, window, bw), CACHE.rope(extents, dh), tuple(extents),
                   tuple(window))
     if foreign:
-        return _wrap_foreign(x, xd.to("cpu", torch.float64).numpy(), params, prefix)
+        return _wrap_foreign(x, xd.to("cpu", torch.float64).numpy(), params, prefix, extents, window, heads)
     return Tensor(device=xd)
 
 

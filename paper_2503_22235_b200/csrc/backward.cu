@@ -1,0 +1,372 @@
+// Reverse-mode pieces of one processor block (reference autodiff.py backward rules of layernorm :400-424, gelu
+// :372-382, matmul :350-369, the attention gather / softmax / matmuls attention.py:166-178 and the rotary
+// rotation :87-92).  The block VJP (paper_2503_22235_b200/backward.py) chains them with the forward GEMM kernel:
+// every weight / input gradient GEMM runs on the tcgen05 GEMM (gemm.cu) with 16-bit operands, so gradients are
+// cast with a per-tensor power-of-two scale (wm3_bw_amax) that puts their largest magnitude near 2^14 — fp16
+// holds them without underflow — and the consumers of the fp32 GEMM results divide the scale back out.
+//
+// Everything here is deterministic: maxima use order-independent atomicMax, sums run in a fixed order (column
+// sums as fixed row chunks + an ordered second pass; the attention key gradients walk an inverse neighbor list
+// sorted by query), so a recomputed segment's gradients are bitwise those of the first computation (the
+// reference's checkpoint / offload parity contract, autodiff.py:893-924, offload.py:287-412).
+#include <cmath>
+
+#include "common.cuh"
+#include "launch.h"
+#include "../../include/wm3.h"
+
+namespace wm3 {
+
+DEVI float to_f(__half v) { return __half2float(v); }
+DEVI float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+// scale for a tensor whose max |x| has the bits `amax_bits` (non-negative float bits order as unsigned)
+DEVI float grad_scale(const unsigned* amax_bits) {
+  if (amax_bits == nullptr) return 1.f;
+  const float amax = __uint_as_float(*amax_bits);
+  if (!(amax > 0.f) || !isfinite(amax)) return 1.f;
+  return exp2f(14.f - ceilf(log2f(amax)));
+}
+
+__global__ void bw_amax_kernel(const float* __restrict__ x, int rows, int cols, int ld, unsigned* amax_bits) {
+  float m = 0.f;
+  const long long n = static_cast<long long>(rows) * cols;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / cols, c = i - r * cols;
+    m = fmaxf(m, fabsf(x[r * ld + c]));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(amax_bits, __float_as_uint(m));
+}
+
+// dst = operand(src * scale), row-major [rows][ld_dst] (columns >= cols zero) or transposed [cols][ld_dst]
+// (columns >= rows zero); src fp32 (f32 = 1) or 16-bit operand.  32 x 32 tiles through shared memory.
+__global__ void bw_cast_kernel(const void* __restrict__ src, int f32, int rows, int cols, int lds,
+                               elem_t* __restrict__ dst, int ldd, int transpose, const unsigned* amax_bits) {
+  __shared__ float tile[32][33];
+  const float s = grad_scale(amax_bits);
+  const int tr = blockIdx.y * 32, tc = blockIdx.x * 32;  // tile origin in dst coordinates
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+  if (!transpose) {
+    for (int i = ty; i < 32; i += 8) {
+      const int r = tr + i, c = tc + tx;
+      if (r >= rows || c >= ldd) continue;
+      float v = 0.f;
+      if (c < cols) {
+        const size_t o = static_cast<size_t>(r) * lds + c;
+        v = f32 ? static_cast<const float*>(src)[o] : unpack_elem2(static_cast<const uint16_t*>(src)[o]).x;
+      }
+      dst[static_cast<size_t>(r) * ldd + c] = to_elem(v * s);
+    }
+    return;
+  }
+  // dst [cols][ldd] = src^T: dst row = src column
+  for (int i = ty; i < 32; i += 8) {
+    const int sr = tc + i, sc = tr + tx;  // read src (row sr = dst column, col sc = dst row), coalesced over sc
+    float v = 0.f;
+    if (sr < rows && sc < cols) {
+      const size_t o = static_cast<size_t>(sr) * lds + sc;
+      v = f32 ? static_cast<const float*>(src)[o] : unpack_elem2(static_cast<const uint16_t*>(src)[o]).x;
+    }
+    tile[i][tx] = v;
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const int dr = tr + i, dc = tc + tx;
+    if (dr < cols && dc < ldd) dst[static_cast<size_t>(dr) * ldd + dc] = to_elem(tile[tx][i] * s);
+  }
+}
+
+// partial[chunk][c] = sum over rows [chunk * 256, +256) of src[r][c] (optionally times src2[r][c]), row order
+constexpr int BW_CHUNK = 256;
+__global__ void bw_colsum_partial_kernel(const float* __restrict__ src, const float* __restrict__ src2, int rows,
+                                         int cols, int ld, float* __restrict__ partial) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  const int r0 = blockIdx.y * BW_CHUNK, r1 = min(rows, r0 + BW_CHUNK);
+  float acc = 0.f;
+  for (int r = r0; r < r1; ++r) {
+    const float v = src[static_cast<size_t>(r) * ld + c];
+    acc += src2 != nullptr ? v * src2[static_cast<size_t>(r) * ld + c] : v;
+  }
+  partial[static_cast<size_t>(blockIdx.y) * cols + c] = acc;
+}
+
+__global__ void bw_colsum_final_kernel(const float* __restrict__ partial, int chunks, int cols,
+                                       const unsigned* amax_bits, float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  float acc = 0.f;
+  for (int k = 0; k < chunks; ++k) acc += partial[static_cast<size_t>(k) * cols + c];
+  out[c] = acc / grad_scale(amax_bits);
+}
+
+// out = (g / scale) * gelu'(a + bias), exact-erf GELU derivative Phi(z) + z phi(z) (autodiff.py:372-382)
+__global__ void bw_gelu_kernel(const float* __restrict__ g, int ldg, const float* __restrict__ a, int lda,
+                               const float* __restrict__ bias, int rows, int cols, const unsigned* amax_bits,
+                               float* __restrict__ out, int ldo) {
+  const float inv = 1.f / grad_scale(amax_bits);
+  const long long n = static_cast<long long>(rows) * cols;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / cols, c = i - r * cols;
+    const float z = a[r * lda + c] + bias[c];
+    const float d = 0.5f * (1.f + erff(z * 0.70710678118654752f)) + z * 0.39894228040143268f * expf(-0.5f * z * z);
+    out[r * ldo + c] = g[r * ldg + c] * inv * d;
+  }
+}
+
+// LayerNorm backward per row (one warp), forward statistics recomputed as layernorm_kernel does (mean, biased
+// variance, eps): ghat = (g / scale) * gamma, gx = rstd * (ghat - mean(ghat) - xhat * mean(ghat * xhat)) (+ add);
+// gxh[r][c] = (g / scale) * xhat (gain gradient = its column sum), gsc[r][c] = g / scale (bias gradient).
+__global__ void bw_layernorm_kernel(const float* __restrict__ x, int ldx, int rows, int n, float eps,
+                                    const float* __restrict__ gamma, const float* __restrict__ g, int ldg,
+                                    const unsigned* amax_bits, const float* __restrict__ add, float* __restrict__ gx,
+                                    float* __restrict__ gxh, float* __restrict__ gsc) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const float inv = 1.f / grad_scale(amax_bits);
+  const float* xr = x + static_cast<size_t>(warp) * ldx;
+  const float* gr = g + static_cast<size_t>(warp) * ldg;
+  float s = 0.f;
+  for (int c = lane; c < n; c += 32) s += xr[c];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mu = s / n;
+  float q = 0.f;
+  for (int c = lane; c < n; c += 32) {
+    const float d = xr[c] - mu;
+    q += d * d;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float rstd = rsqrtf(q / n + eps);
+  float a1 = 0.f, a2 = 0.f;
+  for (int c = lane; c < n; c += 32) {
+    const float xh = (xr[c] - mu) * rstd;
+    const float gh = gr[c] * inv * gamma[c];
+    a1 += gh;
+    a2 += gh * xh;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+  }
+  a1 /= n;
+  a2 /= n;
+  for (int c = lane; c < n; c += 32) {
+    const size_t o = static_cast<size_t>(warp) * n + c;
+    const float xh = (xr[c] - mu) * rstd;
+    const float gu = gr[c] * inv;
+    const float gh = gu * gamma[c];
+    gx[o] = rstd * (gh - a1 - xh * a2) + (add != nullptr ? add[o] : 0.f);
+    gxh[o] = gu * xh;
+    gsc[o] = gu;
+  }
+}
+
+// Attention backward, query side (one warp per (token, head)): logits over the token's K window keys
+// (neighbor table, grid.py K order) recomputed from the rotated q, k exactly as scored (scale after rotary),
+// softmax in fp32, dP_k = g_ctx . v_k, D = sum_k p_k dP_k, dS_k = p_k (dP_k - D), g_q = scale * sum_k dS_k k_k.
+// Stores P and dS [T][heads][K] for the key side.  qkv: [T][3][heads][dhp] (16-bit), g_ctx [T][heads * dhp]
+// fp32 with scale `amax_bits`; g_out [T][3][heads][dhp] fp32 (q section written here).
+__global__ void bw_na_query_kernel(const elem_t* __restrict__ qkv, int ldq, const int64_t* __restrict__ nbr, int T,
+                                   int K, int heads, int dhp, float scale, const float* __restrict__ gctx, int ldc,
+                                   const unsigned* amax_bits, float* __restrict__ P, float* __restrict__ dS,
+                                   float* __restrict__ gout, int ldg, float* __restrict__ work) {
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wid >= T * heads) return;
+  const int t = wid / heads, h = wid - t * heads;
+  const int sec = heads * dhp;
+  const float inv = 1.f / grad_scale(amax_bits);
+  const int per = dhp / 32;  // 2 or 4 channels per lane
+  float qv[4], gc[4], acc[4];
+  for (int e = 0; e < per; ++e) {
+    const int c = lane * per + e;
+    qv[e] = to_f(qkv[static_cast<size_t>(t) * ldq + h * dhp + c]);
+    gc[e] = gctx[static_cast<size_t>(t) * ldc + h * dhp + c] * inv;
+    acc[e] = 0.f;
+  }
+  float* s = work + static_cast<size_t>(wid) * 2 * K;  // logits, then dP
+  float mx = -INFINITY;
+  for (int k = 0; k < K; ++k) {
+    const int64_t j = nbr[static_cast<size_t>(t) * K + k];
+    const elem_t* kr = qkv + static_cast<size_t>(j) * ldq + sec + h * dhp;
+    const elem_t* vr = kr + sec;
+    float d = 0.f, dp = 0.f;
+    for (int e = 0; e < per; ++e) {
+      const int c = lane * per + e;
+      d += qv[e] * to_f(kr[c]);
+      dp += gc[e] * to_f(vr[c]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      d += __shfl_xor_sync(0xffffffffu, d, o);
+      dp += __shfl_xor_sync(0xffffffffu, dp, o);
+    }
+    d *= scale;
+    mx = fmaxf(mx, d);
+    if (lane == 0) {
+      s[k] = d;
+      s[K + k] = dp;
+    }
+  }
+  __syncwarp();
+  float l = 0.f;
+  for (int k = lane; k < K; k += 32) l += expf(s[k] - mx);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+  float dsum = 0.f;
+  for (int k = lane; k < K; k += 32) dsum += expf(s[k] - mx) / l * s[K + k];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+  const size_t pbase = (static_cast<size_t>(t) * heads + h) * K;
+  for (int k = lane; k < K; k += 32) {
+    const float p = expf(s[k] - mx) / l;
+    P[pbase + k] = p;
+    dS[pbase + k] = p * (s[K + k] - dsum);
+  }
+  __syncwarp();
+  for (int k = 0; k < K; ++k) {
+    const float ds = dS[pbase + k];
+    const int64_t j = nbr[static_cast<size_t>(t) * K + k];
+    const elem_t* kr = qkv + static_cast<size_t>(j) * ldq + sec + h * dhp;
+    for (int e = 0; e < per; ++e)
+      acc[e] += ds * to_f(kr[lane * per + e]);
+  }
+  for (int e = 0; e < per; ++e) gout[static_cast<size_t>(t) * ldg + h * dhp + lane * per + e] = acc[e] * scale;
+}
+
+// Attention backward, key side (one warp per (key token, head)): the inverse neighbor list of key j (entries
+// (t, k) with nbr[t][k] = j, sorted by t) gives g_k = scale * sum dS[t][h][k] q_t and g_v = sum P[t][h][k] g_ctx_t,
+// in a fixed order.
+__global__ void bw_na_key_kernel(const elem_t* __restrict__ qkv, int ldq, const int* __restrict__ inv_off,
+                                 const int* __restrict__ inv_ent, int T, int K, int heads, int dhp, float scale,
+                                 const float* __restrict__ gctx, int ldc, const unsigned* amax_bits,
+                                 const float* __restrict__ P, const float* __restrict__ dS, float* __restrict__ gout,
+                                 int ldg) {
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wid >= T * heads) return;
+  const int j = wid / heads, h = wid - j * heads;
+  const int sec = heads * dhp;
+  const float inv = 1.f / grad_scale(amax_bits);
+  const int per = dhp / 32;
+  float gk[4] = {0.f, 0.f, 0.f, 0.f}, gv[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int e = inv_off[j]; e < inv_off[j + 1]; ++e) {
+    const int t = inv_ent[2 * e], k = inv_ent[2 * e + 1];
+    const size_t pi = (static_cast<size_t>(t) * heads + h) * K + k;
+    const float ds = dS[pi], p = P[pi];
+    for (int c = 0; c < per; ++c) {
+      const int ch = lane * per + c;
+      gk[c] += ds * to_f(qkv[static_cast<size_t>(t) * ldq + h * dhp + ch]);
+      gv[c] += p * gctx[static_cast<size_t>(t) * ldc + h * dhp + ch] * inv;
+    }
+  }
+  for (int c = 0; c < per; ++c) {
+    const int ch = lane * per + c;
+    gout[static_cast<size_t>(j) * ldg + sec + h * dhp + ch] = gk[c] * scale;
+    gout[static_cast<size_t>(j) * ldg + 2 * sec + h * dhp + ch] = gv[c];
+  }
+}
+
+// In place on the q and k sections of g [T][3][heads][dhp]: the transpose of the rotary rotation of the
+// interleaved pairs (2i, 2i + 1) (forward: v0' = v0 c - v1 s, v1' = v0 s + v1 c), cos / sin [T][dhp / 2].
+__global__ void bw_rope_kernel(float* __restrict__ g, int ldg, int T, int heads, int dhp,
+                               const float* __restrict__ cs, const float* __restrict__ sn) {
+  const int half = dhp / 2;
+  const long long n = static_cast<long long>(T) * 2 * heads * half;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int pr = static_cast<int>(i % half);
+    long long rest = i / half;
+    const int hs = static_cast<int>(rest % (2 * heads));  // section (q / k) x head
+    const int t = static_cast<int>(rest / (2 * heads));
+    float* p = g + static_cast<size_t>(t) * ldg + static_cast<size_t>(hs) * dhp + 2 * pr;
+    const float c = cs[static_cast<size_t>(t) * half + pr], s = sn[static_cast<size_t>(t) * half + pr];
+    const float g0 = p[0], g1 = p[1];
+    p[0] = g0 * c + g1 * s;
+    p[1] = -g0 * s + g1 * c;
+  }
+}
+
+static int grid_for(long long n, int threads) {
+  long long b = (n + threads - 1) / threads;
+  if (b > 148LL * 32) b = 148LL * 32;
+  return static_cast<int>(b < 1 ? 1 : b);
+}
+
+}  // namespace wm3
+
+using namespace wm3;
+
+extern "C" int wm3_bw_amax(const float* x, int rows, int cols, int ld, unsigned* amax_bits, void* stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(amax_bits, 0, sizeof(unsigned), s) != cudaSuccess) return set_error("wm3_bw_amax: memset");
+  bw_amax_kernel<<<grid_for(static_cast<long long>(rows) * cols, 256), 256, 0, s>>>(x, rows, cols, ld, amax_bits);
+  return check_launch("bw_amax_kernel");
+}
+
+extern "C" int wm3_bw_cast(const void* src, int src_f32, int rows, int cols, int lds, void* dst, int ldd,
+                           int transpose, const unsigned* amax_bits, void* stream) {
+  if (rows < 1 || cols < 1) return set_error("wm3_bw_cast: empty");
+  const int drows = transpose ? cols : rows;
+  dim3 grid((ldd + 31) / 32, (drows + 31) / 32);
+  bw_cast_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      src, src_f32, rows, cols, lds, reinterpret_cast<elem_t*>(dst), ldd, transpose, amax_bits);
+  return check_launch("bw_cast_kernel");
+}
+
+extern "C" int wm3_bw_colsum(const float* src, const float* src2, int rows, int cols, int ld, const unsigned* amax_bits,
+                             float* partial, float* out, void* stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int chunks = (rows + BW_CHUNK - 1) / BW_CHUNK;
+  bw_colsum_partial_kernel<<<dim3((cols + 127) / 128, chunks), 128, 0, s>>>(src, src2, rows, cols, ld, partial);
+  if (check_launch("bw_colsum_partial_kernel")) return -1;
+  bw_colsum_final_kernel<<<(cols + 127) / 128, 128, 0, s>>>(partial, chunks, cols, amax_bits, out);
+  return check_launch("bw_colsum_final_kernel");
+}
+
+extern "C" int wm3_bw_gelu(const float* g, int ldg, const float* a, int lda, const float* bias, int rows, int cols,
+                           const unsigned* amax_bits, float* out, int ldo, void* stream) {
+  bw_gelu_kernel<<<grid_for(static_cast<long long>(rows) * cols, 256), 256, 0,
+                   reinterpret_cast<cudaStream_t>(stream)>>>(g, ldg, a, lda, bias, rows, cols, amax_bits, out, ldo);
+  return check_launch("bw_gelu_kernel");
+}
+
+extern "C" int wm3_bw_layernorm(const float* x, int ldx, int rows, int n, float eps, const float* gamma, const float* g,
+                                int ldg, const unsigned* amax_bits, const float* add, float* gx, float* gxh, float* gsc,
+                                void* stream) {
+  const int threads = 256, blocks = (rows * 32 + threads - 1) / threads;
+  bw_layernorm_kernel<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      x, ldx, rows, n, eps, gamma, g, ldg, amax_bits, add, gx, gxh, gsc);
+  return check_launch("bw_layernorm_kernel");
+}
+
+extern "C" int wm3_bw_natten(const void* qkv, int ldq, const int64_t* nbr, const int* inv_off, const int* inv_ent, int T,
+                             int K, int heads, int dhp, float scale, const float* gctx, int ldc,
+                             const unsigned* amax_bits, float* P, float* dS, float* work, float* gout, int ldg,
+                             void* stream) {
+  if (dhp != 64 && dhp != 128) return set_error("wm3_bw_natten: dhp must be 64 or 128");
+  if (ldg < 3 * heads * dhp) return set_error("wm3_bw_natten: ldg < 3 * heads * dhp");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int threads = 256, blocks = (T * heads * 32 + threads - 1) / threads;
+  bw_na_query_kernel<<<blocks, threads, 0, s>>>(reinterpret_cast<const elem_t*>(qkv), ldq, nbr, T, K, heads, dhp,
+                                                scale, gctx, ldc, amax_bits, P, dS, gout, ldg, work);
+  if (check_launch("bw_na_query_kernel")) return -1;
+  bw_na_key_kernel<<<blocks, threads, 0, s>>>(reinterpret_cast<const elem_t*>(qkv), ldq, inv_off, inv_ent, T, K, heads,
+                                              dhp, scale, gctx, ldc, amax_bits, P, dS, gout, ldg);
+  return check_launch("bw_na_key_kernel");
+}
+
+extern "C" int wm3_bw_rope(float* g, int ldg, int T, int heads, int dhp, const float* cos_t, const float* sin_t,
+                           void* stream) {
+  bw_rope_kernel<<<grid_for(static_cast<long long>(T) * heads * dhp, 256), 256, 0,
+                   reinterpret_cast<cudaStream_t>(stream)>>>(g, ldg, T, heads, dhp, cos_t, sin_t);
+  return check_launch("bw_rope_kernel");
+}

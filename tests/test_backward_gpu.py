@@ -1,0 +1,155 @@
+"""§8f4 on the B200: the processor block's reverse mode (backward.block_vjp) and the reference's own training
+machinery running on it through the operator seam (integration.install(operator=True)).
+
+Oracle: the reference's float64 tape (gridcast.autodiff backward over attention.natten_block, staged into
+baseline/_ref by baseline/stage_ref.sh).  Tolerances: relative L2 <= 1e-2 per gradient (fp16 tensor-core operands,
+fp32 accumulation; measured values printed); determinism and the checkpoint / offload parity of verify.py:73-113
+bitwise.
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+GRAD_TOL = 1e-2
+
+
+@pytest.fixture(scope="module")
+def gc():
+    if not os.path.isdir(os.path.join(REF, "gridcast")):
+        pytest.skip("reference not staged: run baseline/stage_ref.sh")
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    import gridcast
+    import gridcast.attention
+    import gridcast.autodiff
+    import gridcast.model
+    import gridcast.training
+    import gridcast.verify
+    return gridcast
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.mark.parametrize("ext,win,dim,heads", [
+    ((3, 5, 10), (3, 3, 3), 48, 4),     # desk latent
+    ((2, 7, 10), (1, 3, 3), 24, 4),     # dh = 6 (heads padded to 64)
+    ((7, 9, 18), (5, 7, 7), 256, 2),    # paper window: depth bump, row bump, column wrap
+    ((4, 6, 10), (2, 4, 4), 128, 2),    # even windows
+])
+def test_block_vjp_matches_reference_tape(gc, ext, win, dim, heads):
+    """Input and all 16 parameter gradients of one block vs the reference tape's float64 gradients of
+    sum(natten_block(x) * R)."""
+    from gridcast import autodiff as ad
+    from paper_2503_22235_b200.backward import block_vjp
+    t = int(np.prod(ext))
+    rng = np.random.default_rng(t)
+    params = gc.attention.init_block_params(rng, dim, heads, "blk", zero_residual=False)
+    xv = rng.standard_normal((t, dim))
+    r = rng.standard_normal((t, dim))
+    x = ad.Tensor(xv, requires_grad=True)
+    y = gc.attention.natten_block(x, params, "blk", ext, win, heads)
+    grads = ad.backward((y * ad.Tensor(r)).sum(), leaves=[x] + list(params.values()))
+    gx, pg = block_vjp(xv, params, "blk", ext, win, heads, r)
+    errs = {"x": _rel(gx, grads[x])}
+    for n, p in params.items():
+        assert pg[n].shape == p.values.shape, n
+        errs[n] = _rel(pg[n], grads[p])
+    worst = max(errs, key=errs.get)
+    print(f"block VJP {ext} {win} D={dim}: worst {worst} {errs[worst]:.2e}, x {errs['x']:.2e}")
+    assert errs[worst] < GRAD_TOL, (worst, errs[worst])
+
+
+def test_block_vjp_deterministic(gc):
+    from paper_2503_22235_b200.backward import block_vjp
+    ext, win, dim, heads = (7, 9, 18), (5, 7, 7), 256, 2
+    rng = np.random.default_rng(3)
+    params = gc.attention.init_block_params(rng, dim, heads, "blk", zero_residual=False)
+    x = rng.standard_normal((int(np.prod(ext)), dim))
+    r = rng.standard_normal(x.shape)
+    a = block_vjp(x, params, "blk", ext, win, heads, r)
+    b = block_vjp(x, params, "blk", ext, win, heads, r)
+    assert np.array_equal(a[0], b[0])
+    assert all(np.array_equal(a[1][n], b[1][n]) for n in a[1])
+
+
+def test_reference_offload_parity_check_through_seam(gc):
+    """The reference's own verify.check_offload_parity (checkpointed vs OffloadEngine segments of the tiny
+    processor, gradients compared as bytes) with every block on the B200, forward and backward; and its
+    gradients against the pure-reference run of the same construction."""
+    from gridcast import autodiff as ad
+    from gridcast.model import LatentState, init_model_params, process, tiny_config
+    from paper_2503_22235_b200 import integration
+
+    cfg = tiny_config()
+    params = init_model_params(cfg, seed=0, zero_residual=False)
+    ext = (cfg.depth_planes, cfg.grid.rows // 8, cfg.grid.cols // 8)
+    z0v = np.random.default_rng(2).standard_normal((int(np.prod(ext)), cfg.hidden))
+
+    def run():
+        z0 = ad.Tensor(z0v, requires_grad=True)
+        z = z0
+        for _ in range(3):
+            z = ad.checkpoint_segment(lambda tk: process(LatentState(tk, 0, ext), params, cfg, 6).tokens, z)
+        loss = (z * z).mean()
+        return loss.values, ad.backward(loss, leaves=[z0])[z0]
+
+    ref_loss, ref_g = run()
+    integration.install(gc, operator=True, model_level=False)
+    try:
+        gc.verify.check_offload_parity()  # raises AssertionError on any byte difference
+        loss, g = run()
+    finally:
+        integration.uninstall(gc)
+    print(f"tiny 3-segment loss {float(loss):.6f} vs reference {float(ref_loss):.6f}; "
+          f"dL/dz0 rel {_rel(g, ref_g):.2e}")
+    assert abs(float(loss) - float(ref_loss)) < 1e-2 * abs(float(ref_loss))
+    assert _rel(g, ref_g) < GRAD_TOL
+
+
+def test_reference_train_step_and_driver_through_seam(gc):
+    """The reference's shared-prefix train_step (training.py:211-241: encode, 6 h chain, hour tails, decode,
+    normalized loss) and its training driver with the B200 blocks: loss and every block parameter gradient vs
+    the pure reference; the driver's 20-step loss curve is repeatable and falls (reference test_training.py:204)."""
+    from gridcast import autodiff as ad
+    from gridcast.model import init_model_params, tiny_config
+    from gridcast.synthdata import generate_dataset
+    from gridcast.training import train, train_step
+    from paper_2503_22235_b200 import integration
+
+    cfg = tiny_config()
+    ds = generate_dataset(cfg.grid, cfg.surface_in, cfg.surface_out, cfg.atmos_vars, cfg.levels, hours=26, seed=2)
+    sig = ds.plane_sigmas()
+
+    def step():
+        params = init_model_params(cfg, seed=0, zero_residual=False)
+        loss = train_step(params, cfg, ds, (1, 6, 7), 0, sig, stage="1h")
+        grads = ad.backward(loss, leaves=list(params.values()))
+        return float(loss.values), {n: grads[p] for n, p in params.items()}
+
+    ref_loss, ref_grads = step()
+    integration.install(gc, operator=True, model_level=False)
+    try:
+        loss, grads = step()
+        hist = [train(init_model_params(cfg, seed=0), cfg, ds, "pretrain", steps=20, seed=5, lr_max=3e-3)
+                for _ in range(2)]
+    finally:
+        integration.uninstall(gc)
+    blk = [n for n in grads if ".blk" in n]
+    errs = {n: _rel(grads[n], ref_grads[n]) for n in blk if np.linalg.norm(ref_grads[n]) > 0}
+    worst = max(errs, key=errs.get)
+    print(f"train_step loss {loss:.6f} vs reference {ref_loss:.6f}; worst block grad {worst} {errs[worst]:.2e}")
+    assert abs(loss - ref_loss) < 1e-2 * abs(ref_loss)
+    assert errs[worst] < 2 * GRAD_TOL, (worst, errs[worst])
+    # the reference's test_training.py:204-216 on the B200 blocks: deterministic, and the loss falls
+    l1, l2 = [r["loss"] for r in hist[0]], [r["loss"] for r in hist[1]]
+    assert l1 == l2
+    assert np.mean(l1[-5:]) < 0.8 * np.mean(l1[:5]), l1
