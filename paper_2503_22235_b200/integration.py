@@ -8,11 +8,11 @@ copy in one place (INTEGRATION.md §2 shows the same assignments); `uninstall` r
 
 Latents and decoded fields produced by the B200 functions are device-backed (`.values` = float64 numpy); a
 reference function that receives one must therefore itself be rebound, which is why the model-level names
-are rebound in `gridcast.model` too.  `gridcast.training` and `gridcast.verify` keep the reference (the B200
-block is forward-only): with `operator=True` the operator seam `gridcast.model.natten_block` /
+are rebound in `gridcast.model` too.  With `operator=True` the operator seam `gridcast.model.natten_block` /
 `gridcast.attention.natten_block` is also rebound, so the reference's own model functions still held by
-other modules call the B200 block — on reference Tensors it returns reference Tensors, and a call the
-reference would record on its tape raises NotImplementedError rather than cutting the gradient.
+other modules (`gridcast.training`, `gridcast.verify`) call the B200 block — on reference Tensors it returns
+reference Tensors, and a call the reference would record on its tape is recorded with the B200 block VJP
+(backward.block_vjp) as its backward rule.
 """
 
 from __future__ import annotations
