@@ -251,7 +251,7 @@ __global__ void natten_bias_table_kernel(NaParams p, uint8_t* table) {
   *reinterpret_cast<uint4*>(img + xtra_off(threadIdx.x, 1)) = make_uint4(u[4], u[5], u[6], u[7]);
 }
 
-template <bool BIAS>
+template <bool BIAS, int DHP>
 __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
     natten_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, NaParams p) {
   griddep_launch_dependents();  // PDL: the next kernel may start its prologue
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
     if (lane == 0) {
       tma_prefetch(&tmQ);
       tma_prefetch(&tmKV);
-      const int halves = p.dhp / 64;
+      constexpr int halves = DHP / 64;
       const uint32_t qbytes = halves * 128u * p.TW * p.TH * p.TD;
       const uint32_t kbytes = halves * 128u * p.ncp * p.nrpc;
       int chunk_ctr = 0, tile_ctr = 0;
@@ -370,72 +370,89 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
     //   S0(c) S1(c) | PV0(c) S0(c+1) | PV1(c) S1(c+1) | PV0(c+1) S0(c+2) | ...
     // S_h(c + 1) overwrites the TMEM columns [64 h, 64 h + 64) whose P_h(c) the preceding PV_h(c) reads (in
     // order), so the softmax of half 0 of the next chunk overlaps P V of half 1 of this one.
-    if (lane == 0) {
-      const uint32_t idesc_s = make_idesc(128, 64, 0, 0);
-      const uint32_t idesc_o = make_idesc(128, p.dhp, 0, 1);
-      const int ksteps = p.dhp / 16;
-      const uint32_t tO = tmem + NA_TMEM_O;
-      auto issue_s = [&](int h, int c) {  // c: the chunk's running index (B_x buffer parity)
-        // S_h = Q K_h^T: keys [64 h, 64 h + 64) are rows [64 h, +64) of the K tile (SW128 K-major)
-        for (int s = 0; s < ((p.dbg & 2) ? 0 : ksteps); ++s) {
-          const uint32_t off = (s >> 2) * 16384u + (s & 3) * 32u;
-          umma_bf16_ss(tmem + 64 * h, make_sdesc_sw128(sQ + off, 16, 1024),
-                       make_sdesc_sw128(sK + off + h * 8192u, 16, 1024), idesc_s, s > 0 ? 1u : 0u);
+    // The whole warp walks the schedule (warp-wide waits) so the descriptors are warp-uniform and live in
+    // uniform registers; one elected lane issues the MMAs and commits.  (A lane-0-only loop made every MMA a
+    // ~27-instruction R2UR.BROADCAST sequence and kept this warp ~80 % busy on the critical path.)
+    constexpr int KSTEPS = DHP / 16;
+    const uint32_t idesc_s = make_idesc(128, 64, 0, 0);
+    const uint32_t idesc_o = make_idesc(128, DHP, 0, 1);
+    const uint32_t tO = tmem + NA_TMEM_O;
+    const uint64_t dQ = make_sdesc_sw128(sQ, 16, 1024), dK = make_sdesc_sw128(sK, 16, 1024);
+    const uint64_t dV = make_sdesc_sw128(sV, 16384, 1024);
+    const uint64_t dXA = make_sdesc_interleave(sXA), dXB = make_sdesc_interleave(sXB);
+    auto issue_s = [&](int h) {
+      // S_h = Q K_h^T: keys [64 h, 64 h + 64) are rows [64 h, +64) of the K tile (SW128 K-major); descriptor
+      // start addresses advance in 16-byte units
+      if (elect_one()) {
+        if (!(p.dbg & 2)) {
+#pragma unroll
+          for (int s = 0; s < KSTEPS; ++s) {
+            const uint32_t off = ((s >> 2) * 16384u + (s & 3) * 32u) >> 4;
+            umma_bf16_ss(tmem + 64 * h, dQ + off, dK + off + h * 512u, idesc_s, s > 0 ? 1u : 0u);
+          }
         }
         if (BIAS)  // + window mask: one-hot query classes x key bias (keys 64 h ..)
-          umma_bf16_ss(tmem + 64 * h, make_sdesc_interleave(sXA),
-                       make_sdesc_interleave(sXB + h * 2048u), idesc_s, (p.dbg & 2) ? 0u : 1u);
+          umma_bf16_ss(tmem + 64 * h, dXA, dXB + h * 128u, idesc_s, (p.dbg & 2) ? 0u : 1u);
         umma_commit(bar_sfull(h));
-      };
-      auto issue_pv = [&](int h, bool first) {
-        // O += P_h V_h: A = P_h from TMEM columns [64 h, 64 h + 32) (fp16 pairs), B = V rows 64 h.. (MN-major)
-        for (int s = 0; s < ((p.dbg & 4) ? 0 : 4); ++s) {
-          const uint64_t bd = make_sdesc_sw128(sV + (4 * h + s) * 2048u, 16384, 1024);
-          umma_f16_ts(tO, tmem + 64 * h + 8 * s, bd, idesc_o, (!first || s > 0) ? 1u : 0u);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int h, bool first, uint32_t extra_bar) {
+      // O += P_h V_h: A = P_h from TMEM columns [64 h, 64 h + 32) (fp16 pairs), B = V rows 64 h.. (MN-major)
+      if (elect_one()) {
+        if (!(p.dbg & 4)) {
+#pragma unroll
+          for (int s = 0; s < 4; ++s)
+            umma_f16_ts(tO, tmem + 64 * h + 8 * s, dV + (4 * h + s) * 128u, idesc_o, (!first || s > 0) ? 1u : 0u);
         }
         umma_commit(bar_pvdone(h));
-      };
-      int chunk_ctr = 0, tile_ctr = 0;
-      for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
-        const TileGeo g = tile_geo(p, item);
-        mbar_wait(bar_qfull, tile_ctr & 1);
-        // prologue: both S halves of the tile's first chunk
-        mbar_wait(bar_kfull, chunk_ctr & 1);
+        if (extra_bar) umma_commit(extra_bar);
+      }
+      __syncwarp();
+    };
+    auto commit = [&](uint32_t bar) {
+      if (elect_one()) umma_commit(bar);
+      __syncwarp();
+    };
+    int chunk_ctr = 0, tile_ctr = 0;
+    for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
+      const TileGeo g = tile_geo(p, item);
+      mbar_wait(bar_qfull, tile_ctr & 1);
+      // prologue: both S halves of the tile's first chunk
+      mbar_wait(bar_kfull, chunk_ctr & 1);
+      tc_fence_after();
+      issue_s(0);
+      issue_s(1);
+      commit(bar_kempty);
+      if (g.nchunks == 1) commit(bar_qempty);
+      for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
+        const uint32_t ph = chunk_ctr & 1;
+        const bool more = j + 1 < g.nchunks;
+        NA_EV(3, 2 * chunk_ctr);
+        mbar_wait(bar_pfull(0), ph);
+        NA_EV(4, 2 * chunk_ctr);
+        mbar_wait(bar_vfull, ph);
+        NA_EV(6, chunk_ctr);
+        if (j == 0) mbar_wait(bar_oempty, (tile_ctr & 1) ^ 1);
         tc_fence_after();
-        issue_s(0, chunk_ctr);
-        issue_s(1, chunk_ctr);
-        umma_commit(bar_kempty);
-        if (g.nchunks == 1) umma_commit(bar_qempty);
-        for (int j = 0; j < g.nchunks; ++j, ++chunk_ctr) {
-          const uint32_t ph = chunk_ctr & 1;
-          const bool more = j + 1 < g.nchunks;
-          NA_EV(3, 2 * chunk_ctr);
-          mbar_wait(bar_pfull(0), ph);
-          NA_EV(4, 2 * chunk_ctr);
-          mbar_wait(bar_vfull, ph);
-          NA_EV(6, chunk_ctr);
-          if (j == 0) mbar_wait(bar_oempty, (tile_ctr & 1) ^ 1);
+        issue_pv(0, j == 0, 0u);
+        if (more) {
+          NA_EV(7, chunk_ctr);
+          mbar_wait(bar_kfull, ph ^ 1);
+          NA_EV(8, chunk_ctr);
           tc_fence_after();
-          issue_pv(0, j == 0);
-          if (more) {
-            NA_EV(7, chunk_ctr);
-            mbar_wait(bar_kfull, ph ^ 1);
-            NA_EV(8, chunk_ctr);
-            tc_fence_after();
-            issue_s(0, chunk_ctr + 1);
-          }
-          NA_EV(3, 2 * chunk_ctr + 1);
-          mbar_wait(bar_pfull(1), ph);
-          NA_EV(4, 2 * chunk_ctr + 1);
-          tc_fence_after();
-          issue_pv(1, false);
-          umma_commit(bar_vempty);
-          if (!more) umma_commit(bar_ofull);
-          if (more) {
-            issue_s(1, chunk_ctr + 1);
-            umma_commit(bar_kempty);
-            if (j + 1 == g.nchunks - 1) umma_commit(bar_qempty);
-          }
+          issue_s(0);
+        }
+        NA_EV(3, 2 * chunk_ctr + 1);
+        mbar_wait(bar_pfull(1), ph);
+        NA_EV(4, 2 * chunk_ctr + 1);
+        tc_fence_after();
+        issue_pv(1, false, bar_vempty);
+        if (!more) commit(bar_ofull);
+        if (more) {
+          issue_s(1);
+          commit(bar_kempty);
+          if (j + 1 == g.nchunks - 1) commit(bar_qempty);
         }
       }
     }
@@ -451,7 +468,8 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
     const uint32_t tS = tmem + lane_off, tO = tmem + NA_TMEM_O + lane_off;
     const int hw = (p.ww - 1) / 2;
     const size_t member_tokens = static_cast<size_t>(p.depth) * p.rows * p.cols;
-    const int ocols = p.dhp / NA_SPLIT, oc0 = sub * ocols;  // O columns this thread rescales / stores
+    constexpr int ocols = DHP / NA_SPLIT;
+    const int oc0 = sub * ocols;  // O columns this thread rescales / stores
     int chunk_ctr = 0, tile_ctr = 0;
     for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
       const TileGeo g = tile_geo(p, item);
@@ -738,7 +756,8 @@ static int natten_launch(const void* qkv, int ldqkv, void* out, int ldo, int bat
   CUtensorMap tq, tkv;
   if (make_tmap(&tq, qkv, TMAP_BF16, 4, dims, strides, qbox, nullptr)) return -1;
   if (make_tmap(&tkv, qkv, TMAP_BF16, 4, dims, strides, kvbox, nullptr)) return -1;
-  for (auto kern : {natten_fwd_kernel<true>, natten_fwd_kernel<false>})
+  for (auto kern : {natten_fwd_kernel<true, 64>, natten_fwd_kernel<false, 64>, natten_fwd_kernel<true, 128>,
+                    natten_fwd_kernel<false, 128>})
     if (ensure_smem_attr(reinterpret_cast<const void*>(kern), NA_SMEM, "natten")) return -1;
   // window mask in the MMA when the tile's query classes fit the extra K = 16 step (WM3_NA_BIAS=0: softmax mask)
   static const bool bias_env = [] {
@@ -800,7 +819,9 @@ static int natten_launch(const void* qkv, int ldqkv, void* out, int ldo, int bat
   }
   const int slots = NA_CTAS_PER_SM * sm_count();
   const int grid = p.nitems < slots ? p.nitems : slots;
-  if (launch_pdl(bias ? natten_fwd_kernel<true> : natten_fwd_kernel<false>, dim3(grid), dim3(NA_THREADS), NA_SMEM,
+  auto kern = dhp == 64 ? (bias ? natten_fwd_kernel<true, 64> : natten_fwd_kernel<false, 64>)
+                        : (bias ? natten_fwd_kernel<true, 128> : natten_fwd_kernel<false, 128>);
+  if (launch_pdl(kern, dim3(grid), dim3(NA_THREADS), NA_SMEM,
                  reinterpret_cast<cudaStream_t>(stream), tq,
                  tkv, p))
     return -1;
