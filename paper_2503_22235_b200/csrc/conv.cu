@@ -147,32 +147,35 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc(CV_BM, BN, 0, 0);
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t aphase = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        mbar_wait(tempty_bar(acc), aphase ^ 1);
+    // The whole warp walks the k-blocks (warp-wide waits, warp-uniform descriptors in uniform registers);
+    // one elected lane issues the MMAs and commits.
+    constexpr uint32_t idesc = make_idesc(CV_BM, BN, 0, 0);
+    const uint64_t d0 = make_sdesc_sw128(sbase, 16, 1024);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      mbar_wait(tempty_bar(acc), aphase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(full_bar(stage), phase);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(full_bar(stage), phase);
-          tc_fence_after();
-          const uint32_t sa = sbase + stage * Cfg::STAGE_BYTES;
-          const uint32_t sb = sa + Cfg::A_BYTES;
+        const uint64_t da = d0 + ((stage * Cfg::STAGE_BYTES) >> 4), db = da + (Cfg::A_BYTES >> 4);
+        if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < CV_BK / 16; ++k)
-            umma_bf16_ss(d_tmem, make_sdesc_sw128(sa + k * 32, 16, 1024), make_sdesc_sw128(sb + k * 32, 16, 1024),
-                         idesc, (kb | k) != 0 ? 1u : 0u);
+            umma_bf16_ss(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
           umma_commit(empty_bar(stage));
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(tfull_bar(acc));
-        acc ^= 1;
-        if (acc == 0) aphase ^= 1;
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (elect_one()) umma_commit(tfull_bar(acc));
+      __syncwarp();
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
     }
   } else if (warp >= 4) {
     const int g = (warp - 4) >> 2;

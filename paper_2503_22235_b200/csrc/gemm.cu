@@ -273,8 +273,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {  // the leader issues the pair's MMAs
+    if (rank == 0) {  // the leader issues the pair's MMAs
+      // The whole warp walks the k-blocks (warp-wide waits, warp-uniform descriptors in uniform registers);
+      // one elected lane issues the MMAs and commits.
       constexpr uint32_t idesc = make_idesc(GEMM_BM * CG, BN, 0, 0);
+      const uint64_t d0 = make_sdesc_sw128(sbase, 16, 1024);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -286,27 +289,30 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(full_bar(stage), phase);
           tc_fence_after();
-          const uint32_t sa = sbase + stage * Cfg::STAGE_BYTES;
-          const uint32_t sb = sa + Cfg::A_BYTES;
+          const uint64_t ad = d0 + ((stage * Cfg::STAGE_BYTES) >> 4), bd = ad + (Cfg::A_BYTES >> 4);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < GEMM_BK / 16; ++k) {
-            const uint64_t ad = make_sdesc_sw128(sa + k * 32, 16, 1024);
-            const uint64_t bd = make_sdesc_sw128(sb + k * 32, 16, 1024);
+            for (int k = 0; k < GEMM_BK / 16; ++k) {
+              if (CG == 2)
+                umma_ss_cg2(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+              else
+                umma_bf16_ss(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+            }
             if (CG == 2)
-              umma_ss_cg2(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+              umma_commit_mc(empty_bar(stage), 0x3);  // frees the stage in both CTAs
             else
-              umma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+              umma_commit(empty_bar(stage));
           }
-          if (CG == 2)
-            umma_commit_mc(empty_bar(stage), 0x3);  // frees the stage in both CTAs
-          else
-            umma_commit(empty_bar(stage));
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        if (CG == 2)
-          umma_commit_mc(tfull_bar(acc), 0x3);
-        else
-          umma_commit(tfull_bar(acc));
+        if (elect_one()) {
+          if (CG == 2)
+            umma_commit_mc(tfull_bar(acc), 0x3);
+          else
+            umma_commit(tfull_bar(acc));
+        }
+        __syncwarp();
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
       }
