@@ -1,7 +1,7 @@
 # Build libwm3.so (sm_100a only) and the oracle's C helpers.
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr -Xptxas -v
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr -Xptxas -v $(NVFLAGS_EXTRA)
 PKG := paper_2503_22235_b200
 SRCS := $(wildcard $(PKG)/csrc/*.cu)
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/wm3.h

@@ -40,7 +40,7 @@ constexpr int NA_TRACE_MAX = 1 << 16;
 __device__ long long g_na_trace[NA_TRACE_MAX][3];
 __device__ int g_na_trace_n;
 DEVI void na_ev(int e, int c) {
-  if (blockIdx.x != 0) return;
+  if (blockIdx.x != 0 || (threadIdx.x & 31) != 0) return;
   const int i = atomicAdd(&g_na_trace_n, 1);
   if (i < NA_TRACE_MAX) {
     g_na_trace[i][0] = e;
@@ -99,6 +99,29 @@ constexpr uint32_t NA_SMEM = NA_SMEM_BODY + 1024 /*align*/ + 256 /*barriers*/ + 
 // because tcgen05.mma ops of one thread execute in issue order and S(c + 1) is issued after P V(c).
 constexpr uint32_t NA_TMEM_COLS = 256, NA_TMEM_O = 128;
 constexpr float NA_RESCALE_LOG2 = 8.0f;
+#ifndef WM3_NA_EMU
+#define WM3_NA_EMU 0
+#endif
+// Of every 8 key pairs of a half, NA_EMU have their exp2 evaluated on the FMA pipe (exp2_fma2) instead of the
+// MUFU, which otherwise is the softmax's binding pipe (64 MUFU.EX2 per thread per 64-key half).
+constexpr int NA_EMU = WM3_NA_EMU;
+
+// 2^x for a pair on the FMA / ALU pipes: x = n + f (n = rint(x) by the 1.5 * 2^23 shift, f in [-0.5, 0.5]),
+// 2^f by a degree-3 polynomial (relative error 7.5e-5, below the fp16 rounding of P), n added to the exponent
+// field.  x is clamped at -125 (masked keys: the result is ~2^-125, i.e. 0 once rounded to fp16).
+DEVI void exp2_fma2(float& p0, float& p1, float x0, float x1) {
+  x0 = fmaxf(x0, -125.f);
+  x1 = fmaxf(x1, -125.f);
+  float t0, t1, n0, n1, f0, f1, q0, q1;
+  fadd2(t0, t1, x0, x1, 12582912.f, 12582912.f);
+  fadd2(n0, n1, t0, t1, -12582912.f, -12582912.f);
+  fadd2(f0, f1, x0, x1, -n0, -n1);
+  ffma2(q0, q1, f0, f1, 0.05517132207751274f, 0.05517132207751274f, 0.24261054396629333f, 0.24261054396629333f);
+  ffma2(q0, q1, q0, q1, f0, f1, 0.6932609677314758f, 0.6932609677314758f);
+  ffma2(q0, q1, q0, q1, f0, f1, 0.9999281167984009f, 0.9999281167984009f);
+  p0 = __int_as_float(__float_as_int(q0) + (__float_as_int(t0) << 23));
+  p1 = __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23));
+}
 
 struct TileGeo {
   int head, b, d0, d1, h0, h1, w0, w1;
@@ -590,7 +613,10 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
               float e0, e1;  // exp2(-inf) = 0
               ffma2(e0, e1, __uint_as_float(x[k]), __uint_as_float(x[k + 1]), p.scale_log2, p.scale_log2, -m_use,
                     -m_use);
-              const float p0 = fast_exp2(e0), p1 = fast_exp2(e1);
+              float p0, p1;
+              if (NA_EMU > 0 && ((k >> 1) & 7) < NA_EMU) exp2_fma2(p0, p1, e0, e1);  // FMA pipe
+              else { p0 = fast_exp2(e0); p1 = fast_exp2(e1); }                      // MUFU
+
               const int a = (k >> 1) & 3;
               fadd2(lsa[2 * a], lsa[2 * a + 1], lsa[2 * a], lsa[2 * a + 1], p0, p1);
               pk[k >> 1] = pack_elem(p0, p1);
