@@ -66,7 +66,6 @@ struct NaParams {
   float scale_log2;
   const uint8_t* bias_table;  // BIAS: [tile][maxch] B_x images (4 KB each), built once per geometry
   int maxch;
-  int dbg;  // profiling switch (WM3_NA_DEBUG, bit flags): 1 skip softmax arithmetic, 2 skip Q K^T, 4 skip P V, 8 skip K/V loads
 };
 
 #ifndef WM3_NA_SPLIT
@@ -99,6 +98,12 @@ constexpr uint32_t NA_SMEM = NA_SMEM_BODY + 1024 /*align*/ + 256 /*barriers*/ + 
 // because tcgen05.mma ops of one thread execute in issue order and S(c + 1) is issued after P V(c).
 constexpr uint32_t NA_TMEM_COLS = 256, NA_TMEM_O = 128;
 constexpr float NA_RESCALE_LOG2 = 8.0f;
+#ifndef WM3_NA_DBG
+#define WM3_NA_DBG 0
+#endif
+// Profiling build switch (tools/build_variant.sh -DWM3_NA_DBG=...), bit flags: 1 skip softmax arithmetic,
+// 2 skip Q K^T, 4 skip P V, 8 skip K/V loads.  Compile-time so the product build carries no checks.
+constexpr int NA_DBG = WM3_NA_DBG;
 #ifndef WM3_NA_EMU
 #define WM3_NA_EMU 0
 #endif
@@ -358,7 +363,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
         NA_EV(10, c);
         mbar_wait(is_v ? bar_vempty : bar_kempty, (c & 1) ^ 1);
         NA_EV(11, c);
-        if (p.dbg & 8) {
+        if (NA_DBG & 8) {
           mbar_arrive(full);
           return;
         }
@@ -407,7 +412,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
       // S_h = Q K_h^T: keys [64 h, 64 h + 64) are rows [64 h, +64) of the K tile (SW128 K-major); descriptor
       // start addresses advance in 16-byte units
       if (elect_one()) {
-        if (!(p.dbg & 2)) {
+        if (!(NA_DBG & 2)) {
 #pragma unroll
           for (int s = 0; s < KSTEPS; ++s) {
             const uint32_t off = ((s >> 2) * 16384u + (s & 3) * 32u) >> 4;
@@ -415,7 +420,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
           }
         }
         if (BIAS)  // + window mask: one-hot query classes x key bias (keys 64 h ..)
-          umma_bf16_ss(tmem + 64 * h, dXA, dXB + h * 128u, idesc_s, (p.dbg & 2) ? 0u : 1u);
+          umma_bf16_ss(tmem + 64 * h, dXA, dXB + h * 128u, idesc_s, (NA_DBG & 2) ? 0u : 1u);
         umma_commit(bar_sfull(h));
       }
       __syncwarp();
@@ -423,7 +428,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
     auto issue_pv = [&](int h, bool first, uint32_t extra_bar) {
       // O += P_h V_h: A = P_h from TMEM columns [64 h, 64 h + 32) (fp16 pairs), B = V rows 64 h.. (MN-major)
       if (elect_one()) {
-        if (!(p.dbg & 4)) {
+        if (!(NA_DBG & 4)) {
 #pragma unroll
           for (int s = 0; s < 4; ++s)
             umma_f16_ts(tO, tmem + 64 * h + 8 * s, dV + (4 * h + s) * 128u, idesc_o, (!first || s > 0) ? 1u : 0u);
@@ -546,7 +551,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
           if (threadIdx.x == 0) NA_EV(1, 2 * chunk_ctr + h);
           tc_fence_after();
           uint32_t pk[CW / 2];
-          if (p.dbg & 1) {
+          if (NA_DBG & 1) {
 #pragma unroll
             for (int i = 0; i < CW / 2; ++i) pk[i] = 0u;
           } else {
@@ -768,10 +773,6 @@ static int natten_launch(const void* qkv, int ldqkv, void* out, int ldo, int bat
   p.ntw = (cols + p.TW - 1) / p.TW;
   p.nitems = p.ntd * p.nth * p.ntw * heads * batch;
   p.scale_log2 = scale * 1.4426950408889634f;
-  {
-    const char* e = getenv("WM3_NA_DEBUG");
-    p.dbg = e ? atoi(e) : 0;
-  }
 
   const uint64_t wp = cols;
   const uint64_t dims[4] = {static_cast<uint64_t>(3 * heads * dhp), wp, static_cast<uint64_t>(p.rows_ext),

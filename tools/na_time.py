@@ -17,4 +17,4 @@ for _ in range(20):
     ops.natten(qkv, grid, heads, dhp, dhp, win, out=out)
 e1.record()
 torch.cuda.synchronize()
-print(f"NA dbg={os.environ.get('WM3_NA_DEBUG', '0')}: {e0.elapsed_time(e1) / 20:.4f} ms")
+print(f"NA {os.environ.get('WM3_LIB') or 'default'}: {e0.elapsed_time(e1) / 20:.4f} ms")
