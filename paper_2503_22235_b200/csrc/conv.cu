@@ -48,32 +48,44 @@ struct ConvParams {
   int chan_div;
 };
 
-template <int BN>
+// CG = 2: CTA pairs (cluster of 2 on a TPC, tcgen05.mma.cta_group::2, M = 256): each CTA stages its own 128
+// output pixels and half of the BN weight rows, the leader issues the pair's MMAs, so per-SM operand traffic
+// from L2 drops from (16 KB A + BN x 128 B) to (16 KB A + BN x 64 B) per 64-deep k-block and the freed shared
+// memory deepens the ring.  (The Cout = 192 convs at 720 x 1440 were bound by that L2 -> SM operand stream.)
+template <int BN, int CG = 1>
 struct ConvCfg {
-  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 64 ? 8 : 5);
   static constexpr uint32_t A_BYTES = CV_BM * CV_BK * 2;
-  static constexpr uint32_t B_BYTES = BN * CV_BK * 2;
+  static constexpr uint32_t B_BYTES = (BN / CG) * CV_BK * 2;
+  static constexpr int STAGES_FIT = static_cast<int>((200u * 1024u) / (A_BYTES + B_BYTES));
+  static constexpr int STAGES = CG == 1 ? ((BN == 256) ? 4 : (BN == 64 ? 8 : 5)) : (STAGES_FIT < 8 ? STAGES_FIT : 8);
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
 };
 
-// m-tile -> image, class, output sub-grid row, first column
-DEVI void conv_tile(const ConvParams& p, int mt, int& img, int& cls, int& r, int& c0) {
-  const int per_img = p.nclass * p.tiles_per_class;
+// m-tile -> image, class, output sub-grid row, first column.  With CTA pairs an m-tile is a pair of
+// consecutive 128-pixel tiles of one (image, class) (the two halves of an M = 256 MMA share the class's
+// weights, not their pixels); rank r takes the r-th; a missing second tile (odd count) is a dummy (`valid`
+// false: its loads stay in bounds and nothing is stored).
+template <int CG>
+DEVI void conv_tile(const ConvParams& p, int mt, int rank, int& img, int& cls, int& r, int& c0, bool& valid) {
+  const int per_class = (p.tiles_per_class + CG - 1) / CG;
+  const int per_img = p.nclass * per_class;
   img = mt / per_img;
   int rest = mt - img * per_img;
-  cls = rest / p.tiles_per_class;
-  rest -= cls * p.tiles_per_class;
-  r = rest / p.tiles_per_row;
-  c0 = (rest - r * p.tiles_per_row) * CV_BM;
+  cls = rest / per_class;
+  int t = (rest - cls * per_class) * CG + rank;
+  valid = t < p.tiles_per_class;
+  if (!valid) t = p.tiles_per_class - 1;
+  r = t / p.tiles_per_row;
+  c0 = (t - r * p.tiles_per_row) * CV_BM;
 }
 
-template <int BN>
+template <int BN, int CG>
 __global__ void __launch_bounds__(CV_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, ConvParams p) {
   griddep_launch_dependents();  // PDL: the next kernel may start its prologue
-  using Cfg = ConvCfg<BN>;
+  using Cfg = ConvCfg<BN, CG>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -89,8 +101,12 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nn = p.cout_pad / BN;
-  const int ntiles = p.imgs * p.nclass * p.tiles_per_class * nn;
+  const int ntiles = p.imgs * p.nclass * ((p.tiles_per_class + CG - 1) / CG) * nn;
   const int nk = p.ntap * p.ncb;
+  // CTA pairs: cluster = (2k, 2k + 1) walks the pair tiles together
+  const int rank = (CG == 2) ? static_cast<int>(cluster_ctarank()) : 0;
+  const int tile0 = (CG == 2) ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int tstep = (CG == 2) ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -101,16 +117,24 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
-      mbar_init(tempty_bar(a), 8);
+      mbar_init(tempty_bar(a), 8 * CG);  // every epilogue warp of the pair arrives on the leader's barrier
     }
     fence_barrier_init();
   }
   if (warp == 2) {
-    tmem_alloc(smem_u32(tmem_slot), Cfg::TMEM_COLS);
-    tmem_relinquish();
+    if (CG == 2) {
+      tmem_alloc_cg2(smem_u32(tmem_slot), Cfg::TMEM_COLS);
+      tmem_relinquish_cg2();
+    } else {
+      tmem_alloc(smem_u32(tmem_slot), Cfg::TMEM_COLS);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();  // both CTAs' barriers exist before any cross-CTA arrive / TMA completion
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   griddep_wait();  // PDL: inputs are complete from here on
@@ -120,62 +144,78 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       const int hp = p.hin + 2;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int tile = tile0; tile < ntiles; tile += tstep) {
         int img, cls, r, c0;
-        conv_tile(p, tile / nn, img, cls, r, c0);
-        const int n0 = (tile % nn) * BN;
+        bool valid;
+        conv_tile<CG>(p, tile / nn, rank, img, cls, r, c0, valid);
+        const int n0 = (tile % nn) * BN + rank * (BN / CG);
         const int a = cls >> 1, b = cls & 1;
         for (int kb = 0; kb < nk; ++kb) {
           const int tap = kb / p.ncb, cb = kb - tap * p.ncb;
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sa = sbase + stage * Cfg::STAGE_BYTES;
           const uint32_t sb = sa + Cfg::A_BYTES;
-          mbar_arrive_expect_tx(full_bar(stage), Cfg::STAGE_BYTES);
+          // pairs: both CTAs' bytes complete on the leader's full barrier; only the leader arms it
+          const uint32_t fb = (CG == 2) ? mapa_shared(full_bar(stage), 0) : full_bar(stage);
+          if (rank == 0) mbar_arrive_expect_tx(full_bar(stage), CG * Cfg::STAGE_BYTES);
           if (p.mode == WM3_CONV_S2) {
             const int kh = tap / 3, kw = tap - 3 * (tap / 3);
-            tma_load_4d(sa, &tmA, full_bar(stage), cb * CV_BK, kw & 1, c0 + (kw >> 1), img * hp + 2 * r + kh);
+            if (CG == 2) tma_load_4d_cg2(sa, &tmA, fb, cb * CV_BK, kw & 1, c0 + (kw >> 1), img * hp + 2 * r + kh);
+            else tma_load_4d(sa, &tmA, fb, cb * CV_BK, kw & 1, c0 + (kw >> 1), img * hp + 2 * r + kh);
           } else if (p.mode == WM3_CONV_S1) {
             const int kh = tap / 3, kw = tap - 3 * (tap / 3);
-            tma_load_3d(sa, &tmA, full_bar(stage), cb * CV_BK, c0 + kw, img * hp + r + kh);
+            if (CG == 2) tma_load_3d_cg2(sa, &tmA, fb, cb * CV_BK, c0 + kw, img * hp + r + kh);
+            else tma_load_3d(sa, &tmA, fb, cb * CV_BK, c0 + kw, img * hp + r + kh);
           } else {  // transposed, parity class (a, b), tap (tr, tc)
             const int tr = tap >> 1, tc = tap & 1;
-            tma_load_3d(sa, &tmA, full_bar(stage), cb * CV_BK, c0 + b + tc, img * hp + r + a + tr);
+            if (CG == 2) tma_load_3d_cg2(sa, &tmA, fb, cb * CV_BK, c0 + b + tc, img * hp + r + a + tr);
+            else tma_load_3d(sa, &tmA, fb, cb * CV_BK, c0 + b + tc, img * hp + r + a + tr);
           }
-          tma_load_2d(sb, &tmB, full_bar(stage), kb * CV_BK, cls * p.cout_pad + n0);
+          if (CG == 2) tma_load_2d_cg2(sb, &tmB, fb, kb * CV_BK, cls * p.cout_pad + n0);
+          else tma_load_2d(sb, &tmB, fb, kb * CV_BK, cls * p.cout_pad + n0);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // The whole warp walks the k-blocks (warp-wide waits, warp-uniform descriptors in uniform registers);
-    // one elected lane issues the MMAs and commits.
-    constexpr uint32_t idesc = make_idesc(CV_BM, BN, 0, 0);
-    const uint64_t d0 = make_sdesc_sw128(sbase, 16, 1024);
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t aphase = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      mbar_wait(tempty_bar(acc), aphase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < nk; ++kb) {
-        mbar_wait(full_bar(stage), phase);
+    // one elected lane issues the MMAs and commits.  Pairs: the leader issues M = 256 MMAs for both CTAs and
+    // its commits arrive on both CTAs' barriers.
+    if (rank == 0) {
+      constexpr uint32_t idesc = make_idesc(CV_BM * CG, BN, 0, 0);
+      const uint64_t d0 = make_sdesc_sw128(sbase, 16, 1024);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int tile = tile0; tile < ntiles; tile += tstep) {
+        mbar_wait(tempty_bar(acc), aphase ^ 1);
         tc_fence_after();
-        const uint64_t da = d0 + ((stage * Cfg::STAGE_BYTES) >> 4), db = da + (Cfg::A_BYTES >> 4);
-        if (elect_one()) {
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(full_bar(stage), phase);
+          tc_fence_after();
+          const uint64_t da = d0 + ((stage * Cfg::STAGE_BYTES) >> 4), db = da + (Cfg::A_BYTES >> 4);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < CV_BK / 16; ++k)
-            umma_bf16_ss(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
-          umma_commit(empty_bar(stage));
+            for (int k = 0; k < CV_BK / 16; ++k) {
+              if (CG == 2) umma_ss_cg2(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+              else umma_bf16_ss(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+            }
+            if (CG == 2) umma_commit_mc(empty_bar(stage), 0x3);  // frees the stage in both CTAs
+            else umma_commit(empty_bar(stage));
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (elect_one()) {
+          if (CG == 2) umma_commit_mc(tfull_bar(acc), 0x3);
+          else umma_commit(tfull_bar(acc));
         }
         __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
       }
-      if (elect_one()) umma_commit(tfull_bar(acc));
-      __syncwarp();
-      acc ^= 1;
-      if (acc == 0) aphase ^= 1;
     }
   } else if (warp >= 4) {
     const int g = (warp - 4) >> 2;
@@ -183,12 +223,14 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
     const int i = 32 * q + lane;  // pixel within the tile
     int acc = 0;
     uint32_t aphase = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t tempty_leader0 = (CG == 2) ? mapa_shared(tempty_bar(0), 0) : 0u;
+    for (int tile = tile0; tile < ntiles; tile += tstep) {
       int img, cls, r, c0;
-      conv_tile(p, tile / nn, img, cls, r, c0);
+      bool valid;
+      conv_tile<CG>(p, tile / nn, rank, img, cls, r, c0, valid);
       const int n0 = (tile % nn) * BN;
       const int col = c0 + i;
-      const bool ok = col < p.cols_t;
+      const bool ok = valid && col < p.cols_t;
       // output pixel
       int orow = r, ocol = col;
       if (p.mode == WM3_CONV_T2) { orow = 2 * r + (cls >> 1); ocol = 2 * col + (cls & 1); }
@@ -263,16 +305,23 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty_bar(acc));
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(tempty_leader0 + 8u * acc);  // the leader's MMA warp reuses it
+        else mbar_arrive(tempty_bar(acc));
+      }
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();  // the pair's MMAs read this CTA's smem and write its TMEM until the last tile
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    if (CG == 2) tmem_dealloc_cg2(tmem_base, Cfg::TMEM_COLS);
+    else tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
 }
 
@@ -363,13 +412,34 @@ __global__ void tokens_to_nhwc_kernel(const float* __restrict__ tok, int imgs, i
   }
 }
 
-template <int BN>
+template <int BN, int CG>
 static int launch_conv(const CUtensorMap& ta, const CUtensorMap& tb, const ConvParams& p, cudaStream_t s) {
-  using Cfg = ConvCfg<BN>;
-  if (ensure_smem_attr(reinterpret_cast<const void*>(conv_tc_kernel<BN>), Cfg::SMEM, "conv")) return -1;
-  const long long ntiles = static_cast<long long>(p.imgs) * p.nclass * p.tiles_per_class * (p.cout_pad / BN);
-  const int grid = static_cast<int>(ntiles < sm_count() ? ntiles : sm_count());
-  if (launch_pdl(conv_tc_kernel<BN>, dim3(grid), dim3(CV_THREADS), Cfg::SMEM, s, ta, tb, p)) return -1;
+  using Cfg = ConvCfg<BN, CG>;
+  const void* kern = reinterpret_cast<const void*>(conv_tc_kernel<BN, CG>);
+  if (ensure_smem_attr(kern, Cfg::SMEM, "conv")) return -1;
+  const long long ntiles =
+      static_cast<long long>(p.imgs) * p.nclass * ((p.tiles_per_class + CG - 1) / CG) * (p.cout_pad / BN);
+  if (CG == 1) {
+    const int grid = static_cast<int>(ntiles < sm_count() ? ntiles : sm_count());
+    if (launch_pdl(conv_tc_kernel<BN, 1>, dim3(grid), dim3(CV_THREADS), Cfg::SMEM, s, ta, tb, p)) return -1;
+    return check_launch("conv_tc_kernel");
+  }
+  const int pairs = sm_count() / 2;
+  const int grid = 2 * static_cast<int>(ntiles < pairs ? ntiles : pairs);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(CV_THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, conv_tc_kernel<BN, 2>, ta, tb, p) != cudaSuccess)
+    return set_error("conv_tc_kernel (pairs): launch failed: %s", cudaGetErrorString(cudaGetLastError()));
   return check_launch("conv_tc_kernel");
 }
 
@@ -434,12 +504,25 @@ extern "C" int wm3_conv(int mode, const void* in, int imgs, int hin, int win, in
   }
   // B: weights [class][cout_pad][ntap * cinp], K-major
   const int kdim = p.ntap * cinp;
-  if (make_tmap_2d_bf16(&tb, w, kdim, static_cast<uint64_t>(p.nclass) * p.cout_pad, kdim, CV_BK, bn)) return -1;
+  // CTA pairs (WM3_CONV_PAIRS=0 turns them off, A/B aid): each CTA's weight box is half of the BN rows.
+  // Measured (full-scale encode + decode, one B200): the 3x3 / transposed convs with Cout >= 128 run 7-12 %
+  // faster (encode 27.3 -> 25.4 ms device time); the BN = 64 heads 20-25 % slower, so they stay single-CTA.
+  static const bool pairs_env = [] {
+    const char* e = getenv("WM3_CONV_PAIRS");
+    return !(e && e[0] == '0');
+  }();
+  const int cg = (pairs_env && bn >= 128) ? 2 : 1;  // heads (BN = 64) stream A only: pairs measured slower
+  if (make_tmap_2d_bf16(&tb, w, kdim, static_cast<uint64_t>(p.nclass) * p.cout_pad, kdim, CV_BK, bn / cg)) return -1;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (bn == 64) return launch_conv<64>(ta, tb, p, s);
-  if (bn == 128) return launch_conv<128>(ta, tb, p, s);
-  if (bn == 192) return launch_conv<192>(ta, tb, p, s);
-  return launch_conv<256>(ta, tb, p, s);
+  if (cg == 2) {
+    if (bn == 128) return launch_conv<128, 2>(ta, tb, p, s);
+    if (bn == 192) return launch_conv<192, 2>(ta, tb, p, s);
+    return launch_conv<256, 2>(ta, tb, p, s);
+  }
+  if (bn == 64) return launch_conv<64, 1>(ta, tb, p, s);
+  if (bn == 128) return launch_conv<128, 1>(ta, tb, p, s);
+  if (bn == 192) return launch_conv<192, 1>(ta, tb, p, s);
+  return launch_conv<256, 1>(ta, tb, p, s);
 }
 
 extern "C" int wm3_fields_to_nhwc(const float* src, long long img_stride, long long a_stride, long long p_stride,
