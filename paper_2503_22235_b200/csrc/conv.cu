@@ -52,13 +52,22 @@ struct ConvParams {
 // output pixels and half of the BN weight rows, the leader issues the pair's MMAs, so per-SM operand traffic
 // from L2 drops from (16 KB A + BN x 128 B) to (16 KB A + BN x 64 B) per 64-deep k-block and the freed shared
 // memory deepens the ring.  (The Cout = 192 convs at 720 x 1440 were bound by that L2 -> SM operand stream.)
-template <int BN, int CG = 1>
+// STRIP (stride-1 convs): a stage holds one strip of 130 input pixels of a kernel row (kh, channel block) and
+// the three column taps' weight boxes; the MMAs of tap kw read the strip from row kw (descriptor start + kw x
+// 128 B), so the A operand crosses L2 -> SM once per kernel row instead of once per tap.
+constexpr int CV_STRIP_ROWS = CV_BM + 2;
+template <int BN, int CG = 1, bool STRIP = false>
 struct ConvCfg {
-  static constexpr uint32_t A_BYTES = CV_BM * CV_BK * 2;
-  static constexpr uint32_t B_BYTES = (BN / CG) * CV_BK * 2;
-  static constexpr int STAGES_FIT = static_cast<int>((200u * 1024u) / (A_BYTES + B_BYTES));
-  static constexpr int STAGES = CG == 1 ? ((BN == 256) ? 4 : (BN == 64 ? 8 : 5)) : (STAGES_FIT < 8 ? STAGES_FIT : 8);
+  static constexpr int TAPS = STRIP ? 3 : 1;  // weight boxes per stage
+  static constexpr uint32_t A_BYTES = STRIP ? 17408u : CV_BM * CV_BK * 2;  // 130 rows x 128 B, 1 KB aligned
+  static constexpr uint32_t B1_BYTES = (BN / CG) * CV_BK * 2;
+  static constexpr uint32_t B_BYTES = TAPS * B1_BYTES;
+  static constexpr uint32_t A_TX = STRIP ? CV_STRIP_ROWS * 128u : A_BYTES;  // bytes TMA writes
+  static constexpr int STAGES_FIT = static_cast<int>((224u * 1024u - 1280u) / (A_BYTES + B_BYTES));
+  static constexpr int STAGES = (CG == 1 && !STRIP) ? ((BN == 256) ? 4 : (BN == 64 ? 8 : 5))
+                                                    : (STAGES_FIT < 8 ? STAGES_FIT : 8);
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t TX_BYTES = A_TX + B_BYTES;
   static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
 };
@@ -81,11 +90,11 @@ DEVI void conv_tile(const ConvParams& p, int mt, int rank, int& img, int& cls, i
   c0 = (t - r * p.tiles_per_row) * CV_BM;
 }
 
-template <int BN, int CG>
+template <int BN, int CG, bool STRIP>
 __global__ void __launch_bounds__(CV_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, ConvParams p) {
   griddep_launch_dependents();  // PDL: the next kernel may start its prologue
-  using Cfg = ConvCfg<BN, CG>;
+  using Cfg = ConvCfg<BN, CG, STRIP>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -102,7 +111,7 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
   const int lane = threadIdx.x & 31;
   const int nn = p.cout_pad / BN;
   const int ntiles = p.imgs * p.nclass * ((p.tiles_per_class + CG - 1) / CG) * nn;
-  const int nk = p.ntap * p.ncb;
+  const int nk = (STRIP ? 3 : p.ntap) * p.ncb;  // stages per tile
   // CTA pairs: cluster = (2k, 2k + 1) walks the pair tiles together
   const int rank = (CG == 2) ? static_cast<int>(cluster_ctarank()) : 0;
   const int tile0 = (CG == 2) ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
@@ -151,14 +160,24 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
         const int n0 = (tile % nn) * BN + rank * (BN / CG);
         const int a = cls >> 1, b = cls & 1;
         for (int kb = 0; kb < nk; ++kb) {
-          const int tap = kb / p.ncb, cb = kb - tap * p.ncb;
+          const int tap = kb / p.ncb, cb = kb - tap * p.ncb;  // STRIP: `tap` is the kernel row kh
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sa = sbase + stage * Cfg::STAGE_BYTES;
           const uint32_t sb = sa + Cfg::A_BYTES;
           // pairs: both CTAs' bytes complete on the leader's full barrier; only the leader arms it
           const uint32_t fb = (CG == 2) ? mapa_shared(full_bar(stage), 0) : full_bar(stage);
-          if (rank == 0) mbar_arrive_expect_tx(full_bar(stage), CG * Cfg::STAGE_BYTES);
-          if (p.mode == WM3_CONV_S2) {
+          if (rank == 0) mbar_arrive_expect_tx(full_bar(stage), CG * Cfg::TX_BYTES);
+          if (STRIP) {
+            // strip of padded columns [c0, c0 + 130) of input row r + kh; weights of taps (kh, 0..2)
+            if (CG == 2) tma_load_3d_cg2(sa, &tmA, fb, cb * CV_BK, c0, img * hp + r + tap);
+            else tma_load_3d(sa, &tmA, fb, cb * CV_BK, c0, img * hp + r + tap);
+#pragma unroll
+            for (int kw = 0; kw < 3; ++kw) {
+              const int kcol = ((3 * tap + kw) * p.ncb + cb) * CV_BK;
+              if (CG == 2) tma_load_2d_cg2(sb + kw * Cfg::B1_BYTES, &tmB, fb, kcol, cls * p.cout_pad + n0);
+              else tma_load_2d(sb + kw * Cfg::B1_BYTES, &tmB, fb, kcol, cls * p.cout_pad + n0);
+            }
+          } else if (p.mode == WM3_CONV_S2) {
             const int kh = tap / 3, kw = tap - 3 * (tap / 3);
             if (CG == 2) tma_load_4d_cg2(sa, &tmA, fb, cb * CV_BK, kw & 1, c0 + (kw >> 1), img * hp + 2 * r + kh);
             else tma_load_4d(sa, &tmA, fb, cb * CV_BK, kw & 1, c0 + (kw >> 1), img * hp + 2 * r + kh);
@@ -171,8 +190,10 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
             if (CG == 2) tma_load_3d_cg2(sa, &tmA, fb, cb * CV_BK, c0 + b + tc, img * hp + r + a + tr);
             else tma_load_3d(sa, &tmA, fb, cb * CV_BK, c0 + b + tc, img * hp + r + a + tr);
           }
-          if (CG == 2) tma_load_2d_cg2(sb, &tmB, fb, kb * CV_BK, cls * p.cout_pad + n0);
-          else tma_load_2d(sb, &tmB, fb, kb * CV_BK, cls * p.cout_pad + n0);
+          if (!STRIP) {
+            if (CG == 2) tma_load_2d_cg2(sb, &tmB, fb, kb * CV_BK, cls * p.cout_pad + n0);
+            else tma_load_2d(sb, &tmB, fb, kb * CV_BK, cls * p.cout_pad + n0);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -198,9 +219,18 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
           const uint64_t da = d0 + ((stage * Cfg::STAGE_BYTES) >> 4), db = da + (Cfg::A_BYTES >> 4);
           if (elect_one()) {
 #pragma unroll
-            for (int k = 0; k < CV_BK / 16; ++k) {
-              if (CG == 2) umma_ss_cg2(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
-              else umma_bf16_ss(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+            for (int kw = 0; kw < Cfg::TAPS; ++kw) {
+              // tap kw reads strip rows [kw, kw + 128): start address + kw x 128 B.  The MMA unit swizzles on
+              // the absolute shared-memory address (as TMA wrote it), so the descriptor's base-offset field
+              // stays 0 (setting it to kw broke parity, measured).
+              const uint64_t dak = da + 8u * kw;
+              const uint64_t dbk = db + kw * (Cfg::B1_BYTES >> 4);
+#pragma unroll
+              for (int k = 0; k < CV_BK / 16; ++k) {
+                const uint32_t acc_on = (kb | kw | k) != 0 ? 1u : 0u;
+                if (CG == 2) umma_ss_cg2(d_tmem, dak + 2 * k, dbk + 2 * k, idesc, acc_on);
+                else umma_bf16_ss(d_tmem, dak + 2 * k, dbk + 2 * k, idesc, acc_on);
+              }
             }
             if (CG == 2) umma_commit_mc(empty_bar(stage), 0x3);  // frees the stage in both CTAs
             else umma_commit(empty_bar(stage));
@@ -412,16 +442,16 @@ __global__ void tokens_to_nhwc_kernel(const float* __restrict__ tok, int imgs, i
   }
 }
 
-template <int BN, int CG>
+template <int BN, int CG, bool STRIP>
 static int launch_conv(const CUtensorMap& ta, const CUtensorMap& tb, const ConvParams& p, cudaStream_t s) {
-  using Cfg = ConvCfg<BN, CG>;
-  const void* kern = reinterpret_cast<const void*>(conv_tc_kernel<BN, CG>);
-  if (ensure_smem_attr(kern, Cfg::SMEM, "conv")) return -1;
+  using Cfg = ConvCfg<BN, CG, STRIP>;
+  auto kern = conv_tc_kernel<BN, CG, STRIP>;
+  if (ensure_smem_attr(reinterpret_cast<const void*>(kern), Cfg::SMEM, "conv")) return -1;
   const long long ntiles =
       static_cast<long long>(p.imgs) * p.nclass * ((p.tiles_per_class + CG - 1) / CG) * (p.cout_pad / BN);
   if (CG == 1) {
     const int grid = static_cast<int>(ntiles < sm_count() ? ntiles : sm_count());
-    if (launch_pdl(conv_tc_kernel<BN, 1>, dim3(grid), dim3(CV_THREADS), Cfg::SMEM, s, ta, tb, p)) return -1;
+    if (launch_pdl(kern, dim3(grid), dim3(CV_THREADS), Cfg::SMEM, s, ta, tb, p)) return -1;
     return check_launch("conv_tc_kernel");
   }
   const int pairs = sm_count() / 2;
@@ -438,14 +468,45 @@ static int launch_conv(const CUtensorMap& ta, const CUtensorMap& tb, const ConvP
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, conv_tc_kernel<BN, 2>, ta, tb, p) != cudaSuccess)
+  if (cudaLaunchKernelEx(&cfg, kern, ta, tb, p) != cudaSuccess)
     return set_error("conv_tc_kernel (pairs): launch failed: %s", cudaGetErrorString(cudaGetLastError()));
   return check_launch("conv_tc_kernel");
+}
+
+template <int BN, int CG>
+static int launch_conv_mode(const CUtensorMap& ta, const CUtensorMap& tb, const ConvParams& p, cudaStream_t s,
+                            bool strip) {
+  // the strip stage (A strip + three weight boxes) must still leave a 3-deep ring
+  if (strip && ConvCfg<BN, CG, true>::STAGES_FIT >= 3) return launch_conv<BN, CG, true>(ta, tb, p, s);
+  return launch_conv<BN, CG, false>(ta, tb, p, s);
 }
 
 }  // namespace wm3
 
 using namespace wm3;
+
+// CTA pairs (WM3_CONV_PAIRS=0 turns them off, A/B aid): each CTA's weight box is half of the BN rows.
+// Measured (full-scale encode + decode, one B200): the 3x3 / transposed convs with Cout >= 128 run 7-12 %
+// faster (encode 27.3 -> 25.4 ms device time); the BN = 64 heads 20-25 % slower, so they stay single-CTA.
+static bool conv_pairs_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("WM3_CONV_PAIRS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+static bool conv_strip_fits(int bn, int cg) {
+  switch (bn * 4 + cg) {
+    case 64 * 4 + 1: return ConvCfg<64, 1, true>::STAGES_FIT >= 3;
+    case 128 * 4 + 1: return ConvCfg<128, 1, true>::STAGES_FIT >= 3;
+    case 192 * 4 + 1: return ConvCfg<192, 1, true>::STAGES_FIT >= 3;
+    case 256 * 4 + 1: return ConvCfg<256, 1, true>::STAGES_FIT >= 3;
+    case 128 * 4 + 2: return ConvCfg<128, 2, true>::STAGES_FIT >= 3;
+    case 192 * 4 + 2: return ConvCfg<192, 2, true>::STAGES_FIT >= 3;
+    case 256 * 4 + 2: return ConvCfg<256, 2, true>::STAGES_FIT >= 3;
+    default: return false;
+  }
+}
 
 extern "C" int wm3_conv_bn(int cout) {
   if (cout <= 64) return 64;  // decoder heads (17 / 35 channels): half the MMA columns of a 128 tile
@@ -487,6 +548,14 @@ extern "C" int wm3_conv(int mode, const void* in, int imgs, int hin, int win, in
   p.out_cp = out_cp;
   p.img_stride = img_stride; p.a_stride = a_stride; p.p_stride = p_stride; p.chan_div = chan_div > 0 ? chan_div : 1;
   if (out_kind == WM3_CONV_OUT_NHWC && (out_cp % 64 || out_cp < cout)) return set_error("wm3_conv: bad out_cp");
+  // stride-1 convs stage one 130-pixel strip per kernel row for its three column taps (WM3_CONV_STRIP=0: per tap)
+  static const bool strip_env = [] {
+    const char* e = getenv("WM3_CONV_STRIP");
+    return !(e && e[0] == '0');
+  }();
+  const int bn_ = wm3_conv_bn(cout);
+  const bool pairs_ = conv_pairs_enabled() && bn_ >= 128;
+  const bool strip = strip_env && mode == WM3_CONV_S1 && conv_strip_fits(bn_, pairs_ ? 2 : 1);
   // A: padded NHWC input, images stacked along rows
   CUtensorMap ta, tb;
   const uint64_t wp = win + 2;
@@ -499,30 +568,23 @@ extern "C" int wm3_conv(int mode, const void* in, int imgs, int hin, int win, in
   } else {
     const uint64_t dims[3] = {static_cast<uint64_t>(cinp), wp, rows};
     const uint64_t strides[2] = {static_cast<uint64_t>(cinp), wp * cinp};
-    const uint32_t box[3] = {64, CV_BM, 1};
+    const uint32_t box[3] = {64, static_cast<uint32_t>(strip ? CV_STRIP_ROWS : CV_BM), 1};
     if (make_tmap(&ta, in, TMAP_BF16, 3, dims, strides, box, nullptr)) return -1;
   }
   // B: weights [class][cout_pad][ntap * cinp], K-major
   const int kdim = p.ntap * cinp;
-  // CTA pairs (WM3_CONV_PAIRS=0 turns them off, A/B aid): each CTA's weight box is half of the BN rows.
-  // Measured (full-scale encode + decode, one B200): the 3x3 / transposed convs with Cout >= 128 run 7-12 %
-  // faster (encode 27.3 -> 25.4 ms device time); the BN = 64 heads 20-25 % slower, so they stay single-CTA.
-  static const bool pairs_env = [] {
-    const char* e = getenv("WM3_CONV_PAIRS");
-    return !(e && e[0] == '0');
-  }();
-  const int cg = (pairs_env && bn >= 128) ? 2 : 1;  // heads (BN = 64) stream A only: pairs measured slower
+  const int cg = pairs_ ? 2 : 1;
   if (make_tmap_2d_bf16(&tb, w, kdim, static_cast<uint64_t>(p.nclass) * p.cout_pad, kdim, CV_BK, bn / cg)) return -1;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (cg == 2) {
-    if (bn == 128) return launch_conv<128, 2>(ta, tb, p, s);
-    if (bn == 192) return launch_conv<192, 2>(ta, tb, p, s);
-    return launch_conv<256, 2>(ta, tb, p, s);
+    if (bn == 128) return launch_conv_mode<128, 2>(ta, tb, p, s, strip);
+    if (bn == 192) return launch_conv_mode<192, 2>(ta, tb, p, s, strip);
+    return launch_conv_mode<256, 2>(ta, tb, p, s, strip);
   }
-  if (bn == 64) return launch_conv<64, 1>(ta, tb, p, s);
-  if (bn == 128) return launch_conv<128, 1>(ta, tb, p, s);
-  if (bn == 192) return launch_conv<192, 1>(ta, tb, p, s);
-  return launch_conv<256, 1>(ta, tb, p, s);
+  if (bn == 64) return launch_conv_mode<64, 1>(ta, tb, p, s, strip);
+  if (bn == 128) return launch_conv_mode<128, 1>(ta, tb, p, s, strip);
+  if (bn == 192) return launch_conv_mode<192, 1>(ta, tb, p, s, strip);
+  return launch_conv_mode<256, 1>(ta, tb, p, s, strip);
 }
 
 extern "C" int wm3_fields_to_nhwc(const float* src, long long img_stride, long long a_stride, long long p_stride,
