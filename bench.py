@@ -217,7 +217,7 @@ def timed(fn, steps, stream, world):
 def load_traffic() -> dict:
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from the committed ncu capture."""
     try:
-        return json.load(open(os.path.join(ROOT, "profiles", "traffic_r1.json")))["bytes_per_launch"]
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic_r2.json")))["bytes_per_launch"]
     except Exception:
         return {}
 
