@@ -51,6 +51,14 @@ class _Scale:
             return 1.0
         return 2.0 ** (14 - math.ceil(math.log2(amax)))
 
+    def inv(self) -> torch.Tensor:
+        """1 / value() as a one-element device tensor (no host synchronisation)."""
+        amax = self.bits.view(torch.float32)
+        ok = (amax > 0) & torch.isfinite(amax)
+        e = torch.where(ok, torch.ceil(torch.log2(torch.where(ok, amax, torch.ones_like(amax)))) - 14,
+                        torch.zeros_like(amax))
+        return torch.exp2(e)
+
 
 def _amax(g: torch.Tensor, rows: int, cols: int) -> _Scale:
     s = _Scale(g.device)
@@ -137,22 +145,35 @@ def _transposed_weights(bw) -> dict:
     return t
 
 
-def block_vjp(x, params: dict, prefix: str, extents, window, heads: int, gy):
-    """(gx, grads) of y = natten_block(x) for the output gradient gy; numpy float64 in the reference layouts."""
-    from .attention import to_device_f32, validate_block_args
-    extents = tuple(int(e) for e in extents)
-    window = tuple(int(w) for w in window)
-    xd = to_device_f32(x)
+class BlockGrads:
+    """Device fp32 accumulators of one block's parameter gradients, in the kernel layouts (padded, q/k pairs
+    interleaved) and unscaled; `add` sums repeated applications of the block (a rollout reuses its processor)."""
+
+    def __init__(self):
+        self.t: dict = {}
+
+    def add(self, name: str, g: torch.Tensor, scale: _Scale | None = None) -> None:
+        if scale is not None:
+            g = g * scale.inv()
+        cur = self.t.get(name)
+        if cur is None:
+            self.t[name] = g.clone() if scale is None else g
+        else:
+            cur.add_(g)
+
+
+def block_vjp_device(xd: torch.Tensor, bw, extents, window, heads: int, dh: int, gyd: torch.Tensor,
+                     acc: BlockGrads) -> torch.Tensor:
+    """Device reverse mode of one block: returns gx (fp32, (T, hidden)) for the output cotangent gyd and adds the
+    parameter gradients to `acc`.  Forward recompute from the block input xd (nothing else is saved, like a
+    checkpointed segment, autodiff.py:893-924); one stream, no host synchronisation."""
     T, D = xd.shape
-    dh = validate_block_args((T, D), extents, window, heads)
-    bw = CACHE.block(params, prefix, heads)
     dev = xd.device
     dhp, hd, kp, np_, nm = bw.dhp, bw.heads * bw.dhp, bw.kp, bw.np_, bw.nm
     Tp = _r8(T)
     L = _lib
     wt = _transposed_weights(bw)
     rope = CACHE.rope(extents, dh)
-
     # ---- forward recompute (the kernels of the block forward, keeping the intermediates) ----
     hn = ops.layernorm_bf16(xd, bw.ln1_g, bw.ln1_b, ldo=kp)
     grid = ops.KVGrid(extents, window)
@@ -166,7 +187,6 @@ def block_vjp(x, params: dict, prefix: str, extents, window, heads: int, gy):
     mid = ops.linear(hn2, bw.w_1, L.WM3_EPI_BIAS_GELU_BF16, bias=bw.b_1)  # GELU output as the forward stores it
 
     # ---- W2 ----
-    gyd = to_device_f32(gy)
     s1 = _amax(gyd, T, D)
     gyh = _cast(gyd, T, D, np_, scale=s1)
     gyT = _cast(gyd, T, D, Tp, transpose=True, scale=s1)
@@ -220,14 +240,31 @@ def block_vjp(x, params: dict, prefix: str, extents, window, heads: int, gy):
     dln1_g = _colsum(gxh1, T, D)
     dln1_b = _colsum(gsc1, T, D)
 
-    # ---- back to the reference layouts (float64, (in, out) matrices) ----
-    def h(t, s=None):
-        a = t.double().cpu().numpy()
-        return a / s.value() if s is not None else a
+    acc.add("w_qkv", dwqkv, s4)
+    acc.add("b_qkv", dbqkv)
+    acc.add("w_o", dwo, s3)
+    acc.add("b_o", dbo)
+    acc.add("w_1", dw1, s2)
+    acc.add("b_1", db1)
+    acc.add("w_2", dw2, s1)
+    acc.add("b_2", db2)
+    acc.add("ln1_g", dln1_g)
+    acc.add("ln1_b", dln1_b)
+    acc.add("ln2_g", dln2_g)
+    acc.add("ln2_b", dln2_b)
+    return gx
 
+
+def block_grads_to_reference(acc: BlockGrads, bw, params: dict, prefix: str, dh: int, hidden: int) -> dict:
+    """The accumulated kernel-layout gradients in the reference's layouts: float64, (in, out) matrices, parameter
+    names of attention.py:105-139."""
+    D = hidden
+    heads, dhp = bw.heads, bw.dhp
+    hd = heads * dhp
+    g = {k: v.double().cpu().numpy() for k, v in acc.t.items()}
     qk = _qk_perm(heads, dh, dhp)
     vv = _v_perm(heads, dh, dhp)
-    Wqkv, Bqkv = h(dwqkv, s4)[:, :D], h(dbqkv)
+    Wqkv, Bqkv = g["w_qkv"][:, :D], g["b_qkv"]
     grads = {}
     for sec_i, (wn, bn, perm) in enumerate((("attn.wq", "attn.bq", qk), ("attn.wk", "attn.bk", qk),
                                             ("attn.wv", "attn.bv", vv))):
@@ -240,15 +277,199 @@ def block_vjp(x, params: dict, prefix: str, extents, window, heads: int, gy):
         grads[wn], grads[bn] = gw, gb
     gwo = np.zeros((D, D))
     okv = vv >= 0
-    gwo[vv[okv]] = h(dwo, s3)[:, okv].T
-    grads["attn.wo"], grads["attn.bo"] = gwo, h(dbo)
+    gwo[vv[okv]] = g["w_o"][:, okv].T
+    grads["attn.wo"], grads["attn.bo"] = gwo, g["b_o"]
     from .tensor import host_values
     hidden_mlp = host_values(params[f"{prefix}.mlp.w1"]).shape[1]
-    grads["mlp.w1"] = h(dw1, s2)[:hidden_mlp, :D].T.copy()
-    grads["mlp.b1"] = h(db1)[:hidden_mlp]
-    grads["mlp.w2"] = h(dw2, s1)[:D, :hidden_mlp].T.copy()
-    grads["mlp.b2"] = h(db2)
-    grads["ln1.gain"], grads["ln1.bias"] = h(dln1_g), h(dln1_b)
-    grads["ln2.gain"], grads["ln2.bias"] = h(dln2_g), h(dln2_b)
+    grads["mlp.w1"] = g["w_1"][:hidden_mlp, :D].T.copy()
+    grads["mlp.b1"] = g["b_1"][:hidden_mlp]
+    grads["mlp.w2"] = g["w_2"][:D, :hidden_mlp].T.copy()
+    grads["mlp.b2"] = g["b_2"]
+    grads["ln1.gain"], grads["ln1.bias"] = g["ln1_g"], g["ln1_b"]
+    grads["ln2.gain"], grads["ln2.bias"] = g["ln2_g"], g["ln2_b"]
     names = dict(zip([n[len(prefix) + 1:] for n in block_param_names(prefix)], block_param_names(prefix)))
-    return h(gx), {names[k]: np.ascontiguousarray(v) for k, v in grads.items()}
+    return {names[k]: np.ascontiguousarray(v) for k, v in grads.items()}
+
+
+def block_vjp(x, params: dict, prefix: str, extents, window, heads: int, gy):
+    """(gx, grads) of y = natten_block(x) for the output gradient gy; numpy float64 in the reference layouts."""
+    from .attention import to_device_f32, validate_block_args
+    extents = tuple(int(e) for e in extents)
+    window = tuple(int(w) for w in window)
+    xd = to_device_f32(x)
+    dh = validate_block_args(tuple(xd.shape), extents, window, heads)
+    bw = CACHE.block(params, prefix, heads)
+    acc = BlockGrads()
+    gx = block_vjp_device(xd, bw, extents, window, heads, dh, to_device_f32(gy), acc)
+    return gx.double().cpu().numpy(), block_grads_to_reference(acc, bw, params, prefix, dh, xd.shape[1])
+
+
+# ------------------------------------------------------------------------------------------------------------
+# Reverse mode of the latent rollout with checkpointed blocks and host offload (SURVEY.md §8f4)
+# ------------------------------------------------------------------------------------------------------------
+class DeviceActivationStore:
+    """Saved block inputs kept in HBM: plain per-block checkpointing (autodiff.py:893-924), one latent per block."""
+
+    def __init__(self):
+        self.slots: dict = {}
+        self.resident = 0
+        self.high_water = 0
+        self.demand_stalls = 0
+
+    def put(self, k: int, x: torch.Tensor) -> None:
+        self.slots[k] = x.clone()
+        self.resident += x.numel() * x.element_size()
+        self.high_water = max(self.high_water, self.resident)
+
+    def begin_backward(self, order) -> None:
+        pass
+
+    def take(self, k: int) -> torch.Tensor:
+        return self.slots[k]
+
+    def release(self, k: int) -> None:
+        x = self.slots.pop(k)
+        self.resident -= x.numel() * x.element_size()
+
+    def stats(self) -> dict:
+        return {"kind": "device", "high_water_bytes": self.high_water, "demand_stalls": 0}
+
+
+class HostOffloadStore:
+    """Saved block inputs in page-locked host memory, moved on a side CUDA stream: the B200 counterpart of the
+    reference's OffloadEngine / PrefetchPipeline (offload.py:287-412, 226-285).
+
+    Forward, put(k, x): x is staged into one of `lookahead + 1` device ring slots on the compute stream (the slot
+    is reused only after its previous device-to-host copy completed), and the side stream copies the slot out to
+    the host.  Backward, in the order given to begin_backward(): the side stream brings inputs back into the ring
+    `lookahead` blocks ahead of need (each slot reused once the compute stream's recompute of its previous block
+    is done), take(k) makes the compute stream wait for that copy, release(k) frees the slot and issues the next
+    prefetch.  Transfers overlap recompute; device residency of saved inputs is the ring, whatever the number of
+    blocks; the bytes are exact copies, so gradients are bitwise those of the in-HBM store."""
+
+    def __init__(self, shape, lookahead: int = 2):
+        if lookahead < 1:
+            raise ValueError(f"lookahead must be >= 1, got {lookahead}")
+        self.shape = tuple(shape)
+        self.lookahead = int(lookahead)
+        self.side = torch.cuda.Stream()
+        self.ring = [torch.empty(self.shape, dtype=torch.float32, device="cuda") for _ in range(self.lookahead + 1)]
+        self.slot_free = [None] * len(self.ring)  # event after the last use of the slot (any stream)
+        self.host: dict = {}
+        self.ready: dict = {}  # k -> (slot, event) of a fetched input
+        self.order: list = []
+        self.next_fetch = 0
+        self.demand_stalls = 0
+        self.transfers = 0
+        self.high_water = len(self.ring) * self.ring[0].numel() * 4
+
+    def _wait_slot(self, stream, i: int) -> None:
+        if self.slot_free[i] is not None:
+            stream.wait_event(self.slot_free[i])
+
+    def put(self, k: int, x: torch.Tensor) -> None:
+        i = k % len(self.ring)
+        main = torch.cuda.current_stream()
+        self._wait_slot(main, i)
+        self.ring[i].copy_(x)
+        staged = torch.cuda.Event()
+        staged.record(main)
+        h = self.host.get(k)
+        if h is None:
+            h = torch.empty(self.shape, dtype=torch.float32, pin_memory=True)
+            self.host[k] = h
+        with torch.cuda.stream(self.side):
+            self.side.wait_event(staged)
+            h.copy_(self.ring[i], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(self.side)
+        self.slot_free[i] = done
+        self.transfers += 1
+
+    def begin_backward(self, order) -> None:
+        self.order = list(order)
+        self.next_fetch = 0
+        self.slot_rr = 0
+        for _ in range(min(self.lookahead, len(self.order))):
+            self._prefetch()
+
+    def _prefetch(self) -> None:
+        if self.next_fetch >= len(self.order):
+            return
+        k = self.order[self.next_fetch]
+        self.next_fetch += 1
+        i = self.slot_rr
+        self.slot_rr = (self.slot_rr + 1) % len(self.ring)
+        with torch.cuda.stream(self.side):
+            self._wait_slot(self.side, i)
+            self.ring[i].copy_(self.host[k], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.side)
+        self.ready[k] = (i, ev)
+        self.transfers += 1
+
+    def take(self, k: int) -> torch.Tensor:
+        if k not in self.ready:  # not prefetched in time (out-of-order request): fetch on demand
+            self.demand_stalls += 1
+            while k not in self.ready:
+                self._prefetch()
+        i, ev = self.ready[k]
+        torch.cuda.current_stream().wait_event(ev)
+        return self.ring[i]
+
+    def release(self, k: int) -> None:
+        i, _ = self.ready.pop(k)
+        done = torch.cuda.Event()
+        done.record(torch.cuda.current_stream())
+        self.slot_free[i] = done
+        self._prefetch()
+
+    def stats(self) -> dict:
+        return {"kind": "host", "high_water_bytes": self.high_water, "demand_stalls": self.demand_stalls,
+                "transfers": self.transfers, "lookahead": self.lookahead}
+
+
+def rollout_vjp(z0, plan, params: dict, cfg, g_out, offload: bool = False, lookahead: int = 2):
+    """Reverse mode of the greedy latent rollout (rollout.py:56-81) on the device.
+
+    z0: the initial latent tokens (T, hidden); plan: processor horizons in order (e.g. (6, 6, 1)); g_out: the
+    cotangent of the final latent tokens.  Returns (z_final, dL/dz0, {parameter name: gradient}, store stats):
+    z_final as a device fp32 tensor, dL/dz0 as float64 numpy, every processor block's parameter gradients summed
+    over the steps that applied it (float64, the reference's layouts).  Like the reference's checkpoint_segment
+    per block (autodiff.py:893-924) the forward keeps only each block's input and the backward recomputes the
+    block from it (block_vjp_device); with offload=True those inputs live in page-locked host memory and return
+    `lookahead` blocks ahead of need (HostOffloadStore), bitwise the same gradients as offload=False.
+    """
+    from .attention import to_device_f32
+    from .blocks import block_forward
+    from .config import as_config
+    cfg = as_config(cfg)
+    ext, win, heads, dh = cfg.latent_extents, cfg.window, cfg.heads, cfg.head_dim
+    for h in plan:
+        if f"proc{h}.blk0.ln1.gain" not in params:
+            from .errors import ConfigError
+            raise ConfigError(f"parameters carry no {h} h processor")
+    prefixes = [f"proc{h}.blk{i}" for h in plan for i in range(cfg.proc_blocks)]
+    x = to_device_f32(z0)
+    store = HostOffloadStore(x.shape, lookahead) if offload else DeviceActivationStore()
+    rope = CACHE.rope(ext, dh)
+    for k, pre in enumerate(prefixes):
+        bw = CACHE.block(params, pre, heads)
+        store.put(k, x)
+        block_forward(x, bw, CACHE.workspace(ext, win, bw), rope, ext, win)
+    z = x
+    g = to_device_f32(g_out)
+    accs: dict = {}
+    order = list(reversed(range(len(prefixes))))
+    store.begin_backward(order)
+    for k in order:
+        pre = prefixes[k]
+        bw = CACHE.block(params, pre, heads)
+        xk = store.take(k)
+        g = block_vjp_device(xk, bw, ext, win, heads, dh, g, accs.setdefault(pre, BlockGrads()))
+        store.release(k)
+    grads: dict = {}
+    for pre, acc in accs.items():
+        grads.update(block_grads_to_reference(acc, CACHE.block(params, pre, heads), params, pre, dh, cfg.hidden))
+    torch.cuda.synchronize()
+    return z, g.double().cpu().numpy(), grads, store.stats()

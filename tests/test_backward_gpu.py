@@ -153,3 +153,75 @@ def test_reference_train_step_and_driver_through_seam(gc):
     l1, l2 = [r["loss"] for r in hist[0]], [r["loss"] for r in hist[1]]
     assert l1 == l2
     assert np.mean(l1[-5:]) < 0.8 * np.mean(l1[:5]), l1
+
+
+def _ref_rollout_grads(gc, cfg_ref, params_ref, z0v, plan, R):
+    from gridcast import autodiff as ad
+    from gridcast.model import LatentState, process
+    z0 = ad.Tensor(z0v, requires_grad=True)
+    z = z0
+    for h in plan:
+        z = process(LatentState(z, 0, cfg_ref.latent_extents), params_ref, cfg_ref, h).tokens
+    loss = (z * ad.Tensor(R)).sum()
+    names = [n for n in params_ref if n.startswith("proc")]
+    g = ad.backward(loss, leaves=[z0] + [params_ref[n] for n in names])
+    return z.values, g[z0], {n: g[params_ref[n]] for n in names}
+
+
+def test_rollout_vjp_matches_reference_tape(gc):
+    """backward.rollout_vjp (device reverse mode of a (6, 1) greedy rollout, checkpointed per block) vs the
+    reference tape through its own process() chain (float64): final latent, dL/dz0 and every processor-block
+    parameter gradient (summed over the steps that apply it)."""
+    import paper_2503_22235_b200.model as M
+    from paper_2503_22235_b200.backward import rollout_vjp
+    cfg = M.desk_config()
+    params = M.init_model_params(cfg, seed=3, zero_residual=False)
+    cfg_ref = gc.model.desk_config()
+    params_ref = gc.model.init_model_params(cfg_ref, seed=3, zero_residual=False)
+    t = int(np.prod(cfg.latent_extents))
+    rng = np.random.default_rng(11)
+    z0v = rng.standard_normal((t, cfg.hidden))
+    R = rng.standard_normal((t, cfg.hidden))
+    plan = (6, 1)
+    ref_z, ref_gz, ref_pg = _ref_rollout_grads(gc, cfg_ref, params_ref, z0v, plan, R)
+    z, gz, pg, st = rollout_vjp(z0v, plan, params, cfg, R)
+    errs = {n: _rel(pg[n], ref_pg[n]) for n in pg if np.linalg.norm(ref_pg[n]) > 0}
+    worst = max(errs, key=errs.get)
+    zr, gr = _rel(z.double().cpu().numpy(), ref_z), _rel(gz, ref_gz)
+    print(f"rollout (6, 1) desk: z {zr:.2e}, dL/dz0 {gr:.2e}, worst param {worst} {errs[worst]:.2e} "
+          f"({len(errs)} tensors), store {st}")
+    assert set(pg) == {n for n in ref_pg if any(n.startswith(f"proc{h}.") for h in plan)}
+    assert zr < 1e-2 and gr < GRAD_TOL, (zr, gr)
+    assert errs[worst] < GRAD_TOL, (worst, errs[worst])
+
+
+@pytest.mark.parametrize("lookahead", [1, 2, 3])
+def test_rollout_vjp_host_offload_bitwise(lookahead):
+    """Saved block inputs offloaded to page-locked host memory on a side stream and prefetched `lookahead`
+    blocks ahead (HostOffloadStore, the OffloadEngine counterpart of offload.py:287-412): gradients bitwise equal
+    to keeping them in HBM (verify.py:73-113's offload-parity contract), no demand stalls, and device residency
+    of saved inputs bounded by the ring (lookahead + 1 latents) instead of one latent per block."""
+    import paper_2503_22235_b200.model as M
+    from paper_2503_22235_b200.backward import rollout_vjp
+    cfg = M.mid_config()
+    params = M.init_model_params(cfg, seed=5, zero_residual=False)
+    t = int(np.prod(cfg.latent_extents))
+    rng = np.random.default_rng(4)
+    z0v = rng.standard_normal((t, cfg.hidden))
+    R = rng.standard_normal((t, cfg.hidden))
+    plan = (6, 1)
+    z_a, g_a, p_a, st_a = rollout_vjp(z0v, plan, params, cfg, R, offload=False)
+    z_b, g_b, p_b, st_b = rollout_vjp(z0v, plan, params, cfg, R, offload=True, lookahead=lookahead)
+    print(f"lookahead {lookahead}: {st_a} vs {st_b}")
+    assert torch_equal(z_a, z_b)
+    assert np.array_equal(g_a, g_b)
+    assert set(p_a) == set(p_b) and all(np.array_equal(p_a[n], p_b[n]) for n in p_a)
+    nbytes = t * cfg.hidden * 4
+    assert st_a["high_water_bytes"] == 2 * cfg.proc_blocks * nbytes
+    assert st_b["high_water_bytes"] == (lookahead + 1) * nbytes
+    assert st_b["demand_stalls"] == 0 and st_b["transfers"] == 2 * 2 * cfg.proc_blocks
+
+
+def torch_equal(a, b):
+    import torch
+    return bool(torch.equal(a, b))
