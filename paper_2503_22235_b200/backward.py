@@ -120,9 +120,20 @@ class _InverseNeighbors:
         return hit
 
 
+_ROPE_PAIRS: dict = {}
+
+
 def _rope_pair_tables(extents, dh: int, dhp: int, dev) -> tuple[torch.Tensor, torch.Tensor]:
     """cos / sin (T, dhp / 2) of the interleaved pairs (pair j = reference columns (j, j + dh/2), attention.py:48-92);
-    padding pairs are the identity."""
+    padding pairs are the identity.  Built once per geometry and device."""
+    key = (tuple(extents), dh, dhp, str(dev))
+    hit = _ROPE_PAIRS.get(key)
+    if hit is None:
+        hit = _ROPE_PAIRS[key] = _rope_pair_tables_build(extents, dh, dhp, dev)
+    return hit
+
+
+def _rope_pair_tables_build(extents, dh: int, dhp: int, dev) -> tuple[torch.Tensor, torch.Tensor]:
     from .attention import rotary_tables
     cos, sin = rotary_tables(extents, dh)  # (T, 1, dh / 2) float64
     t = cos.shape[0]
