@@ -259,6 +259,33 @@ def roofline(per_ms: dict, tokens: int, traffic: bool = True) -> tuple[dict, dic
     return roof, table
 
 
+def measure_backward(reps: int = 3) -> dict:
+    """§8f4: the full-shape block's reverse mode on the device (backward.block_vjp_device: forward recompute from
+    the block input + backward, fp32 parameter-gradient accumulation), CUDA events; not the headline metric."""
+    from paper_2503_22235_b200.backward import BlockGrads, block_vjp_device
+    from paper_2503_22235_b200.params import init_block_params
+    from paper_2503_22235_b200.runtime import CACHE
+    t = int(np.prod(EXT))
+    params = init_block_params(np.random.default_rng(0), DIM, HEADS, "bwd", zero_residual=False)
+    bw = CACHE.block(params, "bwd", HEADS)
+    x = torch.randn(t, DIM, device="cuda")
+    gy = torch.randn(t, DIM, device="cuda")
+    dh = DIM // HEADS
+    block_vjp_device(x, bw, EXT, WIN, HEADS, dh, gy, BlockGrads())
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        block_vjp_device(x, bw, EXT, WIN, HEADS, dh, gy, BlockGrads())
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    tf = 3.0 * block_flops(t) / 1e12  # forward recompute + 2x for the backward, algorithmic
+    return {"block_vjp_ms": round(ms, 3), "algorithmic_tflop": round(tf, 3), "tflops": round(tf / (ms / 1e3), 1),
+            "note": "one full-shape block: forward recompute + backward (dX and all parameter gradients); the "
+                    "attention backward is a CUDA-core kernel pair (query side / key side), see DESIGN.md §9"}
+
+
 def measure_config3(state, params, cfg, reps: int = 3) -> dict:
     """BASELINE configs[2]: full 0.25 deg encode -> one 6 h processor application -> decode through the public API
     (host page-locked fields in, host fields out), each part timed with CUDA events on the launching stream
@@ -604,6 +631,12 @@ def run_gpu(args, world, rank, local_rank):
             traceback.print_exc(file=sys.stderr)
             fc = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
+    bwd = None
+    if world == 1 and not args.no_backward:
+        try:
+            bwd = measure_backward()
+        except Exception as exc:
+            bwd = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     n_launch = 7
     if world > 1:  # LN1, QKV, O-proj, LN2, W1, W2 + the attention launches of the row split
         from paper_2503_22235_b200.bands import interior_rows
@@ -638,6 +671,7 @@ def run_gpu(args, world, rank, local_rank):
             "roofline": roof,
             "kernels": table,
             "forecast_14d": fc,
+            "backward": bwd,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }
@@ -657,6 +691,7 @@ def main():
     ap.add_argument("--forecast-hours", type=int, default=336)
     ap.add_argument("--forecast-reps", type=int, default=2)
     ap.add_argument("--ensemble", type=int, default=8, help="members of the 14-day ensemble forecast (0/1: skip)")
+    ap.add_argument("--no-backward", action="store_true", help="skip the block reverse-mode measurement")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":
