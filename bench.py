@@ -262,6 +262,7 @@ def roofline(per_ms: dict, tokens: int, traffic: bool = True) -> tuple[dict, dic
 def measure_backward(reps: int = 3) -> dict:
     """§8f4: the full-shape block's reverse mode on the device (backward.block_vjp_device: forward recompute from
     the block input + backward, fp32 parameter-gradient accumulation), CUDA events; not the headline metric."""
+    import torch
     from paper_2503_22235_b200.backward import BlockGrads, block_vjp_device
     from paper_2503_22235_b200.params import init_block_params
     from paper_2503_22235_b200.runtime import CACHE

@@ -264,6 +264,13 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
       // output pixel
       int orow = r, ocol = col;
       if (p.mode == WM3_CONV_T2) { orow = 2 * r + (cls >> 1); ocol = 2 * col + (cls & 1); }
+      if (p.resid != nullptr && ok) {
+        // pull this pixel's residual channels toward L2 while the accumulator is still being computed
+        const size_t rpix = (static_cast<size_t>(img) * (p.hout + 2) + orow + 1) * (p.wout + 2) + ocol + 1;
+        const char* rb = reinterpret_cast<const char*>(p.resid + rpix * p.resid_cp + n0);
+        for (int off = 64 * g; off < BN * 2; off += 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(rb + off));
+      }
       mbar_wait(tfull_bar(acc), aphase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(32 * q) << 16);
