@@ -292,6 +292,32 @@ int wm3_bw_natten(const void* qkv, int ldq, const int64_t* nbr, const int* inv_o
                   float* dS, float* work, float* gout, int ldg, void* stream);
 int wm3_bw_rope(float* g, int ldg, int T, int heads, int dhp, const float* cos_t, const float* sin_t, void* stream);
 
+/* Attention backward on the tensor cores (replaces wm3_bw_natten when wm3_natten_bwd_info reports support: head
+ * dim padded to 128, window mask in the MMA).  Same reference rules (attention.py:173-178 through autodiff.py's
+ * matmul / softmax / take VJPs); full domain, one member.
+ *   wm3_natten_fwd_lse     the forward (wm3_natten_fwd) also writing lse [T][heads] (log2-domain log-sum-exp)
+ *   wm3_bw_na_prep         dO (fp16, [T][heads * dhp]) = gctx * sigma with sigma a power of two keeping
+ *                          |dO . v| <= 2^13; factors[2] = (scale / (sigma s), 1 / (sigma s)), s = gctx's grad
+ *                          scale (amax bits); maxima[2] scratch
+ *   wm3_natten_bwd_info    tiles and per-tile chunk slots of the geometry; supported = 1 if the tcgen05 path applies
+ *   wm3_natten_slot_table  int32 [tiles][maxch][128]: key token of every chunk slot (-1: none), for the CSR
+ *                          (csr_off [T + 1], csr_ent = (tile * maxch + chunk) * 128 + slot, by token, fixed order)
+ *   wm3_natten_bwd         dQ into gqkv's q section, dK / dV (the CSR-ordered sum of per-chunk partials, partial =
+ *                          [tiles * heads][maxch][2][2][64][128] fp32 scratch) into its k / v sections (fp32) */
+int wm3_natten_fwd_lse(const void* qkv, int ldqkv, void* out, int ldo, int depth, int rows, int cols, int heads, int dhp,
+                       int wd, int wh, int ww, float scale, float* lse, void* stream);
+int wm3_bw_na_prep(const void* qkv, int ldq, int T, int heads, int dhp, const float* gctx, int ldc,
+                   const unsigned* gscale_bits, float scale, void* dout, int ldd, unsigned* maxima, float* factors,
+                   void* stream);
+int wm3_natten_bwd_info(int depth, int rows, int cols, int heads, int dhp, int wd, int wh, int ww, int* ntiles,
+                        int* maxch, int* supported, void* stream);
+int wm3_natten_slot_table(int depth, int rows, int cols, int heads, int dhp, int wd, int wh, int ww, int32_t* table,
+                          void* stream);
+int wm3_natten_bwd(const void* qkv, int ldqkv, const void* dout, int ldd, const void* o, int ldo, const float* lse,
+                   float* gqkv, int ldg, float* partial, const int32_t* csr_off, const int32_t* csr_ent,
+                   const float* factors, int depth, int rows, int cols, int heads, int dhp, int wd, int wh, int ww,
+                   float scale, void* stream);
+
 /* Debug export of the kernel's own window arithmetic: per token, the (start_d, start_h, col_off)
  * it uses; int32 [T][3]. */
 int wm3_natten_windows(int depth, int rows, int cols, int rows_global, int row0, int wd, int wh, int ww,

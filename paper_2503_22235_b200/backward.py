@@ -123,6 +123,55 @@ class _InverseNeighbors:
 _ROPE_PAIRS: dict = {}
 
 
+class _TcAttention:
+    """Per-geometry state of the tensor-core attention backward (wm3_natten_bwd): the CSR of chunk slots per key
+    token (fixed order: the deterministic dK / dV reduction), the partial scratch and the small operand buffers.
+    None when the geometry is unsupported (head dim padded to 64, or the window mask does not fit the MMA bias
+    step) or WM3_BW_NA=cuda selects the CUDA-core kernels (A/B aid)."""
+
+    _cache: dict = {}
+
+    @classmethod
+    def get(cls, extents, window, heads: int, dhp: int):
+        import os
+        if os.environ.get("WM3_BW_NA", "tc") == "cuda":
+            return None
+        key = (tuple(extents), tuple(window), heads, dhp, torch.cuda.current_device())
+        if key not in cls._cache:
+            cls._cache[key] = cls._build(extents, window, heads, dhp)
+        return cls._cache[key]
+
+    @classmethod
+    def _build(cls, extents, window, heads: int, dhp: int):
+        import ctypes
+        d, h, w = (int(e) for e in extents)
+        wd, wh, ww = (int(e) for e in window)
+        nt, mc, sup = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        check(_lib.lib().wm3_natten_bwd_info(d, h, w, heads, dhp, wd, wh, ww, ctypes.byref(nt), ctypes.byref(mc),
+                                             ctypes.byref(sup), stream_ptr()), "wm3_natten_bwd_info")
+        if not sup.value:
+            return None
+        ntiles, maxch = nt.value, mc.value
+        table = torch.empty(ntiles * maxch * 128, dtype=torch.int32, device="cuda")
+        check(_lib.lib().wm3_natten_slot_table(d, h, w, heads, dhp, wd, wh, ww, ptr(table), stream_ptr()),
+              "wm3_natten_slot_table")
+        tab = table.cpu().numpy()
+        t_count = d * h * w
+        codes = np.nonzero(tab >= 0)[0]
+        toks = tab[codes]
+        order = np.argsort(toks, kind="stable")  # by key token, then (tile, chunk, slot)
+        off = np.zeros(t_count + 1, dtype=np.int32)
+        np.cumsum(np.bincount(toks, minlength=t_count), out=off[1:])
+        st = cls()
+        st.ntiles, st.maxch = ntiles, maxch
+        st.off = torch.from_numpy(off).cuda()
+        st.ent = torch.from_numpy(codes[order].astype(np.int32)).cuda()
+        st.partial = torch.empty(ntiles * heads * maxch * 2 * 2 * 64 * dhp, dtype=torch.float32, device="cuda")
+        st.maxima = torch.zeros(2, dtype=torch.int32, device="cuda")
+        st.factors = torch.zeros(2, dtype=torch.float32, device="cuda")
+        return st
+
+
 def _rope_pair_tables(extents, dh: int, dhp: int, dev) -> tuple[torch.Tensor, torch.Tensor]:
     """cos / sin (T, dhp / 2) of the interleaved pairs (pair j = reference columns (j, j + dh/2), attention.py:48-92);
     padding pairs are the identity.  Built once per geometry and device."""
@@ -190,7 +239,14 @@ def block_vjp_device(xd: torch.Tensor, bw, extents, window, heads: int, dh: int,
     grid = ops.KVGrid(extents, window)
     qkv = torch.zeros((grid.tokens, 3 * hd), dtype=L.ELEM, device=dev)
     ops.linear_grid(hn, bw.w_qkv, L.WM3_EPI_QKV_ROPE, bw.b_qkv, qkv, grid, rope=rope.struct(extents, 0, heads, dhp))
-    ctx = ops.natten(qkv, grid, heads, dhp, dh, window)
+    tca = _TcAttention.get(extents, window, heads, dhp)
+    if tca is not None:
+        ctx = torch.empty((T, hd), dtype=L.ELEM, device=dev)
+        lse = torch.empty((T, heads), dtype=torch.float32, device=dev)
+        check(L.lib().wm3_natten_fwd_lse(ptr(qkv), qkv.stride(0), ptr(ctx), ctx.stride(0), *extents, heads, dhp,
+                                         *window, 1.0 / math.sqrt(dh), ptr(lse), stream_ptr()), "wm3_natten_fwd_lse")
+    else:
+        ctx = ops.natten(qkv, grid, heads, dhp, dh, window)
     x1 = xd.clone()
     ops.linear(ctx, bw.w_o, L.WM3_EPI_BIAS_RESID_F32, bias=bw.b_o, out=x1, n_valid=D)
     hn2 = ops.layernorm_bf16(x1, bw.ln2_g, bw.ln2_b, ldo=kp)
@@ -226,14 +282,23 @@ def block_vjp_device(xd: torch.Tensor, bw, extents, window, heads: int, dh: int,
     dbo = _colsum(gx1, T, D)
     g_ctx = _gemm(_cast(gx1, T, D, np_, scale=s3), wt["w_o"], T, hd, np_)  # x s3
     # ---- attention (query and key sides) and the rotary transpose ----
-    nbr, inv_off, inv_ent, K = _InverseNeighbors.get(extents, window)
-    P = torch.empty((T, heads, K), dtype=torch.float32, device=dev)
-    dS = torch.empty_like(P)
-    work = torch.empty((T, heads, 2 * K), dtype=torch.float32, device=dev)
     g_qkv = torch.zeros((T, 3 * hd), dtype=torch.float32, device=dev)
-    check(L.lib().wm3_bw_natten(ptr(qkv), 3 * hd, ptr(nbr), ptr(inv_off), ptr(inv_ent), T, K, heads, dhp,
-                                1.0 / math.sqrt(dh), ptr(g_ctx), hd, s3.ptr(), ptr(P), ptr(dS), ptr(work), ptr(g_qkv),
-                                3 * hd, stream_ptr()), "wm3_bw_natten")
+    if tca is not None:
+        # tensor cores: dQ per query tile, dK / dV as deterministic sums of per-chunk partials (natten.cu)
+        dout = torch.empty((T, hd), dtype=L.ELEM, device=dev)
+        check(L.lib().wm3_bw_na_prep(ptr(qkv), 3 * hd, T, heads, dhp, ptr(g_ctx), hd, s3.ptr(), 1.0 / math.sqrt(dh),
+                                     ptr(dout), hd, ptr(tca.maxima), ptr(tca.factors), stream_ptr()), "wm3_bw_na_prep")
+        check(L.lib().wm3_natten_bwd(ptr(qkv), 3 * hd, ptr(dout), hd, ptr(ctx), hd, ptr(lse), ptr(g_qkv), 3 * hd,
+                                     ptr(tca.partial), ptr(tca.off), ptr(tca.ent), ptr(tca.factors), *extents, heads,
+                                     dhp, *window, 1.0 / math.sqrt(dh), stream_ptr()), "wm3_natten_bwd")
+    else:
+        nbr, inv_off, inv_ent, K = _InverseNeighbors.get(extents, window)
+        P = torch.empty((T, heads, K), dtype=torch.float32, device=dev)
+        dS = torch.empty_like(P)
+        work = torch.empty((T, heads, 2 * K), dtype=torch.float32, device=dev)
+        check(L.lib().wm3_bw_natten(ptr(qkv), 3 * hd, ptr(nbr), ptr(inv_off), ptr(inv_ent), T, K, heads, dhp,
+                                    1.0 / math.sqrt(dh), ptr(g_ctx), hd, s3.ptr(), ptr(P), ptr(dS), ptr(work),
+                                    ptr(g_qkv), 3 * hd, stream_ptr()), "wm3_bw_natten")
     cs, sn = _rope_pair_tables(extents, dh, dhp, dev)
     check(L.lib().wm3_bw_rope(ptr(g_qkv), 3 * hd, T, heads, dhp, ptr(cs), ptr(sn), stream_ptr()), "wm3_bw_rope")
     # ---- QKV ----

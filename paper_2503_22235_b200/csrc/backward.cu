@@ -370,3 +370,68 @@ extern "C" int wm3_bw_rope(float* g, int ldg, int T, int heads, int dhp, const f
                    reinterpret_cast<cudaStream_t>(stream)>>>(g, ldg, T, heads, dhp, cos_t, sin_t);
   return check_launch("bw_rope_kernel");
 }
+
+// ---------------------------------------------------------------------------------------------------------------
+// Operands of the tcgen05 attention backward (natten.cu wm3_natten_bwd): dO as fp16 scaled by a power of two
+// sigma with sigma * max|g_ctx| * max_k ||v_k||_1 <= 2^13 (so |dP| and |Delta| <= 2^13 and dS = P (dP - Delta) fits
+// fp16), and the unscale factors of dQ / dK (scale / (sigma s)) and dV (1 / (sigma s)), s = the g_ctx grad scale.
+// ---------------------------------------------------------------------------------------------------------------
+__global__ void bw_na_prep_reduce_kernel(const elem_t* __restrict__ qkv, int ldq, int T, int heads, int dhp,
+                                         const float* __restrict__ gctx, int ldc, unsigned* __restrict__ maxima) {
+  // maxima[0] = max |g_ctx| over the (T, heads * dhp) block, maxima[1] = max over (token, head) of sum |v|
+  const int sec = heads * dhp;
+  float mg = 0.f, mv = 0.f;
+  const long long n = static_cast<long long>(T) * heads;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int t = static_cast<int>(i / heads), h = static_cast<int>(i - static_cast<long long>(t) * heads);
+    const elem_t* v = qkv + static_cast<size_t>(t) * ldq + 2 * sec + h * dhp;
+    const float* g = gctx + static_cast<size_t>(t) * ldc + h * dhp;
+    float l1 = 0.f;
+    for (int c = 0; c < dhp; ++c) {
+      l1 += fabsf(to_f(v[c]));
+      mg = fmaxf(mg, fabsf(g[c]));
+    }
+    mv = fmaxf(mv, l1);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, o));
+    mv = fmaxf(mv, __shfl_xor_sync(0xffffffffu, mv, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(maxima, __float_as_uint(mg));
+    atomicMax(maxima + 1, __float_as_uint(mv));
+  }
+}
+
+__global__ void bw_na_prep_scale_kernel(const float* __restrict__ gctx, int ldc, int T, int cols,
+                                        const unsigned* __restrict__ maxima, const unsigned* gscale_bits, float scale,
+                                        elem_t* __restrict__ dout, int ldd, float* __restrict__ factors) {
+  const float bound = __uint_as_float(maxima[0]) * __uint_as_float(maxima[1]);
+  const float sigma = (bound > 0.f && isfinite(bound)) ? exp2f(floorf(log2f(8192.f / bound))) : 1.f;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const float s = grad_scale(gscale_bits);
+    factors[0] = scale / (sigma * s);
+    factors[1] = 1.f / (sigma * s);
+  }
+  const long long n = static_cast<long long>(T) * cols;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int t = static_cast<int>(i / cols), c = static_cast<int>(i - static_cast<long long>(t) * cols);
+    dout[static_cast<size_t>(t) * ldd + c] = to_elem(gctx[static_cast<size_t>(t) * ldc + c] * sigma);
+  }
+}
+
+extern "C" int wm3_bw_na_prep(const void* qkv, int ldq, int T, int heads, int dhp, const float* gctx, int ldc,
+                              const unsigned* gscale_bits, float scale, void* dout, int ldd, unsigned* maxima,
+                              float* factors, void* stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(maxima, 0, 2 * sizeof(unsigned), s);
+  bw_na_prep_reduce_kernel<<<grid_for(static_cast<long long>(T) * heads, 256), 256, 0, s>>>(
+      reinterpret_cast<const elem_t*>(qkv), ldq, T, heads, dhp, gctx, ldc, maxima);
+  if (check_launch("bw_na_prep_reduce_kernel")) return -1;
+  bw_na_prep_scale_kernel<<<grid_for(static_cast<long long>(T) * heads * dhp, 256), 256, 0, s>>>(
+      gctx, ldc, T, heads * dhp, maxima, gscale_bits, scale, reinterpret_cast<elem_t*>(dout), ldd, factors);
+  return check_launch("bw_na_prep_scale_kernel");
+}

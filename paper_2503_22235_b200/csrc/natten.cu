@@ -64,6 +64,7 @@ struct NaParams {
   int q_lo, q_hi;  // global query rows this launch computes and stores: [q_lo, q_hi) within the band
   int ncp, nrpc;  // key-chunk box: ncp columns x nrpc rows (fixed for every tile)
   float scale_log2;
+  float* lse;  // optional [token][head]: log2-domain log-sum-exp of the row (m + log2 l), for the backward
   const uint8_t* bias_table;  // BIAS: [tile][maxch] B_x images (4 KB each), built once per geometry
   int maxch;
 };
@@ -654,6 +655,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
       tc_fence_after();
       const size_t tok = g.b * member_tokens + static_cast<size_t>((qd * p.rows + (qh - p.row0)) * p.cols + qw);
       elem_t* orow = p.out + (qvalid ? tok * p.ldo + g.head * p.dhp : 0);
+      if (p.lse != nullptr && qvalid) p.lse[tok * p.heads + g.head] = m_run + __log2f(l_run);
       // this thread's O columns in batches of 32 TMEM columns, then 256-bit stores (whole 32-byte sectors)
 #pragma unroll 1
       for (int c0 = oc0; c0 < oc0 + ocols; c0 += 32) {
@@ -682,6 +684,418 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
     tc_fence_after();
     tmem_dealloc(tmem, NA_TMEM_COLS);
   }
+}
+
+// ------------------------------------------------------------------------------------------------------------
+// Attention backward on tcgen05 (the block VJP's attention step; reference autodiff rules of
+// matmul / softmax / take in attention.py:173-178).  Work item = (query tile, head) as in the forward, one CTA
+// per SM (320 threads, all 512 TMEM columns, ~205 KB smem).  Per key half h of every chunk:
+//   S_h = Q K_h^T (+ window bias), dP_h = dO V_h^T          (M128 N64, TMEM S [0,128), dP [128,256))
+//   softmax warps (thread = query row): P = exp2(S * scale_log2 - lse), dS = P (dP - Delta)   (Delta = dO . O)
+//     dS_h (fp16) over the S_h columns (A operand of dQ), P_h and dS_h rows into shared memory (SW128)
+//   dQ += dS_h K_h                                            (M128 N=dh K=64, TMEM [256,384))
+//   dV_h^T = dO^T P_h, dK_h^T = Q^T dS_h                      (M = dh 128, N64, K = 128 queries; TMEM [384,512))
+//   drain warps (thread = dh row) store dK_h^T / dV_h^T as per-(item, chunk, half) partials [slot][dh] (fp32)
+// dQ leaves once per tile; natten_bwd_reduce_kernel then sums every key's partials over the (tile, chunk, slot)
+// entries that hold it, in a fixed order (CSR built from natten_slot_table_kernel), so dK / dV are deterministic
+// without atomics.  Operands: dO enters as fp16 scaled by a power of two sigma chosen so |dP|, |Delta| <= 2^13
+// (|dP| <= max|dO| * max_k ||v_k||_1), which keeps dS = P (dP - Delta) inside fp16.
+struct NaBwd {
+  const elem_t* dout;  // dO * sigma (fp16), [token][heads * dhp] (ldd)
+  int ldd;
+  const elem_t* o;     // O = ctx (fp16), [token][heads * dhp] (ldo)
+  int ldo;
+  const float* lse;    // [token][heads], log2 domain (forward with lse)
+  float* gqkv;         // fp32 [token][3][heads][dhp] (ldg): dQ into the q section (this kernel)
+  int ldg;
+  float* partial;      // [item][maxch][2 halves][2 (dK, dV)][64 slots][dhp]
+  const float* factors;  // device: [0] dQ / dK factor (scale / (sigma s)), [1] dV factor (1 / (sigma s))
+};
+
+constexpr int NB_THREADS = 320;
+constexpr int NB_MMA_WARP = 4, NB_TMA_WARP = 5;  // warps 0-3 softmax, 6-9 partial drain
+constexpr uint32_t NB_Q = 0, NB_DO = 32768, NB_K = 65536, NB_V = 131072, NB_P = 163840, NB_DS = 180224,
+                   NB_XB = 196608, NB_XA = 204800, NB_BODY = 208896;
+constexpr uint32_t NB_SMEM = NB_BODY + 1024 + 256;
+
+template <bool BIAS>
+__global__ void __launch_bounds__(NB_THREADS, 1)
+    natten_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
+                      const __grid_constant__ CUtensorMap tmDO, NaParams p, NaBwd bw) {
+  constexpr int DHP = 128;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  const uint32_t sQ = sb + NB_Q, sDO = sb + NB_DO, sV = sb + NB_V, sP = sb + NB_P, sDS = sb + NB_DS, sXA = sb + NB_XA;
+  auto sK = [&](int i) { return sb + NB_K + NA_TILE * i; };
+  auto sXB = [&](int i) { return sb + NB_XB + 4096u * i; };
+  const uint32_t b0 = sb + NB_BODY;
+  const uint32_t bar_qfull = b0, bar_qempty = b0 + 8, bar_vfull = b0 + 16, bar_vempty = b0 + 24;
+  auto bar_kfull = [&](int i) { return b0 + 32 + 8 * i; };
+  auto bar_kempty = [&](int i) { return b0 + 48 + 8 * i; };
+  auto bar_sfull = [&](int h) { return b0 + 64 + 8 * h; };  // S_h and dP_h in TMEM
+  auto bar_pfull = [&](int h) { return b0 + 80 + 8 * h; };  // dS_h in TMEM, P_h / dS_h in smem
+  const uint32_t bar_psfree = b0 + 96;    // the partial MMAs read P / dS smem (once per half)
+  const uint32_t bar_partfull = b0 + 104;  // dK^T / dV^T of a half in TMEM
+  const uint32_t bar_partempty = b0 + 112; // drained (4 warps)
+  const uint32_t bar_dqfull = b0 + 120, bar_dqempty = b0 + 128;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + NB_BODY + 200);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  if (tid == 0) {
+    mbar_init(bar_qfull, 1);
+    mbar_init(bar_qempty, 1);
+    mbar_init(bar_vfull, 1);
+    mbar_init(bar_vempty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar_kfull(i), 1);
+      mbar_init(bar_kempty(i), 1);
+      mbar_init(bar_sfull(i), 1);
+      mbar_init(bar_pfull(i), 4);
+    }
+    mbar_init(bar_psfree, 1);
+    mbar_init(bar_partfull, 1);
+    mbar_init(bar_partempty, 4);
+    mbar_init(bar_dqfull, 1);
+    mbar_init(bar_dqempty, 4);
+    fence_barrier_init();
+  }
+  if (warp == NB_MMA_WARP) {
+    tmem_alloc(smem_u32(tmem_slot), 512);
+    tmem_relinquish();
+  }
+  for (uint32_t off = tid * 16u; off < NB_BODY; off += NB_THREADS * 16u) st_shared_v4(sb + off, 0, 0, 0, 0);
+  if (BIAS && tid < 128) {
+    __syncwarp();
+    uint32_t u[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    if (tid < p.TD * p.TH * p.TW) {
+      const uint32_t one = pack_elem(1.f, 0.f) & 0xffffu;
+      const int c3[3] = {tid / (p.TH * p.TW), p.TD + (tid / p.TW) % p.TH, p.TD + p.TH + tid % p.TW};
+      for (int i = 0; i < 3; ++i) u[c3[i] >> 1] |= one << (16 * (c3[i] & 1));
+    }
+    st_shared_v4(sXA + xtra_off(tid, 0), u[0], u[1], u[2], u[3]);
+    st_shared_v4(sXA + xtra_off(tid, 1), u[4], u[5], u[6], u[7]);
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int sec = p.heads * DHP;
+  const int brow0 = p.row0 - p.halo_lo;
+  const int ntiles = p.ntd * p.nth * p.ntw;
+
+  if (warp == NB_TMA_WARP) {
+    // ---------------- producer: Q + dO per tile, K (2 slots) and V (1 slot) per chunk ----------------
+    if (lane == 0) {
+      tma_prefetch(&tmQ);
+      tma_prefetch(&tmKV);
+      tma_prefetch(&tmDO);
+      const uint32_t qbytes = 2 * 128u * p.TW * p.TH * p.TD;
+      const uint32_t kbytes = 2 * 128u * p.ncp * p.nrpc;
+      int c = 0, t = 0;
+      for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++t) {
+        const TileGeo g = tile_geo(p, item);
+        mbar_wait(bar_qempty, (t & 1) ^ 1);
+        mbar_arrive_expect_tx(bar_qfull, 2 * qbytes);
+        for (int h = 0; h < 2; ++h) {
+          tma_load_4d(sQ + h * 16384u, &tmQ, bar_qfull, g.head * DHP + 64 * h, g.w0, g.h0 - brow0,
+                      g.b * p.depth + g.d0);
+          tma_load_4d(sDO + h * 16384u, &tmDO, bar_qfull, g.head * DHP + 64 * h, g.w0, g.h0 - brow0,
+                      g.b * p.depth + g.d0);
+        }
+        for (int j = 0; j < g.nchunks; ++j, ++c) {
+          int kd, kr0, nr, origin, vlo, vhi;
+          chunk_geo(g, p.cols, j, kd, kr0, nr, origin, vlo, vhi);
+          const int s = c & 1;
+          mbar_wait(bar_kempty(s), ((c >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(bar_kfull(s), kbytes + (BIAS ? 4096u : 0u));
+          for (int h = 0; h < 2; ++h)
+            tma_load_4d(sK(s) + h * 16384u, &tmKV, bar_kfull(s), sec + g.head * DHP + 64 * h, origin, kr0 - brow0,
+                        g.b * p.depth + kd);
+          if (BIAS)
+            bulk_load(sXB(s), p.bias_table + (static_cast<size_t>(item % ntiles) * p.maxch + j) * 4096, 4096u,
+                      bar_kfull(s));
+          mbar_wait(bar_vempty, (c & 1) ^ 1);
+          mbar_arrive_expect_tx(bar_vfull, kbytes);
+          for (int h = 0; h < 2; ++h)
+            tma_load_4d(sV + h * 16384u, &tmKV, bar_vfull, 2 * sec + g.head * DHP + 64 * h, origin, kr0 - brow0,
+                        g.b * p.depth + kd);
+        }
+      }
+    }
+  } else if (warp == NB_MMA_WARP) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc_s = make_idesc(128, 64, 0, 0);      // S, dP: K-major Q / dO and K / V rows
+    const uint32_t idesc_q = make_idesc(128, DHP, 0, 1);     // dQ: A = dS (TMEM), B = K MN-major
+    const uint32_t idesc_p = make_idesc(128, 64, 1, 1);      // dK^T / dV^T: A = Q / dO MN-major, B = dS / P
+    const uint64_t dQd = make_sdesc_sw128(sQ, 16, 1024), dDOd = make_sdesc_sw128(sDO, 16, 1024);
+    const uint64_t dK0 = make_sdesc_sw128(sK(0), 16, 1024), dV0 = make_sdesc_sw128(sV, 16, 1024);
+    const uint64_t dKmn = make_sdesc_sw128(sK(0), 16384, 1024);   // K as an MN-major B (N = dh)
+    const uint64_t dQmn = make_sdesc_sw128(sQ, 16384, 1024), dDOmn = make_sdesc_sw128(sDO, 16384, 1024);
+    const uint64_t dPs = make_sdesc_sw128(sP, 16384, 1024), dDSs = make_sdesc_sw128(sDS, 16384, 1024);
+    const uint64_t dXA = make_sdesc_interleave(sXA), dXB0 = make_sdesc_interleave(sXB(0));
+    constexpr uint32_t T16 = NA_TILE >> 4;
+    const uint32_t tS = tmem, tDP = tmem + 128, tDQ = tmem + 256, tPK = tmem + 384, tPV = tmem + 448;
+    auto issue_s = [&](int h, int ks) {  // S_h and dP_h of the chunk in K slot ks
+      if (elect_one()) {
+#pragma unroll
+        for (int s = 0; s < DHP / 16; ++s) {
+          const uint32_t off = ((s >> 2) * 16384u + (s & 3) * 32u) >> 4;
+          umma_bf16_ss(tS + 64 * h, dQd + off, dK0 + ks * T16 + off + h * 512u, idesc_s, s > 0 ? 1u : 0u);
+        }
+        if (BIAS) umma_bf16_ss(tS + 64 * h, dXA, dXB0 + ks * 256u + h * 128u, idesc_s, 1u);
+#pragma unroll
+        for (int s = 0; s < DHP / 16; ++s) {
+          const uint32_t off = ((s >> 2) * 16384u + (s & 3) * 32u) >> 4;
+          umma_bf16_ss(tDP + 64 * h, dDOd + off, dV0 + off + h * 512u, idesc_s, s > 0 ? 1u : 0u);
+        }
+        umma_commit(bar_sfull(h));
+      }
+      __syncwarp();
+    };
+    auto commit = [&](uint32_t bar) {
+      if (elect_one()) umma_commit(bar);
+      __syncwarp();
+    };
+    int c = 0, t = 0, hc = 0;
+    for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++t) {
+      const TileGeo g = tile_geo(p, item);
+      mbar_wait(bar_qfull, t & 1);
+      mbar_wait(bar_kfull(c & 1), (c >> 1) & 1);
+      mbar_wait(bar_vfull, c & 1);
+      tc_fence_after();
+      issue_s(0, c & 1);
+      issue_s(1, c & 1);
+      commit(bar_vempty);
+      for (int j = 0; j < g.nchunks; ++j, ++c) {
+        const int ks = c & 1;
+        const bool more = j + 1 < g.nchunks;
+        for (int h = 0; h < 2; ++h, ++hc) {
+          mbar_wait(bar_pfull(h), c & 1);
+          if (j == 0 && h == 0) mbar_wait(bar_dqempty, (t & 1) ^ 1);
+          tc_fence_after();
+          if (elect_one()) {
+            // dQ += dS_h K_h: A = dS_h from TMEM (fp16 pairs over S_h), B = K rows 64 h.. (MN-major, N = dh)
+#pragma unroll
+            for (int s = 0; s < 4; ++s)
+              umma_f16_ts(tDQ, tS + 64 * h + 8 * s, dKmn + ks * T16 + (4 * h + s) * 128u, idesc_q,
+                          (j > 0 || h > 0 || s > 0) ? 1u : 0u);
+          }
+          __syncwarp();
+          mbar_wait(bar_partempty, (hc & 1) ^ 1);
+          tc_fence_after();
+          if (elect_one()) {
+            // dV_h^T = dO^T P_h, dK_h^T = Q^T dS_h over the 128 query rows (K = queries, 16 per MMA)
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+              umma_bf16_ss(tPV, dDOmn + s * 128u, dPs + s * 128u, idesc_p, s > 0 ? 1u : 0u);
+              umma_bf16_ss(tPK, dQmn + s * 128u, dDSs + s * 128u, idesc_p, s > 0 ? 1u : 0u);
+            }
+            umma_commit(bar_partfull);
+            umma_commit(bar_psfree);
+            if (h == 1) umma_commit(bar_kempty(ks));
+            if (h == 1 && !more) {
+              umma_commit(bar_dqfull);
+              umma_commit(bar_qempty);
+            }
+          }
+          __syncwarp();
+          if (more) {
+            if (h == 0) {
+              mbar_wait(bar_kfull((c + 1) & 1), ((c + 1) >> 1) & 1);
+              mbar_wait(bar_vfull, (c + 1) & 1);
+              tc_fence_after();
+            }
+            issue_s(h, (c + 1) & 1);
+            if (h == 1) commit(bar_vempty);
+          }
+        }
+      }
+    }
+  } else if (warp < 4) {
+    // ---------------- softmax: P, dS per query row; dQ epilogue ----------------
+    const int row = 32 * warp + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(32 * warp) << 16;
+    const uint32_t tS = tmem + lane_off, tDP = tmem + 128 + lane_off, tDQ = tmem + 256 + lane_off;
+    const size_t member_tokens = static_cast<size_t>(p.depth) * p.rows * p.cols;
+    int c = 0, t = 0, hc = 0;
+    for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++t) {
+      const TileGeo g = tile_geo(p, item);
+      const int qd = g.d0 + row / (p.TH * p.TW);
+      const int qh = g.h0 + (row / p.TW) % p.TH;
+      const int qw = g.w0 + row % p.TW;
+      const bool qvalid = row < p.TD * p.TH * p.TW && qd < g.d1 && qh < g.h1 && qh >= p.q_lo && qh < p.q_hi &&
+                          qw < g.w1;
+      const size_t tok = g.b * member_tokens + static_cast<size_t>((qd * p.rows + (qh - p.row0)) * p.cols + qw);
+      const float lse = qvalid ? __ldg(bw.lse + tok * p.heads + g.head) : 0.f;
+      // Delta = dO . O of this row (dO from the staged tile, O from global)
+      mbar_wait(bar_qfull, t & 1);
+      float delta = 0.f;
+      if (qvalid) {
+        const uint4* orow = reinterpret_cast<const uint4*>(bw.o + tok * bw.ldo + g.head * DHP);
+#pragma unroll
+        for (int ch = 0; ch < 16; ++ch) {
+          uint32_t a0, a1, a2, a3;
+          ld_shared_v4u(sDO + (ch >> 3) * 16384u + sw128_off(row, ch & 7), a0, a1, a2, a3);
+          const uint4 o4 = __ldg(orow + ch);
+          const uint32_t da[4] = {a0, a1, a2, a3}, oa[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 x = unpack_elem2(da[e]), y = unpack_elem2(oa[e]);
+            delta = fmaf(x.x, y.x, fmaf(x.y, y.y, delta));
+          }
+        }
+      }
+      for (int j = 0; j < g.nchunks; ++j, ++c) {
+        for (int h = 0; h < 2; ++h, ++hc) {
+          mbar_wait(bar_sfull(h), c & 1);
+          tc_fence_after();
+          // the previous half's partial MMAs must be done reading the P / dS staging rows
+          mbar_wait(bar_psfree, (hc & 1) ^ 1);
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub) {
+            uint32_t xs[32], xp[32];
+            tmem_ld32(tS + 64 * h + 32 * sub, xs);
+            tmem_ld32(tDP + 64 * h + 32 * sub, xp);
+            tmem_ld_wait();
+            uint32_t pp[16], pd[16];
+#pragma unroll
+            for (int k = 0; k < 32; k += 2) {
+              float e0, e1;
+              ffma2(e0, e1, __uint_as_float(xs[k]), __uint_as_float(xs[k + 1]), p.scale_log2, p.scale_log2, -lse,
+                    -lse);
+              float p0 = qvalid ? fast_exp2(e0) : 0.f, p1 = qvalid ? fast_exp2(e1) : 0.f;
+              const float d0 = p0 * (__uint_as_float(xp[k]) - delta), d1 = p1 * (__uint_as_float(xp[k + 1]) - delta);
+              pp[k >> 1] = pack_elem(p0, p1);
+              pd[k >> 1] = pack_elem(d0, d1);
+            }
+            // dS (fp16 pairs) over the consumed S columns: A operand of dQ
+            tmem_st16(tS + 64 * h + 16 * sub, pd);
+            // P / dS rows into the SW128 staging tiles (keys 32 sub .. 32 sub + 31 = 16-byte chunks 4 sub ..)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              st_shared_v4(sP + sw128_off(row, 4 * sub + q), pp[4 * q], pp[4 * q + 1], pp[4 * q + 2], pp[4 * q + 3]);
+              st_shared_v4(sDS + sw128_off(row, 4 * sub + q), pd[4 * q], pd[4 * q + 1], pd[4 * q + 2], pd[4 * q + 3]);
+            }
+          }
+          tmem_st_wait();
+          fence_proxy_async();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_pfull(h));
+        }
+      }
+      // ---- dQ epilogue ----
+      mbar_wait(bar_dqfull, t & 1);
+      tc_fence_after();
+      const float f = __ldg(bw.factors);
+      float* gq = bw.gqkv + tok * bw.ldg + g.head * DHP;
+#pragma unroll 1
+      for (int c0 = 0; c0 < DHP; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tDQ + c0, r);
+        tmem_ld_wait();
+        if (qvalid) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<float4*>(gq + c0 + e) =
+                make_float4(__uint_as_float(r[e]) * f, __uint_as_float(r[e + 1]) * f, __uint_as_float(r[e + 2]) * f,
+                            __uint_as_float(r[e + 3]) * f);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_dqempty);
+    }
+  } else if (warp >= 6) {
+    // ---------------- partial drain: thread = dh row ----------------
+    const int q4 = warp & 3;
+    const int d = 32 * q4 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(32 * q4) << 16;
+    int hc = 0;
+    for (int item = blockIdx.x; item < p.nitems; item += gridDim.x) {
+      const TileGeo g = tile_geo(p, item);
+      for (int j = 0; j < g.nchunks; ++j) {
+        for (int h = 0; h < 2; ++h, ++hc) {
+          mbar_wait(bar_partfull, hc & 1);
+          tc_fence_after();
+          float* base = bw.partial + (((static_cast<size_t>(item) * p.maxch + j) * 2 + h) * 2) * 64 * DHP + d;
+#pragma unroll
+          for (int kv = 0; kv < 2; ++kv) {
+#pragma unroll
+            for (int c0 = 0; c0 < 64; c0 += 32) {
+              uint32_t r[32];
+              tmem_ld32(tmem + lane_off + 384 + 64 * kv + c0, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) base[(static_cast<size_t>(kv) * 64 + c0 + e) * DHP] = __uint_as_float(r[e]);
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_partempty);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == NB_MMA_WARP) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// Key token held by every slot of every (tile, chunk): -1 for padding / zero-filled / out-of-grid slots.
+__global__ void natten_slot_table_kernel(NaParams p, int32_t* table) {
+  const int tile = blockIdx.x / p.maxch, j = blockIdx.x % p.maxch;
+  const TileGeo g = tile_geo(p, tile);
+  const int k = threadIdx.x;
+  int32_t tok = -1;
+  if (j < g.nchunks) {
+    int kd, kr0, nr, origin, vlo, vhi;
+    chunk_geo(g, p.cols, j, kd, kr0, nr, origin, vlo, vhi);
+    const int rr = k / g.ncp, cc = k - rr * g.ncp;
+    if (rr < nr && cc >= vlo && cc < vhi) {
+      const int kr = kr0 + rr;
+      const int col = wrap_col(g.pc0 + cc, p.cols);
+      if (kr >= 0 && kr < p.rows_global) tok = (kd * p.rows + (kr - p.row0)) * p.cols + col;
+    }
+  }
+  table[static_cast<size_t>(blockIdx.x) * 128 + k] = tok;
+}
+
+// dK / dV of every (key token, head): the sum of the partials of the (tile, chunk, slot) entries holding the key,
+// in CSR order (fixed), times the factors; one warp per (token, head), 4 channels per lane.
+__global__ void natten_bwd_reduce_kernel(const float* __restrict__ partial, const int32_t* __restrict__ off,
+                                         const int32_t* __restrict__ ent, int T, int heads, int ntiles, int maxch,
+                                         const float* __restrict__ factors, float* __restrict__ gqkv, int ldg) {
+  constexpr int DHP = 128;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wid >= T * heads) return;
+  const int tk = wid / heads, h = wid - tk * heads;
+  float4 ak = make_float4(0.f, 0.f, 0.f, 0.f), av = ak;
+  for (int e = off[tk]; e < off[tk + 1]; ++e) {
+    const int32_t code = ent[e];  // (tile * maxch + chunk) * 128 + slot
+    const int slot = code & 127, tc = code >> 7;
+    const int tile = tc / maxch, j = tc - tile * maxch;
+    const size_t item = static_cast<size_t>(h) * ntiles + tile;
+    const float* base = partial + (((item * maxch + j) * 2 + (slot >> 6)) * 2) * 64 * DHP +
+                        static_cast<size_t>(slot & 63) * DHP + 4 * lane;
+    const float4 k4 = __ldg(reinterpret_cast<const float4*>(base));
+    const float4 v4 = __ldg(reinterpret_cast<const float4*>(base + 64 * DHP));
+    ak.x += k4.x; ak.y += k4.y; ak.z += k4.z; ak.w += k4.w;
+    av.x += v4.x; av.y += v4.y; av.z += v4.z; av.w += v4.w;
+  }
+  const float fk = __ldg(factors), fv = __ldg(factors + 1);
+  float* g = gqkv + static_cast<size_t>(tk) * ldg + h * DHP + 4 * lane;
+  const int sec = heads * DHP;
+  *reinterpret_cast<float4*>(g + sec) = make_float4(ak.x * fk, ak.y * fk, ak.z * fk, ak.w * fk);
+  *reinterpret_cast<float4*>(g + 2 * sec) = make_float4(av.x * fv, av.y * fv, av.z * fv, av.w * fv);
 }
 
 __global__ void natten_windows_kernel(int depth, int rows, int cols, int rows_global, int row0, int wd, int wh,
@@ -722,9 +1136,11 @@ static void choose_tile(int depth, int cols, int rows_global, int wd, int wh, in
 
 using namespace wm3;
 
-static int natten_launch(const void* qkv, int ldqkv, void* out, int ldo, int batch, int depth, int rows, int cols,
-                         int rows_global, int row0, int halo_lo, int halo_hi, int heads, int dhp, int wd, int wh,
-                         int ww, float scale, int q_lo, int q_rows, void* stream) {
+// Geometry, tensor maps and (once per geometry) the window-bias images of an NA launch.
+static int natten_setup(const void* qkv, int ldqkv, void* out, int ldo, int batch, int depth, int rows, int cols,
+                        int rows_global, int row0, int halo_lo, int halo_hi, int heads, int dhp, int wd, int wh,
+                        int ww, float scale, int q_lo, int q_rows, void* stream, NaParams& p, CUtensorMap& tq,
+                        CUtensorMap& tkv, bool& bias) {
   if (dhp != 64 && dhp != 128) return set_error("wm3_natten_fwd: dhp must be 64 or 128 (got %d)", dhp);
   if (batch < 1) return set_error("wm3_natten_fwd: batch must be >= 1 (got %d)", batch);
   if (wd > depth || wh > rows_global || ww > cols) return set_error("wm3_natten_fwd: window exceeds extents");
@@ -745,7 +1161,7 @@ static int natten_launch(const void* qkv, int ldqkv, void* out, int ldo, int bat
   if ((ldqkv % 8) || (ldo % 16)) return set_error("wm3_natten_fwd: ldqkv must be a multiple of 8, ldo of 16");
   if (reinterpret_cast<uintptr_t>(out) % 32) return set_error("wm3_natten_fwd: out must be 32-byte aligned");
   if (ldqkv < 3 * heads * dhp) return set_error("wm3_natten_fwd: ldqkv < 3 * heads * dhp");
-  NaParams p{};
+  p = NaParams{};
   p.out = reinterpret_cast<elem_t*>(out);
   p.ldo = ldo;
   p.batch = batch;
@@ -780,7 +1196,6 @@ static int natten_launch(const void* qkv, int ldqkv, void* out, int ldo, int bat
   const uint64_t strides[3] = {static_cast<uint64_t>(ldqkv), wp * ldqkv, wp * p.rows_ext * ldqkv};
   const uint32_t qbox[4] = {64, static_cast<uint32_t>(p.TW), static_cast<uint32_t>(p.TH), static_cast<uint32_t>(p.TD)};
   const uint32_t kvbox[4] = {64, static_cast<uint32_t>(p.ncp), static_cast<uint32_t>(p.nrpc), 1};
-  CUtensorMap tq, tkv;
   if (make_tmap(&tq, qkv, TMAP_BF16, 4, dims, strides, qbox, nullptr)) return -1;
   if (make_tmap(&tkv, qkv, TMAP_BF16, 4, dims, strides, kvbox, nullptr)) return -1;
   for (auto kern : {natten_fwd_kernel<true, 64>, natten_fwd_kernel<false, 64>, natten_fwd_kernel<true, 128>,
@@ -791,13 +1206,16 @@ static int natten_launch(const void* qkv, int ldqkv, void* out, int ldo, int bat
     const char* e = getenv("WM3_NA_BIAS");
     return !(e && e[0] == '0');
   }();
-  const bool bias = bias_env && p.TD + p.TH + p.TW <= 16;
+  bias = bias_env && p.TD + p.TH + p.TW <= 16;
+  {
+    // depth planes of a tile's key patch x row chunks x parts: the chunk-slot stride of every per-chunk table
+    p.maxch = p.wd + p.TD - 1;
+    p.maxch = (p.maxch < depth ? p.maxch : depth) * ((p.wh + p.TH - 1 + p.nrpc - 1) / p.nrpc) * 2;
+  }
   if (bias) {
     // B_x images of every (tile, chunk): built once per geometry on this stream, kept for the process (a few
     // tens of MB at full scale, shared by every head, member, block and step)
     const int ntiles = p.ntd * p.nth * p.ntw;
-    p.maxch = p.wd + p.TD - 1;  // depth planes of a tile's key patch ...
-    p.maxch = (p.maxch < depth ? p.maxch : depth) * ((p.wh + p.TH - 1 + p.nrpc - 1) / p.nrpc) * 2;  // x row chunks x parts
     struct Key {
       // the images depend on the launch's global tile rows only (not on the band or its halos)
       int dev, depth, cols, rows_global, th_first, nth, wd, wh, ww, TD, TH, TW, ncp, nrpc;
@@ -844,6 +1262,19 @@ static int natten_launch(const void* qkv, int ldqkv, void* out, int ldo, int bat
     }
     p.bias_table = it->second;
   }
+  return 0;
+}
+
+static int natten_launch(const void* qkv, int ldqkv, void* out, int ldo, int batch, int depth, int rows, int cols,
+                         int rows_global, int row0, int halo_lo, int halo_hi, int heads, int dhp, int wd, int wh,
+                         int ww, float scale, int q_lo, int q_rows, void* stream, float* lse = nullptr) {
+  NaParams p;
+  CUtensorMap tq, tkv;
+  bool bias = false;
+  if (natten_setup(qkv, ldqkv, out, ldo, batch, depth, rows, cols, rows_global, row0, halo_lo, halo_hi, heads, dhp,
+                   wd, wh, ww, scale, q_lo, q_rows, stream, p, tq, tkv, bias))
+    return -1;
+  p.lse = lse;
   const int slots = NA_CTAS_PER_SM * sm_count();
   const int grid = p.nitems < slots ? p.nitems : slots;
   auto kern = dhp == 64 ? (bias ? natten_fwd_kernel<true, 64> : natten_fwd_kernel<false, 64>)
@@ -892,3 +1323,88 @@ extern "C" int wm3_na_trace(long long* out, int max_events) {
   return n;
 }
 #endif
+
+// ---------------------------------------------------------------------------------------------------------------
+// Attention backward (natten_bwd_kernel + natten_bwd_reduce_kernel), full domain (no band / halo), batch 1.
+// ---------------------------------------------------------------------------------------------------------------
+extern "C" int wm3_natten_fwd_lse(const void* qkv, int ldqkv, void* out, int ldo, int depth, int rows, int cols,
+                                  int heads, int dhp, int wd, int wh, int ww, float scale, float* lse, void* stream) {
+  return natten_launch(qkv, ldqkv, out, ldo, 1, depth, rows, cols, rows, 0, 0, 0, heads, dhp, wd, wh, ww, scale, 0,
+                       rows, stream, lse);
+}
+
+static int natten_bwd_geom(int depth, int rows, int cols, int heads, int dhp, int wd, int wh, int ww, void* stream,
+                           NaParams& p, CUtensorMap& tq, CUtensorMap& tkv, bool& bias) {
+  // geometry only: the tensor maps are rebuilt by the launch with the real operands
+  void* dummy = reinterpret_cast<void*>(static_cast<uintptr_t>(1) << 20);
+  return natten_setup(dummy, 3 * heads * dhp, dummy, heads * dhp, 1, depth, rows, cols, rows, 0, 0, 0, heads, dhp, wd,
+                      wh, ww, 1.f, 0, rows, stream, p, tq, tkv, bias);
+}
+
+// Tiles and chunk-slot stride of the backward's geometry; supported = 1 when the tcgen05 backward applies
+// (head dim padded to 128 and the window mask in the MMA), else the caller uses wm3_bw_natten.
+extern "C" int wm3_natten_bwd_info(int depth, int rows, int cols, int heads, int dhp, int wd, int wh, int ww,
+                                   int* ntiles, int* maxch, int* supported, void* stream) {
+  NaParams p;
+  CUtensorMap tq, tkv;
+  bool bias = false;
+  if (natten_bwd_geom(depth, rows, cols, heads, dhp, wd, wh, ww, stream, p, tq, tkv, bias)) return -1;
+  *ntiles = p.ntd * p.nth * p.ntw;
+  *maxch = p.maxch;
+  *supported = (dhp == 128 && bias) ? 1 : 0;
+  return 0;
+}
+
+// [tile][maxch][128] key token of every chunk slot (-1: none), for the host-built CSR of the dK / dV reduction.
+extern "C" int wm3_natten_slot_table(int depth, int rows, int cols, int heads, int dhp, int wd, int wh, int ww,
+                                     int32_t* table, void* stream) {
+  NaParams p;
+  CUtensorMap tq, tkv;
+  bool bias = false;
+  if (natten_bwd_geom(depth, rows, cols, heads, dhp, wd, wh, ww, stream, p, tq, tkv, bias)) return -1;
+  const int ntiles = p.ntd * p.nth * p.ntw;
+  natten_slot_table_kernel<<<ntiles * p.maxch, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p, table);
+  return check_launch("natten_slot_table_kernel");
+}
+
+extern "C" int wm3_natten_bwd(const void* qkv, int ldqkv, const void* dout, int ldd, const void* o, int ldo,
+                              const float* lse, float* gqkv, int ldg, float* partial, const int32_t* csr_off,
+                              const int32_t* csr_ent, const float* factors, int depth, int rows, int cols, int heads,
+                              int dhp, int wd, int wh, int ww, float scale, void* stream) {
+  if (dhp != 128) return set_error("wm3_natten_bwd: head dim must be padded to 128 (got %d)", dhp);
+  if ((ldd % 8) || (ldo % 8) || (ldg % 4)) return set_error("wm3_natten_bwd: bad leading dimensions");
+  NaParams p;
+  CUtensorMap tq, tkv;
+  bool bias = false;
+  if (natten_setup(qkv, ldqkv, const_cast<void*>(o), ldo, 1, depth, rows, cols, rows, 0, 0, 0, heads, dhp, wd, wh, ww,
+                   scale, 0, rows, stream, p, tq, tkv, bias))
+    return -1;
+  if (!bias) return set_error("wm3_natten_bwd: the window mask must fit the MMA bias step (TD + TH + TW <= 16)");
+  const uint64_t dims[4] = {static_cast<uint64_t>(heads * dhp), static_cast<uint64_t>(cols),
+                            static_cast<uint64_t>(rows), static_cast<uint64_t>(depth)};
+  const uint64_t strides[3] = {static_cast<uint64_t>(ldd), static_cast<uint64_t>(cols) * ldd,
+                               static_cast<uint64_t>(cols) * rows * ldd};
+  const uint32_t box[4] = {64, static_cast<uint32_t>(p.TW), static_cast<uint32_t>(p.TH), static_cast<uint32_t>(p.TD)};
+  CUtensorMap tdo;
+  if (make_tmap(&tdo, dout, TMAP_BF16, 4, dims, strides, box, nullptr)) return -1;
+  NaBwd b{};
+  b.dout = reinterpret_cast<const elem_t*>(dout);
+  b.ldd = ldd;
+  b.o = reinterpret_cast<const elem_t*>(o);
+  b.ldo = ldo;
+  b.lse = lse;
+  b.gqkv = gqkv;
+  b.ldg = ldg;
+  b.partial = partial;
+  b.factors = factors;
+  if (ensure_smem_attr(reinterpret_cast<const void*>(natten_bwd_kernel<true>), NB_SMEM, "natten_bwd")) return -1;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int grid = p.nitems < sm_count() ? p.nitems : sm_count();
+  natten_bwd_kernel<true><<<grid, NB_THREADS, NB_SMEM, s>>>(tq, tkv, tdo, p, b);
+  if (check_launch("natten_bwd_kernel")) return -1;
+  const int T = depth * rows * cols;
+  const int blocks = (T * heads * 32 + 255) / 256;
+  natten_bwd_reduce_kernel<<<blocks, 256, 0, s>>>(partial, csr_off, csr_ent, T, heads, p.ntd * p.nth * p.ntw,
+                                                  p.maxch, factors, gqkv, ldg);
+  return check_launch("natten_bwd_reduce_kernel");
+}

@@ -225,3 +225,36 @@ def test_rollout_vjp_host_offload_bitwise(lookahead):
 def torch_equal(a, b):
     import torch
     return bool(torch.equal(a, b))
+
+
+@pytest.mark.parametrize("ext,win,dim,heads", [
+    ((5, 18, 36), (5, 7, 7), 1024, 8),   # full-scale block width on a smaller grid: row bump, column wrap
+    ((5, 30, 60), (5, 7, 7), 256, 2),
+    ((5, 90, 180), (5, 7, 7), 1024, 8),  # full scale
+    ((6, 12, 20), (3, 5, 5), 256, 2),    # depth bump, smaller window
+])
+def test_tensor_core_attention_backward_matches_cuda_core(ext, win, dim, heads, monkeypatch):
+    """The tcgen05 attention backward (wm3_natten_bwd: dQ per query tile, dK / dV as CSR-ordered sums of per-chunk
+    partials) against the CUDA-core gather kernels (wm3_bw_natten) inside the same block VJP: input and every
+    parameter gradient, and bitwise repeatable."""
+    from paper_2503_22235_b200.backward import _TcAttention, block_vjp
+    from paper_2503_22235_b200.params import init_block_params
+    t = int(np.prod(ext))
+    rng = np.random.default_rng(t + dim)
+    params = init_block_params(rng, dim, heads, "blk", zero_residual=False)
+    x = rng.standard_normal((t, dim))
+    gy = rng.standard_normal((t, dim))
+    dhp = (dim // heads + 63) // 64 * 64
+    if _TcAttention.get(ext, win, heads, dhp) is None:
+        assert ext != (5, 90, 180), "the full-scale geometry must run on the tensor-core path"
+        pytest.skip("geometry outside the tensor-core backward (window mask does not fit the MMA bias step)")
+    gx_tc, pg_tc = block_vjp(x, params, "blk", ext, win, heads, gy)
+    gx_tc2, pg_tc2 = block_vjp(x, params, "blk", ext, win, heads, gy)
+    monkeypatch.setenv("WM3_BW_NA", "cuda")
+    gx_cc, pg_cc = block_vjp(x, params, "blk", ext, win, heads, gy)
+    errs = {"x": _rel(gx_tc, gx_cc)}
+    errs.update({n: _rel(pg_tc[n], pg_cc[n]) for n in pg_cc if np.linalg.norm(pg_cc[n]) > 0})
+    worst = max(errs, key=errs.get)
+    print(f"tc vs cuda-core attention backward {ext} D={dim}: x {errs['x']:.2e}, worst {worst} {errs[worst]:.2e}")
+    assert errs[worst] < 5e-3, (worst, errs[worst])
+    assert np.array_equal(gx_tc, gx_tc2) and all(np.array_equal(pg_tc[n], pg_tc2[n]) for n in pg_tc)
