@@ -284,7 +284,8 @@ def measure_backward(reps: int = 3) -> dict:
     tf = 3.0 * block_flops(t) / 1e12  # forward recompute + 2x for the backward, algorithmic
     return {"block_vjp_ms": round(ms, 3), "algorithmic_tflop": round(tf, 3), "tflops": round(tf / (ms / 1e3), 1),
             "note": "one full-shape block: forward recompute + backward (dX and all parameter gradients); the "
-                    "attention backward is a CUDA-core kernel pair (query side / key side), see DESIGN.md §9"}
+                    "attention backward on tcgen05 (wm3_natten_bwd: dQ per query tile, dK / dV as per-chunk partials "
+                    "reduced per key in a fixed order)"}
 
 
 def measure_config3(state, params, cfg, reps: int = 3) -> dict:
