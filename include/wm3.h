@@ -292,6 +292,12 @@ int wm3_bw_natten(const void* qkv, int ldq, const int64_t* nbr, const int* inv_o
                   float* dS, float* work, float* gout, int ldg, void* stream);
 int wm3_bw_rope(float* g, int ldg, int T, int heads, int dhp, const float* cos_t, const float* sin_t, void* stream);
 
+/* C[m][n] (fp32) = sum_t A[t][m] B[t][n] with A [k][m], B [k][n] row-major 16-bit (the backward's weight gradients
+ * over the token axis, autodiff.py:350 matmul VJP): MN-major tcgen05 operands, no transposed copies; m, n multiples
+ * of 64. */
+int wm3_linear_tn(const void* a, int lda, const void* b, int ldb, int m, int n, int k, float* out, int ldo,
+                  void* stream);
+
 /* Attention backward on the tensor cores (replaces wm3_bw_natten when wm3_natten_bwd_info reports support: head
  * dim padded to 128, window mask in the MMA).  Same reference rules (attention.py:173-178 through autodiff.py's
  * matmul / softmax / take VJPs); full domain, one member.

@@ -109,6 +109,7 @@ SIGNATURES = {
     "wm3_bw_layernorm": [_vp, _i, _i, _i, _f, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp],
     "wm3_bw_natten": [_vp, _i, _vp, _vp, _vp, _i, _i, _i, _i, _f, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp],
     "wm3_bw_rope": [_vp, _i, _i, _i, _i, _vp, _vp, _vp],
+    "wm3_linear_tn": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _i, _vp],
     "wm3_bw_na_prep": [_vp, _i, _i, _i, _i, _vp, _i, _vp, _f, _vp, _i, _vp, _vp, _vp],
     "wm3_natten_fwd_lse": [_vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _f, _vp, _vp],
     "wm3_natten_bwd_info": [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp],

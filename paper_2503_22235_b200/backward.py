@@ -88,6 +88,15 @@ def _colsum(src: torch.Tensor, rows: int, cols: int, src2: torch.Tensor | None =
     return out
 
 
+def _gemm_tn(a: torch.Tensor, b: torch.Tensor, m: int, n: int, k: int) -> torch.Tensor:
+    """fp32 C[m][n] = sum_t A[t][:m] B[t][:n] over k rows (the weight gradients over tokens): MN-major tcgen05
+    operands straight from the row-major 16-bit tensors, no transposed copies."""
+    out = torch.empty((m, n), dtype=torch.float32, device=a.device)
+    check(_lib.lib().wm3_linear_tn(ptr(a), a.stride(0), ptr(b), b.stride(0), m, n, k, ptr(out), out.stride(0),
+                                   stream_ptr()), "wm3_linear_tn")
+    return out
+
+
 def _gemm(a: torch.Tensor, b: torch.Tensor, m: int, n: int, k: int) -> torch.Tensor:
     """fp32 C[m][n] = A[m][:k] . B[n][:k]^T on the tcgen05 GEMM (raw accumulators, scaled operands)."""
     out = torch.empty((m, n), dtype=torch.float32, device=a.device)
@@ -230,7 +239,6 @@ def block_vjp_device(xd: torch.Tensor, bw, extents, window, heads: int, dh: int,
     T, D = xd.shape
     dev = xd.device
     dhp, hd, kp, np_, nm = bw.dhp, bw.heads * bw.dhp, bw.kp, bw.np_, bw.nm
-    Tp = _r8(T)
     L = _lib
     wt = _transposed_weights(bw)
     rope = CACHE.rope(extents, dh)
@@ -255,9 +263,8 @@ def block_vjp_device(xd: torch.Tensor, bw, extents, window, heads: int, dh: int,
 
     # ---- W2 ----
     s1 = _amax(gyd, T, D)
-    gyh = _cast(gyd, T, D, np_, scale=s1)
-    gyT = _cast(gyd, T, D, Tp, transpose=True, scale=s1)
-    dw2 = _gemm(gyT, _cast(mid, T, nm, Tp, transpose=True), D, nm, T)   # (D, nm), x s1
+    gyh = _cast(gyd, T, D, kp, scale=s1)                                # zero-padded to kp >= np_
+    dw2 = _gemm_tn(gyh, mid, kp, nm, T)                                 # (kp, nm), x s1
     db2 = _colsum(gyd, T, D)
     g_mid = _gemm(gyh, wt["w_2"], T, nm, np_)                           # x s1
     # ---- GELU' and W1 ----
@@ -265,9 +272,10 @@ def block_vjp_device(xd: torch.Tensor, bw, extents, window, heads: int, dh: int,
     check(L.lib().wm3_bw_gelu(ptr(g_mid), nm, ptr(a0), nm, ptr(bw.b_1), T, nm, s1.ptr(), ptr(g_a), nm, stream_ptr()),
           "wm3_bw_gelu")
     s2 = _amax(g_a, T, nm)
-    dw1 = _gemm(_cast(g_a, T, nm, Tp, transpose=True, scale=s2), _cast(hn2, T, kp, Tp, transpose=True), nm, kp, T)
+    gah = _cast(g_a, T, nm, nm, scale=s2)
+    dw1 = _gemm_tn(gah, hn2, nm, kp, T)
     db1 = _colsum(g_a, T, nm)
-    g_hn2 = _gemm(_cast(g_a, T, nm, nm, scale=s2), wt["w_1"], T, kp, nm)   # x s2
+    g_hn2 = _gemm(gah, wt["w_1"], T, kp, nm)   # x s2
     # ---- LN2 (+ the residual path gy) ----
     gx1 = torch.empty((T, D), dtype=torch.float32, device=dev)
     gxh2 = torch.empty_like(gx1)
@@ -278,9 +286,10 @@ def block_vjp_device(xd: torch.Tensor, bw, extents, window, heads: int, dh: int,
     dln2_b = _colsum(gsc2, T, D)
     # ---- O-proj ----
     s3 = _amax(gx1, T, D)
-    dwo = _gemm(_cast(gx1, T, D, Tp, transpose=True, scale=s3), _cast(ctx, T, hd, Tp, transpose=True), D, hd, T)
+    gx1h = _cast(gx1, T, D, kp, scale=s3)
+    dwo = _gemm_tn(gx1h, ctx, kp, hd, T)
     dbo = _colsum(gx1, T, D)
-    g_ctx = _gemm(_cast(gx1, T, D, np_, scale=s3), wt["w_o"], T, hd, np_)  # x s3
+    g_ctx = _gemm(gx1h, wt["w_o"], T, hd, np_)  # x s3
     # ---- attention (query and key sides) and the rotary transpose ----
     g_qkv = torch.zeros((T, 3 * hd), dtype=torch.float32, device=dev)
     if tca is not None:
@@ -303,10 +312,10 @@ def block_vjp_device(xd: torch.Tensor, bw, extents, window, heads: int, dh: int,
     check(L.lib().wm3_bw_rope(ptr(g_qkv), 3 * hd, T, heads, dhp, ptr(cs), ptr(sn), stream_ptr()), "wm3_bw_rope")
     # ---- QKV ----
     s4 = _amax(g_qkv, T, 3 * hd)
-    dwqkv = _gemm(_cast(g_qkv, T, 3 * hd, Tp, transpose=True, scale=s4), _cast(hn, T, kp, Tp, transpose=True),
-                  3 * hd, kp, T)
+    gqh = _cast(g_qkv, T, 3 * hd, 3 * hd, scale=s4)
+    dwqkv = _gemm_tn(gqh, hn, 3 * hd, kp, T)
     dbqkv = _colsum(g_qkv, T, 3 * hd)
-    g_hn = _gemm(_cast(g_qkv, T, 3 * hd, 3 * hd, scale=s4), wt["w_qkv"], T, kp, 3 * hd)  # x s4
+    g_hn = _gemm(gqh, wt["w_qkv"], T, kp, 3 * hd)  # x s4
     # ---- LN1 (+ gx1) ----
     gx = torch.empty((T, D), dtype=torch.float32, device=dev)
     gxh1 = torch.empty_like(gx)
@@ -353,7 +362,7 @@ def block_grads_to_reference(acc: BlockGrads, bw, params: dict, prefix: str, dh:
         grads[wn], grads[bn] = gw, gb
     gwo = np.zeros((D, D))
     okv = vv >= 0
-    gwo[vv[okv]] = g["w_o"][:, okv].T
+    gwo[vv[okv]] = g["w_o"][:D, okv].T
     grads["attn.wo"], grads["attn.bo"] = gwo, g["b_o"]
     from .tensor import host_values
     hidden_mlp = host_values(params[f"{prefix}.mlp.w1"]).shape[1]

@@ -38,6 +38,7 @@ struct EpiParams {
   int has_halo;
   wm3_ln_fold_t fold;  // LayerNorm fold (include/wm3.h): producer (residual epilogue) / consumer (next GEMM)
   int ln_prod, ln_cons;
+  int mn;  // operands MN-major (wm3_linear_tn: C = A^T B with A [K][M], B [K][N] row-major, 64 x 64 boxes)
 };
 
 constexpr int GEMM_BM = 128;
@@ -257,7 +258,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sa = sbase + stage * Cfg::STAGE_BYTES;
           const uint32_t sb = sa + Cfg::A_BYTES;
-          if (CG == 2) {
+          if (ep.mn) {
+            // MN-major operands: 64 (M or N) x 64 (K) boxes, each 64 K-rows of 128 B
+            const uint32_t fb = (CG == 2) ? mapa_shared(full_bar(stage), 0) : full_bar(stage);
+            if (rank == 0) mbar_arrive_expect_tx(full_bar(stage), CG * Cfg::STAGE_BYTES);
+            for (int i = 0; i < GEMM_BM / 64; ++i) {
+              if (CG == 2) tma_load_2d_cg2(sa + i * 8192u, &tmA, fb, m0 + 64 * i, kb * GEMM_BK);
+              else tma_load_2d(sa + i * 8192u, &tmA, fb, m0 + 64 * i, kb * GEMM_BK);
+            }
+            for (int i = 0; i < BN / CG / 64; ++i) {
+              if (CG == 2) tma_load_2d_cg2(sb + i * 8192u, &tmB, fb, n0 + 64 * i, kb * GEMM_BK);
+              else tma_load_2d(sb + i * 8192u, &tmB, fb, n0 + 64 * i, kb * GEMM_BK);
+            }
+          } else if (CG == 2) {
             // both CTAs' bytes complete on the leader's full barrier; only the leader arms it
             const uint32_t fb = mapa_shared(full_bar(stage), 0);
             if (rank == 0) mbar_arrive_expect_tx(full_bar(stage), 2 * Cfg::STAGE_BYTES);
@@ -276,8 +289,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (rank == 0) {  // the leader issues the pair's MMAs
       // The whole warp walks the k-blocks (warp-wide waits, warp-uniform descriptors in uniform registers);
       // one elected lane issues the MMAs and commits.
-      constexpr uint32_t idesc = make_idesc(GEMM_BM * CG, BN, 0, 0);
-      const uint64_t d0 = make_sdesc_sw128(sbase, 16, 1024);
+      const uint32_t idesc = make_idesc(GEMM_BM * CG, BN, ep.mn, ep.mn);
+      // K-major: k-steps of 16 elements are 32 B apart in a row; MN-major: 16 K-rows (2 KB), 64-wide M / N
+      // chunks 8 KB apart (LBO)
+      const uint64_t d0 = make_sdesc_sw128(sbase, ep.mn ? 8192u : 16u, 1024);
+      const uint32_t kstep = ep.mn ? 128u : 2u;
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -294,9 +310,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
             for (int k = 0; k < GEMM_BK / 16; ++k) {
               if (CG == 2)
-                umma_ss_cg2(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+                umma_ss_cg2(d_tmem, ad + kstep * k, bd + kstep * k, idesc, (kb | k) != 0 ? 1u : 0u);
               else
-                umma_bf16_ss(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+                umma_bf16_ss(d_tmem, ad + kstep * k, bd + kstep * k, idesc, (kb | k) != 0 ? 1u : 0u);
             }
             if (CG == 2)
               umma_commit_mc(empty_bar(stage), 0x3);  // frees the stage in both CTAs
@@ -631,7 +647,8 @@ struct OutPlanes {
 
 static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi, void* out,
                        int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, const OutPlanes& op,
-                       void* stream, const wm3_halo_t* halo = nullptr, const wm3_ln_fold_t* fold = nullptr) {
+                       void* stream, const wm3_halo_t* halo = nullptr, const wm3_ln_fold_t* fold = nullptr,
+                       bool mn = false) {
   if (m <= 0 || n <= 0 || k <= 0) return set_error("wm3_linear: bad sizes m=%d n=%d k=%d", m, n, k);
   const bool f32_out = (epi == WM3_EPI_F32 || epi == WM3_EPI_BIAS_RESID_F32);
   if ((lda % 8) || (ldb % 8) || (ldo % (f32_out ? 4 : 8)))
@@ -700,8 +717,14 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
     if (ep.rope.dhp != 64 && ep.rope.dhp != 128) return set_error("wm3_linear: dhp must be 64 or 128");
   }
   CUtensorMap ta, tb, to;
-  if (make_tmap_2d_bf16(&ta, a, k, m, lda, GEMM_BK, GEMM_BM)) return -1;
-  if (make_tmap_2d_bf16(&tb, b, k, n, ldb, GEMM_BK, bn / cg)) return -1;  // each CTA of a pair loads half
+  ep.mn = mn ? 1 : 0;
+  if (mn) {  // A [k][m], B [k][n] row-major: 64 x 64 boxes (M / N inner)
+    if (make_tmap_2d_bf16(&ta, a, m, k, lda, 64, GEMM_BK)) return -1;
+    if (make_tmap_2d_bf16(&tb, b, n, k, ldb, 64, GEMM_BK)) return -1;
+  } else {
+    if (make_tmap_2d_bf16(&ta, a, k, m, lda, GEMM_BK, GEMM_BM)) return -1;
+    if (make_tmap_2d_bf16(&tb, b, k, n, ldb, GEMM_BK, bn / cg)) return -1;  // each CTA of a pair loads half
+  }
   {
     const int cw = f32_out ? 32 : 64;
     const size_t esz = f32_out ? 4 : 2;
@@ -782,4 +805,14 @@ extern "C" int wm3_halo_wait(const int* flags, int n, int epoch, void* stream) {
   if (n <= 0) return 0;
   halo_wait_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(flags, n, epoch);
   return check_launch("halo_wait_kernel");
+}
+
+// C[m][n] (fp32) = sum_t A[t][m] B[t][n]: both operands row-major over the reduction axis (the backward's
+// weight gradients over tokens, autodiff.py:350 matmul VJP), read as MN-major tiles: no transposed copies.
+extern "C" int wm3_linear_tn(const void* a, int lda, const void* b, int ldb, int m, int n, int k, float* out, int ldo,
+                             void* stream) {
+  if ((m % 64) || (n % 64)) return set_error("wm3_linear_tn: m=%d and n=%d must be multiples of 64", m, n);
+  const OutPlanes op{1, m, m, 0};
+  return linear_impl(a, lda, b, ldb, m, n, k, WM3_EPI_F32, out, ldo, n, nullptr, nullptr, op, stream, nullptr,
+                     nullptr, true);
 }
