@@ -28,17 +28,33 @@ DEVI float grad_scale(const unsigned* amax_bits) {
   return exp2f(14.f - ceilf(log2f(amax)));
 }
 
+// Row strips: block b takes rows b, b + grid, ...; its threads sweep the columns (4 at a time when the rows are
+// 16-byte aligned), so there is no per-element 64-bit index division; one atomic per block.
 __global__ void bw_amax_kernel(const float* __restrict__ x, int rows, int cols, int ld, unsigned* amax_bits) {
+  __shared__ float red[32];
   float m = 0.f;
-  const long long n = static_cast<long long>(rows) * cols;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long r = i / cols, c = i - r * cols;
-    m = fmaxf(m, fabsf(x[r * ld + c]));
+  const bool v4 = (cols % 4 == 0) && (ld % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    const float* xr = x + static_cast<size_t>(r) * ld;
+    if (v4) {
+      for (int c = 4 * threadIdx.x; c < cols; c += 4 * blockDim.x) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(xr + c));
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(q.x), fabsf(q.y)), fmaxf(fabsf(q.z), fabsf(q.w))));
+      }
+    } else {
+      for (int c = threadIdx.x; c < cols; c += blockDim.x) m = fmaxf(m, fabsf(xr[c]));
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(amax_bits, __float_as_uint(m));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) atomicMax(amax_bits, __float_as_uint(m));
+  }
 }
 
 // dst = operand(src * scale), row-major [rows][ld_dst] (columns >= cols zero) or transposed [cols][ld_dst]
@@ -49,7 +65,7 @@ __global__ void bw_cast_kernel(const void* __restrict__ src, int f32, int rows, 
   const float s = grad_scale(amax_bits);
   const int tr = blockIdx.y * 32, tc = blockIdx.x * 32;  // tile origin in dst coordinates
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
-  if (!transpose) {
+  if (!transpose) {  // (row-major casts take bw_cast_rows_kernel; kept for completeness)
     for (int i = ty; i < 32; i += 8) {
       const int r = tr + i, c = tc + tx;
       if (r >= rows || c >= ldd) continue;
@@ -76,6 +92,27 @@ __global__ void bw_cast_kernel(const void* __restrict__ src, int f32, int rows, 
   for (int i = ty; i < 32; i += 8) {
     const int dr = tr + i, dc = tc + tx;
     if (dr < cols && dc < ldd) dst[static_cast<size_t>(dr) * ldd + dc] = to_elem(tile[tx][i] * s);
+  }
+}
+
+// Row-major fp32 -> 16-bit operand copy (times the scale), 8 elements per thread-step: two 16-byte loads, one
+// 16-byte store; columns in [cols, ldd) are zero.  Needs cols, lds, ldd multiples of 8 and aligned bases.
+__global__ void bw_cast_rows_kernel(const float* __restrict__ src, int rows, int cols, int lds, elem_t* __restrict__ dst,
+                                    int ldd, const unsigned* amax_bits) {
+  const float s = grad_scale(amax_bits);
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    const float* sr = src + static_cast<size_t>(r) * lds;
+    elem_t* dr = dst + static_cast<size_t>(r) * ldd;
+    for (int c = 8 * threadIdx.x; c < ldd; c += 8 * blockDim.x) {
+      uint4 o = make_uint4(0u, 0u, 0u, 0u);
+      if (c < cols) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(sr + c));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(sr + c + 4));
+        o = make_uint4(pack_elem(a.x * s, a.y * s), pack_elem(a.z * s, a.w * s), pack_elem(b.x * s, b.y * s),
+                       pack_elem(b.z * s, b.w * s));
+      }
+      *reinterpret_cast<uint4*>(dr + c) = o;
+    }
   }
 }
 
@@ -108,13 +145,15 @@ __global__ void bw_gelu_kernel(const float* __restrict__ g, int ldg, const float
                                const float* __restrict__ bias, int rows, int cols, const unsigned* amax_bits,
                                float* __restrict__ out, int ldo) {
   const float inv = 1.f / grad_scale(amax_bits);
-  const long long n = static_cast<long long>(rows) * cols;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long r = i / cols, c = i - r * cols;
-    const float z = a[r * lda + c] + bias[c];
-    const float d = 0.5f * (1.f + erff(z * 0.70710678118654752f)) + z * 0.39894228040143268f * expf(-0.5f * z * z);
-    out[r * ldo + c] = g[r * ldg + c] * inv * d;
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {  // row strips (see bw_amax_kernel)
+    const float* gr = g + static_cast<size_t>(r) * ldg;
+    const float* ar = a + static_cast<size_t>(r) * lda;
+    float* orow = out + static_cast<size_t>(r) * ldo;
+    for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+      const float z = ar[c] + __ldg(bias + c);
+      const float d = 0.5f * (1.f + erff(z * 0.70710678118654752f)) + z * 0.39894228040143268f * __expf(-0.5f * z * z);
+      orow[c] = gr[c] * inv * d;
+    }
   }
 }
 
@@ -308,13 +347,19 @@ using namespace wm3;
 extern "C" int wm3_bw_amax(const float* x, int rows, int cols, int ld, unsigned* amax_bits, void* stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(amax_bits, 0, sizeof(unsigned), s) != cudaSuccess) return set_error("wm3_bw_amax: memset");
-  bw_amax_kernel<<<grid_for(static_cast<long long>(rows) * cols, 256), 256, 0, s>>>(x, rows, cols, ld, amax_bits);
+  bw_amax_kernel<<<rows < 148 * 8 ? rows : 148 * 8, 256, 0, s>>>(x, rows, cols, ld, amax_bits);
   return check_launch("bw_amax_kernel");
 }
 
 extern "C" int wm3_bw_cast(const void* src, int src_f32, int rows, int cols, int lds, void* dst, int ldd,
                            int transpose, const unsigned* amax_bits, void* stream) {
   if (rows < 1 || cols < 1) return set_error("wm3_bw_cast: empty");
+  if (!transpose && src_f32 && cols % 8 == 0 && lds % 8 == 0 && ldd % 8 == 0 &&
+      reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0) {
+    bw_cast_rows_kernel<<<rows < 148 * 8 ? rows : 148 * 8, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        static_cast<const float*>(src), rows, cols, lds, reinterpret_cast<elem_t*>(dst), ldd, amax_bits);
+    return check_launch("bw_cast_rows_kernel");
+  }
   const int drows = transpose ? cols : rows;
   dim3 grid((ldd + 31) / 32, (drows + 31) / 32);
   bw_cast_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
@@ -334,7 +379,7 @@ extern "C" int wm3_bw_colsum(const float* src, const float* src2, int rows, int 
 
 extern "C" int wm3_bw_gelu(const float* g, int ldg, const float* a, int lda, const float* bias, int rows, int cols,
                            const unsigned* amax_bits, float* out, int ldo, void* stream) {
-  bw_gelu_kernel<<<grid_for(static_cast<long long>(rows) * cols, 256), 256, 0,
+  bw_gelu_kernel<<<rows < 148 * 8 ? rows : 148 * 8, 256, 0,
                    reinterpret_cast<cudaStream_t>(stream)>>>(g, ldg, a, lda, bias, rows, cols, amax_bits, out, ldo);
   return check_launch("bw_gelu_kernel");
 }
@@ -378,28 +423,29 @@ extern "C" int wm3_bw_rope(float* g, int ldg, int T, int heads, int dhp, const f
 // ---------------------------------------------------------------------------------------------------------------
 __global__ void bw_na_prep_reduce_kernel(const elem_t* __restrict__ qkv, int ldq, int T, int heads, int dhp,
                                          const float* __restrict__ gctx, int ldc, unsigned* __restrict__ maxima) {
-  // maxima[0] = max |g_ctx| over the (T, heads * dhp) block, maxima[1] = max over (token, head) of sum |v|
+  // maxima[0] = max |g_ctx| over the (T, heads * dhp) block, maxima[1] = max over (token, head) of sum |v|;
+  // one warp per (token, head) at a time, lanes over the channels (coalesced), one atomic pair per warp
   const int sec = heads * dhp;
+  const int lane = threadIdx.x & 31;
+  const long long nw = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
   float mg = 0.f, mv = 0.f;
-  const long long n = static_cast<long long>(T) * heads;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int t = static_cast<int>(i / heads), h = static_cast<int>(i - static_cast<long long>(t) * heads);
+  for (long long w = blockIdx.x * static_cast<long long>(blockDim.x >> 5) + (threadIdx.x >> 5);
+       w < static_cast<long long>(T) * heads; w += nw) {
+    const int t = static_cast<int>(w / heads), h = static_cast<int>(w - static_cast<long long>(t) * heads);
     const elem_t* v = qkv + static_cast<size_t>(t) * ldq + 2 * sec + h * dhp;
     const float* g = gctx + static_cast<size_t>(t) * ldc + h * dhp;
     float l1 = 0.f;
-    for (int c = 0; c < dhp; ++c) {
+    for (int c = lane; c < dhp; c += 32) {
       l1 += fabsf(to_f(v[c]));
       mg = fmaxf(mg, fabsf(g[c]));
     }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
     mv = fmaxf(mv, l1);
   }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, o));
-    mv = fmaxf(mv, __shfl_xor_sync(0xffffffffu, mv, o));
-  }
-  if ((threadIdx.x & 31) == 0) {
+  for (int o = 16; o; o >>= 1) mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, o));
+  if (lane == 0) {
     atomicMax(maxima, __float_as_uint(mg));
     atomicMax(maxima + 1, __float_as_uint(mv));
   }
@@ -428,7 +474,7 @@ extern "C" int wm3_bw_na_prep(const void* qkv, int ldq, int T, int heads, int dh
                               float* factors, void* stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaMemsetAsync(maxima, 0, 2 * sizeof(unsigned), s);
-  bw_na_prep_reduce_kernel<<<grid_for(static_cast<long long>(T) * heads, 256), 256, 0, s>>>(
+  bw_na_prep_reduce_kernel<<<148 * 8, 256, 0, s>>>(
       reinterpret_cast<const elem_t*>(qkv), ldq, T, heads, dhp, gctx, ldc, maxima);
   if (check_launch("bw_na_prep_reduce_kernel")) return -1;
   bw_na_prep_scale_kernel<<<grid_for(static_cast<long long>(T) * heads * dhp, 256), 256, 0, s>>>(
