@@ -342,38 +342,45 @@ def block_vjp_device(xd: torch.Tensor, bw, extents, window, heads: int, dh: int,
 
 def block_grads_to_reference(acc: BlockGrads, bw, params: dict, prefix: str, dh: int, hidden: int) -> dict:
     """The accumulated kernel-layout gradients in the reference's layouts: float64, (in, out) matrices, parameter
-    names of attention.py:105-139."""
+    names of attention.py:105-139.  The re-layout (q / k pair de-interleaving, head padding, transposes) runs on the
+    device in fp32 (exact copies); one page-locked download per tensor, float64 on the host."""
     D = hidden
     heads, dhp = bw.heads, bw.dhp
     hd = heads * dhp
-    g = {k: v.double().cpu().numpy() for k, v in acc.t.items()}
-    qk = _qk_perm(heads, dh, dhp)
-    vv = _v_perm(heads, dh, dhp)
-    Wqkv, Bqkv = g["w_qkv"][:, :D], g["b_qkv"]
-    grads = {}
-    for sec_i, (wn, bn, perm) in enumerate((("attn.wq", "attn.bq", qk), ("attn.wk", "attn.bk", qk),
-                                            ("attn.wv", "attn.bv", vv))):
-        rows = np.arange(hd) + sec_i * hd
-        ok = perm >= 0
-        gw = np.zeros((D, D))
-        gb = np.zeros(D)
-        gw[:, perm[ok]] = Wqkv[rows[ok]].T
-        gb[perm[ok]] = Bqkv[rows[ok]]
-        grads[wn], grads[bn] = gw, gb
-    gwo = np.zeros((D, D))
-    okv = vv >= 0
-    gwo[vv[okv]] = g["w_o"][:D, okv].T
-    grads["attn.wo"], grads["attn.bo"] = gwo, g["b_o"]
+    g = acc.t
+    dev = g["w_qkv"].device
     from .tensor import host_values
     hidden_mlp = host_values(params[f"{prefix}.mlp.w1"]).shape[1]
-    grads["mlp.w1"] = g["w_1"][:hidden_mlp, :D].T.copy()
-    grads["mlp.b1"] = g["b_1"][:hidden_mlp]
-    grads["mlp.w2"] = g["w_2"][:D, :hidden_mlp].T.copy()
-    grads["mlp.b2"] = g["b_2"]
-    grads["ln1.gain"], grads["ln1.bias"] = g["ln1_g"], g["ln1_b"]
-    grads["ln2.gain"], grads["ln2.bias"] = g["ln2_g"], g["ln2_b"]
+    qk = _qk_perm(heads, dh, dhp)
+    vv = _v_perm(heads, dh, dhp)
+    out: dict = {}
+    for sec_i, (wn, bn, perm) in enumerate((("attn.wq", "attn.bq", qk), ("attn.wk", "attn.bk", qk),
+                                            ("attn.wv", "attn.bv", vv))):
+        ok = np.nonzero(perm >= 0)[0]
+        src = torch.from_numpy(ok + sec_i * hd).to(dev)
+        dst = torch.from_numpy(perm[ok]).to(dev)
+        gw = torch.zeros((D, D), dtype=torch.float32, device=dev)
+        gb = torch.zeros(D, dtype=torch.float32, device=dev)
+        gw[:, dst] = g["w_qkv"][src, :D].t()
+        gb[dst] = g["b_qkv"][src]
+        out[wn], out[bn] = gw, gb
+    okv = np.nonzero(vv >= 0)[0]
+    gwo = torch.zeros((D, D), dtype=torch.float32, device=dev)
+    gwo[torch.from_numpy(vv[okv]).to(dev)] = g["w_o"][:D, torch.from_numpy(okv).to(dev)].t()
+    out["attn.wo"], out["attn.bo"] = gwo, g["b_o"][:D]
+    out["mlp.w1"] = g["w_1"][:hidden_mlp, :D].t()
+    out["mlp.b1"] = g["b_1"][:hidden_mlp]
+    out["mlp.w2"] = g["w_2"][:D, :hidden_mlp].t()
+    out["mlp.b2"] = g["b_2"][:D]
+    out["ln1.gain"], out["ln1.bias"] = g["ln1_g"][:D], g["ln1_b"][:D]
+    out["ln2.gain"], out["ln2.bias"] = g["ln2_g"][:D], g["ln2_b"][:D]
     names = dict(zip([n[len(prefix) + 1:] for n in block_param_names(prefix)], block_param_names(prefix)))
-    return {names[k]: np.ascontiguousarray(v) for k, v in grads.items()}
+    res = {}
+    for k, v in out.items():
+        h = torch.empty(tuple(v.shape), dtype=torch.float32, pin_memory=True)
+        h.copy_(v.contiguous())
+        res[names[k]] = h.numpy().astype(np.float64)
+    return res
 
 
 def block_vjp(x, params: dict, prefix: str, extents, window, heads: int, gy):
@@ -514,7 +521,8 @@ class HostOffloadStore:
                 "transfers": self.transfers, "lookahead": self.lookahead}
 
 
-def rollout_vjp(z0, plan, params: dict, cfg, g_out, offload: bool = False, lookahead: int = 2):
+def rollout_vjp(z0, plan, params: dict, cfg, g_out, offload: bool = False, lookahead: int = 2,
+                reference_grads: bool = True):
     """Reverse mode of the greedy latent rollout (rollout.py:56-81) on the device.
 
     z0: the initial latent tokens (T, hidden); plan: processor horizons in order (e.g. (6, 6, 1)); g_out: the
@@ -524,6 +532,8 @@ def rollout_vjp(z0, plan, params: dict, cfg, g_out, offload: bool = False, looka
     per block (autodiff.py:893-924) the forward keeps only each block's input and the backward recomputes the
     block from it (block_vjp_device); with offload=True those inputs live in page-locked host memory and return
     `lookahead` blocks ahead of need (HostOffloadStore), bitwise the same gradients as offload=False.
+    reference_grads=False returns the device accumulators ({block prefix: BlockGrads}, kernel layouts) and dL/dz0
+    as a device tensor instead, for a training loop that stays on the device.
     """
     from .attention import to_device_f32
     from .blocks import block_forward
@@ -553,6 +563,8 @@ def rollout_vjp(z0, plan, params: dict, cfg, g_out, offload: bool = False, looka
         xk = store.take(k)
         g = block_vjp_device(xk, bw, ext, win, heads, dh, g, accs.setdefault(pre, BlockGrads()))
         store.release(k)
+    if not reference_grads:
+        return z, g, accs, store.stats()
     grads: dict = {}
     for pre, acc in accs.items():
         grads.update(block_grads_to_reference(acc, CACHE.block(params, pre, heads), params, pre, dh, cfg.hidden))
