@@ -67,6 +67,7 @@ struct NaParams {
   float* lse;  // optional [token][head]: log2-domain log-sum-exp of the row (m + log2 l), for the backward
   const uint8_t* bias_table;  // BIAS: [tile][maxch] B_x images (4 KB each), built once per geometry
   int maxch;
+  int heavy_lo, heavy_hi;  // first / last column tile crosses the longitude seam (2 chunk parts: twice the work)
 };
 
 #ifndef WM3_NA_SPLIT
@@ -130,6 +131,7 @@ DEVI void exp2_fma2(float& p0, float& p1, float x0, float x1) {
 }
 
 struct TileGeo {
+  int tile, hb;  // raw tile index (d-, h-, w-major) and head x member index of the work item
   int head, b, d0, d1, h0, h1, w0, w1;
   int kd_lo, kr_lo, kr_hi, pc0, ncp, nrpc, nrchunks, nparts, nchunks;
 };
@@ -139,13 +141,40 @@ struct TileGeo {
 // may cross the longitude seam.  A crossing arc is fetched as two TMA boxes of the same shape: part 0 at
 // origin pc0 and part 1 at origin pc0 -/+ W; out-of-range columns of each box are zero-filled by TMA and
 // masked, so together the two parts hold every key of the arc exactly once.
-DEVI TileGeo tile_geo(const NaParams& p, int item) {
-  TileGeo g;
+// Work item -> (head x member, tile).  The seam-crossing column tiles (heavy_lo / heavy_hi: two chunk parts, twice
+// the work) come first, for every head and member, then the rest head-major: with the persistent CTAs taking items
+// round-robin every CTA gets at most one heavy item, instead of some CTAs collecting them (measured: 8 % of the
+// launch lost to the most loaded CTA with a plain head-major order at full scale).
+DEVI void item_tile(const NaParams& p, int item, int& hb, int& tile) {
   const int ntiles = p.ntd * p.nth * p.ntw;
-  const int hb = item / ntiles;  // head-major, member-minor: concurrent CTAs share a head's K/V in L2
+  const int nhv = p.heavy_lo + p.heavy_hi;
+  const int nh = nhv * p.ntd * p.nth;  // heavy tiles per head x member
+  const int nhb = p.nitems / ntiles;
+  if (nh == 0) {
+    hb = item / ntiles;
+    tile = item - hb * ntiles;
+    return;
+  }
+  if (item < nh * nhb) {
+    hb = item / nh;
+    const int k = item - hb * nh;
+    const int dh = k / nhv, v = k - dh * nhv;
+    tile = dh * p.ntw + ((p.heavy_lo && v == 0) ? 0 : p.ntw - 1);
+  } else {
+    const int j = item - nh * nhb, nl = ntiles - nh, nlw = p.ntw - nhv;
+    hb = j / nl;
+    const int k = j - hb * nl;
+    const int dh = k / nlw;
+    tile = dh * p.ntw + p.heavy_lo + (k - dh * nlw);
+  }
+}
+
+DEVI TileGeo tile_geo_raw(const NaParams& p, int hb, int tile) {
+  TileGeo g;
+  g.tile = tile;
+  g.hb = hb;
   g.head = hb / p.batch;
   g.b = hb - g.head * p.batch;
-  const int tile = item - hb * ntiles;
   const int tw_i = tile % p.ntw;
   const int th_i = (tile / p.ntw) % p.nth;
   const int td_i = tile / (p.ntw * p.nth);
@@ -171,6 +200,12 @@ DEVI TileGeo tile_geo(const NaParams& p, int item) {
   g.nrchunks = (nrows_u + g.nrpc - 1) / g.nrpc;
   g.nchunks = (kd_hi - g.kd_lo) * g.nrchunks * g.nparts;
   return g;
+}
+
+DEVI TileGeo tile_geo(const NaParams& p, int item) {
+  int hb, tile;
+  item_tile(p, item, hb, tile);
+  return tile_geo_raw(p, hb, tile);
 }
 
 // chunk j -> depth plane, first key row, column origin and the patch columns [vlo, vhi) it holds
@@ -271,7 +306,7 @@ DEVI void bx_row(const NaParams& p, const TileGeo& g, int j, int k, uint32_t (&u
 // no-swizzle core-matrix layout the MMA descriptor reads (copied into shared memory with one bulk copy).
 __global__ void natten_bias_table_kernel(NaParams p, uint8_t* table) {
   const int tile = blockIdx.x / p.maxch, j = blockIdx.x % p.maxch;
-  const TileGeo g = tile_geo(p, tile);  // item = tile: head 0, member 0 (the geometry is head-independent)
+  const TileGeo g = tile_geo_raw(p, 0, tile);  // the geometry is head-independent
   if (j >= g.nchunks) return;
   uint32_t u[8];
   bx_row(p, g, j, threadIdx.x, u);
@@ -376,8 +411,7 @@ __global__ void __launch_bounds__(NA_THREADS, NA_CTAS_PER_SM)
         for (int h = 0; h < halves; ++h)
           tma_load_4d(dst + h * 16384u, &tmKV, full, col + 64 * h, c1, c2, g.b * p.depth + kd);
         if (with_bx) {
-          const int tile = item % (p.ntd * p.nth * p.ntw);
-          bulk_load(sXB, p.bias_table + (static_cast<size_t>(tile) * p.maxch + j) * 4096, 4096u, full);
+          bulk_load(sXB, p.bias_table + (static_cast<size_t>(g.tile) * p.maxch + j) * 4096, 4096u, full);
         }
       };
       for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++tile_ctr) {
@@ -816,7 +850,7 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
             tma_load_4d(sK(s) + h * 16384u, &tmKV, bar_kfull(s), sec + g.head * DHP + 64 * h, origin, kr0 - brow0,
                         g.b * p.depth + kd);
           if (BIAS)
-            bulk_load(sXB(s), p.bias_table + (static_cast<size_t>(item % ntiles) * p.maxch + j) * 4096, 4096u,
+            bulk_load(sXB(s), p.bias_table + (static_cast<size_t>(g.tile) * p.maxch + j) * 4096, 4096u,
                       bar_kfull(s));
           mbar_wait(bar_vempty, (c & 1) ^ 1);
           mbar_arrive_expect_tx(bar_vfull, kbytes);
@@ -1022,7 +1056,8 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
         for (int h = 0; h < 2; ++h, ++hc) {
           mbar_wait(bar_partfull, hc & 1);
           tc_fence_after();
-          float* base = bw.partial + (((static_cast<size_t>(item) * p.maxch + j) * 2 + h) * 2) * 64 * DHP + d;
+          const size_t raw = static_cast<size_t>(g.hb) * (p.ntd * p.nth * p.ntw) + g.tile;  // reduce-kernel index
+          float* base = bw.partial + (((raw * p.maxch + j) * 2 + h) * 2) * 64 * DHP + d;
 #pragma unroll
           for (int kv = 0; kv < 2; ++kv) {
 #pragma unroll
@@ -1052,7 +1087,7 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
 // Key token held by every slot of every (tile, chunk): -1 for padding / zero-filled / out-of-grid slots.
 __global__ void natten_slot_table_kernel(NaParams p, int32_t* table) {
   const int tile = blockIdx.x / p.maxch, j = blockIdx.x % p.maxch;
-  const TileGeo g = tile_geo(p, tile);
+  const TileGeo g = tile_geo_raw(p, 0, tile);
   const int k = threadIdx.x;
   int32_t tok = -1;
   if (j < g.nchunks) {
@@ -1188,6 +1223,13 @@ static int natten_setup(const void* qkv, int ldqkv, void* out, int ldo, int batc
   p.nth = (p.q_hi - 1) / p.TH - p.th_first + 1;
   p.ntw = (cols + p.TW - 1) / p.TW;
   p.nitems = p.ntd * p.nth * p.ntw * heads * batch;
+  {  // seam-crossing first / last column tiles (item_tile schedules them first)
+    const int hw = (ww - 1) / 2;
+    const bool circle = p.ncp == cols;
+    const int w0 = (p.ntw - 1) * p.TW, w1 = (w0 + p.TW < cols) ? w0 + p.TW : cols;
+    p.heavy_lo = (!circle && hw > 0) ? 1 : 0;
+    p.heavy_hi = (!circle && p.ntw > 1 && (w0 - hw < 0 || w1 - 1 + (ww - 1 - hw) >= cols)) ? 1 : 0;
+  }
   p.scale_log2 = scale * 1.4426950408889634f;
 
   const uint64_t wp = cols;
