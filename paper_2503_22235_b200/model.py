@@ -62,7 +62,11 @@ class DecodedFields:
 
     def to_host(self, out=None):
         """(surface, atmos) as float32 host tensors in page-locked memory (one DMA each, no float64 widening).
-        Pass `out` = a previous result to reuse its pinned buffers (steady-state: no host allocation)."""
+        Pass `out` = a previous result to reuse its pinned buffers (steady-state: no host allocation).  Fields
+        decoded with decode(..., host_out=out) are already streamed there: this only waits for the copies."""
+        if out is not None and getattr(self, "_host", None) is out:
+            torch.cuda.current_stream().synchronize()
+            return out
         if out is None:
             out = tuple(torch.empty(t.device.shape, dtype=torch.float32, pin_memory=True)
                         for t in (self.surface, self.atmos))
@@ -250,18 +254,59 @@ def process(lat: LatentState, params: dict, cfg: ModelConfig, horizon: int) -> L
     return LatentState(Tensor(device=x), lat.valid_time + horizon, lat.extents)
 
 
-def decode(lat: LatentState, params: dict, cfg: ModelConfig) -> DecodedFields:
-    """Project the latent token grid back to gridded fields (model.py:408-421)."""
+_copy_streams: dict = {}
+
+
+def _copy_stream() -> torch.cuda.Stream:
+    dev = torch.cuda.current_device()
+    if dev not in _copy_streams:
+        _copy_streams[dev] = torch.cuda.Stream()
+    return _copy_streams[dev]
+
+
+def decode(lat: LatentState, params: dict, cfg: ModelConfig, host_out=None) -> DecodedFields:
+    """Project the latent token grid back to gridded fields (model.py:408-421).
+
+    host_out = (surface, atmos) page-locked float32 host tensors of the fields' shapes (e.g. a previous
+    DecodedFields.to_host() result): the full-resolution decoder stage then runs plane by plane and each plane's
+    fields are copied out on a side stream while the next plane is convolved (the device->host transfer hides
+    behind the decoder); the returned fields' to_host(host_out) only waits."""
     cfg = as_config(cfg)
     x = latent_tokens(lat, cfg).clone()
     CALL_COUNTS["decode"] += 1
     dm = device_model(params, cfg)
-    dm.run_blocks(x, [f"dec.blk{i}" for i in range(cfg.dec_blocks)])
     g = cfg.grid
-    surface = torch.empty((cfg.surface_out, g.rows, g.cols), dtype=torch.float32, device="cuda")
-    atmos = torch.empty((cfg.atmos_vars, cfg.levels, g.rows, g.cols), dtype=torch.float32, device="cuda")
-    decode_planes(dm.decoder(), dm.buffers(), cfg, x, surface, atmos)
-    return DecodedFields(lat.valid_time, Tensor(device=surface), Tensor(device=atmos))
+    sshape, ashape = (cfg.surface_out, g.rows, g.cols), (cfg.atmos_vars, cfg.levels, g.rows, g.cols)
+    if host_out is not None:
+        hs, ha = host_out
+        if tuple(hs.shape) != sshape or tuple(ha.shape) != ashape or hs.dtype != torch.float32 or \
+                ha.dtype != torch.float32 or hs.device.type != "cpu" or ha.device.type != "cpu":
+            raise ConfigError(f"host_out must be float32 host tensors of shapes {sshape} and {ashape}")
+    dm.run_blocks(x, [f"dec.blk{i}" for i in range(cfg.dec_blocks)])
+    surface = torch.empty(sshape, dtype=torch.float32, device="cuda")
+    atmos = torch.empty(ashape, dtype=torch.float32, device="cuda")
+    if host_out is None:
+        decode_planes(dm.decoder(), dm.buffers(), cfg, x, surface, atmos)
+        return DecodedFields(lat.valid_time, Tensor(device=surface), Tensor(device=atmos))
+    main, side = torch.cuda.current_stream(), _copy_stream()
+    pl = cfg.level_patch
+
+    def on_plane(q: int) -> None:
+        ev = torch.cuda.Event()
+        ev.record(main)
+        side.wait_event(ev)
+        with torch.cuda.stream(side):
+            if q == 0:
+                hs.copy_(surface, non_blocking=True)
+            else:  # level group q - 1: one contiguous run of levels per variable
+                for a in range(cfg.atmos_vars):
+                    ha[a, (q - 1) * pl:q * pl].copy_(atmos[a, (q - 1) * pl:q * pl], non_blocking=True)
+
+    decode_planes(dm.decoder(), dm.buffers(), cfg, x, surface, atmos, on_plane=on_plane)
+    main.wait_stream(side)  # the device buffers stay alive and the caller's synchronisation covers the copies
+    out = DecodedFields(lat.valid_time, Tensor(device=surface), Tensor(device=atmos))
+    out._host = host_out
+    return out
 
 
 def blend_latents(latents: list, weights) -> LatentState:

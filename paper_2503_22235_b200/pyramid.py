@@ -266,11 +266,15 @@ def encode_planes(ew: EncoderWeights, bufs: PyramidBuffers, cfg: ModelConfig, to
 
 
 def decode_planes(dw: DecoderWeights, bufs: PyramidBuffers, cfg: ModelConfig, tokens: torch.Tensor,
-                  surface_out: torch.Tensor, atmos_out: torch.Tensor, planes: tuple[int, int] | None = None) -> None:
+                  surface_out: torch.Tensor, atmos_out: torch.Tensor, planes: tuple[int, int] | None = None,
+                  on_plane=None) -> None:
     """latent tokens (fp32) -> surface (surface_out, H, W) and atmos (A, L, H, W) fp32 fields.
 
     planes = (lo, hi): only depth planes [lo, hi) (surface if lo == 0, atmosphere levels of groups lo-1..hi-2)
-    are decoded; the up-pyramid treats planes independently, so the split is exact."""
+    are decoded; the up-pyramid treats planes independently, so the split is exact.
+    on_plane(q): with it, the full-resolution stage and the heads run plane by plane and on_plane(q) is called
+    (on the host, after queueing) once plane q's fields are written, so a caller can stream them out while the
+    next plane is convolved; the per-plane launches write the same bytes as the batched ones."""
     g = cfg.grid
     d, h, w = cfg.latent_extents
     lo, hi = (0, d) if planes is None else (int(planes[0]), int(planes[1]))
@@ -281,25 +285,39 @@ def decode_planes(dw: DecoderWeights, bufs: PyramidBuffers, cfg: ModelConfig, to
     x = bufs.buf(lvl, 0, cfg.hidden)[lo:hi]
     tokens_to_nhwc(tokens[lo * h * w:hi * h * w], n, h, w, x)
     chans = [cfg.hidden] + list(cfg.stage_channels[-2::-1]) + [cfg.stem_channels]
+    hh, ww = g.rows, g.cols
+    p = cfg.level_patch
+
+    def heads(a: int, b: int, full) -> None:  # fields of planes [a, b)
+        if a == 0:
+            run_conv(dw.head_sfc, full[0:1], 1, hh, ww, surface_out, kind=_lib.WM3_CONV_OUT_FIELD, img_stride=0,
+                     a_stride=hh * ww, p_stride=0, chan_div=1)
+        a0 = max(a, 1)
+        if b > a0:  # level groups a0 - 1 .. b - 2 -> levels [(a0 - 1) p, (b - 1) p)
+            dst = atmos_out.view(-1)[(a0 - 1) * p * hh * ww:]
+            run_conv(dw.head_atm, full[a0:b], b - a0, hh, ww, dst, kind=_lib.WM3_CONV_OUT_FIELD,
+                     img_stride=p * hh * ww, a_stride=cfg.levels * hh * ww, p_stride=hh * ww, chan_div=p)
+
     x_idx = 0
-    for i, st in enumerate(dw.stages):
-        src = bufs.buf(lvl - i, x_idx, chans[i])[lo:hi]
+    stages = list(enumerate(dw.stages))
+    last_i = len(stages) - 1
+    for i, st in stages:
         lvl_out = lvl - i - 1
         ho, wo = g.rows >> lvl_out, g.cols >> lvl_out
+        if i == last_i and on_plane is not None:
+            for q in range(lo, hi):
+                src = bufs.buf(lvl - i, x_idx, chans[i])[q:q + 1]
+                y = bufs.buf(lvl_out, 0, chans[i + 1])[q:q + 1]
+                run_conv(st.resample, src, 1, ho // 2, wo // 2, y)
+                q_idx = _res_block(st, bufs, lvl_out, 0, 1, ho, wo, chans[i + 1], q)
+                heads(q, q + 1, bufs.buf(0, q_idx, cfg.stem_channels))
+                on_plane(q)
+            return
+        src = bufs.buf(lvl - i, x_idx, chans[i])[lo:hi]
         y = bufs.buf(lvl_out, 0, chans[i + 1])[lo:hi]
         run_conv(st.resample, src, n, ho // 2, wo // 2, y)
         x_idx = _res_block(st, bufs, lvl_out, 0, n, ho, wo, chans[i + 1], lo)
-    full = bufs.buf(0, x_idx, cfg.stem_channels)
-    hh, ww = g.rows, g.cols
-    if lo == 0:
-        run_conv(dw.head_sfc, full[0:1], 1, hh, ww, surface_out, kind=_lib.WM3_CONV_OUT_FIELD, img_stride=0,
-                 a_stride=hh * ww, p_stride=0, chan_div=1)
-    p = cfg.level_patch
-    a0 = max(lo, 1)
-    if hi > a0:  # level groups a0 - 1 .. hi - 2 -> levels [(a0 - 1) p, (hi - 1) p)
-        dst = atmos_out.view(-1)[(a0 - 1) * p * hh * ww:]
-        run_conv(dw.head_atm, full[a0:hi], hi - a0, hh, ww, dst, kind=_lib.WM3_CONV_OUT_FIELD,
-                 img_stride=p * hh * ww, a_stride=cfg.levels * hh * ww, p_stride=hh * ww, chan_div=p)
+    heads(lo, hi, bufs.buf(0, x_idx, cfg.stem_channels))
 
 
 def check_grid(cfg: ModelConfig) -> None:

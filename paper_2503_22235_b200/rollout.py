@@ -120,13 +120,14 @@ def rollout(lat: LatentState, plan, params: dict, cfg: ModelConfig, engine=None,
 
 
 def forecast(state: WeatherState, dt: int, params: dict, cfg: ModelConfig, source: str = PRIMARY_SOURCE,
-             engine=None) -> DecodedFields:
-    """encode -> greedy latent rollout -> decode (rollout.py:84-91)."""
+             engine=None, host_out=None) -> DecodedFields:
+    """encode -> greedy latent rollout -> decode (rollout.py:84-91).  host_out: see model.decode (the fields
+    stream to page-locked host tensors while the decoder runs)."""
     cfg = as_config(cfg)
     plan = greedy_plan(dt, cfg.max_dt)
     lat = encode(state, params, cfg, source=source)
     lat = rollout(lat, plan, params, cfg, engine=engine)
-    return decode(lat, params, cfg)
+    return decode(lat, params, cfg, host_out=host_out)
 
 
 def rollout_ensemble(latents, plan, params: dict, cfg: ModelConfig, graphs: bool = True) -> list:

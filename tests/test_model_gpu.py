@@ -225,3 +225,24 @@ def test_input_range_guard(scale):
     print(f"inputs x{scale:g}: worst per-variable rel L2 {rel[worst]:.2e} ({worst})")
     assert np.isfinite(out.surface.values).all() and np.isfinite(out.atmos.values).all()
     assert rel[worst] < 1e-2, (worst, rel[worst])
+
+
+def test_decode_streamed_to_host_equals_batched():
+    """decode(..., host_out=bufs): the full-resolution stage runs plane by plane with each plane's fields copied out
+    on a side stream; the host fields are bitwise the batched decode's, and to_host(bufs) returns them as is."""
+    import torch
+    import paper_2503_22235_b200.model as M
+    from paper_2503_22235_b200.tensor import Tensor
+    for cfg in (M.desk_config(), M.mid_config()):
+        params = M.init_model_params(cfg, seed=4, zero_residual=False)
+        rng = np.random.default_rng(9)
+        lat = M.LatentState(Tensor(rng.standard_normal((cfg.tokens, cfg.hidden))), 6, cfg.latent_extents)
+        ref = M.decode(lat, params, cfg)
+        s_ref, a_ref = ref.to_host()
+        bufs = (torch.full_like(s_ref, float("nan")), torch.full_like(a_ref, float("nan")))
+        bufs = tuple(b.pin_memory() for b in bufs)
+        out = M.decode(lat, params, cfg, host_out=bufs)
+        s, a = out.to_host(bufs)
+        assert s is bufs[0] and a is bufs[1]
+        assert torch.equal(s, s_ref) and torch.equal(a, a_ref)
+        assert torch.equal(out.surface.device.cpu(), s_ref)
