@@ -461,7 +461,7 @@ def run_forecast(args, world: int = 1) -> dict:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        outs = R.forecast_ensemble(states, dt, params, cfg)
+        outs = R.forecast_ensemble(states, dt, params, cfg, host_outs=bufs)  # fields stream out per member
         hosts = [o.to_host(b) for o, b in zip(outs, bufs)]
         torch.cuda.synchronize()
         ens_s = sync_max(time.perf_counter() - t0)

@@ -164,13 +164,17 @@ def rollout_ensemble(latents, plan, params: dict, cfg: ModelConfig, graphs: bool
             for m, lt in enumerate(latents)]
 
 
-def forecast_ensemble(states, dt: int, params: dict, cfg: ModelConfig, source: str = PRIMARY_SOURCE) -> list:
-    """forecast() of every member: per-member encode, one batched greedy rollout, per-member decode."""
+def forecast_ensemble(states, dt: int, params: dict, cfg: ModelConfig, source: str = PRIMARY_SOURCE,
+                      host_outs=None) -> list:
+    """forecast() of every member: per-member encode, one batched greedy rollout, per-member decode.
+    host_outs: per-member (surface, atmos) page-locked host buffers the decoded fields stream to (model.decode)."""
     cfg = as_config(cfg)
     plan = greedy_plan(dt, cfg.max_dt)
     lats = [encode(s, params, cfg, source=source) for s in states]
     lats = rollout_ensemble(lats, plan, params, cfg)
-    return [decode(lt, params, cfg) for lt in lats]
+    if host_outs is None:
+        host_outs = [None] * len(lats)
+    return [decode(lt, params, cfg, host_out=h) for lt, h in zip(lats, host_outs)]
 
 
 def perturbed_members(state: WeatherState, members: int, scale: float = 0.01, seed: int = 100) -> list:
