@@ -52,6 +52,9 @@ constexpr int EPI_WARP0 = 4;
 #ifndef WM3_RESID_TMA
 #define WM3_RESID_TMA 1
 #endif
+#ifndef WM3_RSLOTS
+#define WM3_RSLOTS 2  // residual slots (even); each pair of slots costs one mainloop stage
+#endif
 template <int BN, int CG = 1, int EPI = 0>
 struct GemmCfg {
   // Residual epilogue: the fp32 residual chunks stream into RSLOTS smem slots by TMA (warp 3), ahead of the
@@ -61,9 +64,11 @@ struct GemmCfg {
   // Two slots: with an even slot count and even units per tile, slot c % RSLOTS has the parity of the unit, so
   // each slot is consumed by one epilogue group only, in order (an odd count interleaves the groups on a slot
   // and a fast group can then pass a parity wait one phase early).
-  static constexpr int RSLOTS = RESID_TMA ? 2 : 0;
+  static constexpr int RSLOTS = RESID_TMA ? WM3_RSLOTS : 0;
   // CTA pairs free 16 KB per stage: 6 stages, or 5 stages with double-buffered epilogue staging
-  static constexpr int STAGES = (CG == 2) ? ((WM3_PAIR_STAGING == 2 || RESID_TMA) ? 5 : 6) : (RESID_TMA ? 3 : 4);
+  static constexpr int STAGES = (CG == 2) ? ((WM3_PAIR_STAGING == 2 || RESID_TMA) ? (RESID_TMA ? 6 - WM3_RSLOTS / 2 : 5)
+                                                                                  : 6)
+                                          : (RESID_TMA ? 3 : 4);
   static constexpr int STAGING_PER_GROUP = (BN == 256) ? ((CG == 2) ? WM3_PAIR_STAGING : 1) : 2;
   static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
   static constexpr uint32_t B_BYTES = (BN / CG) * GEMM_BK * 2;  // this CTA's share of the B tile
