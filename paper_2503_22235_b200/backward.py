@@ -481,36 +481,56 @@ class HostOffloadStore:
     def begin_backward(self, order) -> None:
         self.order = list(order)
         self.next_fetch = 0
-        self.slot_rr = 0
+        self.occupied: set = set()  # ring slots holding a fetched input not yet released
         for _ in range(min(self.lookahead, len(self.order))):
             self._prefetch()
 
-    def _prefetch(self) -> None:
-        if self.next_fetch >= len(self.order):
-            return
-        k = self.order[self.next_fetch]
-        self.next_fetch += 1
-        i = self.slot_rr
-        self.slot_rr = (self.slot_rr + 1) % len(self.ring)
+    def _slot(self, grow: bool):
+        """A ring slot no fetched-but-unreleased input holds; with grow, a new slot when all are taken (an
+        out-of-order request beyond the lookahead), else None."""
+        for i in range(len(self.ring)):
+            if i not in self.occupied:
+                return i
+        if not grow:
+            return None
+        self.ring.append(torch.empty(self.shape, dtype=torch.float32, device="cuda"))
+        self.slot_free.append(None)
+        self.high_water = max(self.high_water, len(self.ring) * self.ring[0].numel() * 4)
+        return len(self.ring) - 1
+
+    def _fetch(self, k: int, i: int) -> None:
         with torch.cuda.stream(self.side):
             self._wait_slot(self.side, i)
             self.ring[i].copy_(self.host[k], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(self.side)
         self.ready[k] = (i, ev)
+        self.occupied.add(i)
         self.transfers += 1
 
+    def _prefetch(self) -> None:
+        while self.next_fetch < len(self.order) and self.order[self.next_fetch] in self.ready:
+            self.next_fetch += 1
+        if self.next_fetch >= len(self.order):
+            return
+        i = self._slot(grow=False)
+        if i is None:
+            return
+        k = self.order[self.next_fetch]
+        self.next_fetch += 1
+        self._fetch(k, i)
+
     def take(self, k: int) -> torch.Tensor:
-        if k not in self.ready:  # not prefetched in time (out-of-order request): fetch on demand
+        if k not in self.ready:  # not prefetched (out-of-order request): fetch on demand
             self.demand_stalls += 1
-            while k not in self.ready:
-                self._prefetch()
+            self._fetch(k, self._slot(grow=True))
         i, ev = self.ready[k]
         torch.cuda.current_stream().wait_event(ev)
         return self.ring[i]
 
     def release(self, k: int) -> None:
         i, _ = self.ready.pop(k)
+        self.occupied.discard(i)
         done = torch.cuda.Event()
         done.record(torch.cuda.current_stream())
         self.slot_free[i] = done

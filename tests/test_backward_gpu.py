@@ -258,3 +258,24 @@ def test_tensor_core_attention_backward_matches_cuda_core(ext, win, dim, heads, 
     print(f"tc vs cuda-core attention backward {ext} D={dim}: x {errs['x']:.2e}, worst {worst} {errs[worst]:.2e}")
     assert errs[worst] < 5e-3, (worst, errs[worst])
     assert np.array_equal(gx_tc, gx_tc2) and all(np.array_equal(pg_tc[n], pg_tc2[n]) for n in pg_tc)
+
+
+def test_host_offload_store_out_of_order_take():
+    """HostOffloadStore: a take() the prefetch order did not anticipate is served on demand (counted as a stall)
+    with the exact bytes; the ring slots are reused only after their last use (every saved latent comes back
+    intact even with lookahead 1)."""
+    import torch
+    from paper_2503_22235_b200.backward import HostOffloadStore
+    shape = (1000, 64)
+    xs = [torch.randn(shape, device="cuda") for _ in range(6)]
+    st = HostOffloadStore(shape, lookahead=1)
+    for k, x in enumerate(xs):
+        st.put(k, x)
+    st.begin_backward([5, 4, 3, 2, 1, 0])
+    got = {}
+    for k in (5, 3, 4, 0, 2, 1):  # 3 and 0 out of order
+        got[k] = st.take(k).clone()
+        st.release(k)
+    torch.cuda.synchronize()
+    assert all(torch.equal(got[k], xs[k]) for k in range(6))
+    assert st.stats()["demand_stalls"] >= 1
