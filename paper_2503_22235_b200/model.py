@@ -193,7 +193,8 @@ def check_token_buffer(x: torch.Tensor, cfg: ModelConfig, batch: int = 1) -> Non
 # ------------------------------------------------------------------------------------------------
 # API
 # ------------------------------------------------------------------------------------------------
-def stage_inputs(state: WeatherState, params: dict, cfg: ModelConfig, source: str = PRIMARY_SOURCE):
+def stage_inputs(state: WeatherState, params: dict, cfg: ModelConfig, source: str = PRIMARY_SOURCE,
+                 upload: bool = True):
     """encode()'s validation (ConfigError before any launch) and the host->device copy of the state into the
     pyramid input buffers; returns (device model, encoder weight prefix)."""
     cfg = as_config(cfg)
@@ -212,18 +213,52 @@ def stage_inputs(state: WeatherState, params: dict, cfg: ModelConfig, source: st
     if not bufs.statics_ready:
         bufs.sfc_in[cfg.surface_in:] = torch.from_numpy(static_fields(g).astype(np.float32)).to("cuda")
         bufs.statics_ready = True
+    if not upload:
+        return dm, prefix  # encode() streams the planes in (_stream_inputs)
     bufs.sfc_in[:cfg.surface_in].copy_(_to_device(state.surface, None), non_blocking=True)
     bufs.atm_in.copy_(_to_device(state.atmos, None), non_blocking=True)
     return dm, prefix
 
 
+def _pinned_f32(a) -> bool:
+    return isinstance(a, torch.Tensor) and a.device.type == "cpu" and a.dtype == torch.float32 and a.is_pinned() \
+        and a.is_contiguous()
+
+
+def _stream_inputs(state: WeatherState, bufs, cfg: ModelConfig) -> list:
+    """Page-locked host fields -> the pyramid input buffers on the copy stream, one event per depth plane (surface,
+    then each atmosphere level group: one contiguous run of levels per variable)."""
+    main, side = torch.cuda.current_stream(), _copy_stream()
+    side.wait_stream(main)  # the input buffers are free once earlier work on them is done
+    p = cfg.level_patch
+    evs = []
+    with torch.cuda.stream(side):
+        bufs.sfc_in[:cfg.surface_in].copy_(state.surface, non_blocking=True)
+        evs.append(torch.cuda.Event())
+        evs[-1].record(side)
+        for g_ in range(cfg.levels // p):
+            for a in range(cfg.atmos_vars):
+                bufs.atm_in[a, g_ * p:(g_ + 1) * p].copy_(state.atmos[a, g_ * p:(g_ + 1) * p], non_blocking=True)
+            evs.append(torch.cuda.Event())
+            evs[-1].record(side)
+    return evs
+
+
 def encode(state: WeatherState, params: dict, cfg: ModelConfig, source: str = PRIMARY_SOURCE) -> LatentState:
     """Lift one gridded state into the latent token grid (model.py:363-390)."""
     cfg = as_config(cfg)
-    dm, prefix = stage_inputs(state, params, cfg, source)
+    streamed = _pinned_f32(state.surface) and _pinned_f32(state.atmos)
+    dm, prefix = stage_inputs(state, params, cfg, source, upload=not streamed)
     bufs = dm.buffers()
     tokens = torch.empty((cfg.tokens, cfg.hidden), dtype=torch.float32, device="cuda")
-    encode_planes(dm.encoder(prefix), bufs, cfg, tokens)
+    if streamed:
+        # page-locked fields: plane q + 1 uploads on the copy stream while plane q's stem convolution runs
+        evs = _stream_inputs(state, bufs, cfg)
+        main = torch.cuda.current_stream()
+        encode_planes(dm.encoder(prefix), bufs, cfg, tokens, before_plane=lambda q: main.wait_event(evs[q]))
+        evs[-1].synchronize()  # the caller may reuse its host buffers once encode() returns
+    else:
+        encode_planes(dm.encoder(prefix), bufs, cfg, tokens)
     check_input_range(bufs)
     dm.run_blocks(tokens, [f"{prefix}.blk{i}" for i in range(cfg.enc_blocks)])
     return LatentState(Tensor(device=tokens), state.valid_time, cfg.latent_extents)

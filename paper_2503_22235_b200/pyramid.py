@@ -214,12 +214,15 @@ def _res_block(ws: StageW, bufs: PyramidBuffers, level: int, x_idx: int, imgs: i
 
 
 def encode_planes(ew: EncoderWeights, bufs: PyramidBuffers, cfg: ModelConfig, tokens_out: torch.Tensor,
-                  planes: tuple[int, int] | None = None) -> None:
+                  planes: tuple[int, int] | None = None, before_plane=None) -> None:
     """bufs.sfc_in / atm_in (device fp32) -> latent tokens (D*h*w, hidden) fp32.
 
     planes = (lo, hi) encodes only depth planes [lo, hi) (plane 0 = surface, p >= 1 = atmosphere level group
     p - 1) into their token rows: the planes share the pyramid weights and never interact before the encoder
-    blocks, so the split is exact (bands.forecast_banded runs one range per rank)."""
+    blocks, so the split is exact (bands.forecast_banded runs one range per rank).
+    before_plane(q): with it, the input layout copy and the stem convolution run plane by plane, each after
+    before_plane(q) (model.encode: make the stream wait for that plane's host upload), so the upload of plane
+    q + 1 overlaps the stem of plane q; the per-plane launches write the same bytes as the batched ones."""
     g = cfg.grid
     hh, ww = g.rows, g.cols
     d = cfg.depth_planes
@@ -232,17 +235,39 @@ def encode_planes(ew: EncoderWeights, bufs: PyramidBuffers, cfg: ModelConfig, to
     hw = hh * ww
     x0 = bufs.buf(0, 0, cfg.stem_channels)
     bufs.overflow.zero_()
-    if lo == 0:
-        fields_to_nhwc(bufs.sfc_in, 1, csfc, hh, ww, bufs.in_sfc, 0, hw, 0, 1, bufs.overflow)
-        run_conv(ew.stem_sfc, bufs.in_sfc, 1, hh, ww, x0[0:1])
-    a0 = max(lo, 1)
-    if hi > a0:  # atmosphere level groups a0 - 1 .. hi - 2
-        fields_to_nhwc(bufs.atm_in.view(-1)[(a0 - 1) * cfg.level_patch * hw:], hi - a0, catm, hh, ww,
-                       bufs.in_atm[a0 - 1:hi - 1], cfg.level_patch * hw, cfg.levels * hw, hw, cfg.level_patch,
-                       bufs.overflow)
-        run_conv(ew.stem_atm, bufs.in_atm[a0 - 1:hi - 1], hi - a0, hh, ww, x0[a0:hi])
+    def stems(a: int, b: int) -> None:  # input layout + stem conv of planes [a, b)
+        if a == 0:
+            fields_to_nhwc(bufs.sfc_in, 1, csfc, hh, ww, bufs.in_sfc, 0, hw, 0, 1, bufs.overflow)
+            run_conv(ew.stem_sfc, bufs.in_sfc, 1, hh, ww, x0[0:1])
+        a0 = max(a, 1)
+        if b > a0:  # atmosphere level groups a0 - 1 .. b - 2
+            fields_to_nhwc(bufs.atm_in.view(-1)[(a0 - 1) * cfg.level_patch * hw:], b - a0, catm, hh, ww,
+                           bufs.in_atm[a0 - 1:b - 1], cfg.level_patch * hw, cfg.levels * hw, hw, cfg.level_patch,
+                           bufs.overflow)
+            run_conv(ew.stem_atm, bufs.in_atm[a0 - 1:b - 1], b - a0, hh, ww, x0[a0:b])
+
     x_idx, c = 0, cfg.stem_channels
+    first = 0
+    if before_plane is None:
+        stems(lo, hi)
+    elif DOWNSAMPLE_STAGES > 1:
+        # per plane: stem and the first (full -> half resolution) stage, while the next plane uploads
+        st = ew.stages[0]
+        h2, w2 = hh >> 1, ww >> 1
+        c_out = cfg.stage_channels[0]
+        for q in range(lo, hi):
+            before_plane(q)
+            stems(q, q + 1)
+            run_conv(st.resample, bufs.buf(0, 0, c)[q:q + 1], 1, hh, ww, bufs.buf(1, 0, c_out)[q:q + 1])
+            x_idx = _res_block(st, bufs, 1, 0, 1, h2, w2, c_out, q)
+        c, first = c_out, 1
+    else:
+        for q in range(lo, hi):
+            before_plane(q)
+            stems(q, q + 1)
     for i, st in enumerate(ew.stages):
+        if i < first:
+            continue
         h2, w2 = hh >> (i + 1), ww >> (i + 1)
         c_out = cfg.stage_channels[i]
         last = i == DOWNSAMPLE_STAGES - 1
@@ -305,7 +330,8 @@ def decode_planes(dw: DecoderWeights, bufs: PyramidBuffers, cfg: ModelConfig, to
         lvl_out = lvl - i - 1
         ho, wo = g.rows >> lvl_out, g.cols >> lvl_out
         if i == last_i and on_plane is not None:
-            for q in range(lo, hi):
+            # the surface plane (smallest download) last, so the copy left after the decoder is the shortest
+            for q in [q for q in range(lo, hi) if q != 0] + ([0] if lo == 0 else []):
                 src = bufs.buf(lvl - i, x_idx, chans[i])[q:q + 1]
                 y = bufs.buf(lvl_out, 0, chans[i + 1])[q:q + 1]
                 run_conv(st.resample, src, 1, ho // 2, wo // 2, y)

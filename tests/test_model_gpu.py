@@ -246,3 +246,20 @@ def test_decode_streamed_to_host_equals_batched():
         assert s is bufs[0] and a is bufs[1]
         assert torch.equal(s, s_ref) and torch.equal(a, a_ref)
         assert torch.equal(out.surface.device.cpu(), s_ref)
+
+
+def test_encode_streamed_from_pinned_equals_numpy():
+    """encode() of page-locked float32 host fields streams the planes in on a copy stream with per-plane stem
+    convolutions; the latent is bitwise the one encoded from the same values as numpy arrays."""
+    import torch
+    import paper_2503_22235_b200.model as M
+    for cfg in (M.desk_config(), M.mid_config()):
+        params = M.init_model_params(cfg, seed=6, zero_residual=False)
+        g = cfg.grid
+        rng = np.random.default_rng(2)
+        s = rng.standard_normal((cfg.surface_in, g.rows, g.cols)).astype(np.float32)
+        a = rng.standard_normal((cfg.atmos_vars, cfg.levels, g.rows, g.cols)).astype(np.float32)
+        ref = M.encode(M.WeatherState(0, s, a), params, cfg).tokens.device.clone()
+        st = M.WeatherState(0, torch.from_numpy(s).pin_memory(), torch.from_numpy(a).pin_memory())
+        got = M.encode(st, params, cfg).tokens.device
+        assert torch.equal(got, ref)
