@@ -270,6 +270,11 @@ int wm3_zonal_power(int dtype, const void* field, long long member_stride, int k
  *                     src fp32 (src_f32 = 1) or 16-bit operand
  *   wm3_bw_colsum     out[c] = sum_r src[r][c] (* src2[r][c]) / scale, fixed order (partial: ceil(rows/256) * cols)
  *   wm3_bw_gelu       out = g / scale * gelu'(a + bias) (exact-erf GELU, autodiff.py:372-382)
+ *   wm3_bw_gelu_fwd   out = operand(GELU(a + bias)) exactly as the W1 GEMM epilogue computes it (the forward's
+ *                     activation, bitwise, from the stored fp32 pre-activation; cols, lda, ldo multiples of 8)
+ *   wm3_bw_colsum_amax  one pass: colsum[c] = sum_r v[r][c] (wm3_bw_colsum's order) and *amax_bits = bits of
+ *                     max |v|, v = g; with a != NULL, v = g / scale(in_scale_bits) * gelu'(a + bias) is also
+ *                     stored to out (the GELU backward, its bias gradient and the next operand scale at once)
  *   wm3_bw_layernorm  gx = LayerNorm-backward(x, gamma, g / scale) (+ add); gxh = g / scale * xhat; gsc = g / scale
  *                     (autodiff.py:400-424: mean, biased variance, eps)
  *   wm3_bw_natten     attention backward over the neighbor table nbr [T][K] (grid.py K order) of the 16-bit qkv
@@ -285,6 +290,10 @@ int wm3_bw_colsum(const float* src, const float* src2, int rows, int cols, int l
                   float* partial, float* out, void* stream);
 int wm3_bw_gelu(const float* g, int ldg, const float* a, int lda, const float* bias, int rows, int cols,
                 const unsigned* amax_bits, float* out, int ldo, void* stream);
+int wm3_bw_gelu_fwd(const float* a, int lda, const float* bias, int rows, int cols, void* out, int ldo, void* stream);
+int wm3_bw_colsum_amax(const float* g, int ldg, const float* a, int lda, const float* bias,
+                       const unsigned* in_scale_bits, int rows, int cols, float* out, int ldo, float* partial,
+                       float* colsum, unsigned* amax_bits, void* stream);
 int wm3_bw_layernorm(const float* x, int ldx, int rows, int n, float eps, const float* gamma, const float* g, int ldg,
                      const unsigned* amax_bits, const float* add, float* gx, float* gxh, float* gsc, void* stream);
 int wm3_bw_natten(const void* qkv, int ldq, const int64_t* nbr, const int* inv_off, const int* inv_ent, int T, int K,

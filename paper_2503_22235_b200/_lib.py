@@ -106,6 +106,8 @@ SIGNATURES = {
     "wm3_bw_cast": [_vp, _i, _i, _i, _i, _vp, _i, _i, _vp, _vp],
     "wm3_bw_colsum": [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp],
     "wm3_bw_gelu": [_vp, _i, _vp, _i, _vp, _i, _i, _vp, _vp, _i, _vp],
+    "wm3_bw_gelu_fwd": [_vp, _i, _vp, _i, _i, _vp, _i, _vp],
+    "wm3_bw_colsum_amax": [_vp, _i, _vp, _i, _vp, _vp, _i, _i, _vp, _i, _vp, _vp, _vp, _vp],
     "wm3_bw_layernorm": [_vp, _i, _i, _i, _f, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp],
     "wm3_bw_natten": [_vp, _i, _vp, _vp, _vp, _i, _i, _i, _i, _f, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp],
     "wm3_bw_rope": [_vp, _i, _i, _i, _i, _vp, _vp, _vp],

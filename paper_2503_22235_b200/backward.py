@@ -88,6 +88,41 @@ def _colsum(src: torch.Tensor, rows: int, cols: int, src2: torch.Tensor | None =
     return out
 
 
+def _colsum_amax(src: torch.Tensor, rows: int, cols: int, gelu_of: torch.Tensor | None = None,
+                 bias: torch.Tensor | None = None, in_scale: _Scale | None = None):
+    """(column sums, _Scale of max |v|) in one pass over v = src, or v = GELU backward of src (pre-activation
+    `gelu_of` + bias, src divided by in_scale), which is then returned too: (colsum, scale, v)."""
+    chunks = (rows + 255) // 256
+    partial = torch.empty((chunks, cols), dtype=torch.float32, device=src.device)
+    colsum = torch.empty(cols, dtype=torch.float32, device=src.device)
+    s = _Scale(src.device)
+    out = None if gelu_of is None else torch.empty((rows, cols), dtype=torch.float32, device=src.device)
+    check(_lib.lib().wm3_bw_colsum_amax(ptr(src), src.stride(0), ptr(gelu_of),
+                                        0 if gelu_of is None else gelu_of.stride(0), ptr(bias),
+                                        None if in_scale is None else in_scale.ptr(), rows, cols, ptr(out),
+                                        0 if out is None else out.stride(0), ptr(partial), ptr(colsum), s.ptr(),
+                                        stream_ptr()), "wm3_bw_colsum_amax")
+    return (colsum, s) if out is None else (colsum, s, out)
+
+
+def _layernorm_backward(x: torch.Tensor, gamma: torch.Tensor, g: torch.Tensor, scale: _Scale,
+                        add: torch.Tensor | None):
+    """LayerNorm reverse mode over rows of x [T][D] fp32 (autodiff.py:400-424) for the scaled output gradient g
+    (row pitch g.stride(0)), plus `add` (the residual path): (gx, dgamma, dbeta), the parameter gradients as
+    deterministic column sums of the kernel's per-row products.  (Folding those sums into the row kernel measured
+    slower: a warp must then own a run of rows, which costs the occupancy the one-row-per-warp kernel hides its
+    loads with.)"""
+    T, D = x.shape
+    dev = x.device
+    gx = torch.empty((T, D), dtype=torch.float32, device=dev)
+    gxh = torch.empty_like(gx)
+    gsc = torch.empty_like(gx)
+    check(_lib.lib().wm3_bw_layernorm(ptr(x), x.stride(0), T, D, LN_EPS, ptr(gamma), ptr(g), g.stride(0),
+                                      scale.ptr(), ptr(add), ptr(gx), ptr(gxh), ptr(gsc), stream_ptr()),
+          "wm3_bw_layernorm")
+    return gx, _colsum(gxh, T, D), _colsum(gsc, T, D)
+
+
 def _gemm_tn(a: torch.Tensor, b: torch.Tensor, m: int, n: int, k: int) -> torch.Tensor:
     """fp32 C[m][n] = sum_t A[t][:m] B[t][:n] over k rows (the weight gradients over tokens): MN-major tcgen05
     operands straight from the row-major 16-bit tensors, no transposed copies."""
@@ -259,36 +294,25 @@ def block_vjp_device(xd: torch.Tensor, bw, extents, window, heads: int, dh: int,
     ops.linear(ctx, bw.w_o, L.WM3_EPI_BIAS_RESID_F32, bias=bw.b_o, out=x1, n_valid=D)
     hn2 = ops.layernorm_bf16(x1, bw.ln2_g, bw.ln2_b, ldo=kp)
     a0 = _gemm(hn2, bw.w_1, T, nm, kp)                                   # W1 pre-activation without bias
-    mid = ops.linear(hn2, bw.w_1, L.WM3_EPI_BIAS_GELU_BF16, bias=bw.b_1)  # GELU output as the forward stores it
+    mid = torch.empty((T, nm), dtype=L.ELEM, device=dev)                # GELU output as the forward stores it
+    check(L.lib().wm3_bw_gelu_fwd(ptr(a0), nm, ptr(bw.b_1), T, nm, ptr(mid), nm, stream_ptr()), "wm3_bw_gelu_fwd")
 
     # ---- W2 ----
-    s1 = _amax(gyd, T, D)
+    db2, s1 = _colsum_amax(gyd, T, D)
     gyh = _cast(gyd, T, D, kp, scale=s1)                                # zero-padded to kp >= np_
     dw2 = _gemm_tn(gyh, mid, kp, nm, T)                                 # (kp, nm), x s1
-    db2 = _colsum(gyd, T, D)
     g_mid = _gemm(gyh, wt["w_2"], T, nm, np_)                           # x s1
     # ---- GELU' and W1 ----
-    g_a = torch.empty((T, nm), dtype=torch.float32, device=dev)
-    check(L.lib().wm3_bw_gelu(ptr(g_mid), nm, ptr(a0), nm, ptr(bw.b_1), T, nm, s1.ptr(), ptr(g_a), nm, stream_ptr()),
-          "wm3_bw_gelu")
-    s2 = _amax(g_a, T, nm)
+    db1, s2, g_a = _colsum_amax(g_mid, T, nm, gelu_of=a0, bias=bw.b_1, in_scale=s1)
     gah = _cast(g_a, T, nm, nm, scale=s2)
     dw1 = _gemm_tn(gah, hn2, nm, kp, T)
-    db1 = _colsum(g_a, T, nm)
     g_hn2 = _gemm(gah, wt["w_1"], T, kp, nm)   # x s2
     # ---- LN2 (+ the residual path gy) ----
-    gx1 = torch.empty((T, D), dtype=torch.float32, device=dev)
-    gxh2 = torch.empty_like(gx1)
-    gsc2 = torch.empty_like(gx1)
-    check(L.lib().wm3_bw_layernorm(ptr(x1), D, T, D, LN_EPS, ptr(bw.ln2_g), ptr(g_hn2), kp, s2.ptr(), ptr(gyd),
-                                   ptr(gx1), ptr(gxh2), ptr(gsc2), stream_ptr()), "wm3_bw_layernorm")
-    dln2_g = _colsum(gxh2, T, D)
-    dln2_b = _colsum(gsc2, T, D)
+    gx1, dln2_g, dln2_b = _layernorm_backward(x1, bw.ln2_g, g_hn2, s2, gyd)
     # ---- O-proj ----
-    s3 = _amax(gx1, T, D)
+    dbo, s3 = _colsum_amax(gx1, T, D)
     gx1h = _cast(gx1, T, D, kp, scale=s3)
     dwo = _gemm_tn(gx1h, ctx, kp, hd, T)
-    dbo = _colsum(gx1, T, D)
     g_ctx = _gemm(gx1h, wt["w_o"], T, hd, np_)  # x s3
     # ---- attention (query and key sides) and the rotary transpose ----
     g_qkv = torch.zeros((T, 3 * hd), dtype=torch.float32, device=dev)
@@ -311,19 +335,12 @@ def block_vjp_device(xd: torch.Tensor, bw, extents, window, heads: int, dh: int,
     cs, sn = _rope_pair_tables(extents, dh, dhp, dev)
     check(L.lib().wm3_bw_rope(ptr(g_qkv), 3 * hd, T, heads, dhp, ptr(cs), ptr(sn), stream_ptr()), "wm3_bw_rope")
     # ---- QKV ----
-    s4 = _amax(g_qkv, T, 3 * hd)
+    dbqkv, s4 = _colsum_amax(g_qkv, T, 3 * hd)
     gqh = _cast(g_qkv, T, 3 * hd, 3 * hd, scale=s4)
     dwqkv = _gemm_tn(gqh, hn, 3 * hd, kp, T)
-    dbqkv = _colsum(g_qkv, T, 3 * hd)
     g_hn = _gemm(gqh, wt["w_qkv"], T, kp, 3 * hd)  # x s4
     # ---- LN1 (+ gx1) ----
-    gx = torch.empty((T, D), dtype=torch.float32, device=dev)
-    gxh1 = torch.empty_like(gx)
-    gsc1 = torch.empty_like(gx)
-    check(L.lib().wm3_bw_layernorm(ptr(xd), D, T, D, LN_EPS, ptr(bw.ln1_g), ptr(g_hn), kp, s4.ptr(), ptr(gx1),
-                                   ptr(gx), ptr(gxh1), ptr(gsc1), stream_ptr()), "wm3_bw_layernorm")
-    dln1_g = _colsum(gxh1, T, D)
-    dln1_b = _colsum(gsc1, T, D)
+    gx, dln1_g, dln1_b = _layernorm_backward(xd, bw.ln1_g, g_hn, s4, gx1)
 
     acc.add("w_qkv", dwqkv, s4)
     acc.add("b_qkv", dbqkv)

@@ -131,13 +131,103 @@ __global__ void bw_colsum_partial_kernel(const float* __restrict__ src, const fl
   partial[static_cast<size_t>(blockIdx.y) * cols + c] = acc;
 }
 
-__global__ void bw_colsum_final_kernel(const float* __restrict__ partial, int chunks, int cols,
-                                       const unsigned* amax_bits, float* __restrict__ out) {
+// One pass for a gradient that needs both its column sums (a bias gradient) and its max |x| (the operand
+// scale of the next cast): bw_colsum_partial_kernel's fixed row chunks plus one atomicMax per block.  With `a`
+// set it first applies the GELU derivative, out = (g / scale) * gelu'(a + bias) (bw_gelu_kernel), and stores
+// it — the GELU backward, the bias gradient and the scale of the W1 operands read the tensor once.
+__global__ void bw_colsum_amax_kernel(const float* __restrict__ g, int ldg, const float* __restrict__ a, int lda,
+                                      const float* __restrict__ bias, const unsigned* in_scale_bits, int rows,
+                                      int cols, float* __restrict__ out, int ldo, float* __restrict__ partial,
+                                      unsigned* amax_bits) {
+  __shared__ float red[32];
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
+  float acc = 0.f, m = 0.f;
+  if (c < cols) {
+    const int r0 = blockIdx.y * BW_CHUNK, r1 = min(rows, r0 + BW_CHUNK);
+    if (a != nullptr) {
+      const float inv = 1.f / grad_scale(in_scale_bits), b = __ldg(bias + c);
+#pragma unroll 4
+      for (int r = r0; r < r1; ++r) {
+        const float z = a[static_cast<size_t>(r) * lda + c] + b;
+        const float d =
+            0.5f * (1.f + erff(z * 0.70710678118654752f)) + z * 0.39894228040143268f * __expf(-0.5f * z * z);
+        const float v = g[static_cast<size_t>(r) * ldg + c] * inv * d;
+        out[static_cast<size_t>(r) * ldo + c] = v;
+        acc += v;
+        m = fmaxf(m, fabsf(v));
+      }
+    } else {
+#pragma unroll 4
+      for (int r = r0; r < r1; ++r) {
+        const float v = g[static_cast<size_t>(r) * ldg + c];
+        acc += v;
+        m = fmaxf(m, fabsf(v));
+      }
+    }
+    partial[static_cast<size_t>(blockIdx.y) * cols + c] = acc;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) atomicMax(amax_bits, __float_as_uint(m));
+  }
+}
+
+// out[c] = (sum over k of partial[k][c]) / scale.  Block: 32 columns x 8 lanes groups; group q adds partials
+// q, q + 8, q + 16, ... in order, then the 8 group sums are added in group order (a fixed order for any launch).
+__global__ void __launch_bounds__(256) bw_colsum_final_kernel(const float* __restrict__ partial, int chunks, int cols,
+                                                              const unsigned* amax_bits, float* __restrict__ out) {
+  __shared__ float red[8][33];
+  const int cl = threadIdx.x & 31, q = threadIdx.x >> 5, c = blockIdx.x * 32 + cl;
   float acc = 0.f;
-  for (int k = 0; k < chunks; ++k) acc += partial[static_cast<size_t>(k) * cols + c];
-  out[c] = acc / grad_scale(amax_bits);
+  if (c < cols) {
+#pragma unroll 4
+    for (int k = q; k < chunks; k += 8) acc += __ldg(partial + static_cast<size_t>(k) * cols + c);
+  }
+  red[q][cl] = acc;
+  __syncthreads();
+  if (q == 0 && c < cols) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k][cl];
+    out[c] = t / grad_scale(amax_bits);
+  }
+}
+
+// The forward's GELU activation rebuilt from the stored pre-activation: out = operand(GELU(a + bias)) with the
+// W1 GEMM epilogue's exact arithmetic (gemm.cu WM3_EPI_BIAS_GELU_BF16: fp32 a + bias, then the same GELU and
+// packing), so it is bitwise the forward's activation without re-running the W1 GEMM.  8 elements per
+// thread-step; cols, lda, ldo multiples of 8.
+__global__ void bw_gelu_fwd_kernel(const float* __restrict__ a, int lda, const float* __restrict__ bias, int rows,
+                                   int cols, elem_t* __restrict__ out, int ldo) {
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    const float* ar = a + static_cast<size_t>(r) * lda;
+    elem_t* orow = out + static_cast<size_t>(r) * ldo;
+    for (int c = 8 * threadIdx.x; c < cols; c += 8 * blockDim.x) {
+      float v[8];
+      const float4 x0 = __ldg(reinterpret_cast<const float4*>(ar + c));
+      const float4 x1 = __ldg(reinterpret_cast<const float4*>(ar + c + 4));
+      const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + c));
+      const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + c + 4));
+      v[0] = x0.x + b0.x; v[1] = x0.y + b0.y; v[2] = x0.z + b0.z; v[3] = x0.w + b0.w;
+      v[4] = x1.x + b1.x; v[5] = x1.y + b1.y; v[6] = x1.z + b1.z; v[7] = x1.w + b1.w;
+      uint32_t pk[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+#if !defined(WM3_OPERAND_BF16) && WM3_GELU_VARIANT == 2
+        pk[e] = gelu_tanh_h2(v[2 * e], v[2 * e + 1]);
+#else
+        pk[e] = pack_elem(gelu_epi(v[2 * e]), gelu_epi(v[2 * e + 1]));
+#endif
+      }
+      *reinterpret_cast<uint4*>(orow + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    }
+  }
 }
 
 // out = (g / scale) * gelu'(a + bias), exact-erf GELU derivative Phi(z) + z phi(z) (autodiff.py:372-382)
@@ -373,8 +463,31 @@ extern "C" int wm3_bw_colsum(const float* src, const float* src2, int rows, int 
   const int chunks = (rows + BW_CHUNK - 1) / BW_CHUNK;
   bw_colsum_partial_kernel<<<dim3((cols + 127) / 128, chunks), 128, 0, s>>>(src, src2, rows, cols, ld, partial);
   if (check_launch("bw_colsum_partial_kernel")) return -1;
-  bw_colsum_final_kernel<<<(cols + 127) / 128, 128, 0, s>>>(partial, chunks, cols, amax_bits, out);
+  bw_colsum_final_kernel<<<(cols + 31) / 32, 256, 0, s>>>(partial, chunks, cols, amax_bits, out);
   return check_launch("bw_colsum_final_kernel");
+}
+
+extern "C" int wm3_bw_colsum_amax(const float* g, int ldg, const float* a, int lda, const float* bias,
+                                  const unsigned* in_scale_bits, int rows, int cols, float* out, int ldo,
+                                  float* partial, float* colsum, unsigned* amax_bits, void* stream) {
+  if (rows < 1 || cols < 1) return set_error("wm3_bw_colsum_amax: empty");
+  if (a != nullptr && (out == nullptr || bias == nullptr)) return set_error("wm3_bw_colsum_amax: GELU needs out, bias");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(amax_bits, 0, sizeof(unsigned), s) != cudaSuccess) return set_error("wm3_bw_colsum_amax: memset");
+  const int chunks = (rows + BW_CHUNK - 1) / BW_CHUNK;
+  bw_colsum_amax_kernel<<<dim3((cols + 255) / 256, chunks), 256, 0, s>>>(g, ldg, a, lda, bias, in_scale_bits, rows,
+                                                                         cols, out, ldo, partial, amax_bits);
+  if (check_launch("bw_colsum_amax_kernel")) return -1;
+  bw_colsum_final_kernel<<<(cols + 31) / 32, 256, 0, s>>>(partial, chunks, cols, nullptr, colsum);
+  return check_launch("bw_colsum_final_kernel");
+}
+
+extern "C" int wm3_bw_gelu_fwd(const float* a, int lda, const float* bias, int rows, int cols, void* out, int ldo,
+                               void* stream) {
+  if (rows < 1 || cols < 1 || cols % 8 || lda % 8 || ldo % 8) return set_error("wm3_bw_gelu_fwd: shape");
+  bw_gelu_fwd_kernel<<<rows < 148 * 8 ? rows : 148 * 8, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      a, lda, bias, rows, cols, static_cast<elem_t*>(out), ldo);
+  return check_launch("bw_gelu_fwd_kernel");
 }
 
 extern "C" int wm3_bw_gelu(const float* g, int ldg, const float* a, int lda, const float* bias, int rows, int cols,

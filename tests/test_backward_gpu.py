@@ -279,3 +279,36 @@ def test_host_offload_store_out_of_order_take():
     torch.cuda.synchronize()
     assert all(torch.equal(got[k], xs[k]) for k in range(6))
     assert st.stats()["demand_stalls"] >= 1
+
+
+def test_gelu_rebuild_and_fused_stats_kernels():
+    """wm3_bw_gelu_fwd rebuilds the forward's GELU activation bitwise from the fp32 pre-activation (the W1 GEMM
+    is not re-run in the backward); wm3_bw_colsum_amax gives the same column sums and maxima as the separate
+    wm3_bw_colsum / wm3_bw_amax passes, and its fused GELU backward the same values as wm3_bw_gelu."""
+    import torch
+    from paper_2503_22235_b200 import _lib, ops
+    from paper_2503_22235_b200 import backward as bwd
+    from paper_2503_22235_b200._lib import check, ptr, stream_ptr
+    torch.manual_seed(3)
+    T, k, n = 1000, 256, 512
+    a = (torch.randn(T, k, device="cuda") * 0.5).to(_lib.ELEM)
+    w = (torch.randn(n, k, device="cuda") * 0.1).to(_lib.ELEM)
+    b = torch.randn(n, device="cuda") * 0.3
+    ref = ops.linear(a, w, _lib.WM3_EPI_BIAS_GELU_BF16, bias=b)
+    a0 = bwd._gemm(a, w, T, n, k)
+    mid = torch.empty((T, n), dtype=_lib.ELEM, device="cuda")
+    check(_lib.lib().wm3_bw_gelu_fwd(ptr(a0), n, ptr(b), T, n, ptr(mid), n, stream_ptr()), "wm3_bw_gelu_fwd")
+    assert torch.equal(mid.view(torch.int16), ref[:, :n].contiguous().view(torch.int16))
+
+    g = torch.randn(T, n, device="cuda") * 1e3
+    cs, s = bwd._colsum_amax(g, T, n)
+    assert torch.equal(cs, bwd._colsum(g, T, n))
+    assert torch.equal(s.bits, bwd._amax(g, T, n).bits)
+    s_in = bwd._amax(g, T, n)
+    cs2, s2, ga = bwd._colsum_amax(g, T, n, gelu_of=a0, bias=b, in_scale=s_in)
+    ga_ref = torch.empty_like(g)
+    check(_lib.lib().wm3_bw_gelu(ptr(g), n, ptr(a0), n, ptr(b), T, n, s_in.ptr(), ptr(ga_ref), n, stream_ptr()),
+          "wm3_bw_gelu")
+    torch.testing.assert_close(ga, ga_ref, rtol=1e-6, atol=0)
+    torch.testing.assert_close(cs2, bwd._colsum(ga, T, n), rtol=0, atol=0)
+    assert torch.equal(s2.bits, bwd._amax(ga, T, n).bits)
