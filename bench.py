@@ -613,6 +613,19 @@ def run_gpu(args, world, rank, local_rank):
         e_ms = e0.elapsed_time(e1)
         e2e_api = ("attention.NattenBlockStream: page-locked host batches, H2D / block / D2H on three CUDA "
                    "streams, neighbouring batches' transfers overlapped")
+        # the bound of this leg: the same bytes moved both ways at once with no compute (PCIe, not HBM / SMs)
+        for k in range(4):  # each round: both copies start together, the next round starts when both are done
+            if k == 1:
+                e0.record(runner.s_in)
+            runner.s_out.wait_stream(runner.s_in)
+            with torch.cuda.stream(runner.s_in):
+                runner.buf[0].copy_(hin[0], non_blocking=True)
+            with torch.cuda.stream(runner.s_out):
+                hout[0].copy_(runner.buf[1], non_blocking=True)
+            runner.s_in.wait_stream(runner.s_out)
+        e1.record(runner.s_in)
+        runner.synchronize()
+        link_ms = e0.elapsed_time(e1) / 3
     else:
         def e2e_step():
             xd.copy_(x_host, non_blocking=True)
@@ -622,6 +635,7 @@ def run_gpu(args, world, rank, local_rank):
         e2e_step()
         e_ms = timed(e2e_step, e_steps, stream, world)
         e2e_api = "BandedProcessor block (overlapped halo exchange) with pinned host copies of the band"
+        link_ms = None
     e2e_value = flops * e_steps / (e_ms / 1e3) / 1e12
     clk.__exit__(None, None, None)
 
@@ -669,7 +683,11 @@ def run_gpu(args, world, rank, local_rank):
                                      "blocks") if bw.folded else "separate LayerNorm launches"},
             "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": int(x.numel() * 4),
                     "d2h_bytes_per_step": int(x.numel() * 4), "ms_per_step": e_ms / e_steps,
-                    "api": e2e_api},
+                    "api": e2e_api,
+                    "link_ms_per_step": link_ms,
+                    "link_note": ("the step's H2D and D2H bytes copied both ways at once with no compute, same "
+                                  "streams and buffers: the PCIe bound of this leg (the block itself takes "
+                                  "ms_per_step of the device-timed value)") if link_ms else None},
             "gpu_launches": n_launch * args.steps,
             "roofline": roof,
             "kernels": table,
