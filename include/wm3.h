@@ -24,6 +24,8 @@
  *                             WM3_EPI_BIAS_RESID_F32  attention.py:179,183  x += ctx Wo + bo / mid W2 + b2
  *                             WM3_EPI_QKV_ROPE        attention.py:167-171  q,k,v + bias, rotary on q,k
  *                             WM3_EPI_F32             raw fp32 accumulator (tests)
+ *                             WM3_EPI_GELU_GRAD_F32   autodiff.py:372-382  out = acc / scale * gelu'(out + bias),
+ *                                                     in place over the stored pre-activation (wm3_linear_gelu_grad)
  *   wm3_natten_fwd          attention.py:173-178 gather + q k^T/sqrt(dh) + softmax + @V, fused
  *   wm3_block_fwd           attention.py:146-184 the whole block (7 launches) in one call
  *   wm3_conv  WM3_CONV_S1/S2  model.py:296-301 + autodiff.py:677-713  3x3, row zero pad, col wrap, stride 1/2
@@ -46,6 +48,7 @@ enum {
   WM3_EPI_BIAS_GELU_BF16 = 2,
   WM3_EPI_BIAS_RESID_F32 = 3,
   WM3_EPI_QKV_ROPE = 4,
+  WM3_EPI_GELU_GRAD_F32 = 5,
 };
 
 /* Rotary description for WM3_EPI_QKV_ROPE (attention.py:48-92).  Output columns are laid out
@@ -300,6 +303,12 @@ int wm3_bw_natten(const void* qkv, int ldq, const int64_t* nbr, const int* inv_o
                   int heads, int dhp, float scale, const float* gctx, int ldc, const unsigned* amax_bits, float* P,
                   float* dS, float* work, float* gout, int ldg, void* stream);
 int wm3_bw_rope(float* g, int ldg, int T, int heads, int dhp, const float* cos_t, const float* sin_t, void* stream);
+
+/* The MLP's GELU backward fused into the gradient GEMM (autodiff.py:372-382 after the W2 matmul VJP :350):
+ * preact_inout [m][n] fp32 holds the W1 pre-activation without bias on entry and
+ * (A . B^T) / scale(amax_bits) * gelu'(preact + bias) on exit (the residual epilogue's in-place read-then-write). */
+int wm3_linear_gelu_grad(const void* a, int lda, const void* b, int ldb, int m, int n, int k, float* preact_inout,
+                         int ldo, const float* bias, const unsigned* amax_bits, void* stream);
 
 /* C[m][n] (fp32) = sum_t A[t][m] B[t][n] with A [k][m], B [k][n] row-major 16-bit (the backward's weight gradients
  * over the token axis, autodiff.py:350 matmul VJP): MN-major tcgen05 operands, no transposed copies; m, n multiples

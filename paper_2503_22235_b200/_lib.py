@@ -25,6 +25,7 @@ WM3_EPI_BIAS_BF16 = 1
 WM3_EPI_BIAS_GELU_BF16 = 2
 WM3_EPI_BIAS_RESID_F32 = 3
 WM3_EPI_QKV_ROPE = 4
+WM3_EPI_GELU_GRAD_F32 = 5
 
 _vp = ctypes.c_void_p
 _i = ctypes.c_int
@@ -111,6 +112,7 @@ SIGNATURES = {
     "wm3_bw_layernorm": [_vp, _i, _i, _i, _f, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp],
     "wm3_bw_natten": [_vp, _i, _vp, _vp, _vp, _i, _i, _i, _i, _f, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp],
     "wm3_bw_rope": [_vp, _i, _i, _i, _i, _vp, _vp, _vp],
+    "wm3_linear_gelu_grad": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _i, _vp, _vp, _vp],
     "wm3_linear_tn": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _i, _vp],
     "wm3_bw_na_prep": [_vp, _i, _i, _i, _i, _vp, _i, _vp, _f, _vp, _i, _vp, _vp, _vp],
     "wm3_natten_fwd_lse": [_vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _f, _vp, _vp],

@@ -301,9 +301,13 @@ def block_vjp_device(xd: torch.Tensor, bw, extents, window, heads: int, dh: int,
     db2, s1 = _colsum_amax(gyd, T, D)
     gyh = _cast(gyd, T, D, kp, scale=s1)                                # zero-padded to kp >= np_
     dw2 = _gemm_tn(gyh, mid, kp, nm, T)                                 # (kp, nm), x s1
-    g_mid = _gemm(gyh, wt["w_2"], T, nm, np_)                           # x s1
     # ---- GELU' and W1 ----
-    db1, s2, g_a = _colsum_amax(g_mid, T, nm, gelu_of=a0, bias=bw.b_1, in_scale=s1)
+    # g_a = (gy . W2) / s1 * gelu'(a0 + b1), the GELU backward in the gradient GEMM's epilogue, in place over a0
+    check(L.lib().wm3_linear_gelu_grad(ptr(gyh), gyh.stride(0), ptr(wt["w_2"]), wt["w_2"].stride(0), T, nm, np_,
+                                       ptr(a0), a0.stride(0), ptr(bw.b_1), s1.ptr(), stream_ptr()),
+          "wm3_linear_gelu_grad")
+    g_a, a0 = a0, None
+    db1, s2 = _colsum_amax(g_a, T, nm)
     gah = _cast(g_a, T, nm, nm, scale=s2)
     dw1 = _gemm_tn(gah, hn2, nm, kp, T)
     g_hn2 = _gemm(gah, wt["w_1"], T, kp, nm)   # x s2

@@ -20,14 +20,6 @@ namespace wm3 {
 DEVI float to_f(__half v) { return __half2float(v); }
 DEVI float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
 
-// scale for a tensor whose max |x| has the bits `amax_bits` (non-negative float bits order as unsigned)
-DEVI float grad_scale(const unsigned* amax_bits) {
-  if (amax_bits == nullptr) return 1.f;
-  const float amax = __uint_as_float(*amax_bits);
-  if (!(amax > 0.f) || !isfinite(amax)) return 1.f;
-  return exp2f(14.f - ceilf(log2f(amax)));
-}
-
 // Row strips: block b takes rows b, b + grid, ...; its threads sweep the columns (4 at a time when the rows are
 // 16-byte aligned), so there is no per-element 64-bit index division; one atomic per block.
 __global__ void bw_amax_kernel(const float* __restrict__ x, int rows, int cols, int ld, unsigned* amax_bits) {
@@ -130,6 +122,76 @@ __global__ void bw_colsum_partial_kernel(const float* __restrict__ src, const fl
   }
   partial[static_cast<size_t>(blockIdx.y) * cols + c] = acc;
 }
+
+// Vectorised column sums over one BW_CHUNK-row chunk (cols, leading dims multiple of 4, 16-byte aligned bases):
+// block = 256 columns x 4 row groups, thread (quad q, group k) adds rows r0 + k, r0 + k + 4, ... of columns
+// 4q .. 4q + 3 with 16-byte loads, and the 4 group sums are added in group order through shared memory into
+// partial[chunk][c] — a fixed order, and 4x the bytes in flight of one float per thread.  MODE 0: v = g;
+// MODE 1: v = g * a (product sums); MODE 2: v = (g / scale) * gelu'(a + bias), stored to out.  With amax_bits,
+// also atomicMax of max |v| (one per block).
+template <int MODE>
+__global__ void __launch_bounds__(256) bw_colsum4_kernel(const float* __restrict__ g, int ldg,
+                                                         const float* __restrict__ a, int lda,
+                                                         const float* __restrict__ bias,
+                                                         const unsigned* in_scale_bits, int rows, int cols,
+                                                         float* __restrict__ out, int ldo,
+                                                         float* __restrict__ partial, unsigned* amax_bits) {
+  __shared__ float red[4][257];
+  __shared__ float redm[8];
+  const int q = threadIdx.x & 63, k = threadIdx.x >> 6;
+  const int c = blockIdx.x * 256 + 4 * q;
+  const bool ok = c < cols;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float m = 0.f;
+  if (ok) {
+    const int r0 = blockIdx.y * BW_CHUNK, r1 = min(rows, r0 + BW_CHUNK);
+    float inv = 1.f;
+    float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (MODE == 2) {
+      inv = 1.f / grad_scale(in_scale_bits);
+      b = __ldg(reinterpret_cast<const float4*>(bias + c));
+    }
+#pragma unroll 4
+    for (int r = r0 + k; r < r1; r += 4) {
+      float4 v = __ldg(reinterpret_cast<const float4*>(g + static_cast<size_t>(r) * ldg + c));
+      if (MODE == 1) {
+        const float4 w = __ldg(reinterpret_cast<const float4*>(a + static_cast<size_t>(r) * lda + c));
+        v.x *= w.x; v.y *= w.y; v.z *= w.z; v.w *= w.w;
+      } else if (MODE == 2) {
+        const float4 z = __ldg(reinterpret_cast<const float4*>(a + static_cast<size_t>(r) * lda + c));
+        v.x = v.x * inv * gelu_grad(z.x + b.x);
+        v.y = v.y * inv * gelu_grad(z.y + b.y);
+        v.z = v.z * inv * gelu_grad(z.z + b.z);
+        v.w = v.w * inv * gelu_grad(z.w + b.w);
+        *reinterpret_cast<float4*>(out + static_cast<size_t>(r) * ldo + c) = v;
+      }
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+  }
+  red[k][4 * q + 0] = acc.x;
+  red[k][4 * q + 1] = acc.y;
+  red[k][4 * q + 2] = acc.z;
+  red[k][4 * q + 3] = acc.w;
+  if (amax_bits != nullptr) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) redm[threadIdx.x >> 5] = m;
+  }
+  __syncthreads();
+  const int cc = blockIdx.x * 256 + threadIdx.x;
+  if (cc < cols)
+    partial[static_cast<size_t>(blockIdx.y) * cols + cc] =
+        ((red[0][threadIdx.x] + red[1][threadIdx.x]) + red[2][threadIdx.x]) + red[3][threadIdx.x];
+  if (amax_bits != nullptr && threadIdx.x == 0) {
+    float t = redm[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) t = fmaxf(t, redm[w]);
+    atomicMax(amax_bits, __float_as_uint(t));
+  }
+}
+
+static inline bool aligned16(const void* p) { return p == nullptr || reinterpret_cast<uintptr_t>(p) % 16 == 0; }
 
 // One pass for a gradient that needs both its column sums (a bias gradient) and its max |x| (the operand
 // scale of the next cast): bw_colsum_partial_kernel's fixed row chunks plus one atomicMax per block.  With `a`
@@ -461,8 +523,18 @@ extern "C" int wm3_bw_colsum(const float* src, const float* src2, int rows, int 
                              float* partial, float* out, void* stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int chunks = (rows + BW_CHUNK - 1) / BW_CHUNK;
-  bw_colsum_partial_kernel<<<dim3((cols + 127) / 128, chunks), 128, 0, s>>>(src, src2, rows, cols, ld, partial);
-  if (check_launch("bw_colsum_partial_kernel")) return -1;
+  if (cols % 4 == 0 && ld % 4 == 0 && aligned16(src) && aligned16(src2)) {
+    if (src2 != nullptr)
+      bw_colsum4_kernel<1><<<dim3((cols + 255) / 256, chunks), 256, 0, s>>>(src, ld, src2, ld, nullptr, nullptr, rows,
+                                                                            cols, nullptr, 0, partial, nullptr);
+    else
+      bw_colsum4_kernel<0><<<dim3((cols + 255) / 256, chunks), 256, 0, s>>>(src, ld, nullptr, 0, nullptr, nullptr,
+                                                                            rows, cols, nullptr, 0, partial, nullptr);
+    if (check_launch("bw_colsum4_kernel")) return -1;
+  } else {
+    bw_colsum_partial_kernel<<<dim3((cols + 127) / 128, chunks), 128, 0, s>>>(src, src2, rows, cols, ld, partial);
+    if (check_launch("bw_colsum_partial_kernel")) return -1;
+  }
   bw_colsum_final_kernel<<<(cols + 31) / 32, 256, 0, s>>>(partial, chunks, cols, amax_bits, out);
   return check_launch("bw_colsum_final_kernel");
 }
@@ -475,9 +547,21 @@ extern "C" int wm3_bw_colsum_amax(const float* g, int ldg, const float* a, int l
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(amax_bits, 0, sizeof(unsigned), s) != cudaSuccess) return set_error("wm3_bw_colsum_amax: memset");
   const int chunks = (rows + BW_CHUNK - 1) / BW_CHUNK;
-  bw_colsum_amax_kernel<<<dim3((cols + 255) / 256, chunks), 256, 0, s>>>(g, ldg, a, lda, bias, in_scale_bits, rows,
-                                                                         cols, out, ldo, partial, amax_bits);
-  if (check_launch("bw_colsum_amax_kernel")) return -1;
+  const bool v4 = cols % 4 == 0 && ldg % 4 == 0 && aligned16(g) &&
+                  (a == nullptr || (lda % 4 == 0 && ldo % 4 == 0 && aligned16(a) && aligned16(out) && aligned16(bias)));
+  if (v4) {
+    if (a != nullptr)
+      bw_colsum4_kernel<2><<<dim3((cols + 255) / 256, chunks), 256, 0, s>>>(g, ldg, a, lda, bias, in_scale_bits, rows,
+                                                                            cols, out, ldo, partial, amax_bits);
+    else
+      bw_colsum4_kernel<0><<<dim3((cols + 255) / 256, chunks), 256, 0, s>>>(g, ldg, nullptr, 0, nullptr, nullptr, rows,
+                                                                            cols, nullptr, 0, partial, amax_bits);
+    if (check_launch("bw_colsum4_kernel")) return -1;
+  } else {
+    bw_colsum_amax_kernel<<<dim3((cols + 255) / 256, chunks), 256, 0, s>>>(g, ldg, a, lda, bias, in_scale_bits, rows,
+                                                                           cols, out, ldo, partial, amax_bits);
+    if (check_launch("bw_colsum_amax_kernel")) return -1;
+  }
   bw_colsum_final_kernel<<<(cols + 31) / 32, 256, 0, s>>>(partial, chunks, cols, nullptr, colsum);
   return check_launch("bw_colsum_final_kernel");
 }

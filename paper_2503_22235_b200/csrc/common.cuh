@@ -367,6 +367,18 @@ DEVI void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "me
 // ---------------------------------------------------------------------------------------------
 // small math
 // ---------------------------------------------------------------------------------------------
+// power-of-two operand scale of a gradient tensor whose max |x| has the float bits *amax_bits (non-negative float
+// bits order as unsigned): 2^(14 - ceil(log2 amax)), 1 for NULL / zero / non-finite (backward.cu, gemm.cu)
+DEVI float grad_scale(const unsigned* amax_bits) {
+  if (amax_bits == nullptr) return 1.f;
+  const float amax = __uint_as_float(*amax_bits);
+  if (!(amax > 0.f) || !isfinite(amax)) return 1.f;
+  return exp2f(14.f - ceilf(log2f(amax)));
+}
+// exact-erf GELU derivative Phi(z) + z phi(z) (autodiff.py:372-382)
+DEVI float gelu_grad(float z) {
+  return 0.5f * (1.f + erff(z * 0.70710678118654752f)) + z * 0.39894228040143268f * __expf(-0.5f * z * z);
+}
 DEVI float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 // Exact-erf GELU x * Phi(x) (autodiff.py:372-382) with Phi from the Abramowitz-Stegun 7.1.26 erfc form
 // (|error| < 1.5e-7, far below the fp16 output rounding): Phi(x) = 1 - q/2 (x >= 0) or q/2 (x < 0),

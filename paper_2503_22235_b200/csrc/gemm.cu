@@ -39,7 +39,14 @@ struct EpiParams {
   wm3_ln_fold_t fold;  // LayerNorm fold (include/wm3.h): producer (residual epilogue) / consumer (next GEMM)
   int ln_prod, ln_cons;
   int mn;  // operands MN-major (wm3_linear_tn: C = A^T B with A [K][M], B [K][N] row-major, 64 x 64 boxes)
+  const unsigned* gscale;  // WM3_EPI_GELU_GRAD_F32: amax bits of the output gradient's operand scale
 };
+
+// epilogues that read the fp32 output buffer before overwriting it (the residual stream, or the stored GELU
+// pre-activation of the in-place GELU backward)
+__host__ __device__ constexpr bool epi_reads_out(int e) {
+  return e == WM3_EPI_BIAS_RESID_F32 || e == WM3_EPI_GELU_GRAD_F32;
+}
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
@@ -60,7 +67,7 @@ struct GemmCfg {
   // Residual epilogue: the fp32 residual chunks stream into RSLOTS smem slots by TMA (warp 3), ahead of the
   // epilogue, instead of per-thread global loads (the O-proj epilogue was HBM-latency bound); one mainloop
   // stage gives up its smem for them.
-  static constexpr bool RESID_TMA = (EPI == WM3_EPI_BIAS_RESID_F32) && WM3_RESID_TMA;
+  static constexpr bool RESID_TMA = epi_reads_out(EPI) && WM3_RESID_TMA;
   // Two slots: with an even slot count and even units per tile, slot c % RSLOTS has the parity of the unit, so
   // each slot is consumed by one epilogue group only, in order (an odd count interleaves the groups on a slot
   // and a fast group can then pass a parity wait one phase early).
@@ -82,7 +89,7 @@ struct GemmCfg {
 
 template <int EPI>
 struct EpiTraits {
-  static constexpr bool F32 = (EPI == WM3_EPI_F32 || EPI == WM3_EPI_BIAS_RESID_F32);
+  static constexpr bool F32 = (EPI == WM3_EPI_F32 || epi_reads_out(EPI));
   static constexpr int CW = F32 ? 32 : 64;  // columns per staged chunk (128 B rows)
 };
 
@@ -368,7 +375,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int tile_it = 0;
     // LayerNorm fold, consumer side: the row's (rstd, rstd * mean), loaded one tile ahead so its latency never
     // sits between the accumulator and the epilogue.
-    constexpr bool kCons = (EPI != WM3_EPI_BIAS_RESID_F32 && EPI != WM3_EPI_F32);
+    constexpr bool kCons = (!epi_reads_out(EPI) && EPI != WM3_EPI_F32);
     const bool cons = kCons && ep.ln_cons;
     auto stats_load = [&](int t) {
       int pl, rr;
@@ -376,6 +383,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       return __ldg(reinterpret_cast<const float2*>(ep.fold.row_stats) + (rw < M ? rw : 0));
     };
     float2 ln_next = cons ? stats_load(tile0) : make_float2(0.f, 0.f);
+    const float ginv = (EPI == WM3_EPI_GELU_GRAD_F32) ? 1.f / grad_scale(ep.gscale) : 1.f;
     for (int tile = tile0; tile < ntiles; tile += tstep, ++tile_it) {
       int plane, r0;
       const int m0 = tile_rows(tile, plane, r0);
@@ -394,7 +402,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #endif
       constexpr int RESID_DEPTH = WM3_RESID_DEPTH;
       float xr[RESID_DEPTH + 1][32];
-      if (EPI == WM3_EPI_BIAS_RESID_F32 && !Cfg::RESID_TMA) {
+      if (epi_reads_out(EPI) && !Cfg::RESID_TMA) {
 #pragma unroll
         for (int i = 0; i < RESID_DEPTH; ++i)
           if (g + 2 * i < NUNITS) load_resid(ep, row, row_ok, n0 + (g + 2 * i) * CW, xr[i]);
@@ -407,14 +415,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int n = n0 + u * CW;
         const int it = (u - g) >> 1;  // compile-time after unrolling
         const float* xa = Cfg::RESID_TMA ? nullptr : xr[it % (RESID_DEPTH + 1)];
-        if (EPI == WM3_EPI_BIAS_RESID_F32 && !Cfg::RESID_TMA && u + 2 * RESID_DEPTH < NUNITS)
+        if (epi_reads_out(EPI) && !Cfg::RESID_TMA && u + 2 * RESID_DEPTH < NUNITS)
           load_resid(ep, row, row_ok, n + 2 * RESID_DEPTH * CW, xr[(it + RESID_DEPTH) % (RESID_DEPTH + 1)]);
         if (Tr::F32) {
           uint32_t r[32];
           tmem_ld32(taddr + u * CW, r);
           tmem_ld_wait();
           float* v = reinterpret_cast<float*>(r);  // accumulate in place: no extra 32-register copy
-          if (EPI == WM3_EPI_BIAS_RESID_F32) {
+          if (epi_reads_out(EPI)) {
             // residual chunk: from its TMA smem slot (SWIZZLE_128B rows, as the box landed), or the registers
             int rslot = 0;
             uint32_t rb = 0;
@@ -433,10 +441,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 ld_shared_v4(rb + sw128_off(r_in_tile, j), xv.x, xv.y, xv.z, xv.w);
               else
                 xv = make_float4(xa[4 * j + 0], xa[4 * j + 1], xa[4 * j + 2], xa[4 * j + 3]);
-              v[4 * j + 0] += b.x + xv.x;
-              v[4 * j + 1] += b.y + xv.y;
-              v[4 * j + 2] += b.z + xv.z;
-              v[4 * j + 3] += b.w + xv.w;
+              if (EPI == WM3_EPI_GELU_GRAD_F32) {  // in-place GELU backward: out held the pre-activation
+                v[4 * j + 0] = v[4 * j + 0] * ginv * gelu_grad(xv.x + b.x);
+                v[4 * j + 1] = v[4 * j + 1] * ginv * gelu_grad(xv.y + b.y);
+                v[4 * j + 2] = v[4 * j + 2] * ginv * gelu_grad(xv.z + b.z);
+                v[4 * j + 3] = v[4 * j + 3] * ginv * gelu_grad(xv.w + b.w);
+              } else {
+                v[4 * j + 0] += b.x + xv.x;
+                v[4 * j + 1] += b.y + xv.y;
+                v[4 * j + 2] += b.z + xv.z;
+                v[4 * j + 3] += b.w + xv.w;
+              }
             }
             if (Cfg::RESID_TMA) {
               // the slot's next TMA load (async proxy) must not overtake these generic-proxy reads
@@ -639,6 +654,7 @@ static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, c
     case WM3_EPI_BIAS_BF16: return launch_gemm<BN, WM3_EPI_BIAS_BF16, CG>(ta, tb, to, M, N, K, ep, s);
     case WM3_EPI_BIAS_GELU_BF16: return launch_gemm<BN, WM3_EPI_BIAS_GELU_BF16, CG>(ta, tb, to, M, N, K, ep, s);
     case WM3_EPI_BIAS_RESID_F32: return launch_gemm<BN, WM3_EPI_BIAS_RESID_F32, CG>(ta, tb, to, M, N, K, ep, s);
+    case WM3_EPI_GELU_GRAD_F32: return launch_gemm<BN, WM3_EPI_GELU_GRAD_F32, CG>(ta, tb, to, M, N, K, ep, s);
     case WM3_EPI_QKV_ROPE: return launch_gemm<BN, WM3_EPI_QKV_ROPE, CG>(ta, tb, to, M, N, K, ep, s);
     default: return set_error("wm3_linear: unknown epilogue %d", epi);
   }
@@ -653,9 +669,9 @@ struct OutPlanes {
 static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi, void* out,
                        int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, const OutPlanes& op,
                        void* stream, const wm3_halo_t* halo = nullptr, const wm3_ln_fold_t* fold = nullptr,
-                       bool mn = false) {
+                       bool mn = false, const unsigned* gscale = nullptr) {
   if (m <= 0 || n <= 0 || k <= 0) return set_error("wm3_linear: bad sizes m=%d n=%d k=%d", m, n, k);
-  const bool f32_out = (epi == WM3_EPI_F32 || epi == WM3_EPI_BIAS_RESID_F32);
+  const bool f32_out = (epi == WM3_EPI_F32 || epi_reads_out(epi));
   if ((lda % 8) || (ldb % 8) || (ldo % (f32_out ? 4 : 8)))
     return set_error("wm3_linear: pitches must be multiples of 8 (bf16) / 4 (f32 out)");
   if (n % 32) return set_error("wm3_linear: n=%d must be a multiple of 32", n);
@@ -666,7 +682,7 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
   if (op.planes < 1 || static_cast<long long>(op.planes) * op.plane_rows != m || op.plane_stride < op.plane_rows)
     return set_error("wm3_linear: %d planes x %d rows (stride %lld) do not tile m=%d", op.planes, op.plane_rows,
                      op.plane_stride, m);
-  if (epi == WM3_EPI_BIAS_RESID_F32 && op.planes != 1) return set_error("wm3_linear: residual output must be 2D");
+  if (epi_reads_out(epi) && op.planes != 1) return set_error("wm3_linear: residual output must be 2D");
   if (epi == WM3_EPI_QKV_ROPE && rope != nullptr) {
     if (reinterpret_cast<uintptr_t>(rope->dr) % 32 || rope->col == nullptr)
       return set_error("wm3_linear: rope dr table must be 32-byte aligned and the column table given");
@@ -680,6 +696,7 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
   ep.ld_resid = ldo;
   ep.resid_v8 = (ldo % 8 == 0) && (reinterpret_cast<uintptr_t>(out) % 32 == 0);
   ep.bias = bias;
+  ep.gscale = gscale;
   ep.n_valid = n_valid;
   ep.plane_rows = op.plane_rows;
   ep.planes = op.planes;
@@ -755,6 +772,14 @@ extern "C" int wm3_linear(const void* a, int lda, const void* b, int ldb, int m,
                           int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, void* stream) {
   const OutPlanes op{1, m, m, 0};
   return linear_impl(a, lda, b, ldb, m, n, k, epi, out, ldo, n_valid, bias, rope, op, stream);
+}
+
+extern "C" int wm3_linear_gelu_grad(const void* a, int lda, const void* b, int ldb, int m, int n, int k,
+                                    float* preact_inout, int ldo, const float* bias, const unsigned* amax_bits,
+                                    void* stream) {
+  const OutPlanes op{1, m, m, 0};
+  return linear_impl(a, lda, b, ldb, m, n, k, WM3_EPI_GELU_GRAD_F32, preact_inout, ldo, n, bias, nullptr, op, stream,
+                     nullptr, nullptr, false, amax_bits);
 }
 
 extern "C" int wm3_linear_planes(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi,

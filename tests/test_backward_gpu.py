@@ -312,3 +312,28 @@ def test_gelu_rebuild_and_fused_stats_kernels():
     torch.testing.assert_close(ga, ga_ref, rtol=1e-6, atol=0)
     torch.testing.assert_close(cs2, bwd._colsum(ga, T, n), rtol=0, atol=0)
     assert torch.equal(s2.bits, bwd._amax(ga, T, n).bits)
+
+
+def test_gelu_grad_gemm_epilogue():
+    """wm3_linear_gelu_grad (the GELU backward in the gradient GEMM's epilogue, in place over the stored
+    pre-activation) equals the separate path: fp32 GEMM, then wm3_bw_gelu."""
+    import torch
+    from paper_2503_22235_b200 import _lib
+    from paper_2503_22235_b200 import backward as bwd
+    from paper_2503_22235_b200._lib import check, ptr, stream_ptr
+    torch.manual_seed(5)
+    for T, n, k in ((1000, 512, 256), (333, 256, 64), (4096, 1024, 1024)):
+        a = (torch.randn(T, k, device="cuda")).to(_lib.ELEM)
+        w = (torch.randn(n, k, device="cuda") * 0.1).to(_lib.ELEM)
+        b = torch.randn(n, device="cuda") * 0.3
+        pre = torch.randn(T, n, device="cuda") * 2
+        s = bwd._Scale(a.device)
+        s.bits.view(torch.float32).fill_(3.0e-3)   # scale 2^(14 - ceil(log2 3e-3)) = 2^23
+        g = bwd._gemm(a, w, T, n, k)
+        ref = torch.empty_like(g)
+        check(_lib.lib().wm3_bw_gelu(ptr(g), n, ptr(pre), n, ptr(b), T, n, s.ptr(), ptr(ref), n, stream_ptr()),
+              "wm3_bw_gelu")
+        out = pre.clone()
+        check(_lib.lib().wm3_linear_gelu_grad(ptr(a), k, ptr(w), k, T, n, k, ptr(out), n, ptr(b), s.ptr(),
+                                              stream_ptr()), "wm3_linear_gelu_grad")
+        torch.testing.assert_close(out, ref, rtol=2e-6, atol=1e-30)
