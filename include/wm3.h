@@ -284,6 +284,7 @@ int wm3_zonal_power(int dtype, const void* field, long long member_stride, int k
  *                     [T][3][heads][dhp] (rotated q, k): the q gradient per query, the k / v gradients per key from
  *                     the inverse neighbor list (inv_off [T + 1], inv_ent [(t, k)] sorted by t); P, dS
  *                     [T][heads][K] and work [T][heads][2K] scratch; gout [T][3][heads][dhp] fp32
+ *   wm3_bw_rope_q     wm3_bw_rope on the q section only (the tensor-core attention backward rotates dK itself)
  *   wm3_bw_rope       in place on the q / k sections of gout: the transpose of the rotary rotation (cos / sin
  *                     [T][dhp / 2] of the interleaved pairs) */
 int wm3_bw_amax(const float* x, int rows, int cols, int ld, unsigned* amax_bits, void* stream);
@@ -302,6 +303,7 @@ int wm3_bw_layernorm(const float* x, int ldx, int rows, int n, float eps, const 
 int wm3_bw_natten(const void* qkv, int ldq, const int64_t* nbr, const int* inv_off, const int* inv_ent, int T, int K,
                   int heads, int dhp, float scale, const float* gctx, int ldc, const unsigned* amax_bits, float* P,
                   float* dS, float* work, float* gout, int ldg, void* stream);
+int wm3_bw_rope_q(float* g, int ldg, int T, int heads, int dhp, const float* cos_t, const float* sin_t, void* stream);
 int wm3_bw_rope(float* g, int ldg, int T, int heads, int dhp, const float* cos_t, const float* sin_t, void* stream);
 
 /* The MLP's GELU backward fused into the gradient GEMM (autodiff.py:372-382 after the W2 matmul VJP :350):
@@ -327,7 +329,9 @@ int wm3_linear_tn(const void* a, int lda, const void* b, int ldb, int m, int n, 
  *   wm3_natten_slot_table  int32 [tiles][maxch][128]: key token of every chunk slot (-1: none), for the CSR
  *                          (csr_off [T + 1], csr_ent = (tile * maxch + chunk) * 128 + slot, by token, fixed order)
  *   wm3_natten_bwd         dQ into gqkv's q section, dK / dV (the CSR-ordered sum of per-chunk partials, partial =
- *                          [tiles * heads][maxch][2][2][64][128] fp32 scratch) into its k / v sections (fp32) */
+ *                          [tiles * heads][maxch][2][2][64][128] fp32 scratch) into its k / v sections (fp32);
+ *                          with rope_cos / rope_sin ([T][dhp / 2] pair tables, or both NULL) dK leaves through the
+ *                          transpose of the rotary rotation (dQ then takes wm3_bw_rope_q) */
 int wm3_natten_fwd_lse(const void* qkv, int ldqkv, void* out, int ldo, int depth, int rows, int cols, int heads, int dhp,
                        int wd, int wh, int ww, float scale, float* lse, void* stream);
 int wm3_bw_na_prep(const void* qkv, int ldq, int T, int heads, int dhp, const float* gctx, int ldc,
@@ -339,8 +343,8 @@ int wm3_natten_slot_table(int depth, int rows, int cols, int heads, int dhp, int
                           void* stream);
 int wm3_natten_bwd(const void* qkv, int ldqkv, const void* dout, int ldd, const void* o, int ldo, const float* lse,
                    float* gqkv, int ldg, float* partial, const int32_t* csr_off, const int32_t* csr_ent,
-                   const float* factors, int depth, int rows, int cols, int heads, int dhp, int wd, int wh, int ww,
-                   float scale, void* stream);
+                   const float* factors, const float* rope_cos, const float* rope_sin, int depth, int rows, int cols,
+                   int heads, int dhp, int wd, int wh, int ww, float scale, void* stream);
 
 /* Debug export of the kernel's own window arithmetic: per token, the (start_d, start_h, col_off)
  * it uses; int32 [T][3]. */

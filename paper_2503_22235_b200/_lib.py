@@ -111,6 +111,7 @@ SIGNATURES = {
     "wm3_bw_colsum_amax": [_vp, _i, _vp, _i, _vp, _vp, _i, _i, _vp, _i, _vp, _vp, _vp, _vp],
     "wm3_bw_layernorm": [_vp, _i, _i, _i, _f, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp],
     "wm3_bw_natten": [_vp, _i, _vp, _vp, _vp, _i, _i, _i, _i, _f, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp],
+    "wm3_bw_rope_q": [_vp, _i, _i, _i, _i, _vp, _vp, _vp],
     "wm3_bw_rope": [_vp, _i, _i, _i, _i, _vp, _vp, _vp],
     "wm3_linear_gelu_grad": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _i, _vp, _vp, _vp],
     "wm3_linear_tn": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _i, _vp],
@@ -118,8 +119,8 @@ SIGNATURES = {
     "wm3_natten_fwd_lse": [_vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _f, _vp, _vp],
     "wm3_natten_bwd_info": [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp],
     "wm3_natten_slot_table": [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp],
-    "wm3_natten_bwd": [_vp, _i, _vp, _i, _vp, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _i,
-                       _f, _vp],
+    "wm3_natten_bwd": [_vp, _i, _vp, _i, _vp, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i,
+                       _i, _i, _f, _vp],
     "wm3_zonal_power": [_i, _vp, _ll, _i, _i, _i, _i, _vp, _vp],
 }
 

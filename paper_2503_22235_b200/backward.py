@@ -319,16 +319,21 @@ def block_vjp_device(xd: torch.Tensor, bw, extents, window, heads: int, dh: int,
     dwo = _gemm_tn(gx1h, ctx, kp, hd, T)
     g_ctx = _gemm(gx1h, wt["w_o"], T, hd, np_)  # x s3
     # ---- attention (query and key sides) and the rotary transpose ----
-    g_qkv = torch.zeros((T, 3 * hd), dtype=torch.float32, device=dev)
+    cs, sn = _rope_pair_tables(extents, dh, dhp, dev)
     if tca is not None:
+        g_qkv = torch.empty((T, 3 * hd), dtype=torch.float32, device=dev)  # every element written below
         # tensor cores: dQ per query tile, dK / dV as deterministic sums of per-chunk partials (natten.cu)
         dout = torch.empty((T, hd), dtype=L.ELEM, device=dev)
         check(L.lib().wm3_bw_na_prep(ptr(qkv), 3 * hd, T, heads, dhp, ptr(g_ctx), hd, s3.ptr(), 1.0 / math.sqrt(dh),
                                      ptr(dout), hd, ptr(tca.maxima), ptr(tca.factors), stream_ptr()), "wm3_bw_na_prep")
         check(L.lib().wm3_natten_bwd(ptr(qkv), 3 * hd, ptr(dout), hd, ptr(ctx), hd, ptr(lse), ptr(g_qkv), 3 * hd,
-                                     ptr(tca.partial), ptr(tca.off), ptr(tca.ent), ptr(tca.factors), *extents, heads,
-                                     dhp, *window, 1.0 / math.sqrt(dh), stream_ptr()), "wm3_natten_bwd")
+                                     ptr(tca.partial), ptr(tca.off), ptr(tca.ent), ptr(tca.factors), ptr(cs), ptr(sn),
+                                     *extents, heads, dhp, *window, 1.0 / math.sqrt(dh), stream_ptr()),
+              "wm3_natten_bwd")  # dK leaves through the rotary transpose (coalesced per key in the reduction)
+        check(L.lib().wm3_bw_rope_q(ptr(g_qkv), 3 * hd, T, heads, dhp, ptr(cs), ptr(sn), stream_ptr()),
+              "wm3_bw_rope_q")
     else:
+        g_qkv = torch.zeros((T, 3 * hd), dtype=torch.float32, device=dev)
         nbr, inv_off, inv_ent, K = _InverseNeighbors.get(extents, window)
         P = torch.empty((T, heads, K), dtype=torch.float32, device=dev)
         dS = torch.empty_like(P)
@@ -336,8 +341,7 @@ def block_vjp_device(xd: torch.Tensor, bw, extents, window, heads: int, dh: int,
         check(L.lib().wm3_bw_natten(ptr(qkv), 3 * hd, ptr(nbr), ptr(inv_off), ptr(inv_ent), T, K, heads, dhp,
                                     1.0 / math.sqrt(dh), ptr(g_ctx), hd, s3.ptr(), ptr(P), ptr(dS), ptr(work),
                                     ptr(g_qkv), 3 * hd, stream_ptr()), "wm3_bw_natten")
-    cs, sn = _rope_pair_tables(extents, dh, dhp, dev)
-    check(L.lib().wm3_bw_rope(ptr(g_qkv), 3 * hd, T, heads, dhp, ptr(cs), ptr(sn), stream_ptr()), "wm3_bw_rope")
+        check(L.lib().wm3_bw_rope(ptr(g_qkv), 3 * hd, T, heads, dhp, ptr(cs), ptr(sn), stream_ptr()), "wm3_bw_rope")
     # ---- QKV ----
     dbqkv, s4 = _colsum_amax(g_qkv, T, 3 * hd)
     gqh = _cast(g_qkv, T, 3 * hd, 3 * hd, scale=s4)

@@ -469,15 +469,15 @@ __global__ void bw_na_key_kernel(const elem_t* __restrict__ qkv, int ldq, const 
 // In place on the q and k sections of g [T][3][heads][dhp]: the transpose of the rotary rotation of the
 // interleaved pairs (2i, 2i + 1) (forward: v0' = v0 c - v1 s, v1' = v0 s + v1 c), cos / sin [T][dhp / 2].
 __global__ void bw_rope_kernel(float* __restrict__ g, int ldg, int T, int heads, int dhp,
-                               const float* __restrict__ cs, const float* __restrict__ sn) {
+                               const float* __restrict__ cs, const float* __restrict__ sn, int sections = 2) {
   const int half = dhp / 2;
-  const long long n = static_cast<long long>(T) * 2 * heads * half;
+  const long long n = static_cast<long long>(T) * sections * heads * half;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int pr = static_cast<int>(i % half);
     long long rest = i / half;
-    const int hs = static_cast<int>(rest % (2 * heads));  // section (q / k) x head
-    const int t = static_cast<int>(rest / (2 * heads));
+    const int hs = static_cast<int>(rest % (sections * heads));  // section (q / k) x head
+    const int t = static_cast<int>(rest / (sections * heads));
     float* p = g + static_cast<size_t>(t) * ldg + static_cast<size_t>(hs) * dhp + 2 * pr;
     const float c = cs[static_cast<size_t>(t) * half + pr], s = sn[static_cast<size_t>(t) * half + pr];
     const float g0 = p[0], g1 = p[1];
@@ -604,6 +604,13 @@ extern "C" int wm3_bw_natten(const void* qkv, int ldq, const int64_t* nbr, const
   bw_na_key_kernel<<<blocks, threads, 0, s>>>(reinterpret_cast<const elem_t*>(qkv), ldq, inv_off, inv_ent, T, K, heads,
                                               dhp, scale, gctx, ldc, amax_bits, P, dS, gout, ldg);
   return check_launch("bw_na_key_kernel");
+}
+
+extern "C" int wm3_bw_rope_q(float* g, int ldg, int T, int heads, int dhp, const float* cos_t, const float* sin_t,
+                             void* stream) {
+  bw_rope_kernel<<<grid_for(static_cast<long long>(T) * heads * dhp / 2, 256), 256, 0,
+                   reinterpret_cast<cudaStream_t>(stream)>>>(g, ldg, T, heads, dhp, cos_t, sin_t, 1);
+  return check_launch("bw_rope_kernel");
 }
 
 extern "C" int wm3_bw_rope(float* g, int ldg, int T, int heads, int dhp, const float* cos_t, const float* sin_t,

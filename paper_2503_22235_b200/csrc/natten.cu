@@ -746,6 +746,11 @@ struct NaBwd {
   const float* factors;  // device: [0] dQ / dK factor (scale / (sigma s)), [1] dV factor (1 / (sigma s))
 };
 
+// transpose of the rotary rotation (attention.py:87-92 backward) on two interleaved pairs (g0, g1), (g2, g3) with pair tables c, s
+DEVI float4 rope_t2(float4 g, float2 c, float2 s) {
+  return make_float4(g.x * c.x + g.y * s.x, -g.x * s.x + g.y * c.x, g.z * c.y + g.w * s.y, -g.z * s.y + g.w * c.y);
+}
+
 constexpr int NB_THREADS = 320;
 constexpr int NB_MMA_WARP = 4, NB_TMA_WARP = 5;  // warps 0-3 softmax, 6-9 partial drain
 constexpr uint32_t NB_Q = 0, NB_DO = 32768, NB_K = 65536, NB_V = 131072, NB_P = 163840, NB_DS = 180224,
@@ -1034,10 +1039,11 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
         tmem_ld_wait();
         if (qvalid) {
 #pragma unroll
-          for (int e = 0; e < 32; e += 4)
+          for (int e = 0; e < 32; e += 4) {
             *reinterpret_cast<float4*>(gq + c0 + e) =
                 make_float4(__uint_as_float(r[e]) * f, __uint_as_float(r[e + 1]) * f, __uint_as_float(r[e + 2]) * f,
                             __uint_as_float(r[e + 3]) * f);
+          }
         }
       }
       tc_fence_before();
@@ -1107,7 +1113,8 @@ __global__ void natten_slot_table_kernel(NaParams p, int32_t* table) {
 // in CSR order (fixed), times the factors; one warp per (token, head), 4 channels per lane.
 __global__ void natten_bwd_reduce_kernel(const float* __restrict__ partial, const int32_t* __restrict__ off,
                                          const int32_t* __restrict__ ent, int T, int heads, int ntiles, int maxch,
-                                         const float* __restrict__ factors, float* __restrict__ gqkv, int ldg) {
+                                         const float* __restrict__ factors, float* __restrict__ gqkv, int ldg,
+                                         const float* __restrict__ rope_cos, const float* __restrict__ rope_sin) {
   constexpr int DHP = 128;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -1129,7 +1136,13 @@ __global__ void natten_bwd_reduce_kernel(const float* __restrict__ partial, cons
   const float fk = __ldg(factors), fv = __ldg(factors + 1);
   float* g = gqkv + static_cast<size_t>(tk) * ldg + h * DHP + 4 * lane;
   const int sec = heads * DHP;
-  *reinterpret_cast<float4*>(g + sec) = make_float4(ak.x * fk, ak.y * fk, ak.z * fk, ak.w * fk);
+  float4 k4 = make_float4(ak.x * fk, ak.y * fk, ak.z * fk, ak.w * fk);
+  if (rope_cos != nullptr) {
+    const size_t pi = static_cast<size_t>(tk) * (DHP / 2) + 2 * lane;
+    k4 = rope_t2(k4, __ldg(reinterpret_cast<const float2*>(rope_cos + pi)),
+                 __ldg(reinterpret_cast<const float2*>(rope_sin + pi)));
+  }
+  *reinterpret_cast<float4*>(g + sec) = k4;
   *reinterpret_cast<float4*>(g + 2 * sec) = make_float4(av.x * fv, av.y * fv, av.z * fv, av.w * fv);
 }
 
@@ -1411,8 +1424,9 @@ extern "C" int wm3_natten_slot_table(int depth, int rows, int cols, int heads, i
 
 extern "C" int wm3_natten_bwd(const void* qkv, int ldqkv, const void* dout, int ldd, const void* o, int ldo,
                               const float* lse, float* gqkv, int ldg, float* partial, const int32_t* csr_off,
-                              const int32_t* csr_ent, const float* factors, int depth, int rows, int cols, int heads,
-                              int dhp, int wd, int wh, int ww, float scale, void* stream) {
+                              const int32_t* csr_ent, const float* factors, const float* rope_cos,
+                              const float* rope_sin, int depth, int rows, int cols, int heads, int dhp, int wd, int wh,
+                              int ww, float scale, void* stream) {
   if (dhp != 128) return set_error("wm3_natten_bwd: head dim must be padded to 128 (got %d)", dhp);
   if ((ldd % 8) || (ldo % 8) || (ldg % 4)) return set_error("wm3_natten_bwd: bad leading dimensions");
   NaParams p;
@@ -1439,6 +1453,7 @@ extern "C" int wm3_natten_bwd(const void* qkv, int ldqkv, const void* dout, int 
   b.ldg = ldg;
   b.partial = partial;
   b.factors = factors;
+  if ((rope_cos == nullptr) != (rope_sin == nullptr)) return set_error("wm3_natten_bwd: give both rotary tables or none");
   if (ensure_smem_attr(reinterpret_cast<const void*>(natten_bwd_kernel<true>), NB_SMEM, "natten_bwd")) return -1;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int grid = p.nitems < sm_count() ? p.nitems : sm_count();
@@ -1447,6 +1462,6 @@ extern "C" int wm3_natten_bwd(const void* qkv, int ldqkv, const void* dout, int 
   const int T = depth * rows * cols;
   const int blocks = (T * heads * 32 + 255) / 256;
   natten_bwd_reduce_kernel<<<blocks, 256, 0, s>>>(partial, csr_off, csr_ent, T, heads, p.ntd * p.nth * p.ntw,
-                                                  p.maxch, factors, gqkv, ldg);
+                                                  p.maxch, factors, gqkv, ldg, rope_cos, rope_sin);
   return check_launch("natten_bwd_reduce_kernel");
 }
