@@ -279,7 +279,7 @@ int wm3_zonal_power(int dtype, const void* field, long long member_stride, int k
  *                     max |v|, v = g; with a != NULL, v = g / scale(in_scale_bits) * gelu'(a + bias) is also
  *                     stored to out (the GELU backward, its bias gradient and the next operand scale at once)
  *   wm3_bw_layernorm  gx = LayerNorm-backward(x, gamma, g / scale) (+ add); gxh = g / scale * xhat; gsc = g / scale
- *                     (autodiff.py:400-424: mean, biased variance, eps)
+ *                     (autodiff.py:400-424: mean, biased variance, eps); gsc may be NULL
  *   wm3_bw_natten     attention backward over the neighbor table nbr [T][K] (grid.py K order) of the 16-bit qkv
  *                     [T][3][heads][dhp] (rotated q, k): the q gradient per query, the k / v gradients per key from
  *                     the inverse neighbor list (inv_off [T + 1], inv_ent [(t, k)] sorted by t); P, dS

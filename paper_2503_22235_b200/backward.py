@@ -116,11 +116,11 @@ def _layernorm_backward(x: torch.Tensor, gamma: torch.Tensor, g: torch.Tensor, s
     dev = x.device
     gx = torch.empty((T, D), dtype=torch.float32, device=dev)
     gxh = torch.empty_like(gx)
-    gsc = torch.empty_like(gx)
     check(_lib.lib().wm3_bw_layernorm(ptr(x), x.stride(0), T, D, LN_EPS, ptr(gamma), ptr(g), g.stride(0),
-                                      scale.ptr(), ptr(add), ptr(gx), ptr(gxh), ptr(gsc), stream_ptr()),
+                                      scale.ptr(), ptr(add), ptr(gx), ptr(gxh), None, stream_ptr()),
           "wm3_bw_layernorm")
-    return gx, _colsum(gxh, T, D), _colsum(gsc, T, D)
+    # the bias gradient is the column sum of g / scale itself: no [T][D] copy of it
+    return gx, _colsum(gxh, T, D), _colsum(g, T, D, scale=scale)
 
 
 def _gemm_tn(a: torch.Tensor, b: torch.Tensor, m: int, n: int, k: int) -> torch.Tensor:

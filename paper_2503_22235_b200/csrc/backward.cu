@@ -356,7 +356,7 @@ __global__ void bw_layernorm_kernel(const float* __restrict__ x, int ldx, int ro
     const float gh = gu * gamma[c];
     gx[o] = rstd * (gh - a1 - xh * a2) + (add != nullptr ? add[o] : 0.f);
     gxh[o] = gu * xh;
-    gsc[o] = gu;
+    if (gsc != nullptr) gsc[o] = gu;
   }
 }
 
