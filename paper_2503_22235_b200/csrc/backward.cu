@@ -471,6 +471,23 @@ __global__ void bw_na_key_kernel(const elem_t* __restrict__ qkv, int ldq, const 
 __global__ void bw_rope_kernel(float* __restrict__ g, int ldg, int T, int heads, int dhp,
                                const float* __restrict__ cs, const float* __restrict__ sn, int sections = 2) {
   const int half = dhp / 2;
+  if (ldg % 4 == 0 && dhp % 4 == 0) {  // row strips, two pairs per thread-step (16-byte I/O)
+    const int w = sections * heads * dhp;
+    for (int t = blockIdx.x; t < T; t += gridDim.x) {
+      float* gr = g + static_cast<size_t>(t) * ldg;
+      const float* ct = cs + static_cast<size_t>(t) * half;
+      const float* st = sn + static_cast<size_t>(t) * half;
+      for (int c = 4 * threadIdx.x; c < w; c += 4 * blockDim.x) {
+        const int pr = (c % dhp) >> 1;
+        const float4 v = *reinterpret_cast<const float4*>(gr + c);
+        const float2 cc = __ldg(reinterpret_cast<const float2*>(ct + pr));
+        const float2 ss = __ldg(reinterpret_cast<const float2*>(st + pr));
+        *reinterpret_cast<float4*>(gr + c) = make_float4(v.x * cc.x + v.y * ss.x, -v.x * ss.x + v.y * cc.x,
+                                                         v.z * cc.y + v.w * ss.y, -v.z * ss.y + v.w * cc.y);
+      }
+    }
+    return;
+  }
   const long long n = static_cast<long long>(T) * sections * heads * half;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -608,8 +625,8 @@ extern "C" int wm3_bw_natten(const void* qkv, int ldq, const int64_t* nbr, const
 
 extern "C" int wm3_bw_rope_q(float* g, int ldg, int T, int heads, int dhp, const float* cos_t, const float* sin_t,
                              void* stream) {
-  bw_rope_kernel<<<grid_for(static_cast<long long>(T) * heads * dhp / 2, 256), 256, 0,
-                   reinterpret_cast<cudaStream_t>(stream)>>>(g, ldg, T, heads, dhp, cos_t, sin_t, 1);
+  bw_rope_kernel<<<T < 148 * 8 ? T : 148 * 8, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(g, ldg, T, heads, dhp,
+                                                                                               cos_t, sin_t, 1);
   return check_launch("bw_rope_kernel");
 }
 
@@ -665,6 +682,20 @@ __global__ void bw_na_prep_scale_kernel(const float* __restrict__ gctx, int ldc,
     factors[0] = scale / (sigma * s);
     factors[1] = 1.f / (sigma * s);
   }
+  if (cols % 8 == 0 && ldc % 4 == 0 && ldd % 8 == 0) {  // row strips, 8 elements per thread-step (16-byte I/O)
+    for (int t = blockIdx.x; t < T; t += gridDim.x) {
+      const float* gr = gctx + static_cast<size_t>(t) * ldc;
+      elem_t* dr = dout + static_cast<size_t>(t) * ldd;
+      for (int c = 8 * threadIdx.x; c < cols; c += 8 * blockDim.x) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(gr + c));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(gr + c + 4));
+        *reinterpret_cast<uint4*>(dr + c) =
+            make_uint4(pack_elem(a.x * sigma, a.y * sigma), pack_elem(a.z * sigma, a.w * sigma),
+                       pack_elem(b.x * sigma, b.y * sigma), pack_elem(b.z * sigma, b.w * sigma));
+      }
+    }
+    return;
+  }
   const long long n = static_cast<long long>(T) * cols;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -681,7 +712,7 @@ extern "C" int wm3_bw_na_prep(const void* qkv, int ldq, int T, int heads, int dh
   bw_na_prep_reduce_kernel<<<148 * 8, 256, 0, s>>>(
       reinterpret_cast<const elem_t*>(qkv), ldq, T, heads, dhp, gctx, ldc, maxima);
   if (check_launch("bw_na_prep_reduce_kernel")) return -1;
-  bw_na_prep_scale_kernel<<<grid_for(static_cast<long long>(T) * heads * dhp, 256), 256, 0, s>>>(
+  bw_na_prep_scale_kernel<<<T < 148 * 8 ? T : 148 * 8, 128, 0, s>>>(
       gctx, ldc, T, heads * dhp, maxima, gscale_bits, scale, reinterpret_cast<elem_t*>(dout), ldd, factors);
   return check_launch("bw_na_prep_scale_kernel");
 }
