@@ -317,6 +317,11 @@ int wm3_linear_gelu_grad(const void* a, int lda, const void* b, int ldb, int m, 
  * of 64. */
 int wm3_linear_tn(const void* a, int lda, const void* b, int ldb, int m, int n, int k, float* out, int ldo,
                   void* stream);
+/* wm3_linear_tn with the K range split over CTA pairs when the output has too few 256 x 256 tiles to fill the GPU
+ * (the split count minimises tile waves per split, <= 16, >= 8 k-blocks per split, sp * m * n <= scratch_floats):
+ * per-split fp32 partials in scratch, then summed in split order (deterministic).  NULL scratch = no split. */
+int wm3_linear_tn_split(const void* a, int lda, const void* b, int ldb, int m, int n, int k, float* out, int ldo,
+                        float* scratch, size_t scratch_floats, void* stream);
 
 /* Attention backward on the tensor cores (replaces wm3_bw_natten when wm3_natten_bwd_info reports support: head
  * dim padded to 128, window mask in the MMA).  Same reference rules (attention.py:173-178 through autodiff.py's

@@ -31,6 +31,7 @@ _vp = ctypes.c_void_p
 _i = ctypes.c_int
 _f = ctypes.c_float
 _ll = ctypes.c_longlong
+_sz = ctypes.c_size_t
 
 
 class RopeT(ctypes.Structure):
@@ -114,6 +115,7 @@ SIGNATURES = {
     "wm3_bw_rope_q": [_vp, _i, _i, _i, _i, _vp, _vp, _vp],
     "wm3_bw_rope": [_vp, _i, _i, _i, _i, _vp, _vp, _vp],
     "wm3_linear_gelu_grad": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _i, _vp, _vp, _vp],
+    "wm3_linear_tn_split": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _i, _vp, _sz, _vp],
     "wm3_linear_tn": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _i, _vp],
     "wm3_bw_na_prep": [_vp, _i, _i, _i, _i, _vp, _i, _vp, _f, _vp, _i, _vp, _vp, _vp],
     "wm3_natten_fwd_lse": [_vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _f, _vp, _vp],

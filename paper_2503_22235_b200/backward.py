@@ -125,10 +125,13 @@ def _layernorm_backward(x: torch.Tensor, gamma: torch.Tensor, g: torch.Tensor, s
 
 def _gemm_tn(a: torch.Tensor, b: torch.Tensor, m: int, n: int, k: int) -> torch.Tensor:
     """fp32 C[m][n] = sum_t A[t][:m] B[t][:n] over k rows (the weight gradients over tokens): MN-major tcgen05
-    operands straight from the row-major 16-bit tensors, no transposed copies."""
+    operands straight from the row-major 16-bit tensors, no transposed copies; the token range split over the CTA
+    pairs when the weight has few output tiles (deterministic ordered sum of the partials)."""
     out = torch.empty((m, n), dtype=torch.float32, device=a.device)
-    check(_lib.lib().wm3_linear_tn(ptr(a), a.stride(0), ptr(b), b.stride(0), m, n, k, ptr(out), out.stride(0),
-                                   stream_ptr()), "wm3_linear_tn")
+    # split-K scratch (the library picks the split count; <= 16 partial planes of the output)
+    scratch = torch.empty(16 * m * n, dtype=torch.float32, device=a.device)
+    check(_lib.lib().wm3_linear_tn_split(ptr(a), a.stride(0), ptr(b), b.stride(0), m, n, k, ptr(out), out.stride(0),
+                                         ptr(scratch), scratch.numel(), stream_ptr()), "wm3_linear_tn_split")
     return out
 
 

@@ -40,6 +40,7 @@ struct EpiParams {
   int ln_prod, ln_cons;
   int mn;  // operands MN-major (wm3_linear_tn: C = A^T B with A [K][M], B [K][N] row-major, 64 x 64 boxes)
   const unsigned* gscale;  // WM3_EPI_GELU_GRAD_F32: amax bits of the output gradient's operand scale
+  int ksplit;  // > 1: split-K — output plane p = the partial product over k-block range p (A rows = plane rows)
 };
 
 // epilogues that read the fp32 output buffer before overwriting it (the residual stream, or the stored GELU
@@ -264,9 +265,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0;
       for (int tile = tile0; tile < ntiles; tile += tstep) {
         int plane, r0;
-        const int m0 = tile_rows(tile, plane, r0);
+        const int mrow = tile_rows(tile, plane, r0);
+        const int m0 = ep.ksplit > 1 ? r0 : mrow;  // split-K: every plane reads the same A rows
         const int n0 = (tile % nn) * BN + static_cast<int>(rank) * (BN / CG);
-        for (int kb = 0; kb < nk; ++kb) {
+        const int kb0 = ep.ksplit > 1 ? plane * nk / ep.ksplit : 0;
+        const int kb1 = ep.ksplit > 1 ? (plane + 1) * nk / ep.ksplit : nk;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sa = sbase + stage * Cfg::STAGE_BYTES;
           const uint32_t sb = sa + Cfg::A_BYTES;
@@ -314,7 +318,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_wait(tempty_bar(acc), aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < nk; ++kb) {
+        int kb0 = 0, kb1 = nk;
+        if (ep.ksplit > 1) {
+          int plane, r0;
+          tile_rows(tile, plane, r0);
+          kb0 = plane * nk / ep.ksplit;
+          kb1 = (plane + 1) * nk / ep.ksplit;
+        }
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(full_bar(stage), phase);
           tc_fence_after();
           const uint64_t ad = d0 + ((stage * Cfg::STAGE_BYTES) >> 4), bd = ad + (Cfg::A_BYTES >> 4);
@@ -322,9 +333,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
             for (int k = 0; k < GEMM_BK / 16; ++k) {
               if (CG == 2)
-                umma_ss_cg2(d_tmem, ad + kstep * k, bd + kstep * k, idesc, (kb | k) != 0 ? 1u : 0u);
+                umma_ss_cg2(d_tmem, ad + kstep * k, bd + kstep * k, idesc, ((kb - kb0) | k) != 0 ? 1u : 0u);
               else
-                umma_bf16_ss(d_tmem, ad + kstep * k, bd + kstep * k, idesc, (kb | k) != 0 ? 1u : 0u);
+                umma_bf16_ss(d_tmem, ad + kstep * k, bd + kstep * k, idesc, ((kb - kb0) | k) != 0 ? 1u : 0u);
             }
             if (CG == 2)
               umma_commit_mc(empty_bar(stage), 0x3);  // frees the stage in both CTAs
@@ -669,7 +680,7 @@ struct OutPlanes {
 static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi, void* out,
                        int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, const OutPlanes& op,
                        void* stream, const wm3_halo_t* halo = nullptr, const wm3_ln_fold_t* fold = nullptr,
-                       bool mn = false, const unsigned* gscale = nullptr) {
+                       bool mn = false, const unsigned* gscale = nullptr, int ksplit = 1) {
   if (m <= 0 || n <= 0 || k <= 0) return set_error("wm3_linear: bad sizes m=%d n=%d k=%d", m, n, k);
   const bool f32_out = (epi == WM3_EPI_F32 || epi_reads_out(epi));
   if ((lda % 8) || (ldb % 8) || (ldo % (f32_out ? 4 : 8)))
@@ -697,6 +708,9 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
   ep.resid_v8 = (ldo % 8 == 0) && (reinterpret_cast<uintptr_t>(out) % 32 == 0);
   ep.bias = bias;
   ep.gscale = gscale;
+  ep.ksplit = ksplit;
+  if (ksplit > 1 && (epi != WM3_EPI_F32 || op.planes != ksplit || op.row_off != 0 || (k + GEMM_BK - 1) / GEMM_BK < ksplit))
+    return set_error("wm3_linear: bad split-K (%d splits, %d planes, k=%d)", ksplit, op.planes, k);
   ep.n_valid = n_valid;
   ep.plane_rows = op.plane_rows;
   ep.planes = op.planes;
@@ -740,11 +754,12 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
   }
   CUtensorMap ta, tb, to;
   ep.mn = mn ? 1 : 0;
+  const int am = ksplit > 1 ? op.plane_rows : m;  // split-K: every output plane reads the same A rows
   if (mn) {  // A [k][m], B [k][n] row-major: 64 x 64 boxes (M / N inner)
-    if (make_tmap_2d_bf16(&ta, a, m, k, lda, 64, GEMM_BK)) return -1;
+    if (make_tmap_2d_bf16(&ta, a, am, k, lda, 64, GEMM_BK)) return -1;
     if (make_tmap_2d_bf16(&tb, b, n, k, ldb, 64, GEMM_BK)) return -1;
   } else {
-    if (make_tmap_2d_bf16(&ta, a, k, m, lda, GEMM_BK, GEMM_BM)) return -1;
+    if (make_tmap_2d_bf16(&ta, a, k, am, lda, GEMM_BK, GEMM_BM)) return -1;
     if (make_tmap_2d_bf16(&tb, b, k, n, ldb, GEMM_BK, bn / cg)) return -1;  // each CTA of a pair loads half
   }
   {
@@ -839,6 +854,62 @@ extern "C" int wm3_halo_wait(const int* flags, int n, int epoch, void* stream) {
 
 // C[m][n] (fp32) = sum_t A[t][m] B[t][n]: both operands row-major over the reduction axis (the backward's
 // weight gradients over tokens, autodiff.py:350 matmul VJP), read as MN-major tiles: no transposed copies.
+namespace wm3 {
+// out[r][c] = sum over s = 0 .. splits-1 in order of part[s][r][c] (split-K partials, [splits][m][n] dense)
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits, int m, int n, float* __restrict__ out,
+                                     int ldo) {
+  const size_t plane = static_cast<size_t>(m) * n;
+  const int n4 = n / 4;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < static_cast<size_t>(m) * n4;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = i / n4, c = 4 * (i - r * n4);
+    float4 acc = __ldg(reinterpret_cast<const float4*>(part + r * n + c));
+    for (int sp = 1; sp < splits; ++sp) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(part + sp * plane + r * n + c));
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    *reinterpret_cast<float4*>(out + r * ldo + c) = acc;
+  }
+}
+}  // namespace wm3
+
+// Splits of the K range for an MN-major C = A^T B of m x n on CTA-pair tiles of 256 x 256: the count in [1, 16]
+// that minimises (waves of tiles x splits over the pairs) / splits — the long-K weight gradients (K = tokens)
+// have few output tiles (16 for a 1024 x 1024 weight: 22 % of the pairs) — limited by the scratch and by >= 8
+// k-blocks per split.
+static int choose_ksplit(int m, int n, int k, size_t scratch_floats) {
+  const int pairs = sm_count() / 2;
+  const int tiles = ((m + 255) / 256) * ((n + 255) / 256);
+  const int nk = (k + GEMM_BK - 1) / GEMM_BK;
+  int best = 1;
+  double best_t = static_cast<double>((tiles + pairs - 1) / pairs);
+  for (int sp = 2; sp <= 16; ++sp) {
+    if (nk / sp < 8 || static_cast<size_t>(sp) * m * n > scratch_floats) break;
+    const double t = static_cast<double>((tiles * sp + pairs - 1) / pairs) / sp + 0.02;  // + reduce pass
+    if (t < best_t) { best_t = t; best = sp; }
+  }
+  return best;
+}
+
+extern "C" int wm3_linear_tn_split(const void* a, int lda, const void* b, int ldb, int m, int n, int k, float* out,
+                                   int ldo, float* scratch, size_t scratch_floats, void* stream) {
+  if ((m % 64) || (n % 64)) return set_error("wm3_linear_tn_split: m=%d and n=%d must be multiples of 64", m, n);
+  const int sp = scratch != nullptr ? choose_ksplit(m, n, k, scratch_floats) : 1;
+  if (sp == 1) {
+    const OutPlanes op{1, m, m, 0};
+    return linear_impl(a, lda, b, ldb, m, n, k, WM3_EPI_F32, out, ldo, n, nullptr, nullptr, op, stream, nullptr,
+                       nullptr, true);
+  }
+  const OutPlanes op{sp, m, m, 0};
+  if (linear_impl(a, lda, b, ldb, sp * m, n, k, WM3_EPI_F32, scratch, n, n, nullptr, nullptr, op, stream, nullptr,
+                  nullptr, true, nullptr, sp))
+    return -1;
+  const long long n4 = static_cast<long long>(m) * n / 4;
+  const int blocks = static_cast<int>(n4 / 256 + 1 < 148 * 8 ? n4 / 256 + 1 : 148 * 8);
+  splitk_reduce_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(scratch, sp, m, n, out, ldo);
+  return check_launch("splitk_reduce_kernel");
+}
+
 extern "C" int wm3_linear_tn(const void* a, int lda, const void* b, int ldb, int m, int n, int k, float* out, int ldo,
                              void* stream) {
   if ((m % 64) || (n % 64)) return set_error("wm3_linear_tn: m=%d and n=%d must be multiples of 64", m, n);

@@ -337,3 +337,22 @@ def test_gelu_grad_gemm_epilogue():
         check(_lib.lib().wm3_linear_gelu_grad(ptr(a), k, ptr(w), k, T, n, k, ptr(out), n, ptr(b), s.ptr(),
                                               stream_ptr()), "wm3_linear_gelu_grad")
         torch.testing.assert_close(out, ref, rtol=2e-6, atol=1e-30)
+
+
+@pytest.mark.parametrize("m,n,k", [(256, 256, 20000), (1024, 1024, 81000), (3072, 1024, 5000), (128, 192, 700)])
+def test_linear_tn_split_k(m, n, k):
+    """wm3_linear_tn_split (weight-gradient GEMM C = A^T B over the token axis, K range split over the CTA pairs
+    when the output has few tiles): equal to the fp64 product within fp32 accumulation error, and run-to-run
+    bitwise (the split partials are summed in a fixed order)."""
+    import torch
+    from paper_2503_22235_b200 import _lib
+    from paper_2503_22235_b200 import backward as bwd
+    torch.manual_seed(m + k)
+    a = torch.randn(k, m, device="cuda").to(_lib.ELEM)
+    b = torch.randn(k, n, device="cuda").to(_lib.ELEM)
+    c = bwd._gemm_tn(a, b, m, n, k)
+    ref = a.double().T @ b.double()
+    err = float((c.double() - ref).norm() / ref.norm())
+    print(f"linear_tn_split {m}x{n}x{k}: rel err {err:.2e}")
+    assert err < 2e-6 * max(1.0, (k / 1000) ** 0.5), err  # fp32 accumulation over k terms
+    assert torch.equal(c, bwd._gemm_tn(a, b, m, n, k))
