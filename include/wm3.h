@@ -322,6 +322,9 @@ int wm3_linear_tn(const void* a, int lda, const void* b, int ldb, int m, int n, 
  * per-split fp32 partials in scratch, then summed in split order (deterministic).  NULL scratch = no split. */
 int wm3_linear_tn_split(const void* a, int lda, const void* b, int ldb, int m, int n, int k, float* out, int ldo,
                         float* scratch, size_t scratch_floats, void* stream);
+/* the split count wm3_linear_tn_split picks for m x n x k with unlimited scratch (size the scratch as count * m * n
+ * floats; 1 = no split, no scratch needed) */
+int wm3_linear_tn_split_count(int m, int n, int k);
 
 /* Attention backward on the tensor cores (replaces wm3_bw_natten when wm3_natten_bwd_info reports support: head
  * dim padded to 128, window mask in the MMA).  Same reference rules (attention.py:173-178 through autodiff.py's

@@ -115,6 +115,7 @@ SIGNATURES = {
     "wm3_bw_rope_q": [_vp, _i, _i, _i, _i, _vp, _vp, _vp],
     "wm3_bw_rope": [_vp, _i, _i, _i, _i, _vp, _vp, _vp],
     "wm3_linear_gelu_grad": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _i, _vp, _vp, _vp],
+    "wm3_linear_tn_split_count": [_i, _i, _i],
     "wm3_linear_tn_split": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _i, _vp, _sz, _vp],
     "wm3_linear_tn": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _i, _vp],
     "wm3_bw_na_prep": [_vp, _i, _i, _i, _i, _vp, _i, _vp, _f, _vp, _i, _vp, _vp, _vp],

@@ -128,10 +128,11 @@ def _gemm_tn(a: torch.Tensor, b: torch.Tensor, m: int, n: int, k: int) -> torch.
     operands straight from the row-major 16-bit tensors, no transposed copies; the token range split over the CTA
     pairs when the weight has few output tiles (deterministic ordered sum of the partials)."""
     out = torch.empty((m, n), dtype=torch.float32, device=a.device)
-    # split-K scratch (the library picks the split count; <= 16 partial planes of the output)
-    scratch = torch.empty(16 * m * n, dtype=torch.float32, device=a.device)
+    sp = _lib.lib().wm3_linear_tn_split_count(m, n, k)  # split-K partial planes the library will use
+    scratch = torch.empty(sp * m * n, dtype=torch.float32, device=a.device) if sp > 1 else None
     check(_lib.lib().wm3_linear_tn_split(ptr(a), a.stride(0), ptr(b), b.stride(0), m, n, k, ptr(out), out.stride(0),
-                                         ptr(scratch), scratch.numel(), stream_ptr()), "wm3_linear_tn_split")
+                                         ptr(scratch), 0 if scratch is None else scratch.numel(), stream_ptr()),
+          "wm3_linear_tn_split")
     return out
 
 

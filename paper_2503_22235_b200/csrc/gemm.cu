@@ -891,6 +891,10 @@ static int choose_ksplit(int m, int n, int k, size_t scratch_floats) {
   return best;
 }
 
+extern "C" int wm3_linear_tn_split_count(int m, int n, int k) {
+  return choose_ksplit(m, n, k, static_cast<size_t>(-1));
+}
+
 extern "C" int wm3_linear_tn_split(const void* a, int lda, const void* b, int ldb, int m, int n, int k, float* out,
                                    int ldo, float* scratch, size_t scratch_floats, void* stream) {
   if ((m % 64) || (n % 64)) return set_error("wm3_linear_tn_split: m=%d and n=%d must be multiples of 64", m, n);
