@@ -325,10 +325,23 @@ class BandedProcessor:
         d, h, w = cfg.latent_extents
         self.rope = CACHE.rope(cfg.latent_extents, cfg.head_dim)
         self.local = [(d, b.rows, w) for b in self.held]
-        self.interior = [interior_rows(b, h, cfg.window[1]) for b in self.held]
+        self.interior = [interior_rows(b, h, cfg.window[1]) if self._split_na(b) else (b.row0, b.row0)
+                         for b in self.held]
         self._bufs = None
         self._graphs: dict = {}
         self.timing = None  # optional callback(name) between phases (bench: CUDA events per phase)
+
+    @staticmethod
+    def _split_na(band: Band) -> bool:
+        """Split this band's attention into interior rows (run while the halo exchange is in flight) and
+        boundary rows (after it)?  WM3_NA_SPLIT=1 / 0 forces it; by default only bands of >= 40 rows split:
+        each extra launch covers whole 5-row query tiles for a few rows, which on a narrow band costs more than
+        the exchange it hides (tools/band_projection.py)."""
+        import os
+        env = os.environ.get("WM3_NA_SPLIT")
+        if env in ("0", "1"):
+            return env == "1"
+        return band.rows >= 40
 
     def _ws(self, bw):
         from .runtime import CACHE
