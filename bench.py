@@ -513,8 +513,8 @@ def run_gpu(args, world, rank, local_rank):
     params, bw, me, local, ws, rope, exch, x = block_setup(world, rank)
     stream = torch.cuda.current_stream()
     if world > 1:
-        # the banded block as the forecast runs it: BandedProcessor (attention split by query rows, the interior
-        # rows overlapping the NCCL halo exchange), with CUDA events between its phases
+        # the banded block as the forecast runs it: BandedProcessor (on bands of >= 40 rows the attention is split
+        # by query rows, the interior rows overlapping the NCCL halo exchange), with CUDA events between its phases
         from paper_2503_22235_b200.bands import BandedProcessor, plan_bands
         from paper_2503_22235_b200.model import full_scale_config
         cfg = full_scale_config()
@@ -656,8 +656,7 @@ def run_gpu(args, world, rank, local_rank):
             bwd = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     n_launch = 7
     if world > 1:  # LN1, QKV, O-proj, LN2, W1, W2 + the attention launches of the row split
-        from paper_2503_22235_b200.bands import interior_rows
-        a_, z_ = interior_rows(me, EXT[1], WIN[1])
+        a_, z_ = proc.interior[0]  # (row0, row0) when the band's attention runs as one launch
         n_launch = 6 + ((z_ > a_) + (a_ > me.row0) + (z_ < me.row0 + me.rows) if z_ > a_ else 1)
     if rank == 0:
         cpu = None
