@@ -725,6 +725,22 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
   // in by TMA (0.195 vs 0.204 ms isolated)
   const int cg = (bn == 256 && cg_env == 2) ? 2 : 1;
   ep.tiles_per_plane = (op.plane_rows + GEMM_BM * cg - 1) / (GEMM_BM * cg);
+  // Narrow pair tiles (256 x 128) when the 256 x 256 tiles leave most of their last wave idle: a latitude band's
+  // 1024-wide GEMMs at 8 GPUs have 156 tiles for 74 pairs (3 rounds for 2.1 waves; 256 x 128: 5 rounds of half
+  // the work).  Same per-element MMA / epilogue arithmetic, so results do not depend on the choice.
+  // WM3_GEMM_NARROW=0 never, 2 always (A/B, tests).
+  static const int narrow_env = [] {
+    const char* e = getenv("WM3_GEMM_NARROW");
+    return e ? atoi(e) : 1;
+  }();
+  bool narrow = false;
+  if (cg == 2 && narrow_env != 0 && fold == nullptr && !mn && ksplit == 1) {
+    const long long mt = static_cast<long long>(op.planes) * ep.tiles_per_plane;
+    const long long pairs = sm_count() / 2;
+    const long long r256 = (mt * ((n + 255) / 256) + pairs - 1) / pairs;
+    const long long r128 = (mt * ((n + 127) / 128) + pairs - 1) / pairs;
+    narrow = narrow_env == 2 || static_cast<double>(r128) * 0.5 * 1.08 < static_cast<double>(r256);
+  }
   if (halo != nullptr) {
     if (epi != WM3_EPI_QKV_ROPE) return set_error("wm3_linear: halo stores need the QKV epilogue");
     if ((halo->ld % 16) || (halo->col_lo % 64) || halo->n_up < 0 || halo->n_dn < 0 ||
@@ -760,7 +776,7 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
     if (make_tmap_2d_bf16(&tb, b, n, k, ldb, 64, GEMM_BK)) return -1;
   } else {
     if (make_tmap_2d_bf16(&ta, a, k, am, lda, GEMM_BK, GEMM_BM)) return -1;
-    if (make_tmap_2d_bf16(&tb, b, k, n, ldb, GEMM_BK, bn / cg)) return -1;  // each CTA of a pair loads half
+    if (make_tmap_2d_bf16(&tb, b, k, n, ldb, GEMM_BK, (narrow ? 128 : bn) / cg)) return -1;  // each CTA of a pair loads half
   }
   {
     const int cw = f32_out ? 32 : 64;
@@ -773,6 +789,7 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
     if (make_tmap(&to, base, f32_out ? TMAP_F32 : TMAP_BF16, 3, dims, strides, box, nullptr)) return -1;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (narrow) return dispatch_epi<128, 2>(epi, ta, tb, to, m, n, k, ep, s);
   if (bn == 256)
     return cg == 2 ? dispatch_epi<256, 2>(epi, ta, tb, to, m, n, k, ep, s)
                    : dispatch_epi<256, 1>(epi, ta, tb, to, m, n, k, ep, s);
