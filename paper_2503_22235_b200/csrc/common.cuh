@@ -223,6 +223,13 @@ DEVI uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
 DEVI void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// The accumulator hand-back of the CTA-pair epilogues (TMEM free for the leader's next MMAs): relaxed, because
+// the only thing it orders is TMEM reads that tcgen05.wait::ld already completed (+ fence::before_thread_sync);
+// the release form compiles to MEMBAR.ALL.GPU, which stalls the arriving lane until its own global stores of
+// the tile are acknowledged.
+DEVI void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 // TMA load into this CTA's smem whose completion bytes count on the leader CTA's mbarrier (cluster address)
 DEVI void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* m, uint32_t bar_cluster, int c0, int c1) {
   asm volatile(

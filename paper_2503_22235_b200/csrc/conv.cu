@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (CG == 2) mbar_arrive_cluster(tempty_leader0 + 8u * acc);  // the leader's MMA warp reuses it
+        if (CG == 2) mbar_arrive_cluster_relaxed(tempty_leader0 + 8u * acc);  // the leader's MMA warp reuses it
         else mbar_arrive(tempty_bar(acc));
       }
       acc ^= 1;

@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       __syncwarp();
       if (lane == 0) {
         if (CG == 2)
-          mbar_arrive_cluster(tempty_leader0 + 8u * acc);  // the leader's MMA thread reuses the accumulator
+          mbar_arrive_cluster_relaxed(tempty_leader0 + 8u * acc);  // the leader's MMA thread reuses the accumulator
         else
           mbar_arrive(tempty_bar(acc));
       }
