@@ -279,12 +279,16 @@ int wm3_zonal_power(int dtype, const void* field, long long member_stride, int k
  *                     max |v|, v = g; with a != NULL, v = g / scale(in_scale_bits) * gelu'(a + bias) is also
  *                     stored to out (the GELU backward, its bias gradient and the next operand scale at once)
  *   wm3_bw_layernorm  gx = LayerNorm-backward(x, gamma, g / scale) (+ add); gxh = g / scale * xhat; gsc = g / scale
- *                     (autodiff.py:400-424: mean, biased variance, eps); gsc may be NULL
+ *                     (autodiff.py:400-424: mean, biased variance, eps); gsc may be NULL; gx_amax (or NULL): atomicMax
+ *                     of max |gx| (the producer leaves the next cast's scale: no separate amax pass)
+ *   wm3_bw_cast_colsum  one pass: dst = operand(src * scale(amax_bits)) [rows][ldd] (columns >= cols zero) and
+ *                     colsum[c] = sum_r src[r][c] (fixed order; partial: ceil(rows / 256) * cols floats)
  *   wm3_bw_natten     attention backward over the neighbor table nbr [T][K] (grid.py K order) of the 16-bit qkv
  *                     [T][3][heads][dhp] (rotated q, k): the q gradient per query, the k / v gradients per key from
  *                     the inverse neighbor list (inv_off [T + 1], inv_ent [(t, k)] sorted by t); P, dS
  *                     [T][heads][K] and work [T][heads][2K] scratch; gout [T][3][heads][dhp] fp32
- *   wm3_bw_rope_q     wm3_bw_rope on the q section only (the tensor-core attention backward rotates dK itself)
+ *   wm3_bw_rope_q     wm3_bw_rope on the q section only (the tensor-core attention backward rotates dK itself);
+ *                     amax (or NULL): atomicMax of the rotated values' max |.|
  *   wm3_bw_rope       in place on the q / k sections of gout: the transpose of the rotary rotation (cos / sin
  *                     [T][dhp / 2] of the interleaved pairs) */
 int wm3_bw_amax(const float* x, int rows, int cols, int ld, unsigned* amax_bits, void* stream);
@@ -299,18 +303,23 @@ int wm3_bw_colsum_amax(const float* g, int ldg, const float* a, int lda, const f
                        const unsigned* in_scale_bits, int rows, int cols, float* out, int ldo, float* partial,
                        float* colsum, unsigned* amax_bits, void* stream);
 int wm3_bw_layernorm(const float* x, int ldx, int rows, int n, float eps, const float* gamma, const float* g, int ldg,
-                     const unsigned* amax_bits, const float* add, float* gx, float* gxh, float* gsc, void* stream);
+                     const unsigned* amax_bits, const float* add, float* gx, float* gxh, float* gsc, unsigned* gx_amax,
+                     void* stream);
 int wm3_bw_natten(const void* qkv, int ldq, const int64_t* nbr, const int* inv_off, const int* inv_ent, int T, int K,
                   int heads, int dhp, float scale, const float* gctx, int ldc, const unsigned* amax_bits, float* P,
                   float* dS, float* work, float* gout, int ldg, void* stream);
-int wm3_bw_rope_q(float* g, int ldg, int T, int heads, int dhp, const float* cos_t, const float* sin_t, void* stream);
+int wm3_bw_rope_q(float* g, int ldg, int T, int heads, int dhp, const float* cos_t, const float* sin_t, unsigned* amax,
+                  void* stream);
+int wm3_bw_cast_colsum(const float* src, int rows, int cols, int lds, void* dst, int ldd, const unsigned* amax_bits,
+                       float* partial, float* colsum, void* stream);
 int wm3_bw_rope(float* g, int ldg, int T, int heads, int dhp, const float* cos_t, const float* sin_t, void* stream);
 
 /* The MLP's GELU backward fused into the gradient GEMM (autodiff.py:372-382 after the W2 matmul VJP :350):
  * preact_inout [m][n] fp32 holds the W1 pre-activation without bias on entry and
- * (A . B^T) / scale(amax_bits) * gelu'(preact + bias) on exit (the residual epilogue's in-place read-then-write). */
+ * (A . B^T) / scale(amax_bits) * gelu'(preact + bias) on exit (the residual epilogue's in-place read-then-write);
+ * out_amax_bits (or NULL): atomicMax of the result's max |.| (zeroed by the caller). */
 int wm3_linear_gelu_grad(const void* a, int lda, const void* b, int ldb, int m, int n, int k, float* preact_inout,
-                         int ldo, const float* bias, const unsigned* amax_bits, void* stream);
+                         int ldo, const float* bias, const unsigned* amax_bits, unsigned* out_amax_bits, void* stream);
 
 /* C[m][n] (fp32) = sum_t A[t][m] B[t][n] with A [k][m], B [k][n] row-major 16-bit (the backward's weight gradients
  * over the token axis, autodiff.py:350 matmul VJP): MN-major tcgen05 operands, no transposed copies; m, n multiples
@@ -339,7 +348,8 @@ int wm3_linear_tn_split_count(int m, int n, int k);
  *   wm3_natten_bwd         dQ into gqkv's q section, dK / dV (the CSR-ordered sum of per-chunk partials, partial =
  *                          [tiles * heads][maxch][2][2][64][128] fp32 scratch) into its k / v sections (fp32);
  *                          with rope_cos / rope_sin ([T][dhp / 2] pair tables, or both NULL) dK leaves through the
- *                          transpose of the rotary rotation (dQ then takes wm3_bw_rope_q) */
+ *                          transpose of the rotary rotation (dQ then takes wm3_bw_rope_q); kv_amax (or NULL):
+ *                          atomicMax of max |dK|, |dV| */
 int wm3_natten_fwd_lse(const void* qkv, int ldqkv, void* out, int ldo, int depth, int rows, int cols, int heads, int dhp,
                        int wd, int wh, int ww, float scale, float* lse, void* stream);
 int wm3_bw_na_prep(const void* qkv, int ldq, int T, int heads, int dhp, const float* gctx, int ldc,
@@ -351,8 +361,8 @@ int wm3_natten_slot_table(int depth, int rows, int cols, int heads, int dhp, int
                           void* stream);
 int wm3_natten_bwd(const void* qkv, int ldqkv, const void* dout, int ldd, const void* o, int ldo, const float* lse,
                    float* gqkv, int ldg, float* partial, const int32_t* csr_off, const int32_t* csr_ent,
-                   const float* factors, const float* rope_cos, const float* rope_sin, int depth, int rows, int cols,
-                   int heads, int dhp, int wd, int wh, int ww, float scale, void* stream);
+                   const float* factors, const float* rope_cos, const float* rope_sin, unsigned* kv_amax, int depth,
+                   int rows, int cols, int heads, int dhp, int wd, int wh, int ww, float scale, void* stream);
 
 /* Debug export of the kernel's own window arithmetic: per token, the (start_d, start_h, col_off)
  * it uses; int32 [T][3]. */

@@ -110,11 +110,12 @@ SIGNATURES = {
     "wm3_bw_gelu": [_vp, _i, _vp, _i, _vp, _i, _i, _vp, _vp, _i, _vp],
     "wm3_bw_gelu_fwd": [_vp, _i, _vp, _i, _i, _vp, _i, _vp],
     "wm3_bw_colsum_amax": [_vp, _i, _vp, _i, _vp, _vp, _i, _i, _vp, _i, _vp, _vp, _vp, _vp],
-    "wm3_bw_layernorm": [_vp, _i, _i, _i, _f, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp],
+    "wm3_bw_layernorm": [_vp, _i, _i, _i, _f, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "wm3_bw_natten": [_vp, _i, _vp, _vp, _vp, _i, _i, _i, _i, _f, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp],
-    "wm3_bw_rope_q": [_vp, _i, _i, _i, _i, _vp, _vp, _vp],
+    "wm3_bw_cast_colsum": [_vp, _i, _i, _i, _vp, _i, _vp, _vp, _vp, _vp],
+    "wm3_bw_rope_q": [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp],
     "wm3_bw_rope": [_vp, _i, _i, _i, _i, _vp, _vp, _vp],
-    "wm3_linear_gelu_grad": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _i, _vp, _vp, _vp],
+    "wm3_linear_gelu_grad": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _i, _vp, _vp, _vp, _vp],
     "wm3_linear_tn_split_count": [_i, _i, _i],
     "wm3_linear_tn_split": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _i, _vp, _sz, _vp],
     "wm3_linear_tn": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _i, _vp],
@@ -122,8 +123,8 @@ SIGNATURES = {
     "wm3_natten_fwd_lse": [_vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _f, _vp, _vp],
     "wm3_natten_bwd_info": [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp],
     "wm3_natten_slot_table": [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp],
-    "wm3_natten_bwd": [_vp, _i, _vp, _i, _vp, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i,
-                       _i, _i, _f, _vp],
+    "wm3_natten_bwd": [_vp, _i, _vp, _i, _vp, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i,
+                       _i, _i, _i, _f, _vp],
     "wm3_zonal_power": [_i, _vp, _ll, _i, _i, _i, _i, _vp, _vp],
 }
 

@@ -106,21 +106,34 @@ def _colsum_amax(src: torch.Tensor, rows: int, cols: int, gelu_of: torch.Tensor 
 
 
 def _layernorm_backward(x: torch.Tensor, gamma: torch.Tensor, g: torch.Tensor, scale: _Scale,
-                        add: torch.Tensor | None):
+                        add: torch.Tensor | None, gx_scale: _Scale | None = None):
     """LayerNorm reverse mode over rows of x [T][D] fp32 (autodiff.py:400-424) for the scaled output gradient g
     (row pitch g.stride(0)), plus `add` (the residual path): (gx, dgamma, dbeta), the parameter gradients as
     deterministic column sums of the kernel's per-row products.  (Folding those sums into the row kernel measured
     slower: a warp must then own a run of rows, which costs the occupancy the one-row-per-warp kernel hides its
-    loads with.)"""
+    loads with.)  gx_scale (or None) receives max |gx| from the same kernel (the next cast's operand scale)."""
     T, D = x.shape
     dev = x.device
     gx = torch.empty((T, D), dtype=torch.float32, device=dev)
     gxh = torch.empty_like(gx)
     check(_lib.lib().wm3_bw_layernorm(ptr(x), x.stride(0), T, D, LN_EPS, ptr(gamma), ptr(g), g.stride(0),
-                                      scale.ptr(), ptr(add), ptr(gx), ptr(gxh), None, stream_ptr()),
+                                      scale.ptr(), ptr(add), ptr(gx), ptr(gxh), None,
+                                      None if gx_scale is None else gx_scale.ptr(), stream_ptr()),
           "wm3_bw_layernorm")
     # the bias gradient is the column sum of g / scale itself: no [T][D] copy of it
     return gx, _colsum(gxh, T, D), _colsum(g, T, D, scale=scale)
+
+
+def _cast_colsum(src: torch.Tensor, rows: int, cols: int, ldd: int, scale: _Scale):
+    """(16-bit operand copy of src[:rows, :cols] times the scale, zero padded to [rows][ldd]; column sums of src)
+    in one pass — the producer already left max |src| in `scale`."""
+    chunks = (rows + 255) // 256
+    partial = torch.empty((chunks, cols), dtype=torch.float32, device=src.device)
+    colsum = torch.empty(cols, dtype=torch.float32, device=src.device)
+    out = torch.empty((rows, ldd), dtype=_lib.ELEM, device=src.device)
+    check(_lib.lib().wm3_bw_cast_colsum(ptr(src), rows, cols, src.stride(0), ptr(out), ldd, scale.ptr(), ptr(partial),
+                                        ptr(colsum), stream_ptr()), "wm3_bw_cast_colsum")
+    return out, colsum
 
 
 def _gemm_tn(a: torch.Tensor, b: torch.Tensor, m: int, n: int, k: int) -> torch.Tensor:
@@ -307,23 +320,26 @@ def block_vjp_device(xd: torch.Tensor, bw, extents, window, heads: int, dh: int,
     dw2 = _gemm_tn(gyh, mid, kp, nm, T)                                 # (kp, nm), x s1
     # ---- GELU' and W1 ----
     # g_a = (gy . W2) / s1 * gelu'(a0 + b1), the GELU backward in the gradient GEMM's epilogue, in place over a0
+    # (and its max |.| for the operand scale s2: every gradient's scale comes from its producer, so the cast and
+    # the bias gradient are one pass over it)
+    s2 = _Scale(dev)
     check(L.lib().wm3_linear_gelu_grad(ptr(gyh), gyh.stride(0), ptr(wt["w_2"]), wt["w_2"].stride(0), T, nm, np_,
-                                       ptr(a0), a0.stride(0), ptr(bw.b_1), s1.ptr(), stream_ptr()),
+                                       ptr(a0), a0.stride(0), ptr(bw.b_1), s1.ptr(), s2.ptr(), stream_ptr()),
           "wm3_linear_gelu_grad")
     g_a, a0 = a0, None
-    db1, s2 = _colsum_amax(g_a, T, nm)
-    gah = _cast(g_a, T, nm, nm, scale=s2)
+    gah, db1 = _cast_colsum(g_a, T, nm, nm, s2)
     dw1 = _gemm_tn(gah, hn2, nm, kp, T)
     g_hn2 = _gemm(gah, wt["w_1"], T, kp, nm)   # x s2
     # ---- LN2 (+ the residual path gy) ----
-    gx1, dln2_g, dln2_b = _layernorm_backward(x1, bw.ln2_g, g_hn2, s2, gyd)
+    s3 = _Scale(dev)
+    gx1, dln2_g, dln2_b = _layernorm_backward(x1, bw.ln2_g, g_hn2, s2, gyd, gx_scale=s3)
     # ---- O-proj ----
-    dbo, s3 = _colsum_amax(gx1, T, D)
-    gx1h = _cast(gx1, T, D, kp, scale=s3)
+    gx1h, dbo = _cast_colsum(gx1, T, D, kp, s3)
     dwo = _gemm_tn(gx1h, ctx, kp, hd, T)
     g_ctx = _gemm(gx1h, wt["w_o"], T, hd, np_)  # x s3
     # ---- attention (query and key sides) and the rotary transpose ----
     cs, sn = _rope_pair_tables(extents, dh, dhp, dev)
+    s4 = _Scale(dev)  # max |g_qkv|, left by the kernels that write it (tensor-core path)
     if tca is not None:
         g_qkv = torch.empty((T, 3 * hd), dtype=torch.float32, device=dev)  # every element written below
         # tensor cores: dQ per query tile, dK / dV as deterministic sums of per-chunk partials (natten.cu)
@@ -332,9 +348,9 @@ def block_vjp_device(xd: torch.Tensor, bw, extents, window, heads: int, dh: int,
                                      ptr(dout), hd, ptr(tca.maxima), ptr(tca.factors), stream_ptr()), "wm3_bw_na_prep")
         check(L.lib().wm3_natten_bwd(ptr(qkv), 3 * hd, ptr(dout), hd, ptr(ctx), hd, ptr(lse), ptr(g_qkv), 3 * hd,
                                      ptr(tca.partial), ptr(tca.off), ptr(tca.ent), ptr(tca.factors), ptr(cs), ptr(sn),
-                                     *extents, heads, dhp, *window, 1.0 / math.sqrt(dh), stream_ptr()),
+                                     s4.ptr(), *extents, heads, dhp, *window, 1.0 / math.sqrt(dh), stream_ptr()),
               "wm3_natten_bwd")  # dK leaves through the rotary transpose (coalesced per key in the reduction)
-        check(L.lib().wm3_bw_rope_q(ptr(g_qkv), 3 * hd, T, heads, dhp, ptr(cs), ptr(sn), stream_ptr()),
+        check(L.lib().wm3_bw_rope_q(ptr(g_qkv), 3 * hd, T, heads, dhp, ptr(cs), ptr(sn), s4.ptr(), stream_ptr()),
               "wm3_bw_rope_q")
     else:
         g_qkv = torch.zeros((T, 3 * hd), dtype=torch.float32, device=dev)
@@ -346,9 +362,9 @@ def block_vjp_device(xd: torch.Tensor, bw, extents, window, heads: int, dh: int,
                                     1.0 / math.sqrt(dh), ptr(g_ctx), hd, s3.ptr(), ptr(P), ptr(dS), ptr(work),
                                     ptr(g_qkv), 3 * hd, stream_ptr()), "wm3_bw_natten")
         check(L.lib().wm3_bw_rope(ptr(g_qkv), 3 * hd, T, heads, dhp, ptr(cs), ptr(sn), stream_ptr()), "wm3_bw_rope")
+        check(L.lib().wm3_bw_amax(ptr(g_qkv), T, 3 * hd, g_qkv.stride(0), s4.ptr(), stream_ptr()), "wm3_bw_amax")
     # ---- QKV ----
-    dbqkv, s4 = _colsum_amax(g_qkv, T, 3 * hd)
-    gqh = _cast(g_qkv, T, 3 * hd, 3 * hd, scale=s4)
+    gqh, dbqkv = _cast_colsum(g_qkv, T, 3 * hd, 3 * hd, s4)
     dwqkv = _gemm_tn(gqh, hn, 3 * hd, kp, T)
     g_hn = _gemm(gqh, wt["w_qkv"], T, kp, 3 * hd)  # x s4
     # ---- LN1 (+ gx1) ----

@@ -127,7 +127,9 @@ __global__ void bw_colsum_partial_kernel(const float* __restrict__ src, const fl
 // block = 256 columns x 4 row groups, thread (quad q, group k) adds rows r0 + k, r0 + k + 4, ... of columns
 // 4q .. 4q + 3 with 16-byte loads, and the 4 group sums are added in group order through shared memory into
 // partial[chunk][c] — a fixed order, and 4x the bytes in flight of one float per thread.  MODE 0: v = g;
-// MODE 1: v = g * a (product sums); MODE 2: v = (g / scale) * gelu'(a + bias), stored to out.  With amax_bits,
+// MODE 1: v = g * a (product sums); MODE 2: v = (g / scale) * gelu'(a + bias), stored to out; MODE 3: v = g, and
+// the 16-bit operand copy v * scale(in_scale_bits) stored to out ([rows][ldo], columns [cols, ldo) zero — the
+// cast and the bias gradient in one pass once the producer has left max |g| in in_scale_bits).  With amax_bits,
 // also atomicMax of max |v| (one per block).
 template <int MODE>
 __global__ void __launch_bounds__(256) bw_colsum4_kernel(const float* __restrict__ g, int ldg,
@@ -151,12 +153,16 @@ __global__ void __launch_bounds__(256) bw_colsum4_kernel(const float* __restrict
       inv = 1.f / grad_scale(in_scale_bits);
       b = __ldg(reinterpret_cast<const float4*>(bias + c));
     }
+    const float sc = MODE == 3 ? grad_scale(in_scale_bits) : 1.f;
 #pragma unroll 4
     for (int r = r0 + k; r < r1; r += 4) {
       float4 v = __ldg(reinterpret_cast<const float4*>(g + static_cast<size_t>(r) * ldg + c));
       if (MODE == 1) {
         const float4 w = __ldg(reinterpret_cast<const float4*>(a + static_cast<size_t>(r) * lda + c));
         v.x *= w.x; v.y *= w.y; v.z *= w.z; v.w *= w.w;
+      } else if (MODE == 3) {  // operand copy times the scale (the cast), column sums of the unscaled values
+        *reinterpret_cast<uint2*>(reinterpret_cast<elem_t*>(out) + static_cast<size_t>(r) * ldo + c) =
+            make_uint2(pack_elem(v.x * sc, v.y * sc), pack_elem(v.z * sc, v.w * sc));
       } else if (MODE == 2) {
         const float4 z = __ldg(reinterpret_cast<const float4*>(a + static_cast<size_t>(r) * lda + c));
         v.x = v.x * inv * gelu_grad(z.x + b.x);
@@ -168,6 +174,11 @@ __global__ void __launch_bounds__(256) bw_colsum4_kernel(const float* __restrict
       acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
     }
+  }
+  if (MODE == 3 && !ok && c < ldo) {  // operand padding columns [cols, ldo) are zero
+    const int r0 = blockIdx.y * BW_CHUNK, r1 = min(rows, r0 + BW_CHUNK);
+    for (int r = r0 + k; r < r1; r += 4)
+      *reinterpret_cast<uint2*>(reinterpret_cast<elem_t*>(out) + static_cast<size_t>(r) * ldo + c) = make_uint2(0u, 0u);
   }
   red[k][4 * q + 0] = acc.x;
   red[k][4 * q + 1] = acc.y;
@@ -315,48 +326,64 @@ __global__ void bw_gelu_kernel(const float* __restrict__ g, int ldg, const float
 __global__ void bw_layernorm_kernel(const float* __restrict__ x, int ldx, int rows, int n, float eps,
                                     const float* __restrict__ gamma, const float* __restrict__ g, int ldg,
                                     const unsigned* amax_bits, const float* __restrict__ add, float* __restrict__ gx,
-                                    float* __restrict__ gxh, float* __restrict__ gsc) {
+                                    float* __restrict__ gxh, float* __restrict__ gsc, unsigned* gx_amax) {
+  __shared__ float redm[8];
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp >= rows) return;
-  const float inv = 1.f / grad_scale(amax_bits);
-  const float* xr = x + static_cast<size_t>(warp) * ldx;
-  const float* gr = g + static_cast<size_t>(warp) * ldg;
-  float s = 0.f;
-  for (int c = lane; c < n; c += 32) s += xr[c];
+  float gm = 0.f;  // max |gx| of this warp's row (gx_amax: the next operand scale without another pass)
+  if (warp < rows) {
+    const float inv = 1.f / grad_scale(amax_bits);
+    const float* xr = x + static_cast<size_t>(warp) * ldx;
+    const float* gr = g + static_cast<size_t>(warp) * ldg;
+    float s = 0.f;
+    for (int c = lane; c < n; c += 32) s += xr[c];
 #pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  const float mu = s / n;
-  float q = 0.f;
-  for (int c = lane; c < n; c += 32) {
-    const float d = xr[c] - mu;
-    q += d * d;
-  }
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float mu = s / n;
+    float q = 0.f;
+    for (int c = lane; c < n; c += 32) {
+      const float d = xr[c] - mu;
+      q += d * d;
+    }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-  const float rstd = rsqrtf(q / n + eps);
-  float a1 = 0.f, a2 = 0.f;
-  for (int c = lane; c < n; c += 32) {
-    const float xh = (xr[c] - mu) * rstd;
-    const float gh = gr[c] * inv * gamma[c];
-    a1 += gh;
-    a2 += gh * xh;
-  }
+    for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    const float rstd = rsqrtf(q / n + eps);
+    float a1 = 0.f, a2 = 0.f;
+    for (int c = lane; c < n; c += 32) {
+      const float xh = (xr[c] - mu) * rstd;
+      const float gh = gr[c] * inv * gamma[c];
+      a1 += gh;
+      a2 += gh * xh;
+    }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    for (int o = 16; o; o >>= 1) {
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    a1 /= n;
+    a2 /= n;
+    for (int c = lane; c < n; c += 32) {
+      const size_t o = static_cast<size_t>(warp) * n + c;
+      const float xh = (xr[c] - mu) * rstd;
+      const float gu = gr[c] * inv;
+      const float gh = gu * gamma[c];
+      const float gv = rstd * (gh - a1 - xh * a2) + (add != nullptr ? add[o] : 0.f);
+      gx[o] = gv;
+      gm = fmaxf(gm, fabsf(gv));
+      gxh[o] = gu * xh;
+      if (gsc != nullptr) gsc[o] = gu;
+    }
   }
-  a1 /= n;
-  a2 /= n;
-  for (int c = lane; c < n; c += 32) {
-    const size_t o = static_cast<size_t>(warp) * n + c;
-    const float xh = (xr[c] - mu) * rstd;
-    const float gu = gr[c] * inv;
-    const float gh = gu * gamma[c];
-    gx[o] = rstd * (gh - a1 - xh * a2) + (add != nullptr ? add[o] : 0.f);
-    gxh[o] = gu * xh;
-    if (gsc != nullptr) gsc[o] = gu;
+  if (gx_amax != nullptr) {  // block-level max, one atomic per block (order-independent)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+    if (lane == 0) redm[threadIdx.x >> 5] = gm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float t = redm[0];
+      for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) t = fmaxf(t, redm[w]);
+      atomicMax(gx_amax, __float_as_uint(t));
+    }
   }
 }
 
@@ -469,10 +496,13 @@ __global__ void bw_na_key_kernel(const elem_t* __restrict__ qkv, int ldq, const 
 // In place on the q and k sections of g [T][3][heads][dhp]: the transpose of the rotary rotation of the
 // interleaved pairs (2i, 2i + 1) (forward: v0' = v0 c - v1 s, v1' = v0 s + v1 c), cos / sin [T][dhp / 2].
 __global__ void bw_rope_kernel(float* __restrict__ g, int ldg, int T, int heads, int dhp,
-                               const float* __restrict__ cs, const float* __restrict__ sn, int sections = 2) {
+                               const float* __restrict__ cs, const float* __restrict__ sn, int sections = 2,
+                               unsigned* amax = nullptr) {
   const int half = dhp / 2;
   if (ldg % 4 == 0 && dhp % 4 == 0) {  // row strips, two pairs per thread-step (16-byte I/O)
+    __shared__ float redm[32];
     const int w = sections * heads * dhp;
+    float m = 0.f;  // max |rotated value| (amax: the operand scale of the q section)
     for (int t = blockIdx.x; t < T; t += gridDim.x) {
       float* gr = g + static_cast<size_t>(t) * ldg;
       const float* ct = cs + static_cast<size_t>(t) * half;
@@ -482,8 +512,21 @@ __global__ void bw_rope_kernel(float* __restrict__ g, int ldg, int T, int heads,
         const float4 v = *reinterpret_cast<const float4*>(gr + c);
         const float2 cc = __ldg(reinterpret_cast<const float2*>(ct + pr));
         const float2 ss = __ldg(reinterpret_cast<const float2*>(st + pr));
-        *reinterpret_cast<float4*>(gr + c) = make_float4(v.x * cc.x + v.y * ss.x, -v.x * ss.x + v.y * cc.x,
-                                                         v.z * cc.y + v.w * ss.y, -v.z * ss.y + v.w * cc.y);
+        const float4 r = make_float4(v.x * cc.x + v.y * ss.x, -v.x * ss.x + v.y * cc.x, v.z * cc.y + v.w * ss.y,
+                                     -v.z * ss.y + v.w * cc.y);
+        *reinterpret_cast<float4*>(gr + c) = r;
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(r.x), fabsf(r.y)), fmaxf(fabsf(r.z), fabsf(r.w))));
+      }
+    }
+    if (amax != nullptr) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if ((threadIdx.x & 31) == 0) redm[threadIdx.x >> 5] = m;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float t = redm[0];
+        for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k) t = fmaxf(t, redm[k]);
+        atomicMax(amax, __float_as_uint(t));
       }
     }
     return;
@@ -556,6 +599,20 @@ extern "C" int wm3_bw_colsum(const float* src, const float* src2, int rows, int 
   return check_launch("bw_colsum_final_kernel");
 }
 
+extern "C" int wm3_bw_cast_colsum(const float* src, int rows, int cols, int lds, void* dst, int ldd,
+                                  const unsigned* amax_bits, float* partial, float* colsum, void* stream) {
+  if (rows < 1 || cols < 1 || ldd < cols) return set_error("wm3_bw_cast_colsum: bad shape");
+  if ((cols % 4) || (lds % 4) || (ldd % 4) || !aligned16(src) || reinterpret_cast<uintptr_t>(dst) % 8)
+    return set_error("wm3_bw_cast_colsum: cols / pitches multiples of 4, aligned bases required");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int chunks = (rows + BW_CHUNK - 1) / BW_CHUNK;
+  bw_colsum4_kernel<3><<<dim3((ldd + 255) / 256, chunks), 256, 0, s>>>(
+      src, lds, nullptr, 0, nullptr, amax_bits, rows, cols, reinterpret_cast<float*>(dst), ldd, partial, nullptr);
+  if (check_launch("bw_colsum4_kernel")) return -1;
+  bw_colsum_final_kernel<<<(cols + 31) / 32, 256, 0, s>>>(partial, chunks, cols, nullptr, colsum);
+  return check_launch("bw_colsum_final_kernel");
+}
+
 extern "C" int wm3_bw_colsum_amax(const float* g, int ldg, const float* a, int lda, const float* bias,
                                   const unsigned* in_scale_bits, int rows, int cols, float* out, int ldo,
                                   float* partial, float* colsum, unsigned* amax_bits, void* stream) {
@@ -600,10 +657,10 @@ extern "C" int wm3_bw_gelu(const float* g, int ldg, const float* a, int lda, con
 
 extern "C" int wm3_bw_layernorm(const float* x, int ldx, int rows, int n, float eps, const float* gamma, const float* g,
                                 int ldg, const unsigned* amax_bits, const float* add, float* gx, float* gxh, float* gsc,
-                                void* stream) {
+                                unsigned* gx_amax, void* stream) {
   const int threads = 256, blocks = (rows * 32 + threads - 1) / threads;
   bw_layernorm_kernel<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      x, ldx, rows, n, eps, gamma, g, ldg, amax_bits, add, gx, gxh, gsc);
+      x, ldx, rows, n, eps, gamma, g, ldg, amax_bits, add, gx, gxh, gsc, gx_amax);
   return check_launch("bw_layernorm_kernel");
 }
 
@@ -624,9 +681,10 @@ extern "C" int wm3_bw_natten(const void* qkv, int ldq, const int64_t* nbr, const
 }
 
 extern "C" int wm3_bw_rope_q(float* g, int ldg, int T, int heads, int dhp, const float* cos_t, const float* sin_t,
-                             void* stream) {
+                             unsigned* amax, void* stream) {
+  if ((ldg % 4) || (dhp % 4)) return set_error("wm3_bw_rope_q: ldg and dhp must be multiples of 4");
   bw_rope_kernel<<<T < 148 * 8 ? T : 148 * 8, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(g, ldg, T, heads, dhp,
-                                                                                               cos_t, sin_t, 1);
+                                                                                               cos_t, sin_t, 1, amax);
   return check_launch("bw_rope_kernel");
 }
 

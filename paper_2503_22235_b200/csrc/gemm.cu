@@ -41,6 +41,7 @@ struct EpiParams {
   int mn;  // operands MN-major (wm3_linear_tn: C = A^T B with A [K][M], B [K][N] row-major, 64 x 64 boxes)
   const unsigned* gscale;  // WM3_EPI_GELU_GRAD_F32: amax bits of the output gradient's operand scale
   int ksplit;  // > 1: split-K — output plane p = the partial product over k-block range p (A rows = plane rows)
+  unsigned* amax_out;  // WM3_EPI_GELU_GRAD_F32: atomicMax of max |out| (float bits), NULL = none
 };
 
 // epilogues that read the fp32 output buffer before overwriting it (the residual stream, or the stored GELU
@@ -395,6 +396,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     };
     float2 ln_next = cons ? stats_load(tile0) : make_float2(0.f, 0.f);
     const float ginv = (EPI == WM3_EPI_GELU_GRAD_F32) ? 1.f / grad_scale(ep.gscale) : 1.f;
+    float gmax = 0.f;  // WM3_EPI_GELU_GRAD_F32: this thread's max |out| (the next operand scale, no extra pass)
     for (int tile = tile0; tile < ntiles; tile += tstep, ++tile_it) {
       int plane, r0;
       const int m0 = tile_rows(tile, plane, r0);
@@ -457,6 +459,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 v[4 * j + 1] = v[4 * j + 1] * ginv * gelu_grad(xv.y + b.y);
                 v[4 * j + 2] = v[4 * j + 2] * ginv * gelu_grad(xv.z + b.z);
                 v[4 * j + 3] = v[4 * j + 3] * ginv * gelu_grad(xv.w + b.w);
+                if (row_ok)
+                  gmax = fmaxf(gmax, fmaxf(fmaxf(fabsf(v[4 * j + 0]), fabsf(v[4 * j + 1])),
+                                           fmaxf(fabsf(v[4 * j + 2]), fabsf(v[4 * j + 3]))));
               } else {
                 v[4 * j + 0] += b.x + xv.x;
                 v[4 * j + 1] += b.y + xv.y;
@@ -611,6 +616,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (acc == 0) aphase ^= 1;
     }
     if (elected) bulk_wait<0>();
+    if (EPI == WM3_EPI_GELU_GRAD_F32 && ep.amax_out != nullptr) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+      if (lane == 0) atomicMax(ep.amax_out, __float_as_uint(gmax));  // order-independent: deterministic
+    }
     if (EPI == WM3_EPI_QKV_ROPE && ep.has_halo) __threadfence_system();  // peer halo rows visible system-wide
   }
   tc_fence_before();
@@ -680,7 +690,8 @@ struct OutPlanes {
 static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi, void* out,
                        int ldo, int n_valid, const float* bias, const wm3_rope_t* rope, const OutPlanes& op,
                        void* stream, const wm3_halo_t* halo = nullptr, const wm3_ln_fold_t* fold = nullptr,
-                       bool mn = false, const unsigned* gscale = nullptr, int ksplit = 1) {
+                       bool mn = false, const unsigned* gscale = nullptr, int ksplit = 1,
+                       unsigned* amax_out = nullptr) {
   if (m <= 0 || n <= 0 || k <= 0) return set_error("wm3_linear: bad sizes m=%d n=%d k=%d", m, n, k);
   const bool f32_out = (epi == WM3_EPI_F32 || epi_reads_out(epi));
   if ((lda % 8) || (ldb % 8) || (ldo % (f32_out ? 4 : 8)))
@@ -709,6 +720,7 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
   ep.bias = bias;
   ep.gscale = gscale;
   ep.ksplit = ksplit;
+  ep.amax_out = amax_out;
   if (ksplit > 1 && (epi != WM3_EPI_F32 || op.planes != ksplit || op.row_off != 0 || (k + GEMM_BK - 1) / GEMM_BK < ksplit))
     return set_error("wm3_linear: bad split-K (%d splits, %d planes, k=%d)", ksplit, op.planes, k);
   ep.n_valid = n_valid;
@@ -808,10 +820,10 @@ extern "C" int wm3_linear(const void* a, int lda, const void* b, int ldb, int m,
 
 extern "C" int wm3_linear_gelu_grad(const void* a, int lda, const void* b, int ldb, int m, int n, int k,
                                     float* preact_inout, int ldo, const float* bias, const unsigned* amax_bits,
-                                    void* stream) {
+                                    unsigned* out_amax_bits, void* stream) {
   const OutPlanes op{1, m, m, 0};
   return linear_impl(a, lda, b, ldb, m, n, k, WM3_EPI_GELU_GRAD_F32, preact_inout, ldo, n, bias, nullptr, op, stream,
-                     nullptr, nullptr, false, amax_bits);
+                     nullptr, nullptr, false, amax_bits, 1, out_amax_bits);
 }
 
 extern "C" int wm3_linear_planes(const void* a, int lda, const void* b, int ldb, int m, int n, int k, int epi,

@@ -1114,36 +1114,56 @@ __global__ void natten_slot_table_kernel(NaParams p, int32_t* table) {
 __global__ void natten_bwd_reduce_kernel(const float* __restrict__ partial, const int32_t* __restrict__ off,
                                          const int32_t* __restrict__ ent, int T, int heads, int ntiles, int maxch,
                                          const float* __restrict__ factors, float* __restrict__ gqkv, int ldg,
-                                         const float* __restrict__ rope_cos, const float* __restrict__ rope_sin) {
+                                         const float* __restrict__ rope_cos, const float* __restrict__ rope_sin,
+                                         unsigned* amax) {
   constexpr int DHP = 128;
-  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  __shared__ float redm[32];
   const int lane = threadIdx.x & 31;
-  if (wid >= T * heads) return;
-  const int tk = wid / heads, h = wid - tk * heads;
-  float4 ak = make_float4(0.f, 0.f, 0.f, 0.f), av = ak;
-  for (int e = off[tk]; e < off[tk + 1]; ++e) {
-    const int32_t code = ent[e];  // (tile * maxch + chunk) * 128 + slot
-    const int slot = code & 127, tc = code >> 7;
-    const int tile = tc / maxch, j = tc - tile * maxch;
-    const size_t item = static_cast<size_t>(h) * ntiles + tile;
-    const float* base = partial + (((item * maxch + j) * 2 + (slot >> 6)) * 2) * 64 * DHP +
-                        static_cast<size_t>(slot & 63) * DHP + 4 * lane;
-    const float4 k4 = __ldg(reinterpret_cast<const float4*>(base));
-    const float4 v4 = __ldg(reinterpret_cast<const float4*>(base + 64 * DHP));
-    ak.x += k4.x; ak.y += k4.y; ak.z += k4.z; ak.w += k4.w;
-    av.x += v4.x; av.y += v4.y; av.z += v4.z; av.w += v4.w;
-  }
-  const float fk = __ldg(factors), fv = __ldg(factors + 1);
-  float* g = gqkv + static_cast<size_t>(tk) * ldg + h * DHP + 4 * lane;
   const int sec = heads * DHP;
-  float4 k4 = make_float4(ak.x * fk, ak.y * fk, ak.z * fk, ak.w * fk);
-  if (rope_cos != nullptr) {
-    const size_t pi = static_cast<size_t>(tk) * (DHP / 2) + 2 * lane;
-    k4 = rope_t2(k4, __ldg(reinterpret_cast<const float2*>(rope_cos + pi)),
-                 __ldg(reinterpret_cast<const float2*>(rope_sin + pi)));
+  const float fk = __ldg(factors), fv = __ldg(factors + 1);
+  float m = 0.f;  // max |dK|, |dV| of this thread's elements (the QKV weight gradient's operand scale)
+  // warps stride over the (key token, head) pairs; one atomic per block at the end (thousands of warps
+  // hitting one address measured slower than the whole reduction)
+  for (int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wid < T * heads;
+       wid += (gridDim.x * blockDim.x) >> 5) {
+    const int tk = wid / heads, h = wid - tk * heads;
+    float4 ak = make_float4(0.f, 0.f, 0.f, 0.f), av = ak;
+    for (int e = off[tk]; e < off[tk + 1]; ++e) {
+      const int32_t code = ent[e];  // (tile * maxch + chunk) * 128 + slot
+      const int slot = code & 127, tc = code >> 7;
+      const int tile = tc / maxch, j = tc - tile * maxch;
+      const size_t item = static_cast<size_t>(h) * ntiles + tile;
+      const float* base = partial + (((item * maxch + j) * 2 + (slot >> 6)) * 2) * 64 * DHP +
+                          static_cast<size_t>(slot & 63) * DHP + 4 * lane;
+      const float4 k4 = __ldg(reinterpret_cast<const float4*>(base));
+      const float4 v4 = __ldg(reinterpret_cast<const float4*>(base + 64 * DHP));
+      ak.x += k4.x; ak.y += k4.y; ak.z += k4.z; ak.w += k4.w;
+      av.x += v4.x; av.y += v4.y; av.z += v4.z; av.w += v4.w;
+    }
+    float* g = gqkv + static_cast<size_t>(tk) * ldg + h * DHP + 4 * lane;
+    float4 k4 = make_float4(ak.x * fk, ak.y * fk, ak.z * fk, ak.w * fk);
+    if (rope_cos != nullptr) {
+      const size_t pi = static_cast<size_t>(tk) * (DHP / 2) + 2 * lane;
+      k4 = rope_t2(k4, __ldg(reinterpret_cast<const float2*>(rope_cos + pi)),
+                   __ldg(reinterpret_cast<const float2*>(rope_sin + pi)));
+    }
+    *reinterpret_cast<float4*>(g + sec) = k4;
+    const float4 v4 = make_float4(av.x * fv, av.y * fv, av.z * fv, av.w * fv);
+    *reinterpret_cast<float4*>(g + 2 * sec) = v4;
+    m = fmaxf(m, fmaxf(fmaxf(fmaxf(fabsf(k4.x), fabsf(k4.y)), fmaxf(fabsf(k4.z), fabsf(k4.w))),
+                       fmaxf(fmaxf(fabsf(v4.x), fabsf(v4.y)), fmaxf(fabsf(v4.z), fabsf(v4.w)))));
   }
-  *reinterpret_cast<float4*>(g + sec) = k4;
-  *reinterpret_cast<float4*>(g + 2 * sec) = make_float4(av.x * fv, av.y * fv, av.z * fv, av.w * fv);
+  if (amax != nullptr) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) redm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float t = redm[0];
+      for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) t = fmaxf(t, redm[w]);
+      atomicMax(amax, __float_as_uint(t));
+    }
+  }
 }
 
 __global__ void natten_windows_kernel(int depth, int rows, int cols, int rows_global, int row0, int wd, int wh,
@@ -1425,8 +1445,8 @@ extern "C" int wm3_natten_slot_table(int depth, int rows, int cols, int heads, i
 extern "C" int wm3_natten_bwd(const void* qkv, int ldqkv, const void* dout, int ldd, const void* o, int ldo,
                               const float* lse, float* gqkv, int ldg, float* partial, const int32_t* csr_off,
                               const int32_t* csr_ent, const float* factors, const float* rope_cos,
-                              const float* rope_sin, int depth, int rows, int cols, int heads, int dhp, int wd, int wh,
-                              int ww, float scale, void* stream) {
+                              const float* rope_sin, unsigned* kv_amax, int depth, int rows, int cols, int heads,
+                              int dhp, int wd, int wh, int ww, float scale, void* stream) {
   if (dhp != 128) return set_error("wm3_natten_bwd: head dim must be padded to 128 (got %d)", dhp);
   if ((ldd % 8) || (ldo % 8) || (ldg % 4)) return set_error("wm3_natten_bwd: bad leading dimensions");
   NaParams p;
@@ -1460,8 +1480,8 @@ extern "C" int wm3_natten_bwd(const void* qkv, int ldqkv, const void* dout, int 
   natten_bwd_kernel<true><<<grid, NB_THREADS, NB_SMEM, s>>>(tq, tkv, tdo, p, b);
   if (check_launch("natten_bwd_kernel")) return -1;
   const int T = depth * rows * cols;
-  const int blocks = (T * heads * 32 + 255) / 256;
+  const int blocks = std::min((T * heads * 32 + 255) / 256, sm_count() * 32);
   natten_bwd_reduce_kernel<<<blocks, 256, 0, s>>>(partial, csr_off, csr_ent, T, heads, p.ntd * p.nth * p.ntw,
-                                                  p.maxch, factors, gqkv, ldg, rope_cos, rope_sin);
+                                                  p.maxch, factors, gqkv, ldg, rope_cos, rope_sin, kv_amax);
   return check_launch("natten_bwd_reduce_kernel");
 }

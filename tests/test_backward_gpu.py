@@ -334,9 +334,15 @@ def test_gelu_grad_gemm_epilogue():
         check(_lib.lib().wm3_bw_gelu(ptr(g), n, ptr(pre), n, ptr(b), T, n, s.ptr(), ptr(ref), n, stream_ptr()),
               "wm3_bw_gelu")
         out = pre.clone()
-        check(_lib.lib().wm3_linear_gelu_grad(ptr(a), k, ptr(w), k, T, n, k, ptr(out), n, ptr(b), s.ptr(),
+        so = bwd._Scale(a.device)
+        check(_lib.lib().wm3_linear_gelu_grad(ptr(a), k, ptr(w), k, T, n, k, ptr(out), n, ptr(b), s.ptr(), so.ptr(),
                                               stream_ptr()), "wm3_linear_gelu_grad")
         torch.testing.assert_close(out, ref, rtol=2e-6, atol=1e-30)
+        assert torch.equal(so.bits, bwd._amax(out, T, n).bits)  # the epilogue's max |out| = a separate pass
+        # the one-pass cast + column sums against the separate cast and column sums
+        oh, cs = bwd._cast_colsum(out, T, n, n + 64, so)
+        assert torch.equal(oh[:, :n], bwd._cast(out, T, n, n, scale=so)) and not oh[:, n:].any()
+        torch.testing.assert_close(cs, bwd._colsum(out, T, n), rtol=0, atol=0)
 
 
 @pytest.mark.parametrize("m,n,k", [(256, 256, 20000), (1024, 1024, 81000), (3072, 1024, 5000), (128, 192, 700)])
