@@ -97,24 +97,41 @@ class DeviceModel:
         self._enc: dict = {}
         self._dec = None
         self._bufs = None
-        self._fp = None
+
+    def fingerprint(self, prefix: str | None = None, blocks: bool = True) -> tuple:
+        """Content tags (tensor.content_tag) of the parameters named `prefix.*` (all with None; without the
+        `.blk*` transformer blocks when blocks=False — runtime.CACHE checks those per block).  Scoped so a call
+        checks only the arrays it uses: tagging all ~450 arrays of the full model costs ~5-10 ms of host time,
+        which left the GPU idle at the start of every encode / process / decode."""
+        return tuple(content_tag(v) for k, v in self.params.items()
+                     if (prefix is None or k.startswith(prefix + ".")) and (blocks or ".blk" not in k))
 
     def refresh(self) -> None:
-        fp = tuple(content_tag(v) for v in self.params.values())
-        if fp != self._fp:
-            self._enc.clear()
+        """Drop the converted pyramid weights whose host arrays changed (kept for callers that want an explicit
+        check; encoder() / decoder() check their own arrays on every access)."""
+        for pre in list(self._enc):
+            if self._enc[pre][0] != self.fingerprint(pre, blocks=False):
+                del self._enc[pre]
+        if self._dec is not None and self._dec[0] != self.fingerprint("dec", blocks=False):
             self._dec = None
-            self._fp = fp
+
+    @property
+    def _fp(self) -> tuple:
+        """Content tags of the processor blocks (what the captured rollout graphs hold)."""
+        return tuple(content_tag(v) for k, v in self.params.items() if k.startswith("proc"))
 
     def encoder(self, prefix: str) -> EncoderWeights:
-        if prefix not in self._enc:
-            self._enc[prefix] = EncoderWeights(self.params, prefix)
-        return self._enc[prefix]
+        fp = self.fingerprint(prefix, blocks=False)
+        hit = self._enc.get(prefix)
+        if hit is None or hit[0] != fp:
+            hit = self._enc[prefix] = (fp, EncoderWeights(self.params, prefix))
+        return hit[1]
 
     def decoder(self) -> DecoderWeights:
-        if self._dec is None:
-            self._dec = DecoderWeights(self.params)
-        return self._dec
+        fp = self.fingerprint("dec", blocks=False)
+        if self._dec is None or self._dec[0] != fp:
+            self._dec = (fp, DecoderWeights(self.params))
+        return self._dec[1]
 
     def buffers(self) -> PyramidBuffers:
         if self._bufs is None:
@@ -144,7 +161,6 @@ def device_model(params: dict, cfg: ModelConfig) -> DeviceModel:
         if hit is None or hit.params is not params:
             hit = DeviceModel(params, cfg)
             _models[key] = hit
-    hit.refresh()
     return hit
 
 

@@ -79,7 +79,7 @@ def host_values(t) -> np.ndarray:
 
 
 # at most this many elements of a host parameter array are hashed per content check
-TAG_SAMPLES = 2048
+TAG_SAMPLES = 256
 
 
 def content_tag(x) -> tuple:
