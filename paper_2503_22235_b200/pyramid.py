@@ -213,6 +213,10 @@ def _res_block(ws: StageW, bufs: PyramidBuffers, level: int, x_idx: int, imgs: i
     return x_idx
 
 
+# encoder stages run plane by plane while the host fields upload (encode_planes with before_plane)
+PER_PLANE_STAGES = 2
+
+
 def encode_planes(ew: EncoderWeights, bufs: PyramidBuffers, cfg: ModelConfig, tokens_out: torch.Tensor,
                   planes: tuple[int, int] | None = None, before_plane=None) -> None:
     """bufs.sfc_in / atm_in (device fp32) -> latent tokens (D*h*w, hidden) fp32.
@@ -220,9 +224,10 @@ def encode_planes(ew: EncoderWeights, bufs: PyramidBuffers, cfg: ModelConfig, to
     planes = (lo, hi) encodes only depth planes [lo, hi) (plane 0 = surface, p >= 1 = atmosphere level group
     p - 1) into their token rows: the planes share the pyramid weights and never interact before the encoder
     blocks, so the split is exact (bands.forecast_banded runs one range per rank).
-    before_plane(q): with it, the input layout copy and the stem convolution run plane by plane, each after
-    before_plane(q) (model.encode: make the stream wait for that plane's host upload), so the upload of plane
-    q + 1 overlaps the stem of plane q; the per-plane launches write the same bytes as the batched ones."""
+    before_plane(q): with it, the input layout copy, the stem convolution and the first PER_PLANE_STAGES stages
+    run plane by plane, each plane after before_plane(q) (model.encode: make the stream wait for that plane's
+    host upload), so the upload of plane q + 1 overlaps the convolutions of plane q; the per-plane launches write
+    the same bytes as the batched ones."""
     g = cfg.grid
     hh, ww = g.rows, g.cols
     d = cfg.depth_planes
@@ -251,16 +256,21 @@ def encode_planes(ew: EncoderWeights, bufs: PyramidBuffers, cfg: ModelConfig, to
     if before_plane is None:
         stems(lo, hi)
     elif DOWNSAMPLE_STAGES > 1:
-        # per plane: stem and the first (full -> half resolution) stage, while the next plane uploads
-        st = ew.stages[0]
-        h2, w2 = hh >> 1, ww >> 1
-        c_out = cfg.stage_channels[0]
+        # per plane: stem and the first PER_PLANE_STAGES stages (not the token-writing last one), while the next
+        # plane uploads — a plane's stem + two stages take longer than its upload, so only the first plane's
+        # upload is exposed
+        first = min(PER_PLANE_STAGES, DOWNSAMPLE_STAGES - 1)
         for q in range(lo, hi):
             before_plane(q)
             stems(q, q + 1)
-            run_conv(st.resample, bufs.buf(0, 0, c)[q:q + 1], 1, hh, ww, bufs.buf(1, 0, c_out)[q:q + 1])
-            x_idx = _res_block(st, bufs, 1, 0, 1, h2, w2, c_out, q)
-        c, first = c_out, 1
+            xi, ci = 0, cfg.stem_channels
+            for i in range(first):
+                st = ew.stages[i]
+                h2, w2 = hh >> (i + 1), ww >> (i + 1)
+                c_out = cfg.stage_channels[i]
+                run_conv(st.resample, bufs.buf(i, xi, ci)[q:q + 1], 1, h2 * 2, w2 * 2, bufs.buf(i + 1, 0, c_out)[q:q + 1])
+                xi, ci = _res_block(st, bufs, i + 1, 0, 1, h2, w2, c_out, q), c_out
+        x_idx, c = xi, ci
     else:
         for q in range(lo, hi):
             before_plane(q)
