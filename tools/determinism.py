@@ -1,5 +1,6 @@
+"""Run-to-run bitwise check of the full block (same inputs, repeated launches): the determinism the checkpoint / offload parity relies on."""
 import numpy as np, torch, sys
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 from paper_2503_22235_b200 import _lib, ops
 from paper_2503_22235_b200.blocks import RopeTables, Workspace, block_forward, prepare_block
 from paper_2503_22235_b200.params import init_block_params

@@ -1,3 +1,4 @@
+"""Probe: can a gloo process group all-gather CUDA tensors on this box (the WM3_DIST_BACKEND=gloo path of bench.py --gpus 2 on one GPU)?"""
 import torch, torch.distributed as dist, os
 dist.init_process_group("gloo")
 r = dist.get_rank()

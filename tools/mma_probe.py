@@ -1,3 +1,4 @@
+"""Probe of the tcgen05 MMA issue latency / throughput (tools/csrc/mma_probe.cu built as a separate library; not part of the product ABI)."""
 import os, sys
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
