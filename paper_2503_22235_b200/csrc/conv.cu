@@ -56,6 +56,11 @@ struct ConvParams {
 // the three column taps' weight boxes; the MMAs of tap kw read the strip from row kw (descriptor start + kw x
 // 128 B), so the A operand crosses L2 -> SM once per kernel row instead of once per tap.
 constexpr int CV_STRIP_ROWS = CV_BM + 2;
+#if !defined(WM3_OPERAND_BF16) && WM3_GELU_VARIANT == 2
+#define CONV_GELU_H2 true
+#else
+#define CONV_GELU_H2 false
+#endif
 template <int BN, int CG = 1, bool STRIP = false>
 struct ConvCfg {
   static constexpr int TAPS = STRIP ? 3 : 1;  // weight boxes per stage
@@ -282,9 +287,27 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
         if (!ok || n >= p.cout) continue;
         const int nvalid = min(32, p.cout - n);
         float v[32];
+        if (nvalid == 32 && (p.cout & 3) == 0) {  // bias as 8 16-byte loads (the same 128 B for every lane)
 #pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(rr[e]) + (e < nvalid ? __ldg(p.bias + n + e) : 0.f);
-        if (p.act_gelu) {
+          for (int j = 0; j < 8; ++j) {
+            const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + n) + j);
+            v[4 * j + 0] = __uint_as_float(rr[4 * j + 0]) + b.x;
+            v[4 * j + 1] = __uint_as_float(rr[4 * j + 1]) + b.y;
+            v[4 * j + 2] = __uint_as_float(rr[4 * j + 2]) + b.z;
+            v[4 * j + 3] = __uint_as_float(rr[4 * j + 3]) + b.w;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(rr[e]) + (e < nvalid ? __ldg(p.bias + n + e) : 0.f);
+        }
+        // GELU (res-block conv1, NHWC 16-bit out): packed f16x2 straight to the output pairs, as the W1 GEMM
+        // epilogue (gemm.cu); the fp32 form for the other outputs
+        uint32_t gpk[16];
+        const bool gelu_h2 = p.act_gelu && p.out_kind == WM3_CONV_OUT_NHWC && p.resid == nullptr && CONV_GELU_H2;
+        if (gelu_h2) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) gpk[e] = gelu_tanh_h2(v[2 * e], v[2 * e + 1]);
+        } else if (p.act_gelu) {
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = gelu_epi(v[e]);
         }
@@ -305,10 +328,15 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
         }
         if (p.out_kind == WM3_CONV_OUT_NHWC) {
           uint4 pk[4];
+          if (gelu_h2) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            pk[j] = make_uint4(pack_elem(v[8 * j], v[8 * j + 1]), pack_elem(v[8 * j + 2], v[8 * j + 3]),
-                               pack_elem(v[8 * j + 4], v[8 * j + 5]), pack_elem(v[8 * j + 6], v[8 * j + 7]));
+            for (int j = 0; j < 4; ++j) pk[j] = make_uint4(gpk[4 * j], gpk[4 * j + 1], gpk[4 * j + 2], gpk[4 * j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              pk[j] = make_uint4(pack_elem(v[8 * j], v[8 * j + 1]), pack_elem(v[8 * j + 2], v[8 * j + 3]),
+                                 pack_elem(v[8 * j + 4], v[8 * j + 5]), pack_elem(v[8 * j + 6], v[8 * j + 7]));
+          }
           elem_t* ob = reinterpret_cast<elem_t*>(p.out);
           uint4* d = reinterpret_cast<uint4*>(ob + pix * p.out_cp + n);
 #pragma unroll
