@@ -46,6 +46,7 @@ struct ConvParams {
   long long img_stride;        // FIELD: elements between images;   TOKENS: unused
   long long a_stride, p_stride;  // FIELD: channel c -> (c / chan_div) * a_stride + (c % chan_div) * p_stride
   int chan_div;
+  int tma_out;  // NHWC output of a stride-1 / stride-2 conv: TMA-staged epilogue stores (tmO), residual via tmR
 };
 
 // CG = 2: CTA pairs (cluster of 2 on a TPC, tcgen05.mma.cta_group::2, M = 256): each CTA stages its own 128
@@ -56,6 +57,9 @@ struct ConvParams {
 // the three column taps' weight boxes; the MMAs of tap kw read the strip from row kw (descriptor start + kw x
 // 128 B), so the A operand crosses L2 -> SM once per kernel row instead of once per tap.
 constexpr int CV_STRIP_ROWS = CV_BM + 2;
+#ifndef WM3_CONV_TMA_EPI
+#define WM3_CONV_TMA_EPI 1
+#endif
 #if !defined(WM3_OPERAND_BF16) && WM3_GELU_VARIANT == 2
 #define CONV_GELU_H2 true
 #else
@@ -69,11 +73,18 @@ struct ConvCfg {
   static constexpr uint32_t B_BYTES = TAPS * B1_BYTES;
   static constexpr uint32_t A_TX = STRIP ? CV_STRIP_ROWS * 128u : A_BYTES;  // bytes TMA writes
   static constexpr int STAGES_FIT = static_cast<int>((224u * 1024u - 1280u) / (A_BYTES + B_BYTES));
-  static constexpr int STAGES = (CG == 1 && !STRIP) ? ((BN == 256) ? 4 : (BN == 64 ? 8 : 5))
-                                                    : (STAGES_FIT < 8 ? STAGES_FIT : 8);
+  static constexpr int STAGES_NT = (CG == 1 && !STRIP) ? ((BN == 256) ? 4 : (BN == 64 ? 8 : 5))
+                                                       : (STAGES_FIT < 8 ? STAGES_FIT : 8);
+  // TMA-staged epilogue: each epilogue warp owns a 2 KB staging tile (32 pixels x 32 channels, 64-byte swizzle)
+  // that takes its residual chunk by TMA and sends its output chunk back by TMA, instead of per-thread 16-byte
+  // global accesses one pixel (384-512 B) apart; WM3_CONV_TMA_EPI=2 keeps it only where no ring stage is lost
+  static constexpr uint32_t EPI_STAGING = 8u * 2048u;
+  static constexpr int FIT_T = static_cast<int>((224u * 1024u - 1280u - EPI_STAGING) / (A_BYTES + B_BYTES));
+  static constexpr bool TMA_EPI = (WM3_CONV_TMA_EPI == 1 && FIT_T >= 3) || (WM3_CONV_TMA_EPI == 2 && FIT_T >= STAGES_NT);
+  static constexpr int STAGES = TMA_EPI ? (FIT_T < STAGES_NT ? FIT_T : STAGES_NT) : STAGES_NT;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t TX_BYTES = A_TX + B_BYTES;
-  static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + (TMA_EPI ? EPI_STAGING : 0u) + 1024 + 256;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
 };
 
@@ -97,20 +108,23 @@ DEVI void conv_tile(const ConvParams& p, int mt, int rank, int& img, int& cls, i
 
 template <int BN, int CG, bool STRIP>
 __global__ void __launch_bounds__(CV_THREADS, 1)
-    conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, ConvParams p) {
+    conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR, ConvParams p) {
   griddep_launch_dependents();  // PDL: the next kernel may start its prologue
   using Cfg = ConvCfg<BN, CG, STRIP>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  const uint32_t staging0 = sbase + STAGES * Cfg::STAGE_BYTES;  // TMA_EPI: 8 x 2 KB, one per epilogue warp
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + (Cfg::TMA_EPI ? Cfg::EPI_STAGING : 0u));
   const uint32_t bar0 = smem_u32(bars);
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
   auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + a); };
   auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + 2 + a); };
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  auto res_bar = [&](int w) { return bar0 + 8u * (2 * STAGES + 4 + w); };  // TMA_EPI: residual chunk landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4 + 8);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -125,10 +139,15 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if (Cfg::TMA_EPI && p.tma_out) {
+      tma_prefetch(&tmO);
+      if (p.resid != nullptr) tma_prefetch(&tmR);
+    }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
     }
+    for (int w = 0; w < 8; ++w) mbar_init(res_bar(w), 1);
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
       mbar_init(tempty_bar(a), 8 * CG);  // every epilogue warp of the pair arrives on the leader's barrier
@@ -259,6 +278,11 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
     int acc = 0;
     uint32_t aphase = 0;
     const uint32_t tempty_leader0 = (CG == 2) ? mapa_shared(tempty_bar(0), 0) : 0u;
+    const uint32_t stg = staging0 + (warp - 4) * 2048u;  // TMA_EPI: this warp's 32 x 32 staging tile
+    const uint32_t rbar = res_bar(warp - 4);
+    uint32_t rph = 0;
+    // 64-byte swizzle of the staging tile (rows = pixels, 4 x 16-byte chunks of 8 channels)
+    const uint32_t srow = stg + 64u * lane, sxor = (lane >> 1) & 3;
     for (int tile = tile0; tile < ntiles; tile += tstep) {
       int img, cls, r, c0;
       bool valid;
@@ -269,7 +293,8 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
       // output pixel
       int orow = r, ocol = col;
       if (p.mode == WM3_CONV_T2) { orow = 2 * r + (cls >> 1); ocol = 2 * col + (cls & 1); }
-      if (p.resid != nullptr && ok) {
+      const bool tma_tile = Cfg::TMA_EPI && p.tma_out && valid;  // uniform over the CTA
+      if (p.resid != nullptr && ok && !tma_tile) {
         // pull this pixel's residual channels toward L2 while the accumulator is still being computed
         const size_t rpix = (static_cast<size_t>(img) * (p.hout + 2) + orow + 1) * (p.wout + 2) + ocol + 1;
         const char* rb = reinterpret_cast<const char*>(p.resid + rpix * p.resid_cp + n0);
@@ -280,11 +305,18 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(32 * q) << 16);
       for (int u = g; u < BN / 32; u += 2) {
+        const int n = n0 + 32 * u;
+        const bool tma = tma_tile && n < p.cout;  // uniform over the warp
+        if (tma && p.resid != nullptr && lane == 0) {
+          // this warp's residual chunk (its 32 pixels x 32 channels) into its staging tile, under the TMEM load
+          bulk_wait_read<0>();  // the previous output chunk has left the staging tile
+          mbar_arrive_expect_tx(rbar, 2048u);
+          tma_load_4d(stg, &tmR, rbar, n, c0 + 32 * q + 1, orow + 1, img);
+        }
         uint32_t rr[32];
         tmem_ld32(taddr + 32 * u, rr);
         tmem_ld_wait();
-        const int n = n0 + 32 * u;
-        if (!ok || n >= p.cout) continue;
+        if (!tma && (!ok || n >= p.cout)) continue;
         const int nvalid = min(32, p.cout - n);
         float v[32];
         if (nvalid == 32 && (p.cout & 3) == 0) {  // bias as 8 16-byte loads (the same 128 B for every lane)
@@ -312,6 +344,55 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
           for (int e = 0; e < 32; ++e) v[e] = gelu_epi(v[e]);
         }
         const size_t pix = (static_cast<size_t>(img) * (p.hout + 2) + orow + 1) * (p.wout + 2) + ocol + 1;
+        if (tma) {
+          // residual from the staging tile (the TMA landed it), output back into it, one TMA store per warp;
+          // pixels past the row end are clipped by the output map (its column extent stops at the last pixel)
+          if (p.resid != nullptr) {
+            mbar_wait(rbar, rph & 1);
+            ++rph;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint32_t w0, w1, w2, w3;
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(srow + ((j ^ sxor) << 4)));
+              const uint32_t ws[4] = {w0, w1, w2, w3};
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const float2 h2 = unpack_elem2(ws[t]);
+                v[8 * j + 2 * t] += h2.x;
+                v[8 * j + 2 * t + 1] += h2.y;
+              }
+            }
+          } else {
+            if (lane == 0) bulk_wait_read<0>();  // the previous output chunk has left the staging tile
+            __syncwarp();
+          }
+          uint4 pk[4];
+          if (gelu_h2) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) pk[j] = make_uint4(gpk[4 * j], gpk[4 * j + 1], gpk[4 * j + 2], gpk[4 * j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              pk[j] = make_uint4(pack_elem(v[8 * j], v[8 * j + 1]), pack_elem(v[8 * j + 2], v[8 * j + 3]),
+                                 pack_elem(v[8 * j + 4], v[8 * j + 5]), pack_elem(v[8 * j + 6], v[8 * j + 7]));
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) st_shared_v4(srow + ((j ^ sxor) << 4), pk[j].x, pk[j].y, pk[j].z, pk[j].w);
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_4d(&tmO, stg, n, c0 + 32 * q + 1, orow + 1, img);
+            bulk_commit();
+          }
+          if (ok && (ocol == 0 || ocol == p.wout - 1)) {  // longitude wrap columns of the padded output
+            const size_t hp = pix + (ocol == 0 ? p.wout : -static_cast<long long>(p.wout));
+            uint4* d2 = reinterpret_cast<uint4*>(reinterpret_cast<elem_t*>(p.out) + hp * p.out_cp + n);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) d2[j] = pk[j];
+          }
+          continue;
+        }
         if (p.resid != nullptr) {
           const uint4* rs = reinterpret_cast<const uint4*>(p.resid + pix * p.resid_cp + n);
 #pragma unroll
@@ -377,6 +458,7 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }
+    if (Cfg::TMA_EPI && lane == 0) bulk_wait<0>();  // output chunks written before the CTA (and its smem) retires
   }
   tc_fence_before();
   if (CG == 2)
@@ -478,7 +560,9 @@ __global__ void tokens_to_nhwc_kernel(const float* __restrict__ tok, int imgs, i
 }
 
 template <int BN, int CG, bool STRIP>
-static int launch_conv(const CUtensorMap& ta, const CUtensorMap& tb, const ConvParams& p, cudaStream_t s) {
+static int launch_conv(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& tr,
+                       ConvParams p, cudaStream_t s) {
+  if (!ConvCfg<BN, CG, STRIP>::TMA_EPI) p.tma_out = 0;
   using Cfg = ConvCfg<BN, CG, STRIP>;
   auto kern = conv_tc_kernel<BN, CG, STRIP>;
   if (ensure_smem_attr(reinterpret_cast<const void*>(kern), Cfg::SMEM, "conv")) return -1;
@@ -486,7 +570,7 @@ static int launch_conv(const CUtensorMap& ta, const CUtensorMap& tb, const ConvP
       static_cast<long long>(p.imgs) * p.nclass * ((p.tiles_per_class + CG - 1) / CG) * (p.cout_pad / BN);
   if (CG == 1) {
     const int grid = static_cast<int>(ntiles < sm_count() ? ntiles : sm_count());
-    if (launch_pdl(kern, dim3(grid), dim3(CV_THREADS), Cfg::SMEM, s, ta, tb, p)) return -1;
+    if (launch_pdl(kern, dim3(grid), dim3(CV_THREADS), Cfg::SMEM, s, ta, tb, to, tr, p)) return -1;
     return check_launch("conv_tc_kernel");
   }
   const int pairs = sm_count() / 2;
@@ -503,22 +587,31 @@ static int launch_conv(const CUtensorMap& ta, const CUtensorMap& tb, const ConvP
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, kern, ta, tb, p) != cudaSuccess)
+  if (cudaLaunchKernelEx(&cfg, kern, ta, tb, to, tr, p) != cudaSuccess)
     return set_error("conv_tc_kernel (pairs): launch failed: %s", cudaGetErrorString(cudaGetLastError()));
   return check_launch("conv_tc_kernel");
 }
 
 template <int BN, int CG>
-static int launch_conv_mode(const CUtensorMap& ta, const CUtensorMap& tb, const ConvParams& p, cudaStream_t s,
-                            bool strip) {
+static int launch_conv_mode(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& tr,
+                            const ConvParams& p, cudaStream_t s, bool strip) {
   // the strip stage (A strip + three weight boxes) must still leave a 3-deep ring
-  if (strip && ConvCfg<BN, CG, true>::STAGES_FIT >= 3) return launch_conv<BN, CG, true>(ta, tb, p, s);
-  return launch_conv<BN, CG, false>(ta, tb, p, s);
+  if (strip && ConvCfg<BN, CG, true>::STAGES_FIT >= 3) return launch_conv<BN, CG, true>(ta, tb, to, tr, p, s);
+  return launch_conv<BN, CG, false>(ta, tb, to, tr, p, s);
 }
 
 }  // namespace wm3
 
 using namespace wm3;
+
+// TMA-staged conv epilogue (WM3_CONV_TMA=0 turns it off, A/B aid)
+static bool conv_tma_epi_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("WM3_CONV_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 // CTA pairs (WM3_CONV_PAIRS=0 turns them off, A/B aid): each CTA's weight box is half of the BN rows.
 // Measured (full-scale encode + decode, one B200): the 3x3 / transposed convs with Cout >= 128 run 7-12 %
@@ -610,16 +703,35 @@ extern "C" int wm3_conv(int mode, const void* in, int imgs, int hin, int win, in
   const int kdim = p.ntap * cinp;
   const int cg = pairs_ ? 2 : 1;
   if (make_tmap_2d_bf16(&tb, w, kdim, static_cast<uint64_t>(p.nclass) * p.cout_pad, kdim, CV_BK, bn / cg)) return -1;
+  // output / residual maps for the TMA-staged epilogue (NHWC output of a stride-1 / stride-2 conv: a tile's
+  // pixels are consecutive columns of one output row): boxes of 32 channels x 32 pixels, 64-byte swizzle; the
+  // output map's column extent ends at the last real pixel (padded column W + 1 is the wrap copy of pixel 0,
+  // written by the thread that owns pixel 0), so a tile's overhang past the row end is clipped
+  CUtensorMap to{}, tr{};
+  p.tma_out = 0;
+  if (out_kind == WM3_CONV_OUT_NHWC && mode != WM3_CONV_T2 && conv_tma_epi_enabled()) {
+    const uint64_t wpo = static_cast<uint64_t>(p.wout) + 2, hpo = static_cast<uint64_t>(p.hout) + 2;
+    const uint32_t box[4] = {32, 32, 1, 1};
+    const uint64_t od[4] = {static_cast<uint64_t>(out_cp), wpo - 1, hpo, static_cast<uint64_t>(imgs)};
+    const uint64_t os[3] = {static_cast<uint64_t>(out_cp), wpo * out_cp, hpo * wpo * out_cp};
+    if (make_tmap_swz(&to, out, TMAP_BF16, 4, od, os, box, nullptr, 64)) return -1;
+    if (resid) {
+      const uint64_t rd[4] = {static_cast<uint64_t>(resid_cp), wpo, hpo, static_cast<uint64_t>(imgs)};
+      const uint64_t rs[3] = {static_cast<uint64_t>(resid_cp), wpo * resid_cp, hpo * wpo * resid_cp};
+      if (make_tmap_swz(&tr, resid, TMAP_BF16, 4, rd, rs, box, nullptr, 64)) return -1;
+    }
+    p.tma_out = 1;
+  }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (cg == 2) {
-    if (bn == 128) return launch_conv_mode<128, 2>(ta, tb, p, s, strip);
-    if (bn == 192) return launch_conv_mode<192, 2>(ta, tb, p, s, strip);
-    return launch_conv_mode<256, 2>(ta, tb, p, s, strip);
+    if (bn == 128) return launch_conv_mode<128, 2>(ta, tb, to, tr, p, s, strip);
+    if (bn == 192) return launch_conv_mode<192, 2>(ta, tb, to, tr, p, s, strip);
+    return launch_conv_mode<256, 2>(ta, tb, to, tr, p, s, strip);
   }
-  if (bn == 64) return launch_conv_mode<64, 1>(ta, tb, p, s, strip);
-  if (bn == 128) return launch_conv_mode<128, 1>(ta, tb, p, s, strip);
-  if (bn == 192) return launch_conv_mode<192, 1>(ta, tb, p, s, strip);
-  return launch_conv_mode<256, 1>(ta, tb, p, s, strip);
+  if (bn == 64) return launch_conv_mode<64, 1>(ta, tb, to, tr, p, s, strip);
+  if (bn == 128) return launch_conv_mode<128, 1>(ta, tb, to, tr, p, s, strip);
+  if (bn == 192) return launch_conv_mode<192, 1>(ta, tb, to, tr, p, s, strip);
+  return launch_conv_mode<256, 1>(ta, tb, to, tr, p, s, strip);
 }
 
 extern "C" int wm3_fields_to_nhwc(const float* src, long long img_stride, long long a_stride, long long p_stride,

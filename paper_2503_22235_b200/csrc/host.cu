@@ -86,6 +86,11 @@ static EncodeTiledFn encode_fn() {
 
 int make_tmap(CUtensorMap* map, const void* ptr, int dtype, int rank, const uint64_t* dims,
               const uint64_t* strides_elems, const uint32_t* box, const uint32_t* elem_strides) {
+  return make_tmap_swz(map, ptr, dtype, rank, dims, strides_elems, box, elem_strides, 128);
+}
+
+int make_tmap_swz(CUtensorMap* map, const void* ptr, int dtype, int rank, const uint64_t* dims,
+                  const uint64_t* strides_elems, const uint32_t* box, const uint32_t* elem_strides, int swizzle_bytes) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return set_error("cuTensorMapEncodeTiled unavailable");
   const uint64_t esz = dtype == TMAP_F32 ? 4 : 2;
@@ -98,7 +103,9 @@ int make_tmap(CUtensorMap* map, const void* ptr, int dtype, int rank, const uint
   }
   for (int i = 0; i + 1 < rank; ++i) st[i] = strides_elems[i] * esz;
   CUresult r = fn(map, dtype == TMAP_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank,
-                  const_cast<void*>(ptr), d, st, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  const_cast<void*>(ptr), d, st, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                      : (swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B),
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return set_error("cuTensorMapEncodeTiled failed (%d): rank %d dims %llu %llu %llu box %u %u", int(r), rank,

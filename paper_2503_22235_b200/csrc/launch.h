@@ -22,6 +22,9 @@ enum { TMAP_BF16 = 0, TMAP_F32 = 1 };
 // General tensor map (SWIZZLE_128B, zero OOB fill), rank <= 5; strides in elements for dims 1..rank-1.
 int make_tmap(CUtensorMap* map, const void* ptr, int dtype, int rank, const uint64_t* dims,
               const uint64_t* strides_elems, const uint32_t* box, const uint32_t* elem_strides);
+// make_tmap with the shared-memory swizzle chosen (32 / 64 / 128 bytes; make_tmap uses 128)
+int make_tmap_swz(CUtensorMap* map, const void* ptr, int dtype, int rank, const uint64_t* dims,
+                  const uint64_t* strides_elems, const uint32_t* box, const uint32_t* elem_strides, int swizzle_bytes);
 // General bf16 tensor map, rank <= 5; strides in elements for dims 1..rank-1.
 int make_tmap_bf16(CUtensorMap* map, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_elems,
                    const uint32_t* box, const uint32_t* elem_strides);
