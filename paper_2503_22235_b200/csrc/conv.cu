@@ -46,7 +46,7 @@ struct ConvParams {
   long long img_stride;        // FIELD: elements between images;   TOKENS: unused
   long long a_stride, p_stride;  // FIELD: channel c -> (c / chan_div) * a_stride + (c % chan_div) * p_stride
   int chan_div;
-  int tma_out;  // NHWC output of a stride-1 / stride-2 conv: TMA-staged epilogue stores (tmO), residual via tmR
+  int tma_out;  // NHWC output: TMA-staged epilogue stores (tmO), residual chunks via tmR
 };
 
 // CG = 2: CTA pairs (cluster of 2 on a TPC, tcgen05.mma.cta_group::2, M = 256): each CTA stages its own 128
@@ -382,7 +382,9 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
-            tma_store_4d(&tmO, stg, n, c0 + 32 * q + 1, orow + 1, img);
+            // first padded column of the warp's 32 pixels (transposed convs: every other column of the class)
+            const int pc = p.mode == WM3_CONV_T2 ? 2 * (c0 + 32 * q) + (cls & 1) + 1 : c0 + 32 * q + 1;
+            tma_store_4d(&tmO, stg, n, pc, orow + 1, img);
             bulk_commit();
           }
           if (ok && (ocol == 0 || ocol == p.wout - 1)) {  // longitude wrap columns of the padded output
@@ -703,18 +705,23 @@ extern "C" int wm3_conv(int mode, const void* in, int imgs, int hin, int win, in
   const int kdim = p.ntap * cinp;
   const int cg = pairs_ ? 2 : 1;
   if (make_tmap_2d_bf16(&tb, w, kdim, static_cast<uint64_t>(p.nclass) * p.cout_pad, kdim, CV_BK, bn / cg)) return -1;
-  // output / residual maps for the TMA-staged epilogue (NHWC output of a stride-1 / stride-2 conv: a tile's
-  // pixels are consecutive columns of one output row): boxes of 32 channels x 32 pixels, 64-byte swizzle; the
+  // output / residual maps for the TMA-staged epilogue (NHWC output: a warp's 32 pixels are consecutive columns
+  // of one output row, or every other column for a transposed conv): boxes of 32 channels x 32 pixels, 64-byte
+  // swizzle; the
   // output map's column extent ends at the last real pixel (padded column W + 1 is the wrap copy of pixel 0,
   // written by the thread that owns pixel 0), so a tile's overhang past the row end is clipped
   CUtensorMap to{}, tr{};
   p.tma_out = 0;
-  if (out_kind == WM3_CONV_OUT_NHWC && mode != WM3_CONV_T2 && conv_tma_epi_enabled()) {
+  if (out_kind == WM3_CONV_OUT_NHWC && conv_tma_epi_enabled() && !(mode == WM3_CONV_T2 && resid)) {
     const uint64_t wpo = static_cast<uint64_t>(p.wout) + 2, hpo = static_cast<uint64_t>(p.hout) + 2;
     const uint32_t box[4] = {32, 32, 1, 1};
+    // transposed convs: a warp's 32 pixels are every other output column (one parity class), so the store box
+    // spans 64 columns with traversal stride 2 (32 rows in shared memory)
+    const uint32_t tbox[4] = {32, 64, 1, 1}, tstr[4] = {1, 2, 1, 1};
+    const bool t2 = mode == WM3_CONV_T2;
     const uint64_t od[4] = {static_cast<uint64_t>(out_cp), wpo - 1, hpo, static_cast<uint64_t>(imgs)};
     const uint64_t os[3] = {static_cast<uint64_t>(out_cp), wpo * out_cp, hpo * wpo * out_cp};
-    if (make_tmap_swz(&to, out, TMAP_BF16, 4, od, os, box, nullptr, 64)) return -1;
+    if (make_tmap_swz(&to, out, TMAP_BF16, 4, od, os, t2 ? tbox : box, t2 ? tstr : nullptr, 64)) return -1;
     if (resid) {
       const uint64_t rd[4] = {static_cast<uint64_t>(resid_cp), wpo, hpo, static_cast<uint64_t>(imgs)};
       const uint64_t rs[3] = {static_cast<uint64_t>(resid_cp), wpo * resid_cp, hpo * wpo * resid_cp};
