@@ -214,3 +214,30 @@ def test_in_place_parameter_update_reaches_the_device():
     assert not np.array_equal(after_p, before_p) and not np.array_equal(after_r, before_r)
     assert np.array_equal(after_p, want_p)
     assert np.array_equal(after_r, want_r)
+
+
+def test_in_place_pyramid_update_reaches_the_device():
+    """Encoder / decoder pyramid weights updated in place (the same optimizer step) are picked up by the next
+    encode / decode: the device model checks the content of the pyramid arrays it uses on every call."""
+    import paper_2503_22235_b200.model as M
+    from paper_2503_22235_b200.tensor import Tensor
+    cfg = M.desk_config()
+    params = M.init_model_params(cfg, seed=11, zero_residual=False)
+    rng = np.random.default_rng(5)
+    g = cfg.grid
+    st = M.WeatherState(0, rng.standard_normal((cfg.surface_in, g.rows, g.cols)).astype(np.float32),
+                        rng.standard_normal((cfg.atmos_vars, cfg.levels, g.rows, g.cols)).astype(np.float32))
+    lat0 = M.encode(st, params, cfg)
+    dec0 = M.decode(lat0, params, cfg).surface.device.cpu().numpy()
+    before = lat0.tokens.device.cpu().numpy()
+    for name in ("enc.stem_atm.w", "enc.stage1.res0.conv2.w", "dec.stage0.res1.conv1.w"):
+        if name in params:
+            params[name].values -= 0.05 * rng.standard_normal(params[name].values.shape)
+    fresh = {k: Tensor(v.values.copy()) for k, v in params.items()}
+    lat1 = M.encode(st, params, cfg)
+    after = lat1.tokens.device.cpu().numpy()
+    want = M.encode(st, fresh, cfg).tokens.device.cpu().numpy()
+    assert not np.array_equal(after, before) and np.array_equal(after, want)
+    dec1 = M.decode(lat0, params, cfg).surface.device.cpu().numpy()
+    dec_want = M.decode(lat0, fresh, cfg).surface.device.cpu().numpy()
+    assert not np.array_equal(dec1, dec0) and np.array_equal(dec1, dec_want)
