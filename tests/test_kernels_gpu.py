@@ -234,3 +234,38 @@ def test_natten_both_mask_paths_match_reference(tile, monkeypatch):
     rel = ((out.float() - ref).norm() / ref.norm()).item()
     print(f"NA tile {tile}: rel L2 {rel:.2e} max abs {err:.2e}")
     assert rel < 2e-3 and err < 1e-2, (tile, err, rel)
+
+
+_TILE_PROBE = r"""
+import hashlib, sys, torch
+sys.path.insert(0, {root!r})
+from paper_2503_22235_b200 import _lib, ops
+g = torch.Generator(device="cuda").manual_seed(0)
+h = hashlib.sha256()
+for m, n, k in ((9900, 1024, 1024), (5000, 3072, 1024), (777, 1024, 4096)):
+    a = torch.randn(m, k, device="cuda", generator=g).to(_lib.ELEM)
+    w = (torch.randn(n, k, device="cuda", generator=g) / 32).to(_lib.ELEM)
+    b = torch.randn(n, device="cuda", generator=g)
+    x = torch.randn(m, n, device="cuda", generator=g)
+    ops.linear(a, w, _lib.WM3_EPI_BIAS_RESID_F32, bias=b, out=x, n_valid=n)
+    y = ops.linear(a, w, _lib.WM3_EPI_BIAS_GELU_BF16, bias=b)
+    torch.cuda.synchronize()
+    h.update(x.cpu().numpy().tobytes()); h.update(y.cpu().view(torch.int16).numpy().tobytes())
+print(h.hexdigest())
+"""
+
+
+def test_gemm_results_independent_of_tile_width():
+    """The CTA-pair GEMM picks 256 x 128 tiles where 256 x 256 ones would leave most of a wave idle (latitude
+    bands at 8 GPUs); per-element MMA and epilogue arithmetic must not depend on that choice (band results are
+    bitwise the single-GPU ones): every pair GEMM on 256-wide vs on 128-wide tiles, bitwise."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _TILE_PROBE.format(root=root)
+    out = {}
+    for v in ("0", "2"):
+        env = dict(os.environ, WM3_GEMM_NARROW=v)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[v] = r.stdout.strip().splitlines()[-1]
+    assert out["0"] == out["2"], out
