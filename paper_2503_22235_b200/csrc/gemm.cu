@@ -737,13 +737,14 @@ static int linear_impl(const void* a, int lda, const void* b, int ldb, int m, in
   // in by TMA (0.195 vs 0.204 ms isolated)
   const int cg = (bn == 256 && cg_env == 2) ? 2 : 1;
   ep.tiles_per_plane = (op.plane_rows + GEMM_BM * cg - 1) / (GEMM_BM * cg);
-  // Narrow pair tiles (256 x 128) when the 256 x 256 tiles leave most of their last wave idle: a latitude band's
-  // 1024-wide GEMMs at 8 GPUs have 156 tiles for 74 pairs (3 rounds for 2.1 waves; 256 x 128: 5 rounds of half
-  // the work).  Same per-element MMA / epilogue arithmetic, so results do not depend on the choice.
-  // WM3_GEMM_NARROW=0 never, 2 always (A/B, tests).
+  // Narrow pair tiles (256 x 128) for outputs whose 256 x 256 tiles leave most of their last wave idle (a
+  // latitude band's 1024-wide GEMMs at 8 GPUs: 156 tiles for 74 pairs).  Off by default: measured per tile they
+  // are ~30 % less efficient (half the MMA per operand byte), which costs more than the idle tail — O-proj / W2
+  // at M = 9900: 29 / 80 us on 256-wide tiles, 33 / 94 us on 128-wide.  Same per-element arithmetic, so
+  // results do not depend on the choice.  WM3_GEMM_NARROW=1 heuristic, 2 always (A/B, tests).
   static const int narrow_env = [] {
     const char* e = getenv("WM3_GEMM_NARROW");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 0;
   }();
   bool narrow = false;
   if (cg == 2 && narrow_env != 0 && fold == nullptr && !mn && ksplit == 1) {
