@@ -130,7 +130,10 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
   const int lane = threadIdx.x & 31;
   const int nn = p.cout_pad / BN;
   const int ntiles = p.imgs * p.nclass * ((p.tiles_per_class + CG - 1) / CG) * nn;
-  const int nk = (STRIP ? 3 : p.ntap) * p.ncb;  // stages per tile
+  // strip stages: one per (kernel row, channel block); a stride-1 strip serves 3 column taps, a transposed
+  // conv's (parity class) strip its 2
+  const int strip_taps = (p.mode == WM3_CONV_T2) ? 2 : 3;
+  const int nk = (STRIP ? (p.mode == WM3_CONV_T2 ? 2 : 3) : p.ntap) * p.ncb;  // stages per tile
   // CTA pairs: cluster = (2k, 2k + 1) walks the pair tiles together
   const int rank = (CG == 2) ? static_cast<int>(cluster_ctarank()) : 0;
   const int tile0 = (CG == 2) ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
@@ -190,14 +193,21 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
           const uint32_t sb = sa + Cfg::A_BYTES;
           // pairs: both CTAs' bytes complete on the leader's full barrier; only the leader arms it
           const uint32_t fb = (CG == 2) ? mapa_shared(full_bar(stage), 0) : full_bar(stage);
-          if (rank == 0) mbar_arrive_expect_tx(full_bar(stage), CG * Cfg::TX_BYTES);
+          if (rank == 0)
+            mbar_arrive_expect_tx(full_bar(stage),
+                                  CG * (STRIP ? Cfg::A_TX + strip_taps * Cfg::B1_BYTES : Cfg::TX_BYTES));
           if (STRIP) {
-            // strip of padded columns [c0, c0 + 130) of input row r + kh; weights of taps (kh, 0..2)
-            if (CG == 2) tma_load_3d_cg2(sa, &tmA, fb, cb * CV_BK, c0, img * hp + r + tap);
-            else tma_load_3d(sa, &tmA, fb, cb * CV_BK, c0, img * hp + r + tap);
+            // stride 1: strip of padded columns [c0, c0 + 130) of input row r + kh, weights of taps (kh, 0..2);
+            // transposed (class (a, b)): strip of columns [c0 + b, +130) of input row r + a + tr, weights of
+            // taps (tr, 0..1) — its two column taps read input columns one apart
+            const bool t2 = p.mode == WM3_CONV_T2;
+            const int scol = t2 ? c0 + b : c0, srow = img * hp + r + (t2 ? a : 0) + tap;
+            if (CG == 2) tma_load_3d_cg2(sa, &tmA, fb, cb * CV_BK, scol, srow);
+            else tma_load_3d(sa, &tmA, fb, cb * CV_BK, scol, srow);
 #pragma unroll
             for (int kw = 0; kw < 3; ++kw) {
-              const int kcol = ((3 * tap + kw) * p.ncb + cb) * CV_BK;
+              if (kw >= strip_taps) break;
+              const int kcol = ((strip_taps * tap + kw) * p.ncb + cb) * CV_BK;
               if (CG == 2) tma_load_2d_cg2(sb + kw * Cfg::B1_BYTES, &tmB, fb, kcol, cls * p.cout_pad + n0);
               else tma_load_2d(sb + kw * Cfg::B1_BYTES, &tmB, fb, kcol, cls * p.cout_pad + n0);
             }
@@ -244,6 +254,7 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
           if (elect_one()) {
 #pragma unroll
             for (int kw = 0; kw < Cfg::TAPS; ++kw) {
+              if (STRIP && kw >= strip_taps) break;
               // tap kw reads strip rows [kw, kw + 128): start address + kw x 128 B.  The MMA unit swizzles on
               // the absolute shared-memory address (as TMA wrote it), so the descriptor's base-offset field
               // stays 0 (setting it to kw broke parity, measured).
@@ -606,6 +617,15 @@ static int launch_conv_mode(const CUtensorMap& ta, const CUtensorMap& tb, const 
 
 using namespace wm3;
 
+// transposed convs on A strips (WM3_CONV_T2STRIP=0 turns it off, A/B aid)
+static bool conv_t2_strip_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("WM3_CONV_T2STRIP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // TMA-staged conv epilogue (WM3_CONV_TMA=0 turns it off, A/B aid)
 static bool conv_tma_epi_enabled() {
   static const bool on = [] {
@@ -685,7 +705,8 @@ extern "C" int wm3_conv(int mode, const void* in, int imgs, int hin, int win, in
   }();
   const int bn_ = wm3_conv_bn(cout);
   const bool pairs_ = conv_pairs_enabled() && bn_ >= 128;
-  const bool strip = strip_env && mode == WM3_CONV_S1 && conv_strip_fits(bn_, pairs_ ? 2 : 1);
+  const bool strip = strip_env && (mode == WM3_CONV_S1 || (mode == WM3_CONV_T2 && conv_t2_strip_enabled())) &&
+                     conv_strip_fits(bn_, pairs_ ? 2 : 1);
   // A: padded NHWC input, images stacked along rows
   CUtensorMap ta, tb;
   const uint64_t wp = win + 2;
