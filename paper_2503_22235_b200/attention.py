@@ -17,7 +17,7 @@ from .blocks import rope_axis_tables
 from .errors import ConfigError
 from .params import block_param_names, init_block_params  # noqa: F401  (re-exported API)
 from .runtime import CACHE
-from .tensor import Tensor, host_array
+from .tensor import payload, Tensor, host_array
 
 __all__ = ["natten_block", "NattenBlockStream", "attention_weights", "rotary_tables", "apply_rotary",
            "init_block_params", "block_param_names", "to_device_f32", "validate_block_args"]
@@ -30,6 +30,11 @@ def to_device_f32(x) -> torch.Tensor:
     elif isinstance(x, torch.Tensor):
         src = x
     else:
+        v = np.asarray(payload(x))
+        if v.nbytes >= (1 << 22):  # large host arrays: cast into page-locked memory, one fast upload
+            h = torch.empty(v.shape, dtype=torch.float32, pin_memory=True)
+            np.copyto(h.numpy(), v, casting="unsafe")
+            return h.to(device="cuda").contiguous()
         src = torch.from_numpy(np.ascontiguousarray(host_array(x, np.float32)))
     return src.to(device="cuda", dtype=torch.float32, copy=True).contiguous()
 
@@ -106,7 +111,8 @@ def natten_block(x, params: dict, prefix: str, extents, window, heads: int):
     block_forward(xd, bw, CACHE.workspace(extents, window, bw), CACHE.rope(extents, dh), tuple(extents),
                   tuple(window))
     if foreign:
-        return _wrap_foreign(x, xd.to("cpu", torch.float64).numpy(), params, prefix, extents, window, heads)
+        from .tensor import device_to_host_f64
+        return _wrap_foreign(x, device_to_host_f64(xd), params, prefix, extents, window, heads)
     return Tensor(device=xd)
 
 

@@ -434,11 +434,9 @@ def block_grads_to_reference(acc: BlockGrads, bw, params: dict, prefix: str, dh:
 
 
 def _to_host_f64(t: torch.Tensor) -> np.ndarray:
-    """float64 numpy copy of a device tensor through page-locked memory (pageable device -> host copies of
-    the 0.66 GB latent gradient ran at ~2 GB/s); the array keeps its page-locked buffer alive."""
-    h = torch.empty(tuple(t.shape), dtype=torch.float64, pin_memory=True)
-    h.copy_(t.to(torch.float64))
-    return h.numpy()
+    """float64 numpy copy through page-locked memory (tensor.device_to_host_f64)."""
+    from .tensor import device_to_host_f64
+    return device_to_host_f64(t)
 
 
 def block_vjp(x, params: dict, prefix: str, extents, window, heads: int, gy):
