@@ -13,9 +13,11 @@
 //   convT s2    output parity class (a, b), taps (tr, tc) in {0,1}^2: out (2r + a, 2c + b) reads padded
 //               (r + a + tr, c + b + tc) with kernel tap (3 - a - 2 tr, 3 - b - 2 tc)
 // GEMM view: M = output pixels of one row (128-pixel tiles), N = Cout, K = taps x Cp (weights pre-arranged
-// [class][Cout_pad][tap][Cp], K-major).  Warp roles as in gemm.cu; the epilogue writes straight from
-// registers (one pixel per thread): bias, optional exact GELU, optional residual (res-block skip), and
-// either the next padded NHWC activation (incl. its wrap columns), fp32 tokens, or fp32 NCHW fields.
+// [class][Cout_pad][tap][Cp], K-major).  Warp roles as in gemm.cu; the epilogue (one pixel per thread) applies
+// bias, optional GELU and the optional residual (res-block skip) and writes the next padded NHWC activation
+// through a per-warp shared-memory tile — residual chunk in and output chunk out by TMA (32 pixels x 32
+// channels, 64-byte swizzle; the two wrap-column copies per row by their owning threads) — or, straight from
+// registers, fp32 tokens or fp32 NCHW fields.
 #include "common.cuh"
 #include "launch.h"
 #include "../../include/wm3.h"
