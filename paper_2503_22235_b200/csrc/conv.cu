@@ -453,14 +453,20 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
 #pragma unroll
             for (int j = 0; j < 8; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           } else {
-            for (int e = 0; e < nvalid; ++e) ot[e] = v[e];
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (e < nvalid) ot[e] = v[e];
           }
         } else {  // fp32 NCHW fields with channel remap (model.py:340-347 level unfold)
           float* of = reinterpret_cast<float*>(p.out) + static_cast<size_t>(img) * p.img_stride +
                       static_cast<size_t>(orow) * p.wout + ocol;
-          for (int e = 0; e < nvalid; ++e) {
-            const int c = n + e;
-            of[(c / p.chan_div) * p.a_stride + (c % p.chan_div) * p.p_stride] = v[e];
+          // channel c -> (c / chan_div, c % chan_div), stepped from n (no division per element; the unrolled
+          // loop keeps v[] in registers)
+          int cq = n / p.chan_div, cr = n - cq * p.chan_div;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            if (e < nvalid) of[cq * p.a_stride + cr * p.p_stride] = v[e];
+            if (++cr == p.chan_div) { cr = 0; ++cq; }
           }
         }
       }
