@@ -37,6 +37,7 @@ struct ConvParams {
   int nclass, ntap, ncb;
   int cout, cout_pad;  // real output channels, per-class padded N
   int tiles_per_row, tiles_per_class;
+  int tile_rows, tile_cols;  // a 128-pixel tile = tile_rows output rows x tile_cols columns (1 x 128 or 2 x 64)
   // epilogue
   const float* bias;
   int act_gelu;
@@ -104,8 +105,9 @@ DEVI void conv_tile(const ConvParams& p, int mt, int rank, int& img, int& cls, i
   int t = (rest - cls * per_class) * CG + rank;
   valid = t < p.tiles_per_class;
   if (!valid) t = p.tiles_per_class - 1;
-  r = t / p.tiles_per_row;
-  c0 = (t - r * p.tiles_per_row) * CV_BM;
+  const int tr = t / p.tiles_per_row;
+  r = tr * p.tile_rows;
+  c0 = (t - tr * p.tiles_per_row) * p.tile_cols;
 }
 
 template <int BN, int CG, bool STRIP>
@@ -301,11 +303,13 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
       bool valid;
       conv_tile<CG>(p, tile / nn, rank, img, cls, r, c0, valid);
       const int n0 = (tile % nn) * BN;
-      const int col = c0 + i;
-      const bool ok = valid && col < p.cols_t;
+      // this thread's pixel of the tile (tile_rows x tile_cols) and the first pixel of this warp's 32
+      const int di = i / p.tile_cols, row = r + di, col = c0 + i - di * p.tile_cols;
+      const int dw = (32 * q) / p.tile_cols, roww = r + dw, colw = c0 + 32 * q - dw * p.tile_cols;
+      const bool ok = valid && col < p.cols_t && row < p.rows_t;
       // output pixel
-      int orow = r, ocol = col;
-      if (p.mode == WM3_CONV_T2) { orow = 2 * r + (cls >> 1); ocol = 2 * col + (cls & 1); }
+      int orow = row, ocol = col;
+      if (p.mode == WM3_CONV_T2) { orow = 2 * row + (cls >> 1); ocol = 2 * col + (cls & 1); }
       const bool tma_tile = Cfg::TMA_EPI && p.tma_out && valid;  // uniform over the CTA
       if (p.resid != nullptr && ok && !tma_tile) {
         // pull this pixel's residual channels toward L2 while the accumulator is still being computed
@@ -324,7 +328,7 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
           // this warp's residual chunk (its 32 pixels x 32 channels) into its staging tile, under the TMEM load
           bulk_wait_read<0>();  // the previous output chunk has left the staging tile
           mbar_arrive_expect_tx(rbar, 2048u);
-          tma_load_4d(stg, &tmR, rbar, n, c0 + 32 * q + 1, orow + 1, img);
+          tma_load_4d(stg, &tmR, rbar, n, colw + 1, roww + 1, img);  // (residual convs are stride 1)
         }
         uint32_t rr[32];
         tmem_ld32(taddr + 32 * u, rr);
@@ -396,8 +400,10 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
           __syncwarp();
           if (lane == 0) {
             // first padded column of the warp's 32 pixels (transposed convs: every other column of the class)
-            const int pc = p.mode == WM3_CONV_T2 ? 2 * (c0 + 32 * q) + (cls & 1) + 1 : c0 + 32 * q + 1;
-            tma_store_4d(&tmO, stg, n, pc, orow + 1, img);
+            const bool t2 = p.mode == WM3_CONV_T2;
+            const int pc = t2 ? 2 * colw + (cls & 1) + 1 : colw + 1;
+            const int pr = t2 ? 2 * roww + (cls >> 1) + 1 : roww + 1;
+            tma_store_4d(&tmO, stg, n, pc, pr, img);
             bulk_commit();
           }
           if (ok && (ocol == 0 || ocol == p.wout - 1)) {  // longitude wrap columns of the padded output
@@ -625,6 +631,15 @@ static int launch_conv_mode(const CUtensorMap& ta, const CUtensorMap& tb, const 
 
 using namespace wm3;
 
+// two-row conv tiles for rows that 128-pixel tiles would mostly pad (WM3_CONV_TWOROW=0 turns them off, A/B aid)
+static bool conv_two_row_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("WM3_CONV_TWOROW");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // transposed convs on A strips (WM3_CONV_T2STRIP=0 turns it off, A/B aid)
 static bool conv_t2_strip_enabled() {
   static const bool on = [] {
@@ -694,8 +709,8 @@ extern "C" int wm3_conv(int mode, const void* in, int imgs, int hin, int win, in
   p.cout = cout;
   const int bn = wm3_conv_bn(cout);
   p.cout_pad = ((cout + bn - 1) / bn) * bn;
-  p.tiles_per_row = (p.cols_t + CV_BM - 1) / CV_BM;
-  p.tiles_per_class = p.rows_t * p.tiles_per_row;
+  p.tile_rows = 1;
+  p.tile_cols = CV_BM;
   p.bias = bias;
   p.act_gelu = act_gelu;
   p.resid = reinterpret_cast<const elem_t*>(resid);
@@ -713,8 +728,20 @@ extern "C" int wm3_conv(int mode, const void* in, int imgs, int hin, int win, in
   }();
   const int bn_ = wm3_conv_bn(cout);
   const bool pairs_ = conv_pairs_enabled() && bn_ >= 128;
-  const bool strip = strip_env && (mode == WM3_CONV_S1 || (mode == WM3_CONV_T2 && conv_t2_strip_enabled())) &&
-                     conv_strip_fits(bn_, pairs_ ? 2 : 1);
+  bool strip = strip_env && (mode == WM3_CONV_S1 || (mode == WM3_CONV_T2 && conv_t2_strip_enabled())) &&
+               conv_strip_fits(bn_, pairs_ ? 2 : 1);
+  // two-row tiles (2 x 64 pixels) where a row's 128-pixel tiles would be mostly padding (a 180-pixel row: 128 +
+  // 52 valid of 256 computed; 2 x 64: 180 of 192); they take one A box per tap (no strip)
+  if (mode != WM3_CONV_S2 && conv_two_row_enabled()) {
+    const double w1 = ((p.cols_t + 127) / 128) * 128.0 / p.cols_t, w2 = ((p.cols_t + 63) / 64) * 64.0 / p.cols_t;
+    if (w2 < 0.85 * w1) {
+      p.tile_rows = 2;
+      p.tile_cols = 64;
+      strip = false;
+    }
+  }
+  p.tiles_per_row = (p.cols_t + p.tile_cols - 1) / p.tile_cols;
+  p.tiles_per_class = ((p.rows_t + p.tile_rows - 1) / p.tile_rows) * p.tiles_per_row;
   // A: padded NHWC input, images stacked along rows
   CUtensorMap ta, tb;
   const uint64_t wp = win + 2;
@@ -727,7 +754,8 @@ extern "C" int wm3_conv(int mode, const void* in, int imgs, int hin, int win, in
   } else {
     const uint64_t dims[3] = {static_cast<uint64_t>(cinp), wp, rows};
     const uint64_t strides[2] = {static_cast<uint64_t>(cinp), wp * cinp};
-    const uint32_t box[3] = {64, static_cast<uint32_t>(strip ? CV_STRIP_ROWS : CV_BM), 1};
+    const uint32_t box[3] = {64, static_cast<uint32_t>(strip ? CV_STRIP_ROWS : p.tile_cols),
+                             static_cast<uint32_t>(p.tile_rows)};
     if (make_tmap(&ta, in, TMAP_BF16, 3, dims, strides, box, nullptr)) return -1;
   }
   // B: weights [class][cout_pad][ntap * cinp], K-major
@@ -748,7 +776,9 @@ extern "C" int wm3_conv(int mode, const void* in, int imgs, int hin, int win, in
     // spans 64 columns with traversal stride 2 (32 rows in shared memory)
     const uint32_t tbox[4] = {32, 64, 1, 1}, tstr[4] = {1, 2, 1, 1};
     const bool t2 = mode == WM3_CONV_T2;
-    const uint64_t od[4] = {static_cast<uint64_t>(out_cp), wpo - 1, hpo, static_cast<uint64_t>(imgs)};
+    // column extent ends at the last real pixel (pad column W + 1 is the wrap copy), row extent at the last
+    // real row (the bottom pad row stays zero): a tile's overhang past either edge is clipped
+    const uint64_t od[4] = {static_cast<uint64_t>(out_cp), wpo - 1, hpo - 1, static_cast<uint64_t>(imgs)};
     const uint64_t os[3] = {static_cast<uint64_t>(out_cp), wpo * out_cp, hpo * wpo * out_cp};
     if (make_tmap_swz(&to, out, TMAP_BF16, 4, od, os, t2 ? tbox : box, t2 ? tstr : nullptr, 64)) return -1;
     if (resid) {
