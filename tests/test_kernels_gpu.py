@@ -269,3 +269,90 @@ def test_gemm_results_independent_of_tile_width():
         assert r.returncode == 0, r.stderr[-2000:]
         out[v] = r.stdout.strip().splitlines()[-1]
     assert out["0"] == out["2"], out
+
+
+def _pad_nhwc(x, cinp):
+    """(imgs, c, h, w) fp32 -> padded NHWC (imgs, h + 2, w + 2, cinp) operand: zero rows, wrapped columns."""
+    from paper_2503_22235_b200 import _lib
+    imgs, c, h, w = x.shape
+    p = torch.zeros((imgs, h + 2, w + 2, cinp), dtype=_lib.ELEM, device="cuda")
+    xn = x.permute(0, 2, 3, 1).to(_lib.ELEM)
+    p[:, 1:h + 1, 1:w + 1, :c] = xn
+    p[:, 1:h + 1, 0, :c] = xn[:, :, w - 1]
+    p[:, 1:h + 1, w + 1, :c] = xn[:, :, 0]
+    return p
+
+
+def _ref_conv(mode, xq, w, b):
+    """fp32 reference of the three conv modes on the (fp16-rounded) input, reference geometry (model.py:296-325):
+    rows zero-padded by 1, columns periodic."""
+    import torch.nn.functional as F
+    from paper_2503_22235_b200 import _lib
+    xp = F.pad(F.pad(xq, (1, 1, 0, 0), mode="circular"), (0, 0, 1, 1))
+    if mode == _lib.WM3_CONV_S1:
+        return F.conv2d(xp, w) + b[None, :, None, None]
+    if mode == _lib.WM3_CONV_S2:
+        return F.conv2d(xp, w, stride=2) + b[None, :, None, None]
+    imgs, cin, h, wd = xq.shape
+    cout = w.shape[1]
+    out = torch.zeros((imgs, cout, 2 * h, 2 * wd), device=xq.device)
+    for a in range(2):
+        for bb in range(2):
+            acc = torch.zeros((imgs, cout, h, wd), device=xq.device)
+            for tr in range(2):
+                for tc in range(2):
+                    tap = w[:, :, 3 - a - 2 * tr, 3 - bb - 2 * tc]  # (cin, cout)
+                    win = xp[:, :, a + tr:a + tr + h, bb + tc:bb + tc + wd]
+                    acc += torch.einsum("nchw,co->nohw", win, tap)
+            out[:, :, a::2, bb::2] = acc
+    return out + b[None, :, None, None]
+
+
+@pytest.mark.parametrize("mode,h,w,cin,cout,gelu,resid", [
+    ("s1", 7, 36, 96, 64, True, False),     # two-row tiles, odd rows: the bottom pad row must stay zero
+    ("s1", 5, 250, 64, 192, False, True),   # one-row tiles, CTA pairs, A strips, TMA residual / output
+    ("s1", 6, 180, 128, 256, False, True),  # two-row tiles with residual (the 90 x 180 stage shape class)
+    ("s2", 6, 72, 64, 128, False, False),   # stride 2
+    ("t2", 5, 36, 128, 64, False, False),   # transposed, two-row tiles, strided store box
+    ("t2", 4, 250, 64, 192, False, False),  # transposed, one-row tiles, A strips over two column taps
+])
+def test_conv_kernel_against_torch(mode, h, w, cin, cout, gelu, resid):
+    """wm3_conv (epilogue through TMA staging, one- and two-row tiles, strips) against an fp32 torch conv on
+    the same fp16 operands, interior within fp16 output rounding; the padded output's halo: pad rows zero, pad
+    columns the wrapped copies of the opposite edge."""
+    from paper_2503_22235_b200 import _lib
+    from paper_2503_22235_b200.pyramid import conv3_weights, convT_weights, cpad, run_conv
+    torch.manual_seed(h * w + cin)
+    imgs = 2
+    x = torch.randn(imgs, cin, h, w, device="cuda")
+    xq = x.to(_lib.ELEM).float()
+    m = {"s1": _lib.WM3_CONV_S1, "s2": _lib.WM3_CONV_S2, "t2": _lib.WM3_CONV_T2}[mode]
+    if m == _lib.WM3_CONV_T2:
+        wt = torch.randn(cin, cout, 4, 4, device="cuda") / (2 * cin) ** 0.5
+        cw = convT_weights(wt.cpu().numpy(), np.zeros(cout, np.float32))
+        ho, wo = 2 * h, 2 * w
+    else:
+        wt = torch.randn(cout, cin, 3, 3, device="cuda") / (9 * cin) ** 0.5
+        cw = conv3_weights(wt.cpu().numpy(), np.zeros(cout, np.float32), 1 if m == _lib.WM3_CONV_S1 else 2)
+        ho, wo = (h, w) if m == _lib.WM3_CONV_S1 else ((h - 1) // 2 + 1, w // 2)
+    bias = torch.randn(cout, device="cuda") * 0.1
+    cw.b[:cout] = bias
+    wt_q = wt.to(_lib.ELEM).float()  # the kernel's operand weights are the same rounding
+    ref = _ref_conv(m, xq, wt_q, bias)
+    rp = None
+    if resid:
+        r = torch.randn(imgs, cout, ho, wo, device="cuda")
+        rp = _pad_nhwc(r, cpad(cout))
+        ref = ref + r.to(_lib.ELEM).float()
+    if gelu:
+        ref = torch.nn.functional.gelu(ref)
+    out = torch.zeros((imgs, ho + 2, wo + 2, cpad(cout)), dtype=_lib.ELEM, device="cuda")
+    run_conv(cw, _pad_nhwc(x, cw.cinp), imgs, h, w, out, gelu=gelu, resid=rp)
+    torch.cuda.synchronize()
+    got = out[:, 1:ho + 1, 1:wo + 1, :cout].float().permute(0, 3, 1, 2)
+    err = float((got - ref).norm() / ref.norm())
+    print(f"conv {mode} {h}x{w} {cin}->{cout}: rel err {err:.2e}")
+    assert err < 3e-3, err
+    assert not out[:, 0].any() and not out[:, ho + 1].any()  # pad rows untouched
+    assert torch.equal(out[:, 1:ho + 1, 0], out[:, 1:ho + 1, wo]) and torch.equal(out[:, 1:ho + 1, wo + 1],
+                                                                                    out[:, 1:ho + 1, 1])
