@@ -732,7 +732,7 @@ extern "C" int wm3_conv(int mode, const void* in, int imgs, int hin, int win, in
                conv_strip_fits(bn_, pairs_ ? 2 : 1);
   // two-row tiles (2 x 64 pixels) where a row's 128-pixel tiles would be mostly padding (a 180-pixel row: 128 +
   // 52 valid of 256 computed; 2 x 64: 180 of 192); they take one A box per tap (no strip)
-  if (mode != WM3_CONV_S2 && conv_two_row_enabled()) {
+  if (conv_two_row_enabled()) {
     const double w1 = ((p.cols_t + 127) / 128) * 128.0 / p.cols_t, w2 = ((p.cols_t + 63) / 64) * 64.0 / p.cols_t;
     if (w2 < 0.85 * w1) {
       p.tile_rows = 2;
@@ -749,8 +749,11 @@ extern "C" int wm3_conv(int mode, const void* in, int imgs, int hin, int win, in
   if (mode == WM3_CONV_S2) {
     const uint64_t dims[4] = {static_cast<uint64_t>(cinp), 2, wp / 2, rows};
     const uint64_t strides[3] = {static_cast<uint64_t>(cinp), 2ull * cinp, wp * cinp};
-    const uint32_t box[4] = {64, 1, CV_BM, 1};
-    if (make_tmap(&ta, in, TMAP_BF16, 4, dims, strides, box, nullptr)) return -1;
+    // two-row tiles: output rows r, r + 1 read input rows 2r + kh, 2r + 2 + kh (a row box of 4 at stride 2)
+    const bool two = p.tile_rows == 2;
+    const uint32_t box[4] = {64, 1, static_cast<uint32_t>(p.tile_cols), two ? 4u : 1u};
+    const uint32_t es[4] = {1, 1, 1, two ? 2u : 1u};
+    if (make_tmap(&ta, in, TMAP_BF16, 4, dims, strides, box, es)) return -1;
   } else {
     const uint64_t dims[3] = {static_cast<uint64_t>(cinp), wp, rows};
     const uint64_t strides[2] = {static_cast<uint64_t>(cinp), wp * cinp};

@@ -297,7 +297,15 @@ def test_natten_row_split_bitwise():
         for lo, hi in ((a, z), (b.row0, a), (z, b.row0 + b.rows)):
             if hi > lo:
                 ops.natten(buf, grid, heads, dhp, dhp, win, out=split, rows_global=h, row0=b.row0, q_rows=(lo, hi))
-        assert torch.equal(split, one), b
+        if not torch.equal(split, one):
+            diff = split.float() - one.float()
+            bad = torch.nonzero(torch.isnan(split).any(1) | torch.isnan(one).any(1) | (diff.abs() > 0).any(1)).flatten()
+            rows = ((bad.cpu() // w) % b.rows + b.row0).unique().tolist()
+            again = ops.natten(buf, grid, heads, dhp, dhp, win, rows_global=h, row0=b.row0)
+            raise AssertionError(f"{b}: {bad.numel()} tokens differ (NaN in split {int(torch.isnan(split).any(1).sum())}, "
+                                 f"in one {int(torch.isnan(one).any(1).sum())}), global rows {rows[:16]}, "
+                                 f"split launches {(a, z)}, a repeat of the one-launch result equal: "
+                                 f"{bool(torch.equal(again, one))}")
 
 
 @pytest.mark.parametrize("name,world", [("mid", 2), ("desk", 2)])
